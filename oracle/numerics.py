@@ -1,0 +1,169 @@
+"""Oracle (TEST INFRASTRUCTURE ONLY): numpy fp32 restatement of the MoE block.
+
+The reference executes no numerics ("Combination weights at the MoE output
+are not simulated numerically"; "No numerical execution of
+experts"), so this module is PARITY UNPINNED by any reference
+vector: it restates the builder-defined contract of DESIGN.md §3 (SURVEY.md
+Appendix B), which follows PAPER.md:110-114 (gate on the post-attention
+hidden state), PAPER.md:234,319,329 (next-layer prediction from x_l) and the
+Mixtral top-2 renormalisation.
+
+Contract (per layer l, residual h fp32 (T, d)):
+    x      = bf16( (h * rsqrt(mean(h^2) + eps)) * gamma_l )
+    z      = x . Wg_l^T          (fp32 accumulate)       p  = softmax(z)
+    z_hat  = x . Wg_{l+1}^T      (l + 1 < L)             p^ = softmax(z_hat)
+    sel    = topk(p, k)          (ties -> lower index; decisions.topk_rows)
+    w_j    = p[sel_j] / sum_j p[sel_j]
+    a      = bf16( silu(x . W1_e^T) * (x . W3_e^T) )      (fp32 accumulate)
+    y_e    = a . W2_e^T                                   (fp32 accumulate)
+    h'     = h + sum_{j=0..k-1} w_j y_{sel_j}             (fixed j order)
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import rng
+from .decisions import topk_rows
+
+RMS_EPS = 1e-5
+
+
+# ------------------------------------------------------------------ weights
+
+
+class OracleModel:
+    """Lazily generated random-init weights (bit-identical to the CUDA init)."""
+
+    def __init__(self, num_layers, num_experts, top_k, d_model, d_ff, seed=0):
+        self.L, self.E, self.k = num_layers, num_experts, top_k
+        self.d, self.ffn, self.seed = d_model, d_ff, seed
+        self.scale_in = float(np.float32(1.0 / np.sqrt(d_model)))
+        self.scale_ff = float(np.float32(1.0 / np.sqrt(d_ff)))
+
+    def gate(self, layer):
+        return rng.tensor_bf16(self.seed, rng.make_tag(rng.KIND_GATE, layer),
+                               (self.E, self.d), self.scale_in)
+
+    def norm(self, layer):
+        return rng.norm_weight(self.seed, layer, self.d)
+
+    def w1(self, layer, e):
+        return rng.tensor_bf16(self.seed, rng.make_tag(rng.KIND_EXPERT, layer, e, 0),
+                               (self.ffn, self.d), self.scale_in)
+
+    def w3(self, layer, e):
+        return rng.tensor_bf16(self.seed, rng.make_tag(rng.KIND_EXPERT, layer, e, 1),
+                               (self.ffn, self.d), self.scale_in)
+
+    def w2(self, layer, e):
+        return rng.tensor_bf16(self.seed, rng.make_tag(rng.KIND_EXPERT, layer, e, 2),
+                               (self.d, self.ffn), self.scale_ff)
+
+
+def input_hidden(seed: int, stream: int, step: int, t: int, d: int) -> np.ndarray:
+    """Synthetic residual-stream input h (T, d) fp32, unit variance U(-√3, √3)."""
+    tag = rng.make_tag(rng.KIND_INPUT, stream, step)
+    return rng.tensor_f32(seed, tag, (t, d), float(np.float32(np.sqrt(3.0))))
+
+
+# ------------------------------------------------------------------ blocks
+
+
+def rmsnorm(h: np.ndarray, gamma: np.ndarray) -> np.ndarray:
+    h = h.astype(np.float32)
+    ms = (h.astype(np.float64) ** 2).mean(axis=-1, keepdims=True).astype(np.float32)
+    r = np.float32(1.0) / np.sqrt(ms + np.float32(RMS_EPS))
+    return rng.round_bf16((h * r) * gamma.astype(np.float32))
+
+
+def softmax(z: np.ndarray) -> np.ndarray:
+    z = z.astype(np.float32)
+    m = z.max(axis=-1, keepdims=True)
+    ez = np.exp(z - m)
+    return ez / ez.sum(axis=-1, keepdims=True)
+
+
+def router(x, wg_true, wg_pred=None):
+    """Fused-router contract: probs of the own gate and of the next layer's gate
+    from ONE read of x."""
+    p = softmax(x.astype(np.float32) @ wg_true.T.astype(np.float32))
+    ph = None
+    if wg_pred is not None:
+        ph = softmax(x.astype(np.float32) @ wg_pred.T.astype(np.float32))
+    return p, ph
+
+
+def renorm_weights(p_rows: np.ndarray, sel: np.ndarray) -> np.ndarray:
+    g = np.take_along_axis(p_rows, sel, axis=1).astype(np.float32)
+    return g / g.sum(axis=1, keepdims=True)
+
+
+def silu(a: np.ndarray) -> np.ndarray:
+    return a / (np.float32(1.0) + np.exp(-a))
+
+
+def expert_act(x, w1, w3):
+    """a = bf16(silu(x W1^T) * (x W3^T)) -- the SwiGLU intermediate."""
+    g = x.astype(np.float32) @ w1.T
+    u = x.astype(np.float32) @ w3.T
+    return rng.round_bf16(silu(g) * u)
+
+
+def expert_ffn(x, w1, w3, w2):
+    return expert_act(x, w1, w3) @ w2.T
+
+
+def permutation(topk_idx: np.ndarray, num_experts: int):
+    """Stable token->expert permutation by histogram + exclusive scan.
+
+    Rows (t, j) sorted by (expert, t, j).  Returns (offsets (E+1,), perm
+    (T*k,) flat source index t*k+j for each sorted position, inv (T, k)
+    sorted position of each (t, j)).
+    """
+    t, k = topk_idx.shape
+    flat = topk_idx.reshape(-1).astype(np.int64)
+    hist = np.bincount(flat, minlength=num_experts)
+    offsets = np.zeros(num_experts + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum(hist)
+    perm = np.argsort(flat, kind="stable").astype(np.int64)
+    inv = np.empty(t * k, dtype=np.int64)
+    inv[perm] = np.arange(t * k)
+    return offsets, perm, inv.reshape(t, k)
+
+
+def combine(h, y_sorted, inv, w):
+    """h' = h + sum_j w_j y[inv[t, j]] in fixed j order."""
+    out = h.astype(np.float32).copy()
+    for j in range(inv.shape[1]):
+        out = out + w[:, j:j + 1] * y_sorted[inv[:, j]]
+    return out
+
+
+def moe_layer(model: OracleModel, layer: int, h: np.ndarray, sel=None, w=None,
+              x=None):
+    """One MoE block on all tokens with every expert exact on current input.
+
+    sel / w may be injected (teacher forcing with the GPU's decisions);
+    x may be injected (teacher forcing with the GPU's normalised input).
+    Returns dict(x, p, p_hat, sel, w, out).
+    """
+    if x is None:
+        x = rmsnorm(h, model.norm(layer))
+    wg_pred = model.gate(layer + 1) if layer + 1 < model.L else None
+    p, ph = router(x, model.gate(layer), wg_pred)
+    if sel is None:
+        sel = topk_rows(p.astype(np.float64), model.k)
+    if w is None:
+        w = renorm_weights(p, sel)
+    offsets, perm, inv = permutation(sel, model.E)
+    y = np.zeros((sel.size, model.d), dtype=np.float32)
+    for e in range(model.E):
+        a, b = int(offsets[e]), int(offsets[e + 1])
+        if a == b:
+            continue
+        rows = perm[a:b] // model.k
+        y[a:b] = expert_ffn(x[rows], model.w1(layer, e), model.w3(layer, e),
+                            model.w2(layer, e))
+    out = combine(h, y, inv, w)
+    return {"x": x, "p": p, "p_hat": ph, "sel": sel, "w": w, "out": out}
