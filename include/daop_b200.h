@@ -1,0 +1,124 @@
+/* daop_b200.h -- C ABI of the B200-native DAOP MoE-block hot path.
+ *
+ * One shared library (libdaop_b200.so, built from paper_2501_10375_b200/csrc)
+ * exporting plain C entry points: raw pointers, sizes and a cudaStream_t
+ * passed as an opaque handle.  No C++ or torch types cross this boundary.
+ *
+ * Conventions
+ *   - every function returns 0 (DAOP_OK) or a negative DAOP_ERR_* code and
+ *     then sets a thread-local message readable with daop_last_error();
+ *     the Python layer maps codes onto the reference's MoesimError classes
+ *     (moesim/errors.py:8-45).
+ *   - "d_" pointers are device memory, "h_" pointers host memory; functions
+ *     without a stream argument are host-only and synchronous.
+ *   - device functions are asynchronous and stream ordered; callers own all
+ *     buffers.  The library owns nothing except what *_create returns.
+ *
+ * Each entry point names the reference interface it replaces (file:line in
+ * /root/reference/pkg/src/moesim).
+ */
+#ifndef DAOP_B200_H
+#define DAOP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* daop_stream_t; /* cudaStream_t */
+
+#define DAOP_OK 0
+#define DAOP_ERR_SHAPE (-1)              /* ShapeMismatchError      errors.py:16 */
+#define DAOP_ERR_NORMALIZATION (-2)      /* NormalizationError      errors.py:20 */
+#define DAOP_ERR_BUDGET (-3)             /* BudgetError             errors.py:40 */
+#define DAOP_ERR_PREDICTION_MISSING (-4) /* PredictionMissingError  errors.py:32 */
+#define DAOP_ERR_CONFIG (-5)             /* ConfigError             errors.py:44 */
+#define DAOP_ERR_EMPTY_PHASE (-6)        /* EmptyPhaseError         errors.py:24 */
+#define DAOP_ERR_CUDA (-100)             /* CUDA runtime failure (no reference analogue) */
+#define DAOP_ERR_UNSUPPORTED (-101)      /* shape outside the kernel envelope */
+
+#define DAOP_ENGINE_FIDDLER 2 /* policies.py:32 ENGINES index */
+#define DAOP_ENGINE_DAOP 3
+
+/* ------------------------------------------------------------------ library */
+const char* daop_last_error(void);
+int daop_version(void);
+/* sm count and compute capability of the current device (fails without GPU) */
+int daop_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---------------------------------------------- operator table (_kernels.py)
+ * Device replacements of the reference's module-level operator table,
+ * resolved at call time by metrics.py:59,70 and policies.py:180,302,318. */
+
+/* replaces _kernels.topk_rows (_kernels.py:32-40,63-79,104-105):
+ * (n, e) scores -> (n, k) int64 ids, highest first, ties to the lower index */
+int daop_topk_rows_f64(const double* d_scores, int64_t n, int32_t e, int32_t k, int64_t* d_out,
+                       daop_stream_t stream);
+int daop_topk_rows_f32(const float* d_scores, int64_t n, int32_t e, int32_t k, int64_t* d_out,
+                       daop_stream_t stream);
+/* replaces _kernels.activation_counts (_kernels.py:52-58,94-102):
+ * (t, l, k) int64 ids -> d_counts (l, e) int64 += counts (caller zeroes) */
+int daop_activation_counts(const int64_t* d_topk, int64_t t, int32_t l, int32_t k, int32_t e,
+                           int64_t* d_counts, daop_stream_t stream);
+/* replaces _kernels.pair_overlap (_kernels.py:43-49,81-92) */
+int daop_pair_overlap(const int64_t* d_a, const int64_t* d_b, int64_t n, int32_t ka, int32_t kb,
+                      int64_t* d_out, daop_stream_t stream);
+
+/* --------------------------------------- host decisions (placement/policies)
+ * Pure host functions, bit-exact restatements of the reference. */
+
+/* replaces placement.slot_budget_for_ecr (placement.py:123-125) */
+int daop_slot_budget(double ecr, int32_t num_layers, int32_t num_experts, int64_t* h_budget);
+/* replaces placement.init_from_calibration (placement.py:128-185):
+ * h_calib (L, E) float64 -> h_on_fast (L, E) uint8 membership, h_budget */
+int daop_placement_init(const double* h_calib, int32_t num_layers, int32_t num_experts, double ecr,
+                        uint8_t* h_on_fast, int64_t* h_budget);
+/* replaces placement.allocate_for_sequence (placement.py:188-237), threshold
+ * given as the exact rational thr_num/thr_den = Fraction(str(float(s))).
+ * h_events: capacity L*(E/2) rows of (layer, in, out, hot, cold). */
+int daop_allocate(const uint8_t* h_on_fast, const int64_t* h_counts, int32_t num_layers,
+                  int32_t num_experts, int64_t thr_num, int64_t thr_den, uint8_t* h_on_fast_out,
+                  int64_t* h_events, int32_t* h_n_events);
+/* replaces policies.degrade_selection (policies.py:264-296): h_sel_io (k) is
+ * edited in place; h_drop/h_sub (capacity k) receive the degradation pairs */
+int daop_degrade_f64(const double* h_scores, int32_t num_experts, int32_t* h_sel_io, int32_t k,
+                     const uint8_t* h_fast, int32_t* h_drop, int32_t* h_sub, int32_t* h_n_deg);
+/* replaces {Fiddler,Daop}Planner.plan_token (policies.py:248-261,299-336)
+ * for one token: h_true (L,E), h_pred (L,E) with h_pred_mask (L), h_on_fast
+ * (L,E).  Outputs h_sel (L,k), h_is_fast (L,k), h_drop/h_sub (L,k), h_n_deg (L). */
+int daop_plan_token_f64(const double* h_true, const double* h_pred, const uint8_t* h_pred_mask,
+                        const uint8_t* h_on_fast, int32_t num_layers, int32_t num_experts,
+                        int32_t k, int32_t start_layer, int32_t engine, int32_t graceful,
+                        int32_t* h_sel, uint8_t* h_is_fast, int32_t* h_drop, int32_t* h_sub,
+                        int32_t* h_n_deg);
+
+/* ------------------------------------------------ device decision kernel
+ * The same plan as daop_plan_token_f64, on the router's exported float32
+ * probabilities, for n tokens at one layer, entirely on device (the decode
+ * loop never syncs to the host for a decision).  d_pred_prev may be NULL
+ * when the layer is below start (or engine is fiddler). */
+int daop_plan_layer_f32(const float* d_true, const float* d_pred_prev, const uint8_t* d_fast_row,
+                        int64_t n, int32_t layer, int32_t num_experts, int32_t k,
+                        int32_t start_layer, int32_t engine, int32_t graceful, int32_t* d_sel,
+                        uint8_t* d_is_fast, int32_t* d_drop, int32_t* d_sub, int32_t* d_n_deg,
+                        daop_stream_t stream);
+
+/* ------------------------------------------------ random-init tensors
+ * Counter-based generator shared bit-for-bit with oracle/rng.py. */
+int daop_fill_uniform_bf16(uint16_t* d_dst, int64_t n, uint64_t seed, uint64_t tag, float scale,
+                           int64_t index_offset, daop_stream_t stream);
+int daop_fill_uniform_f32(float* d_dst, int64_t n, uint64_t seed, uint64_t tag, float scale,
+                          int64_t index_offset, daop_stream_t stream);
+/* RMSNorm weight bf16(1 + 0.25 u) of one layer */
+int daop_fill_norm_bf16(uint16_t* d_dst, int64_t d, uint64_t seed, int32_t layer,
+                        daop_stream_t stream);
+/* host-side fill (for the pinned slow-tier pool), multi-threaded */
+int daop_fill_uniform_bf16_host(uint16_t* h_dst, int64_t n, uint64_t seed, uint64_t tag,
+                                float scale, int64_t index_offset, int32_t threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DAOP_B200_H */

@@ -1,0 +1,101 @@
+"""ctypes binding of libdaop_b200.so (the C ABI in include/daop_b200.h).
+
+There is exactly one backend: if the shared library is missing the import
+fails loudly -- there is no Python/CPU fallback for any hot-path operation.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+from . import errors as E
+
+LIB_PATH = Path(__file__).resolve().parent / "libdaop_b200.so"
+
+P = C.c_void_p
+I32, I64, U64, F32, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
+
+# name -> argtypes (every function returns int status)
+PROTOS = {
+    "daop_version": [],
+    "daop_device_info": [P, P, P],
+    "daop_topk_rows_f64": [P, I64, I32, I32, P, P],
+    "daop_topk_rows_f32": [P, I64, I32, I32, P, P],
+    "daop_activation_counts": [P, I64, I32, I32, I32, P, P],
+    "daop_pair_overlap": [P, P, I64, I32, I32, P, P],
+    "daop_slot_budget": [F64, I32, I32, P],
+    "daop_placement_init": [P, I32, I32, F64, P, P],
+    "daop_allocate": [P, P, I32, I32, I64, I64, P, P, P],
+    "daop_degrade_f64": [P, I32, P, I32, P, P, P, P],
+    "daop_plan_token_f64": [P, P, P, P, I32, I32, I32, I32, I32, I32, P, P, P, P, P],
+    "daop_plan_layer_f32": [P, P, P, I64, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P],
+    "daop_fill_uniform_bf16": [P, I64, U64, U64, F32, I64, P],
+    "daop_fill_uniform_f32": [P, I64, U64, U64, F32, I64, P],
+    "daop_fill_norm_bf16": [P, I64, U64, I32, P],
+    "daop_fill_uniform_bf16_host": [P, I64, U64, U64, F32, I64, I32],
+}
+
+_CODES = {
+    -1: E.ShapeMismatchError,
+    -2: E.NormalizationError,
+    -3: E.BudgetError,
+    -4: E.PredictionMissingError,
+    -5: E.ConfigError,
+    -6: E.EmptyPhaseError,
+}
+
+
+def _load():
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH.name} is not built; run `python -m paper_2501_10375_b200.build` "
+            "(nvcc, sm_100a). There is no CPU fallback."
+        )
+    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+    for name, args in PROTOS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    lib.daop_last_error.argtypes = []
+    lib.daop_last_error.restype = C.c_char_p
+    return lib
+
+
+LIB = _load()
+
+
+def exported_symbols():
+    return sorted(PROTOS) + ["daop_last_error"]
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = LIB.daop_last_error().decode(errors="replace")
+    cls = _CODES.get(rc)
+    if cls is not None:
+        raise cls(msg)
+    raise E.DeviceError(f"{what}: {msg} (code {rc})")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(LIB, name)(*args), name)
+
+
+def ptr(a) -> int:
+    """Raw address of a numpy array or torch tensor (no copies)."""
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream

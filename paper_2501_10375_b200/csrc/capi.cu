@@ -1,0 +1,244 @@
+// Library plumbing + host decision entry points (placement.py / policies.py).
+//
+// The host decisions are pure C++ restatements of the reference, bit-exact:
+// they are pinned by tests/test_host_decisions.py against the golden vectors
+// recorded from moesim itself.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <numeric>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "decide.cuh"
+#include "rng.cuh"
+
+namespace daop {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %d (%s) at %s", static_cast<int>(e), cudaGetErrorString(e), what);
+  return DAOP_ERR_CUDA;
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+}  // namespace daop
+
+using namespace daop;
+
+extern "C" {
+
+const char* daop_last_error(void) { return g_err; }
+
+int daop_version(void) { return 1; }
+
+int daop_device_info(int* sms, int* major, int* minor) {
+  int dev = 0;
+  DAOP_CUDA(cudaGetDevice(&dev));
+  DAOP_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
+  DAOP_CUDA(cudaDeviceGetAttribute(major, cudaDevAttrComputeCapabilityMajor, dev));
+  DAOP_CUDA(cudaDeviceGetAttribute(minor, cudaDevAttrComputeCapabilityMinor, dev));
+  return DAOP_OK;
+}
+
+// placement.py:123-125 -- math.floor(ecr * L * E), left to right in double
+int daop_slot_budget(double ecr, int32_t L, int32_t E, int64_t* budget) {
+  double v = (ecr * static_cast<double>(L)) * static_cast<double>(E);
+  if (!std::isfinite(v)) {
+    set_error("slot budget of ecr=%g is not finite", ecr);
+    return DAOP_ERR_BUDGET;
+  }
+  *budget = static_cast<int64_t>(std::floor(v));
+  return DAOP_OK;
+}
+
+// placement.py:128-185
+int daop_placement_init(const double* calib, int32_t L, int32_t E, double ecr, uint8_t* on_fast,
+                        int64_t* budget_out) {
+  if (L < 1 || E < 2) {
+    set_error("invalid calibration shape (%d, %d)", L, E);
+    return DAOP_ERR_SHAPE;
+  }
+  if (!(0.0 < ecr && ecr <= 1.0)) {  // :151-152 (NaN fails too)
+    set_error("ecr must be in (0, 1], got %g", ecr);
+    return DAOP_ERR_BUDGET;
+  }
+  int64_t budget = 0;
+  int rc = daop_slot_budget(ecr, L, E, &budget);
+  if (rc) return rc;
+  if (budget < L) {  // :154-157
+    set_error("budget %lld cannot give every one of %d layers a slot",
+              static_cast<long long>(budget), L);
+    return DAOP_ERR_BUDGET;
+  }
+  const int64_t base = budget / L, rem = budget - base * L;
+  std::fill(on_fast, on_fast + static_cast<size_t>(L) * E, uint8_t(0));
+  std::vector<int> order(E);
+  for (int l = 0; l < L; ++l) {  // :166-169 per-layer top-base by (-v, j)
+    const double* v = calib + static_cast<size_t>(l) * E;
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return -v[a] < -v[b]; });
+    for (int64_t i = 0; i < base && i < E; ++i) on_fast[static_cast<size_t>(l) * E + order[i]] = 1;
+  }
+  if (rem) {  // :171-183 remainder by (-v, l, j), at most one extra per layer
+    std::vector<std::pair<int, int>> cand;
+    for (int l = 0; l < L; ++l)
+      for (int j = 0; j < E; ++j)
+        if (!on_fast[static_cast<size_t>(l) * E + j]) cand.emplace_back(l, j);
+    std::stable_sort(cand.begin(), cand.end(), [&](const auto& a, const auto& b) {
+      return -calib[static_cast<size_t>(a.first) * E + a.second] <
+             -calib[static_cast<size_t>(b.first) * E + b.second];
+    });  // candidates were generated in (l, j) order, so stability breaks ties
+    std::vector<uint8_t> granted(L, 0);
+    int64_t n_granted = 0;
+    for (const auto& c : cand) {
+      if (n_granted == rem) break;
+      if (granted[c.first]) continue;
+      on_fast[static_cast<size_t>(c.first) * E + c.second] = 1;
+      granted[c.first] = 1;
+      ++n_granted;
+    }
+  }
+  *budget_out = budget;
+  return DAOP_OK;
+}
+
+// placement.py:188-237 (Alg. 1), exact rational threshold num/den
+int daop_allocate(const uint8_t* on_fast, const int64_t* counts, int32_t L, int32_t E,
+                  int64_t thr_num, int64_t thr_den, uint8_t* out, int64_t* events,
+                  int32_t* n_events) {
+  if (thr_den <= 0) {
+    set_error("threshold denominator must be positive");
+    return DAOP_ERR_CONFIG;
+  }
+  for (int64_t i = 0; i < static_cast<int64_t>(L) * E; ++i) {
+    if (counts[i] < 0) {
+      set_error("prefill counts must be nonnegative integers");
+      return DAOP_ERR_SHAPE;
+    }
+  }
+  const int swap_num = E / 2;  // :213
+  int ne = 0;
+  std::vector<int> hot, cold;
+  for (int l = 0; l < L; ++l) {
+    const uint8_t* in = on_fast + static_cast<size_t>(l) * E;
+    uint8_t* o = out + static_cast<size_t>(l) * E;
+    const int64_t* act = counts + static_cast<size_t>(l) * E;
+    std::copy(in, in + E, o);
+    hot.clear();
+    cold.clear();
+    for (int j = 0; j < E; ++j) (in[j] ? cold : hot).push_back(j);
+    // :221 hot = slow sorted by (-act, j); :222 cold = cached sorted by (act, j)
+    std::stable_sort(hot.begin(), hot.end(), [&](int a, int b) { return act[a] > act[b]; });
+    std::stable_sort(cold.begin(), cold.end(), [&](int a, int b) { return act[a] < act[b]; });
+    const int pairs = std::min<int>(swap_num, std::min(hot.size(), cold.size()));
+    for (int i = 0; i < pairs; ++i) {
+      const int h = hot[i], c = cold[i];
+      // :224 Fraction(h) >= Fraction(num, den) * c  <=>  h*den >= num*c
+      const __int128 lhs = static_cast<__int128>(act[h]) * thr_den;
+      const __int128 rhs = static_cast<__int128>(thr_num) * act[c];
+      if (lhs >= rhs) {
+        o[c] = 0;
+        o[h] = 1;
+        int64_t* ev = events + static_cast<size_t>(ne) * 5;
+        ev[0] = l;
+        ev[1] = h;
+        ev[2] = c;
+        ev[3] = act[h];
+        ev[4] = act[c];
+        ++ne;
+      }
+    }
+  }
+  *n_events = ne;
+  return DAOP_OK;
+}
+
+int daop_degrade_f64(const double* scores, int32_t E, int32_t* sel, int32_t k,
+                     const uint8_t* fast, int32_t* drop, int32_t* sub, int32_t* n_deg) {
+  for (int q = 0; q < k; ++q) {
+    if (sel[q] < 0 || sel[q] >= E) {
+      set_error("selection id %d out of range", sel[q]);
+      return DAOP_ERR_SHAPE;
+    }
+  }
+  *n_deg = degrade(scores, E, sel, k, fast, drop, sub);
+  return DAOP_OK;
+}
+
+int daop_plan_token_f64(const double* tr, const double* pr, const uint8_t* pmask,
+                        const uint8_t* on_fast, int32_t L, int32_t E, int32_t k, int32_t start,
+                        int32_t engine, int32_t graceful, int32_t* sel, uint8_t* is_fast,
+                        int32_t* drop, int32_t* sub, int32_t* n_deg) {
+  if (k < 1 || k > E) {
+    set_error("top_k must be in [1, %d], got %d", E, k);
+    return DAOP_ERR_SHAPE;
+  }
+  if (engine != DAOP_ENGINE_DAOP && engine != DAOP_ENGINE_FIDDLER) {
+    set_error("engine %d has no native planner", engine);
+    return DAOP_ERR_CONFIG;
+  }
+  const bool daop_engine = engine == DAOP_ENGINE_DAOP;
+  for (int l = 0; l < L; ++l) {
+    const size_t o = static_cast<size_t>(l) * E, ok = static_cast<size_t>(l) * k;
+    const bool present = l > 0 && pmask[l - 1];
+    int nd = plan_layer(l, tr + o, l > 0 ? pr + o - E : nullptr, present, on_fast + o, E, k, start,
+                        daop_engine, graceful != 0, sel + ok, is_fast + ok, drop + ok, sub + ok);
+    if (nd < 0) {
+      set_error("layer %d record carries no prediction for layer %d", l - 1, l);
+      return DAOP_ERR_PREDICTION_MISSING;
+    }
+    n_deg[l] = nd;
+  }
+  return DAOP_OK;
+}
+
+int daop_fill_uniform_bf16_host(uint16_t* dst, int64_t n, uint64_t seed, uint64_t tag, float scale,
+                                int64_t off, int32_t threads) {
+  const uint64_t key = stream_key(seed, tag);
+  if (threads < 1) threads = 1;
+  auto work = [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+      uint64_t z = mix64(key + (static_cast<uint64_t>(i + off) + 1ull) * kGolden);
+      float u = static_cast<float>(static_cast<uint32_t>(z >> 40)) * 1.1920928955078125e-07f - 1.0f;
+      float v = u * scale;
+      uint32_t bits;
+      std::memcpy(&bits, &v, 4);
+      bits = (bits + 0x7FFFu + ((bits >> 16) & 1u)) >> 16;
+      dst[i] = static_cast<uint16_t>(bits);
+    }
+  };
+  std::vector<std::thread> pool;
+  const int64_t chunk = (n + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    int64_t a = t * chunk, b = std::min(n, a + chunk);
+    if (a < b) pool.emplace_back(work, a, b);
+  }
+  for (auto& th : pool) th.join();
+  return DAOP_OK;
+}
+
+}  // extern "C"
