@@ -118,6 +118,72 @@ int daop_fill_norm_bf16(uint16_t* d_dst, int64_t d, uint64_t seed, int32_t layer
 int daop_fill_uniform_bf16_host(uint16_t* h_dst, int64_t n, uint64_t seed, uint64_t tag,
                                 float scale, int64_t index_offset, int32_t threads);
 
+/* ------------------------------------------------ fused router (prefill)
+ * Realises SURVEY a1+a2+a3+a9 in one pass per token: x = bf16(rmsnorm(h) *
+ * gamma) (written to d_x when non-NULL), p = softmax(x.Wg^T), p_pred =
+ * softmax(x.Wg_next^T) (when d_wg_next != NULL), top-k of p with ties to the
+ * lower id (_kernels.py:63-79), renormalised weights, and the per-sequence
+ * activation counter d_hist[(t / tokens_per_seq) * hist_seq_stride + e] += 1
+ * (metrics.expert_counts, metrics.py:64-71) when d_hist != NULL. */
+int daop_router(const float* d_h, const uint16_t* d_gamma, const uint16_t* d_wg,
+                const uint16_t* d_wg_next, int64_t t, int32_t d, int32_t num_experts, int32_t k,
+                float eps, uint16_t* d_x, float* d_p_true, float* d_p_pred, int32_t* d_topk_idx,
+                float* d_topk_w, int32_t* d_hist, int64_t tokens_per_seq,
+                int64_t hist_seq_stride, daop_stream_t stream);
+
+/* ------------------------------------------------ permutation + combine
+ * Stable token->expert permutation (histogram + exclusive scan): rows (t, j)
+ * sorted by (expert, t, j); d_offsets (E+1) int64, d_perm[p] = t*k + j,
+ * d_inv[t*k + j] = p, d_x_perm[p] = d_x[t] (skipped when NULL).  No reference
+ * analogue; builder-defined contract in DESIGN.md. */
+int daop_permute_workspace(int64_t t, int32_t k, int32_t num_experts, int64_t* h_bytes);
+int daop_permute(const int32_t* d_topk_idx, int64_t t, int32_t k, int32_t num_experts,
+                 const uint16_t* d_x, int32_t d, int64_t* d_offsets, int32_t* d_perm,
+                 int32_t* d_inv, uint16_t* d_x_perm, void* d_workspace, int64_t ws_bytes,
+                 daop_stream_t stream);
+/* d_out[t] = d_h[t] + sum_{j<k} d_w[t,j] * d_y[d_inv[t,j]]   (fixed j order) */
+int daop_combine(const float* d_h, const float* d_y_sorted, const int32_t* d_inv,
+                 const float* d_w, int64_t t, int32_t k, int32_t d, float* d_out,
+                 daop_stream_t stream);
+
+/* ------------------------------------------------ grouped expert GEMMs (prefill)
+ * tcgen05/TMEM/TMA grouped GEMMs over expert-sorted rows.  Expert e owns rows
+ * [d_offsets[e], d_offsets[e+1]) and its weights live in slab slot
+ * d_slot_of[e]; a slot is [W1 (ffn,d) | W3 (ffn,d) | W2 (d,ffn)] bf16.
+ *   up:   d_act (rows, ffn) bf16 = silu(x W1^T) * (x W3^T)
+ *   down: d_y   (rows, d)   f32  = act W2^T
+ * group_m <= 0 picks the default rasterisation group. */
+int daop_expert_gemm_up(const uint16_t* d_x_perm, int64_t rows, int32_t d, int32_t ffn,
+                        const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
+                        const int64_t* d_offsets, const int32_t* d_slot_of, int32_t num_experts,
+                        uint16_t* d_act, int32_t group_m, daop_stream_t stream);
+int daop_expert_gemm_down(const uint16_t* d_act, int64_t rows, int32_t d, int32_t ffn,
+                          const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
+                          const int64_t* d_offsets, const int32_t* d_slot_of,
+                          int32_t num_experts, float* d_y, int32_t group_m,
+                          daop_stream_t stream);
+
+/* ------------------------------------------------ decode layer (b = 1)
+ * One persistent cooperative launch: RMSNorm + gate + next-layer gate, the
+ * selection (mode 0: true top-k -- Fiddler / l < start; mode 1: DAOP plan
+ * from d_pred_prev with graceful degradation, policies.py:299-336), then the
+ * HBM-streaming SwiGLU GEMV of every HBM-resident pick and the combine
+ * d_h_out = d_h + sum_q w_q y_q (written only when every pick is resident;
+ * otherwise d_y holds the resident picks' outputs for an external combine
+ * with the slow tier).  d_deg: drop[k] | sub[k] | count.
+ * d_workspace: daop_decode_workspace() bytes, zeroed once, self-resetting. */
+int daop_decode_workspace(int32_t d, int32_t ffn, int32_t num_experts, int32_t k,
+                          int64_t* h_bytes);
+int daop_decode_layer(const float* d_h, const uint16_t* d_gamma, const uint16_t* d_wg,
+                      const uint16_t* d_wg_next, const float* d_pred_prev,
+                      const uint8_t* d_fast_row, const int32_t* d_slot_of,
+                      const uint16_t* d_slab, int64_t slot_stride_elems, int32_t d, int32_t ffn,
+                      int32_t num_experts, int32_t k, int32_t mode, int32_t graceful,
+                      int32_t weights_from_pred, float eps, uint16_t* d_x_out, float* d_p_true,
+                      float* d_p_pred, int32_t* d_sel, float* d_w, uint8_t* d_is_fast,
+                      int32_t* d_deg, float* d_y, float* d_h_out, void* d_workspace,
+                      int32_t grid, daop_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -37,6 +37,15 @@ PROTOS = {
     "daop_fill_uniform_f32": [P, I64, U64, U64, F32, I64, P],
     "daop_fill_norm_bf16": [P, I64, U64, I32, P],
     "daop_fill_uniform_bf16_host": [P, I64, U64, U64, F32, I64, I32],
+    "daop_router": [P, P, P, P, I64, I32, I32, I32, F32, P, P, P, P, P, P, I64, I64, P],
+    "daop_permute_workspace": [I64, I32, I32, P],
+    "daop_permute": [P, I64, I32, I32, P, I32, P, P, P, P, P, I64, P],
+    "daop_combine": [P, P, P, P, I64, I32, I32, P, P],
+    "daop_expert_gemm_up": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
+    "daop_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
+    "daop_decode_workspace": [I32, I32, I32, I32, P],
+    "daop_decode_layer": [P, P, P, P, P, P, P, P, I64, I32, I32, I32, I32, I32, I32, I32, F32,
+                          P, P, P, P, P, P, P, P, P, P, I32, P],
 }
 
 _CODES = {

@@ -1,0 +1,370 @@
+// Grouped SwiGLU expert FFN for prefill on the 5th-gen tensor cores.
+//
+// Two persistent, warp-specialised tcgen05 GEMMs over the expert-sorted token
+// rows produced by the permutation (offsets[e] .. offsets[e+1] belong to
+// expert e; the weights of expert e live in HBM slot slot_of[e] of the slab):
+//
+//   up   : act[r, :] = bf16( silu(x_r . W1_e^T) * (x_r . W3_e^T) )   K = d
+//          one 128x256 tile = 128 W1 rows + the matching 128 W3 rows, so the
+//          SwiGLU is applied in the epilogue straight out of TMEM.
+//   down : y[r, :]   = act_r . W2_e^T  (fp32)                          K = ffn
+//
+// Roles per CTA (one CTA per SM, 192 threads):
+//   warp 0     TMA producer: A box 64x128 + two B boxes 64x128 per stage
+//              (cp.async.bulk.tensor, SWIZZLE_128B), 4-stage mbarrier ring
+//   warp 1     MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16
+//              M=128 N=256 K=16 (x4 per stage) into a TMEM accumulator,
+//              tcgen05.commit frees the smem stage / publishes the accumulator
+//   warps 2-5  epilogue: tcgen05.ld 32x32b -> registers -> SwiGLU / fp32 store;
+//              two TMEM accumulators (2 x 256 columns) double-buffer MMA vs
+//              epilogue.
+// Tiles are (expert, m-tile, n-tile), rasterised in groups of G m-tiles so
+// the weight tile is shared in L2 by the CTAs working on the same group.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+namespace daop {
+
+constexpr int GB_M = 128, GB_N = 256, GB_K = 64, G_STAGES = 4;
+constexpr int G_A_BYTES = GB_M * GB_K * 2;               // 16 KB
+constexpr int G_B_BYTES = GB_N * GB_K * 2;               // 32 KB
+constexpr int G_STAGE_BYTES = G_A_BYTES + G_B_BYTES;      // 48 KB
+constexpr int G_THREADS = 192;
+constexpr int G_MAX_EXPERTS = 64;
+constexpr uint32_t G_IDESC = umma_idesc_bf16_f32(GB_M, GB_N);
+
+struct GemmParams {
+  const int64_t* offsets;  // [E+1] expert row offsets (device)
+  const int32_t* slot_of;  // [E] HBM slot of each expert (device)
+  int E;
+  int k_blocks;    // K / 64
+  int n_tiles;     // output tiles per expert
+  int group_m;     // rasterisation group
+  int b_tile_rows; // B row advance per n-tile (up: 128, down: 256)
+  int b_half2;     // B row offset of the second 128-row box (up: ffn, down: 128)
+  void* out;       // up: bf16 act (rows, out_ld); down: fp32 y (rows, out_ld)
+  int64_t out_ld;
+  int out_cols_per_tile;  // up: 128, down: 256
+};
+
+struct GemmSmem {
+  uint64_t full[G_STAGES];
+  uint64_t empty[G_STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  int32_t prefix[G_MAX_EXPERTS + 1];  // tile prefix over experts
+  int32_t mt[G_MAX_EXPERTS];           // m-tiles per expert
+  int64_t off[G_MAX_EXPERTS + 1];
+};
+
+__device__ __forceinline__ bool map_tile(const GemmSmem& s, int E, int nt, int G, int t, int& e,
+                                         int& m, int& n) {
+  if (t >= s.prefix[E]) return false;
+  e = 0;
+  while (s.prefix[e + 1] <= t) ++e;
+  const int u = t - s.prefix[e];
+  const int grp = u / (G * nt);
+  const int r = u - grp * G * nt;
+  const int gm = min(G, s.mt[e] - grp * G);
+  m = grp * G + r % gm;
+  n = r / gm;
+  return true;
+}
+
+template <bool SWIGLU>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  // SWIZZLE_128B needs 1024-byte aligned tiles
+  const uint32_t base_u32 = smem_u32(smem_raw);
+  uint8_t* tiles = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+  GemmSmem& s = *reinterpret_cast<GemmSmem*>(tiles + G_STAGES * G_STAGE_BYTES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = p.E;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < G_STAGES; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s.tfull[i], 1);
+      mbar_init(&s.tempty[i], 4);
+    }
+    fence_mbar_init();
+    int acc = 0;
+    s.prefix[0] = 0;
+    for (int e = 0; e <= E; ++e) s.off[e] = p.offsets[e];
+    for (int e = 0; e < E; ++e) {
+      const int64_t me = s.off[e + 1] - s.off[e];
+      s.mt[e] = static_cast<int>((me + GB_M - 1) / GB_M);
+      acc += s.mt[e] * p.n_tiles;
+      s.prefix[e + 1] = acc;
+    }
+  }
+  if (warp == 2) tmem_alloc<512>(&s.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = s.tmem_base;
+  const int nt = p.n_tiles, G = p.group_m;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_a = l2_evict_last_policy();
+      const uint64_t pol_b = l2_evict_last_policy();
+      int stage = 0;
+      uint32_t phase = 0;
+      int e, m, n;
+      for (int t = blockIdx.x; map_tile(s, E, nt, G, t, e, m, n); t += gridDim.x) {
+        const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * GB_M);
+        const int slot = p.slot_of[e];
+        const int brow = n * p.b_tile_rows;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&s.empty[stage], phase ^ 1);
+          uint8_t* st = tiles + stage * G_STAGE_BYTES;
+          mbar_arrive_expect_tx(&s.full[stage], G_STAGE_BYTES);
+          tma_load_2d(st, &tmA, &s.full[stage], kb * GB_K, row0, pol_a);
+          tma_load_3d(st + G_A_BYTES, &tmB, &s.full[stage], kb * GB_K, brow, slot, pol_b);
+          tma_load_3d(st + G_A_BYTES + G_B_BYTES / 2, &tmB, &s.full[stage], kb * GB_K,
+                      brow + p.b_half2, slot, pol_b);
+          if (++stage == G_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      int e, m, n;
+      for (int t = blockIdx.x; map_tile(s, E, nt, G, t, e, m, n); t += gridDim.x) {
+        mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * GB_N;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&s.full[stage], phase);
+          tc_fence_after();
+          uint8_t* st = tiles + stage * G_STAGE_BYTES;
+          const uint64_t adesc = umma_desc_sw128(smem_u32(st));
+          const uint64_t bdesc = umma_desc_sw128(smem_u32(st + G_A_BYTES));
+#pragma unroll
+          for (int k = 0; k < GB_K / 16; ++k)  // +32 bytes along K per UMMA_K=16
+            umma_bf16(tmem_d, adesc + 2 * k, bdesc + 2 * k, G_IDESC, (kb | k) != 0);
+          umma_commit(&s.empty[stage]);
+          if (++stage == G_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&s.tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int e, m, n;
+    for (int t = blockIdx.x; map_tile(s, E, nt, G, t, e, m, n); t += gridDim.x) {
+      mbar_wait(&s.tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row_in_tile = q * 32 + lane;
+      const int64_t me = s.off[e + 1] - s.off[e];
+      const bool valid = static_cast<int64_t>(m) * GB_M + row_in_tile < me;
+      const int64_t grow = s.off[e] + static_cast<int64_t>(m) * GB_M + row_in_tile;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * GB_N;
+      if constexpr (SWIGLU) {
+        uint16_t* out = static_cast<uint16_t*>(p.out) + grow * p.out_ld + n * 128;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tb + c, g);
+          tmem_ld32(tb + 128 + c, u);
+          tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = __uint_as_float(g[2 * i]), a1 = __uint_as_float(g[2 * i + 1]);
+            const float b0 = __uint_as_float(u[2 * i]), b1 = __uint_as_float(u[2 * i + 1]);
+            const float h0 = silu_f32(a0) * b0, h1 = silu_f32(a1) * b1;
+            packed[i] = static_cast<uint32_t>(f32_to_bf16_bits(h0)) |
+                        (static_cast<uint32_t>(f32_to_bf16_bits(h1)) << 16);
+          }
+          if (valid) {
+            uint4* o = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
+        }
+      } else {
+        float* out = static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
+#pragma unroll 1
+        for (int c = 0; c < GB_N; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tb + c, v);
+          tmem_ld_wait();
+          if (valid) {
+            float4* o = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              o[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                   const uint64_t* strides_bytes, const uint32_t* box) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return DAOP_ERR_CUDA;
+  }
+  cuuint64_t gd[3], gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs,
+                   bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return DAOP_ERR_CUDA;
+  }
+  return DAOP_OK;
+}
+
+static size_t gemm_smem_bytes() { return 1024 + G_STAGES * G_STAGE_BYTES + sizeof(GemmSmem); }
+
+template <bool SWIGLU>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                       int64_t rows_total, cudaStream_t st) {
+  const size_t smem = gemm_smem_bytes();
+  DAOP_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<SWIGLU>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  const int64_t max_tiles = (rows_total / GB_M + p.E) * static_cast<int64_t>(p.n_tiles);
+  int grid = sm_count();
+  if (max_tiles < grid) grid = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
+  grouped_gemm_kernel<SWIGLU><<<grid, G_THREADS, smem, st>>>(ta, tb, p);
+  DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_up" : "grouped_gemm_down");
+  return DAOP_OK;
+}
+
+}  // namespace daop
+
+using namespace daop;
+
+static int check_ffn_shape(int64_t rows, int32_t d, int32_t ffn, int32_t E) {
+  if (E < 1 || E > G_MAX_EXPERTS || d % 256 != 0 || ffn % 128 != 0 || d < 64 || ffn < 64 ||
+      rows >= (1ll << 31)) {
+    set_error("expert GEMM: unsupported shape (rows=%lld d=%d ffn=%d E=%d): needs d %% 256 == 0, "
+              "ffn %% 128 == 0, E <= %d",
+              static_cast<long long>(rows), d, ffn, E, G_MAX_EXPERTS);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  return DAOP_OK;
+}
+
+extern "C" int daop_expert_gemm_up(const uint16_t* x_perm, int64_t rows, int32_t d, int32_t ffn,
+                                   const uint16_t* slab, int64_t n_slots,
+                                   int64_t slot_stride_elems, const int64_t* d_offsets,
+                                   const int32_t* d_slot_of, int32_t E, uint16_t* act,
+                                   int32_t group_m, daop_stream_t stream) {
+  int rc = check_ffn_shape(rows, d, ffn, E);
+  if (rc) return rc;
+  if (rows == 0) return DAOP_OK;
+  CUtensorMap ta, tb;
+  const uint64_t adims[2] = {static_cast<uint64_t>(d), static_cast<uint64_t>(rows)};
+  const uint64_t astr[1] = {static_cast<uint64_t>(d) * 2};
+  const uint32_t abox[2] = {GB_K, GB_M};
+  if ((rc = make_tmap_bf16(&ta, x_perm, 2, adims, astr, abox))) return rc;
+  const uint64_t bdims[3] = {static_cast<uint64_t>(d), static_cast<uint64_t>(2 * ffn),
+                             static_cast<uint64_t>(n_slots)};
+  const uint64_t bstr[2] = {static_cast<uint64_t>(d) * 2,
+                            static_cast<uint64_t>(slot_stride_elems) * 2};
+  const uint32_t bbox[3] = {GB_K, 128, 1};
+  if ((rc = make_tmap_bf16(&tb, slab, 3, bdims, bstr, bbox))) return rc;
+  GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : 64,
+               128, ffn, act, ffn, 128};
+  return launch_gemm<true>(ta, tb, p, rows, as_stream(stream));
+}
+
+extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t d, int32_t ffn,
+                                     const uint16_t* slab, int64_t n_slots,
+                                     int64_t slot_stride_elems, const int64_t* d_offsets,
+                                     const int32_t* d_slot_of, int32_t E, float* y,
+                                     int32_t group_m, daop_stream_t stream) {
+  int rc = check_ffn_shape(rows, d, ffn, E);
+  if (rc) return rc;
+  if (rows == 0) return DAOP_OK;
+  CUtensorMap ta, tb;
+  const uint64_t adims[2] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(rows)};
+  const uint64_t astr[1] = {static_cast<uint64_t>(ffn) * 2};
+  const uint32_t abox[2] = {GB_K, GB_M};
+  if ((rc = make_tmap_bf16(&ta, act, 2, adims, astr, abox))) return rc;
+  const uint64_t bdims[3] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(d),
+                             static_cast<uint64_t>(n_slots)};
+  const uint64_t bstr[2] = {static_cast<uint64_t>(ffn) * 2,
+                            static_cast<uint64_t>(slot_stride_elems) * 2};
+  const uint32_t bbox[3] = {GB_K, 128, 1};
+  const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
+  if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
+  GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, group_m > 0 ? group_m : 16,
+               GB_N, 128, y, d, GB_N};
+  return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
+}

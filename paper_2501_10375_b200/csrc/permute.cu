@@ -1,0 +1,193 @@
+// Token -> expert permutation by histogram + exclusive scan, and the
+// weighted combine / unpermute.
+//
+// Order contract (deterministic, stable): the T*k assignments (t, j) are
+// sorted by (expert, t, j).  offsets[e] is the exclusive scan of the expert
+// histogram; perm[p] = t*k + j of the row at sorted position p; inv[t*k+j] =
+// p.  x_perm[p] = x[t] feeds the grouped GEMM's A operand through TMA.
+//
+//   count   : per-CTA expert histograms of contiguous assignment chunks
+//   scan    : one CTA, exclusive scan over (expert, chunk) -> chunk bases
+//   scatter : per chunk, stable in-chunk ranks with __match_any_sync,
+//             warp totals prefix-summed in shared memory
+//   gather  : one warp per sorted row, 16-byte coalesced row copy
+//   combine : h'[t] = h[t] + sum_{j=0..k-1} w[t,j] * y[inv[t,j]]  (fixed j order)
+#include "common.cuh"
+
+namespace daop {
+
+constexpr int P_THREADS = 256;
+constexpr int P_MAX_E = 256;
+
+__global__ void perm_count_kernel(const int32_t* __restrict__ ids, int64_t n, int64_t chunk, int E,
+                                  int32_t* __restrict__ counts /* [chunks][E] */) {
+  __shared__ int32_t h[P_MAX_E];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t a = blockIdx.x * chunk, b = min(n, a + chunk);
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) atomicAdd(&h[ids[i]], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) counts[blockIdx.x * (int64_t)E + i] = h[i];
+}
+
+__global__ void perm_scan_kernel(int32_t* __restrict__ counts, int nchunks, int E,
+                                 int64_t* __restrict__ offsets) {
+  // thread e: serial scan over chunks of expert e (totals), then thread 0 scans experts
+  __shared__ int64_t tot[P_MAX_E + 1];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int64_t s = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int32_t v = counts[c * (int64_t)E + e];
+      counts[c * (int64_t)E + e] = static_cast<int32_t>(s);  // in-expert base of chunk c
+      s += v;
+    }
+    tot[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t s = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = s;
+      s += tot[e];
+    }
+    offsets[E] = s;
+  }
+}
+
+__global__ void perm_scatter_kernel(const int32_t* __restrict__ ids, int64_t n, int64_t chunk,
+                                    int E, const int32_t* __restrict__ chunk_base,
+                                    const int64_t* __restrict__ offsets,
+                                    int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+  __shared__ int32_t run[P_MAX_E];                   // running count per expert in this chunk
+  __shared__ int32_t wtot[P_THREADS / 32][P_MAX_E];  // per-warp totals of the current tile
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) run[i] = 0;
+  const int64_t a = blockIdx.x * chunk, b = min(n, a + chunk);
+  for (int64_t base = a; base < b; base += P_THREADS) {
+    for (int i = threadIdx.x; i < (P_THREADS / 32) * E; i += blockDim.x)
+      wtot[i / E][i % E] = 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    const bool ok = i < b;
+    const int e = ok ? ids[i] : -1 - lane;  // distinct dummies never match real ids
+    const unsigned same = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(same & ((1u << lane) - 1u));
+    if (ok && rank == 0) wtot[warp][e] = __popc(same);
+    __syncthreads();
+    if (ok) {
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += wtot[w][e];
+      const int64_t pos = offsets[e] + chunk_base[blockIdx.x * (int64_t)E + e] + run[e] + before + rank;
+      perm[pos] = static_cast<int32_t>(i);
+      inv[i] = static_cast<int32_t>(pos);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < E; x += blockDim.x) {
+      int s = 0;
+      for (int w = 0; w < P_THREADS / 32; ++w) s += wtot[w][x];
+      run[x] += s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void perm_gather_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ perm,
+                                   int64_t rows, int k, int n16, uint4* __restrict__ x_perm) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t src = perm[r] / k;
+    const uint4* s = x + src * n16;
+    uint4* d = x_perm + r * n16;
+    for (int c = lane; c < n16; c += 32) d[c] = s[c];
+  }
+}
+
+__global__ void combine_kernel(const float* __restrict__ h, const float* __restrict__ y,
+                               const int32_t* __restrict__ inv, const float* __restrict__ w,
+                               int64_t T, int k, int d4, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const float4* hr = reinterpret_cast<const float4*>(h) + t * d4;
+    float4* o = reinterpret_cast<float4*>(out) + t * d4;
+    for (int c = lane; c < d4; c += 32) {
+      float4 acc = hr[c];
+      for (int j = 0; j < k; ++j) {
+        const float wj = w[t * k + j];
+        const float4 v = reinterpret_cast<const float4*>(y)[static_cast<int64_t>(inv[t * k + j]) * d4 + c];
+        acc.x = fmaf(wj, v.x, acc.x);
+        acc.y = fmaf(wj, v.y, acc.y);
+        acc.z = fmaf(wj, v.z, acc.z);
+        acc.w = fmaf(wj, v.w, acc.w);
+      }
+      o[c] = acc;
+    }
+  }
+}
+
+}  // namespace daop
+
+using namespace daop;
+
+extern "C" {
+
+int daop_permute_workspace(int64_t T, int32_t k, int32_t E, int64_t* bytes) {
+  const int64_t n = T * k;
+  int64_t chunks = (n + 4095) / 4096;
+  if (chunks < 1) chunks = 1;
+  *bytes = chunks * E * 4 + 256;
+  return DAOP_OK;
+}
+
+int daop_permute(const int32_t* ids, int64_t T, int32_t k, int32_t E, const uint16_t* x, int32_t d,
+                 int64_t* offsets, int32_t* perm, int32_t* inv, uint16_t* x_perm,
+                 void* workspace, int64_t ws_bytes, daop_stream_t stream) {
+  if (E < 1 || E > P_MAX_E || k < 1 || (x_perm && d % 8 != 0)) {
+    set_error("permute: unsupported (E=%d, k=%d, d=%d)", E, k, d);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  const int64_t n = T * k;
+  int64_t need = 0;
+  daop_permute_workspace(T, k, E, &need);
+  if (ws_bytes < need) {
+    set_error("permute: workspace %lld < %lld bytes", (long long)ws_bytes, (long long)need);
+    return DAOP_ERR_SHAPE;
+  }
+  cudaStream_t st = as_stream(stream);
+  const int64_t chunk = 4096;
+  int nchunks = static_cast<int>((n + chunk - 1) / chunk);
+  if (nchunks < 1) nchunks = 1;
+  int32_t* counts = static_cast<int32_t*>(workspace);
+  perm_count_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts);
+  perm_scan_kernel<<<1, 256, 0, st>>>(counts, nchunks, E, offsets);
+  if (n > 0) perm_scatter_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts, offsets, perm, inv);
+  DAOP_CHECK_LAUNCH("permute");
+  if (x_perm && n > 0) {
+    int64_t blocks = (n * 32 + 255) / 256;
+    const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+    if (blocks > cap) blocks = cap;
+    perm_gather_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(
+        reinterpret_cast<const uint4*>(x), perm, n, k, d / 8, reinterpret_cast<uint4*>(x_perm));
+    DAOP_CHECK_LAUNCH("permute_gather");
+  }
+  return DAOP_OK;
+}
+
+int daop_combine(const float* h, const float* y_sorted, const int32_t* inv, const float* w,
+                 int64_t T, int32_t k, int32_t d, float* out, daop_stream_t stream) {
+  if (d % 4 != 0) {
+    set_error("combine: d must be a multiple of 4");
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (T == 0) return DAOP_OK;
+  int64_t blocks = (T * 32 + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+  if (blocks > cap) blocks = cap;
+  combine_kernel<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(h, y_sorted, inv, w, T, k,
+                                                                          d / 4, out);
+  DAOP_CHECK_LAUNCH("combine");
+  return DAOP_OK;
+}
+
+}  // extern "C"

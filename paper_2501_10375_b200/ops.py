@@ -1,0 +1,159 @@
+"""Device operations of the MoE-block hot path (torch CUDA tensors in/out).
+
+Each function is a thin marshalling layer over one C-ABI entry point of
+libdaop_b200.so -- torch owns device memory and streams, the kernels do the
+work.  No function here has a CPU path: inputs must already be on the
+device, and a missing device raises DeviceError.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .errors import DeviceError, ShapeMismatchError
+
+RMS_EPS = 1e-5
+
+
+def _dev(*ts):
+    for t in ts:
+        if t is not None and (not isinstance(t, torch.Tensor) or not t.is_cuda):
+            raise DeviceError("hot-path ops take CUDA tensors (there is no CPU fallback)")
+        if t is not None and not t.is_contiguous():
+            raise ShapeMismatchError("hot-path ops take contiguous tensors")
+
+
+def _p(t):
+    return 0 if t is None else t.data_ptr()
+
+
+def _s():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def fill_uniform_bf16(out: torch.Tensor, seed: int, tag: int, scale: float, offset: int = 0):
+    _dev(out)
+    _lib.call("daop_fill_uniform_bf16", out.data_ptr(), out.numel(), seed, tag, float(scale),
+              offset, _s())
+    return out
+
+
+def fill_uniform_f32(out: torch.Tensor, seed: int, tag: int, scale: float, offset: int = 0):
+    _dev(out)
+    _lib.call("daop_fill_uniform_f32", out.data_ptr(), out.numel(), seed, tag, float(scale),
+              offset, _s())
+    return out
+
+
+def fill_norm_bf16(out: torch.Tensor, seed: int, layer: int):
+    _dev(out)
+    _lib.call("daop_fill_norm_bf16", out.data_ptr(), out.numel(), seed, layer, _s())
+    return out
+
+
+def router(h, gamma, wg, wg_next, k, *, hist=None, tokens_per_seq=0, hist_seq_stride=0,
+           write_x=True, eps=RMS_EPS):
+    """Fused router over T tokens (see daop_router)."""
+    _dev(h, gamma, wg, wg_next)
+    if hist is not None and not hist.is_cuda:  # hist may be a strided (seq, E) view
+        raise DeviceError("hist must live on the device")
+    t, d = h.shape
+    e = wg.shape[0]
+    dev = h.device
+    x = torch.empty((t, d), dtype=torch.bfloat16, device=dev) if write_x else None
+    p = torch.empty((t, e), dtype=torch.float32, device=dev)
+    pp = torch.empty((t, e), dtype=torch.float32, device=dev) if wg_next is not None else None
+    idx = torch.empty((t, k), dtype=torch.int32, device=dev)
+    w = torch.empty((t, k), dtype=torch.float32, device=dev)
+    _lib.call("daop_router", h.data_ptr(), gamma.data_ptr(), wg.data_ptr(), _p(wg_next), t, d,
+              e, k, float(eps), _p(x), p.data_ptr(), _p(pp), idx.data_ptr(), w.data_ptr(),
+              _p(hist), int(tokens_per_seq), int(hist_seq_stride), _s())
+    return {"x": x, "p": p, "p_pred": pp, "topk_idx": idx, "topk_w": w}
+
+
+def permute(topk_idx, num_experts, x=None):
+    """Stable (expert, token, j) permutation; gathers x rows when given."""
+    _dev(topk_idx, x)
+    t, k = topk_idx.shape
+    dev = topk_idx.device
+    ws_bytes = torch.zeros(1, dtype=torch.int64)
+    _lib.call("daop_permute_workspace", t, k, num_experts, ws_bytes.data_ptr())
+    ws = torch.empty(int(ws_bytes[0]), dtype=torch.uint8, device=dev)
+    offsets = torch.empty(num_experts + 1, dtype=torch.int64, device=dev)
+    perm = torch.empty(t * k, dtype=torch.int32, device=dev)
+    inv = torch.empty(t * k, dtype=torch.int32, device=dev)
+    x_perm = None
+    d = 0
+    if x is not None:
+        d = x.shape[1]
+        x_perm = torch.empty((t * k, d), dtype=x.dtype, device=dev)
+    _lib.call("daop_permute", topk_idx.data_ptr(), t, k, num_experts, _p(x), d,
+              offsets.data_ptr(), perm.data_ptr(), inv.data_ptr(), _p(x_perm), ws.data_ptr(),
+              ws.numel(), _s())
+    return {"offsets": offsets, "perm": perm, "inv": inv.view(t, k), "x_perm": x_perm}
+
+
+def expert_gemm_up(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, group_m=0):
+    _dev(x_perm, offsets, slot_of, slab)
+    rows = x_perm.shape[0]
+    act = torch.empty((rows, ffn), dtype=torch.bfloat16, device=x_perm.device)
+    _lib.call("daop_expert_gemm_up", x_perm.data_ptr(), rows, d, ffn, slab.data_ptr(), n_slots,
+              slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
+              act.data_ptr(), group_m, _s())
+    return act
+
+
+def expert_gemm_down(act, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, group_m=0):
+    _dev(act, offsets, slot_of, slab)
+    rows = act.shape[0]
+    y = torch.empty((rows, d), dtype=torch.float32, device=act.device)
+    _lib.call("daop_expert_gemm_down", act.data_ptr(), rows, d, ffn, slab.data_ptr(), n_slots,
+              slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
+              y.data_ptr(), group_m, _s())
+    return y
+
+
+def combine(h, y_sorted, inv, w, out=None):
+    _dev(h, y_sorted, inv, w, out)
+    t, d = h.shape
+    k = inv.shape[1]
+    out = torch.empty_like(h) if out is None else out
+    _lib.call("daop_combine", h.data_ptr(), y_sorted.data_ptr(), inv.data_ptr(), w.data_ptr(),
+              t, k, d, out.data_ptr(), _s())
+    return out
+
+
+class DecodeBuffers:
+    """Preallocated outputs + self-resetting workspace of one decode layer call
+    (fixed addresses, so a decode step can be captured in a CUDA graph)."""
+
+    def __init__(self, d, ffn, num_experts, k, device):
+        nb = torch.zeros(1, dtype=torch.int64)
+        _lib.call("daop_decode_workspace", d, ffn, num_experts, k, nb.data_ptr())
+        self.ws = torch.zeros(int(nb[0]), dtype=torch.uint8, device=device)
+        f32 = dict(dtype=torch.float32, device=device)
+        self.x = torch.empty(d, dtype=torch.bfloat16, device=device)
+        self.p = torch.empty(num_experts, **f32)
+        self.p_pred = torch.empty(num_experts, **f32)
+        self.sel = torch.empty(k, dtype=torch.int32, device=device)
+        self.w = torch.empty(k, **f32)
+        self.is_fast = torch.empty(k, dtype=torch.uint8, device=device)
+        self.deg = torch.empty(2 * k + 1, dtype=torch.int32, device=device)
+        self.y = torch.zeros((k, d), **f32)
+        self.h_out = torch.empty(d, **f32)
+
+
+def decode_layer(h, gamma, wg, wg_next, fast_row, slot_of, slab, slot_elems, d, ffn, k,
+                 bufs: DecodeBuffers, *, pred_prev=None, mode=0, graceful=True,
+                 weights_from_pred=False, grid=0, eps=RMS_EPS):
+    """One decode token through one MoE layer in a single launch."""
+    _dev(h, gamma, wg, wg_next, pred_prev, fast_row, slot_of, slab)
+    e = wg.shape[0]
+    _lib.call("daop_decode_layer", h.data_ptr(), gamma.data_ptr(), wg.data_ptr(), _p(wg_next),
+              _p(pred_prev), fast_row.data_ptr(), slot_of.data_ptr(), slab.data_ptr(),
+              slot_elems, d, ffn, e, k, mode, int(graceful), int(weights_from_pred), float(eps),
+              bufs.x.data_ptr(), bufs.p.data_ptr(), bufs.p_pred.data_ptr(), bufs.sel.data_ptr(),
+              bufs.w.data_ptr(), bufs.is_fast.data_ptr(), bufs.deg.data_ptr(),
+              bufs.y.data_ptr(), bufs.h_out.data_ptr(), bufs.ws.data_ptr(), grid, _s())
+    return bufs
