@@ -172,6 +172,10 @@ int daop_expert_gemm_down(const uint16_t* d_act, int64_t rows, int32_t d, int32_
  * otherwise d_y holds the resident picks' outputs for an external combine
  * with the slow tier).  d_deg: drop[k] | sub[k] | count.
  * d_workspace: daop_decode_workspace() bytes, zeroed once, self-resetting. */
+/* profiling aid: enable (1) / read back the per-CTA phase timeline of the
+ * last decode_layer launches (globaltimer ns: start, selection, phase-1 done,
+ * barrier released, end); enabling also clears it. */
+int daop_decode_timeline(int32_t enable, uint64_t* h_out, int32_t n_cta);
 int daop_decode_workspace(int32_t d, int32_t ffn, int32_t num_experts, int32_t k,
                           int64_t* h_bytes);
 int daop_decode_layer(const float* d_h, const uint16_t* d_gamma, const uint16_t* d_wg,

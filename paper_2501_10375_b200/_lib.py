@@ -44,6 +44,7 @@ PROTOS = {
     "daop_expert_gemm_up": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_decode_workspace": [I32, I32, I32, I32, P],
+    "daop_decode_timeline": [I32, P, I32],
     "daop_decode_layer": [P, P, P, P, P, P, P, P, I64, I32, I32, I32, I32, I32, I32, I32, F32,
                           P, P, P, P, P, P, P, P, P, P, I32, P],
 }
@@ -61,7 +62,7 @@ _CODES = {
 def _load():
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH.name} is not built; run `python -m paper_2501_10375_b200.build` "
+            f"{LIB_PATH.name} is not built; run `python paper_2501_10375_b200/build.py` "
             "(nvcc, sm_100a). There is no CPU fallback."
         )
     lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)

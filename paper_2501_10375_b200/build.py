@@ -1,6 +1,8 @@
 """Build libdaop_b200.so in-tree with nvcc for sm_100a (no GPU needed).
 
-    python -m paper_2501_10375_b200.build        # or __graft_entry__.build()
+    python paper_2501_10375_b200/build.py        # or __graft_entry__.build()
+
+(run by path: importing the package loads the library this script builds)
 
 Every ``csrc/*.cu`` is compiled with ``-gencode arch=compute_100a,code=sm_100a``
 only (``-arch=sm_100a`` would also emit compute_100 PTX, which ptxas rejects

@@ -115,6 +115,16 @@ __device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint3
       : "memory");
 }
 
+// non-coherent 16-byte global load issued exactly here (volatile: the
+// compiler may not sink it to the first use)
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 // ---------------------------------------------------------------- global sync
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {

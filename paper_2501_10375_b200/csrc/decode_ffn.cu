@@ -1,37 +1,43 @@
 // Decode MoE layer for one token: fused router + DAOP decision + HBM-streaming
-// SwiGLU expert GEMV + combine, in ONE persistent launch.
+// SwiGLU expert GEMV + combine, in ONE persistent launch with no grid barrier.
 //
-//   phase 0 (every CTA, redundant & bit-identical):
-//       x = bf16(rmsnorm(h) * gamma); z = x . Wg_l^T; p = softmax(z)
-//       selection: mode TRUE -> top-k(p)                   (l < start / fiddler)
-//                  mode PLAN -> top-k(pred_prev) + graceful degradation over
-//                               the layer's HBM residence   (DAOP l >= start,
-//                               policies.py:299-336 via decide.cuh)
-//       CTAs 0..E-1 also compute one row each of the next-layer gate
-//       (x . Wg_{l+1}^T -> p_pred) from the same x.
-//   phase 1: W1/W3 rows of every resident (fast) pick, streamed HBM -> smem
-//       by per-warp cp.async.bulk rings, dot with x, act = bf16(silu(g)*u).
-//   grid barrier -- every warp's ring is already streaming its first W2
-//       pieces while it waits, so the phase boundary does not drain HBM.
-//   phase 2: W2 rows (dot with act in smem) -> y[q, r]; the warp (or the last
-//       of the warps sharing a row) writes h'[r] = h[r] + sum_q w_q y[q, r]
-//       in fixed q order.
+// Phase 0 (every CTA, redundant and bit-identical across CTAs)
+//   mode 0 TRUE (l < start / fiddler): h, the E gate rows and (CTAs 0..E-1) one
+//     next-layer gate row land in shared memory with ONE bulk copy at t=0;
+//     x = bf16(rmsnorm(h) * gamma), p = softmax(x . Wg_l^T), selection =
+//     top-k(p) (ties -> lower id, moesim/_kernels.py:63-79), then streaming.
+//   mode 1 PLAN (DAOP l >= start): selection = top-k(pred_prev) + graceful
+//     degradation over the layer's HBM residence (policies.py:299-336 via
+//     decide.cuh) is known at t=0, so the weight stream starts immediately and
+//     the router (needed only for the exported trace and the next prediction)
+//     runs while the first weights are in flight.
+//   CTAs 0..E-1 each compute one row of the next-layer gate from the same x
+//   (PAPER.md:234); the last of them writes p_pred.
+// Phase 1: unit = (pick j, ffn row i) = W1[i] + W3[i]; act[j, i] =
+//   bf16(silu(W1 x) * (W3 x)).  Units are dealt to CTAs round-robin (u = cta +
+//   m * G) and to the CTA's warps dynamically (shared-memory ticket), so each
+//   pick's activations complete early and evenly across the grid.
+// Phase 2: the CTA owns a contiguous block of output rows; its pieces
+//   (pick j, row r, K-chunk c) are dealt to its warps dynamically, partial dot
+//   products are reduced in shared memory by the last arriving warp in fixed
+//   (j, c) order (deterministic), which writes y[q, r] and
+//   h'[r] = h[r] + sum_q w_q y[q, r].
+// The only grid-wide dependency is "all rows of pick j done" before a CTA
+// pulls act_j into shared memory (one counter per pick, one bulk copy per CTA
+// per pick) -- the weight rings never drain at the phase boundary.
 //
-// Bytes per call (Mixtral-8x7B, 2 resident picks): 2 x 3 x 4096 x 14336 x 2 B
-// of weights + 2 x 8 x 4096 x 2 B of gates = 704,774,144 B -> HBM roofline.
-#include <cooperative_groups.h>
-
+// Each warp streams its weight pieces through its own cp.async.bulk ring
+// (DS stages x DSB bytes, L2 evict_first).  Bytes per call (Mixtral-8x7B,
+// 2 resident picks): 2 x 3 x 4096 x 14336 x 2 B of weights + 2 x 8 x 4096 x
+// 2 B of gates = 704,774,144 B -> HBM roofline.
 #include "common.cuh"
 #include "decide.cuh"
 
 namespace daop {
 
-constexpr int DW = 8;          // consumer warps per CTA, each with its own ring
-constexpr int DS = 2;          // ring stages per warp
-constexpr int DSB = 8192;      // bytes per stage (max piece)
-constexpr int DK_MAX = 8;      // max top-k
-constexpr int DE_MAX = 64;     // max experts
-constexpr int D_THREADS = DW * 32;
+constexpr int DK_MAX = 8;       // max top-k
+constexpr int DE_MAX = 64;      // max experts
+constexpr int kMaxChunks = 16;  // max W2 row pieces
 
 struct DecodeArgs {
   const float* h;          // (d) fp32 residual in
@@ -48,67 +54,79 @@ struct DecodeArgs {
   int graceful;
   int weights_from_pred;   // combine weights from pred_prev (PLAN) instead of p
   float eps;
-  // outputs
+  int rows_per_cta;        // phase-2 output rows per CTA (host computed)
   uint16_t* x_out;         // (d) bf16 normalised input (stale input for layer l+1)
   float* p_true;           // (E)
   float* p_pred;           // (E) or null
   int32_t* sel;            // (k)
   float* w;                // (k)
   uint8_t* is_fast;        // (k)
-  int32_t* deg;            // (2k): drop[k], sub[k]; deg[2k] = count
+  int32_t* deg;            // (2k + 1): drop[k] | sub[k] | count
   float* y;                // (k, d) per-pick expert outputs
   float* h_out;            // (d) combined residual (written when every pick is fast)
-  // workspace (zero-initialised once by the caller, self-resetting)
-  unsigned* sync;          // [0] arrive, [1] generation, [2..2+d) per-row counters
+  // self-resetting workspace (zeroed once by the caller)
+  unsigned* ctr;           // [0] finished CTAs, [1] pred rows, [2..2+DK_MAX) rows per pick
   float* pred_logits;      // (E)
   uint16_t* act;           // (k, ffn) bf16 SwiGLU activations
 };
 
+__device__ unsigned long long g_decode_timeline[1024][10];
+__device__ int g_decode_timeline_on;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct Piece {   // what one ring stage holds
+  int kind;      // 1 = W1/W3 piece, 2 = W2 piece, 0 = end of stream
+  int j, row, c; // pick (executed index), row, piece within the unit
+};
+
+template <int DW, int DS>
 struct DecodeSmem {
   uint64_t bar[DW][DS];
-  uint64_t act_bar;
+  uint64_t act_bar[DK_MAX];
+  uint64_t in_bar;
+  Piece rec[DW][DS];
+  int act_req[DK_MAX];
+  int p1_next, p2_next, fin;
+  int done1[DK_MAX];
   float red[DW];
   float z[DE_MAX];
   float p[DE_MAX];
+  float pp[DE_MAX];
+  int slot[DE_MAX];
+  uint8_t fast_row[DE_MAX];
   float wsel[DK_MAX];
   int sel[DK_MAX];
-  int exec_q[DK_MAX];      // pick index of the q-th executed (fast) pick
-  int n_exec;
-  int done1;
-  float rscale;
+  int exec_q[DK_MAX];
+  uint8_t fast[DK_MAX];
+  int n_exec, nd, drop[DK_MAX], sub[DK_MAX];
+  int pred_last;
 };
 
-struct PieceMap {
-  const uint16_t* base[DK_MAX];  // slot base of executed pick
-  int n_exec, d, ffn;
-  int npc1, pe1;  // pieces per W1/W3 row, elements per piece
-  int npc2, pe2;  // pieces per W2 row
-  int64_t u1a, u1b, u2a, u2b;  // unit ranges of this warp
-  int64_t n1, n;               // piece counts (phase 1, total)
+struct Layout {
+  const uint16_t* base[DK_MAX];
+  int n_exec, d, ffn, G, cta;
+  int npc1, pe1, npc2, pe2;
+  int n1c;         // phase-1 units of this CTA
+  int r0, R, P2c;  // phase-2 rows [r0, r0+R) and pieces of this CTA
 };
 
-// piece p of this warp -> source pointer, element count, vector offset
-__device__ __forceinline__ void piece_at(const PieceMap& m, int64_t p, const uint16_t*& src,
-                                         int& elems, int& voff) {
-  if (p < m.n1) {
-    const int64_t u = m.u1a + p / (2 * m.npc1);
-    const int q = static_cast<int>(p % (2 * m.npc1));
-    const int which = q / m.npc1, c = q % m.npc1;
-    const int j = static_cast<int>(u / m.ffn);
-    const int64_t i = u % m.ffn;
-    voff = c * m.pe1;
-    elems = min(m.pe1, m.d - voff);
-    src = m.base[j] + (static_cast<int64_t>(which) * m.ffn + i) * m.d + voff;
-  } else {
-    const int64_t p2 = p - m.n1;
-    const int64_t u = m.u2a + p2 / m.npc2;
-    const int c = static_cast<int>(p2 % m.npc2);
-    const int64_t r = u / m.n_exec;
-    const int j = static_cast<int>(u % m.n_exec);
-    voff = c * m.pe2;
-    elems = min(m.pe2, m.ffn - voff);
-    src = m.base[j] + 2ll * m.ffn * m.d + r * m.ffn + voff;
+__device__ __forceinline__ const uint16_t* piece_src(const Layout& L, const Piece& pc, int& elems,
+                                                     int& voff) {
+  if (pc.kind == 1) {
+    const int which = pc.c >= L.npc1;
+    const int c = pc.c - which * L.npc1;
+    voff = c * L.pe1;
+    elems = min(L.pe1, L.d - voff);
+    return L.base[pc.j] + (static_cast<int64_t>(which) * L.ffn + pc.row) * L.d + voff;
   }
+  voff = pc.c * L.pe2;
+  elems = min(L.pe2, L.ffn - voff);
+  return L.base[pc.j] + 2ll * L.ffn * L.d + static_cast<int64_t>(pc.row) * L.ffn + voff;
 }
 
 __device__ __forceinline__ float dot_piece(const uint4* wp, const uint4* vp, int n16, int lane,
@@ -118,283 +136,486 @@ __device__ __forceinline__ float dot_piece(const uint4* wp, const uint4* vp, int
   return acc;
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned* sync, unsigned nblocks) {
-  const unsigned gen = ld_acquire_gpu(sync + 1);
-  __threadfence();
-  const unsigned ticket = atom_add_acq_rel_gpu(sync, 1u);
-  if (ticket == nblocks - 1) {
-    sync[0] = 0;
-    st_release_gpu(sync + 1, gen + 1);
-  } else {
-    while (ld_acquire_gpu(sync + 1) == gen) __nanosleep(64);
+// number of u in [lo, hi) with u = cta (mod G)
+__device__ __forceinline__ int count_mod(int lo, int hi, int cta, int G) {
+  const int f = lo + ((cta - lo) % G + G) % G;
+  return hi > f ? (hi - 1 - f) / G + 1 : 0;
+}
+
+// warp-parallel softmax of E <= 32 logits (one per lane)
+__device__ __forceinline__ float warp_softmax(float z, int lane, int E) {
+  float m = lane < E ? z : -INFINITY;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float e = lane < E ? expf(z - m) : 0.f;
+  const float sum = warp_sum(e);
+  return lane < E ? e / sum : 0.f;
+}
+
+// warp-parallel top-k (E <= 32): max by value, ties to the lower index -- the
+// same order as topk_scan's strict '>' scan
+__device__ __noinline__ void warp_topk(float v, int lane, int E, int k, int* out) {
+  bool taken = lane >= E;
+  for (int j = 0; j < k; ++j) {
+    float bv = taken ? -INFINITY : v;
+    int bi = taken ? 0x7fffffff : lane;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) out[j] = bi;
+    if (lane == bi) taken = true;
   }
 }
 
-__global__ void __launch_bounds__(D_THREADS, 1) decode_layer_kernel(DecodeArgs a) {
+__device__ __noinline__ int degrade_smem(const float* s, int E, int* sel, int k,
+                                         const uint8_t* fast, int* drop, int* sub) {
+  return degrade(s, E, sel, k, fast, drop, sub);
+}
+
+__device__ __noinline__ void topk_scan_smem(const float* s, int E, int k, int* out) {
+  topk_scan(s, E, k, out);
+}
+
+__device__ __noinline__ void softmax_serial(const float* z, int E, float* p) {
+  float m = z[0], sum = 0.f;
+  for (int i = 1; i < E; ++i) m = fmaxf(m, z[i]);
+  for (int i = 0; i < E; ++i) sum += (p[i] = expf(z[i] - m));
+  for (int i = 0; i < E; ++i) p[i] = p[i] / sum;
+}
+
+template <int DW, int DS, int DSB>
+__global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) {
+  constexpr int NT = DW * 32;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* ring = smem;                                              // DW*DS*DSB
-  uint16_t* act_s = reinterpret_cast<uint16_t*>(smem + DW * DS * DSB);  // k*ffn
-  uint16_t* x_s = act_s + static_cast<size_t>(a.k) * a.ffn;             // d
-  DecodeSmem& s = *reinterpret_cast<DecodeSmem*>(
-      reinterpret_cast<uint8_t*>(x_s) + ((static_cast<size_t>(a.d) * 2 + 127) / 128) * 128);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = a.d, E = a.E, k = a.k;
+  uint8_t* ring = smem;                                                  // DW*DS*DSB
+  uint16_t* act_s = reinterpret_cast<uint16_t*>(smem + DW * DS * DSB);  // k*ffn
+  uint16_t* x_s = act_s + static_cast<size_t>(k) * a.ffn;               // d
+  float* part = reinterpret_cast<float*>(
+      reinterpret_cast<uint8_t*>(x_s) + ((static_cast<size_t>(d) * 2 + 127) / 128) * 128);
+  const int npc2_max = (a.ffn * 2 + DSB - 1) / DSB;
+  int* rcnt = reinterpret_cast<int*>(part + a.rows_per_cta * k * npc2_max);
+  auto& s = *reinterpret_cast<DecodeSmem<DW, DS>*>(
+      reinterpret_cast<uint8_t*>(rcnt) + ((a.rows_per_cta * 4 + 127) / 128) * 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool tl = g_decode_timeline_on != 0 && blockIdx.x < 1024;
+  const bool pred_row = a.wg_next && blockIdx.x < static_cast<unsigned>(E);
+
+  // staging of the router inputs in the (still idle) ring area, mode 0 only
+  float* h_s = reinterpret_cast<float*>(ring);
+  uint16_t* g_s = reinterpret_cast<uint16_t*>(ring + d * 4);
+  uint16_t* gp_s = g_s + static_cast<size_t>(E) * d;
 
   if (threadIdx.x == 0) {
+    if (tl) g_decode_timeline[blockIdx.x][0] = gtimer();
     for (int w = 0; w < DW; ++w)
       for (int q = 0; q < DS; ++q) mbar_init(&s.bar[w][q], 1);
-    mbar_init(&s.act_bar, 1);
+    for (int q = 0; q < DK_MAX; ++q) {
+      mbar_init(&s.act_bar[q], 1);
+      s.act_req[q] = 0;
+      s.done1[q] = 0;
+    }
+    mbar_init(&s.in_bar, 1);
+    s.p1_next = s.p2_next = s.fin = 0;
     fence_mbar_init();
-    s.done1 = 0;
-  }
-  // ---------------------------------------------------------------- phase 0
-  // RMSNorm: x = bf16(h * rsqrt(mean(h^2) + eps) * gamma)
-  float ss = 0.f;
-  const float4* h4 = reinterpret_cast<const float4*>(a.h);
-  for (int i = threadIdx.x; i < d / 4; i += D_THREADS) {
-    const float4 v = h4[i];
-    ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
-  }
-  ss = warp_sum(ss);
-  if (lane == 0) s.red[warp] = ss;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < DW; ++w) t += s.red[w];
-    s.rscale = 1.0f / sqrtf(t / static_cast<float>(d) + a.eps);
-  }
-  __syncthreads();
-  const float r = s.rscale;
-  for (int i = threadIdx.x; i < d / 2; i += D_THREADS) {
-    const float2 hv = reinterpret_cast<const float2*>(a.h)[i];
-    const uint32_t gw = reinterpret_cast<const uint32_t*>(a.gamma)[i];
-    const uint32_t lo = f32_to_bf16_bits(__fmul_rn(__fmul_rn(hv.x, r), bf16lo(gw)));
-    const uint32_t hi = f32_to_bf16_bits(__fmul_rn(__fmul_rn(hv.y, r), bf16hi(gw)));
-    reinterpret_cast<uint32_t*>(x_s)[i] = lo | (hi << 16);
-  }
-  __syncthreads();
-  if (blockIdx.x == 0 && a.x_out)
-    for (int i = threadIdx.x; i < d / 8; i += D_THREADS)
-      reinterpret_cast<uint4*>(a.x_out)[i] = reinterpret_cast<const uint4*>(x_s)[i];
-  // gate logits of this layer (warp per row) + one next-layer row per CTA < E
-  const int n16 = d / 8;
-  for (int e = warp; e < E; e += DW) {
-    const float acc = dot_piece(reinterpret_cast<const uint4*>(a.wg + static_cast<size_t>(e) * d),
-                                reinterpret_cast<const uint4*>(x_s), n16, lane, 0.f);
-    const float z = warp_sum(acc);
-    if (lane == 0) s.z[e] = z;
-  }
-  if (a.wg_next && blockIdx.x < static_cast<unsigned>(E) && warp == DW - 1) {
-    const int e = blockIdx.x;
-    const float acc = dot_piece(
-        reinterpret_cast<const uint4*>(a.wg_next + static_cast<size_t>(e) * d),
-        reinterpret_cast<const uint4*>(x_s), n16, lane, 0.f);
-    const float z = warp_sum(acc);
-    if (lane == 0) a.pred_logits[e] = z;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float m = s.z[0];
-    for (int i = 1; i < E; ++i) m = fmaxf(m, s.z[i]);
-    float sum = 0.f;
-    for (int i = 0; i < E; ++i) {
-      s.p[i] = expf(s.z[i] - m);
-      sum += s.p[i];
-    }
-    for (int i = 0; i < E; ++i) s.p[i] = s.p[i] / sum;
-    int sel[DK_MAX], drop[DK_MAX], sub[DK_MAX];
-    uint8_t fast[DK_MAX];
-    int nd = plan_layer(a.mode ? 1 : 0, s.p, a.pred_prev, a.mode == 1, a.fast_row, E, k, 1,
-                        a.mode == 1, a.graceful != 0, sel, fast, drop, sub);
-    const float* wsrc = (a.mode == 1 && a.weights_from_pred) ? a.pred_prev : s.p;
-    float den = 0.f;
-    for (int q = 0; q < k; ++q) den += wsrc[sel[q]];
-    int ne = 0;
-    for (int q = 0; q < k; ++q) {
-      s.sel[q] = sel[q];
-      s.wsel[q] = wsrc[sel[q]] / den;
-      if (fast[q]) s.exec_q[ne++] = q;
-    }
-    s.n_exec = ne;
-    if (blockIdx.x == 0) {
-      for (int i = 0; i < E; ++i) a.p_true[i] = s.p[i];
-      for (int q = 0; q < k; ++q) {
-        a.sel[q] = sel[q];
-        a.w[q] = s.wsel[q];
-        a.is_fast[q] = fast[q];
-        a.deg[q] = q < nd ? drop[q] : -1;
-        a.deg[k + q] = q < nd ? sub[q] : -1;
-      }
-      a.deg[2 * k] = nd;
+    if (a.mode == 0) {
+      const uint32_t bytes = d * 4 + E * d * 2 + (pred_row ? d * 2 : 0);
+      mbar_arrive_expect_tx(&s.in_bar, bytes);
+      bulk_g2s_plain(h_s, a.h, d * 4, &s.in_bar);
+      bulk_g2s_plain(g_s, a.wg, E * d * 2, &s.in_bar);
+      if (pred_row)
+        bulk_g2s_plain(gp_s, a.wg_next + static_cast<size_t>(blockIdx.x) * d, d * 2, &s.in_bar);
     }
   }
+  if (warp == 1) {
+    for (int e = lane; e < E; e += 32) {
+      s.fast_row[e] = a.fast_row[e];
+      s.slot[e] = a.slot_of[e];
+      s.pp[e] = a.pred_prev ? a.pred_prev[e] : 0.f;
+    }
+  }
+  for (int i = threadIdx.x; i < a.rows_per_cta; i += NT) rcnt[i] = 0;
   __syncthreads();
 
-  // ---------------------------------------------------------------- streaming
-  PieceMap m;
-  m.n_exec = s.n_exec;
-  m.d = d;
-  m.ffn = a.ffn;
-  for (int q = 0; q < m.n_exec; ++q)
-    m.base[q] = a.slab + static_cast<int64_t>(a.slot_of[s.sel[s.exec_q[q]]]) * a.slot_stride;
-  m.npc1 = (d * 2 + DSB - 1) / DSB;
-  m.pe1 = (((d + m.npc1 - 1) / m.npc1) + 7) / 8 * 8;
-  m.npc2 = (a.ffn * 2 + DSB - 1) / DSB;
-  m.pe2 = (((a.ffn + m.npc2 - 1) / m.npc2) + 7) / 8 * 8;
-  const int64_t W = static_cast<int64_t>(gridDim.x) * DW;
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * DW + warp;
-  const int64_t U1 = static_cast<int64_t>(m.n_exec) * a.ffn;
-  const int64_t U2 = static_cast<int64_t>(m.n_exec) * d;
-  m.u1a = U1 * gw / W;
-  m.u1b = U1 * (gw + 1) / W;
-  m.u2a = U2 * gw / W;
-  m.u2b = U2 * (gw + 1) / W;
-  m.n1 = (m.u1b - m.u1a) * 2 * m.npc1;
-  m.n = m.n1 + (m.u2b - m.u2a) * m.npc2;
-  const bool all_fast = m.n_exec == k;
+  Layout L;
+  L.d = d;
+  L.ffn = a.ffn;
+  L.G = gridDim.x;
+  L.cta = blockIdx.x;
+  L.npc1 = (d * 2 + DSB - 1) / DSB;
+  L.pe1 = (((d + L.npc1 - 1) / L.npc1) + 7) / 8 * 8;
+  L.npc2 = npc2_max;
+  L.pe2 = (((a.ffn + L.npc2 - 1) / L.npc2) + 7) / 8 * 8;
+  L.r0 = min(d, static_cast<int>(blockIdx.x) * a.rows_per_cta);
+  L.R = min(d, L.r0 + a.rows_per_cta) - L.r0;
 
-  uint8_t* my_ring = ring + warp * DS * DSB;
-  const uint64_t pol = l2_evict_first_policy();
-  int64_t issued = 0;  // warp-uniform: next piece to issue
-  auto issue_next = [&]() {
-    if (issued < m.n) {
-      if (lane == 0) {
-        const uint16_t* src;
-        int elems, voff;
-        piece_at(m, issued, src, elems, voff);
-        uint64_t* bar = &s.bar[warp][issued % DS];
-        mbar_arrive_expect_tx(bar, elems * 2);
-        bulk_g2s(my_ring + (issued % DS) * DSB, src, elems * 2, bar, pol);
-      }
-      ++issued;
-    }
-  };
-  for (int q = 0; q < DS; ++q) issue_next();
-
-  bool reported = false;
-  auto finish_phase1 = [&]() {
-    // every warp reports once; the CTA's last reporter runs the grid barrier
-    // and pulls the activations into shared memory for phase 2
-    reported = true;
+  // ---- selection helpers (warp 0)
+  auto finish_selection = [&](const float* wsrc) {
     if (lane == 0) {
-      __threadfence();
-      const int old = atomicAdd(&s.done1, 1);
-      if (old == DW - 1) {
-        grid_barrier(a.sync, gridDim.x);
-        if (blockIdx.x == 0 && a.p_pred) {  // next-layer prediction probabilities
-          float z[DE_MAX], mx = -INFINITY, sum = 0.f;
-          for (int i = 0; i < E; ++i) {
-            z[i] = __ldcg(a.pred_logits + i);
-            mx = fmaxf(mx, z[i]);
-          }
-          for (int i = 0; i < E; ++i) {
-            z[i] = expf(z[i] - mx);
-            sum += z[i];
-          }
-          for (int i = 0; i < E; ++i) a.p_pred[i] = z[i] / sum;
-        }
-        asm volatile("fence.proxy.async;" ::: "memory");
-        const uint32_t bytes = static_cast<uint32_t>(m.n_exec) * a.ffn * 2;
-        if (bytes == 0) {
-          mbar_arrive(&s.act_bar);
-        } else {
-          mbar_arrive_expect_tx(&s.act_bar, bytes);
-          for (int q = 0; q < m.n_exec; ++q)
-            bulk_g2s_plain(act_s + static_cast<size_t>(q) * a.ffn,
-                           a.act + static_cast<size_t>(s.exec_q[q]) * a.ffn, a.ffn * 2,
-                           &s.act_bar);
-        }
+      int ne = 0;
+      for (int q = 0; q < k; ++q) {
+        s.fast[q] = s.fast_row[s.sel[q]] ? 1 : 0;
+        if (s.fast[q]) s.exec_q[ne++] = q;
+      }
+      s.n_exec = ne;
+      if (wsrc) {
+        float den = 0.f;
+        for (int q = 0; q < k; ++q) den += wsrc[s.sel[q]];
+        for (int q = 0; q < k; ++q) s.wsel[q] = wsrc[s.sel[q]] / den;
       }
     }
     __syncwarp();
   };
 
-  float acc0 = 0.f, acc1 = 0.f;
-  float yrow[DK_MAX];
-  for (int64_t p = 0; p < m.n; ++p) {
-    if (p == m.n1) {
-      if (!reported) finish_phase1();
-      mbar_wait(&s.act_bar, 0);
-    }
-    const int stg = static_cast<int>(p % DS);
-    mbar_wait(&s.bar[warp][stg], static_cast<uint32_t>((p / DS) & 1));
-    const uint16_t* src;
-    int elems, voff;
-    piece_at(m, p, src, elems, voff);
-    const uint4* wp = reinterpret_cast<const uint4*>(my_ring + stg * DSB);
-    if (p < m.n1) {
-      const int q = static_cast<int>(p % (2 * m.npc1));
-      const float part = dot_piece(wp, reinterpret_cast<const uint4*>(x_s + voff), elems / 8,
-                                   lane, 0.f);
-      if (q < m.npc1) acc0 += part; else acc1 += part;
-      __syncwarp();
-      issue_next();  // refill the stage we just drained
-      if (q == 2 * m.npc1 - 1) {  // end of a (W1 row, W3 row) pair
-        const float g = warp_sum(acc0), u = warp_sum(acc1);
-        acc0 = acc1 = 0.f;
-        if (lane == 0) {
-          const int64_t unit = m.u1a + p / (2 * m.npc1);
-          const int j = static_cast<int>(unit / a.ffn);
-          const int64_t i = unit % a.ffn;
-          a.act[static_cast<int64_t>(s.exec_q[j]) * a.ffn + i] = f32_to_bf16_bits(silu_f32(g) * u);
+  // ---- streaming machinery (warp-uniform state)
+  uint8_t* my_ring = ring + warp * DS * DSB;
+  const uint64_t pol = l2_evict_first_policy();
+  int issued = 0, iss_phase = 1, iss_u = 0, iss_q = 0;
+  bool have_unit = false;
+  auto next_piece = [&](Piece& pc) {
+    pc.kind = 0;
+    if (iss_phase == 1) {
+      if (!have_unit) {
+        int m = 0;
+        if (lane == 0) m = atomicAdd(&s.p1_next, 1);
+        m = __shfl_sync(0xffffffffu, m, 0);
+        if (m < L.n1c) {
+          iss_u = L.cta + m * L.G;
+          iss_q = 0;
+          have_unit = true;
+        } else {
+          iss_phase = 2;
         }
       }
+      if (have_unit) {
+        pc.kind = 1;
+        pc.j = iss_u / L.ffn;
+        pc.row = iss_u - pc.j * L.ffn;
+        pc.c = iss_q;
+        if (++iss_q == 2 * L.npc1) have_unit = false;
+        return;
+      }
+    }
+    if (iss_phase == 2) {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(&s.p2_next, 1);
+      v = __shfl_sync(0xffffffffu, v, 0);
+      if (v >= L.P2c) {
+        iss_phase = 3;
+        return;
+      }
+      const int per_j = L.R * L.npc2;
+      pc.kind = 2;
+      pc.j = v / per_j;
+      const int rem = v - pc.j * per_j;
+      const int rr = rem / L.npc2;
+      pc.c = rem - rr * L.npc2;
+      pc.row = L.r0 + rr;
+    }
+  };
+  auto issue_next = [&]() {
+    Piece pc;
+    next_piece(pc);
+    const int stg = issued % DS;
+    if (lane == 0) {
+      s.rec[warp][stg] = pc;
+      if (pc.kind) {
+        int elems, voff;
+        const uint16_t* src = piece_src(L, pc, elems, voff);
+        mbar_arrive_expect_tx(&s.bar[warp][stg], elems * 2);
+        bulk_g2s(my_ring + stg * DSB, src, elems * 2, &s.bar[warp][stg], pol);
+      }
+    }
+    ++issued;
+  };
+  auto start_stream = [&]() {
+    L.n_exec = s.n_exec;
+    for (int q = 0; q < L.n_exec; ++q)
+      L.base[q] = a.slab + static_cast<int64_t>(s.slot[s.sel[s.exec_q[q]]]) * a.slot_stride;
+    L.n1c = count_mod(0, L.n_exec * a.ffn, L.cta, L.G);
+    L.P2c = L.n_exec * L.R * L.npc2;
+    for (int q = 0; q < DS; ++q) issue_next();
+  };
+
+  float ss = 0.f;
+  if (a.mode == 1) {
+    // ---------------------------------------------------- PLAN: stream first
+    if (warp == 0) {
+      if (E <= 32) warp_topk(lane < E ? s.pp[lane] : 0.f, lane, E, k, s.sel);
+      else if (lane == 0) topk_scan_smem(s.pp, E, k, s.sel);
+      __syncwarp();
+      if (lane == 0) s.nd = a.graceful ? degrade_smem(s.pp, E, s.sel, k, s.fast_row, s.drop, s.sub) : 0;
+      __syncwarp();
+      finish_selection(a.weights_from_pred ? s.pp : nullptr);
+    }
+    __syncthreads();
+    start_stream();
+    for (int i = threadIdx.x; i < d / 4; i += NT) {  // router inputs from global
+      const float4 v = reinterpret_cast<const float4*>(a.h)[i];
+      ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+    }
+  } else {
+    // ---------------------------------------------------- TRUE: router first
+    mbar_wait(&s.in_bar, 0);
+    for (int i = threadIdx.x; i < d / 4; i += NT) {
+      const float4 v = reinterpret_cast<const float4*>(h_s)[i];
+      ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+    }
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) s.red[warp] = ss;
+  __syncthreads();
+  if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][5] = gtimer();
+  {
+    float tot = 0.f;
+    for (int w = 0; w < DW; ++w) tot += s.red[w];
+    const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + a.eps);
+    const float* hsrc = a.mode == 0 ? h_s : a.h;
+    for (int i = threadIdx.x; i < d / 4; i += NT) {
+      const float4 v = reinterpret_cast<const float4*>(hsrc)[i];
+      const uint2 gw = reinterpret_cast<const uint2*>(a.gamma)[i];
+      const uint32_t b0 = f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.x, r), bf16lo(gw.x)));
+      const uint32_t b1 = f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.y, r), bf16hi(gw.x)));
+      const uint32_t b2 = f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.z, r), bf16lo(gw.y)));
+      const uint32_t b3 = f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.w, r), bf16hi(gw.y)));
+      reinterpret_cast<uint2*>(x_s)[i] = make_uint2(b0 | (b1 << 16), b2 | (b3 << 16));
+    }
+  }
+  __syncthreads();
+  if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][6] = gtimer();
+  const uint4* x4 = reinterpret_cast<const uint4*>(x_s);
+  const int n16 = d / 8;
+  for (int e = warp; e < E; e += DW) {
+    const uint16_t* grow = a.mode == 0 ? g_s + static_cast<size_t>(e) * d
+                                       : a.wg + static_cast<size_t>(e) * d;
+    const float z = warp_sum(dot_piece(reinterpret_cast<const uint4*>(grow), x4, n16, lane, 0.f));
+    if (lane == 0) s.z[e] = z;
+  }
+  if (pred_row && warp == DW - 1) {
+    const uint16_t* grow = a.mode == 0 ? gp_s : a.wg_next + static_cast<size_t>(blockIdx.x) * d;
+    const float zp = warp_sum(dot_piece(reinterpret_cast<const uint4*>(grow), x4, n16, lane, 0.f));
+    if (lane == 0) {
+      a.pred_logits[blockIdx.x] = zp;
+      __threadfence();
+      s.pred_last = atomicAdd(a.ctr + 1, 1u) == static_cast<unsigned>(E) - 1;
+    }
+    __syncwarp();
+    if (s.pred_last) {  // the grid's last next-layer row: softmax -> p_pred
+      __threadfence();
+      if (E <= 32) {
+        const float pv = warp_softmax(lane < E ? __ldcg(a.pred_logits + lane) : 0.f, lane, E);
+        if (lane < E) a.p_pred[lane] = pv;
+      } else if (lane == 0) {
+        float m = -INFINITY, sum = 0.f;
+        for (int i = 0; i < E; ++i) m = fmaxf(m, __ldcg(a.pred_logits + i));
+        for (int i = 0; i < E; ++i) sum += expf(__ldcg(a.pred_logits + i) - m);
+        for (int i = 0; i < E; ++i) a.p_pred[i] = expf(__ldcg(a.pred_logits + i) - m) / sum;
+      }
+      if (lane == 0) a.ctr[1] = 0;
+    }
+  }
+  __syncthreads();
+  if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][7] = gtimer();
+  if (warp == 0) {
+    if (E <= 32) {
+      const float pv = warp_softmax(lane < E ? s.z[lane] : 0.f, lane, E);
+      if (lane < E) s.p[lane] = pv;
+    } else if (lane == 0) {
+      softmax_serial(s.z, E, s.p);
+    }
+    __syncwarp();
+    if (a.mode == 0) {
+      if (E <= 32) warp_topk(lane < E ? s.p[lane] : 0.f, lane, E, k, s.sel);
+      else if (lane == 0) topk_scan_smem(s.p, E, k, s.sel);
+      if (lane == 0) s.nd = 0;
+      __syncwarp();
+      finish_selection(s.p);
+    } else if (!a.weights_from_pred) {
+      finish_selection(s.p);
+    }
+    if (blockIdx.x == 0) {
+      for (int i = lane; i < E; i += 32) a.p_true[i] = s.p[i];
+      if (lane < k) {
+        a.sel[lane] = s.sel[lane];
+        a.w[lane] = s.wsel[lane];
+        a.is_fast[lane] = s.fast[lane];
+        a.deg[lane] = lane < s.nd ? s.drop[lane] : -1;
+        a.deg[k + lane] = lane < s.nd ? s.sub[lane] : -1;
+      }
+      if (lane == 0) a.deg[2 * k] = s.nd;
+    }
+  }
+  __syncthreads();
+  if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][8] = gtimer();
+  if (a.mode == 0) start_stream();
+  if (blockIdx.x == 0 && a.x_out)
+    for (int i = threadIdx.x; i < n16; i += NT) reinterpret_cast<uint4*>(a.x_out)[i] = x4[i];
+  if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][1] = gtimer();
+
+  // ---------------------------------------------------------------- stream
+  const bool all_fast = L.n_exec == k;
+  const int row_target = L.n_exec * L.npc2;
+  float acc0 = 0.f, acc1 = 0.f;
+  int cur_j = -1, cur_cnt = 0;  // phase-1 units finished for the current pick
+  auto publish = [&]() {        // CTA-aggregated per-pick completion
+    if (cur_j >= 0 && cur_cnt > 0 && lane == 0) {
+      __threadfence();          // this warp's act rows -> visible GPU-wide
+      const int tot_j = count_mod(cur_j * a.ffn, (cur_j + 1) * a.ffn, L.cta, L.G);
+      if (atomicAdd(&s.done1[cur_j], cur_cnt) + cur_cnt == tot_j)
+        atomicAdd(a.ctr + 2 + cur_j, static_cast<unsigned>(tot_j));
+    }
+    cur_cnt = 0;
+  };
+  bool in_p2 = false;
+  for (int p = 0;; ++p) {
+    const int stg = p % DS;
+    __syncwarp();
+    const Piece pc = s.rec[warp][stg];
+    if (pc.kind == 0) break;
+    int elems, voff;
+    piece_src(L, pc, elems, voff);
+    if (pc.kind == 2) {
+      if (!in_p2) {
+        in_p2 = true;
+        publish();
+        if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][2] = gtimer();
+      }
+      if (lane == 0 && atomicCAS(&s.act_req[pc.j], 0, 1) == 0) {
+        // first use of pick j in this CTA: wait for its rows, pull act_j in
+        const unsigned* cnt = a.ctr + 2 + pc.j;
+        while (ld_acquire_gpu(cnt) < static_cast<unsigned>(a.ffn)) __nanosleep(64);
+        if (tl && pc.j == 0) g_decode_timeline[blockIdx.x][3] = gtimer();
+        asm volatile("fence.proxy.async;" ::: "memory");
+        mbar_arrive_expect_tx(&s.act_bar[pc.j], a.ffn * 2);
+        bulk_g2s_plain(act_s + static_cast<size_t>(pc.j) * a.ffn,
+                       a.act + static_cast<size_t>(s.exec_q[pc.j]) * a.ffn, a.ffn * 2,
+                       &s.act_bar[pc.j]);
+      }
+      mbar_wait(&s.act_bar[pc.j], 0);
+    }
+    mbar_wait(&s.bar[warp][stg], static_cast<uint32_t>((p / DS) & 1));
+    const uint4* wp = reinterpret_cast<const uint4*>(my_ring + stg * DSB);
+    if (pc.kind == 1) {
+      const float v = dot_piece(wp, reinterpret_cast<const uint4*>(x_s + voff), elems / 8, lane, 0.f);
+      if (pc.c < L.npc1) acc0 += v; else acc1 += v;
+      __syncwarp();
+      issue_next();  // refill the stage just drained
+      if (pc.c == 2 * L.npc1 - 1) {  // (W1 row, W3 row) pair complete
+        const float g = warp_sum(acc0), u = warp_sum(acc1);
+        acc0 = acc1 = 0.f;
+        if (lane == 0)
+          a.act[static_cast<int64_t>(s.exec_q[pc.j]) * a.ffn + pc.row] =
+              f32_to_bf16_bits(silu_f32(g) * u);
+        if (pc.j != cur_j) {
+          publish();
+          cur_j = pc.j;
+        }
+        ++cur_cnt;
+      }
     } else {
-      const int64_t p2 = p - m.n1;
-      const int64_t unit = m.u2a + p2 / m.npc2;
-      const int c = static_cast<int>(p2 % m.npc2);
-      const int j = static_cast<int>(unit % m.n_exec);
-      acc0 = dot_piece(wp, reinterpret_cast<const uint4*>(act_s + static_cast<size_t>(j) * a.ffn + voff),
-                       elems / 8, lane, acc0);
+      const float v = warp_sum(dot_piece(
+          wp, reinterpret_cast<const uint4*>(act_s + static_cast<size_t>(pc.j) * a.ffn + voff),
+          elems / 8, lane, 0.f));
       __syncwarp();
       issue_next();
-      if (c == m.npc2 - 1) {  // end of the (row, pick) unit
-        const float yv = warp_sum(acc0);
-        acc0 = 0.f;
-        const int64_t row = unit / m.n_exec;
-        yrow[j] = yv;
-        if (lane == 0) a.y[static_cast<int64_t>(s.exec_q[j]) * d + row] = yv;
-        if (all_fast) {
-          const int64_t first = row * m.n_exec, last = first + m.n_exec - 1;
-          const bool whole = first >= m.u2a && last < m.u2b;
-          if (whole) {
-            if (j == m.n_exec - 1 && lane == 0) {  // whole row is ours: combine in registers
-              float o = a.h[row];
-              for (int q = 0; q < k; ++q) o = fmaf(s.wsel[q], yrow[q], o);
-              a.h_out[row] = o;
-            }
-          } else if (unit == last || unit == m.u2b - 1) {
-            // row shared with a neighbouring warp: the last arriver combines
-            if (lane == 0) {
-              const int64_t lo = first > m.u2a ? first : m.u2a;
-              const unsigned mine = static_cast<unsigned>(unit - lo + 1);
-              __threadfence();
-              const unsigned old = atomicAdd(a.sync + 2 + row, mine);
-              if (old + mine == static_cast<unsigned>(m.n_exec)) {
-                __threadfence();
-                float o = a.h[row];
-                for (int q = 0; q < k; ++q)
-                  o = fmaf(s.wsel[q], __ldcg(a.y + static_cast<int64_t>(q) * d + row), o);
-                a.h_out[row] = o;
-                a.sync[2 + row] = 0;
-              }
-            }
+      if (lane == 0) {
+        const int rr = pc.row - L.r0;
+        float* pr = part + static_cast<size_t>(rr) * k * L.npc2;
+        pr[pc.j * L.npc2 + pc.c] = v;
+        __threadfence_block();
+        if (atomicAdd(&rcnt[rr], 1) == row_target - 1) {  // last piece of row: reduce
+          __threadfence_block();
+          float o = a.h[pc.row];
+          for (int jj = 0; jj < L.n_exec; ++jj) {
+            float yv = 0.f;
+            for (int c = 0; c < L.npc2; ++c) yv += pr[jj * L.npc2 + c];
+            a.y[static_cast<int64_t>(s.exec_q[jj]) * d + pc.row] = yv;
+            o = fmaf(s.wsel[s.exec_q[jj]], yv, o);
           }
+          if (all_fast) a.h_out[pc.row] = o;
         }
       }
     }
   }
-  if (!reported) finish_phase1();
+  publish();
+  if (lane == 0) {
+    if (tl) atomicMax(&g_decode_timeline[blockIdx.x][4], gtimer());
+    if (atomicAdd(&s.fin, 1) == DW - 1) {           // CTA done
+      if (atomicAdd(a.ctr, 1u) == gridDim.x - 1) {  // grid done: reset for the next call
+        for (int q = 0; q < DK_MAX; ++q) a.ctr[2 + q] = 0;
+        a.ctr[0] = 0;
+      }
+    }
+  }
+}
+
+template <int DW, int DS, int DSB>
+static int launch_decode(DecodeArgs a, int grid, cudaStream_t st) {
+  a.rows_per_cta = (a.d + grid - 1) / grid;
+  const int npc2 = (a.ffn * 2 + DSB - 1) / DSB;
+  if (npc2 > kMaxChunks) {
+    set_error("decode_layer: ffn=%d needs %d W2 pieces (max %d)", a.ffn, npc2, kMaxChunks);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  const size_t ring = static_cast<size_t>(DW) * DS * DSB;
+  const size_t stage_in = static_cast<size_t>(a.d) * 4 + static_cast<size_t>(a.E + 1) * a.d * 2;
+  if (a.mode == 0 && stage_in > ring) {
+    set_error("decode_layer: router inputs (%zu B) exceed the ring (%zu B)", stage_in, ring);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  const size_t smem = ring + static_cast<size_t>(a.k) * a.ffn * 2 +
+                      (static_cast<size_t>(a.d) * 2 + 127) / 128 * 128 +
+                      static_cast<size_t>(a.rows_per_cta) * a.k * npc2 * 4 +
+                      (static_cast<size_t>(a.rows_per_cta) * 4 + 127) / 128 * 128 +
+                      sizeof(DecodeSmem<DW, DS>) + 128;
+  if (smem > 227 * 1024) {
+    set_error("decode_layer: %zu B of shared memory exceeds 227 KB (k*ffn too large)", smem);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  auto kern = decode_layer_kernel<DW, DS, DSB>;
+  DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(DW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the per-pick waits
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DAOP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  return DAOP_OK;
 }
 
 }  // namespace daop
 
 using namespace daop;
 
+extern "C" int daop_decode_timeline(int32_t enable, uint64_t* h_out, int32_t n_cta) {
+  if (h_out && n_cta > 0) {
+    DAOP_CUDA(cudaMemcpyFromSymbol(h_out, g_decode_timeline,
+                                   sizeof(unsigned long long) * 10 * (n_cta < 1024 ? n_cta : 1024)));
+  }
+  if (enable) {
+    static unsigned long long zeros[1024][10];
+    DAOP_CUDA(cudaMemcpyToSymbol(g_decode_timeline, zeros, sizeof(zeros)));
+  }
+  DAOP_CUDA(cudaMemcpyToSymbol(g_decode_timeline_on, &enable, sizeof(int)));
+  return DAOP_OK;
+}
+
 extern "C" int daop_decode_workspace(int32_t d, int32_t ffn, int32_t E, int32_t k,
                                      int64_t* bytes) {
-  // sync counters (2 + d uint32) | pred logits (E f32) | act (k*ffn bf16)
-  *bytes = ((2 + static_cast<int64_t>(d)) * 4 + 255) / 256 * 256 + 256 +
+  // ctr (32 u32) | pred logits (E f32, padded) | act (k*ffn bf16)
+  (void)d;
+  *bytes = 128 + (static_cast<int64_t>(E) * 4 + 255) / 256 * 256 +
            (static_cast<int64_t>(k) * ffn * 2 + 255) / 256 * 256;
   return DAOP_OK;
 }
@@ -407,7 +628,7 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
                                  int32_t graceful, int32_t weights_from_pred, float eps,
                                  uint16_t* x_out, float* p_true, float* p_pred, int32_t* sel,
                                  float* w, uint8_t* is_fast, int32_t* deg, float* y,
-                                 float* h_out, void* workspace, int32_t grid,
+                                 float* h_out, void* workspace, int32_t variant,
                                  daop_stream_t stream) {
   if (E < 2 || E > DE_MAX || k < 1 || k > DK_MAX || k > E || d % 8 || ffn % 8) {
     set_error("decode_layer: unsupported shape (E=%d k=%d d=%d ffn=%d)", E, k, d, ffn);
@@ -425,32 +646,17 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
   a.x_out = x_out; a.p_true = p_true; a.p_pred = wg_next ? p_pred : nullptr; a.sel = sel;
   a.w = w; a.is_fast = is_fast; a.deg = deg; a.y = y; a.h_out = h_out;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  a.sync = reinterpret_cast<unsigned*>(ws);
-  const int64_t o1 = ((2 + static_cast<int64_t>(d)) * 4 + 255) / 256 * 256;
-  a.pred_logits = reinterpret_cast<float*>(ws + o1);
-  a.act = reinterpret_cast<uint16_t*>(ws + o1 + 256);
-
-  const size_t smem = static_cast<size_t>(DW) * DS * DSB + static_cast<size_t>(k) * ffn * 2 +
-                      (static_cast<size_t>(d) * 2 + 127) / 128 * 128 + sizeof(DecodeSmem) + 128;
-  if (smem > 227 * 1024) {
-    set_error("decode_layer: %zu B of shared memory exceeds 227 KB (k*ffn too large)", smem);
-    return DAOP_ERR_UNSUPPORTED;
-  }
-  DAOP_CUDA(cudaFuncSetAttribute(decode_layer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-  const int sms = sm_count();
-  if (grid <= 0 || grid > sms) grid = sms;
+  a.ctr = reinterpret_cast<unsigned*>(ws);
+  a.pred_logits = reinterpret_cast<float*>(ws + 128);
+  a.act = reinterpret_cast<uint16_t*>(ws + 128 + (static_cast<int64_t>(E) * 4 + 255) / 256 * 256);
+  int grid = sm_count();
   if (grid < E) grid = E;  // CTAs 0..E-1 own one next-layer gate row each
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(D_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = as_stream(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  DAOP_CUDA(cudaLaunchKernelEx(&cfg, decode_layer_kernel, a));
-  return DAOP_OK;
+  cudaStream_t st = as_stream(stream);
+  switch (variant) {
+    case 1: return launch_decode<4, 4, 10240>(a, grid, st);
+    case 2: return launch_decode<8, 2, 8192>(a, grid, st);
+    case 3: return launch_decode<6, 3, 8192>(a, grid, st);
+    case 4: return launch_decode<16, 1, 10240>(a, grid, st);
+    default: return launch_decode<8, 2, 10240>(a, grid, st);
+  }
 }

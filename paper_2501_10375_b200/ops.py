@@ -146,7 +146,7 @@ class DecodeBuffers:
 
 def decode_layer(h, gamma, wg, wg_next, fast_row, slot_of, slab, slot_elems, d, ffn, k,
                  bufs: DecodeBuffers, *, pred_prev=None, mode=0, graceful=True,
-                 weights_from_pred=False, grid=0, eps=RMS_EPS):
+                 weights_from_pred=False, variant=0, eps=RMS_EPS):
     """One decode token through one MoE layer in a single launch."""
     _dev(h, gamma, wg, wg_next, pred_prev, fast_row, slot_of, slab)
     e = wg.shape[0]
@@ -155,5 +155,5 @@ def decode_layer(h, gamma, wg, wg_next, fast_row, slot_of, slab, slot_elems, d, 
               slot_elems, d, ffn, e, k, mode, int(graceful), int(weights_from_pred), float(eps),
               bufs.x.data_ptr(), bufs.p.data_ptr(), bufs.p_pred.data_ptr(), bufs.sel.data_ptr(),
               bufs.w.data_ptr(), bufs.is_fast.data_ptr(), bufs.deg.data_ptr(),
-              bufs.y.data_ptr(), bufs.h_out.data_ptr(), bufs.ws.data_ptr(), grid, _s())
+              bufs.y.data_ptr(), bufs.h_out.data_ptr(), bufs.ws.data_ptr(), variant, _s())
     return bufs

@@ -1,0 +1,59 @@
+"""Quick kernel timing probe (development aid; bench.py is the contract)."""
+import sys, time
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import paper_2501_10375_b200 as P
+from paper_2501_10375_b200 import model as M, ops
+
+def ev_time(fn, iters=50, warm=5):
+    for _ in range(warm): fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters): fn()
+    e.record(); torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+what = sys.argv[1] if len(sys.argv) > 1 else "all"
+d, ffn, E, k = 4096, 14336, 8, 2
+if what in ("decode", "all"):
+    m = M.MoEModel(P.ModelShape(2, E, k), d, ffn, seed=0, resident_layers=[0])
+    bufs = ops.DecodeBuffers(d, ffn, E, k, "cuda")
+    hs = [m.input_hidden(1, stream=9, step=i)[0] for i in range(16)]
+    it = [0]
+    var = [0]
+    def step():
+        ops.decode_layer(hs[it[0] % 16], m.norm[0], m.gate[0], m.gate[1], m.fast[0], m.slot_of[0],
+                         m.slab, m.slot_elems, d, ffn, k, bufs, variant=var[0])
+        it[0] += 1
+    for v in (0, 2):
+        var[0] = v
+        ms = ev_time(step, iters=200, warm=10)
+        b = 704_774_144
+        print(f"decode_layer variant={v}: {ms*1e3:.1f} us  {b/ms/1e6:.1f} GB/s", flush=True)
+    from paper_2501_10375_b200 import _lib
+    tlb = np.zeros((148, 10), dtype=np.uint64)
+    _lib.call("daop_decode_timeline", 1, 0, 0)
+    torch.cuda.synchronize(); step(); torch.cuda.synchronize()
+    _lib.call("daop_decode_timeline", 0, tlb.ctypes.data, 148)
+    t = tlb.astype(np.int64); t0 = t[:, 0].min()
+    rel = (t - t0) / 1000.0
+    for i, nm in enumerate(["start", "sel+issue", "ph1 done", "act ready", "end", "h loaded", "x ready", "gates", "decided", "streamed"]):
+        print(f"  {nm:12s} min {rel[:, i].min():7.2f}  med {np.median(rel[:, i]):7.2f}  max {rel[:, i].max():7.2f} us")
+if what in ("prefill", "all"):
+    T = 32768
+    m = M.MoEModel(P.ModelShape(1, E, k), d, ffn, seed=0)
+    h = m.input_hidden(T, stream=5)
+    r = ops.router(h, m.norm[0], m.gate[0], None, k)
+    pr = ops.permute(r["topk_idx"], E, r["x"])
+    so = m.slot_of[0].contiguous()
+    t_r = ev_time(lambda: ops.router(h, m.norm[0], m.gate[0], None, k), 10, 2)
+    t_p = ev_time(lambda: ops.permute(r["topk_idx"], E, r["x"]), 10, 2)
+    for g in (0,):
+        t_up = ev_time(lambda: ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g), 5, 2)
+        act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g)
+        t_dn = ev_time(lambda: ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g), 5, 2)
+        fl_up = 2 * T * k * d * 2 * ffn
+        fl_dn = 2 * T * k * d * ffn
+        print(f"group={g} router {t_r:.3f} ms permute {t_p:.3f} ms  up {t_up:.3f} ms ({fl_up/t_up/1e9:.0f} TF/s)  down {t_dn:.3f} ms ({fl_dn/t_dn/1e9:.0f} TF/s)", flush=True)

@@ -232,10 +232,16 @@ def test_grouped_gemm_parity(P, d, ffn, E, T):
             continue
         rows = perm[a:b] // 2
         w1, w3, w2 = om.w1(0, e), om.w3(0, e), om.w2(0, e)
-        # the SwiGLU activation: bf16 of fp32 results -> at most 1 bf16 ulp apart
+        # the SwiGLU activation is bf16 of fp32 dot products summed in a different
+        # order: equal up to one bf16 rounding of a value perturbed by ~1e-7*rms
         a_ref = N.expert_act(x[rows], w1, w3)
         dif = np.abs(act_g[a:b] - a_ref)
-        assert np.all(dif <= np.abs(a_ref) * 2 ** -7 + 1e-6), f"expert {e} act"
+        rms = float(np.sqrt(np.mean(a_ref.astype(np.float64) ** 2)))
+        bound = np.abs(a_ref) * 2.0 ** -7 + 1e-4 * rms  # one bf16 ulp
+        assert np.all(dif <= bound), (
+            f"expert {e} act: max dif {dif.max():.3e} at {np.unravel_index(dif.argmax(), dif.shape)}"
+            f" ref {a_ref.flat[dif.argmax()]:.4e} rms {rms:.3e}; >1ulp frac {(dif > bound).mean():.2e}")
+        assert (dif > 0).mean() < 0.02, f"expert {e}: {(dif > 0).mean():.3f} of act differ"
         hidden_close(y_g[a:b], act_g[a:b] @ w2.T, f"expert {e} down (teacher-forced act)")
     ref = N.moe_layer(om, 0, h.cpu().numpy(), sel=sel, w=r["topk_w"].cpu().numpy(), x=x)
     hidden_close(out.cpu().numpy(), ref["out"], "layer output")
@@ -263,3 +269,51 @@ def test_decode_layer_parity(P, d, ffn, E, k):
         ref = N.moe_layer(om, 0, h.cpu().numpy(), sel=sel[None, :],
                           w=bufs.w.cpu().numpy()[None, :], x=x)
         hidden_close(bufs.h_out.cpu().numpy(), ref["out"][0], f"decode step {step}")
+
+
+@pytest.mark.parametrize("resident,graceful", [((0, 2, 5), True), ((0, 2, 5), False),
+                                               ((1, 3, 4, 6), True), ((), True)])
+def test_decode_layer_plan_mode(P, resident, graceful):
+    """DAOP decode (l >= start): selection = top-k of the prediction carried on
+    layer l-1, graceful degradation over this layer's HBM residence; only the
+    resident picks are streamed.  Decisions bit-exact vs the oracle plan;
+    resident picks' expert outputs within the hidden-state tolerance."""
+    pkg, model_mod, ops = P
+    d, ffn, E, k = 512, 1024, 8, 2
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, k), d, ffn, seed=2, resident_layers=[],
+                           n_slots=max(1, len(resident)))
+    for e in resident:
+        m.load_expert(1, e)
+    om = N.OracleModel(2, E, k, d, ffn, seed=2)
+    bufs = ops.DecodeBuffers(d, ffn, E, k, "cuda")
+    rng = np.random.default_rng(len(resident))
+    for step in range(6):
+        z = rng.normal(size=E).astype(np.float32) * 2
+        pred = N.softmax(z[None, :])[0]
+        pp = torch.tensor(pred, device="cuda")
+        h = m.input_hidden(1, stream=4, step=step)
+        ops.decode_layer(h[0], m.norm[1], m.gate[1], None, m.fast[1], m.slot_of[1], m.slab,
+                         m.slot_elems, d, ffn, k, bufs, pred_prev=pp, mode=1, graceful=graceful,
+                         weights_from_pred=True)
+        torch.cuda.synchronize()
+        sets = [set(), set(resident)]
+        plan = D.plan_token(np.zeros((2, E)), np.stack([pred.astype(np.float64), np.zeros(E)]),
+                            np.array([True, False]), sets, k, "daop", start=1, degrade=graceful)[1]
+        sel = bufs.sel.cpu().tolist()
+        assert sel == [x[0] for x in plan["executed"]]
+        assert bufs.is_fast.cpu().tolist() == [int(x[1] == "fast") for x in plan["executed"]]
+        deg = bufs.deg.cpu().tolist()
+        nd = deg[2 * k]
+        assert [[deg[i], deg[k + i]] for i in range(nd)] == [[a, c] for a, _, c, _ in plan["degraded"]]
+        wref = pred[sel] / pred[sel].sum()
+        assert np.abs(bufs.w.cpu().numpy() - wref).max() <= 1e-6
+        x = bf16_to_f32(bufs.x)[None, :]
+        y = bufs.y.cpu().numpy()
+        for q, e in enumerate(sel):
+            if e in resident:
+                yref = N.expert_ffn(x, om.w1(1, e), om.w3(1, e), om.w2(1, e))[0]
+                hidden_close(y[q], yref, f"pick {q} expert {e}")
+        if all(e in resident for e in sel):
+            ref = h.cpu().numpy()[0] + sum(wref[q] * N.expert_ffn(
+                x, om.w1(1, e), om.w3(1, e), om.w2(1, e))[0] for q, e in enumerate(sel))
+            hidden_close(bufs.h_out.cpu().numpy(), ref, "combined")
