@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native DAOP MoE-block hot path (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Headline workload (BASELINE.json configs[1]): ONE Mixtral-8x7B-shaped MoE
+layer (d=4096, ffn=14336, E=8, top-2), bf16 weights, decode batch 1 on one
+B200, all 8 experts resident in HBM.  A step = one decode token through the
+layer = one persistent kernel launch (fused router + selection + SwiGLU
+expert GEMV streaming both picked experts' 704.8 MB + combine).  Every step
+takes a fresh token, so the picked experts change step to step; the 2.8 GB
+of expert weights exceed the 126 MB L2, so no L2 flush is needed.
+
+  value  tokens/s with the token already in HBM (device clock, max over ranks)
+  e2e    tokens/s through the public host API (MoEBlockEngine.decode_host):
+         pinned h -> H2D -> decode -> D2H of (h_out, picks) -> sync, per step
+  roofline  HBM: algorithmic bytes per launch / CUDA-event launch duration,
+            against MEASURED_PEAKS.json hbm_gbs (driver-measured copy peak)
+  prefill   BASELINE configs[3]: 8 sequences x 4096 tokens through the same
+            layer (router, permutation, tcgen05 grouped GEMMs, combine),
+            tensor roofline against the measured bf16 peak
+  cpu_baseline  the oracle CPU path (oracle/baseline.py) on this host's cores
+            for a bounded sample of the same workload
+
+--impl reference times that CPU path alone as the reference arm (the
+reference package itself executes no numerics -- SPEC.md:347,356 -- so its
+own algorithm restated in oracle/ is the arm).
+With N > 1 (torchrun) every rank runs the same decode on its own GPU as an
+independent replica (weak scaling; decode b=1 touches 2 experts, so expert
+parallelism cannot speed up a single token -- DESIGN.md §7).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE decode tokens/s & prefill tokens/s (Mixtral-8x7B shape), % HBM/tensor roofline"
+D, FFN, E, K = 4096, 14336, 8, 2
+DECODE_BYTES = 2 * 3 * D * FFN * 2 + 2 * E * D * 2          # 704,774,144 B per token-layer
+PREFILL_SEQS, PREFILL_LEN = 8, 4096
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), float(j.get("bf16_tflops_sustained", j["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        import statistics
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def ncu_traffic():
+    """dram bytes per launch of the decode kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_decode_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# ------------------------------------------------------------------ reference arm
+
+
+def cpu_decode_layer():
+    from oracle.baseline import CpuMoELayer
+    return CpuMoELayer(2, E, K, D, FFN, seed=0, layer=0)
+
+
+def cpu_inputs(n, rank=0):
+    from oracle import numerics as N
+    return [N.input_hidden(0, 100 + rank, i, 1, D)[0] for i in range(n)]
+
+
+def run_reference(args, world, rank):
+    import numpy as np  # noqa: F401
+    from oracle.baseline import blas_threads, time_steps
+    if rank != 0:
+        return None
+    layer = cpu_decode_layer()
+    xs = cpu_inputs(16)
+    warm = max(1, min(args.warmup, 3))
+    n, sec = time_steps(layer.decode_step, xs, budget_s=60.0, max_steps=args.steps, warmup=warm)
+    v = n / sec
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
+        "n_gpus": world, "steps": n, "warmup": warm, "ms_per_step": 1e3 * sec / n,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter-RNG random-init weights and tokens)",
+        "config": {"workload": "decode b=1, one Mixtral-8x7B MoE layer (BASELINE configs[1])",
+                   "d_model": D, "d_ff": FFN, "experts": E, "top_k": K,
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{n} decode tokens through one layer (oracle numpy, fp32)"},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+# ------------------------------------------------------------------ B200 arm
+
+
+def run_b200(args, world, rank, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    from paper_2501_10375_b200.model import MoEModel
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    hbm_peak, tf_peak, tf_sus, peak_kind = peaks()
+    model = MoEModel(P.ModelShape(2, E, K), D, FFN, seed=0, device=dev, resident_layers=[0])
+    eng = MoEBlockEngine(model)
+    n_in = 64
+    hs = [model.input_hidden(1, stream=100 + rank, step=i)[0] for i in range(n_in)]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # -------- device-resident timed loop (value)
+    for i in range(args.warmup):
+        eng.decode(hs[i % n_in])
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            eng.decode(hs[i % n_in])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * args.steps / (ms_max / 1e3)
+
+    # -------- per-launch kernel duration for the roofline (events around each launch)
+    nl = min(args.steps, 200)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(nl)]
+    torch.cuda.synchronize()
+    for i in range(nl):
+        evs[i][0].record(stream)
+        eng.decode(hs[i % n_in])
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    launch_ms = sorted(a.elapsed_time(b) for a, b in evs)
+    launch_ms_mean = float(np.mean(launch_ms))
+    achieved = DECODE_BYTES / (launch_ms_mean / 1e3) / 1e9
+
+    # -------- end-to-end through the host API (value measured with host buffers)
+    hh = [torch.empty(D, dtype=torch.float32, pin_memory=True) for _ in range(8)]
+    for i, h in enumerate(hh):
+        h.copy_(hs[i].cpu())
+    h2d, d2h = MoEBlockEngine.host_bytes(D, K)
+    ne = min(args.steps, 1000)
+    for i in range(min(args.warmup, 20)):
+        eng.decode_host(hh[i % 8])
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(ne):
+        eng.decode_host(hh[i % 8])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    te = torch.tensor([max(e0.elapsed_time(e1) / 1e3, wall)], device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = world * ne / float(te.item())
+
+    # -------- prefill (BASELINE configs[3]: 8 x 4096 tokens)
+    prefill = None
+    if not args.no_prefill:
+        T = PREFILL_SEQS * PREFILL_LEN
+        hp = model.input_hidden(T, stream=200 + rank)
+        hist = torch.zeros((PREFILL_SEQS, 2, E), dtype=torch.int32, device=dev)
+        for _ in range(2):
+            eng.prefill(hp, 0, hist=hist[:, 0], tokens_per_seq=PREFILL_LEN, hist_seq_stride=2 * E)
+        barrier()
+        torch.cuda.synchronize()
+        kp = max(3, min(10, args.steps // 200))
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(kp):
+            eng.prefill(hp, 0, hist=hist[:, 0], tokens_per_seq=PREFILL_LEN, hist_seq_stride=2 * E)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pms = p0.elapsed_time(p1) / kp
+        tp = torch.tensor([pms], device=dev)
+        if world > 1:
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+        pms = float(tp.item())
+        flops = 2.0 * K * T * 3 * D * FFN
+        prefill = {
+            "workload": f"prefill {PREFILL_SEQS} x {PREFILL_LEN} tokens, one layer (BASELINE configs[3])",
+            "value": world * T / (pms / 1e3), "unit": "tokens/s", "ms_per_layer": pms,
+            "roofline": {"bound": "tensor", "achieved": flops / (pms / 1e3) / 1e12,
+                         "peak": tf_peak, "unit": "TFLOP/s",
+                         "frac": flops / (pms / 1e3) / 1e12 / tf_peak, "peak_kind": peak_kind,
+                         "flops_per_layer": flops},
+            "gpu_launches": kp * MoEBlockEngine.prefill_kernels(),
+        }
+        del hp
+
+    # -------- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.baseline import blas_threads, time_steps
+        layer = cpu_decode_layer()
+        xs = cpu_inputs(16)
+        n, sec = time_steps(layer.decode_step, xs, budget_s=20.0, max_steps=200, warmup=1)
+        cpu = {"value": n / sec, "unit": "tokens/s", "cores": blas_threads(), "kind": "port",
+               "sample": f"{n} decode tokens through one Mixtral-8x7B layer "
+                         f"(oracle numpy fp32, {sec:.1f} s)"}
+        del layer
+
+    if rank != 0:
+        return None
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (counter-RNG random-init weights and tokens)",
+        "config": {"workload": "decode b=1, one Mixtral-8x7B MoE layer (BASELINE configs[1])",
+                   "d_model": D, "d_ff": FFN, "experts": E, "top_k": K, "global_batch": world,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (2.8 GB of experts, 704.8 MB streamed per step)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic(),
+                     "peak_kind": peak_kind, "bytes_per_launch": DECODE_BYTES,
+                     "launch_us_mean": launch_ms_mean * 1e3,
+                     "launch_us_p50": launch_ms[len(launch_ms) // 2] * 1e3,
+                     "frac_of_8tbs": achieved / 8000.0},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": args.steps,
+        "clocks": clocks,
+        "prefill": prefill,
+    }
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference", "ours"])
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, world, rank)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        line = run_b200(args, world, rank, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,97 @@
+"""MoE-block execution engine: the numeric hot path the reference only prices.
+
+`MoEBlockEngine` runs one MoE layer of a `MoEModel` on the device:
+
+  decode(h, layer, ...)   one token, one persistent launch (daop_decode_layer):
+                          router + DAOP decision + HBM-streaming SwiGLU GEMV +
+                          combine.
+  prefill(h, layer, ...)  T tokens: fused router (with the per-sequence
+                          activation counter) -> stable permutation ->
+                          tcgen05 grouped up/down GEMMs -> combine.
+  decode_host(h_host)     the end-to-end call a user makes with host memory:
+                          H2D of the token, the decode launch, D2H of the
+                          result (used for bench.py's `e2e`).
+
+Every buffer is preallocated per engine so the decode step has fixed
+addresses (CUDA-graph capturable).  The DAOP sequence-level flow
+(calibration init -> prefill counts -> Alg. 1 swaps -> decode plans) is in
+daop.py.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import ops
+from .model import MoEModel
+
+
+class MoEBlockEngine:
+    def __init__(self, model: MoEModel, device=None):
+        self.model = model
+        self.device = model.device if device is None else torch.device(device)
+        s = model.shape
+        self.d, self.ffn, self.E, self.k = model.d, model.ffn, s.num_experts, s.top_k
+        self.bufs = ops.DecodeBuffers(self.d, self.ffn, self.E, self.k, self.device)
+        self._h_dev = torch.empty(self.d, dtype=torch.float32, device=self.device)
+        self._h_host = None
+        self._out_host = None
+        self._sel_host = None
+
+    # ------------------------------------------------------------ decode
+    def decode(self, h: torch.Tensor, layer: int = 0, *, pred_prev=None, mode: int = 0,
+               graceful: bool = True, weights_from_pred: bool = False, variant: int = 0):
+        """One decode token (h: (d,) fp32 on device) through MoE layer `layer`.
+        mode 0 selects by the layer's own gate (true top-k), mode 1 by the DAOP
+        plan on `pred_prev` (the prediction carried on layer-1)."""
+        m = self.model
+        nxt = m.gate[layer + 1] if layer + 1 < m.shape.num_layers else None
+        return ops.decode_layer(h, m.norm[layer], m.gate[layer], nxt, m.fast[layer],
+                                m.slot_of[layer], m.slab, m.slot_elems, self.d, self.ffn, self.k,
+                                self.bufs, pred_prev=pred_prev, mode=mode, graceful=graceful,
+                                weights_from_pred=weights_from_pred, variant=variant)
+
+    def decode_host(self, h_host: torch.Tensor, layer: int = 0):
+        """End-to-end call from host memory: pinned h (d,) -> device -> decode
+        -> (h_out, selected experts) back in pinned host memory."""
+        if self._out_host is None:
+            self._out_host = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
+            self._sel_host = torch.empty(self.k, dtype=torch.int32, pin_memory=True)
+        self._h_dev.copy_(h_host, non_blocking=True)
+        self.decode(self._h_dev, layer)
+        self._out_host.copy_(self.bufs.h_out, non_blocking=True)
+        self._sel_host.copy_(self.bufs.sel, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self._out_host, self._sel_host
+
+    @staticmethod
+    def host_bytes(d: int, k: int):
+        """(h2d, d2h) bytes of one decode_host call."""
+        return d * 4, d * 4 + k * 4
+
+    # ------------------------------------------------------------ prefill
+    def prefill(self, h: torch.Tensor, layer: int = 0, *, hist=None, tokens_per_seq: int = 0,
+                hist_seq_stride: int = 0, group_up: int = 0, group_down: int = 0):
+        """T tokens (h: (T, d) fp32 on device) through MoE layer `layer`.
+        Returns dict(out, p, p_pred, topk_idx, topk_w).  `hist` (optional,
+        int32 view [seq, E] of this layer) receives the activation counts."""
+        m = self.model
+        nxt = m.gate[layer + 1] if layer + 1 < m.shape.num_layers else None
+        r = ops.router(h, m.norm[layer], m.gate[layer], nxt, self.k, hist=hist,
+                       tokens_per_seq=tokens_per_seq, hist_seq_stride=hist_seq_stride)
+        pr = ops.permute(r["topk_idx"], self.E, r["x"])
+        slot_of = m.slot_of[layer]
+        act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_of, m.slab, m.n_slots,
+                                 m.slot_elems, self.d, self.ffn, group_up)
+        y = ops.expert_gemm_down(act, pr["offsets"], slot_of, m.slab, m.n_slots, m.slot_elems,
+                                 self.d, self.ffn, group_down)
+        out = ops.combine(h, y, pr["inv"], r["topk_w"])
+        r["out"] = out
+        r["offsets"] = pr["offsets"]
+        return r
+
+    @staticmethod
+    def prefill_kernels() -> int:
+        """Kernel launches of one prefill layer: router, permute (count, scan,
+        scatter, gather), up GEMM, down GEMM, combine."""
+        return 8
