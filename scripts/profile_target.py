@@ -1,0 +1,23 @@
+"""Minimal launch sequences for ncu captures (never a timing source)."""
+import sys
+import torch
+sys.path.insert(0, ".")
+import paper_2501_10375_b200 as P
+from paper_2501_10375_b200.engine import MoEBlockEngine
+from paper_2501_10375_b200.model import MoEModel
+
+what = sys.argv[1] if len(sys.argv) > 1 else "decode"
+d, ffn, E, k = 4096, 14336, 8, 2
+m = MoEModel(P.ModelShape(2, E, k), d, ffn, seed=0, resident_layers=[0])
+eng = MoEBlockEngine(m)
+if what == "decode":
+    hs = [m.input_hidden(1, stream=9, step=i)[0] for i in range(8)]
+    for i in range(8):
+        eng.decode(hs[i])
+else:
+    T = 32768
+    h = m.input_hidden(T, stream=5)
+    for _ in range(2):
+        eng.prefill(h, 0)
+torch.cuda.synchronize()
+print("done", what)
