@@ -146,6 +146,21 @@ int daop_combine(const float* d_h, const float* d_y_sorted, const int32_t* d_inv
                  const float* d_w, int64_t t, int32_t k, int32_t d, float* d_out,
                  daop_stream_t stream);
 
+/* decode-side combine when some picks ran on the slow (host) tier:
+ * d_out[i] = d_h[i] + sum_{q<k} d_w[q] * d_y[q*d + i]   (fixed q order) */
+int daop_combine_dense(const float* d_h, const float* d_y, const float* d_w, int32_t k,
+                       int32_t d, float* d_out, daop_stream_t stream);
+
+/* ------------------------------------------------ DAOP slow tier (host CPU)
+ * SwiGLU expert on the host for experts resident in pinned host memory
+ * (moesim "slow device"): h_x (n, d) bf16 -> h_y (n, d) fp32
+ * with act = bf16(silu(x.W1^T) * (x.W3^T)), y = act.W2^T, fp32 accumulation
+ * (AVX-512 BF16 when available).  h_act_scratch (n*ffn bf16) may be NULL. */
+int daop_host_expert_ffn(const uint16_t* h_x, int64_t n, const uint16_t* h_w1,
+                         const uint16_t* h_w3, const uint16_t* h_w2, int32_t d, int32_t ffn,
+                         float* h_y, uint16_t* h_act_scratch, int32_t threads);
+int daop_host_caps(int32_t* avx512_bf16, int32_t* hw_threads);
+
 /* ------------------------------------------------ grouped expert GEMMs (prefill)
  * tcgen05/TMEM/TMA grouped GEMMs over expert-sorted rows.  Expert e owns rows
  * [d_offsets[e], d_offsets[e+1]) and its weights live in slab slot

@@ -167,3 +167,31 @@ def moe_layer(model: OracleModel, layer: int, h: np.ndarray, sel=None, w=None,
                             model.w2(layer, e))
     out = combine(h, y, inv, w)
     return {"x": x, "p": p, "p_hat": ph, "sel": sel, "w": w, "out": out}
+
+
+def daop_decode_token(model: OracleModel, h: np.ndarray, sel_per_layer, start: int,
+                      weights_from_pred: bool = True, engine: str = "daop"):
+    """One decode token through all layers with the engine's decisions injected
+    (teacher forcing).  Below `start` (or for fiddler) picks run on the current
+    x_l with true-gate weights; from `start` on (daop) weights come from the
+    prediction carried on layer l-1 and slow picks -- flagged by the caller --
+    use the stale x_{l-1} (policies.py:325-330).
+
+    sel_per_layer: list of (experts, slow_flags) per layer.  Returns h'."""
+    h = h.astype(np.float32)[None, :]
+    x_prev, ph_prev = None, None
+    for l in range(model.L):
+        x = rmsnorm(h, model.norm(l))
+        wg_next = model.gate(l + 1) if l + 1 < model.L else None
+        p, ph = router(x, model.gate(l), wg_next)
+        experts, slow = sel_per_layer[l]
+        plan_l = engine == "daop" and l >= start
+        src = ph_prev if (plan_l and weights_from_pred) else p
+        g = src[0, experts].astype(np.float32)
+        w = g / g.sum()
+        out = h.copy()
+        for j, e in enumerate(experts):
+            xin = x_prev if (plan_l and slow[j]) else x
+            out = out + w[j] * expert_ffn(xin, model.w1(l, e), model.w3(l, e), model.w2(l, e))
+        h, x_prev, ph_prev = out, x, ph
+    return h[0]

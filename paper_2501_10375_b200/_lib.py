@@ -45,6 +45,9 @@ PROTOS = {
     "daop_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_decode_workspace": [I32, I32, I32, I32, P],
     "daop_decode_timeline": [I32, P, I32],
+    "daop_combine_dense": [P, P, P, I32, I32, P, P],
+    "daop_host_expert_ffn": [P, I64, P, P, P, I32, I32, P, P, I32],
+    "daop_host_caps": [P, P],
     "daop_decode_layer": [P, P, P, P, P, P, P, P, I64, I32, I32, I32, I32, I32, I32, I32, F32,
                           P, P, P, P, P, P, P, P, P, P, I32, P],
 }

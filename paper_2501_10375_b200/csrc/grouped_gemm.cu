@@ -104,7 +104,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     s.prefix[0] = 0;
     for (int e = 0; e <= E; ++e) s.off[e] = p.offsets[e];
     for (int e = 0; e < E; ++e) {
-      const int64_t me = s.off[e + 1] - s.off[e];
+      // experts without an HBM slot (slow tier) get no tiles: their rows are
+      // computed by the host tier and written into the output by the caller
+      const int64_t me = p.slot_of[e] >= 0 ? s.off[e + 1] - s.off[e] : 0;
       s.mt[e] = static_cast<int>((me + GB_M - 1) / GB_M);
       acc += s.mt[e] * p.n_tiles;
       s.prefix[e + 1] = acc;

@@ -1,0 +1,206 @@
+// DAOP slow tier: SwiGLU expert FFN on the host CPU, weights in pinned host
+// memory (the "slow device" of moesim/placement.py:1-8, executed as in
+// slow experts of layer l run on the CPU -- on the current
+// input below the prediction start layer, on the stale x_{l-1} above it).
+//
+// Same numeric contract as the GPU experts: bf16 x, bf16 weights, fp32
+// accumulation, act = bf16(silu(x.W1) * (x.W3)), y = act . W2 in fp32.
+// Inner products use AVX-512 BF16 (vdpbf16ps) when the CPU has it (Sapphire
+// Rapids on the GPU box), a scalar loop otherwise.  Rows are split over a
+// persistent thread pool.  Compiled as host code inside libdaop_b200.so.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include <immintrin.h>
+
+#include "common.cuh"
+
+namespace daop {
+namespace host {
+
+static inline float bf2f(uint16_t b) {
+  uint32_t u = static_cast<uint32_t>(b) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+static inline uint16_t f2bf(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x40);  // NaN
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+static float dot_scalar(const uint16_t* a, const uint16_t* b, int n) {
+  float acc = 0.f;
+  for (int i = 0; i < n; ++i) acc += bf2f(a[i]) * bf2f(b[i]);
+  return acc;
+}
+
+__attribute__((target("avx512f,avx512bf16,avx512bw,avx512vl"))) static float dot_avx512bf16(
+    const uint16_t* a, const uint16_t* b, int n) {
+  __m512 acc0 = _mm512_setzero_ps(), acc1 = _mm512_setzero_ps();
+  int i = 0;
+  for (; i + 64 <= n; i += 64) {
+    __m512bh x0 = (__m512bh)_mm512_loadu_si512(a + i);
+    __m512bh w0 = (__m512bh)_mm512_loadu_si512(b + i);
+    __m512bh x1 = (__m512bh)_mm512_loadu_si512(a + i + 32);
+    __m512bh w1 = (__m512bh)_mm512_loadu_si512(b + i + 32);
+    acc0 = _mm512_dpbf16_ps(acc0, x0, w0);
+    acc1 = _mm512_dpbf16_ps(acc1, x1, w1);
+  }
+  for (; i + 32 <= n; i += 32) {
+    __m512bh x0 = (__m512bh)_mm512_loadu_si512(a + i);
+    __m512bh w0 = (__m512bh)_mm512_loadu_si512(b + i);
+    acc0 = _mm512_dpbf16_ps(acc0, x0, w0);
+  }
+  float r = _mm512_reduce_add_ps(_mm512_add_ps(acc0, acc1));
+  for (; i < n; ++i) r += bf2f(a[i]) * bf2f(b[i]);
+  return r;
+}
+
+static bool have_bf16() {
+  static int v = -1;
+  if (v < 0) v = __builtin_cpu_supports("avx512bf16") && __builtin_cpu_supports("avx512f") ? 1 : 0;
+  return v == 1;
+}
+
+static float dot(const uint16_t* a, const uint16_t* b, int n) {
+  return have_bf16() ? dot_avx512bf16(a, b, n) : dot_scalar(a, b, n);
+}
+
+// ------------------------------------------------------------------ pool
+
+class Pool {
+ public:
+  explicit Pool(int n) : n_(n) {
+    for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return n_; }
+  // run fn(worker, begin, end) over [0, total) split in n_ contiguous parts
+  void run(int64_t total, const std::function<void(int, int64_t, int64_t)>& fn) {
+    std::unique_lock<std::mutex> lk(run_m_);
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      total_ = total;
+      pending_ = n_;
+      ++gen_;
+    }
+    cv_.notify_all();
+    std::unique_lock<std::mutex> g(m_);
+    done_cv_.wait(g, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void loop(int id) {
+    uint64_t seen = 0;
+    while (true) {
+      const std::function<void(int, int64_t, int64_t)>* fn;
+      int64_t total;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        fn = fn_;
+        total = total_;
+      }
+      const int64_t a = total * id / n_, b = total * (id + 1) / n_;
+      if (a < b) (*fn)(id, a, b);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_cv_.notify_all();
+      }
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex m_, run_m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int, int64_t, int64_t)>* fn_ = nullptr;
+  int64_t total_ = 0;
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+static Pool* pool_for(int threads) {
+  static std::mutex m;
+  static Pool* p = nullptr;
+  std::lock_guard<std::mutex> g(m);
+  if (!p || p->size() != threads) {
+    delete p;
+    p = new Pool(threads);
+  }
+  return p;
+}
+
+}  // namespace host
+}  // namespace daop
+
+using namespace daop;
+
+extern "C" int daop_host_expert_ffn(const uint16_t* x, int64_t n, const uint16_t* w1,
+                                    const uint16_t* w3, const uint16_t* w2, int32_t d,
+                                    int32_t ffn, float* y, uint16_t* act_scratch,
+                                    int32_t threads) {
+  if (n < 0 || d <= 0 || ffn <= 0) {
+    set_error("host_expert_ffn: invalid shape");
+    return DAOP_ERR_SHAPE;
+  }
+  if (n == 0) return DAOP_OK;
+  if (threads < 1) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  host::Pool* pool = host::pool_for(threads);
+  std::vector<uint16_t> own;
+  uint16_t* act = act_scratch;
+  if (!act) {
+    own.resize(static_cast<size_t>(n) * ffn);
+    act = own.data();
+  }
+  // up: rows i of W1/W3 split over workers; every token reuses the row from cache
+  pool->run(ffn, [&](int, int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+      const uint16_t* r1 = w1 + i * d;
+      const uint16_t* r3 = w3 + i * d;
+      for (int64_t t = 0; t < n; ++t) {
+        const float g = host::dot(x + t * d, r1, d);
+        const float u = host::dot(x + t * d, r3, d);
+        const float s = g / (1.0f + std::exp(-g));
+        act[t * ffn + i] = host::f2bf(s * u);
+      }
+    }
+  });
+  // down: rows j of W2
+  pool->run(d, [&](int, int64_t a, int64_t b) {
+    for (int64_t j = a; j < b; ++j) {
+      const uint16_t* r2 = w2 + j * ffn;
+      for (int64_t t = 0; t < n; ++t) y[t * d + j] = host::dot(act + t * ffn, r2, ffn);
+    }
+  });
+  return DAOP_OK;
+}
+
+extern "C" int daop_host_caps(int32_t* avx512_bf16, int32_t* hw_threads) {
+  *avx512_bf16 = host::have_bf16() ? 1 : 0;
+  *hw_threads = static_cast<int32_t>(std::thread::hardware_concurrency());
+  return DAOP_OK;
+}

@@ -126,6 +126,18 @@ __global__ void combine_kernel(const float* __restrict__ h, const float* __restr
   }
 }
 
+// decode-side combine when some picks ran on the host tier:
+// out[i] = h[i] + sum_{q<k} w[q] * y[q, i]   (fixed q order, like the fused path)
+__global__ void combine_dense_kernel(const float* __restrict__ h, const float* __restrict__ y,
+                                     const float* __restrict__ w, int k, int d,
+                                     float* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) {
+    float o = h[i];
+    for (int q = 0; q < k; ++q) o = fmaf(w[q], y[static_cast<int64_t>(q) * d + i], o);
+    out[i] = o;
+  }
+}
+
 }  // namespace daop
 
 using namespace daop;
@@ -187,6 +199,13 @@ int daop_combine(const float* h, const float* y_sorted, const int32_t* inv, cons
   combine_kernel<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(h, y_sorted, inv, w, T, k,
                                                                           d / 4, out);
   DAOP_CHECK_LAUNCH("combine");
+  return DAOP_OK;
+}
+
+int daop_combine_dense(const float* h, const float* y, const float* w, int32_t k, int32_t d,
+                       float* out, daop_stream_t stream) {
+  combine_dense_kernel<<<(d + 255) / 256, 256, 0, as_stream(stream)>>>(h, y, w, k, d, out);
+  DAOP_CHECK_LAUNCH("combine_dense");
   return DAOP_OK;
 }
 

@@ -1,0 +1,316 @@
+"""DAOP sequence engine: the reference's `run_single` flow, executed.
+
+moesim/experiment.py:145-211 (`run_single`) *prices* a sequence under DAOP:
+
+  placement0 = init_from_calibration(calib, ecr)              placement.py:128
+  placement, swaps = allocate_for_sequence(placement0,
+                         expert_counts(trace, "prefill"))     placement.py:188
+  simulate_prefill(trace, placement0, swaps)                  simulator.py:408
+  simulate_decode(trace, placement, PolicyConfig("daop"))     simulator.py:259
+
+`DaopEngine` *executes* the same order on the B200 with real numerics:
+
+  * init: placement0 from the calibration matrix (native, bit-exact); the HBM
+    slab holds exactly `slot_budget` expert slots, every expert also lives in
+    a pinned host pool (the slow tier and the migration source).
+  * prefill: per layer, the fused router produces the layer's activation
+    counts on device (`hist`), Alg. 1 runs for that layer right after its gate
+    (swaps are issued after the gate, simulator.py:446-456), each swap is a
+    pinned-host -> HBM `cudaMemcpyAsync` on a side stream, and the layer's
+    experts run at the post-swap residence (resident ones on tcgen05 grouped
+    GEMMs, waiting on the migration event; the rest on the host tier).
+  * decode: per token and layer, one decode launch; below the prediction
+    start layer the selection is the layer's own top-k (Fiddler rule), from
+    it on the DAOP plan on the prediction carried by layer l-1 with graceful
+    degradation -- computed on device inside the launch.  Slow picks run on
+    the host tier on the current input (l < start) or the stale x_{l-1}
+    (pre-calculation, l >= start), and are combined with the resident picks
+    in fixed pick order.
+  * everything the reference consumes is exported: the `RoutingTrace` (true
+    gate of every layer + next-layer predictions, fp32 probabilities widened
+    to float64), placements, `SwapEvent`s, per-token `LayerPlan`s and the
+    simulator's counters (`migrations`, `slow_executions`, `degradations`,
+    `stale_inputs`), so the reference's own decision functions can be run on
+    the exported trace and compared with `==`.
+
+This first version synchronises with the host once per layer (to hand the
+slow tier its inputs); the decision path is fully on device.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .errors import ConfigError, ShapeMismatchError
+from .model import KIND_EXPERT, MoEModel, make_tag
+from .placement import (SWAP_IN_OUT_DEFAULT, ExpertPlacement, SwapEvent,
+                        allocate_for_sequence, init_from_calibration)
+from .policies import PolicyConfig, decode_counters, plans_from_arrays
+from .trace import ModelShape, RoutingTrace
+
+
+class HostExpertPool:
+    """Every expert's [W1 | W3 | W2] in pinned host memory (bf16), generated
+    with the same counter-based generator as the device (bit-identical)."""
+
+    def __init__(self, shape: ModelShape, d: int, ffn: int, seed: int = 0, threads=None):
+        self.shape, self.d, self.ffn, self.seed = shape, d, ffn, seed
+        L, E = shape.num_layers, shape.num_experts
+        self.slot_elems = 3 * ffn * d
+        self.buf = torch.empty((L * E, self.slot_elems), dtype=torch.bfloat16, pin_memory=True)
+        th = threads or len(os.sched_getaffinity(0))
+        sc_in = float(np.float32(1.0 / np.sqrt(d)))
+        sc_ff = float(np.float32(1.0 / np.sqrt(ffn)))
+        for l in range(L):
+            for e in range(E):
+                base = self.buf[l * E + e].data_ptr()
+                for mtx, (off, n, sc) in enumerate(((0, ffn * d, sc_in), (ffn * d, ffn * d, sc_in),
+                                                    (2 * ffn * d, d * ffn, sc_ff))):
+                    _lib.call("daop_fill_uniform_bf16_host", base + off * 2, n, seed,
+                              make_tag(KIND_EXPERT, l, e, mtx), sc, 0, th)
+
+    def slot(self, layer: int, expert: int) -> torch.Tensor:
+        return self.buf[layer * self.shape.num_experts + expert]
+
+    def ptrs(self, layer: int, expert: int):
+        b = self.slot(layer, expert).data_ptr()
+        fd = self.ffn * self.d
+        return b, b + fd * 2, b + 2 * fd * 2
+
+
+def host_expert_ffn(pool: HostExpertPool, layer: int, expert: int, x_bf16: np.ndarray,
+                    threads: int = 0) -> np.ndarray:
+    """Slow-tier execution of one expert on (n, d) bf16 inputs -> (n, d) fp32."""
+    x = np.ascontiguousarray(x_bf16, dtype=np.uint16)
+    n = x.shape[0]
+    y = np.empty((n, pool.d), dtype=np.float32)
+    w1, w3, w2 = pool.ptrs(layer, expert)
+    _lib.call("daop_host_expert_ffn", x.ctypes.data, n, w1, w3, w2, pool.d, pool.ffn,
+              y.ctypes.data, 0, threads)
+    return y
+
+
+@dataclass
+class PrefillResult:
+    out: torch.Tensor
+    counts: np.ndarray                # (L, E) int64, from the device activation counter
+    placement_initial: ExpertPlacement
+    placement: ExpertPlacement
+    swaps: list
+    true_scores: np.ndarray           # (T, L, E) float64 (fp32-exact)
+    pred_scores: np.ndarray           # (T, L, E) float64, zero on the last layer
+    slow_executions: int
+    ms: float
+
+
+@dataclass
+class DecodeResult:
+    out: torch.Tensor
+    plans: list                       # L LayerPlans
+    true_scores: np.ndarray           # (L, E)
+    pred_scores: np.ndarray           # (L, E)
+    ms: float
+
+
+@dataclass
+class SequenceRecord:
+    prefill: PrefillResult
+    decode: list = field(default_factory=list)
+    trace: RoutingTrace | None = None
+    counts: dict = field(default_factory=dict)
+    tokens_per_second: float = float("nan")
+
+
+class DaopEngine:
+    """Executes DAOP (or the Fiddler rule) for one sequence on one B200."""
+
+    def __init__(self, shape: ModelShape, d_model: int, d_ff: int, calib, ecr: float,
+                 config: PolicyConfig | None = None, seed: int = 0, device="cuda",
+                 swap_in_out: float = SWAP_IN_OUT_DEFAULT, weights_from_pred: bool = True,
+                 host_pool: HostExpertPool | None = None, host_threads: int = 0):
+        self.config = config or PolicyConfig("daop")
+        if self.config.engine not in ("daop", "fiddler"):
+            raise ConfigError(f"engine {self.config.engine!r} is outside the DAOP hot path")
+        self.shape = shape
+        self.placement0 = init_from_calibration(calib, ecr, shape)
+        self.swap_in_out = swap_in_out
+        self.weights_from_pred = weights_from_pred
+        self.host_threads = host_threads
+        self.model = MoEModel(shape, d_model, d_ff, seed=seed, device=device,
+                              n_slots=self.placement0.slot_budget, resident_layers=[])
+        self.pool = host_pool or HostExpertPool(shape, d_model, d_ff, seed)
+        self.mig_stream = torch.cuda.Stream(device=self.model.device)
+        self.migrations_done = 0
+        for l, s in enumerate(self.placement0.on_fast):
+            for e in sorted(s):
+                self._migrate_in(l, e, self.model._free[0])
+        torch.cuda.synchronize()
+        self.placement = self.placement0
+        self.migrations_done = 0
+        E, k = shape.num_experts, shape.top_k
+        self.bufs = [ops.DecodeBuffers(d_model, d_ff, E, k, self.model.device) for _ in range(2)]
+
+    # ------------------------------------------------------------ residency
+    def _migrate_in(self, layer: int, expert: int, slot: int):
+        """pinned host pool -> HBM slot on the migration stream; returns its event."""
+        m = self.model
+        if slot in m._free:
+            m._free.remove(slot)
+        # the slot may still be read by work already queued on the compute stream
+        self.mig_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.mig_stream):
+            m.slab[slot].copy_(self.pool.slot(layer, expert), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.mig_stream)
+        torch.cuda.current_stream().wait_event(ev)  # table update ordered after the copy
+        m._bind(layer, expert, slot)
+        self.migrations_done += 1
+        return ev
+
+    def _apply_swaps(self, layer: int, events):
+        evs = []
+        m = self.model
+        for ev in events:
+            slot = m.evict(layer, ev.swapped_out)
+            evs.append(self._migrate_in(layer, ev.swapped_in, slot))
+        return evs
+
+    # ------------------------------------------------------------ prefill
+    def prefill(self, h: torch.Tensor) -> PrefillResult:
+        m = self.model
+        L, E, k = self.shape.num_layers, self.shape.num_experts, self.shape.top_k
+        T, d = h.shape
+        t0 = time.perf_counter()
+        hist = torch.zeros((1, L, E), dtype=torch.int32, device=m.device)
+        true_sc = np.zeros((T, L, E))
+        pred_sc = np.zeros((T, L, E))
+        swaps_all = []
+        new_sets = [set(s) for s in self.placement0.on_fast]
+        slow_execs = 0
+        for l in range(L):
+            nxt = m.gate[l + 1] if l + 1 < L else None
+            r = ops.router(h, m.norm[l], m.gate[l], nxt, k, hist=hist[:, l], tokens_per_seq=T,
+                           hist_seq_stride=L * E)
+            counts_l = hist[0, l].to(torch.int64).cpu().numpy()
+            # Alg. 1 for this layer right after its gate (placement.py:188-237)
+            one = ExpertPlacement(ModelShape(1, E, k), [self.placement0.on_fast[l]],
+                                  self.placement0.slot_budget)
+            after, ev1 = allocate_for_sequence(one, counts_l[None, :], self.swap_in_out)
+            evs = [SwapEvent(l, e.swapped_in, e.swapped_out, e.hot_tokens, e.cold_tokens)
+                   for e in ev1]
+            swaps_all.extend(evs)
+            new_sets[l] = set(after.on_fast[0])
+            self._apply_swaps(l, evs)
+            # experts at the post-swap residence
+            pr = ops.permute(r["topk_idx"], E, r["x"])
+            slot_of = m.slot_of[l]
+            act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_of, m.slab, m.n_slots,
+                                     m.slot_elems, d, m.ffn)
+            y = ops.expert_gemm_down(act, pr["offsets"], slot_of, m.slab, m.n_slots,
+                                     m.slot_elems, d, m.ffn)
+            off = pr["offsets"].cpu().numpy()
+            resident = m.resident_mask()[l]
+            for e in range(E):
+                a, b = int(off[e]), int(off[e + 1])
+                if a == b or resident[e]:
+                    continue
+                xs = pr["x_perm"][a:b].view(torch.int16).cpu().numpy().view(np.uint16)
+                ys = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
+                y[a:b].copy_(torch.from_numpy(ys))
+                slow_execs += 1
+            out = ops.combine(h, y, pr["inv"], r["topk_w"])
+            true_sc[:, l, :] = r["p"].cpu().numpy()
+            if nxt is not None:
+                pred_sc[:, l, :] = r["p_pred"].cpu().numpy()
+            h = out
+        torch.cuda.synchronize()
+        self.placement = ExpertPlacement(self.shape, new_sets, self.placement0.slot_budget)
+        counts = hist[0].to(torch.int64).cpu().numpy()
+        return PrefillResult(h, counts, self.placement0, self.placement, swaps_all, true_sc,
+                             pred_sc, slow_execs, 1e3 * (time.perf_counter() - t0))
+
+    # ------------------------------------------------------------ decode
+    def decode(self, h: torch.Tensor) -> DecodeResult:
+        """One decode token (h: (d,) fp32 on device) through every layer."""
+        m = self.model
+        cfg = self.config
+        L, E, k = self.shape.num_layers, self.shape.num_experts, self.shape.top_k
+        start = cfg.prediction_start_layer
+        daop = cfg.engine == "daop"
+        t0 = time.perf_counter()
+        sel = np.zeros((L, k), dtype=np.int32)
+        fast = np.zeros((L, k), dtype=np.uint8)
+        drop = np.full((L, k), -1, dtype=np.int32)
+        sub = np.full((L, k), -1, dtype=np.int32)
+        nd = np.zeros(L, dtype=np.int32)
+        true_sc = np.zeros((L, E))
+        pred_sc = np.zeros((L, E))
+        prev = None
+        for l in range(L):
+            b = self.bufs[l % 2]
+            mode = 1 if (daop and l >= start) else 0
+            nxt = m.gate[l + 1] if l + 1 < L else None
+            ops.decode_layer(h, m.norm[l], m.gate[l], nxt, m.fast[l], m.slot_of[l], m.slab,
+                             m.slot_elems, m.d, m.ffn, k, b,
+                             pred_prev=prev.p_pred if mode == 1 else None, mode=mode,
+                             graceful=cfg.graceful_degradation,
+                             weights_from_pred=self.weights_from_pred and mode == 1)
+            s_l = b.sel.cpu().numpy()
+            f_l = b.is_fast.cpu().numpy()
+            dg = b.deg.cpu().numpy()
+            sel[l], fast[l] = s_l, f_l
+            nd[l] = dg[2 * k]
+            drop[l, : nd[l]] = dg[: nd[l]]
+            sub[l, : nd[l]] = dg[k: k + nd[l]]
+            true_sc[l] = b.p.cpu().numpy()
+            if nxt is not None:
+                pred_sc[l] = b.p_pred.cpu().numpy()
+            if not f_l.all():
+                # slow tier: stale x_{l-1} for pre-calculated picks, else current x_l
+                xin = prev.x if mode == 1 else b.x
+                xs = xin.view(torch.int16).cpu().numpy().view(np.uint16)[None, :]
+                for q in range(k):
+                    if not f_l[q]:
+                        yq = host_expert_ffn(self.pool, l, int(s_l[q]), xs, self.host_threads)
+                        b.y[q].copy_(torch.from_numpy(yq[0]))
+                out = torch.empty_like(h)
+                _lib.call("daop_combine_dense", h.data_ptr(), b.y.data_ptr(), b.w.data_ptr(), k,
+                          m.d, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                h = out
+            else:
+                h = b.h_out.clone()
+            prev = b
+        torch.cuda.synchronize()
+        plans = plans_from_arrays(sel, fast, drop, sub, nd, pred_sc, cfg)
+        return DecodeResult(h, plans, true_sc, pred_sc, 1e3 * (time.perf_counter() - t0))
+
+    # ------------------------------------------------------------ sequence
+    def run_sequence(self, h_prompt: torch.Tensor, decode_inputs, sequence_id: str = "seq"):
+        """prefill + decode of one sequence; returns a SequenceRecord whose
+        trace / placements / swaps / plans / counters mirror run_single."""
+        pre = self.prefill(h_prompt)
+        rec = SequenceRecord(prefill=pre)
+        lat = 0.0
+        for h in decode_inputs:
+            dr = self.decode(h)
+            rec.decode.append(dr)
+            lat += dr.ms
+        L = self.shape.num_layers
+        pm = np.zeros(pre.true_scores.shape[:2], dtype=bool)
+        pm[:, : L - 1] = True
+        n = len(rec.decode)
+        dt = np.stack([r.true_scores for r in rec.decode]) if n else np.zeros((0, L, self.shape.num_experts))
+        dp = np.stack([r.pred_scores for r in rec.decode]) if n else np.zeros_like(dt)
+        dm = np.zeros(dt.shape[:2], dtype=bool)
+        dm[:, : L - 1] = True
+        rec.trace = RoutingTrace(self.shape, sequence_id, pre.true_scores, dt, pre.pred_scores,
+                                 pm, dp, dm)
+        rec.counts = decode_counters([r.plans for r in rec.decode], self.config)
+        rec.tokens_per_second = 1e3 * n / lat if lat > 0 else float("nan")
+        return rec

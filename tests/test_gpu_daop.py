@@ -1,0 +1,93 @@
+"""End-to-end DAOP sequence on the GPU vs the oracle (reference decisions).
+
+The engine runs calibration placement -> prefill (device activation counter,
+Alg. 1 per layer, pinned-memory migrations, slow experts on the host tier)
+-> decode (device DAOP plans, degradation, stale pre-calculation on the host
+tier).  Then the REFERENCE decision flow (oracle/decisions.py, pinned to
+moesim's golden vectors) is run on the trace the engine exported and every
+decision must agree bit-for-bit; hidden states are checked teacher-forced.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import decisions as D  # noqa: E402
+from oracle import numerics as N  # noqa: E402
+
+
+def _calib(L, E, k, seed):
+    rng = np.random.default_rng(seed)
+    c = rng.dirichlet(np.ones(E) * 0.7, size=L) * k
+    return c
+
+
+@pytest.mark.parametrize("engine,ecr,start", [("daop", 0.5, 4), ("daop", 0.25, 2),
+                                              ("fiddler", 0.5, 4), ("daop", 1.0, 4)])
+def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.daop import DaopEngine
+
+    L, E, k, d, ffn = 8, 8, 2, 256, 512
+    shape = P.ModelShape(L, E, k)
+    calib = _calib(L, E, k, 5)
+    cfg = P.PolicyConfig(engine, prediction_start_layer=start)
+    eng = DaopEngine(shape, d, ffn, calib, ecr, cfg, seed=0, device="cuda")
+    prompt = eng.model.input_hidden(64, stream=11)
+    toks = [eng.model.input_hidden(1, stream=12, step=i)[0] for i in range(10)]
+    rec = eng.run_sequence(prompt, toks, "s0")
+    tr = rec.trace
+
+    # (a5) calibration placement
+    sets0, budget = D.init_from_calibration(calib, ecr)
+    assert [set(s) for s in rec.prefill.placement_initial.on_fast] == sets0
+    assert rec.prefill.placement_initial.slot_budget == budget
+    # (a3) device activation counter == reference expert_counts on the exported trace
+    counts = D.expert_counts(tr.prefill_true, k)
+    assert np.array_equal(rec.prefill.counts, counts)
+    # (a6) Alg. 1 swaps (daop reallocates; moesim/experiment.py:158-163)
+    sets, evs = D.allocate_for_sequence(sets0, counts)
+    assert [(s.layer, s.swapped_in, s.swapped_out, s.hot_tokens, s.cold_tokens)
+            for s in rec.prefill.swaps] == evs
+    assert [set(s) for s in rec.prefill.placement.on_fast] == sets
+    # the HBM slot table follows the placement
+    assert np.array_equal(eng.model.resident_mask(), rec.prefill.placement.mask())
+    # (a7/a8/a9) per-token plans on the exported trace
+    mask = np.array([l < L - 1 for l in range(L)])
+    oplans = [D.plan_token(tr.decode_true[t], tr.decode_predicted[t], mask, sets, k, engine,
+                           start=start) for t in range(tr.num_decode_tokens)]
+    for t, (got, exp) in enumerate(zip([r.plans for r in rec.decode], oplans)):
+        for l in range(L):
+            assert [(x.expert, x.device, x.input_source, x.precalc) for x in got[l].executed] \
+                == [tuple(x) for x in exp[l]["executed"]], (t, l)
+            assert [(g.dropped_expert, g.substitute_expert) for g in got[l].degraded] \
+                == [(a, c) for a, _, c, _ in exp[l]["degraded"]], (t, l)
+    # (a10) simulator counters
+    assert rec.counts == D.decode_counters(oplans, engine, start)
+    # trace is reference-valid: sums to 1 within SCORE_SUM_TOL (checked at construction)
+    assert tr.num_decode_tokens == 10 and tr.num_prefill_tokens == 64
+
+    # numerics, teacher-forced with the engine's decisions
+    om = N.OracleModel(L, E, k, d, ffn, seed=0)
+    h = prompt.cpu().numpy()
+    ptop = D.topk_rows(tr.prefill_true.reshape(-1, E), k).reshape(64, L, k)
+    for l in range(L):
+        p = tr.prefill_true[:, l, :].astype(np.float32)
+        sel = ptop[:, l, :]
+        h = N.moe_layer(om, l, h, sel=sel, w=N.renorm_weights(p, sel))["out"]
+    ref = h
+    got = rec.prefill.out.cpu().numpy()
+    rms = float(np.sqrt(np.mean(ref.astype(np.float64) ** 2)))
+    assert np.abs(got - ref).max() <= 5e-3 * rms + 2e-3 * np.abs(ref).max()
+    for t in range(3):
+        plans = rec.decode[t].plans
+        sel = [([x.expert for x in p.executed], [x.device == "slow" for x in p.executed])
+               for p in plans]
+        ref = N.daop_decode_token(om, toks[t].cpu().numpy(), sel, start, True, engine)
+        got = rec.decode[t].out.cpu().numpy()
+        rms = float(np.sqrt(np.mean(ref.astype(np.float64) ** 2)))
+        assert np.abs(got - ref).max() <= 5e-3 * rms + 2e-3 * np.abs(ref).max(), t

@@ -1,0 +1,31 @@
+"""DAOP slow tier (host CPU expert FFN in libdaop_b200.so) vs the oracle.
+Runs on CPU in the build container (no GPU involved)."""
+
+import numpy as np
+
+from paper_2501_10375_b200 import _lib
+from oracle import numerics as N
+from oracle import rng as R
+
+
+def test_host_expert_ffn_matches_oracle():
+    d, ffn, n = 256, 512, 3
+    om = N.OracleModel(2, 4, 2, d, ffn, seed=7)
+    w1, w3, w2 = om.w1(1, 2), om.w3(1, 2), om.w2(1, 2)
+    to_bits = lambda a: np.ascontiguousarray(R.f32_to_bf16_bits(a))  # noqa: E731
+    b1, b3, b2 = to_bits(w1), to_bits(w3), to_bits(w2)
+    x = R.round_bf16(np.random.default_rng(0).normal(size=(n, d)).astype(np.float32))
+    xb = to_bits(x)
+    y = np.empty((n, d), dtype=np.float32)
+    _lib.call("daop_host_expert_ffn", xb.ctypes.data, n, b1.ctypes.data, b3.ctypes.data,
+              b2.ctypes.data, d, ffn, y.ctypes.data, 0, 4)
+    ref = N.expert_ffn(x, w1, w3, w2)
+    rms = float(np.sqrt(np.mean(ref ** 2)))
+    assert np.abs(y - ref).max() <= 2e-3 * rms + 1e-3 * np.abs(ref).max()
+
+
+def test_host_caps_reports():
+    a = np.zeros(1, dtype=np.int32)
+    t = np.zeros(1, dtype=np.int32)
+    _lib.call("daop_host_caps", a.ctypes.data, t.ctypes.data)
+    assert t[0] >= 1
