@@ -1,0 +1,96 @@
+"""Expert-parallel dispatch/combine with world_size 2 on CPU (gloo).
+
+The expert and router computations are the oracle's (numpy) -- this test
+covers the EP host logic: ownership, stable ordering, count exchange,
+payload all-to-all (incl. bf16 bits), reverse all-to-all and the fixed-order
+combine.  EP(2) must equal the single-process oracle layer over all tokens.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import numerics as N
+
+D, FFN, E, K, T_PER = 64, 128, 8, 2, 24
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2501_10375_b200.ep import ep_moe_layer, local_experts
+    om = N.OracleModel(2, E, K, D, FFN, seed=9)
+    mine = local_experts(rank, E, world)
+    W = {e: (om.w1(0, e), om.w3(0, e), om.w2(0, e)) for e in mine}
+    h_all = N.input_hidden(9, 3, 0, T_PER * world, D)
+    h = torch.from_numpy(h_all[rank * T_PER:(rank + 1) * T_PER].copy())
+
+    def router_fn(hh):
+        x = N.rmsnorm(hh.numpy(), om.norm(0))
+        p, _ = N.router(x, om.gate(0), om.gate(1))
+        from oracle.decisions import topk_rows
+        sel = topk_rows(p.astype(np.float64), K)
+        w = N.renorm_weights(p, sel)
+        xb = torch.from_numpy(x).to(torch.bfloat16)
+        return xb, torch.from_numpy(sel), torch.from_numpy(w)
+
+    def expert_fn(ids, xr):
+        out = np.zeros((xr.shape[0], D), dtype=np.float32)
+        xs = xr.to(torch.float32).numpy()
+        for e in torch.unique(ids).tolist():
+            assert e in mine, f"rank {rank} received expert {e}"
+            rows = (ids == e).numpy()
+            out[rows] = N.expert_ffn(xs[rows], *W[e])
+        return torch.from_numpy(out)
+
+    out, sel, w = ep_moe_layer(h, router_fn, expert_fn, E, K)
+    q.put((rank, out.numpy(), sel.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_ep_matches_single_process(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict()
+    for _ in range(world):
+        r, out, sel = q.get(timeout=60)
+        res[r] = (out, sel)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out = np.concatenate([res[r][0] for r in range(world)])
+    sel = np.concatenate([res[r][1] for r in range(world)])
+    om = N.OracleModel(2, E, K, D, FFN, seed=9)
+    h_all = N.input_hidden(9, 3, 0, T_PER * world, D)
+    ref = N.moe_layer(om, 0, h_all)
+    assert np.array_equal(sel, ref["sel"])
+    assert np.abs(out - ref["out"]).max() <= 1e-5 * (1 + np.abs(ref["out"]).max())
+
+
+def test_ownership_partition():
+    from paper_2501_10375_b200.ep import local_experts, owner_of
+    for G in (1, 2, 4, 8):
+        parts = [local_experts(r, 8, G) for r in range(G)]
+        assert sorted(sum(parts, [])) == list(range(8))
+        assert all(len(p) == 8 // G for p in parts)
+        assert owner_of(torch.arange(8), 8, G).tolist() == [e * G // 8 for e in range(8)]
