@@ -168,6 +168,9 @@ int daop_host_caps(int32_t* avx512_bf16, int32_t* hw_threads);
  *   up:   d_act (rows, ffn) bf16 = silu(x W1^T) * (x W3^T)
  *   down: d_y   (rows, d)   f32  = act W2^T
  * group_m <= 0 picks the default rasterisation group. */
+/* tuning switch: 0 = tcgen05.mma.cta_group::2 CTA-pair kernel (default),
+ * 1 = single-CTA kernel */
+int daop_set_gemm_mode(int32_t mode);
 int daop_expert_gemm_up(const uint16_t* d_x_perm, int64_t rows, int32_t d, int32_t ffn,
                         const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
                         const int64_t* d_offsets, const int32_t* d_slot_of, int32_t num_experts,

@@ -41,6 +41,7 @@ PROTOS = {
     "daop_permute_workspace": [I64, I32, I32, P],
     "daop_permute": [P, I64, I32, I32, P, I32, P, P, P, P, P, I64, P],
     "daop_combine": [P, P, P, P, I64, I32, I32, P, P],
+    "daop_set_gemm_mode": [I32],
     "daop_expert_gemm_up": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_decode_workspace": [I32, I32, I32, I32, P],

@@ -48,6 +48,7 @@ struct GemmParams {
   void* out;       // up: bf16 act (rows, out_ld); down: fp32 y (rows, out_ld)
   int64_t out_ld;
   int out_cols_per_tile;  // up: 128, down: 256
+  int policy;             // L2 hint set (tuning): 0 A last/B normal, 1 both normal, 2 both last, 3 A normal/B last
 };
 
 struct GemmSmem {
@@ -122,8 +123,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      const uint64_t pol_a = l2_evict_last_policy();
-      const uint64_t pol_b = l2_evict_last_policy();
+      // weights are read by every concurrent CTA of the wave (they run the
+      // m-tiles of one n-tile side by side): evict_first would evict a tile
+      // after its first reader and re-fetch it from DRAM for every m-tile
+      const uint64_t pol_a = l2_evict_last_policy();    // activations: re-read across n-tiles
+      const uint64_t pol_b = l2_evict_normal_policy();
       int stage = 0;
       uint32_t phase = 0;
       int e, m, n;
@@ -290,11 +294,271 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t*
   return DAOP_OK;
 }
 
+// ---------------------------------------------------------------- CTA-pair variant
+//
+// Same tiles, scheduled per CTA pair (cluster of 2 on one TPC) with
+// tcgen05.mma.cta_group::2: the pair computes a 256 x 256 tile, each CTA
+// loading its own 128 A rows and ONE of the two 128-row B boxes (up GEMM:
+// the W1 box on the leader, the W3 box on the follower) -- so a stage is 32 KB
+// per CTA instead of 48 KB (6 stages fit) and every B byte is fetched once per
+// pair instead of once per CTA.  The leader issues the MMAs; both CTAs' TMA
+// completions land on the leader's full barrier (2-SM TMA, peer bit cleared);
+// commits are multicast to both CTAs; both CTAs' epilogues release the
+// accumulator by remote-arriving on the leader's TMEM-empty barrier.
+constexpr int P_M = 256;                                  // pair tile rows
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * GB_K * 2;                 // 16 KB per CTA
+constexpr int P_B_BYTES = 128 * GB_K * 2;                 // 16 KB per CTA
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;      // 32 KB
+constexpr uint32_t P_IDESC = umma_idesc_bf16_f32(P_M, GB_N);
+
+struct PairSmem {
+  uint64_t full[P_STAGES];
+  uint64_t empty[P_STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  int32_t prefix[G_MAX_EXPERTS + 1];
+  int32_t mt[G_MAX_EXPERTS];
+  int64_t off[G_MAX_EXPERTS + 1];
+};
+
+__device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, int G, int t,
+                                              int& e, int& m, int& n) {
+  if (t >= s.prefix[E]) return false;
+  e = 0;
+  while (s.prefix[e + 1] <= t) ++e;
+  const int u = t - s.prefix[e];
+  const int grp = u / (G * nt);
+  const int r = u - grp * G * nt;
+  const int gm = min(G, s.mt[e] - grp * G);
+  m = grp * G + r % gm;
+  n = r / gm;
+  return true;
+}
+
+template <bool SWIGLU>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
+    grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                             const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = smem_u32(smem_raw);
+  uint8_t* tiles = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+  PairSmem& s = *reinterpret_cast<PairSmem*>(tiles + P_STAGES * P_STAGE_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int E = p.E;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < P_STAGES; ++i) {
+      mbar_init(&s.full[i], 2);   // leader: own expect_tx arrive + follower's remote arrive
+      mbar_init(&s.empty[i], 1);  // multicast commit
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s.tfull[i], 1);   // multicast commit
+      mbar_init(&s.tempty[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    fence_mbar_init();
+    int acc = 0;
+    s.prefix[0] = 0;
+    for (int e = 0; e <= E; ++e) s.off[e] = p.offsets[e];
+    for (int e = 0; e < E; ++e) {
+      const int64_t me = p.slot_of[e] >= 0 ? s.off[e + 1] - s.off[e] : 0;
+      s.mt[e] = static_cast<int>((me + P_M - 1) / P_M);
+      acc += s.mt[e] * p.n_tiles;
+      s.prefix[e + 1] = acc;
+    }
+  }
+  if (warp == 2) tmem_alloc_pair<512>(&s.tmem_base);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = s.tmem_base;
+  const int nt = p.n_tiles, G = p.group_m;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs)
+      uint64_t pol_a = l2_evict_last_policy();
+      uint64_t pol_b = l2_evict_normal_policy();  // shared by the wave's m-tiles
+      if (p.policy == 1) pol_a = l2_evict_normal_policy();
+      if (p.policy == 2) pol_b = l2_evict_last_policy();
+      if (p.policy == 3) {
+        pol_a = l2_evict_normal_policy();
+        pol_b = l2_evict_last_policy();
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      int e, m, n;
+      for (int t = cluster; map_tile_pair(s, E, nt, G, t, e, m, n); t += nclusters) {
+        const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * P_M) + rank * 128;
+        const int slot = p.slot_of[e];
+        const int brow = n * p.b_tile_rows + (leader ? 0 : p.b_half2);
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&s.empty[stage], phase ^ 1);
+          uint8_t* st = tiles + stage * P_STAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&s.full[stage], 2 * P_STAGE_BYTES);
+          else mbar_arrive_cluster(&s.full[stage], 0);
+          tma_load_2d_pair(st, &tmA, &s.full[stage], kb * GB_K, row0, pol_a);
+          tma_load_3d_pair(st + P_A_BYTES, &tmB, &s.full[stage], kb * GB_K, brow, slot, pol_b);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // MMA issuer (leader only)
+      int stage = 0, acc = 0, iters = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      int e, m, n;
+      for (int t = cluster; map_tile_pair(s, E, nt, G, t, e, m, n); t += nclusters) {
+        mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * GB_N;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&s.full[stage], phase);
+          tc_fence_after();
+          uint8_t* st = tiles + stage * P_STAGE_BYTES;
+          const uint64_t adesc = umma_desc_sw128(smem_u32(st));
+          const uint64_t bdesc = umma_desc_sw128(smem_u32(st + P_A_BYTES));
+#pragma unroll
+          for (int k = 0; k < GB_K / 16; ++k)
+            umma_bf16_pair(tmem_d, adesc + 2 * k, bdesc + 2 * k, P_IDESC, (kb | k) != 0);
+          umma_commit_pair(&s.empty[stage], 0x3);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&s.tfull[acc], 0x3);
+        ++iters;
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      // drain: wait until both epilogues released the last accumulator(s)
+      for (int i = 0; i < 2 && i < iters; ++i) {
+        mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int e, m, n;
+    for (int t = cluster; map_tile_pair(s, E, nt, G, t, e, m, n); t += nclusters) {
+      mbar_wait(&s.tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row_in_tile = rank * 128 + q * 32 + lane;
+      const int64_t me = s.off[e + 1] - s.off[e];
+      const bool valid = static_cast<int64_t>(m) * P_M + row_in_tile < me;
+      const int64_t grow = s.off[e] + static_cast<int64_t>(m) * P_M + row_in_tile;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * GB_N;
+      if constexpr (SWIGLU) {
+        uint16_t* out = static_cast<uint16_t*>(p.out) + grow * p.out_ld + n * 128;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tb + c, g);
+          tmem_ld32(tb + 128 + c, u);
+          tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float h0 = silu_f32(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+            const float h1 = silu_f32(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+            packed[i] = static_cast<uint32_t>(f32_to_bf16_bits(h0)) |
+                        (static_cast<uint32_t>(f32_to_bf16_bits(h1)) << 16);
+          }
+          if (valid) {
+            uint4* o = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
+        }
+      } else {
+        float* out = static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
+#pragma unroll 1
+        for (int c = 0; c < GB_N; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tb + c, v);
+          tmem_ld_wait();
+          if (valid) {
+            float4* o = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              o[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&s.tempty[acc], 0);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem_base);
+  }
+}
+
+static int g_gemm_mode = 0;    // 0: CTA pair (default), 1: single CTA
+static int g_gemm_policy = -1;  // L2 hint set override (tuning); -1 = per-GEMM default
+
 static size_t gemm_smem_bytes() { return 1024 + G_STAGES * G_STAGE_BYTES + sizeof(GemmSmem); }
+static size_t pair_smem_bytes() { return 1024 + P_STAGES * P_STAGE_BYTES + sizeof(PairSmem); }
 
 template <bool SWIGLU>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                        int64_t rows_total, cudaStream_t st) {
+  {
+    // L2::evict_last (the A operand, re-read by every n-tile of its group) is
+    // only honoured inside the persisting L2 set-aside, which defaults to 0
+    static bool done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+      int max_persist = 0;
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      if (max_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist);
+      cudaGetLastError();
+      done[dev] = true;
+    }
+  }
+  if (g_gemm_mode == 0) {
+    const size_t smem = pair_smem_bytes();
+    DAOP_CUDA(cudaFuncSetAttribute(grouped_gemm_pair_kernel<SWIGLU>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    const int64_t max_tiles = (rows_total / P_M + p.E) * static_cast<int64_t>(p.n_tiles);
+    int clusters = sm_count() / 2;
+    if (max_tiles < clusters) clusters = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
+    GemmParams pp = p;
+    pp.group_m = p.group_m > 1 ? p.group_m / 2 : 1;  // group counted in 256-row tiles
+    grouped_gemm_pair_kernel<SWIGLU><<<2 * clusters, G_THREADS, smem, st>>>(ta, tb, pp);
+    DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
+    return DAOP_OK;
+  }
   const size_t smem = gemm_smem_bytes();
   DAOP_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<SWIGLU>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -322,6 +586,17 @@ static int check_ffn_shape(int64_t rows, int32_t d, int32_t ffn, int32_t E) {
   return DAOP_OK;
 }
 
+extern "C" int daop_set_gemm_mode(int32_t mode) {
+  // low nibble: kernel (0 CTA pair, 1 single CTA); bits 4..5: L2 hint set (tuning)
+  if ((mode & 15) > 1 || (mode >> 4) > 3) {
+    set_error("gemm mode must be kernel (0 pair / 1 single) | policy << 4");
+    return DAOP_ERR_CONFIG;
+  }
+  g_gemm_mode = mode & 15;
+  g_gemm_policy = (mode >> 4) ? (mode >> 4) : -1;
+  return DAOP_OK;
+}
+
 extern "C" int daop_expert_gemm_up(const uint16_t* x_perm, int64_t rows, int32_t d, int32_t ffn,
                                    const uint16_t* slab, int64_t n_slots,
                                    int64_t slot_stride_elems, const int64_t* d_offsets,
@@ -342,7 +617,7 @@ extern "C" int daop_expert_gemm_up(const uint16_t* x_perm, int64_t rows, int32_t
   const uint32_t bbox[3] = {GB_K, 128, 1};
   if ((rc = make_tmap_bf16(&tb, slab, 3, bdims, bstr, bbox))) return rc;
   GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : 64,
-               128, ffn, act, ffn, 128};
+               128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0};
   return launch_gemm<true>(ta, tb, p, rows, as_stream(stream));
 }
 
@@ -366,7 +641,7 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
   const uint32_t bbox[3] = {GB_K, 128, 1};
   const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
   if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
-  GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, group_m > 0 ? group_m : 16,
-               GB_N, 128, y, d, GB_N};
+  GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, group_m > 0 ? group_m : 128,
+               GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2};
   return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
 }

@@ -66,6 +66,13 @@ def ep_moe_layer(h: torch.Tensor, router_fn, expert_fn, num_experts: int, k: int
     _a2a(y_back, y_recv, s_split, r_split, group)
     y = torch.empty_like(y_back)
     y[order] = y_back
+    if h.is_cuda:
+        # same fixed-order fused combine kernel as the single-GPU path
+        from . import ops
+        inv = torch.arange(T * k, dtype=torch.int32, device=h.device).view(T, k)
+        out = ops.combine(h.to(torch.float32).contiguous(), y, inv,
+                          w.to(torch.float32).contiguous())
+        return out, sel, w
     y = y.view(T, k, d)
     out = h.to(torch.float32).clone()
     for j in range(k):

@@ -94,6 +94,11 @@ def permute(topk_idx, num_experts, x=None):
     return {"offsets": offsets, "perm": perm, "inv": inv.view(t, k), "x_perm": x_perm}
 
 
+def set_gemm_mode(mode: int) -> None:
+    """0: tcgen05 CTA-pair grouped GEMM (default), 1: single-CTA kernel."""
+    _lib.call("daop_set_gemm_mode", int(mode))
+
+
 def expert_gemm_up(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, group_m=0):
     _dev(x_perm, offsets, slot_of, slab)
     rows = x_perm.shape[0]

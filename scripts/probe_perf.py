@@ -50,10 +50,13 @@ if what in ("prefill", "all"):
     so = m.slot_of[0].contiguous()
     t_r = ev_time(lambda: ops.router(h, m.norm[0], m.gate[0], None, k), 10, 2)
     t_p = ev_time(lambda: ops.permute(r["topk_idx"], E, r["x"]), 10, 2)
-    for g in (0,):
+    import itertools
+    for g in [(pol << 4, gg) for pol in (0, 1, 2, 3) for gg in (0, 4, 16, 128)]:
+        mode, g = g
+        ops.set_gemm_mode(mode)
         t_up = ev_time(lambda: ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g), 5, 2)
         act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g)
         t_dn = ev_time(lambda: ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g), 5, 2)
         fl_up = 2 * T * k * d * 2 * ffn
         fl_dn = 2 * T * k * d * ffn
-        print(f"group={g} router {t_r:.3f} ms permute {t_p:.3f} ms  up {t_up:.3f} ms ({fl_up/t_up/1e9:.0f} TF/s)  down {t_dn:.3f} ms ({fl_dn/t_dn/1e9:.0f} TF/s)", flush=True)
+        print(f"mode={mode} group={g} router {t_r:.3f} ms permute {t_p:.3f} ms  up {t_up:.3f} ms ({fl_up/t_up/1e9:.0f} TF/s)  down {t_dn:.3f} ms ({fl_dn/t_dn/1e9:.0f} TF/s)", flush=True)

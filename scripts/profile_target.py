@@ -7,6 +7,9 @@ from paper_2501_10375_b200.engine import MoEBlockEngine
 from paper_2501_10375_b200.model import MoEModel
 
 what = sys.argv[1] if len(sys.argv) > 1 else "decode"
+import os
+from paper_2501_10375_b200 import ops
+ops.set_gemm_mode(int(os.environ.get("DAOP_GEMM_MODE", "0")))
 d, ffn, E, k = 4096, 14336, 8, 2
 m = MoEModel(P.ModelShape(2, E, k), d, ffn, seed=0, resident_layers=[0])
 eng = MoEBlockEngine(m)
@@ -17,7 +20,8 @@ if what == "decode":
 else:
     T = 32768
     h = m.input_hidden(T, stream=5)
+    g = int(os.environ.get("DAOP_GROUP", "0"))
     for _ in range(2):
-        eng.prefill(h, 0)
+        eng.prefill(h, 0, group_up=g, group_down=g)
 torch.cuda.synchronize()
 print("done", what)

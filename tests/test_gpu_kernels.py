@@ -218,9 +218,14 @@ def _gemm_case(P, d, ffn, E, T, k, seed=0):
     return m, om, h, r, pr, act, y, out
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("d,ffn,E,T", [(256, 512, 8, 64), (512, 1024, 8, 700), (4096, 14336, 8, 256)])
-def test_grouped_gemm_parity(P, d, ffn, E, T):
-    m, om, h, r, pr, act, y, out = _gemm_case(P, d, ffn, E, T, 2)
+def test_grouped_gemm_parity(P, d, ffn, E, T, mode):
+    P[2].set_gemm_mode(mode)
+    try:
+        m, om, h, r, pr, act, y, out = _gemm_case(P, d, ffn, E, T, 2)
+    finally:
+        P[2].set_gemm_mode(0)
     x = bf16_to_f32(r["x"])
     sel = r["topk_idx"].cpu().numpy().astype(np.int64)
     off = pr["offsets"].cpu().numpy()
