@@ -70,14 +70,12 @@ struct DecodeArgs {
   uint16_t* act;           // (k, ffn) bf16 SwiGLU activations
 };
 
-__device__ unsigned long long g_decode_timeline[1024][10];
+__device__ unsigned long long g_decode_timeline[1024][16];
 __device__ int g_decode_timeline_on;
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
+// SM cycle counter (per-SM; phases are compared within one CTA).  %globaltimer
+// was too coarse to resolve the sub-microsecond phase-0 steps.
+__device__ __forceinline__ unsigned long long gtimer() { return clock64(); }
 
 struct Piece {   // what one ring stage holds
   int kind;      // 1 = W1/W3 piece, 2 = W2 piece, 0 = end of stream
@@ -105,10 +103,14 @@ struct DecodeSmem {
   uint8_t fast[DK_MAX];
   int n_exec, nd, drop[DK_MAX], sub[DK_MAX];
   int pred_last;
+  const uint16_t* base[DK_MAX];  // slab slot base of each executed pick
 };
 
 struct Layout {
-  const uint16_t* base[DK_MAX];
+  // slot base per executed pick, in SHARED memory: a register array indexed by
+  // the pick would be demoted to local memory, and with ~225 KB of smem the L1
+  // is nearly gone, so every local access would be an L2 round trip
+  const uint16_t* const* base;
   int n_exec, d, ffn, G, cta;
   int npc1, pe1, npc2, pe2;
   int n1c;         // phase-1 units of this CTA
@@ -154,7 +156,7 @@ __device__ __forceinline__ float warp_softmax(float z, int lane, int E) {
 
 // warp-parallel top-k (E <= 32): max by value, ties to the lower index -- the
 // same order as topk_scan's strict '>' scan
-__device__ __noinline__ void warp_topk(float v, int lane, int E, int k, int* out) {
+__device__ __forceinline__ void warp_topk(float v, int lane, int E, int k, int* out) {
   bool taken = lane >= E;
   for (int j = 0; j < k; ++j) {
     float bv = taken ? -INFINITY : v;
@@ -172,16 +174,16 @@ __device__ __noinline__ void warp_topk(float v, int lane, int E, int k, int* out
   }
 }
 
-__device__ __noinline__ int degrade_smem(const float* s, int E, int* sel, int k,
+__device__ __forceinline__ int degrade_smem(const float* s, int E, int* sel, int k,
                                          const uint8_t* fast, int* drop, int* sub) {
   return degrade(s, E, sel, k, fast, drop, sub);
 }
 
-__device__ __noinline__ void topk_scan_smem(const float* s, int E, int k, int* out) {
+__device__ __forceinline__ void topk_scan_smem(const float* s, int E, int k, int* out) {
   topk_scan(s, E, k, out);
 }
 
-__device__ __noinline__ void softmax_serial(const float* z, int E, float* p) {
+__device__ __forceinline__ void softmax_serial(const float* z, int E, float* p) {
   float m = z[0], sum = 0.f;
   for (int i = 1; i < E; ++i) m = fmaxf(m, z[i]);
   for (int i = 0; i < E; ++i) sum += (p[i] = expf(z[i] - m));
@@ -260,7 +262,10 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
       int ne = 0;
       for (int q = 0; q < k; ++q) {
         s.fast[q] = s.fast_row[s.sel[q]] ? 1 : 0;
-        if (s.fast[q]) s.exec_q[ne++] = q;
+        if (s.fast[q]) {
+          s.base[ne] = a.slab + static_cast<int64_t>(s.slot[s.sel[q]]) * a.slot_stride;
+          s.exec_q[ne++] = q;
+        }
       }
       s.n_exec = ne;
       if (wsrc) {
@@ -335,8 +340,7 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
   };
   auto start_stream = [&]() {
     L.n_exec = s.n_exec;
-    for (int q = 0; q < L.n_exec; ++q)
-      L.base[q] = a.slab + static_cast<int64_t>(s.slot[s.sel[s.exec_q[q]]]) * a.slot_stride;
+    L.base = s.base;
     L.n1c = count_mod(0, L.n_exec * a.ffn, L.cta, L.G);
     L.P2c = L.n_exec * L.R * L.npc2;
     for (int q = 0; q < DS; ++q) issue_next();
@@ -429,12 +433,19 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
       softmax_serial(s.z, E, s.p);
     }
     __syncwarp();
+    if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][10] = gtimer();
     if (a.mode == 0) {
       if (E <= 32) warp_topk(lane < E ? s.p[lane] : 0.f, lane, E, k, s.sel);
       else if (lane == 0) topk_scan_smem(s.p, E, k, s.sel);
+      if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][11] = gtimer();
+      if (tl && E <= 32) {  // probe: the same code a second time (warm I-cache)
+        warp_topk(lane < E ? s.p[lane] : 0.f, lane, E, k, s.drop);
+        if (threadIdx.x == 0) g_decode_timeline[blockIdx.x][12] = gtimer();
+      }
       if (lane == 0) s.nd = 0;
       __syncwarp();
       finish_selection(s.p);
+      if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][13] = gtimer();
     } else if (!a.weights_from_pred) {
       finish_selection(s.p);
     }
@@ -601,10 +612,10 @@ using namespace daop;
 extern "C" int daop_decode_timeline(int32_t enable, uint64_t* h_out, int32_t n_cta) {
   if (h_out && n_cta > 0) {
     DAOP_CUDA(cudaMemcpyFromSymbol(h_out, g_decode_timeline,
-                                   sizeof(unsigned long long) * 10 * (n_cta < 1024 ? n_cta : 1024)));
+                                   sizeof(unsigned long long) * 16 * (n_cta < 1024 ? n_cta : 1024)));
   }
   if (enable) {
-    static unsigned long long zeros[1024][10];
+    static unsigned long long zeros[1024][16];
     DAOP_CUDA(cudaMemcpyToSymbol(g_decode_timeline, zeros, sizeof(zeros)));
   }
   DAOP_CUDA(cudaMemcpyToSymbol(g_decode_timeline_on, &enable, sizeof(int)));

@@ -20,7 +20,7 @@
 
 namespace daop {
 
-constexpr int kRouterWarps = 8;
+constexpr int kRouterWarps = 16;
 constexpr int kMaxGateRows = 32;  // 2E <= 32  (E <= 16)
 
 struct RouterArgs {
@@ -41,15 +41,14 @@ struct RouterArgs {
   int64_t hist_seq_stride;
 };
 
-__device__ __forceinline__ void softmax_row(const float* z, int e, float* p) {
-  float m = z[0];
-  for (int i = 1; i < e; ++i) m = fmaxf(m, z[i]);
-  float s = 0.f;
-  for (int i = 0; i < e; ++i) {
-    p[i] = expf(z[i] - m);
-    s += p[i];
-  }
-  for (int i = 0; i < e; ++i) p[i] = p[i] / s;
+// softmax over E <= 32 logits held one per lane (max-subtracted, fp32)
+static __device__ __forceinline__ float lane_softmax(float z, int lane, int E) {
+  float m = lane < E ? z : -INFINITY;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float e = lane < E ? expf(z - m) : 0.f;
+  const float s = warp_sum(e);
+  return lane < E ? e / s : 0.f;
 }
 
 // GATE_IN_SMEM: gate rows staged in shared memory (they fit for d*2E*2 <= ~200 KB)
@@ -60,6 +59,7 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
   const int d = a.d, E = a.E;
   const int rows = a.wg_next ? 2 * E : E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ float zscratch[kRouterWarps * kMaxGateRows];
   const uint16_t* gate = nullptr;
   if constexpr (GATE_IN_SMEM) {
     uint4* g = reinterpret_cast<uint4*>(smem);
@@ -121,32 +121,53 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
         }
       }
     }
+    // reduce in registers, hand the logits to lane 0 through a per-warp smem
+    // scratch (taking acc's address would demote it to local memory)
+    float* zs = zscratch + warp * kMaxGateRows;
 #pragma unroll
-    for (int q = 0; q < kMaxGateRows; ++q)
-      if (q < rows) acc[q] = warp_sum(acc[q]);
-    if (lane == 0) {
-      float p[kMaxGateRows / 2], ph[kMaxGateRows / 2];
-      softmax_row(acc, E, p);
-      float* pt = a.p_true + t * E;
-      for (int i = 0; i < E; ++i) pt[i] = p[i];
-      if (a.wg_next) {
-        softmax_row(acc + E, E, ph);
-        float* pp = a.p_pred + t * E;
-        for (int i = 0; i < E; ++i) pp[i] = ph[i];
-      }
-      int sel[kMaxGateRows / 2];
-      topk_scan(p, E, a.k, sel);
-      float den = 0.f;
-      for (int j = 0; j < a.k; ++j) den += p[sel[j]];
-      for (int j = 0; j < a.k; ++j) {
-        a.topk_idx[t * a.k + j] = sel[j];
-        a.topk_w[t * a.k + j] = p[sel[j]] / den;
-      }
-      if (a.hist) {
-        int32_t* hrow_hist = a.hist + (t / a.tokens_per_seq) * a.hist_seq_stride;
-        for (int j = 0; j < a.k; ++j) atomicAdd(hrow_hist + sel[j], 1);
+    for (int q = 0; q < kMaxGateRows; ++q) {
+      if (q < rows) {
+        const float z = warp_sum(acc[q]);
+        if (lane == 0) zs[q] = z;
       }
     }
+    __syncwarp();
+    // softmax + top-k + renormalisation, one expert per lane (E <= 16):
+    // top-k by (value desc, index asc) == topk_scan / _kernels.py:63-79
+    const float p = lane_softmax(lane < E ? zs[lane] : 0.f, lane, E);
+    if (lane < E) a.p_true[t * E + lane] = p;
+    if (a.wg_next) {
+      const float ph = lane_softmax(lane < E ? zs[E + lane] : 0.f, lane, E);
+      if (lane < E) a.p_pred[t * E + lane] = ph;
+    }
+    bool taken = lane >= E;
+    int my_sel = -1;
+    float my_p = 0.f, den = 0.f;
+    for (int j = 0; j < a.k; ++j) {
+      float bv = taken ? -INFINITY : p;
+      int bi = taken ? 0x7fffffff : lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      den += bv;  // sum of the picked probabilities in pick order (same on all lanes)
+      if (lane == j) {
+        my_sel = bi;
+        my_p = bv;
+      }
+      if (lane == bi) taken = true;
+    }
+    if (lane < a.k) {
+      a.topk_idx[t * a.k + lane] = my_sel;
+      a.topk_w[t * a.k + lane] = my_p / den;
+      if (a.hist) atomicAdd(a.hist + (t / a.tokens_per_seq) * a.hist_seq_stride + my_sel, 1);
+    }
+    __syncwarp();
   }
 }
 

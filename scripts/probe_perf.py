@@ -27,19 +27,19 @@ if what in ("decode", "all"):
         ops.decode_layer(hs[it[0] % 16], m.norm[0], m.gate[0], m.gate[1], m.fast[0], m.slot_of[0],
                          m.slab, m.slot_elems, d, ffn, k, bufs, variant=var[0])
         it[0] += 1
-    for v in (0, 2):
+    for v in (0,):
         var[0] = v
         ms = ev_time(step, iters=200, warm=10)
         b = 704_774_144
         print(f"decode_layer variant={v}: {ms*1e3:.1f} us  {b/ms/1e6:.1f} GB/s", flush=True)
     from paper_2501_10375_b200 import _lib
-    tlb = np.zeros((148, 10), dtype=np.uint64)
+    tlb = np.zeros((148, 16), dtype=np.uint64)
     _lib.call("daop_decode_timeline", 1, 0, 0)
     torch.cuda.synchronize(); step(); torch.cuda.synchronize()
     _lib.call("daop_decode_timeline", 0, tlb.ctypes.data, 148)
-    t = tlb.astype(np.int64); t0 = t[:, 0].min()
-    rel = (t - t0) / 1000.0
-    for i, nm in enumerate(["start", "sel+issue", "ph1 done", "act ready", "end", "h loaded", "x ready", "gates", "decided", "streamed"]):
+    t = tlb.astype(np.int64)
+    rel = (t - t[:, :1]) / 1.9e3   # SM cycles relative to each CTA's start, ~us at 1.9 GHz
+    for i, nm in enumerate(["start", "sel+issue", "ph1 done", "act ready", "end", "h loaded", "x ready", "gates", "decided", "streamed", "softmax", "topk", "topk again", "finish_sel", "-", "-"]):
         print(f"  {nm:12s} min {rel[:, i].min():7.2f}  med {np.median(rel[:, i]):7.2f}  max {rel[:, i].max():7.2f} us")
 if what in ("prefill", "all"):
     T = 32768
