@@ -69,6 +69,43 @@ class MoEBlockEngine:
         """(h2d, d2h) bytes of one decode_host call."""
         return d * 4, d * 4 + k * 4
 
+    # ------------------------------------------------------------ full decode token
+    def decode_token(self, h: torch.Tensor, *, start: int = 4, daop: bool = True,
+                     weights_from_pred: bool = True) -> torch.Tensor:
+        """One decode token through every layer, all experts HBM-resident:
+        layer l < start (or fiddler) selects by its own gate, layer l >= start
+        by the DAOP plan on the prediction carried by layer l-1 -- known when
+        the launch starts, so its weight stream starts before its router runs.
+        Returns the final residual (a view into a ping-pong buffer)."""
+        m = self.model
+        L = m.shape.num_layers
+        if not hasattr(self, "_pp"):
+            self._pp = [ops.DecodeBuffers(self.d, self.ffn, self.E, self.k, self.device)
+                        for _ in range(2)]
+        cur = h
+        for l in range(L):
+            b = self._pp[l % 2]
+            mode = 1 if (daop and l >= start) else 0
+            nxt = m.gate[l + 1] if l + 1 < L else None
+            ops.decode_layer(cur, m.norm[l], m.gate[l], nxt, m.fast[l], m.slot_of[l], m.slab,
+                             m.slot_elems, self.d, self.ffn, self.k, b,
+                             pred_prev=self._pp[(l + 1) % 2].p_pred if mode else None,
+                             mode=mode, weights_from_pred=weights_from_pred and mode == 1)
+            cur = b.h_out
+        return cur
+
+    def capture_decode_graph(self, *, start: int = 4, daop: bool = True):
+        """Capture decode_token into one CUDA graph (fixed input/output
+        buffers): the L persistent launches replay without host involvement.
+        Returns (graph, h_in, h_out)."""
+        h_in = torch.zeros(self.d, dtype=torch.float32, device=self.device)
+        self.decode_token(h_in, start=start, daop=daop)  # allocate + warm
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.decode_token(h_in, start=start, daop=daop)
+        return g, h_in, out
+
     # ------------------------------------------------------------ prefill
     def prefill(self, h: torch.Tensor, layer: int = 0, *, hist=None, tokens_per_seq: int = 0,
                 hist_seq_stride: int = 0, group_up: int = 0, group_down: int = 0):

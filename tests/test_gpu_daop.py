@@ -91,3 +91,31 @@ def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
         got = rec.decode[t].out.cpu().numpy()
         rms = float(np.sqrt(np.mean(ref.astype(np.float64) ** 2)))
         assert np.abs(got - ref).max() <= 5e-3 * rms + 2e-3 * np.abs(ref).max(), t
+
+
+def test_full_decode_token_and_graph_match_engine():
+    """MoEBlockEngine.decode_token (all layers HBM-resident, DAOP plans from
+    layer `start`) and its CUDA-graph replay == DaopEngine at ECR 1.0, bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.daop import DaopEngine
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    from paper_2501_10375_b200.model import MoEModel
+
+    L, E, k, d, ffn = 6, 8, 2, 256, 512
+    shape = P.ModelShape(L, E, k)
+    m = MoEModel(shape, d, ffn, seed=3)
+    eng = MoEBlockEngine(m)
+    de = DaopEngine(shape, d, ffn, np.full((L, E), k / E), 1.0,
+                    P.PolicyConfig("daop", prediction_start_layer=2), seed=3)
+    g, g_in, g_out = eng.capture_decode_graph(start=2)
+    for t in range(4):
+        h = m.input_hidden(1, stream=21, step=t)[0]
+        a = eng.decode_token(h, start=2).clone()
+        b = de.decode(h).out
+        g_in.copy_(h)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), t
+        assert torch.equal(g_out, a), t
