@@ -438,10 +438,6 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
       if (E <= 32) warp_topk(lane < E ? s.p[lane] : 0.f, lane, E, k, s.sel);
       else if (lane == 0) topk_scan_smem(s.p, E, k, s.sel);
       if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][11] = gtimer();
-      if (tl && E <= 32) {  // probe: the same code a second time (warm I-cache)
-        warp_topk(lane < E ? s.p[lane] : 0.f, lane, E, k, s.drop);
-        if (threadIdx.x == 0) g_decode_timeline[blockIdx.x][12] = gtimer();
-      }
       if (lane == 0) s.nd = 0;
       __syncwarp();
       finish_selection(s.p);
