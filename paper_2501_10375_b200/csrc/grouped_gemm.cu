@@ -49,6 +49,7 @@ struct GemmParams {
   int64_t out_ld;
   int out_cols_per_tile;  // up: 128, down: 256
   int policy;             // L2 hint set (tuning): 0 A last/B normal, 1 both normal, 2 both last, 3 A normal/B last
+  int raster;             // pair kernel tile order: 0 m-groups, 1 n-groups (see map_tile_pair)
 };
 
 struct GemmSmem {
@@ -323,17 +324,30 @@ struct PairSmem {
   int64_t off[G_MAX_EXPERTS + 1];
 };
 
-__device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, int G, int t,
-                                              int& e, int& m, int& n) {
+// raster 0: groups of G m-tiles, m fastest (the wave shares one weight tile
+//           across G m-tiles; the group's activation rows are re-read per n)
+// raster 1: groups of G n-tiles, n fastest (the group's G weight tiles stay
+//           L2-resident while every activation m-tile streams through once)
+__device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, int G,
+                                              int raster, int t, int& e, int& m, int& n) {
   if (t >= s.prefix[E]) return false;
   e = 0;
   while (s.prefix[e + 1] <= t) ++e;
   const int u = t - s.prefix[e];
-  const int grp = u / (G * nt);
-  const int r = u - grp * G * nt;
-  const int gm = min(G, s.mt[e] - grp * G);
-  m = grp * G + r % gm;
-  n = r / gm;
+  if (raster == 0) {
+    const int grp = u / (G * nt);
+    const int r = u - grp * G * nt;
+    const int gm = min(G, s.mt[e] - grp * G);
+    m = grp * G + r % gm;
+    n = r / gm;
+  } else {
+    const int mt = s.mt[e];
+    const int grp = u / (G * mt);
+    const int r = u - grp * G * mt;
+    const int gn = min(G, nt - grp * G);
+    n = grp * G + r % gn;
+    m = r / gn;
+  }
   return true;
 }
 
@@ -393,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int e, m, n;
-      for (int t = cluster; map_tile_pair(s, E, nt, G, t, e, m, n); t += nclusters) {
+      for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
         const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * P_M) + rank * 128;
         const int slot = p.slot_of[e];
         const int brow = n * p.b_tile_rows + (leader ? 0 : p.b_half2);
@@ -417,7 +431,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       int stage = 0, acc = 0, iters = 0;
       uint32_t phase = 0, acc_phase = 0;
       int e, m, n;
-      for (int t = cluster; map_tile_pair(s, E, nt, G, t, e, m, n); t += nclusters) {
+      for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
         mbar_wait(&s.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * GB_N;
@@ -458,7 +472,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int e, m, n;
-    for (int t = cluster; map_tile_pair(s, E, nt, G, t, e, m, n); t += nclusters) {
+    for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
       const int row_in_tile = rank * 128 + q * 32 + lane;
@@ -554,7 +568,13 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
     int clusters = sm_count() / 2;
     if (max_tiles < clusters) clusters = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
     GemmParams pp = p;
-    pp.group_m = p.group_m > 1 ? p.group_m / 2 : 1;  // group counted in 256-row tiles
+    if (p.group_m < 0) {  // negative group = n-grouped raster of |group| weight tiles
+      pp.raster = 1;
+      pp.group_m = -p.group_m;
+    } else {
+      pp.raster = 0;
+      pp.group_m = p.group_m > 1 ? p.group_m / 2 : 1;  // group counted in 256-row tiles
+    }
     grouped_gemm_pair_kernel<SWIGLU><<<2 * clusters, G_THREADS, smem, st>>>(ta, tb, pp);
     DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
     return DAOP_OK;
@@ -566,7 +586,9 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
   const int64_t max_tiles = (rows_total / GB_M + p.E) * static_cast<int64_t>(p.n_tiles);
   int grid = sm_count();
   if (max_tiles < grid) grid = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
-  grouped_gemm_kernel<SWIGLU><<<grid, G_THREADS, smem, st>>>(ta, tb, p);
+  GemmParams q = p;
+  if (q.group_m <= 0) q.group_m = 16;  // the single-CTA kernel only has m-grouped rasters
+  grouped_gemm_kernel<SWIGLU><<<grid, G_THREADS, smem, st>>>(ta, tb, q);
   DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_up" : "grouped_gemm_down");
   return DAOP_OK;
 }
@@ -617,7 +639,7 @@ extern "C" int daop_expert_gemm_up(const uint16_t* x_perm, int64_t rows, int32_t
   const uint32_t bbox[3] = {GB_K, 128, 1};
   if ((rc = make_tmap_bf16(&tb, slab, 3, bdims, bstr, bbox))) return rc;
   GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : 64,
-               128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0};
+               128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0, 0};
   return launch_gemm<true>(ta, tb, p, rows, as_stream(stream));
 }
 
@@ -641,7 +663,9 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
   const uint32_t bbox[3] = {GB_K, 128, 1};
   const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
   if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
-  GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, group_m > 0 ? group_m : 128,
-               GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2};
+  // default: n-grouped raster, 8 weight n-tiles per group (DRAM 20 GB vs 25 GB
+  // for m-groups on 8 x 4096 tokens; profiles/r01/gemm_sweep.txt)
+  GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, group_m != 0 ? group_m : -8,
+               GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0};
   return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
 }
