@@ -36,7 +36,8 @@
 namespace daop {
 
 constexpr int DK_MAX = 8;       // max top-k
-constexpr int DE_MAX = 64;      // max experts
+constexpr int DE_MAX = 16;      // max experts (router logits live on lanes)
+constexpr int DE_FAST = DE_MAX;
 constexpr int kMaxChunks = 16;  // max W2 row pieces
 
 struct DecodeArgs {
@@ -92,7 +93,8 @@ struct DecodeSmem {
   int p1_next, p2_next, fin;
   int done1[DK_MAX];
   float red[DW];
-  float z[DE_MAX];
+  float zpart[DW][DE_MAX];  // per-warp partial gate logits
+  float zpp[DW];            // per-warp partial next-layer logit
   float p[DE_MAX];
   float pp[DE_MAX];
   int slot[DE_MAX];
@@ -144,50 +146,9 @@ __device__ __forceinline__ int count_mod(int lo, int hi, int cta, int G) {
   return hi > f ? (hi - 1 - f) / G + 1 : 0;
 }
 
-// warp-parallel softmax of E <= 32 logits (one per lane)
-__device__ __forceinline__ float warp_softmax(float z, int lane, int E) {
-  float m = lane < E ? z : -INFINITY;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const float e = lane < E ? expf(z - m) : 0.f;
-  const float sum = warp_sum(e);
-  return lane < E ? e / sum : 0.f;
-}
-
-// warp-parallel top-k (E <= 32): max by value, ties to the lower index -- the
-// same order as topk_scan's strict '>' scan
-__device__ __forceinline__ void warp_topk(float v, int lane, int E, int k, int* out) {
-  bool taken = lane >= E;
-  for (int j = 0; j < k; ++j) {
-    float bv = taken ? -INFINITY : v;
-    int bi = taken ? 0x7fffffff : lane;
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (lane == 0) out[j] = bi;
-    if (lane == bi) taken = true;
-  }
-}
-
 __device__ __forceinline__ int degrade_smem(const float* s, int E, int* sel, int k,
                                          const uint8_t* fast, int* drop, int* sub) {
   return degrade(s, E, sel, k, fast, drop, sub);
-}
-
-__device__ __forceinline__ void topk_scan_smem(const float* s, int E, int k, int* out) {
-  topk_scan(s, E, k, out);
-}
-
-__device__ __forceinline__ void softmax_serial(const float* z, int E, float* p) {
-  float m = z[0], sum = 0.f;
-  for (int i = 1; i < E; ++i) m = fmaxf(m, z[i]);
-  for (int i = 0; i < E; ++i) sum += (p[i] = expf(z[i] - m));
-  for (int i = 0; i < E; ++i) p[i] = p[i] / sum;
 }
 
 template <int DW, int DS, int DSB>
@@ -210,7 +171,8 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
 
   // staging of the router inputs in the (still idle) ring area, mode 0 only
   float* h_s = reinterpret_cast<float*>(ring);
-  uint16_t* g_s = reinterpret_cast<uint16_t*>(ring + d * 4);
+  uint16_t* gm_s = reinterpret_cast<uint16_t*>(ring + d * 4);
+  uint16_t* g_s = gm_s + d;
   uint16_t* gp_s = g_s + static_cast<size_t>(E) * d;
 
   if (threadIdx.x == 0) {
@@ -225,10 +187,11 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
     mbar_init(&s.in_bar, 1);
     s.p1_next = s.p2_next = s.fin = 0;
     fence_mbar_init();
-    if (a.mode == 0) {
-      const uint32_t bytes = d * 4 + E * d * 2 + (pred_row ? d * 2 : 0);
+    if (a.mode == 0) {  // h, gamma, the E gate rows, this CTA's next-layer row: one barrier
+      const uint32_t bytes = d * 4 + d * 2 + E * d * 2 + (pred_row ? d * 2 : 0);
       mbar_arrive_expect_tx(&s.in_bar, bytes);
       bulk_g2s_plain(h_s, a.h, d * 4, &s.in_bar);
+      bulk_g2s_plain(gm_s, a.gamma, d * 2, &s.in_bar);
       bulk_g2s_plain(g_s, a.wg, E * d * 2, &s.in_bar);
       if (pred_row)
         bulk_g2s_plain(gp_s, a.wg_next + static_cast<size_t>(blockIdx.x) * d, d * 2, &s.in_bar);
@@ -346,13 +309,43 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
     for (int q = 0; q < DS; ++q) issue_next();
   };
 
+  // ---- lane-parallel softmax / top-k over E <= 16 experts: shuffles span only
+  // the next power of two >= E; ties resolve to the lower id (topk_scan order)
+  int P2 = 1;
+  while (P2 < E) P2 <<= 1;
+  auto lane_softmax = [&](float z) {
+    float m = lane < E ? z : -INFINITY;
+    for (int o = P2 >> 1; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float e = lane < E ? expf(z - m) : 0.f;
+    float sum = e;
+    for (int o = P2 >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    return lane < E ? e / sum : 0.f;
+  };
+  auto lane_topk = [&](float v) {  // -> s.sel[0..k)
+    bool taken = lane >= E;
+    for (int j = 0; j < k; ++j) {
+      float bv = taken ? -INFINITY : v;
+      int bi = taken ? 0x7fffffff : lane;
+      for (int o = P2 >> 1; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      bi = __shfl_sync(0xffffffffu, bi, 0);
+      if (lane == 0) s.sel[j] = bi;
+      if (lane == bi) taken = true;
+    }
+    __syncwarp();
+  };
+
   float ss = 0.f;
   if (a.mode == 1) {
     // ---------------------------------------------------- PLAN: stream first
     if (warp == 0) {
-      if (E <= 32) warp_topk(lane < E ? s.pp[lane] : 0.f, lane, E, k, s.sel);
-      else if (lane == 0) topk_scan_smem(s.pp, E, k, s.sel);
-      __syncwarp();
+      lane_topk(lane < E ? s.pp[lane] : 0.f);
       if (lane == 0) s.nd = a.graceful ? degrade_smem(s.pp, E, s.sel, k, s.fast_row, s.drop, s.sub) : 0;
       __syncwarp();
       finish_selection(a.weights_from_pred ? s.pp : nullptr);
@@ -375,35 +368,79 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
   if (lane == 0) s.red[warp] = ss;
   __syncthreads();
   if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][5] = gtimer();
+  // ---- one fused pass: x = bf16(h * r * gamma) for this warp's slice of d,
+  // and the slice's partial dot products with the E gate rows (+ this CTA's
+  // next-layer gate row); partials are summed over warps in fixed order
+  const bool mode0 = a.mode == 0;
+  const int n16 = d / 8;
   {
     float tot = 0.f;
     for (int w = 0; w < DW; ++w) tot += s.red[w];
     const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + a.eps);
-    const float* hsrc = a.mode == 0 ? h_s : a.h;
-    for (int i = threadIdx.x; i < d / 4; i += NT) {
-      const float4 v = reinterpret_cast<const float4*>(hsrc)[i];
-      const uint2 gw = reinterpret_cast<const uint2*>(a.gamma)[i];
-      const uint32_t b0 = f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.x, r), bf16lo(gw.x)));
-      const uint32_t b1 = f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.y, r), bf16hi(gw.x)));
-      const uint32_t b2 = f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.z, r), bf16lo(gw.y)));
-      const uint32_t b3 = f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.w, r), bf16hi(gw.y)));
-      reinterpret_cast<uint2*>(x_s)[i] = make_uint2(b0 | (b1 << 16), b2 | (b3 << 16));
+    const float4* hsrc = reinterpret_cast<const float4*>(mode0 ? h_s : a.h);
+    const uint4* gmsrc = reinterpret_cast<const uint4*>(mode0 ? gm_s : a.gamma);
+    const uint16_t* gsrc = mode0 ? g_s : a.wg;
+    const uint4* gpsrc = reinterpret_cast<const uint4*>(
+        mode0 ? gp_s : (pred_row ? a.wg_next + static_cast<size_t>(blockIdx.x) * d : a.wg));
+    const int cpw = (n16 + DW - 1) / DW;
+    const int c1 = min(n16, (warp + 1) * cpw);
+    float acc[DE_FAST], accp = 0.f;
+#pragma unroll
+    for (int e = 0; e < DE_FAST; ++e) acc[e] = 0.f;
+    for (int c = warp * cpw + lane; c < c1; c += 32) {
+      const float4 u = hsrc[2 * c], v = hsrc[2 * c + 1];
+      const uint4 gm = gmsrc[c];
+      const uint32_t x0 = static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(u.x, r), bf16lo(gm.x)))) |
+                          (static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(u.y, r), bf16hi(gm.x)))) << 16);
+      const uint32_t x1 = static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(u.z, r), bf16lo(gm.y)))) |
+                          (static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(u.w, r), bf16hi(gm.y)))) << 16);
+      const uint32_t x2 = static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.x, r), bf16lo(gm.z)))) |
+                          (static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.y, r), bf16hi(gm.z)))) << 16);
+      const uint32_t x3 = static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.z, r), bf16lo(gm.w)))) |
+                          (static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.w, r), bf16hi(gm.w)))) << 16);
+      const uint4 x8 = make_uint4(x0, x1, x2, x3);
+      reinterpret_cast<uint4*>(x_s)[c] = x8;
+#pragma unroll
+      for (int e = 0; e < DE_FAST; ++e)
+        if (e < E) acc[e] = dot8(x8, reinterpret_cast<const uint4*>(gsrc + static_cast<size_t>(e) * d)[c], acc[e]);
+      if (pred_row) accp = dot8(x8, gpsrc[c], accp);
+    }
+#pragma unroll
+    for (int e = 0; e < DE_FAST; ++e) {
+      if (e < E) {
+        const float zz = warp_sum(acc[e]);
+        if (lane == 0) s.zpart[warp][e] = zz;
+      }
+    }
+    if (pred_row) {
+      const float zz = warp_sum(accp);
+      if (lane == 0) s.zpp[warp] = zz;
     }
   }
-  __syncthreads();
+  __syncthreads();  // x complete in smem, partial logits visible
   if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][6] = gtimer();
-  const uint4* x4 = reinterpret_cast<const uint4*>(x_s);
-  const int n16 = d / 8;
-  for (int e = warp; e < E; e += DW) {
-    const uint16_t* grow = a.mode == 0 ? g_s + static_cast<size_t>(e) * d
-                                       : a.wg + static_cast<size_t>(e) * d;
-    const float z = warp_sum(dot_piece(reinterpret_cast<const uint4*>(grow), x4, n16, lane, 0.f));
-    if (lane == 0) s.z[e] = z;
+  // ---- every warp: logits (fixed warp order) -> softmax -> selection -> stream
+  {
+    float z = 0.f;
+    if (lane < E)
+      for (int w = 0; w < DW; ++w) z += s.zpart[w][lane];
+    const float p = lane_softmax(z);
+    if (lane < E) s.p[lane] = p;  // identical values from every warp
+    if (mode0) {
+      lane_topk(p);
+      if (lane == 0) s.nd = 0;
+      __syncwarp();
+      finish_selection(s.p);
+      start_stream();
+    } else if (!a.weights_from_pred) {
+      finish_selection(s.p);
+    }
   }
-  if (pred_row && warp == DW - 1) {
-    const uint16_t* grow = a.mode == 0 ? gp_s : a.wg_next + static_cast<size_t>(blockIdx.x) * d;
-    const float zp = warp_sum(dot_piece(reinterpret_cast<const uint4*>(grow), x4, n16, lane, 0.f));
+  if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][8] = gtimer();
+  if (pred_row && warp == DW - 1) {  // this CTA's next-layer row -> grid-wide p_pred
     if (lane == 0) {
+      float zp = 0.f;
+      for (int w = 0; w < DW; ++w) zp += s.zpp[w];
       a.pred_logits[blockIdx.x] = zp;
       __threadfence();
       s.pred_last = atomicAdd(a.ctr + 1, 1u) == static_cast<unsigned>(E) - 1;
@@ -411,42 +448,14 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
     __syncwarp();
     if (s.pred_last) {  // the grid's last next-layer row: softmax -> p_pred
       __threadfence();
-      if (E <= 32) {
-        const float pv = warp_softmax(lane < E ? __ldcg(a.pred_logits + lane) : 0.f, lane, E);
-        if (lane < E) a.p_pred[lane] = pv;
-      } else if (lane == 0) {
-        float m = -INFINITY, sum = 0.f;
-        for (int i = 0; i < E; ++i) m = fmaxf(m, __ldcg(a.pred_logits + i));
-        for (int i = 0; i < E; ++i) sum += expf(__ldcg(a.pred_logits + i) - m);
-        for (int i = 0; i < E; ++i) a.p_pred[i] = expf(__ldcg(a.pred_logits + i) - m) / sum;
-      }
+      const float pv = lane_softmax(lane < E ? __ldcg(a.pred_logits + lane) : 0.f);
+      if (lane < E) a.p_pred[lane] = pv;
       if (lane == 0) a.ctr[1] = 0;
     }
   }
-  __syncthreads();
-  if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][7] = gtimer();
-  if (warp == 0) {
-    if (E <= 32) {
-      const float pv = warp_softmax(lane < E ? s.z[lane] : 0.f, lane, E);
-      if (lane < E) s.p[lane] = pv;
-    } else if (lane == 0) {
-      softmax_serial(s.z, E, s.p);
-    }
-    __syncwarp();
-    if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][10] = gtimer();
-    if (a.mode == 0) {
-      if (E <= 32) warp_topk(lane < E ? s.p[lane] : 0.f, lane, E, k, s.sel);
-      else if (lane == 0) topk_scan_smem(s.p, E, k, s.sel);
-      if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][11] = gtimer();
-      if (lane == 0) s.nd = 0;
-      __syncwarp();
-      finish_selection(s.p);
-      if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][13] = gtimer();
-    } else if (!a.weights_from_pred) {
-      finish_selection(s.p);
-    }
-    if (blockIdx.x == 0) {
-      for (int i = lane; i < E; i += 32) a.p_true[i] = s.p[i];
+  if (blockIdx.x == 0) {
+    if (warp == 0) {
+      if (lane < E) a.p_true[lane] = s.p[lane];
       if (lane < k) {
         a.sel[lane] = s.sel[lane];
         a.w[lane] = s.wsel[lane];
@@ -456,12 +465,10 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
       }
       if (lane == 0) a.deg[2 * k] = s.nd;
     }
+    if (a.x_out)
+      for (int i = threadIdx.x; i < n16; i += NT)
+        reinterpret_cast<uint4*>(a.x_out)[i] = reinterpret_cast<const uint4*>(x_s)[i];
   }
-  __syncthreads();
-  if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][8] = gtimer();
-  if (a.mode == 0) start_stream();
-  if (blockIdx.x == 0 && a.x_out)
-    for (int i = threadIdx.x; i < n16; i += NT) reinterpret_cast<uint4*>(a.x_out)[i] = x4[i];
   if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][1] = gtimer();
 
   // ---------------------------------------------------------------- stream
@@ -570,7 +577,7 @@ static int launch_decode(DecodeArgs a, int grid, cudaStream_t st) {
     return DAOP_ERR_UNSUPPORTED;
   }
   const size_t ring = static_cast<size_t>(DW) * DS * DSB;
-  const size_t stage_in = static_cast<size_t>(a.d) * 4 + static_cast<size_t>(a.E + 1) * a.d * 2;
+  const size_t stage_in = static_cast<size_t>(a.d) * 4 + static_cast<size_t>(a.E + 2) * a.d * 2;
   if (a.mode == 0 && stage_in > ring) {
     set_error("decode_layer: router inputs (%zu B) exceed the ring (%zu B)", stage_in, ring);
     return DAOP_ERR_UNSUPPORTED;
