@@ -191,8 +191,9 @@ int daop_expert_gemm_down(const uint16_t* d_act, int64_t rows, int32_t d, int32_
  * with the slow tier).  d_deg: drop[k] | sub[k] | count.
  * d_workspace: daop_decode_workspace() bytes, zeroed once, self-resetting. */
 /* profiling aid: enable (1) / read back the per-CTA phase timeline of the
- * last decode_layer launches (globaltimer ns: start, selection, phase-1 done,
- * barrier released, end); enabling also clears it. */
+ * last decode_layer launches (SM clock64 cycles: [0] start, [1] phase 0 done,
+ * [2] phase 1 done, [3] act ready, [4] end, [5] rms, [6] x+gates, [8]
+ * selection+first issue); enabling also clears it. */
 int daop_decode_timeline(int32_t enable, uint64_t* h_out, int32_t n_cta);
 int daop_decode_workspace(int32_t d, int32_t ffn, int32_t num_experts, int32_t k,
                           int64_t* h_bytes);
@@ -204,7 +205,19 @@ int daop_decode_layer(const float* d_h, const uint16_t* d_gamma, const uint16_t*
                       int32_t weights_from_pred, float eps, uint16_t* d_x_out, float* d_p_true,
                       float* d_p_pred, int32_t* d_sel, float* d_w, uint8_t* d_is_fast,
                       int32_t* d_deg, float* d_y, float* d_h_out, void* d_workspace,
-                      int32_t grid, daop_stream_t stream);
+                      int32_t variant, daop_stream_t stream);
+/* variant: ring geometry (warps x stages x stage bytes); 0 = default
+ * (8 x 2 x 10 KB), 1..4 = tuning alternatives.  num_experts <= 16. */
+
+/* ------------------------------------------------ trace files (moesim JSONL)
+ * Formats one phase's token records of a RoutingTrace exactly as
+ * moesim/trace.py:328-362 save_trace does ("%.17g" scores, "null" where the
+ * mask is 0, one '\n'-terminated line per token).  true/pred (T, L, E) f64,
+ * mask (T, L) u8, phase 0 = prefill / 1 = decode.  out == NULL: size query
+ * into *written. */
+int daop_trace_format_phase(const double* h_true, const double* h_pred, const uint8_t* h_mask,
+                            int64_t T, int32_t L, int32_t E, int32_t phase, char* h_out,
+                            int64_t cap, int64_t* written);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,8 @@ from .errors import (BudgetError, ConfigError, DeviceError, EmptyPhaseError,
                      PredictionMissingError, ShapeMismatchError,
                      TooShortSequenceError, TraceParseError)
 from .trace import (MIXTRAL_SHAPE, PHI_SHAPE, SCORE_SUM_TOL, ModelShape,
-                    RoutingTrace, TokenRouting, softmax)
+                    RoutingTrace, TokenRouting, load_trace, parse_shape,
+                    save_trace, softmax)
 from . import kernels as _kernels
 from .metrics import (ActivationMatrix, activation_matrix, expert_counts,
                       mean_prediction_accuracy, pooled_decode_probabilities,
@@ -34,7 +35,8 @@ __all__ = [
     "GeneratorTargetError", "MoesimError", "NormalizationError",
     "PredictionMissingError", "ShapeMismatchError", "TooShortSequenceError",
     "TraceParseError", "MIXTRAL_SHAPE", "PHI_SHAPE", "SCORE_SUM_TOL",
-    "ModelShape", "RoutingTrace", "TokenRouting", "softmax", "ActivationMatrix",
+    "ModelShape", "RoutingTrace", "TokenRouting", "softmax", "save_trace",
+    "load_trace", "parse_shape", "ActivationMatrix",
     "activation_matrix", "expert_counts", "mean_prediction_accuracy",
     "pooled_decode_probabilities", "prediction_accuracy", "routing_fidelity",
     "SWAP_IN_OUT_DEFAULT", "ExpertPlacement", "SwapEvent",

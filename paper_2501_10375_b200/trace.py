@@ -10,12 +10,13 @@ compared with the GPU's with ``==``.
 
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
 import numpy as np
 
-from .errors import NormalizationError, ShapeMismatchError
+from .errors import NormalizationError, ShapeMismatchError, TraceParseError
 
 SCORE_SUM_TOL = 1e-6
 PHASES = ("prefill", "decode")
@@ -223,3 +224,171 @@ def softmax(logits: np.ndarray, axis: int = -1) -> np.ndarray:
     z = logits - np.max(logits, axis=axis, keepdims=True)
     ez = np.exp(z)
     return ez / ez.sum(axis=axis, keepdims=True)
+
+
+_PRESETS = {"mixtral": MIXTRAL_SHAPE, "phi": PHI_SHAPE}
+
+
+def parse_shape(text: str) -> ModelShape:
+    """'mixtral' / 'phi' / 'LxExK' (moesim/trace.py:63-77)."""
+    key = text.strip().lower()
+    if key in _PRESETS:
+        return _PRESETS[key]
+    parts = key.split("x")
+    if len(parts) != 3:
+        raise ShapeMismatchError(f"shape must be 'mixtral', 'phi' or 'LxExK', got {text!r}")
+    try:
+        l, e, k = (int(p) for p in parts)
+    except ValueError:
+        raise ShapeMismatchError(f"non-integer component in shape {text!r}") from None
+    return ModelShape(l, e, k)
+
+
+# -- JSON-Lines trace files (moesim/trace.py:325-476) ------------------------
+#
+# The on-disk boundary to the reference's analysis tools: a trace the B200
+# engine exports is byte-identical to what moesim's save_trace would write for
+# the same arrays, so `moesim stats / simulate / sweep` read it unchanged, and
+# load_trace accepts every file moesim writes with moesim's error semantics.
+
+_HEADER_KEYS = {"format_version", "sequence_id", "L", "E", "k", "num_prefill_tokens",
+                "num_decode_tokens"}
+
+
+def save_trace(trace: RoutingTrace, path) -> None:
+    """Write ``trace`` in the canonical JSONL format (moesim/trace.py:332-362).
+    Token records are formatted natively (daop_trace_format_phase, "%.17g")."""
+    import ctypes
+
+    from . import _lib
+
+    s = trace.shape
+    header = {"format_version": 1, "sequence_id": trace.sequence_id, "L": s.num_layers,
+              "E": s.num_experts, "k": s.top_k, "num_prefill_tokens": trace.num_prefill_tokens,
+              "num_decode_tokens": trace.num_decode_tokens}
+    body = []
+    for ph, phase in enumerate(PHASES):
+        true = np.ascontiguousarray(getattr(trace, f"{phase}_true"), dtype=np.float64)
+        pred = np.ascontiguousarray(getattr(trace, f"{phase}_predicted"), dtype=np.float64)
+        mask = np.ascontiguousarray(getattr(trace, f"{phase}_mask"), dtype=np.uint8)
+        n = ctypes.c_int64(0)
+        args = (true.ctypes.data, pred.ctypes.data, mask.ctypes.data, true.shape[0],
+                s.num_layers, s.num_experts, ph)
+        _lib.call("daop_trace_format_phase", *args, None, 0, ctypes.addressof(n))
+        buf = ctypes.create_string_buffer(max(1, n.value))
+        _lib.call("daop_trace_format_phase", *args, buf, n.value, ctypes.addressof(n))
+        body.append(buf.raw[: n.value])
+    with open(path, "wb") as fh:
+        fh.write(json.dumps(header, sort_keys=True).encode("utf-8") + b"\n")
+        for b in body:
+            fh.write(b)
+
+
+def _check_line_scores(vec, path, line_no, token, layer, name) -> None:
+    # moesim/trace.py:465-476
+    if np.any(vec < 0) or not np.all(np.isfinite(vec)):
+        raise NormalizationError(f"{path}: line {line_no}: token {token} layer {layer}: "
+                                 f"{name} has negative or non-finite entries")
+    s = float(vec.sum())
+    if abs(s - 1.0) > SCORE_SUM_TOL:
+        raise NormalizationError(f"{path}: line {line_no}: token {token} layer {layer}: "
+                                 f"{name} sum deviates from 1 by {abs(s - 1.0):.3g}")
+
+
+def _layer_checked(entry, e, path, line_no, idx, li):
+    """The per-layer rules of moesim/trace.py:430-456, in their order."""
+    ts = entry.get("true_scores") if isinstance(entry, dict) else None
+    if not isinstance(ts, list) or len(ts) != e:
+        raise ShapeMismatchError(
+            f"{path}: line {line_no}: token {idx} layer {li}: true_scores length "
+            f"{len(ts) if isinstance(ts, list) else '?'}, expected {e}")
+    vec = np.array(ts, dtype=np.float64)
+    _check_line_scores(vec, path, line_no, idx, li, "true_scores")
+    ps = entry.get("predicted_scores")
+    pvec = None
+    if ps is not None:
+        if not isinstance(ps, list) or len(ps) != e:
+            raise ShapeMismatchError(f"{path}: line {line_no}: token {idx} layer {li}: "
+                                     f"predicted_scores length mismatch, expected {e}")
+        pvec = np.array(ps, dtype=np.float64)
+        _check_line_scores(pvec, path, line_no, idx, li, "predicted_scores")
+    return vec, pvec
+
+
+def load_trace(path) -> RoutingTrace:
+    """Parse and validate a trace file (moesim/trace.py:376-462): same
+    accepted inputs, same error classes and messages.  Each token record is
+    validated as one (L, E) block; the per-layer walk runs only to name the
+    first offending layer."""
+    with open(path, "r", encoding="utf-8") as fh:
+        raw = fh.read().splitlines()
+    if not raw:
+        raise TraceParseError(f"{path}: empty file")
+
+    def parse_line(num, text):
+        try:
+            return json.loads(text)
+        except json.JSONDecodeError as exc:
+            raise TraceParseError(f"{path}: line {num}: {exc}") from None
+
+    header = parse_line(1, raw[0])
+    if not isinstance(header, dict) or not _HEADER_KEYS.issubset(header):
+        raise TraceParseError(f"{path}: line 1: malformed header record")
+    if header["format_version"] != 1:
+        raise TraceParseError(f"{path}: unsupported format_version {header['format_version']!r}")
+    shape = ModelShape(int(header["L"]), int(header["E"]), int(header["k"]))
+    n_prefill, n_decode = int(header["num_prefill_tokens"]), int(header["num_decode_tokens"])
+    body = [ln for ln in raw[1:] if ln.strip()]
+    if len(body) != n_prefill + n_decode:
+        raise TraceParseError(
+            f"{path}: expected {n_prefill + n_decode} token records, found {len(body)}")
+    l, e = shape.num_layers, shape.num_experts
+    arrays = {ph: (np.zeros((n, l, e)), np.zeros((n, l, e)), np.zeros((n, l), dtype=bool))
+              for ph, n in (("prefill", n_prefill), ("decode", n_decode))}
+    counters = {"prefill": 0, "decode": 0}
+    for offset, text in enumerate(body):
+        line_no = offset + 2
+        rec = parse_line(line_no, text)
+        if not isinstance(rec, dict) or "phase" not in rec or "layers" not in rec:
+            raise TraceParseError(f"{path}: line {line_no}: malformed token record")
+        phase = rec["phase"]
+        if phase not in PHASES:
+            raise TraceParseError(f"{path}: line {line_no}: unknown phase {phase!r}")
+        idx = rec.get("token_index")
+        if idx != counters[phase]:
+            raise TraceParseError(
+                f"{path}: line {line_no}: token_index {idx!r} out of order "
+                f"(expected {counters[phase]} for phase {phase})")
+        layers = rec["layers"]
+        if not isinstance(layers, list) or len(layers) != l:
+            raise ShapeMismatchError(
+                f"{path}: line {line_no}: token {idx} ({phase}) has "
+                f"{len(layers) if isinstance(layers, list) else '?'} layers, expected {l}")
+        true, pred, mask = arrays[phase]
+        ok = False
+        try:  # fast path: the whole token as one block
+            ts = np.array([ent["true_scores"] for ent in layers], dtype=np.float64)
+            pm = np.array([ent["predicted_scores"] is not None for ent in layers])
+            ps = np.array([ent["predicted_scores"] if m else [0.0] * e
+                           for ent, m in zip(layers, pm)], dtype=np.float64)
+            if ts.shape == (l, e) and ps.shape == (l, e):
+                good = np.all(ts >= 0) and np.all(np.isfinite(ts)) and np.all(
+                    np.abs(ts.sum(axis=1) - 1.0) <= SCORE_SUM_TOL)
+                pv = ps[pm]
+                good = good and np.all(pv >= 0) and np.all(np.isfinite(pv)) and np.all(
+                    np.abs(pv.sum(axis=1) - 1.0) <= SCORE_SUM_TOL)
+                ok = bool(good)
+        except (TypeError, ValueError, KeyError):
+            ok = False
+        if ok:
+            true[idx], pred[idx], mask[idx] = ts, ps, pm
+        else:  # the reference's sequential walk raises the first error
+            for li, entry in enumerate(layers):
+                vec, pvec = _layer_checked(entry, e, path, line_no, idx, li)
+                true[idx, li] = vec
+                if pvec is not None:
+                    pred[idx, li], mask[idx, li] = pvec, True
+        counters[phase] += 1
+    pt, pp, pm_ = arrays["prefill"]
+    dt, dp, dm = arrays["decode"]
+    return RoutingTrace(shape, header["sequence_id"], pt, dt, pp, pm_, dp, dm)

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--decode", type=int, default=16)
     ap.add_argument("--ecr", type=float, nargs="+", default=[0.75, 0.5, 0.25])
     ap.add_argument("--out", default="")
+    ap.add_argument("--trace-dir", default="", help="save each run's routing trace (moesim JSONL)")
     a = ap.parse_args()
     shape = P.ModelShape(a.layers, 8, 2)
     t0 = time.perf_counter()
@@ -70,6 +71,9 @@ def main():
         torch.cuda.synchronize()
         rec = eng.run_sequence(prompt, toks, f"ecr{ecr}")
         tr = rec.trace
+        if a.trace_dir:
+            Path(a.trace_dir).mkdir(parents=True, exist_ok=True)
+            P.save_trace(tr, Path(a.trace_dir) / f"daop_ecr{ecr}.jsonl")
         n = tr.num_decode_tokens
         runs.append({
             "ecr": ecr,

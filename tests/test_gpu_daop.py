@@ -70,6 +70,11 @@ def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
     assert rec.counts == D.decode_counters(oplans, engine, start)
     # trace is reference-valid: sums to 1 within SCORE_SUM_TOL (checked at construction)
     assert tr.num_decode_tokens == 10 and tr.num_prefill_tokens == 64
+    # ... and survives the moesim JSONL file boundary exactly
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        P.save_trace(tr, f"{td}/t.jsonl")
+        assert P.load_trace(f"{td}/t.jsonl") == tr
 
     # numerics, teacher-forced with the engine's decisions
     om = N.OracleModel(L, E, k, d, ffn, seed=0)
