@@ -48,7 +48,8 @@ struct GemmParams {
   void* out;       // up: bf16 act (rows, out_ld); down: fp32 y (rows, out_ld)
   int64_t out_ld;
   int out_cols_per_tile;  // up: 128, down: 256
-  int policy;             // L2 hint set (tuning): 0 A last/B normal, 1 both normal, 2 both last, 3 A normal/B last
+  int policy;             // L2 hint set (tuning): 0 A last/B normal, 1 both normal, 2 both last, 3 A normal/B last,
+                          // 4 A first/B last, 5 A first/B normal, 6 A last/B first
   int raster;             // pair kernel tile order: 0 m-groups, 1 n-groups (see map_tile_pair)
 };
 
@@ -404,6 +405,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
         pol_a = l2_evict_normal_policy();
         pol_b = l2_evict_last_policy();
       }
+      if (p.policy == 4) {
+        pol_a = l2_evict_first_policy();
+        pol_b = l2_evict_last_policy();
+      }
+      if (p.policy == 5) {
+        pol_a = l2_evict_first_policy();
+        pol_b = l2_evict_normal_policy();
+      }
+      if (p.policy == 6) pol_b = l2_evict_first_policy();
       int stage = 0;
       uint32_t phase = 0;
       int e, m, n;
@@ -609,8 +619,8 @@ static int check_ffn_shape(int64_t rows, int32_t d, int32_t ffn, int32_t E) {
 }
 
 extern "C" int daop_set_gemm_mode(int32_t mode) {
-  // low nibble: kernel (0 CTA pair, 1 single CTA); bits 4..5: L2 hint set (tuning)
-  if ((mode & 15) > 1 || (mode >> 4) > 3) {
+  // low nibble: kernel (0 CTA pair, 1 single CTA); bits 4..6: L2 hint set (tuning)
+  if ((mode & 15) > 1 || (mode >> 4) > 6) {
     set_error("gemm mode must be kernel (0 pair / 1 single) | policy << 4");
     return DAOP_ERR_CONFIG;
   }

@@ -99,29 +99,58 @@ __global__ void perm_gather_kernel(const uint4* __restrict__ x, const int32_t* _
     const int64_t src = perm[r] / k;
     const uint4* s = x + src * n16;
     uint4* d = x_perm + r * n16;
-    for (int c = lane; c < n16; c += 32) d[c] = s[c];
+#pragma unroll 8
+    for (int c = lane; c < n16; c += 32) d[c] = __ldcs(s + c);
   }
 }
 
+// one warp per token row; the k source rows and weights are hoisted, the
+// d-loop is unrolled so each lane keeps (k+1) x 4 independent 16 B loads in
+// flight.  Sum order per element: h, then j = 0..k-1 (fmaf), fixed.
+template <int K>
 __global__ void combine_kernel(const float* __restrict__ h, const float* __restrict__ y,
                                const int32_t* __restrict__ inv, const float* __restrict__ w,
-                               int64_t T, int k, int d4, float* __restrict__ out) {
+                               int64_t T, int k_rt, int d4, float* __restrict__ out) {
   const int lane = threadIdx.x & 31;
+  const int k = K > 0 ? K : k_rt;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
        t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const float4* hr = reinterpret_cast<const float4*>(h) + t * d4;
     float4* o = reinterpret_cast<float4*>(out) + t * d4;
-    for (int c = lane; c < d4; c += 32) {
-      float4 acc = hr[c];
-      for (int j = 0; j < k; ++j) {
-        const float wj = w[t * k + j];
-        const float4 v = reinterpret_cast<const float4*>(y)[static_cast<int64_t>(inv[t * k + j]) * d4 + c];
-        acc.x = fmaf(wj, v.x, acc.x);
-        acc.y = fmaf(wj, v.y, acc.y);
-        acc.z = fmaf(wj, v.z, acc.z);
-        acc.w = fmaf(wj, v.w, acc.w);
+    if constexpr (K > 0) {
+      const float4* yr[K];
+      float wj[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        yr[j] = reinterpret_cast<const float4*>(y) + static_cast<int64_t>(inv[t * K + j]) * d4;
+        wj[j] = w[t * K + j];
       }
-      o[c] = acc;
+#pragma unroll 4
+      for (int c = lane; c < d4; c += 32) {
+        float4 acc = __ldcs(hr + c);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const float4 v = __ldcs(yr[j] + c);
+          acc.x = fmaf(wj[j], v.x, acc.x);
+          acc.y = fmaf(wj[j], v.y, acc.y);
+          acc.z = fmaf(wj[j], v.z, acc.z);
+          acc.w = fmaf(wj[j], v.w, acc.w);
+        }
+        __stcs(o + c, acc);
+      }
+    } else {
+      for (int c = lane; c < d4; c += 32) {
+        float4 acc = hr[c];
+        for (int j = 0; j < k; ++j) {
+          const float wj = w[t * k + j];
+          const float4 v = reinterpret_cast<const float4*>(y)[static_cast<int64_t>(inv[t * k + j]) * d4 + c];
+          acc.x = fmaf(wj, v.x, acc.x);
+          acc.y = fmaf(wj, v.y, acc.y);
+          acc.z = fmaf(wj, v.z, acc.z);
+          acc.w = fmaf(wj, v.w, acc.w);
+        }
+        o[c] = acc;
+      }
     }
   }
 }
@@ -196,8 +225,14 @@ int daop_combine(const float* h, const float* y_sorted, const int32_t* inv, cons
   int64_t blocks = (T * 32 + 255) / 256;
   const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
   if (blocks > cap) blocks = cap;
-  combine_kernel<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(h, y_sorted, inv, w, T, k,
-                                                                          d / 4, out);
+  auto launch = [&](auto kern) {
+    kern<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(h, y_sorted, inv, w, T, k, d / 4,
+                                                                  out);
+  };
+  if (k == 1) launch(combine_kernel<1>);
+  else if (k == 2) launch(combine_kernel<2>);
+  else if (k == 4) launch(combine_kernel<4>);
+  else launch(combine_kernel<0>);
   DAOP_CHECK_LAUNCH("combine");
   return DAOP_OK;
 }

@@ -51,6 +51,16 @@ static __device__ __forceinline__ float lane_softmax(float z, int lane, int E) {
   return lane < E ? e / s : 0.f;
 }
 
+// same, with shuffles limited to the P2 >= E lanes that hold experts
+static __device__ __forceinline__ float lane_softmax_p2(float z, int lane, int E, int P2) {
+  float m = lane < E ? z : -INFINITY;
+  for (int o = P2 >> 1; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float e = lane < E ? expf(z - m) : 0.f;
+  float s = e;
+  for (int o = P2 >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return lane < E ? e / s : 0.f;
+}
+
 // GATE_IN_SMEM: gate rows staged in shared memory (they fit for d*2E*2 <= ~200 KB)
 template <bool GATE_IN_SMEM>
 __global__ void __launch_bounds__(kRouterWarps * 32)
@@ -171,6 +181,201 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core router (2E <= 16 gate rows, d % 256 == 0): the gate logits of
+// 8 tokens are one m16n8k16 MMA chain -- gate rows are the M side (A, bf16
+// from shared memory), the 8 tokens the N side (B, built in registers from
+// this lane's own h values: lane holds token lane/4 at k = 2*(lane%4)+{0,1,8,9}
+// of every 16-wide k-step, exactly the B-fragment layout, so x never touches
+// shared memory).  16 warps split K; per-warp partials are summed in fixed
+// warp order.  Two passes over the 8 rows of h: sum of squares (HBM), then
+// x = bf16(h * r * gamma) + MMA (the rows are still in L2).  The kernel is
+// HBM-bound on the h read + x write (16 + 8 KB per token at d = 4096).
+constexpr int kMmaWarps = 16;
+constexpr int kTokTile = 8;
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_x2(float h0, float h1, float r, uint32_t g2) {
+  const float x0 = __fmul_rn(__fmul_rn(h0, r), bf16lo(g2));
+  const float x1 = __fmul_rn(__fmul_rn(h1, r), bf16hi(g2));
+  return static_cast<uint32_t>(f32_to_bf16_bits(x0)) |
+         (static_cast<uint32_t>(f32_to_bf16_bits(x1)) << 16);
+}
+
+// L2 prefetch of a contiguous byte range (bulk, asynchronous, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)),
+               "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int d = a.d, E = a.E;
+  const int rows = a.wg_next ? 2 * E : E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ld = d + 8;  // padded gate row (bf16): conflict-free fragment loads
+  uint16_t* gs = reinterpret_cast<uint16_t*>(smem);                 // 16 x ld
+  uint16_t* gam = gs + 16 * ld;                                       // d
+  float* sspart = reinterpret_cast<float*>(gam + d);                  // [2][kMmaWarps][8]
+  float* zpart = sspart + 2 * kMmaWarps * kTokTile;                   // [2][kMmaWarps][16][8]
+
+  for (int i = threadIdx.x; i < 16 * (d / 8); i += blockDim.x) {
+    const int r = i / (d / 8), c = i - r * (d / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < E) v = reinterpret_cast<const uint4*>(a.wg + static_cast<size_t>(r) * d)[c];
+    else if (r < rows) v = reinterpret_cast<const uint4*>(a.wg_next + static_cast<size_t>(r - E) * d)[c];
+    *reinterpret_cast<uint4*>(gs + static_cast<size_t>(r) * ld + c * 8) = v;
+  }
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x)
+    reinterpret_cast<uint4*>(gam)[i] = reinterpret_cast<const uint4*>(a.gamma)[i];
+  __syncthreads();
+
+  const int g = lane >> 2, c2 = (lane & 3) * 2;  // fragment row / column pair
+  int P2 = 1;
+  while (P2 < E) P2 <<= 1;
+  const int ksteps = d / (16 * kMmaWarps);
+  const int k0w = warp * ksteps * 16;
+  const int64_t ntiles = (a.T + kTokTile - 1) / kTokTile;
+  // keep the h rows of the next PF tiles streaming into L2 (both passes then
+  // read L2; the HBM stream runs ahead of the compute)
+  constexpr int PF = 2;
+  auto prefetch_tile = [&](int64_t tl) {
+    if (tl >= ntiles) return;
+    const int64_t t0 = tl * kTokTile;
+    const int64_t n = (a.T - t0 < kTokTile ? a.T - t0 : kTokTile);
+    for (int64_t q = 0; q < n; ++q) bulk_prefetch_l2(a.h + (t0 + q) * d, d * 4);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < PF; ++i) prefetch_tile(blockIdx.x + static_cast<int64_t>(i) * gridDim.x);
+  int buf = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+    if (threadIdx.x == 0) prefetch_tile(tile + static_cast<int64_t>(PF) * gridDim.x);
+    const int64_t t = tile * kTokTile + g;  // this lane's token
+    const bool live = t < a.T;
+    const float* hrow = a.h + (live ? t : 0) * d;
+    // pass 1: partial sum of squares over this warp's K-slice
+    float ss = 0.f;
+    if (live) {
+#pragma unroll 16
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const int k = k0w + ks * 16 + c2;
+        const float2 u = __ldg(reinterpret_cast<const float2*>(hrow + k));
+        const float2 v = __ldg(reinterpret_cast<const float2*>(hrow + k + 8));
+        ss = fmaf(u.x, u.x, ss); ss = fmaf(u.y, u.y, ss);
+        ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss);
+      }
+    }
+    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+    float* ssb = sspart + buf * kMmaWarps * kTokTile;
+    if ((lane & 3) == 0) ssb[warp * kTokTile + g] = ss;
+    __syncthreads();
+    float tot = 0.f;
+    for (int w = 0; w < kMmaWarps; ++w) tot += ssb[w * kTokTile + g];
+    const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + a.eps);
+    // pass 2: x fragments, x store, MMA against the gate rows
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint16_t* xrow = a.x_out ? a.x_out + (live ? t : 0) * d : nullptr;
+    // batches of 8 k-steps: all h loads of a batch are issued before the x
+    // stores (which the compiler cannot prove do not alias h)
+    for (int ks0 = 0; ks0 < ksteps; ks0 += 8) {
+      float2 u[8], v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        u[i] = make_float2(0.f, 0.f);
+        v[i] = make_float2(0.f, 0.f);
+        if (live && ks0 + i < ksteps) {
+          const int k = k0w + (ks0 + i) * 16 + c2;
+          u[i] = __ldg(reinterpret_cast<const float2*>(hrow + k));
+          v[i] = __ldg(reinterpret_cast<const float2*>(hrow + k + 8));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (ks0 + i < ksteps) {
+          const int k = k0w + (ks0 + i) * 16 + c2;
+          const uint32_t b0 = pack_x2(u[i].x, u[i].y, r, *reinterpret_cast<const uint32_t*>(gam + k));
+          const uint32_t b1 =
+              pack_x2(v[i].x, v[i].y, r, *reinterpret_cast<const uint32_t*>(gam + k + 8));
+          if (live && xrow) {
+            *reinterpret_cast<uint32_t*>(xrow + k) = b0;
+            *reinterpret_cast<uint32_t*>(xrow + k + 8) = b1;
+          }
+          uint32_t af[4];
+          af[0] = *reinterpret_cast<const uint32_t*>(gs + g * ld + k);
+          af[1] = *reinterpret_cast<const uint32_t*>(gs + (g + 8) * ld + k);
+          af[2] = *reinterpret_cast<const uint32_t*>(gs + g * ld + k + 8);
+          af[3] = *reinterpret_cast<const uint32_t*>(gs + (g + 8) * ld + k + 8);
+          mma_bf16_16816(acc, af, b0, b1);
+        }
+      }
+    }
+    // D fragment: gate rows g, g+8 x tokens c2, c2+1
+    float* zb = zpart + buf * kMmaWarps * 16 * kTokTile + warp * 16 * kTokTile;
+    zb[g * kTokTile + c2] = acc[0];
+    zb[g * kTokTile + c2 + 1] = acc[1];
+    zb[(g + 8) * kTokTile + c2] = acc[2];
+    zb[(g + 8) * kTokTile + c2 + 1] = acc[3];
+    __syncthreads();
+    // token phase: warp w < 8 finishes token w of the tile (one expert per lane)
+    if (warp < kTokTile) {
+      const int64_t tt = tile * kTokTile + warp;
+      if (tt < a.T) {
+        const float* z0 = zpart + buf * kMmaWarps * 16 * kTokTile;
+        float zt = 0.f, zp = 0.f;
+        if (lane < E) {
+          for (int w = 0; w < kMmaWarps; ++w) {
+            zt += z0[(w * 16 + lane) * kTokTile + warp];
+            if (a.wg_next) zp += z0[(w * 16 + E + lane) * kTokTile + warp];
+          }
+        }
+        const float p = lane_softmax_p2(zt, lane, E, P2);
+        if (lane < E) a.p_true[tt * E + lane] = p;
+        if (a.wg_next) {
+          const float ph = lane_softmax_p2(zp, lane, E, P2);
+          if (lane < E) a.p_pred[tt * E + lane] = ph;
+        }
+        bool taken = lane >= E;
+        int my_sel = -1;
+        float my_p = 0.f, den = 0.f;
+        for (int j = 0; j < a.k; ++j) {
+          float bv = taken ? -INFINITY : p;
+          int bi = taken ? 0x7fffffff : lane;
+#pragma unroll
+          for (int o = P2 >> 1; o > 0; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+              bv = ov;
+              bi = oi;
+            }
+          }
+          den += bv;
+          if (lane == j) {
+            my_sel = bi;
+            my_p = bv;
+          }
+          if (lane == bi) taken = true;
+        }
+        if (lane < a.k) {
+          a.topk_idx[tt * a.k + lane] = my_sel;
+          a.topk_w[tt * a.k + lane] = my_p / den;
+          if (a.hist) atomicAdd(a.hist + (tt / a.tokens_per_seq) * a.hist_seq_stride + my_sel, 1);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace daop
 
 using namespace daop;
@@ -193,6 +398,17 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
   RouterArgs a{h, gamma, wg, wg_next, T, d, E, k, eps, x_out, p_true, p_pred,
                topk_idx, topk_w, hist, tokens_per_seq, hist_seq_stride};
   const int rows = wg_next ? 2 * E : E;
+  const size_t smem_mma = static_cast<size_t>(16) * (d + 8) * 2 + static_cast<size_t>(d) * 2 +
+                          2 * kMmaWarps * kTokTile * 4 + 2 * kMmaWarps * 16 * kTokTile * 4;
+  if (rows <= 16 && d % (16 * kMmaWarps) == 0 && smem_mma <= 220 * 1024) {
+    const int64_t ntiles = (T + kTokTile - 1) / kTokTile;
+    const int blocks = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
+    DAOP_CUDA(cudaFuncSetAttribute(router_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem_mma)));
+    router_mma_kernel<<<blocks, kMmaWarps * 32, smem_mma, as_stream(st)>>>(a);
+    DAOP_CHECK_LAUNCH("router");
+    return DAOP_OK;
+  }
   const size_t smem = static_cast<size_t>(rows) * d * 2;
   int64_t blocks = (T + kRouterWarps - 1) / kRouterWarps;
   const int64_t cap = static_cast<int64_t>(sm_count()) * 2;

@@ -52,15 +52,41 @@ class MoEBlockEngine:
                                 weights_from_pred=weights_from_pred, variant=variant)
 
     def decode_host(self, h_host: torch.Tensor, layer: int = 0):
-        """End-to-end call from host memory: pinned h (d,) -> device -> decode
-        -> (h_out, selected experts) back in pinned host memory."""
+        """End-to-end call from host memory: h (d,) fp32 on the host -> device
+        -> decode -> (h_out, selected experts) back in pinned host memory.
+
+        The step is one CUDA graph per layer (captured on first use): H2D copy
+        from a pinned staging buffer, the decode launch, D2H copies of the
+        residual and the selection.  The caller's h is copied into the staging
+        buffer on the host, so any host tensor works; the residual and the
+        selection come back in one D2H copy; one replay + one
+        synchronize per call keeps the host overhead at a few microseconds."""
         if self._out_host is None:
-            self._out_host = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
-            self._sel_host = torch.empty(self.k, dtype=torch.int32, pin_memory=True)
-        self._h_dev.copy_(h_host, non_blocking=True)
-        self.decode(self._h_dev, layer)
-        self._out_host.copy_(self.bufs.h_out, non_blocking=True)
-        self._sel_host.copy_(self.bufs.sel, non_blocking=True)
+            self._h_host = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
+            self._io_host = torch.empty(self.d + self.k, dtype=torch.float32, pin_memory=True)
+            self._out_host = self._io_host[: self.d]
+            self._sel_host = self._io_host[self.d:].view(torch.int32)
+            self._host_graphs = {}
+        g = self._host_graphs.get(layer)
+        if g is None:
+            def step():
+                self._h_dev.copy_(self._h_host, non_blocking=True)
+                self.decode(self._h_dev, layer)
+                self._io_host.copy_(self.bufs.out_io, non_blocking=True)
+
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step()  # warm-up outside capture
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            self._host_graphs[layer] = g
+        if h_host.data_ptr() != self._h_host.data_ptr():
+            self._h_host.copy_(h_host)
+        g.replay()
         torch.cuda.current_stream().synchronize()
         return self._out_host, self._sel_host
 

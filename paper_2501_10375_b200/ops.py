@@ -141,12 +141,14 @@ class DecodeBuffers:
         self.x = torch.empty(d, dtype=torch.bfloat16, device=device)
         self.p = torch.empty(num_experts, **f32)
         self.p_pred = torch.empty(num_experts, **f32)
-        self.sel = torch.empty(k, dtype=torch.int32, device=device)
+        # residual out and selection side by side: one D2H copy returns both
+        self.out_io = torch.empty(d + k, **f32)
+        self.h_out = self.out_io[:d]
+        self.sel = self.out_io[d:].view(torch.int32)
         self.w = torch.empty(k, **f32)
         self.is_fast = torch.empty(k, dtype=torch.uint8, device=device)
         self.deg = torch.empty(2 * k + 1, dtype=torch.int32, device=device)
         self.y = torch.zeros((k, d), **f32)
-        self.h_out = torch.empty(d, **f32)
 
 
 def decode_layer(h, gamma, wg, wg_next, fast_row, slot_of, slab, slot_elems, d, ffn, k,

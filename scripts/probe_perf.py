@@ -42,21 +42,23 @@ if what in ("decode", "all"):
     for i, nm in enumerate(["start", "sel+issue", "ph1 done", "act ready", "end", "h loaded", "x ready", "gates", "decided", "streamed", "softmax", "topk", "topk again", "finish_sel", "-", "-"]):
         print(f"  {nm:12s} min {rel[:, i].min():7.2f}  med {np.median(rel[:, i]):7.2f}  max {rel[:, i].max():7.2f} us")
 if what in ("prefill", "all"):
+    from paper_2501_10375_b200.engine import MoEBlockEngine
     T = 32768
-    m = M.MoEModel(P.ModelShape(1, E, k), d, ffn, seed=0)
+    m = M.MoEModel(P.ModelShape(2, E, k), d, ffn, seed=0, resident_layers=[0])
+    eng = MoEBlockEngine(m)
     h = m.input_hidden(T, stream=5)
-    r = ops.router(h, m.norm[0], m.gate[0], None, k)
+    r = ops.router(h, m.norm[0], m.gate[0], m.gate[1], k)
     pr = ops.permute(r["topk_idx"], E, r["x"])
-    so = m.slot_of[0].contiguous()
-    t_r = ev_time(lambda: ops.router(h, m.norm[0], m.gate[0], None, k), 10, 2)
-    t_p = ev_time(lambda: ops.permute(r["topk_idx"], E, r["x"]), 10, 2)
-    import itertools
-    for g in [(pol << 4, gg) for pol in (0, 1, 2, 3) for gg in (0, 4, 16, 128)]:
-        mode, g = g
-        ops.set_gemm_mode(mode)
-        t_up = ev_time(lambda: ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g), 5, 2)
-        act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g)
-        t_dn = ev_time(lambda: ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn, g), 5, 2)
-        fl_up = 2 * T * k * d * 2 * ffn
-        fl_dn = 2 * T * k * d * ffn
-        print(f"mode={mode} group={g} router {t_r:.3f} ms permute {t_p:.3f} ms  up {t_up:.3f} ms ({fl_up/t_up/1e9:.0f} TF/s)  down {t_dn:.3f} ms ({fl_dn/t_dn/1e9:.0f} TF/s)", flush=True)
+    so = m.slot_of[0]
+    act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn)
+    y = ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn)
+    st = {
+        "router": lambda: ops.router(h, m.norm[0], m.gate[0], m.gate[1], k),
+        "permute+gather": lambda: ops.permute(r["topk_idx"], E, r["x"]),
+        "gemm up": lambda: ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn),
+        "gemm down": lambda: ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn),
+        "combine": lambda: ops.combine(h, y, pr["inv"], r["topk_w"]),
+        "prefill layer": lambda: eng.prefill(h, 0),
+    }
+    for name, fn in st.items():
+        print(f"{name:16s} {ev_time(fn, 10, 3):8.3f} ms", flush=True)

@@ -124,3 +124,27 @@ def test_full_decode_token_and_graph_match_engine():
         torch.cuda.synchronize()
         assert torch.equal(a, b), t
         assert torch.equal(g_out, a), t
+
+
+def test_decode_host_graph_matches_device_decode():
+    """The end-to-end host API (graph: H2D, decode launch, D2H) returns the
+    same residual and selection as the device call, for any host tensor."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    from paper_2501_10375_b200.model import MoEModel
+
+    L, E, k, d, ffn = 2, 8, 2, 256, 512
+    m = MoEModel(P.ModelShape(L, E, k), d, ffn, seed=4)
+    eng = MoEBlockEngine(m)
+    for t in range(4):
+        for layer in (0, 1):
+            h = m.input_hidden(1, stream=31, step=t)[0]
+            h_host = h.cpu()  # pageable on purpose: staged into the pinned buffer
+            out, sel = eng.decode_host(h_host, layer)
+            out, sel = out.clone(), sel.clone()
+            eng.decode(h, layer)
+            torch.cuda.synchronize()
+            assert torch.equal(out, eng.bufs.h_out.cpu()), (t, layer)
+            assert torch.equal(sel, eng.bufs.sel.cpu()), (t, layer)
