@@ -39,7 +39,9 @@ typedef void* daop_stream_t; /* cudaStream_t */
 #define DAOP_ERR_CUDA (-100)             /* CUDA runtime failure (no reference analogue) */
 #define DAOP_ERR_UNSUPPORTED (-101)      /* shape outside the kernel envelope */
 
-#define DAOP_ENGINE_FIDDLER 2 /* policies.py:32 ENGINES index */
+#define DAOP_ENGINE_ONDEMAND 0 /* policies.py:32 ENGINES index */
+#define DAOP_ENGINE_PREFETCH 1
+#define DAOP_ENGINE_FIDDLER 2
 #define DAOP_ENGINE_DAOP 3
 
 /* ------------------------------------------------------------------ library */
@@ -93,6 +95,24 @@ int daop_plan_token_f64(const double* h_true, const double* h_pred, const uint8_
                         int32_t k, int32_t start_layer, int32_t engine, int32_t graceful,
                         int32_t* h_sel, uint8_t* h_is_fast, int32_t* h_drop, int32_t* h_sub,
                         int32_t* h_n_deg);
+
+/* replaces one layer of {OnDemand,Prefetch}Planner.plan_token
+ * (policies.py:103-245): per-layer LRU caches seeded from the placement.
+ * The caller owns the cache state: h_last_use (L,E) int64 recency (-1 = not
+ * cached; seed members with 0), h_capacity (L) = seeded set sizes, *h_step
+ * the global step (ticked once per call).  Call for l = 0..L-1 per token.
+ * h_true_row (E): layer l's true scores; h_pred_row (E) or NULL: the
+ * prediction carried on layer l (prefetch engine, l+1 >= start).
+ * Outputs: h_sel (k) = top-k (all executed on the fast tier); demand
+ * migrations h_mig (k) sorted, with the expert each one evicted in
+ * h_mig_evict (-1: a free slot); prefetches for layer l+1 h_pf / h_pf_evict.
+ * DAOP_ERR_PREDICTION_MISSING after this layer's demand updates (as the
+ * reference). */
+int daop_lru_plan_layer(int32_t layer, int32_t num_layers, int32_t num_experts, int32_t k,
+                        int32_t engine, int32_t start_layer, const double* h_true_row,
+                        const double* h_pred_row, int64_t* h_last_use, const int32_t* h_capacity,
+                        int64_t* h_step, int32_t* h_sel, int32_t* h_mig, int32_t* h_mig_evict,
+                        int32_t* h_n_mig, int32_t* h_pf, int32_t* h_pf_evict, int32_t* h_n_pf);
 
 /* ------------------------------------------------ device decision kernel
  * The same plan as daop_plan_token_f64, on the router's exported float32

@@ -224,15 +224,75 @@ def plan_token(true_le, pred_le, pred_mask, sets, k, engine="daop", start=4,
     return plans
 
 
+class LruCaches:
+    """policies.py:103-140 (_LayerCache / CacheState): one LRU cache per layer
+    seeded with the placement's set (identical recency 0, capacity = size);
+    one global step counter, ticked once per (token, layer)."""
+
+    def __init__(self, sets):
+        self.last_use = [{int(e): 0 for e in sorted(s)} for s in sets]
+        self.capacity = [len(s) for s in sets]
+        self.step = 0
+
+    def insert(self, l, e, step):
+        """policies.py:120-127: evict the least recently used (ties -> lower id)."""
+        lu = self.last_use[l]
+        if e not in lu and len(lu) >= self.capacity[l]:
+            if not lu:
+                raise OracleError("ConfigError", f"layer {l} cache has no capacity")
+            ev = min(lu, key=lambda x: (lu[x], x))
+            del lu[ev]
+        lu[e] = step
+
+
+def plan_token_lru(true_le, pred_le, pred_mask, caches: LruCaches, k, engine, start=4):
+    """policies.py:173-194 (OnDemandPlanner) and :197-245 (PrefetchPlanner).
+
+    Mutates ``caches`` like the reference planner (state persists across
+    tokens; a PredictionMissingError leaves the updates already made)."""
+    l_count = true_le.shape[0]
+    top = topk_rows(true_le, k)
+    plans = []
+    for l in range(l_count):
+        caches.step += 1
+        step = caches.step
+        lu = caches.last_use[l]
+        need = [int(e) for e in top[l]]
+        absent = sorted(e for e in need if e not in lu)
+        for e in need:
+            if e in lu:
+                lu[e] = step
+        for e in absent:
+            caches.insert(l, e, step)
+        issues = []
+        if engine == "prefetch" and l + 1 < l_count and l + 1 >= start:
+            if not pred_mask[l]:
+                raise OracleError("PredictionMissingError", f"layer {l}")
+            pred_top = [int(x) for x in topk_rows(pred_le[l][None, :], k)[0]]
+            nlu = caches.last_use[l + 1]
+            issues = sorted(e for e in pred_top if e not in nlu)
+            for e in issues:
+                caches.insert(l + 1, e, step)
+        plans.append({"executed": [(e, "fast", "current", False) for e in need],
+                      "migrations": absent, "prefetch_issues": issues, "degraded": []})
+    return plans
+
+
 def decode_counters(plans_per_token, engine="daop", start=4):
-    """simulator.py:308-389 counter semantics for fiddler/daop (no migrations):
-    slow_executions = current slow picks + precalc picks; stale_inputs =
-    precalc picks; degradations = len(plan.degraded)."""
+    """simulator.py:297-389 counter semantics: slow_executions = current slow
+    picks + precalc picks; stale_inputs = precalc picks; degradations =
+    len(plan.degraded); migrations = demand migrations; prefetches = early
+    migrations, wasted when the expert is not executed at layer l+1."""
     c = {"migrations": 0, "prefetches": 0, "wasted_prefetches": 0,
          "slow_executions": 0, "degradations": 0, "stale_inputs": 0}
     for plans in plans_per_token:
         l_count = len(plans)
         for l, p in enumerate(plans):
+            c["migrations"] += len(p.get("migrations", ()))
+            for e in p.get("prefetch_issues", ()):
+                c["prefetches"] += 1
+                if e not in [x[0] for x in plans[l + 1]["executed"]]:
+                    c["wasted_prefetches"] += 1
             cur_slow = [x for x in p["executed"] if x[1] == "slow" and not x[3]]
             c["slow_executions"] += len(cur_slow)
             # precalc for l+1 is dispatched at layer l when its pred-gate runs

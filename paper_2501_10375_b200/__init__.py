@@ -24,9 +24,10 @@ from .placement import (SWAP_IN_OUT_DEFAULT, ExpertPlacement, SwapEvent,
                         slot_budget_for_ecr)
 from .policies import (ENGINES, PREDICTION_START_LAYER_DEFAULT, DaopPlanner,
                        Degradation, ExecutedExpert, FiddlerPlanner, LayerPlan,
-                       PolicyConfig, decode_counters, degrade_selection,
-                       make_planner, plan_token_daop, plan_token_fiddler,
-                       plan_trace_decode)
+                       OnDemandPlanner, PolicyConfig, PrefetchPlanner,
+                       decode_counters, degrade_selection, make_planner,
+                       plan_token_daop, plan_token_fiddler, plan_token_ondemand,
+                       plan_token_prefetch, plan_trace_decode)
 
 __version__ = "0.1.0"
 
@@ -44,5 +45,6 @@ __all__ = [
     "ENGINES", "PREDICTION_START_LAYER_DEFAULT", "DaopPlanner", "Degradation",
     "ExecutedExpert", "FiddlerPlanner", "LayerPlan", "PolicyConfig",
     "decode_counters", "degrade_selection", "make_planner", "plan_token_daop",
-    "plan_token_fiddler", "plan_trace_decode",
+    "plan_token_fiddler", "plan_trace_decode", "OnDemandPlanner", "PrefetchPlanner",
+    "plan_token_ondemand", "plan_token_prefetch",
 ]

@@ -216,6 +216,85 @@ int daop_plan_token_f64(const double* tr, const double* pr, const uint8_t* pmask
   return DAOP_OK;
 }
 
+// policies.py:120-127 _LayerCache.insert on row lu (E entries, -1 = absent)
+static int lru_insert(int64_t* lu, int E, int cap, int e, int64_t step, int* evicted) {
+  *evicted = -1;
+  if (lu[e] < 0) {
+    int members = 0;
+    for (int c = 0; c < E; ++c) members += lu[c] >= 0;
+    if (members >= cap) {
+      int ev = -1;
+      for (int c = 0; c < E; ++c)  // min (last_use, id)
+        if (lu[c] >= 0 && (ev < 0 || lu[c] < lu[ev])) ev = c;
+      if (ev < 0) return -1;  // capacity 0
+      lu[ev] = -1;
+      *evicted = ev;
+    }
+  }
+  lu[e] = step;
+  return 0;
+}
+
+int daop_lru_plan_layer(int32_t l, int32_t L, int32_t E, int32_t k, int32_t engine, int32_t start,
+                        const double* tr, const double* pr, int64_t* last_use,
+                        const int32_t* capacity, int64_t* step, int32_t* sel, int32_t* mig,
+                        int32_t* mig_ev, int32_t* n_mig, int32_t* pf, int32_t* pf_ev,
+                        int32_t* n_pf) {
+  if (k < 1 || k > E || l < 0 || l >= L) {
+    set_error("lru_plan_layer: bad shape (layer %d of %d, E=%d, k=%d)", l, L, E, k);
+    return DAOP_ERR_SHAPE;
+  }
+  if (engine != DAOP_ENGINE_ONDEMAND && engine != DAOP_ENGINE_PREFETCH) {
+    set_error("engine %d has no LRU planner", engine);
+    return DAOP_ERR_CONFIG;
+  }
+  const int64_t st = ++*step;
+  int64_t* lu = last_use + static_cast<size_t>(l) * E;
+  int need[64];
+  if (k > 64) {
+    set_error("lru_plan_layer: k=%d > 64", k);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  topk_scan(tr, E, k, need);
+  for (int q = 0; q < k; ++q) sel[q] = need[q];
+  // absent = sorted(need not cached); touch the cached ones (policies.py:181-186)
+  int nm = 0;
+  for (int e = 0; e < E; ++e)
+    for (int q = 0; q < k; ++q)
+      if (need[q] == e && lu[e] < 0) mig[nm++] = e;
+  for (int q = 0; q < k; ++q)
+    if (lu[need[q]] >= 0) lu[need[q]] = st;
+  for (int i = 0; i < nm; ++i) {
+    if (lru_insert(lu, E, capacity[l], mig[i], st, &mig_ev[i]) < 0) {
+      set_error("layer %d cache has no capacity", l);
+      return DAOP_ERR_CONFIG;
+    }
+  }
+  *n_mig = nm;
+  *n_pf = 0;
+  if (engine == DAOP_ENGINE_PREFETCH && l + 1 < L && l + 1 >= start) {  // :223-236
+    if (!pr) {
+      set_error("layer %d record carries no prediction for layer %d", l, l + 1);
+      return DAOP_ERR_PREDICTION_MISSING;
+    }
+    int ptop[64];
+    topk_scan(pr, E, k, ptop);
+    int64_t* nlu = last_use + static_cast<size_t>(l + 1) * E;
+    int np = 0;
+    for (int e = 0; e < E; ++e)
+      for (int q = 0; q < k; ++q)
+        if (ptop[q] == e && nlu[e] < 0) pf[np++] = e;
+    for (int i = 0; i < np; ++i) {
+      if (lru_insert(nlu, E, capacity[l + 1], pf[i], st, &pf_ev[i]) < 0) {
+        set_error("layer %d cache has no capacity", l + 1);
+        return DAOP_ERR_CONFIG;
+      }
+    }
+    *n_pf = np;
+  }
+  return DAOP_OK;
+}
+
 int daop_fill_uniform_bf16_host(uint16_t* dst, int64_t n, uint64_t seed, uint64_t tag, float scale,
                                 int64_t off, int32_t threads) {
   const uint64_t key = stream_key(seed, tag);

@@ -51,7 +51,8 @@ from .errors import ConfigError, ShapeMismatchError
 from .model import KIND_EXPERT, MoEModel, make_tag
 from .placement import (SWAP_IN_OUT_DEFAULT, ExpertPlacement, SwapEvent,
                         allocate_for_sequence, init_from_calibration)
-from .policies import PolicyConfig, decode_counters, plans_from_arrays
+from .policies import (ExecutedExpert, LayerPlan, PolicyConfig, decode_counters, make_planner,
+                       plans_from_arrays)
 from .trace import ModelShape, RoutingTrace
 
 
@@ -135,8 +136,6 @@ class DaopEngine:
                  swap_in_out: float = SWAP_IN_OUT_DEFAULT, weights_from_pred: bool = True,
                  host_pool: HostExpertPool | None = None, host_threads: int = 0):
         self.config = config or PolicyConfig("daop")
-        if self.config.engine not in ("daop", "fiddler"):
-            raise ConfigError(f"engine {self.config.engine!r} is outside the DAOP hot path")
         self.shape = shape
         self.placement0 = init_from_calibration(calib, ecr, shape)
         self.swap_in_out = swap_in_out
@@ -155,6 +154,7 @@ class DaopEngine:
         self.migrations_done = 0
         E, k = shape.num_experts, shape.top_k
         self.bufs = [ops.DecodeBuffers(d_model, d_ff, E, k, self.model.device) for _ in range(2)]
+        self._lru = None  # LRU planner of the ondemand / prefetch engines (after prefill)
 
     # ------------------------------------------------------------ residency
     def _migrate_in(self, layer: int, expert: int, slot: int):
@@ -197,16 +197,18 @@ class DaopEngine:
             nxt = m.gate[l + 1] if l + 1 < L else None
             r = ops.router(h, m.norm[l], m.gate[l], nxt, k, hist=hist[:, l], tokens_per_seq=T,
                            hist_seq_stride=L * E)
-            counts_l = hist[0, l].to(torch.int64).cpu().numpy()
-            # Alg. 1 for this layer right after its gate (placement.py:188-237)
-            one = ExpertPlacement(ModelShape(1, E, k), [self.placement0.on_fast[l]],
-                                  self.placement0.slot_budget)
-            after, ev1 = allocate_for_sequence(one, counts_l[None, :], self.swap_in_out)
-            evs = [SwapEvent(l, e.swapped_in, e.swapped_out, e.hot_tokens, e.cold_tokens)
-                   for e in ev1]
-            swaps_all.extend(evs)
-            new_sets[l] = set(after.on_fast[0])
-            self._apply_swaps(l, evs)
+            if self.config.engine == "daop":
+                # only DAOP reallocates (experiment.py:158-163): Alg. 1 for this
+                # layer right after its gate (placement.py:188-237)
+                counts_l = hist[0, l].to(torch.int64).cpu().numpy()
+                one = ExpertPlacement(ModelShape(1, E, k), [self.placement0.on_fast[l]],
+                                      self.placement0.slot_budget)
+                after, ev1 = allocate_for_sequence(one, counts_l[None, :], self.swap_in_out)
+                evs = [SwapEvent(l, e.swapped_in, e.swapped_out, e.hot_tokens, e.cold_tokens)
+                       for e in ev1]
+                swaps_all.extend(evs)
+                new_sets[l] = set(after.on_fast[0])
+                self._apply_swaps(l, evs)
             # experts at the post-swap residence
             pr = ops.permute(r["topk_idx"], E, r["x"])
             slot_of = m.slot_of[l]
@@ -231,6 +233,8 @@ class DaopEngine:
             h = out
         torch.cuda.synchronize()
         self.placement = ExpertPlacement(self.shape, new_sets, self.placement0.slot_budget)
+        if self.config.engine in ("ondemand", "prefetch"):
+            self._lru = make_planner(self.placement, self.config)
         counts = hist[0].to(torch.int64).cpu().numpy()
         return PrefillResult(h, counts, self.placement0, self.placement, swaps_all, true_sc,
                              pred_sc, slow_execs, 1e3 * (time.perf_counter() - t0))
@@ -238,6 +242,8 @@ class DaopEngine:
     # ------------------------------------------------------------ decode
     def decode(self, h: torch.Tensor) -> DecodeResult:
         """One decode token (h: (d,) fp32 on device) through every layer."""
+        if self.config.engine in ("ondemand", "prefetch"):
+            return self._decode_lru(h)
         m = self.model
         cfg = self.config
         L, E, k = self.shape.num_layers, self.shape.num_experts, self.shape.top_k
@@ -288,6 +294,57 @@ class DaopEngine:
             prev = b
         torch.cuda.synchronize()
         plans = plans_from_arrays(sel, fast, drop, sub, nd, pred_sc, cfg)
+        return DecodeResult(h, plans, true_sc, pred_sc, 1e3 * (time.perf_counter() - t0))
+
+    def _rebind(self, layer: int, expert: int, evicted: int):
+        """Move `expert` of `layer` into the HBM slot of the expert the LRU
+        cache evicted (pinned host -> HBM on the migration stream)."""
+        m = self.model
+        slot = m.evict(layer, evicted) if evicted >= 0 else m._free[0]
+        return self._migrate_in(layer, expert, slot)
+
+    def _decode_lru(self, h: torch.Tensor) -> DecodeResult:
+        """The ondemand / prefetch baselines on the GPU (policies.py:173-245,
+        simulator.py:297-335): every pick runs on the GPU on the current input.
+        A pick absent from HBM is a demand migration into the slot of the
+        layer's least recently used expert, after which the layer is
+        re-launched; the prefetch engine also moves the next layer's predicted
+        experts in as soon as layer l's prediction gate ran."""
+        m = self.model
+        L, E, k = self.shape.num_layers, self.shape.num_experts, self.shape.top_k
+        prefetch = self.config.engine == "prefetch"
+        t0 = time.perf_counter()
+        true_sc = np.zeros((L, E))
+        pred_sc = np.zeros((L, E))
+        plans = []
+        for l in range(L):
+            b = self.bufs[l % 2]
+            nxt = m.gate[l + 1] if l + 1 < L else None
+
+            def launch():
+                ops.decode_layer(h, m.norm[l], m.gate[l], nxt, m.fast[l], m.slot_of[l], m.slab,
+                                 m.slot_elems, m.d, m.ffn, k, b, mode=0)
+
+            launch()
+            true_sc[l] = b.p.cpu().numpy()
+            if nxt is not None:
+                pred_sc[l] = b.p_pred.cpu().numpy()
+            dec = self._lru.plan_layer(l, true_sc[l],
+                                       pred_sc[l] if (prefetch and nxt is not None) else None)
+            if tuple(int(x) for x in b.sel.cpu().tolist()) != dec.selection:
+                raise ShapeMismatchError(f"layer {l}: device top-k differs from the planner's")
+            for e, ev in zip(dec.migrations, dec.migration_evictions):
+                self._rebind(l, e, ev)
+            if dec.migrations:  # demand migrations block this layer
+                launch()
+            for e, ev in zip(dec.prefetch_issues, dec.prefetch_evictions):
+                self._rebind(l + 1, e, ev)
+            h = b.h_out.clone()
+            plans.append(LayerPlan(layer=l, executed=tuple(ExecutedExpert(e, "fast", "current")
+                                                           for e in dec.selection),
+                                   migrations=dec.migrations,
+                                   prefetch_issues=dec.prefetch_issues))
+        torch.cuda.synchronize()
         return DecodeResult(h, plans, true_sc, pred_sc, 1e3 * (time.perf_counter() - t0))
 
     # ------------------------------------------------------------ sequence

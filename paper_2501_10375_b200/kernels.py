@@ -35,6 +35,8 @@ def _to_dev(a, dtype):
     if isinstance(a, torch.Tensor):
         return a.to(device="cuda", dtype=dtype).contiguous(), True
     arr = np.ascontiguousarray(a)
+    if not arr.flags.writeable:  # read-only trace arrays: torch wants a writable buffer
+        arr = arr.copy()
     return torch.from_numpy(arr).to(device="cuda", dtype=dtype).contiguous(), False
 
 

@@ -1,16 +1,16 @@
-"""Per-token execution plans for the DAOP and Fiddler engines.
+"""Per-token execution plans for all four engines.
 
-Same surface as moesim/policies.py for the hot path: ENGINES :32,
-PREDICTION_START_LAYER_DEFAULT :34, PolicyConfig :37-47, ExecutedExpert /
-Degradation / LayerPlan :50-100, FiddlerPlanner :248-261,
-degrade_selection :264-296, DaopPlanner :299-336, make_planner :339-348,
-plan_token_daop / plan_token_fiddler :371-376, plan_trace_decode :379-387.
+Same surface as moesim/policies.py: ENGINES :32, PREDICTION_START_LAYER_DEFAULT
+:34, PolicyConfig :37-47, ExecutedExpert / Degradation / LayerPlan :50-100,
+OnDemandPlanner :173-194 / PrefetchPlanner :197-245 (LRU caches :103-140),
+FiddlerPlanner :248-261, degrade_selection :264-296, DaopPlanner :299-336,
+make_planner :339-348, plan_token_* :359-376, plan_trace_decode :379-387.
 
-The planning itself executes natively (daop_plan_token_f64 on the host for
-this value-type API; the identical device routine runs inside the decode
-path on the router's float32 probabilities -- csrc/decide.cuh).  The
-ondemand / prefetch baselines (policies.py:103-245) are outside the hot-path
-scope; make_planner rejects them with ConfigError.
+The planning executes natively: daop_plan_token_f64 (fiddler / daop; the
+identical device routine runs inside the decode launch on the router's
+float32 probabilities -- csrc/decide.cuh) and daop_lru_plan_layer (the LRU
+baselines, one layer per call, cache state owned by the planner object here
+so the GPU engine can drive it layer by layer and move HBM slots with it).
 """
 
 from __future__ import annotations
@@ -26,6 +26,7 @@ from .placement import ExpertPlacement
 
 ENGINES = ("ondemand", "prefetch", "fiddler", "daop")
 NATIVE_ENGINES = {"fiddler": 2, "daop": 3}
+LRU_ENGINES = {"ondemand": 0, "prefetch": 1}
 PREDICTION_START_LAYER_DEFAULT = 4
 
 
@@ -180,16 +181,84 @@ class DaopPlanner(_NativePlanner):
     pass
 
 
-_PLANNERS = {"fiddler": FiddlerPlanner, "daop": DaopPlanner}
+@dataclass
+class LruLayerDecision:
+    """One layer of an LRU plan with the slot-level detail the GPU engine
+    needs: which expert each migration / prefetch evicted (-1: none)."""
+    selection: tuple
+    migrations: tuple
+    migration_evictions: tuple
+    prefetch_issues: tuple
+    prefetch_evictions: tuple
+
+
+class _LruPlanner:
+    """Per-layer LRU caches seeded from the placement (policies.py:130-140),
+    state persisting across tokens like the reference's planner object."""
+
+    def __init__(self, placement: ExpertPlacement, config: PolicyConfig):
+        self.placement = placement
+        self.config = config
+        self.shape = placement.shape
+        s = self.shape
+        self.last_use = np.full((s.num_layers, s.num_experts), -1, dtype=np.int64)
+        for l, members in enumerate(placement.on_fast):
+            for e in members:
+                self.last_use[l, e] = 0
+        self.capacity = np.array([len(m) for m in placement.on_fast], dtype=np.int32)
+        self.step = np.zeros(1, dtype=np.int64)
+        k = s.top_k
+        self._buf = [np.zeros(k, dtype=np.int32) for _ in range(5)]
+        self._n = np.zeros(2, dtype=np.int32)
+
+    def members(self, layer: int) -> tuple:
+        return tuple(int(e) for e in np.nonzero(self.last_use[layer] >= 0)[0])
+
+    def plan_layer(self, layer: int, true_row, pred_row=None) -> LruLayerDecision:
+        s = self.shape
+        tr = np.ascontiguousarray(true_row, dtype=np.float64)
+        pr = None if pred_row is None else np.ascontiguousarray(pred_row, dtype=np.float64)
+        sel, mig, mev, pf, pev = self._buf
+        _lib.call("daop_lru_plan_layer", layer, s.num_layers, s.num_experts, s.top_k,
+                  LRU_ENGINES[self.config.engine], self.config.prediction_start_layer,
+                  _lib.ptr(tr), 0 if pr is None else _lib.ptr(pr), _lib.ptr(self.last_use),
+                  _lib.ptr(self.capacity), _lib.ptr(self.step), _lib.ptr(sel), _lib.ptr(mig),
+                  _lib.ptr(mev), self._n.ctypes.data, _lib.ptr(pf), _lib.ptr(pev),
+                  self._n.ctypes.data + 4)
+        nm, npf = int(self._n[0]), int(self._n[1])
+        t = lambda a, n: tuple(int(x) for x in a[:n])  # noqa: E731
+        return LruLayerDecision(t(sel, s.top_k), t(mig, nm), t(mev, nm), t(pf, npf), t(pev, npf))
+
+    def plan_token(self, token: Sequence) -> list:
+        s = self.shape
+        true, pred, pmask = _token_arrays(token, s.num_experts)
+        if true.shape[0] != s.num_layers:
+            raise ShapeMismatchError(
+                f"token covers {true.shape[0]} layers, expected {s.num_layers}")
+        plans = []
+        for l in range(s.num_layers):
+            dec = self.plan_layer(l, true[l], pred[l] if pmask[l] else None)
+            plans.append(LayerPlan(
+                layer=l, executed=tuple(ExecutedExpert(e, "fast", "current")
+                                        for e in dec.selection),
+                migrations=dec.migrations, prefetch_issues=dec.prefetch_issues))
+        return plans
+
+
+class OnDemandPlanner(_LruPlanner):
+    pass
+
+
+class PrefetchPlanner(_LruPlanner):
+    pass
+
+
+_PLANNERS = {"ondemand": OnDemandPlanner, "prefetch": PrefetchPlanner,
+             "fiddler": FiddlerPlanner, "daop": DaopPlanner}
 
 
 def make_planner(placement: ExpertPlacement, config: PolicyConfig):
-    cls = _PLANNERS.get(config.engine)
-    if cls is None:
-        raise ConfigError(
-            f"engine {config.engine!r} is a baseline outside the DAOP hot path "
-            "(SURVEY.md §8a a7); only 'daop' and 'fiddler' are built")
-    return cls(placement, config)
+    return _PLANNERS[config.engine](placement, config)
 
 
 def _single(engine, token, placement, config):
@@ -197,6 +266,15 @@ def _single(engine, token, placement, config):
     if cfg.engine != engine:
         cfg = PolicyConfig(engine, cfg.prediction_start_layer, cfg.graceful_degradation)
     return make_planner(placement, cfg).plan_token(token)
+
+
+def plan_token_ondemand(token, placement, config=None) -> list:
+    """Single-token on-demand plan from a fresh cache snapshot."""
+    return _single("ondemand", token, placement, config)
+
+
+def plan_token_prefetch(token, placement, config=None) -> list:
+    return _single("prefetch", token, placement, config)
 
 
 def plan_token_fiddler(token, placement, config=None) -> list:
@@ -213,11 +291,12 @@ def plan_trace_decode(trace, placement: ExpertPlacement, config: PolicyConfig) -
 
 
 def decode_counters(plans_per_token, config: PolicyConfig) -> dict:
-    """The simulator's counter semantics (simulator.py:160-167,308-389) for
-    the DAOP/Fiddler engines: slow_executions counts current slow picks plus
-    pre-calculated picks (dispatched at layer l for layer l+1 when the
-    prediction gate runs), stale_inputs the pre-calculated picks,
-    degradations the substitutions.  DAOP never migrates during decode."""
+    """The simulator's counter semantics (simulator.py:160-167,297-389):
+    slow_executions counts current slow picks plus pre-calculated picks
+    (dispatched at layer l for layer l+1 when the prediction gate runs),
+    stale_inputs the pre-calculated picks, degradations the substitutions,
+    migrations the demand migrations, prefetches the early migrations for
+    layer l+1 (wasted when l+1 does not execute the expert)."""
     c = {"migrations": 0, "prefetches": 0, "wasted_prefetches": 0,
          "slow_executions": 0, "degradations": 0, "stale_inputs": 0}
     daop = config.engine == "daop"
@@ -225,6 +304,11 @@ def decode_counters(plans_per_token, config: PolicyConfig) -> dict:
     for plans in plans_per_token:
         n = len(plans)
         for l, p in enumerate(plans):
+            c["migrations"] += len(p.migrations)
+            for e in p.prefetch_issues:
+                c["prefetches"] += 1
+                if e not in plans[l + 1].executed_experts():
+                    c["wasted_prefetches"] += 1
             c["slow_executions"] += sum(1 for x in p.executed if x.device == "slow" and not x.precalc)
             if daop and l + 1 < n and l + 1 >= start:
                 pre = sum(1 for x in plans[l + 1].executed if x.precalc)

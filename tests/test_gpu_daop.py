@@ -25,7 +25,8 @@ def _calib(L, E, k, seed):
 
 
 @pytest.mark.parametrize("engine,ecr,start", [("daop", 0.5, 4), ("daop", 0.25, 2),
-                                              ("fiddler", 0.5, 4), ("daop", 1.0, 4)])
+                                              ("fiddler", 0.5, 4), ("daop", 1.0, 4),
+                                              ("ondemand", 0.5, 4), ("prefetch", 0.25, 2)])
 def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
@@ -49,23 +50,37 @@ def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
     # (a3) device activation counter == reference expert_counts on the exported trace
     counts = D.expert_counts(tr.prefill_true, k)
     assert np.array_equal(rec.prefill.counts, counts)
-    # (a6) Alg. 1 swaps (daop reallocates; moesim/experiment.py:158-163)
-    sets, evs = D.allocate_for_sequence(sets0, counts)
+    # (a6) Alg. 1 swaps (only daop reallocates; moesim/experiment.py:158-163)
+    if engine == "daop":
+        sets, evs = D.allocate_for_sequence(sets0, counts)
+    else:
+        sets, evs = [set(s) for s in sets0], []
     assert [(s.layer, s.swapped_in, s.swapped_out, s.hot_tokens, s.cold_tokens)
             for s in rec.prefill.swaps] == evs
     assert [set(s) for s in rec.prefill.placement.on_fast] == sets
-    # the HBM slot table follows the placement
-    assert np.array_equal(eng.model.resident_mask(), rec.prefill.placement.mask())
+    # the HBM slot table follows the placement (LRU engines move it during decode)
+    if engine in ("daop", "fiddler"):
+        assert np.array_equal(eng.model.resident_mask(), rec.prefill.placement.mask())
     # (a7/a8/a9) per-token plans on the exported trace
     mask = np.array([l < L - 1 for l in range(L)])
-    oplans = [D.plan_token(tr.decode_true[t], tr.decode_predicted[t], mask, sets, k, engine,
-                           start=start) for t in range(tr.num_decode_tokens)]
+    if engine in ("ondemand", "prefetch"):
+        caches = D.LruCaches(sets)
+        oplans = [D.plan_token_lru(tr.decode_true[t], tr.decode_predicted[t], mask, caches, k,
+                                   engine, start) for t in range(tr.num_decode_tokens)]
+        # the HBM residence ends equal to the replayed LRU caches
+        assert [set(np.nonzero(r)[0].tolist()) for r in eng.model.resident_mask()] \
+            == [set(c) for c in caches.last_use]
+    else:
+        oplans = [D.plan_token(tr.decode_true[t], tr.decode_predicted[t], mask, sets, k, engine,
+                               start=start) for t in range(tr.num_decode_tokens)]
     for t, (got, exp) in enumerate(zip([r.plans for r in rec.decode], oplans)):
         for l in range(L):
             assert [(x.expert, x.device, x.input_source, x.precalc) for x in got[l].executed] \
                 == [tuple(x) for x in exp[l]["executed"]], (t, l)
             assert [(g.dropped_expert, g.substitute_expert) for g in got[l].degraded] \
                 == [(a, c) for a, _, c, _ in exp[l]["degraded"]], (t, l)
+            assert list(got[l].migrations) == list(exp[l].get("migrations", []))
+            assert list(got[l].prefetch_issues) == list(exp[l].get("prefetch_issues", []))
     # (a10) simulator counters
     assert rec.counts == D.decode_counters(oplans, engine, start)
     # trace is reference-valid: sums to 1 within SCORE_SUM_TOL (checked at construction)
@@ -92,7 +107,8 @@ def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
         plans = rec.decode[t].plans
         sel = [([x.expert for x in p.executed], [x.device == "slow" for x in p.executed])
                for p in plans]
-        ref = N.daop_decode_token(om, toks[t].cpu().numpy(), sel, start, True, engine)
+        ref = N.daop_decode_token(om, toks[t].cpu().numpy(), sel, start, True,
+                                  engine if engine in ("daop", "fiddler") else "fiddler")
         got = rec.decode[t].out.cpu().numpy()
         rms = float(np.sqrt(np.mean(ref.astype(np.float64) ** 2)))
         assert np.abs(got - ref).max() <= 5e-3 * rms + 2e-3 * np.abs(ref).max(), t

@@ -95,11 +95,78 @@ def test_plan_missing_prediction_raises():
         P.plan_token_daop(token, pl, P.PolicyConfig("daop", prediction_start_layer=1))
 
 
-def test_baseline_engines_rejected():
-    shape = P.ModelShape(2, 4, 2)
-    pl = P.ExpertPlacement(shape, [{0, 1}, {0, 1}], 4)
-    with pytest.raises(P.ConfigError):
-        P.make_planner(pl, P.PolicyConfig("ondemand"))
+@pytest.fixture(scope="module")
+def lru_golden():
+    import json
+    from pathlib import Path
+    return json.loads((Path(__file__).parent / "golden" / "lru_plans.json").read_text())
+
+
+def _lru_plan_obj(plans):
+    return [{"executed": [[x.expert, x.device, x.input_source, x.precalc] for x in p.executed],
+             "migrations": list(p.migrations), "prefetch_issues": list(p.prefetch_issues)}
+            for p in plans]
+
+
+@pytest.mark.parametrize("engine", ["ondemand", "prefetch"])
+def test_lru_planners_golden(lru_golden, engine):
+    """OnDemand / Prefetch planners (policies.py:103-245), cache state replayed
+    across the decode tokens, vs the reference's plan_trace_decode; counters
+    vs simulate_decode (simulator.py:297-335)."""
+    for c in lru_golden["cases"]:
+        shape = P.ModelShape(c["L"], c["E"], c["k"])
+        pl = P.ExpertPlacement(shape, [set(s) for s in c["sets"]],
+                               sum(len(s) for s in c["sets"]))
+        tr = P.RoutingTrace(shape, "g", np.array(c["prefill_true"]), np.array(c["decode_true"]),
+                            decode_predicted=np.array(c["decode_pred"]),
+                            decode_mask=np.array(c["decode_mask"]))
+        cfg = P.PolicyConfig(engine, prediction_start_layer=c["start"])
+        plans = P.plan_trace_decode(tr, pl, cfg)
+        assert [_lru_plan_obj(p) for p in plans] == c[engine]["plans"]
+        assert P.decode_counters(plans, cfg) == c[engine]["counts"]
+
+
+@pytest.mark.parametrize("engine", ["ondemand", "prefetch"])
+def test_lru_oracle_golden(lru_golden, engine):
+    """The oracle's restatement is pinned to the same vectors."""
+    for c in lru_golden["cases"]:
+        caches = D.LruCaches([set(s) for s in c["sets"]])
+        dt, dp = np.array(c["decode_true"]), np.array(c["decode_pred"])
+        dm = np.array(c["decode_mask"])
+        plans = [D.plan_token_lru(dt[t], dp[t], dm[t], caches, c["k"], engine, c["start"])
+                 for t in range(dt.shape[0])]
+        got = [[{"executed": [list(x) for x in p["executed"]], "migrations": p["migrations"],
+                 "prefetch_issues": p["prefetch_issues"]} for p in tok] for tok in plans]
+        assert got == c[engine]["plans"]
+        assert D.decode_counters(plans, engine, c["start"]) == c[engine]["counts"]
+
+
+def test_prefetch_missing_prediction(lru_golden):
+    for c in lru_golden["missing"]:
+        shape = P.ModelShape(c["L"], c["E"], c["k"])
+        pl = P.ExpertPlacement(shape, [set(s) for s in c["sets"]],
+                               sum(len(s) for s in c["sets"]))
+        rows = np.array(c["rows"])
+        l = c["L"]
+        token = [P.TokenRouting(rows[j], None if (j == c["gap"] or j == l - 1)
+                                else rows[(j + 1) % l]) for j in range(l)]
+        cfg = P.PolicyConfig("prefetch", prediction_start_layer=c["start"])
+        if c["error"]:
+            with pytest.raises(getattr(P, c["error"])):
+                P.plan_token_prefetch(token, pl, cfg)
+        else:
+            P.plan_token_prefetch(token, pl, cfg)
+
+
+def test_lru_state_persists_and_evicts_lru():
+    # capacity 2, need {2,3} at step 1 evicts both seeds (ties -> lower id first)
+    shape = P.ModelShape(1, 4, 2)
+    pl = P.ExpertPlacement(shape, [{0, 1}], 2)
+    planner = P.make_planner(pl, P.PolicyConfig("ondemand"))
+    tok = [P.TokenRouting(np.array([0.1, 0.1, 0.5, 0.3]))]
+    p = planner.plan_token(tok)[0]
+    assert p.migrations == (2, 3) and planner.members(0) == (2, 3)
+    assert planner.plan_token(tok)[0].migrations == ()
 
 
 def test_run_single_decision_flow_golden(golden):
