@@ -180,6 +180,9 @@ int daop_host_expert_ffn(const uint16_t* h_x, int64_t n, const uint16_t* h_w1,
                          const uint16_t* h_w3, const uint16_t* h_w2, int32_t d, int32_t ffn,
                          float* h_y, uint16_t* h_act_scratch, int32_t threads);
 int daop_host_caps(int32_t* avx512_bf16, int32_t* hw_threads);
+/* profiling aid: stream-read `bytes` of host memory on the slow tier's thread
+ * pool (the bandwidth ceiling of its GEMV); *checksum defeats elision */
+int daop_host_stream_read(const void* h_buf, int64_t bytes, int32_t threads, double* checksum);
 
 /* ------------------------------------------------ grouped expert GEMMs (prefill)
  * tcgen05/TMEM/TMA grouped GEMMs over expert-sorted rows.  Expert e owns rows

@@ -335,6 +335,9 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
         }
       }
       bi = __shfl_sync(0xffffffffu, bi, 0);
+      // NaN scores never compare: fall back to the first untaken id
+      // (topk_scan's "best < 0" rule), never an out-of-range id
+      if (bi >= E) bi = __ffs(__ballot_sync(0xffffffffu, !taken)) - 1;
       if (lane == 0) s.sel[j] = bi;
       if (lane == bi) taken = true;
     }

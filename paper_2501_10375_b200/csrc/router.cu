@@ -165,6 +165,12 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
           bi = oi;
         }
       }
+      bi = __shfl_sync(0xffffffffu, bi, 0);
+      bv = __shfl_sync(0xffffffffu, bv, 0);
+      if (bi >= E) {  // NaN scores never compare: first untaken id (topk_scan rule)
+        bi = __ffs(__ballot_sync(0xffffffffu, !taken)) - 1;
+        bv = __shfl_sync(0xffffffffu, p, bi);
+      }
       den += bv;  // sum of the picked probabilities in pick order (same on all lanes)
       if (lane == j) {
         my_sel = bi;
@@ -358,6 +364,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
               bv = ov;
               bi = oi;
             }
+          }
+          bi = __shfl_sync(0xffffffffu, bi, 0);
+          bv = __shfl_sync(0xffffffffu, bv, 0);
+          if (bi >= E) {  // NaN scores never compare: first untaken id
+            bi = __ffs(__ballot_sync(0xffffffffu, !taken)) - 1;
+            bv = __shfl_sync(0xffffffffu, p, bi);
           }
           den += bv;
           if (lane == j) {

@@ -240,8 +240,60 @@ class DaopEngine:
                              pred_sc, slow_execs, 1e3 * (time.perf_counter() - t0))
 
     # ------------------------------------------------------------ decode
+    def _host_views(self):
+        """Pinned mirrors of the two decode buffers' decision prefix, with
+        numpy views (one D2H copy per layer)."""
+        if getattr(self, "_mh", None) is None:
+            E, k, d = self.shape.num_experts, self.shape.top_k, self.model.d
+            self._mh = []
+            for b in self.bufs:
+                t = torch.empty(b.decisions_bytes, dtype=torch.uint8, pin_memory=True)
+                a = t.numpy()
+                o = b.offsets
+                v = {"x": a[o["x"]: o["x"] + 2 * d].view(np.uint16),
+                     "p": a[o["p"]: o["p"] + 4 * E].view(np.float32),
+                     "p_pred": a[o["p_pred"]: o["p_pred"] + 4 * E].view(np.float32),
+                     "deg": a[o["deg"]: o["deg"] + 4 * (2 * k + 1)].view(np.int32),
+                     "is_fast": a[o["is_fast"]: o["is_fast"] + k],
+                     "sel": a[o["sel"]: o["sel"] + 4 * k].view(np.int32)}
+                self._mh.append((t, v))
+            self._y_host = torch.empty((k, d), dtype=torch.float32, pin_memory=True)
+            self._h_pp = [torch.empty(d, dtype=torch.float32, device=self.model.device)
+                          for _ in range(2)]
+        return self._mh
+
+    def _host_plan(self, layer: int, pred_prev: np.ndarray):
+        """The DAOP plan of `layer` from the prediction carried on layer-1
+        (policies.py:299-336), computed on the host from the same float32
+        values the device planner uses -> identical selection; lets the host
+        tier start the pre-calculation before the layer's launch."""
+        E, k = self.shape.num_experts, self.shape.top_k
+        tr = np.zeros((2, E))
+        pr = np.zeros((2, E))
+        pr[0] = pred_prev
+        pm = np.array([1, 0], dtype=np.uint8)
+        fast = np.zeros((2, E), dtype=np.uint8)
+        fast[1] = self.model.resident_mask()[layer]
+        sel = np.zeros((2, k), dtype=np.int32)
+        isf = np.zeros((2, k), dtype=np.uint8)
+        drop = np.zeros((2, k), dtype=np.int32)
+        sub = np.zeros((2, k), dtype=np.int32)
+        nd = np.zeros(2, dtype=np.int32)
+        _lib.call("daop_plan_token_f64", tr.ctypes.data, pr.ctypes.data, pm.ctypes.data,
+                  fast.ctypes.data, 2, E, k, 1, 3, int(self.config.graceful_degradation),
+                  sel.ctypes.data, isf.ctypes.data, drop.ctypes.data, sub.ctypes.data,
+                  nd.ctypes.data)
+        return sel[1], isf[1]
+
     def decode(self, h: torch.Tensor) -> DecodeResult:
-        """One decode token (h: (d,) fp32 on device) through every layer."""
+        """One decode token (h: (d,) fp32 on device) through every layer.
+
+        Per layer: one decode launch, one D2H of the decisions (+ the layer's
+        x for the host tier), one host synchronisation.  From the prediction
+        start layer on (DAOP), the plan is known before the launch (it only
+        depends on layer l-1's prediction), so the host tier computes the
+        slow picks on the stale x_{l-1} while the GPU streams the resident
+        picks -- the pre-calculation overlap of PAPER.md:317-339."""
         if self.config.engine in ("ondemand", "prefetch"):
             return self._decode_lru(h)
         m = self.model
@@ -249,6 +301,8 @@ class DaopEngine:
         L, E, k = self.shape.num_layers, self.shape.num_experts, self.shape.top_k
         start = cfg.prediction_start_layer
         daop = cfg.engine == "daop"
+        mh = self._host_views()
+        stream = torch.cuda.current_stream()
         t0 = time.perf_counter()
         sel = np.zeros((L, k), dtype=np.int32)
         fast = np.zeros((L, k), dtype=np.uint8)
@@ -257,42 +311,57 @@ class DaopEngine:
         nd = np.zeros(L, dtype=np.int32)
         true_sc = np.zeros((L, E))
         pred_sc = np.zeros((L, E))
-        prev = None
+        prev_b, prev_v = None, None
         for l in range(L):
             b = self.bufs[l % 2]
+            ht, v = mh[l % 2]
             mode = 1 if (daop and l >= start) else 0
             nxt = m.gate[l + 1] if l + 1 < L else None
             ops.decode_layer(h, m.norm[l], m.gate[l], nxt, m.fast[l], m.slot_of[l], m.slab,
                              m.slot_elems, m.d, m.ffn, k, b,
-                             pred_prev=prev.p_pred if mode == 1 else None, mode=mode,
+                             pred_prev=prev_b.p_pred if mode == 1 else None, mode=mode,
                              graceful=cfg.graceful_degradation,
                              weights_from_pred=self.weights_from_pred and mode == 1)
-            s_l = b.sel.cpu().numpy()
-            f_l = b.is_fast.cpu().numpy()
-            dg = b.deg.cpu().numpy()
+            ht.copy_(b.meta[: b.decisions_bytes], non_blocking=True)
+            ys = {}
+            if mode == 1:
+                # pre-calculation on the host while the GPU streams the layer
+                hs, hf = self._host_plan(l, prev_v["p_pred"].astype(np.float64))
+                xs = prev_v["x"][None, :]
+                for q in range(k):
+                    if not hf[q]:
+                        ys[q] = host_expert_ffn(self.pool, l, int(hs[q]), xs, self.host_threads)
+            stream.synchronize()
+            s_l, f_l = v["sel"].copy(), v["is_fast"].copy()
+            if mode == 1 and (s_l.tolist() != hs.tolist() or f_l.tolist() != hf.tolist()):
+                raise ShapeMismatchError(f"layer {l}: host plan differs from the device plan")
+            dg = v["deg"]
             sel[l], fast[l] = s_l, f_l
             nd[l] = dg[2 * k]
             drop[l, : nd[l]] = dg[: nd[l]]
             sub[l, : nd[l]] = dg[k: k + nd[l]]
-            true_sc[l] = b.p.cpu().numpy()
+            true_sc[l] = v["p"]
             if nxt is not None:
-                pred_sc[l] = b.p_pred.cpu().numpy()
+                pred_sc[l] = v["p_pred"]
             if not f_l.all():
-                # slow tier: stale x_{l-1} for pre-calculated picks, else current x_l
-                xin = prev.x if mode == 1 else b.x
-                xs = xin.view(torch.int16).cpu().numpy().view(np.uint16)[None, :]
-                for q in range(k):
-                    if not f_l[q]:
-                        yq = host_expert_ffn(self.pool, l, int(s_l[q]), xs, self.host_threads)
-                        b.y[q].copy_(torch.from_numpy(yq[0]))
-                out = torch.empty_like(h)
+                if mode == 0:  # Fiddler rule: current x_l, after the router
+                    xs = v["x"][None, :]
+                    for q in range(k):
+                        if not f_l[q]:
+                            ys[q] = host_expert_ffn(self.pool, l, int(s_l[q]), xs,
+                                                    self.host_threads)
+                for q, yq in ys.items():
+                    self._y_host[q].copy_(torch.from_numpy(yq[0]))
+                    b.y[q].copy_(self._y_host[q], non_blocking=True)
+                out = self._h_pp[l % 2]
                 _lib.call("daop_combine_dense", h.data_ptr(), b.y.data_ptr(), b.w.data_ptr(), k,
-                          m.d, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                          m.d, out.data_ptr(), stream.cuda_stream)
                 h = out
             else:
-                h = b.h_out.clone()
-            prev = b
+                h = b.h_out
+            prev_b, prev_v = b, v
         torch.cuda.synchronize()
+        h = h.clone()
         plans = plans_from_arrays(sel, fast, drop, sub, nd, pred_sc, cfg)
         return DecodeResult(h, plans, true_sc, pred_sc, 1e3 * (time.perf_counter() - t0))
 

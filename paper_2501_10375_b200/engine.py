@@ -62,17 +62,23 @@ class MoEBlockEngine:
         selection come back in one D2H copy; one replay + one
         synchronize per call keeps the host overhead at a few microseconds."""
         if self._out_host is None:
+            b = self.bufs
             self._h_host = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
-            self._io_host = torch.empty(self.d + self.k, dtype=torch.float32, pin_memory=True)
-            self._out_host = self._io_host[: self.d]
-            self._sel_host = self._io_host[self.d:].view(torch.int32)
+            self._io_host = torch.empty(b.meta.numel() - b.io_offset, dtype=torch.uint8,
+                                        pin_memory=True)
+            so = b.offsets["sel"] - b.io_offset
+            ho = b.offsets["h_out"] - b.io_offset
+            self._sel_host = self._io_host[so: so + 4 * self.k].view(torch.int32)
+            self._out_host = self._io_host[ho: ho + 4 * self.d].view(torch.float32)
             self._host_graphs = {}
+        if h_host.data_ptr() != self._h_host.data_ptr():
+            self._h_host.copy_(h_host)
         g = self._host_graphs.get(layer)
         if g is None:
             def step():
                 self._h_dev.copy_(self._h_host, non_blocking=True)
                 self.decode(self._h_dev, layer)
-                self._io_host.copy_(self.bufs.out_io, non_blocking=True)
+                self._io_host.copy_(self.bufs.meta[self.bufs.io_offset:], non_blocking=True)
 
             side = torch.cuda.Stream(self.device)
             side.wait_stream(torch.cuda.current_stream())
@@ -84,16 +90,15 @@ class MoEBlockEngine:
             with torch.cuda.graph(g):
                 step()
             self._host_graphs[layer] = g
-        if h_host.data_ptr() != self._h_host.data_ptr():
-            self._h_host.copy_(h_host)
         g.replay()
         torch.cuda.current_stream().synchronize()
         return self._out_host, self._sel_host
 
     @staticmethod
     def host_bytes(d: int, k: int):
-        """(h2d, d2h) bytes of one decode_host call."""
-        return d * 4, d * 4 + k * 4
+        """(h2d, d2h) bytes of one decode_host call: h in; the selection
+        (16-byte padded) and the residual out in one copy."""
+        return d * 4, (k * 4 + 15) // 16 * 16 + d * 4
 
     # ------------------------------------------------------------ full decode token
     def decode_token(self, h: torch.Tensor, *, start: int = 4, daop: bool = True,

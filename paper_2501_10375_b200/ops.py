@@ -129,26 +129,41 @@ def combine(h, y_sorted, inv, w, out=None):
     return out
 
 
+def _pad16(n: int) -> int:
+    return (n + 15) // 16 * 16
+
+
 class DecodeBuffers:
     """Preallocated outputs + self-resetting workspace of one decode layer call
-    (fixed addresses, so a decode step can be captured in a CUDA graph)."""
+    (fixed addresses, so a decode step can be captured in a CUDA graph).
+
+    All outputs live in ONE device buffer so the host reads what it needs in
+    one copy:  [x | p | p_pred | w | deg | is_fast | sel | h_out]  (16-byte
+    aligned fields).  The DAOP engine copies the prefix up to `sel` (the
+    decisions + the stale input of the host tier); the end-to-end host call
+    copies the suffix [sel | h_out]."""
 
     def __init__(self, d, ffn, num_experts, k, device):
         nb = torch.zeros(1, dtype=torch.int64)
         _lib.call("daop_decode_workspace", d, ffn, num_experts, k, nb.data_ptr())
         self.ws = torch.zeros(int(nb[0]), dtype=torch.uint8, device=device)
-        f32 = dict(dtype=torch.float32, device=device)
-        self.x = torch.empty(d, dtype=torch.bfloat16, device=device)
-        self.p = torch.empty(num_experts, **f32)
-        self.p_pred = torch.empty(num_experts, **f32)
-        # residual out and selection side by side: one D2H copy returns both
-        self.out_io = torch.empty(d + k, **f32)
-        self.h_out = self.out_io[:d]
-        self.sel = self.out_io[d:].view(torch.int32)
-        self.w = torch.empty(k, **f32)
-        self.is_fast = torch.empty(k, dtype=torch.uint8, device=device)
-        self.deg = torch.empty(2 * k + 1, dtype=torch.int32, device=device)
-        self.y = torch.zeros((k, d), **f32)
+        e = num_experts
+        sizes = [("x", 2 * d), ("p", 4 * e), ("p_pred", 4 * e), ("w", 4 * k),
+                 ("deg", 4 * (2 * k + 1)), ("is_fast", k), ("sel", 4 * k), ("h_out", 4 * d)]
+        off, o = {}, 0
+        for name, n in sizes:
+            off[name] = o
+            o += _pad16(n)
+        self.meta = torch.zeros(o, dtype=torch.uint8, device=device)
+        self.offsets = off
+        dt = {"x": torch.bfloat16, "p": torch.float32, "p_pred": torch.float32,
+              "w": torch.float32, "deg": torch.int32, "is_fast": torch.uint8,
+              "sel": torch.int32, "h_out": torch.float32}
+        for name, n in sizes:
+            setattr(self, name, self.meta[off[name]: off[name] + n].view(dt[name]))
+        self.decisions_bytes = off["sel"] + _pad16(4 * k)  # prefix: x .. sel
+        self.io_offset = off["sel"]                         # suffix: sel | h_out
+        self.y = torch.zeros((k, d), dtype=torch.float32, device=device)
 
 
 def decode_layer(h, gamma, wg, wg_next, fast_row, slot_of, slab, slot_elems, d, ffn, k,

@@ -322,3 +322,24 @@ def test_decode_layer_plan_mode(P, resident, graceful):
             ref = h.cpu().numpy()[0] + sum(wref[q] * N.expert_ffn(
                 x, om.w1(1, e), om.w3(1, e), om.w2(1, e))[0] for q, e in enumerate(sel))
             hidden_close(bufs.h_out.cpu().numpy(), ref, "combined")
+
+
+def test_decode_and_router_nan_input_selects_valid_ids(P):
+    """A NaN residual must not produce out-of-range expert ids (the top-k falls
+    back to the first untaken id, like topk_scan's scan): the launch completes
+    and every selected id is in [0, E)."""
+    pkg, model_mod, ops = P
+    d, ffn, E, k = 256, 512, 8, 2
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, k), d, ffn, seed=1, resident_layers=[0])
+    bufs = ops.DecodeBuffers(d, ffn, E, k, "cuda")
+    h = torch.full((d,), float("nan"), device="cuda")
+    ops.decode_layer(h, m.norm[0], m.gate[0], m.gate[1], m.fast[0], m.slot_of[0], m.slab,
+                     m.slot_elems, d, ffn, k, bufs)
+    torch.cuda.synchronize()
+    sel = bufs.sel.cpu().tolist()
+    assert all(0 <= e < E for e in sel) and len(set(sel)) == k
+    r = ops.router(torch.full((40, d), float("nan"), device="cuda"), m.norm[0], m.gate[0],
+                   m.gate[1], k)
+    torch.cuda.synchronize()
+    idx = r["topk_idx"].cpu().numpy()
+    assert ((idx >= 0) & (idx < E)).all()
