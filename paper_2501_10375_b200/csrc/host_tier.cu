@@ -19,6 +19,9 @@
 #include <vector>
 
 #include <immintrin.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+#include <cpuid.h>
 
 #include "common.cuh"
 
@@ -44,28 +47,6 @@ static float dot_scalar(const uint16_t* a, const uint16_t* b, int n) {
   float acc = 0.f;
   for (int i = 0; i < n; ++i) acc += bf2f(a[i]) * bf2f(b[i]);
   return acc;
-}
-
-__attribute__((target("avx512f,avx512bf16,avx512bw,avx512vl"))) static float dot_avx512bf16(
-    const uint16_t* a, const uint16_t* b, int n) {
-  __m512 acc0 = _mm512_setzero_ps(), acc1 = _mm512_setzero_ps();
-  int i = 0;
-  for (; i + 64 <= n; i += 64) {
-    __m512bh x0 = (__m512bh)_mm512_loadu_si512(a + i);
-    __m512bh w0 = (__m512bh)_mm512_loadu_si512(b + i);
-    __m512bh x1 = (__m512bh)_mm512_loadu_si512(a + i + 32);
-    __m512bh w1 = (__m512bh)_mm512_loadu_si512(b + i + 32);
-    acc0 = _mm512_dpbf16_ps(acc0, x0, w0);
-    acc1 = _mm512_dpbf16_ps(acc1, x1, w1);
-  }
-  for (; i + 32 <= n; i += 32) {
-    __m512bh x0 = (__m512bh)_mm512_loadu_si512(a + i);
-    __m512bh w0 = (__m512bh)_mm512_loadu_si512(b + i);
-    acc0 = _mm512_dpbf16_ps(acc0, x0, w0);
-  }
-  float r = _mm512_reduce_add_ps(_mm512_add_ps(acc0, acc1));
-  for (; i < n; ++i) r += bf2f(a[i]) * bf2f(b[i]);
-  return r;
 }
 
 // two rows against one x in one pass (the W1 and W3 rows of the same unit):
@@ -136,10 +117,6 @@ static bool have_bf16() {
   return v == 1;
 }
 
-static float dot(const uint16_t* a, const uint16_t* b, int n) {
-  return have_bf16() ? dot_avx512bf16(a, b, n) : dot_scalar(a, b, n);
-}
-
 static void dot2(const uint16_t* x, const uint16_t* a, const uint16_t* b, int n, float* ra,
                  float* rb) {
   if (have_bf16()) {
@@ -152,6 +129,153 @@ static void dot2(const uint16_t* x, const uint16_t* a, const uint16_t* b, int n,
 
 static float dot_long(const uint16_t* x, const uint16_t* a, int n) {
   return have_bf16() ? dot_long_avx512bf16(x, a, n) : dot_scalar(x, a, n);
+}
+
+// ------------------------------------------------------------------ AMX
+// Batched host experts (prefill: tens of tokens per slow expert) are compute
+// bound on AVX-512; the 5th-gen Xeon's AMX-BF16 tiles do 16x16x32 per
+// TDPBF16PS.  Layout: weights stay row-major (an A tile = 16 weight rows x 32
+// k, loaded straight from the pinned pool); the tokens are the B side, packed
+// once per call into VNNI pairs ([token block][k block][16 k-pairs][16 tokens]).
+// The up pass writes act directly in the down pass's VNNI layout.
+
+struct AmxCfg {
+  uint8_t palette;
+  uint8_t start_row;
+  uint8_t reserved[14];
+  uint16_t colsb[16];
+  uint8_t rows[16];
+};
+
+static bool amx_usable() {
+  static int v = -1;
+  if (v < 0) {
+    unsigned a, b, c, d;
+    bool hw = __get_cpuid_count(7, 0, &a, &b, &c, &d) && (d & (1u << 22)) && (d & (1u << 24));
+    // Linux: the process must request the tile data state once
+    v = hw && syscall(SYS_arch_prctl, 0x1023 /*ARCH_REQ_XCOMP_PERM*/, 18 /*XTILEDATA*/) == 0;
+  }
+  return v == 1;
+}
+
+__attribute__((target("amx-tile,amx-bf16"))) static void amx_config() {
+  AmxCfg cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.palette = 1;
+  for (int t = 0; t < 8; ++t) {
+    cfg.rows[t] = 16;
+    cfg.colsb[t] = 64;
+  }
+  _tile_loadconfig(&cfg);
+}
+
+__attribute__((target("amx-tile"))) static void amx_release() { _tile_release(); }
+
+// pack rows [t0, t0+16) of src (n x K bf16, row-major) into VNNI B tiles for
+// every k block: dst[kb][r][j] = (src[t0+j][32kb+2r], src[t0+j][32kb+2r+1])
+static void pack_vnni(const uint16_t* src, int64_t n, int K, int64_t t0, uint32_t* dst) {
+  const int kbs = K / 32;
+  for (int kb = 0; kb < kbs; ++kb)
+    for (int r = 0; r < 16; ++r)
+      for (int j = 0; j < 16; ++j) {
+        const int64_t t = t0 + j;
+        uint32_t v = 0;
+        if (t < n) {
+          const uint16_t* p = src + t * K + kb * 32 + 2 * r;
+          v = static_cast<uint32_t>(p[0]) | (static_cast<uint32_t>(p[1]) << 16);
+        }
+        dst[(static_cast<size_t>(kb) * 16 + r) * 16 + j] = v;
+      }
+}
+
+// up: rows [i0, i0+16) of W1/W3 against every token block; act written into
+// the down pass's VNNI pack (ffn/32 k-blocks per token block)
+__attribute__((target("amx-tile,amx-bf16"))) static void amx_up_block(
+    const uint16_t* w1, const uint16_t* w3, int d, int ffn, int64_t i0, const uint32_t* xp,
+    int ntb, uint32_t* actp, int64_t n) {
+  alignas(64) float g[2][16][16], u[2][16][16];
+  const int kbs = d / 32;
+  const size_t xtb = static_cast<size_t>(kbs) * 256;           // uint32 per token block
+  const size_t atb = static_cast<size_t>(ffn / 32) * 256;
+  for (int tb = 0; tb < ntb; tb += 2) {
+    const int nb = ntb - tb >= 2 ? 2 : 1;
+    _tile_zero(4);
+    _tile_zero(5);
+    _tile_zero(6);
+    _tile_zero(7);
+    for (int kb = 0; kb < kbs; ++kb) {
+      _tile_loadd(0, w1 + i0 * d + kb * 32, d * 2);
+      _tile_loadd(1, w3 + i0 * d + kb * 32, d * 2);
+      _tile_loadd(2, xp + tb * xtb + static_cast<size_t>(kb) * 256, 64);
+      _tile_dpbf16ps(4, 0, 2);
+      _tile_dpbf16ps(5, 1, 2);
+      if (nb == 2) {
+        _tile_loadd(3, xp + (tb + 1) * xtb + static_cast<size_t>(kb) * 256, 64);
+        _tile_dpbf16ps(6, 0, 3);
+        _tile_dpbf16ps(7, 1, 3);
+      }
+    }
+    _tile_stored(4, g[0], 64);
+    _tile_stored(5, u[0], 64);
+    _tile_stored(6, g[1], 64);
+    _tile_stored(7, u[1], 64);
+    for (int b = 0; b < nb; ++b) {
+      uint16_t* ap = reinterpret_cast<uint16_t*>(actp + (tb + b) * atb);
+      for (int ii = 0; ii < 16; ++ii) {
+        const int64_t i = i0 + ii;
+        const int64_t kb = i / 32, r = (i % 32) / 2, par = i % 2;
+        for (int j = 0; j < 16; ++j) {
+          if ((tb + b) * 16 + j >= n) break;
+          const float gv = g[b][ii][j], uv = u[b][ii][j];
+          const float sv = gv / (1.0f + std::exp(-gv));
+          ap[((kb * 16 + r) * 16 + j) * 2 + par] = f2bf(sv * uv);
+        }
+      }
+    }
+  }
+}
+
+// down: rows [j0, j0+16) of W2 against up to 4 token blocks per pass
+__attribute__((target("amx-tile,amx-bf16"))) static void amx_down_block(
+    const uint16_t* w2, int d, int ffn, int64_t j0, const uint32_t* actp, int ntb, float* y,
+    int64_t n) {
+  alignas(64) float c[4][16][16];
+  const int kbs = ffn / 32;
+  const size_t atb = static_cast<size_t>(kbs) * 256;
+  for (int tb = 0; tb < ntb; tb += 4) {
+    const int nb = ntb - tb >= 4 ? 4 : ntb - tb;
+    _tile_zero(4);
+    _tile_zero(5);
+    _tile_zero(6);
+    _tile_zero(7);
+    for (int kb = 0; kb < kbs; ++kb) {
+      _tile_loadd(0, w2 + j0 * ffn + kb * 32, ffn * 2);
+      _tile_loadd(1, actp + (tb + 0) * atb + static_cast<size_t>(kb) * 256, 64);
+      _tile_dpbf16ps(4, 0, 1);
+      if (nb > 1) {
+        _tile_loadd(2, actp + (tb + 1) * atb + static_cast<size_t>(kb) * 256, 64);
+        _tile_dpbf16ps(5, 0, 2);
+      }
+      if (nb > 2) {
+        _tile_loadd(3, actp + (tb + 2) * atb + static_cast<size_t>(kb) * 256, 64);
+        _tile_dpbf16ps(6, 0, 3);
+      }
+      if (nb > 3) {
+        _tile_loadd(1, actp + (tb + 3) * atb + static_cast<size_t>(kb) * 256, 64);
+        _tile_dpbf16ps(7, 0, 1);
+      }
+    }
+    _tile_stored(4, c[0], 64);
+    _tile_stored(5, c[1], 64);
+    _tile_stored(6, c[2], 64);
+    _tile_stored(7, c[3], 64);
+    for (int b = 0; b < nb; ++b)
+      for (int jj = 0; jj < 16; ++jj)
+        for (int t = 0; t < 16; ++t) {
+          const int64_t tok = (tb + b) * 16 + t;
+          if (tok < n) y[tok * d + j0 + jj] = c[b][jj][t];
+        }
+  }
 }
 
 // ------------------------------------------------------------------ pool
@@ -249,6 +373,39 @@ extern "C" int daop_host_expert_ffn(const uint16_t* x, int64_t n, const uint16_t
   if (threads < 1)
     threads = 2 * static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   host::Pool* pool = host::pool_for(threads);
+  if (n >= 16 && d % 32 == 0 && ffn % 32 == 0 && host::amx_usable()) {
+    // batched experts on AMX tiles (prefill slow tier)
+    const int ntb = static_cast<int>((n + 15) / 16);
+    std::vector<uint32_t> xp(static_cast<size_t>(ntb) * (d / 32) * 256);
+    std::vector<uint32_t> actp(static_cast<size_t>(ntb) * (ffn / 32) * 256, 0u);
+    pool->run(ntb, [&](int, int64_t a, int64_t b) {
+      for (int64_t tb = a; tb < b; ++tb)
+        host::pack_vnni(x, n, d, tb * 16, xp.data() + tb * (d / 32) * 256);
+    });
+    pool->run(ffn / 16, [&](int, int64_t a, int64_t b) {
+      if (a >= b) return;
+      host::amx_config();
+      for (int64_t blk = a; blk < b; ++blk)
+        host::amx_up_block(w1, w3, d, ffn, blk * 16, xp.data(), ntb, actp.data(), n);
+      host::amx_release();
+    });
+    pool->run(d / 16, [&](int, int64_t a, int64_t b) {
+      if (a >= b) return;
+      host::amx_config();
+      for (int64_t blk = a; blk < b; ++blk)
+        host::amx_down_block(w2, d, ffn, blk * 16, actp.data(), ntb, y, n);
+      host::amx_release();
+    });
+    if (act_scratch) {  // unpack act for callers that asked for it
+      for (int64_t t = 0; t < n; ++t)
+        for (int i = 0; i < ffn; ++i) {
+          const int64_t tb = t / 16, j = t % 16, kb = i / 32, r = (i % 32) / 2, par = i % 2;
+          act_scratch[t * ffn + i] = reinterpret_cast<const uint16_t*>(
+              actp.data() + tb * (ffn / 32) * 256)[((kb * 16 + r) * 16 + j) * 2 + par];
+        }
+    }
+    return DAOP_OK;
+  }
   std::vector<uint16_t> own;
   uint16_t* act = act_scratch;
   if (!act) {
@@ -309,7 +466,7 @@ extern "C" int daop_host_stream_read(const void* p, int64_t bytes, int32_t threa
 }
 
 extern "C" int daop_host_caps(int32_t* avx512_bf16, int32_t* hw_threads) {
-  *avx512_bf16 = host::have_bf16() ? 1 : 0;
+  *avx512_bf16 = (host::have_bf16() ? 1 : 0) | (host::amx_usable() ? 2 : 0);
   *hw_threads = static_cast<int32_t>(std::thread::hardware_concurrency());
   return DAOP_OK;
 }

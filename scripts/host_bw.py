@@ -40,3 +40,19 @@ for th in sorted({1, 2, 4, 8, nthreads, 2 * nthreads}):
         dt = (time.perf_counter() - t) / 3
         print(f"threads {th:3d} {name:8s} read {rd:6.1f} GB/s   expert GEMV {dt*1e3:6.2f} ms "
               f"= {nb / dt / 1e9:6.1f} GB/s", flush=True)
+caps = np.zeros(2, dtype=np.int32)
+_lib.call("daop_host_caps", caps.ctypes.data, caps.ctypes.data + 4)
+print("caps: avx512_bf16", bool(caps[0] & 1), "amx", bool(caps[0] & 2))
+p = buf.data_ptr()
+w1, w3, w2 = p, p + d * ffn * 2, p + 2 * d * ffn * 2
+for n in (16, 64, 128, 256):
+    xs = np.random.default_rng(1).integers(0, 1 << 14, size=(n, d), dtype=np.uint16)
+    ys = np.empty((n, d), dtype=np.float32)
+    _lib.call("daop_host_expert_ffn", xs.ctypes.data, n, w1, w3, w2, d, ffn, ys.ctypes.data, 0, 0)
+    t = time.perf_counter()
+    for _ in range(3):
+        _lib.call("daop_host_expert_ffn", xs.ctypes.data, n, w1, w3, w2, d, ffn, ys.ctypes.data,
+                  0, 0)
+    dt = (time.perf_counter() - t) / 3
+    print(f"batched expert n={n:4d}: {dt*1e3:7.2f} ms  {2*n*3*d*ffn/dt/1e12:6.2f} TFLOP/s  "
+          f"{3*d*ffn*2/dt/1e9:6.1f} GB/s of weights", flush=True)

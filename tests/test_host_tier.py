@@ -8,8 +8,14 @@ from oracle import numerics as N
 from oracle import rng as R
 
 
-def test_host_expert_ffn_matches_oracle():
-    d, ffn, n = 256, 512, 3
+import pytest
+
+
+@pytest.mark.parametrize("n", [1, 3, 16, 37, 64])
+def test_host_expert_ffn_matches_oracle(n):
+    """n < 16: AVX-512 BF16 GEMV path; n >= 16: AMX-BF16 tiles when the host
+    has them (token blocks of 16, ragged tail zero-padded)."""
+    d, ffn = 256, 512
     om = N.OracleModel(2, 4, 2, d, ffn, seed=7)
     w1, w3, w2 = om.w1(1, 2), om.w3(1, 2), om.w2(1, 2)
     to_bits = lambda a: np.ascontiguousarray(R.f32_to_bf16_bits(a))  # noqa: E731
@@ -22,6 +28,14 @@ def test_host_expert_ffn_matches_oracle():
     ref = N.expert_ffn(x, w1, w3, w2)
     rms = float(np.sqrt(np.mean(ref ** 2)))
     assert np.abs(y - ref).max() <= 2e-3 * rms + 1e-3 * np.abs(ref).max()
+    act = np.zeros((n, ffn), dtype=np.uint16)
+    y2 = np.empty((n, d), dtype=np.float32)
+    _lib.call("daop_host_expert_ffn", xb.ctypes.data, n, b1.ctypes.data, b3.ctypes.data,
+              b2.ctypes.data, d, ffn, y2.ctypes.data, act.ctypes.data, 4)
+    assert np.array_equal(y, y2)  # deterministic
+    a_ref = N.expert_act(x, w1, w3)
+    a = R.bf16_bits_to_f32(act)
+    assert np.all(np.abs(a - a_ref) <= np.abs(a_ref) * 2 ** -7 + 1e-3 * np.abs(a_ref).max())
 
 
 def test_host_caps_reports():
