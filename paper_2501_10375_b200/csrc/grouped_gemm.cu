@@ -51,7 +51,23 @@ struct GemmParams {
   int policy;             // L2 hint set (tuning): 0 A last/B normal, 1 both normal, 2 both last, 3 A normal/B last,
                           // 4 A first/B last, 5 A first/B normal, 6 A last/B first
   int raster;             // pair kernel tile order: 0 m-groups, 1 n-groups (see map_tile_pair)
+  // L2 demotion at last use (pair kernel): operand lines loaded with
+  // evict_last are switched back to evict_normal by the epilogue once no tile
+  // of this launch reads them again, so the persisting set-aside is free for
+  // the next expert's tiles instead of holding stale ones
+  int demote;              // bit 0: A rows (raster 0), bit 1: B rows (raster 1)
+  const uint16_t* a_ptr;   // A base (rows x a_ld bf16)
+  int64_t a_ld;
+  const uint16_t* b_ptr;   // B base of slot 0 (rows x b_ld bf16)
+  int64_t b_ld;
+  int64_t b_slot_stride;   // elements
 };
+
+__device__ __forceinline__ void l2_demote_range(const void* p, int64_t bytes) {
+  const char* c = static_cast<const char*>(p);
+  for (int64_t o = 0; o < bytes; o += 128)
+    asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(c + o) : "memory");
+}
 
 struct GemmSmem {
   uint64_t full[G_STAGES];
@@ -532,6 +548,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&s.tempty[acc], 0);
+      if (p.demote) {
+        if ((p.demote & 1) && p.raster == 0 && n == nt - 1 && valid)  // A m-tile done
+          l2_demote_range(p.a_ptr + grow * p.a_ld, p.a_ld * 2);
+        if ((p.demote & 2) && p.raster == 1 && m == s.mt[e] - 1) {     // B n-tile done
+          const int brow = n * p.b_tile_rows + (rank == 0 ? 0 : p.b_half2) + q * 32 + lane;
+          l2_demote_range(p.b_ptr + static_cast<int64_t>(p.slot_of[e]) * p.b_slot_stride +
+                              static_cast<int64_t>(brow) * p.b_ld,
+                          p.b_ld * 2);
+        }
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -548,6 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
 
 static int g_gemm_mode = 0;    // 0: CTA pair (default), 1: single CTA
 static int g_gemm_policy = -1;  // L2 hint set override (tuning); -1 = per-GEMM default
+static int g_gemm_demote = 0;   // bit 0: demote A (up), bit 1: demote B (down)
 
 static size_t gemm_smem_bytes() { return 1024 + G_STAGES * G_STAGE_BYTES + sizeof(GemmSmem); }
 static size_t pair_smem_bytes() { return 1024 + P_STAGES * P_STAGE_BYTES + sizeof(PairSmem); }
@@ -569,6 +596,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
       done[dev] = true;
     }
   }
+  if (g_gemm_demote & 4) cudaCtxResetPersistingL2Cache();  // tuning: start from a clean set-aside
   if (g_gemm_mode == 0) {
     const size_t smem = pair_smem_bytes();
     DAOP_CUDA(cudaFuncSetAttribute(grouped_gemm_pair_kernel<SWIGLU>,
@@ -620,12 +648,13 @@ static int check_ffn_shape(int64_t rows, int32_t d, int32_t ffn, int32_t E) {
 
 extern "C" int daop_set_gemm_mode(int32_t mode) {
   // low nibble: kernel (0 CTA pair, 1 single CTA); bits 4..6: L2 hint set (tuning)
-  if ((mode & 15) > 1 || (mode >> 4) > 6) {
+  if ((mode & 15) > 1 || ((mode >> 4) & 15) > 6) {
     set_error("gemm mode must be kernel (0 pair / 1 single) | policy << 4");
     return DAOP_ERR_CONFIG;
   }
   g_gemm_mode = mode & 15;
-  g_gemm_policy = (mode >> 4) ? (mode >> 4) : -1;
+  g_gemm_policy = ((mode >> 4) & 15) ? ((mode >> 4) & 15) : -1;
+  g_gemm_demote = (mode >> 8) & 7;
   return DAOP_OK;
 }
 
@@ -649,7 +678,8 @@ extern "C" int daop_expert_gemm_up(const uint16_t* x_perm, int64_t rows, int32_t
   const uint32_t bbox[3] = {GB_K, 128, 1};
   if ((rc = make_tmap_bf16(&tb, slab, 3, bdims, bstr, bbox))) return rc;
   GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : 64,
-               128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0, 0};
+               128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0, 0,
+               g_gemm_demote & 1, x_perm, d, slab, d, slot_stride_elems};
   return launch_gemm<true>(ta, tb, p, rows, as_stream(stream));
 }
 
@@ -676,6 +706,7 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
   // default: n-grouped raster, 8 weight n-tiles per group (DRAM 20 GB vs 25 GB
   // for m-groups on 8 x 4096 tokens; profiles/r01/gemm_sweep.txt)
   GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, group_m != 0 ? group_m : -8,
-               GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0};
+               GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0,
+               g_gemm_demote & 2, act, ffn, w2, ffn, slot_stride_elems};
   return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
 }

@@ -262,15 +262,19 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
   };
   if (threadIdx.x == 0)
     for (int i = 0; i < PF; ++i) prefetch_tile(blockIdx.x + static_cast<int64_t>(i) * gridDim.x);
+  // software pipeline over this CTA's tiles: the x/MMA pass of tile i and the
+  // sum-of-squares pass of tile i+1 share one batch of loads and one barrier
+  auto ss_partial = [&](float ssv) {  // sum over the 4 lanes of a token
+    ssv += __shfl_xor_sync(0xffffffffu, ssv, 1);
+    ssv += __shfl_xor_sync(0xffffffffu, ssv, 2);
+    return ssv;
+  };
   int buf = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
-    if (threadIdx.x == 0) prefetch_tile(tile + static_cast<int64_t>(PF) * gridDim.x);
-    const int64_t t = tile * kTokTile + g;  // this lane's token
-    const bool live = t < a.T;
-    const float* hrow = a.h + (live ? t : 0) * d;
-    // pass 1: partial sum of squares over this warp's K-slice
+  {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kTokTile + g;
     float ss = 0.f;
-    if (live) {
+    if (blockIdx.x < ntiles && t < a.T) {
+      const float* hrow = a.h + t * d;
 #pragma unroll 16
       for (int ks = 0; ks < ksteps; ++ks) {
         const int k = k0w + ks * 16 + c2;
@@ -280,33 +284,49 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
         ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss);
       }
     }
-    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
-    float* ssb = sspart + buf * kMmaWarps * kTokTile;
-    if ((lane & 3) == 0) ssb[warp * kTokTile + g] = ss;
+    ss = ss_partial(ss);
+    if ((lane & 3) == 0) sspart[warp * kTokTile + g] = ss;
     __syncthreads();
+  }
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+    if (threadIdx.x == 0) prefetch_tile(tile + static_cast<int64_t>(PF) * gridDim.x);
+    const int64_t t = tile * kTokTile + g;  // this lane's token
+    const bool live = t < a.T;
+    const float* hrow = a.h + (live ? t : 0) * d;
+    const int64_t t1 = t + static_cast<int64_t>(gridDim.x) * kTokTile;  // next tile, same lane
+    const bool live1 = t1 < a.T;
+    const float* hrow1 = a.h + (live1 ? t1 : 0) * d;
+    const float* ssb = sspart + buf * kMmaWarps * kTokTile;
     float tot = 0.f;
     for (int w = 0; w < kMmaWarps; ++w) tot += ssb[w * kTokTile + g];
     const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + a.eps);
-    // pass 2: x fragments, x store, MMA against the gate rows
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float ss1 = 0.f;
     uint16_t* xrow = a.x_out ? a.x_out + (live ? t : 0) * d : nullptr;
-    // batches of 8 k-steps: all h loads of a batch are issued before the x
-    // stores (which the compiler cannot prove do not alias h)
-    for (int ks0 = 0; ks0 < ksteps; ks0 += 8) {
-      float2 u[8], v[8];
+    // batches of 4 k-steps: every h load of the batch (this tile's reload and
+    // the next tile's first read) is issued before the x stores, which the
+    // compiler cannot prove do not alias h
+    for (int ks0 = 0; ks0 < ksteps; ks0 += 4) {
+      float2 u[4], v[4], u1[4], v1[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        u[i] = make_float2(0.f, 0.f);
-        v[i] = make_float2(0.f, 0.f);
-        if (live && ks0 + i < ksteps) {
+      for (int i = 0; i < 4; ++i) {
+        u[i] = v[i] = u1[i] = v1[i] = make_float2(0.f, 0.f);
+        if (ks0 + i < ksteps) {
           const int k = k0w + (ks0 + i) * 16 + c2;
-          u[i] = __ldg(reinterpret_cast<const float2*>(hrow + k));
-          v[i] = __ldg(reinterpret_cast<const float2*>(hrow + k + 8));
+          if (live) {
+            u[i] = __ldg(reinterpret_cast<const float2*>(hrow + k));
+            v[i] = __ldg(reinterpret_cast<const float2*>(hrow + k + 8));
+          }
+          if (live1) {
+            u1[i] = __ldg(reinterpret_cast<const float2*>(hrow1 + k));
+            v1[i] = __ldg(reinterpret_cast<const float2*>(hrow1 + k + 8));
+          }
         }
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 4; ++i) {
+        ss1 = fmaf(u1[i].x, u1[i].x, ss1); ss1 = fmaf(u1[i].y, u1[i].y, ss1);
+        ss1 = fmaf(v1[i].x, v1[i].x, ss1); ss1 = fmaf(v1[i].y, v1[i].y, ss1);
         if (ks0 + i < ksteps) {
           const int k = k0w + (ks0 + i) * 16 + c2;
           const uint32_t b0 = pack_x2(u[i].x, u[i].y, r, *reinterpret_cast<const uint32_t*>(gam + k));
@@ -325,6 +345,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
         }
       }
     }
+    ss1 = ss_partial(ss1);
+    if ((lane & 3) == 0) sspart[(buf ^ 1) * kMmaWarps * kTokTile + warp * kTokTile + g] = ss1;
     // D fragment: gate rows g, g+8 x tokens c2, c2+1
     float* zb = zpart + buf * kMmaWarps * 16 * kTokTile + warp * 16 * kTokTile;
     zb[g * kTokTile + c2] = acc[0];
