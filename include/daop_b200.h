@@ -230,7 +230,7 @@ int daop_decode_layer(const float* d_h, const uint16_t* d_gamma, const uint16_t*
                       int32_t* d_deg, float* d_y, float* d_h_out, void* d_workspace,
                       int32_t variant, daop_stream_t stream);
 /* variant: ring geometry (warps x stages x stage bytes); 0 = default
- * (8 x 2 x 10 KB), 1..4 = tuning alternatives.  num_experts <= 16. */
+ * (16 x 1 x 10 KB), 1..9 = tuning alternatives.  num_experts <= 16. */
 
 /* ------------------------------------------------ trace files (moesim JSONL)
  * Formats one phase's token records of a RoutingTrace exactly as
