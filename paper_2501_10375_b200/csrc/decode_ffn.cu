@@ -87,7 +87,8 @@ template <int DW, int DS>
 struct DecodeSmem {
   uint64_t bar[DW][DS];
   uint64_t act_bar[DK_MAX];
-  uint64_t in_bar;
+  uint64_t in_bar;   // h + gamma
+  uint64_t in_bar2;  // gate rows (+ next-layer row)
   Piece rec[DW][DS];
   int act_req[DK_MAX];
   int p1_next, p2_next, fin;
@@ -185,16 +186,18 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
       s.done1[q] = 0;
     }
     mbar_init(&s.in_bar, 1);
-    s.p1_next = s.p2_next = s.fin = 0;
+    mbar_init(&s.in_bar2, 1);
+    s.p1_next = DW;  // tickets 0..DW-1 are taken statically by the warps' first units
+    s.p2_next = s.fin = 0;
     fence_mbar_init();
-    if (a.mode == 0) {  // h, gamma, the E gate rows, this CTA's next-layer row: one barrier
-      const uint32_t bytes = d * 4 + d * 2 + E * d * 2 + (pred_row ? d * 2 : 0);
-      mbar_arrive_expect_tx(&s.in_bar, bytes);
+    if (a.mode == 0) {  // h + gamma (RMSNorm starts on them), then the gate rows
+      mbar_arrive_expect_tx(&s.in_bar, d * 4 + d * 2);
       bulk_g2s_plain(h_s, a.h, d * 4, &s.in_bar);
       bulk_g2s_plain(gm_s, a.gamma, d * 2, &s.in_bar);
-      bulk_g2s_plain(g_s, a.wg, E * d * 2, &s.in_bar);
+      mbar_arrive_expect_tx(&s.in_bar2, E * d * 2 + (pred_row ? d * 2 : 0));
+      bulk_g2s_plain(g_s, a.wg, E * d * 2, &s.in_bar2);
       if (pred_row)
-        bulk_g2s_plain(gp_s, a.wg_next + static_cast<size_t>(blockIdx.x) * d, d * 2, &s.in_bar);
+        bulk_g2s_plain(gp_s, a.wg_next + static_cast<size_t>(blockIdx.x) * d, d * 2, &s.in_bar2);
     }
   }
   if (warp == 1) {
@@ -220,22 +223,33 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
   L.R = min(d, L.r0 + a.rows_per_cta) - L.r0;
 
   // ---- selection helpers (warp 0)
+  // lane-parallel (lane q = pick q): residence, compaction of the resident
+  // picks in pick order, weights w_q = wsrc[sel_q] / sum_q' wsrc[sel_q']
+  // (summed in pick order, like the reference renormalisation)
   auto finish_selection = [&](const float* wsrc) {
-    if (lane == 0) {
-      int ne = 0;
-      for (int q = 0; q < k; ++q) {
-        s.fast[q] = s.fast_row[s.sel[q]] ? 1 : 0;
-        if (s.fast[q]) {
-          s.base[ne] = a.slab + static_cast<int64_t>(s.slot[s.sel[q]]) * a.slot_stride;
-          s.exec_q[ne++] = q;
-        }
+    __syncwarp();
+    int e = 0, slot = 0;
+    bool f = false;
+    if (lane < k) {
+      e = s.sel[lane];
+      f = s.fast_row[e] != 0;
+      slot = s.slot[e];
+    }
+    const unsigned fm = __ballot_sync(0xffffffffu, lane < k && f);
+    if (lane < k) {
+      s.fast[lane] = f ? 1 : 0;
+      if (f) {
+        const int pos = __popc(fm & ((1u << lane) - 1u));
+        s.base[pos] = a.slab + static_cast<int64_t>(slot) * a.slot_stride;
+        s.exec_q[pos] = lane;
       }
-      s.n_exec = ne;
-      if (wsrc) {
-        float den = 0.f;
-        for (int q = 0; q < k; ++q) den += wsrc[s.sel[q]];
-        for (int q = 0; q < k; ++q) s.wsel[q] = wsrc[s.sel[q]] / den;
-      }
+    }
+    if (lane == 0) s.n_exec = __popc(fm);
+    if (wsrc) {
+      const float v = lane < k ? wsrc[e] : 0.f;
+      float den = 0.f;
+      for (int q = 0; q < k; ++q) den += __shfl_sync(0xffffffffu, v, q);
+      if (lane < k) s.wsel[lane] = v / den;
     }
     __syncwarp();
   };
@@ -245,12 +259,14 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
   const uint64_t pol = l2_evict_first_policy();
   int issued = 0, iss_phase = 1, iss_u = 0, iss_q = 0;
   bool have_unit = false;
+  bool first_ticket = true;  // the first phase-1 ticket is the warp index (no smem atomic)
   auto next_piece = [&](Piece& pc) {
     pc.kind = 0;
     if (iss_phase == 1) {
       if (!have_unit) {
         int m = 0;
-        if (lane == 0) m = atomicAdd(&s.p1_next, 1);
+        if (lane == 0) m = first_ticket ? warp : atomicAdd(&s.p1_next, 1);
+        first_ticket = false;
         m = __shfl_sync(0xffffffffu, m, 0);
         if (m < L.n1c) {
           iss_u = L.cta + m * L.G;
@@ -387,9 +403,8 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
         mode0 ? gp_s : (pred_row ? a.wg_next + static_cast<size_t>(blockIdx.x) * d : a.wg));
     const int cpw = (n16 + DW - 1) / DW;
     const int c1 = min(n16, (warp + 1) * cpw);
-    float acc[DE_FAST], accp = 0.f;
-#pragma unroll
-    for (int e = 0; e < DE_FAST; ++e) acc[e] = 0.f;
+    // x for this warp's chunks first (h + gamma have landed; the gate rows
+    // may still be in flight)
     for (int c = warp * cpw + lane; c < c1; c += 32) {
       const float4 u = hsrc[2 * c], v = hsrc[2 * c + 1];
       const uint4 gm = gmsrc[c];
@@ -401,21 +416,60 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
                           (static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.y, r), bf16hi(gm.z)))) << 16);
       const uint32_t x3 = static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.z, r), bf16lo(gm.w)))) |
                           (static_cast<uint32_t>(f32_to_bf16_bits(__fmul_rn(__fmul_rn(v.w, r), bf16hi(gm.w)))) << 16);
-      const uint4 x8 = make_uint4(x0, x1, x2, x3);
-      reinterpret_cast<uint4*>(x_s)[c] = x8;
+      reinterpret_cast<uint4*>(x_s)[c] = make_uint4(x0, x1, x2, x3);
+    }
+    if (mode0) mbar_wait(&s.in_bar2, 0);
+    // partial logits: 16 slots = the E <= 16 gate rows, the next-layer row in
+    // slot 15 when E < 16 (else reduced separately)
+    float v16[16];
 #pragma unroll
-      for (int e = 0; e < DE_FAST; ++e)
-        if (e < E) acc[e] = dot8(x8, reinterpret_cast<const uint4*>(gsrc + static_cast<size_t>(e) * d)[c], acc[e]);
+    for (int e = 0; e < 16; ++e) v16[e] = 0.f;
+    float accp = 0.f;
+    const bool pred_in_slot = pred_row && E < 16;
+    for (int c = warp * cpw + lane; c < c1; c += 32) {
+      const uint4 x8 = reinterpret_cast<const uint4*>(x_s)[c];
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (e < E) v16[e] = dot8(x8, reinterpret_cast<const uint4*>(gsrc + static_cast<size_t>(e) * d)[c], v16[e]);
       if (pred_row) accp = dot8(x8, gpsrc[c], accp);
     }
+    if (pred_in_slot) v16[15] = accp;
+    // reduce-scatter over the warp: 8 + 4 + 2 + 1 + 1 shuffles leave the warp
+    // sum of slot (lane >> 1) on lanes 2i and 2i+1
 #pragma unroll
-    for (int e = 0; e < DE_FAST; ++e) {
-      if (e < E) {
-        const float zz = warp_sum(acc[e]);
-        if (lane == 0) s.zpart[warp][e] = zz;
-      }
+    for (int i = 0; i < 8; ++i) {
+      const bool hi = lane & 16;
+      const float send = hi ? v16[i] : v16[i + 8];
+      const float keep = hi ? v16[i + 8] : v16[i];
+      v16[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    if (pred_row) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool hi = lane & 8;
+      const float send = hi ? v16[i] : v16[i + 4];
+      const float keep = hi ? v16[i + 4] : v16[i];
+      v16[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const bool hi = lane & 4;
+      const float send = hi ? v16[i] : v16[i + 2];
+      const float keep = hi ? v16[i + 2] : v16[i];
+      v16[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    {
+      const bool hi = lane & 2;
+      const float send = hi ? v16[0] : v16[1];
+      const float keep = hi ? v16[1] : v16[0];
+      v16[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      v16[0] += __shfl_xor_sync(0xffffffffu, v16[0], 1);
+    }
+    const int slot16 = lane >> 1;
+    if ((lane & 1) == 0) {
+      if (slot16 < E) s.zpart[warp][slot16] = v16[0];
+      if (pred_in_slot && slot16 == 15) s.zpp[warp] = v16[0];
+    }
+    if (pred_row && !pred_in_slot) {
       const float zz = warp_sum(accp);
       if (lane == 0) s.zpp[warp] = zz;
     }
@@ -427,13 +481,17 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
     float z = 0.f;
     if (lane < E)
       for (int w = 0; w < DW; ++w) z += s.zpart[w][lane];
+    if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][7] = gtimer();
     const float p = lane_softmax(z);
     if (lane < E) s.p[lane] = p;  // identical values from every warp
+    if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][9] = gtimer();
     if (mode0) {
       lane_topk(p);
       if (lane == 0) s.nd = 0;
       __syncwarp();
+      if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][10] = gtimer();
       finish_selection(s.p);
+      if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][11] = gtimer();
       start_stream();
     } else if (!a.weights_from_pred) {
       finish_selection(s.p);

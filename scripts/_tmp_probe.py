@@ -19,5 +19,5 @@ torch.cuda.synchronize()
 _lib.call("daop_decode_timeline", 0, tlb.ctypes.data, 148)
 t = tlb.astype(np.int64)
 rel = (t[:, :12] - t[:, :1])
-for i, nm in enumerate(["start", "phase0 end", "ph1", "act", "end", "rms", "x+gates", "-", "sel+stream", "-", "-", "-"]):
+for i, nm in enumerate(["start", "phase0 end", "ph1", "act", "end", "rms", "x+gates", "z summed", "sel+stream", "softmax", "topk", "finish_sel"]):
     print(f"  {nm:10s} median {np.median(rel[:, i]):10.0f} cycles")
