@@ -20,6 +20,8 @@ daop.py.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import ops
@@ -40,7 +42,8 @@ class MoEBlockEngine:
 
     # ------------------------------------------------------------ decode
     def decode(self, h: torch.Tensor, layer: int = 0, *, pred_prev=None, mode: int = 0,
-               graceful: bool = True, weights_from_pred: bool = False, variant: int = 0):
+               graceful: bool = True, weights_from_pred: bool = False, variant: int = 0,
+               h_out=None, sel_out=None):
         """One decode token (h: (d,) fp32 on device) through MoE layer `layer`.
         mode 0 selects by the layer's own gate (true top-k), mode 1 by the DAOP
         plan on `pred_prev` (the prediction carried on layer-1)."""
@@ -49,36 +52,34 @@ class MoEBlockEngine:
         return ops.decode_layer(h, m.norm[layer], m.gate[layer], nxt, m.fast[layer],
                                 m.slot_of[layer], m.slab, m.slot_elems, self.d, self.ffn, self.k,
                                 self.bufs, pred_prev=pred_prev, mode=mode, graceful=graceful,
-                                weights_from_pred=weights_from_pred, variant=variant)
+                                weights_from_pred=weights_from_pred, variant=variant,
+                                h_out=h_out, sel_out=sel_out)
 
     def decode_host(self, h_host: torch.Tensor, layer: int = 0):
         """End-to-end call from host memory: h (d,) fp32 on the host -> device
-        -> decode -> (h_out, selected experts) back in pinned host memory.
+        -> decode -> (h_out, selected experts) in pinned host memory.
 
-        The step is one CUDA graph per layer (captured on first use): H2D copy
-        from a pinned staging buffer, the decode launch, D2H copies of the
-        residual and the selection.  The caller's h is copied into the staging
-        buffer on the host, so any host tensor works; the residual and the
-        selection come back in one D2H copy; one replay + one
-        synchronize per call keeps the host overhead at a few microseconds."""
+        The step is one CUDA graph per layer (captured on first use): the H2D
+        copy of h from a pinned staging buffer, then the decode launch, which
+        writes the residual and the selection straight into pinned host memory
+        over the bus (no D2H copy node).  The caller's h is copied into the
+        staging buffer on the host; one replay + one synchronize per call."""
         if self._out_host is None:
-            b = self.bufs
             self._h_host = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
-            self._io_host = torch.empty(b.meta.numel() - b.io_offset, dtype=torch.uint8,
-                                        pin_memory=True)
-            so = b.offsets["sel"] - b.io_offset
-            ho = b.offsets["h_out"] - b.io_offset
-            self._sel_host = self._io_host[so: so + 4 * self.k].view(torch.int32)
-            self._out_host = self._io_host[ho: ho + 4 * self.d].view(torch.float32)
+            self._out_host = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
+            self._sel_host = torch.empty(self.k, dtype=torch.int32, pin_memory=True)
             self._host_graphs = {}
         if h_host.data_ptr() != self._h_host.data_ptr():
-            self._h_host.copy_(h_host)
+            if h_host.device.type == "cpu" and h_host.dtype == torch.float32 and \
+                    h_host.is_contiguous() and h_host.numel() == self.d:
+                ctypes.memmove(self._h_host.data_ptr(), h_host.data_ptr(), 4 * self.d)
+            else:
+                self._h_host.copy_(h_host)
         g = self._host_graphs.get(layer)
         if g is None:
             def step():
                 self._h_dev.copy_(self._h_host, non_blocking=True)
-                self.decode(self._h_dev, layer)
-                self._io_host.copy_(self.bufs.meta[self.bufs.io_offset:], non_blocking=True)
+                self.decode(self._h_dev, layer, h_out=self._out_host, sel_out=self._sel_host)
 
             side = torch.cuda.Stream(self.device)
             side.wait_stream(torch.cuda.current_stream())
@@ -96,9 +97,9 @@ class MoEBlockEngine:
 
     @staticmethod
     def host_bytes(d: int, k: int):
-        """(h2d, d2h) bytes of one decode_host call: h in; the selection
-        (16-byte padded) and the residual out in one copy."""
-        return d * 4, (k * 4 + 15) // 16 * 16 + d * 4
+        """(h2d, d2h) bytes of one decode_host call: h in; the residual and
+        the selection written to host memory by the kernel."""
+        return d * 4, d * 4 + k * 4
 
     # ------------------------------------------------------------ full decode token
     def decode_token(self, h: torch.Tensor, *, start: int = 4, daop: bool = True,

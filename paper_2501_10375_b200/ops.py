@@ -168,14 +168,23 @@ class DecodeBuffers:
 
 def decode_layer(h, gamma, wg, wg_next, fast_row, slot_of, slab, slot_elems, d, ffn, k,
                  bufs: DecodeBuffers, *, pred_prev=None, mode=0, graceful=True,
-                 weights_from_pred=False, variant=0, eps=RMS_EPS):
-    """One decode token through one MoE layer in a single launch."""
+                 weights_from_pred=False, variant=0, eps=RMS_EPS, h_out=None, sel_out=None):
+    """One decode token through one MoE layer in a single launch.
+
+    h_out / sel_out (optional) redirect the residual and the selection to
+    other buffers -- e.g. pinned host memory, which the kernel then writes
+    directly over the bus (the end-to-end call needs no D2H copy)."""
     _dev(h, gamma, wg, wg_next, pred_prev, fast_row, slot_of, slab)
+    for t in (h_out, sel_out):
+        if t is not None and not (t.is_cuda or t.is_pinned()):
+            raise DeviceError("h_out / sel_out must be device or pinned host memory")
     e = wg.shape[0]
     _lib.call("daop_decode_layer", h.data_ptr(), gamma.data_ptr(), wg.data_ptr(), _p(wg_next),
               _p(pred_prev), fast_row.data_ptr(), slot_of.data_ptr(), slab.data_ptr(),
               slot_elems, d, ffn, e, k, mode, int(graceful), int(weights_from_pred), float(eps),
-              bufs.x.data_ptr(), bufs.p.data_ptr(), bufs.p_pred.data_ptr(), bufs.sel.data_ptr(),
+              bufs.x.data_ptr(), bufs.p.data_ptr(), bufs.p_pred.data_ptr(),
+              (bufs.sel if sel_out is None else sel_out).data_ptr(),
               bufs.w.data_ptr(), bufs.is_fast.data_ptr(), bufs.deg.data_ptr(),
-              bufs.y.data_ptr(), bufs.h_out.data_ptr(), bufs.ws.data_ptr(), variant, _s())
+              bufs.y.data_ptr(), (bufs.h_out if h_out is None else h_out).data_ptr(),
+              bufs.ws.data_ptr(), variant, _s())
     return bufs
