@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
     mbar_init(&s.in_bar2, 1);
     s.p1_next = DW;  // tickets 0..DW-1 are taken statically by the warps' first units
     s.p2_next = s.fin = 0;
+    *reinterpret_cast<int*>(&s.zpart[1][0]) = 0;  // lazy-gates counter (zpart unused then)
     fence_mbar_init();
     if (a.mode == 0) {  // h + gamma (RMSNorm starts on them), then the gate rows
       mbar_arrive_expect_tx(&s.in_bar, d * 4 + d * 2);
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
     for (int q = 0; q < DS; ++q) issue_next();
   };
 
+
   // ---- lane-parallel softmax / top-k over E <= 16 experts: shuffles span only
   // the next power of two >= E; ties resolve to the lower id (topk_scan order)
   int P2 = 1;
@@ -391,6 +393,11 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
   // and the slice's partial dot products with the E gate rows (+ this CTA's
   // next-layer gate row); partials are summed over warps in fixed order
   const bool mode0 = a.mode == 0;
+  // PLAN mode with prediction weights: the selection and the weights are
+  // known, so the gate logits are off the critical path -- only CTA 0 (the
+  // exported p_true) and the CTAs owning a next-layer row compute them, after
+  // x, from L2, while the other warps already consume the weight stream
+  const bool lazy_gates = a.mode == 1 && a.weights_from_pred;
   const int n16 = d / 8;
   {
     float tot = 0.f;
@@ -419,6 +426,7 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
       reinterpret_cast<uint4*>(x_s)[c] = make_uint4(x0, x1, x2, x3);
     }
     if (mode0) mbar_wait(&s.in_bar2, 0);
+    if (!lazy_gates) {
     // partial logits: 16 slots = the E <= 16 gate rows, the next-layer row in
     // slot 15 when E < 16 (else reduced separately)
     float v16[16];
@@ -473,11 +481,35 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
       const float zz = warp_sum(accp);
       if (lane == 0) s.zpp[warp] = zz;
     }
+    }  // !lazy_gates
   }
   __syncthreads();  // x complete in smem, partial logits visible
   if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][6] = gtimer();
+  if (lazy_gates && blockIdx.x == 0 && warp < E) {
+    // zpart is not used in this mode: row 0 holds the logits, [1][0] the count
+    float* zfull = s.zpart[0];
+    int* zdone = reinterpret_cast<int*>(&s.zpart[1][0]);
+    // warp e: logit e over the full d (fixed lane-strided order + warp sum)
+    const float z = warp_sum(dot_piece(reinterpret_cast<const uint4*>(a.wg + static_cast<size_t>(warp) * d),
+                                       reinterpret_cast<const uint4*>(x_s), n16, lane, 0.f));
+    if (lane == 0) {
+      zfull[warp] = z;
+      __threadfence_block();
+      atomicAdd(zdone, 1);
+    }
+    if (warp == 0) {
+      if (lane == 0)
+        while (*reinterpret_cast<volatile int*>(zdone) < E) {
+        }
+      __syncwarp();
+      __threadfence_block();
+      const float p = lane_softmax(lane < E ? zfull[lane] : 0.f);
+      if (lane < E) s.p[lane] = p;
+      __syncwarp();
+    }
+  }
   // ---- every warp: logits (fixed warp order) -> softmax -> selection -> stream
-  {
+  if (!lazy_gates) {
     float z = 0.f;
     if (lane < E)
       for (int w = 0; w < DW; ++w) z += s.zpart[w][lane];
@@ -499,9 +531,14 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
   }
   if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][8] = gtimer();
   if (pred_row && warp == DW - 1) {  // this CTA's next-layer row -> grid-wide p_pred
+    float zl = 0.f;
+    if (lazy_gates)
+      zl = warp_sum(dot_piece(reinterpret_cast<const uint4*>(a.wg_next + static_cast<size_t>(blockIdx.x) * d),
+                              reinterpret_cast<const uint4*>(x_s), n16, lane, 0.f));
     if (lane == 0) {
-      float zp = 0.f;
-      for (int w = 0; w < DW; ++w) zp += s.zpp[w];
+      float zp = zl;
+      if (!lazy_gates)
+        for (int w = 0; w < DW; ++w) zp += s.zpp[w];
       a.pred_logits[blockIdx.x] = zp;
       __threadfence();
       s.pred_last = atomicAdd(a.ctr + 1, 1u) == static_cast<unsigned>(E) - 1;

@@ -23,13 +23,18 @@ if what in ("decode", "all"):
     hs = [m.input_hidden(1, stream=9, step=i)[0] for i in range(16)]
     it = [0]
     var = [0]
+    mode = [0]
+    pp = torch.softmax(torch.randn(E, device="cuda"), 0)
     def step():
         ops.decode_layer(hs[it[0] % 16], m.norm[0], m.gate[0], m.gate[1], m.fast[0], m.slot_of[0],
-                         m.slab, m.slot_elems, d, ffn, k, bufs, variant=var[0])
+                         m.slab, m.slot_elems, d, ffn, k, bufs, variant=var[0],
+                         mode=mode[0], pred_prev=pp if mode[0] else None,
+                         weights_from_pred=bool(mode[0]))
         it[0] += 1
     from paper_2501_10375_b200 import _lib
-    for v in (0, 9, 7):
+    for v, md in ((0, 0), (0, 1), (9, 1)):
         var[0] = v
+        mode[0] = md
         try:
             ms = ev_time(step, iters=200, warm=10)
         except Exception as exc:  # noqa: BLE001
@@ -43,7 +48,7 @@ if what in ("decode", "all"):
         t = tlb.astype(np.int64)
         rel = (t - t[:, :1]) / 1.9e3   # SM cycles relative to each CTA's start, ~us at 1.9 GHz
         ph = {nm: np.median(rel[:, i]) for i, nm in ((1, "ph0"), (2, "ph1"), (3, "act"), (4, "end"))}
-        print(f"decode_layer variant={v}: {ms*1e3:.1f} us  {b/ms/1e6:.1f} GB/s  phase ends (us, median CTA): "
+        print(f"decode_layer mode={md} variant={v}: {ms*1e3:.1f} us  {b/ms/1e6:.1f} GB/s  phase ends (us, median CTA): "
               + " ".join(f"{k} {x:.1f}" for k, x in ph.items()) + f"  max end {rel[:, 4].max():.1f}",
               flush=True)
 if what in ("prefill", "all"):
