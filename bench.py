@@ -28,6 +28,11 @@ own algorithm restated in oracle/ is the arm).
 With N > 1 (torchrun) every rank runs the same decode on its own GPU as an
 independent replica (weak scaling; decode b=1 touches 2 experts, so expert
 parallelism cannot speed up a single token -- DESIGN.md §7).
+
+  ep        BASELINE configs[4]: a Mixtral-8x22B-shaped layer, prefill of
+            8 x 4096 tokens sharded over the N ranks, experts sharded E/N per
+            rank, expert-parallel with NCCL over NVLink (strong scaling; at
+            N = 1 the same path without a collective)
 """
 
 from __future__ import annotations
@@ -325,6 +330,16 @@ def run_b200(args, world, rank, local_rank):
         }
         del hp
 
+    # -------- expert parallelism (BASELINE configs[4]: Mixtral-8x22B shape)
+    ep = None
+    if not args.no_ep:
+        del eng, model
+        torch.cuda.empty_cache()
+        try:
+            ep = run_ep(args, world, rank, dev, tf_sus, barrier)
+        except Exception as exc:  # keep the headline line if this section fails
+            ep = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # -------- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -362,8 +377,71 @@ def run_b200(args, world, rank, local_rank):
         "clocks": clocks,
         "prefill": prefill,
         "decode32": decode32,
+        "ep": ep,
     }
     return line
+
+
+EP_D, EP_FFN, EP_TOKENS = 6144, 16384, 8 * 4096
+
+
+def run_ep(args, world, rank, dev, tf_sus, barrier):
+    """Mixtral-8x22B-shaped MoE layer (d=6144, ffn=16384, E=8, top-2),
+    prefill 8 x 4096 tokens sharded T/G per rank, experts sharded E/G per
+    rank, expert-parallel over the ranks (ep.py: fused router + permutation
+    -> count all_to_all -> NCCL grouped send/recv into an expert-major
+    receive buffer -> tcgen05 grouped GEMMs -> send/recv back -> combine).
+    Total work is fixed as G grows (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.ep import ep_model, gpu_ep_layer
+
+    if world > 1 and not dist.is_initialized():
+        return None
+    t_local = EP_TOKENS // world
+    m = ep_model(P.ModelShape(2, E, K), EP_D, EP_FFN, rank, world, seed=0, device=dev)
+    h = m.input_hidden(t_local, stream=300 + rank)
+    for _ in range(2):
+        gpu_ep_layer(m, 0, h)
+    barrier()
+    torch.cuda.synchronize()
+    kp = 5
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phases = []
+    e0.record(stream)
+    for i in range(kp):
+        out, sel, w, plan = gpu_ep_layer(m, 0, h, timings=phases if i == kp - 1 else None)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / kp
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    split = {}
+    for (_, a), (name, b) in zip(phases, phases[1:]):
+        split[name] = a.elapsed_time(b)
+    flops = 2.0 * K * EP_TOKENS * 3 * EP_D * EP_FFN
+    sent = sum(n for e, (_, n) in enumerate(plan.send) if e * world // E != rank)
+    return {
+        "workload": f"Mixtral-8x22B-shaped layer (d={EP_D}, ffn={EP_FFN}, E={E}, top-{K}), "
+                    f"prefill {EP_TOKENS} tokens sharded {t_local}/rank, expert-parallel "
+                    f"over {world} GPU(s) (BASELINE configs[4])",
+        "value": EP_TOKENS / (ms / 1e3), "unit": "tokens/s", "ms_per_layer": ms,
+        "scaling": "strong", "experts_per_gpu": E // world,
+        "collective": "nccl all_to_all (counts) + grouped send/recv (payload, outputs)"
+                      if world > 1 else "none (G=1)",
+        "rank0_phase_ms": split,
+        "rank0_rows_sent": sent, "rank0_payload_bytes_sent": sent * EP_D * 2,
+        "roofline": {"bound": "tensor", "achieved_per_gpu": flops / world / (ms / 1e3) / 1e12,
+                     "peak": tf_sus, "unit": "TFLOP/s",
+                     "frac": flops / world / (ms / 1e3) / 1e12 / tf_sus,
+                     "flops_per_layer": flops},
+    }
 
 
 def main():
@@ -375,6 +453,7 @@ def main():
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode32", action="store_true")
+    ap.add_argument("--no-ep", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

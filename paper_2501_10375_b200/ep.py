@@ -1,24 +1,38 @@
 """Expert parallelism over several GPUs.
 
 Experts are independent units: expert e of every layer lives on rank
-owner(e) = floor(e * G / E); tokens are sharded data-parallel.  One MoE layer:
+owner(e) = floor(e * G / E) (E/G consecutive experts per rank); tokens are
+sharded data-parallel.  One MoE layer on rank r:
 
   1. router on the rank's own tokens (fused router kernel): x, top-k, weights
-  2. assignments (t, j) sorted stably by (owner, expert, t, j)
-  3. count exchange (all_to_all of G ints), then payload all_to_all of the
-     bf16 x rows and their expert ids with those split sizes
-  4. the owner runs its local experts on what it received (permutation +
-     tcgen05 grouped GEMMs on its slab)
-  5. reverse all_to_all of the fp32 expert outputs
-  6. combine on the token's rank: h' = h + sum_j w_j y_j in fixed j order
+  2. stable permutation by (expert, t, j) -- the same histogram + scan +
+     scatter + gather kernels as the single-GPU prefill.  owner() is monotone
+     in e, so x_perm is already grouped by destination rank: it IS the send
+     buffer, segment e = rows [offsets[e], offsets[e+1])
+  3. count exchange: all_to_all of the (G, E/G) per-expert counts, so every
+     owner knows how many rows of each of its experts each source sends
+  4. payload exchange as one batch of point-to-point transfers (NCCL groups
+     them into a single launch, like all_to_all): source segment (src, e)
+     lands in the owner's receive buffer at an EXPERT-MAJOR position
+     (expert, then source rank), so the received rows are already grouped by
+     expert and the tcgen05 grouped GEMMs run on them directly (no re-permute)
+  5. up / down grouped GEMMs on the owner's slab (offsets over all E experts,
+     zero rows for non-local experts)
+  6. reverse exchange of the fp32 expert outputs straight into the source's
+     permuted order, then the fixed-order combine kernel with the
+     permutation's inverse -- the single-GPU combine, unchanged
 
 Row results of the expert GEMMs do not depend on which other rows share a
-tile, so the EP output equals the single-GPU output.  The collectives are
-NCCL (NVLink/NVSwitch) on GPUs and gloo in the CPU tests; decisions are made
-before dispatch, so they are identical to the single-GPU decisions.
+tile, so the EP output equals the single-GPU output bit for bit.  Decisions
+are made before dispatch, so they are identical too.  The collectives are
+NCCL over NVLink/NVSwitch on GPUs; the CPU tests run the same exchange over
+gloo (world size 2) with the oracle's permutation / experts / combine
+injected -- this module does no arithmetic of its own.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
@@ -32,56 +46,165 @@ def local_experts(rank: int, num_experts: int, world: int):
     return [e for e in range(num_experts) if (e * world) // num_experts == rank]
 
 
-def ep_moe_layer(h: torch.Tensor, router_fn, expert_fn, num_experts: int, k: int,
-                 group=None):
-    """One expert-parallel MoE layer.
+@dataclass
+class ExchangePlan:
+    """Row segments of one layer's dispatch on one rank (host integers).
 
-    router_fn(h) -> (x, sel, w): x (T, d) rows fed to experts, sel (T, k)
-      int64 expert ids, w (T, k) fp32 combine weights.
-    expert_fn(expert_ids (R,), x_rows (R, d)) -> (R, d) fp32 outputs of this
-      rank's local experts.
-    Returns (h', sel, w).
-    """
-    G = dist.get_world_size(group)
-    T, d = h.shape
+    send[e] = (start, rows) of expert e in this rank's permuted buffer;
+    recv[(src, e)] = (start, rows) of source src's rows of local expert e in
+    the expert-major receive buffer; local_offsets (E+1) = row offsets of
+    every expert in the receive buffer (zero rows for non-local experts)."""
+    rank: int
+    world: int
+    num_experts: int
+    send: list
+    recv: dict
+    local_offsets: list
+    recv_rows: int
+
+
+def plan_exchange(send_offsets, recv_counts, rank: int, world: int,
+                  num_experts: int) -> ExchangePlan:
+    """send_offsets: (E+1) host ints of the permuted buffer; recv_counts:
+    (G, E/G) host ints, recv_counts[src][i] = rows of local expert i from src."""
+    E, G = num_experts, world
+    per = E // G
+    send = [(int(send_offsets[e]), int(send_offsets[e + 1] - send_offsets[e])) for e in range(E)]
+    mine = local_experts(rank, E, G)
+    recv, local = {}, [0] * (E + 1)
+    pos = 0
+    for e in range(E):
+        local[e] = pos
+        if e in mine:
+            i = e - mine[0]
+            for src in range(G):
+                n = int(recv_counts[src][i])
+                recv[(src, e)] = (pos, n)
+                pos += n
+    local[E] = pos
+    assert per * G == E
+    return ExchangePlan(rank, G, E, send, recv, local, pos)
+
+
+def _p2p(ops_list, group):
+    if ops_list:
+        for req in dist.batch_isend_irecv(ops_list):
+            req.wait()
+
+
+def dispatch(plan: ExchangePlan, x_perm: torch.Tensor, group=None) -> torch.Tensor:
+    """Source-permuted rows -> owner's expert-major receive buffer."""
+    E, G, r = plan.num_experts, plan.world, plan.rank
+    if G == 1:
+        return x_perm
+    out = torch.empty((plan.recv_rows,) + tuple(x_perm.shape[1:]), dtype=x_perm.dtype,
+                      device=x_perm.device)
+    ops_list = []
+    for e in range(E):  # sends in expert order; each owner receives in the same order
+        dst = e * G // E
+        a, n = plan.send[e]
+        if n and dst != r:
+            ops_list.append(dist.P2POp(dist.isend, x_perm[a:a + n], _peer(dst, group), group))
+    for (src, e), (a, n) in sorted(plan.recv.items(), key=lambda kv: (kv[0][1], kv[0][0])):
+        if not n:
+            continue
+        if src == r:
+            s, _ = plan.send[e]
+            out[a:a + n].copy_(x_perm[s:s + n])
+        else:
+            ops_list.append(dist.P2POp(dist.irecv, out[a:a + n], _peer(src, group), group))
+    _p2p(ops_list, group)
+    return out
+
+
+def gather_back(plan: ExchangePlan, y_recv: torch.Tensor, group=None) -> torch.Tensor:
+    """Owner's expert-major outputs -> source's permuted order."""
+    E, G, r = plan.num_experts, plan.world, plan.rank
+    if G == 1:
+        return y_recv
+    rows = plan.send[-1][0] + plan.send[-1][1] if plan.send else 0
+    out = torch.empty((rows,) + tuple(y_recv.shape[1:]), dtype=y_recv.dtype,
+                      device=y_recv.device)
+    ops_list = []
+    for (src, e), (a, n) in sorted(plan.recv.items(), key=lambda kv: (kv[0][1], kv[0][0])):
+        if n and src != r:
+            ops_list.append(dist.P2POp(dist.isend, y_recv[a:a + n], _peer(src, group), group))
+    for e in range(E):
+        owner = e * G // E
+        s, n = plan.send[e]
+        if not n:
+            continue
+        if owner == r:
+            a, _ = plan.recv[(r, e)]
+            out[s:s + n].copy_(y_recv[a:a + n])
+        else:
+            ops_list.append(dist.P2POp(dist.irecv, out[s:s + n], _peer(owner, group), group))
+    _p2p(ops_list, group)
+    return out
+
+
+def _peer(rank_in_group, group):
+    return rank_in_group if group is None else dist.get_global_rank(group, rank_in_group)
+
+
+def exchange_counts(send_offsets: torch.Tensor, world: int, group=None):
+    """all_to_all of per-expert row counts: returns (G, E/G) host ints."""
+    counts = (send_offsets[1:] - send_offsets[:-1]).to(torch.int64)
+    E = counts.numel()
+    if world == 1:
+        return counts.view(1, E).tolist()
+    recv = torch.empty_like(counts)
+    dist.all_to_all_single(recv, counts, group=group)
+    return recv.view(world, E // world).tolist()
+
+
+def ep_moe_layer(h: torch.Tensor, router_fn, permute_fn, expert_fn, combine_fn,
+                 num_experts: int, group=None, timings=None):
+    """One expert-parallel MoE layer on this rank's tokens h (T, d).
+
+    router_fn(h) -> (x (T,d), sel (T,k), w (T,k))
+    permute_fn(sel, x) -> (offsets (E+1), x_perm (T*k, d), inv (T,k))
+    expert_fn(x_recv (R,d), local_offsets (E+1) host ints) -> (R, d) fp32
+      outputs of this rank's experts, rows grouped by expert
+    combine_fn(h, y_perm, inv, w) -> h'
+    Returns (h', sel, w, plan).  `timings` (optional list) receives
+    (name, event) pairs around the phases when h is on a GPU."""
+    if dist.is_available() and dist.is_initialized():
+        G, r = dist.get_world_size(group), dist.get_rank(group)
+    else:  # one GPU, no process group: the same path without a collective
+        G, r = 1, 0
+    mark = _marker(h, timings)
     x, sel, w = router_fn(h)
-    sel = sel.to(torch.int64)
-    flat_e = sel.reshape(-1)
-    dest = owner_of(flat_e, num_experts, G)
-    order = torch.argsort(dest * num_experts + flat_e, stable=True)
-    send_counts = torch.bincount(dest, minlength=G).to(torch.int64)
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
-    s_split = send_counts.tolist()
-    r_split = recv_counts.tolist()
-    send_x = x[order // k].contiguous()
-    send_e = flat_e[order].contiguous()
-    R = int(sum(r_split))
-    recv_x = torch.empty((R, x.shape[1]), dtype=x.dtype, device=x.device)
-    recv_e = torch.empty((R,), dtype=send_e.dtype, device=send_e.device)
-    _a2a(recv_x, send_x, r_split, s_split, group)
-    _a2a(recv_e, send_e, r_split, s_split, group)
-    y_recv = expert_fn(recv_e, recv_x).to(torch.float32).contiguous()
-    y_back = torch.empty((T * k, d), dtype=torch.float32, device=h.device)
-    _a2a(y_back, y_recv, s_split, r_split, group)
-    y = torch.empty_like(y_back)
-    y[order] = y_back
-    if h.is_cuda:
-        # same fixed-order fused combine kernel as the single-GPU path
-        from . import ops
-        inv = torch.arange(T * k, dtype=torch.int32, device=h.device).view(T, k)
-        out = ops.combine(h.to(torch.float32).contiguous(), y, inv,
-                          w.to(torch.float32).contiguous())
-        return out, sel, w
-    y = y.view(T, k, d)
-    out = h.to(torch.float32).clone()
-    for j in range(k):
-        out = out + w[:, j:j + 1].to(torch.float32) * y[:, j]
-    return out, sel, w
+    offsets, x_perm, inv = permute_fn(sel, x)
+    mark("route+permute")
+    recv_counts = exchange_counts(offsets, G, group)
+    plan = plan_exchange(offsets.tolist(), recv_counts, r, G, num_experts)
+    x_recv = dispatch(plan, x_perm, group)
+    mark("dispatch")
+    y_recv = expert_fn(x_recv, plan.local_offsets)
+    mark("experts")
+    y_perm = gather_back(plan, y_recv, group)
+    mark("gather")
+    out = combine_fn(h, y_perm, inv, w)
+    mark("combine")
+    return out, sel, w, plan
 
 
-def _a2a(out, inp, out_split, in_split, group):
-    dist.all_to_all_single(out, inp, out_split, in_split, group=group)
+def _marker(h, timings):
+    if timings is None or not h.is_cuda:
+        return lambda name: None
+    ev = torch.cuda.Event(enable_timing=True)
+    ev.record()
+    timings.append(("start", ev))
+
+    def mark(name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        timings.append((name, e))
+    return mark
+
+
+# ------------------------------------------------------------------ GPU functions
 
 
 def gpu_router_fn(model, layer: int):
@@ -91,26 +214,64 @@ def gpu_router_fn(model, layer: int):
     def fn(h):
         nxt = model.gate[layer + 1] if layer + 1 < model.shape.num_layers else None
         r = ops.router(h, model.norm[layer], model.gate[layer], nxt, model.shape.top_k)
-        return r["x"], r["topk_idx"].to(torch.int64), r["topk_w"]
+        return r["x"], r["topk_idx"], r["topk_w"]
+
+    return fn
+
+
+def gpu_permute_fn(num_experts: int):
+    from . import ops
+
+    def fn(sel, x):
+        pr = ops.permute(sel, num_experts, x)
+        return pr["offsets"], pr["x_perm"], pr["inv"]
 
     return fn
 
 
 def gpu_expert_fn(model, layer: int):
-    """This rank's experts on received rows: permutation + tcgen05 grouped
-    GEMMs over the local slab (experts without a local slot get no tiles)."""
+    """This rank's experts on the expert-major receive buffer: tcgen05
+    grouped GEMMs over the local slab, no re-permutation."""
     from . import ops
 
-    def fn(expert_ids, x_rows):
-        if x_rows.shape[0] == 0:
-            return torch.empty((0, model.d), dtype=torch.float32, device=x_rows.device)
-        ids = expert_ids.to(torch.int32).view(-1, 1).contiguous()
-        pr = ops.permute(ids, model.shape.num_experts, x_rows.contiguous())
+    def fn(x_recv, local_offsets):
+        if x_recv.shape[0] == 0:
+            return torch.empty((0, model.d), dtype=torch.float32, device=x_recv.device)
+        off = torch.tensor(local_offsets, dtype=torch.int64).to(x_recv.device, non_blocking=True)
         so = model.slot_of[layer]
-        act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, model.slab, model.n_slots,
+        act = ops.expert_gemm_up(x_recv, off, so, model.slab, model.n_slots,
                                  model.slot_elems, model.d, model.ffn)
-        y = ops.expert_gemm_down(act, pr["offsets"], so, model.slab, model.n_slots,
-                                 model.slot_elems, model.d, model.ffn)
-        return y[pr["inv"].view(-1).to(torch.int64)]
+        return ops.expert_gemm_down(act, off, so, model.slab, model.n_slots,
+                                    model.slot_elems, model.d, model.ffn)
 
     return fn
+
+
+def gpu_combine_fn():
+    from . import ops
+
+    def fn(h, y_perm, inv, w):
+        return ops.combine(h, y_perm, inv, w)
+
+    return fn
+
+
+def gpu_ep_layer(model, layer: int, h: torch.Tensor, group=None, timings=None):
+    """EP MoE layer with every phase on the B200 path."""
+    return ep_moe_layer(h, gpu_router_fn(model, layer), gpu_permute_fn(model.shape.num_experts),
+                        gpu_expert_fn(model, layer), gpu_combine_fn(),
+                        model.shape.num_experts, group=group, timings=timings)
+
+
+def ep_model(shape, d_model: int, d_ff: int, rank: int, world: int, layers=(0,), seed: int = 0,
+             device="cuda"):
+    """A MoEModel holding only this rank's experts (E/G slots per layer)."""
+    from .model import MoEModel
+    E = shape.num_experts
+    mine = local_experts(rank, E, world)
+    m = MoEModel(shape, d_model, d_ff, seed=seed, device=device,
+                 n_slots=len(mine) * len(layers), resident_layers=[])
+    for l in layers:
+        for e in mine:
+            m.load_expert(l, e)
+    return m

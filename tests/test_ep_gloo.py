@@ -48,22 +48,33 @@ def _worker(rank, world, port, q):
         xb = torch.from_numpy(x).to(torch.bfloat16)
         return xb, torch.from_numpy(sel), torch.from_numpy(w)
 
-    def expert_fn(ids, xr):
+    def permute_fn(sel_t, x):
+        offsets, perm, inv = N.permutation(sel_t.numpy(), E)
+        return torch.from_numpy(offsets), x[torch.from_numpy(perm // K)], torch.from_numpy(inv)
+
+    def expert_fn(xr, local_offsets):
         out = np.zeros((xr.shape[0], D), dtype=np.float32)
         xs = xr.to(torch.float32).numpy()
-        for e in torch.unique(ids).tolist():
-            assert e in mine, f"rank {rank} received expert {e}"
-            rows = (ids == e).numpy()
-            out[rows] = N.expert_ffn(xs[rows], *W[e])
+        for e in range(E):
+            a, b = local_offsets[e], local_offsets[e + 1]
+            if b > a:
+                assert e in mine, f"rank {rank} received expert {e}"
+                out[a:b] = N.expert_ffn(xs[a:b], *W[e])
         return torch.from_numpy(out)
 
-    out, sel, w = ep_moe_layer(h, router_fn, expert_fn, E, K)
+    def combine_fn(hh, y_perm, inv, w):
+        return torch.from_numpy(N.combine(hh.numpy(), y_perm.numpy(), inv.numpy(), w.numpy()))
+
+    out, sel, w, plan = ep_moe_layer(h, router_fn, permute_fn, expert_fn, combine_fn, E)
+    # every row this rank sent came back, and the receive buffer is expert-major
+    assert plan.local_offsets[-1] == plan.recv_rows
+    assert sum(n for _, n in plan.send) == T_PER * K
     q.put((rank, out.numpy(), sel.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_ep_matches_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -94,3 +105,14 @@ def test_ownership_partition():
         assert sorted(sum(parts, [])) == list(range(8))
         assert all(len(p) == 8 // G for p in parts)
         assert owner_of(torch.arange(8), 8, G).tolist() == [e * G // 8 for e in range(8)]
+
+
+def test_plan_exchange_expert_major():
+    """Receive buffer groups rows by local expert, then by source rank."""
+    from paper_2501_10375_b200.ep import plan_exchange
+    # world 2, E 4: rank 1 owns experts 2, 3; sources send (5, 7) and (1, 0) rows
+    plan = plan_exchange([0, 3, 4, 9, 16], [[5, 7], [1, 0]], 1, 2, 4)
+    assert plan.send == [(0, 3), (3, 1), (4, 5), (9, 7)]
+    assert plan.recv == {(0, 2): (0, 5), (1, 2): (5, 1), (0, 3): (6, 7), (1, 3): (13, 0)}
+    assert plan.local_offsets == [0, 0, 0, 6, 13]
+    assert plan.recv_rows == 13

@@ -17,7 +17,7 @@ def test_ep_world1_equals_single_gpu():
     import torch.distributed as dist
     import paper_2501_10375_b200 as P
     from paper_2501_10375_b200.engine import MoEBlockEngine
-    from paper_2501_10375_b200.ep import ep_moe_layer, gpu_expert_fn, gpu_router_fn
+    from paper_2501_10375_b200.ep import ep_model, gpu_ep_layer
     from paper_2501_10375_b200.model import MoEModel
 
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -28,9 +28,14 @@ def test_ep_world1_equals_single_gpu():
         m = MoEModel(P.ModelShape(2, 8, 2), 512, 1024, seed=4, resident_layers=[0])
         h = m.input_hidden(300, stream=6)
         ref = MoEBlockEngine(m).prefill(h, 0)
-        out, sel, w = ep_moe_layer(h, gpu_router_fn(m, 0), gpu_expert_fn(m, 0), 8, 2)
+        out, sel, w, plan = gpu_ep_layer(m, 0, h)
         torch.cuda.synchronize()
-        assert torch.equal(sel, ref["topk_idx"].to(torch.int64))
+        assert torch.equal(sel, ref["topk_idx"])
         assert torch.equal(out, ref["out"])
+        assert plan.local_offsets == ref["offsets"].tolist()
+        # a rank model holding only its own experts (world 1: all of them)
+        me = ep_model(P.ModelShape(2, 8, 2), 512, 1024, 0, 1, seed=4)
+        out2, _, _, _ = gpu_ep_layer(me, 0, h)
+        assert torch.equal(out2, ref["out"])
     finally:
         dist.destroy_process_group()
