@@ -232,6 +232,48 @@ def run_b200(args, world, rank, local_rank):
     # reported beside it
     achieved = DECODE_BYTES / (ms_max / args.steps / 1e3) / 1e9
 
+    # -------- prefill (BASELINE configs[3]: 8 x 4096 tokens)
+    prefill = None
+    if not args.no_prefill:
+        T = PREFILL_SEQS * PREFILL_LEN
+        hp = model.input_hidden(T, stream=200 + rank)
+        hist = torch.zeros((PREFILL_SEQS, n_layers, E), dtype=torch.int32, device=dev)
+        for _ in range(2):
+            eng.prefill(hp, 0, hist=hist[:, 0], tokens_per_seq=PREFILL_LEN, hist_seq_stride=n_layers * E)
+        barrier()
+        torch.cuda.synchronize()
+        kp = max(3, min(10, args.steps // 200))
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) as pclk:
+            p0.record(stream)
+            for _ in range(kp):
+                eng.prefill(hp, 0, hist=hist[:, 0], tokens_per_seq=PREFILL_LEN,
+                            hist_seq_stride=n_layers * E)
+            p1.record(stream)
+            torch.cuda.synchronize()
+        pms = p0.elapsed_time(p1) / kp
+        tp = torch.tensor([pms], device=dev)
+        if world > 1:
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+        pms = float(tp.item())
+        flops = 2.0 * K * T * 3 * D * FFN
+        prefill = {
+            "workload": f"prefill {PREFILL_SEQS} x {PREFILL_LEN} tokens, one layer (BASELINE configs[3])",
+            "value": world * T / (pms / 1e3), "unit": "tokens/s", "ms_per_layer": pms,
+            # a prefill step is a long back-to-back run of tensor-core GEMMs
+            # (power-capped like cuBLAS's sustained run): the sustained
+            # measured peak is the denominator, the burst fraction is beside it
+            "roofline": {"bound": "tensor", "achieved": flops / (pms / 1e3) / 1e12,
+                         "peak": tf_sus, "unit": "TFLOP/s",
+                         "frac": flops / (pms / 1e3) / 1e12 / tf_sus,
+                         "peak_kind": f"{peak_kind} sustained",
+                         "frac_of_burst": flops / (pms / 1e3) / 1e12 / tf_peak,
+                         "flops_per_layer": flops},
+            "gpu_launches": kp * MoEBlockEngine.prefill_kernels(),
+            "layers_timed": kp, "clocks": pclk.summary(),
+        }
+        del hp
+
     # -------- end-to-end through the host API (value measured with host buffers)
     hh = [torch.empty(D, dtype=torch.float32, pin_memory=True) for _ in range(8)]
     for i, h in enumerate(hh):
@@ -291,54 +333,21 @@ def run_b200(args, world, rank, local_rank):
             "gpu_launches": nt * 32,
         }
 
-    # -------- prefill (BASELINE configs[3]: 8 x 4096 tokens)
-    prefill = None
-    if not args.no_prefill:
-        T = PREFILL_SEQS * PREFILL_LEN
-        hp = model.input_hidden(T, stream=200 + rank)
-        hist = torch.zeros((PREFILL_SEQS, n_layers, E), dtype=torch.int32, device=dev)
-        for _ in range(2):
-            eng.prefill(hp, 0, hist=hist[:, 0], tokens_per_seq=PREFILL_LEN, hist_seq_stride=n_layers * E)
-        barrier()
-        torch.cuda.synchronize()
-        kp = max(3, min(10, args.steps // 200))
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        for _ in range(kp):
-            eng.prefill(hp, 0, hist=hist[:, 0], tokens_per_seq=PREFILL_LEN, hist_seq_stride=n_layers * E)
-        p1.record(stream)
-        torch.cuda.synchronize()
-        pms = p0.elapsed_time(p1) / kp
-        tp = torch.tensor([pms], device=dev)
-        if world > 1:
-            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
-        pms = float(tp.item())
-        flops = 2.0 * K * T * 3 * D * FFN
-        prefill = {
-            "workload": f"prefill {PREFILL_SEQS} x {PREFILL_LEN} tokens, one layer (BASELINE configs[3])",
-            "value": world * T / (pms / 1e3), "unit": "tokens/s", "ms_per_layer": pms,
-            # a prefill step is a long back-to-back run of tensor-core GEMMs
-            # (power-capped like cuBLAS's sustained run): the sustained
-            # measured peak is the denominator, the burst fraction is beside it
-            "roofline": {"bound": "tensor", "achieved": flops / (pms / 1e3) / 1e12,
-                         "peak": tf_sus, "unit": "TFLOP/s",
-                         "frac": flops / (pms / 1e3) / 1e12 / tf_sus,
-                         "peak_kind": f"{peak_kind} sustained",
-                         "frac_of_burst": flops / (pms / 1e3) / 1e12 / tf_peak,
-                         "flops_per_layer": flops},
-            "gpu_launches": kp * MoEBlockEngine.prefill_kernels(),
-        }
-        del hp
-
     # -------- expert parallelism (BASELINE configs[4]: Mixtral-8x22B shape)
     ep = None
     if not args.no_ep:
         del eng, model
         torch.cuda.empty_cache()
         try:
-            ep = run_ep(args, world, rank, dev, tf_sus, barrier)
+            ep = run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer")
         except Exception as exc:  # keep the headline line if this section fails
             ep = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        try:
+            ep_nccl = run_ep(args, world, rank, dev, tf_sus, barrier, impl="nccl")
+        except Exception as exc:
+            ep_nccl = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        if isinstance(ep, dict):
+            ep["nccl_baseline"] = ep_nccl
 
     # -------- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -385,38 +394,55 @@ def run_b200(args, world, rank, local_rank):
 EP_D, EP_FFN, EP_TOKENS = 6144, 16384, 8 * 4096
 
 
-def run_ep(args, world, rank, dev, tf_sus, barrier):
+def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer"):
     """Mixtral-8x22B-shaped MoE layer (d=6144, ffn=16384, E=8, top-2),
     prefill 8 x 4096 tokens sharded T/G per rank, experts sharded E/G per
-    rank, expert-parallel over the ranks (ep.py: fused router + permutation
-    -> count all_to_all -> NCCL grouped send/recv into an expert-major
-    receive buffer -> tcgen05 grouped GEMMs -> send/recv back -> combine).
-    Total work is fixed as G grows (strong scaling)."""
+    rank, expert-parallel over the ranks.  Total work is fixed as G grows
+    (strong scaling).
+
+    impl "peer" (the product, ep.PeerEP): router + permutation, dispatch
+      kernel storing x rows straight into the owners' receive buffers over
+      NVLink, tcgen05 grouped GEMMs, down-GEMM epilogue storing outputs
+      straight into the sources' buffers, combine -- no host sync.
+    impl "nccl" (baseline, ep.gpu_ep_layer): the same kernels around NCCL
+      count all_to_all + grouped send/recv, with host syncs for the splits."""
     import torch
     import torch.distributed as dist
 
     import paper_2501_10375_b200 as P
-    from paper_2501_10375_b200.ep import ep_model, gpu_ep_layer
+    from paper_2501_10375_b200.ep import PeerEP, ep_model, gpu_ep_layer
 
     if world > 1 and not dist.is_initialized():
         return None
     t_local = EP_TOKENS // world
     m = ep_model(P.ModelShape(2, E, K), EP_D, EP_FFN, rank, world, seed=0, device=dev)
     h = m.input_hidden(t_local, stream=300 + rank)
+    phases = []
+    if impl == "peer":
+        ctx = PeerEP(m, 0, t_local, rank, world)
+
+        def step(record=False):
+            return ctx.layer(h)
+    else:
+        def step(record=False):
+            return gpu_ep_layer(m, 0, h, timings=phases if record else None)[:3]
     for _ in range(2):
-        gpu_ep_layer(m, 0, h)
+        step()
     barrier()
     torch.cuda.synchronize()
     kp = 5
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    phases = []
     e0.record(stream)
     for i in range(kp):
-        out, sel, w, plan = gpu_ep_layer(m, 0, h, timings=phases if i == kp - 1 else None)
+        step(record=i == kp - 1)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    if impl == "peer":
+        ctx.check()
+        off = ctx._cur["offsets"].tolist()
+        sent = off[-1] - sum(off[e + 1] - off[e] for e in range(E) if e * world // E == rank)
     ms = e0.elapsed_time(e1) / kp
     t = torch.tensor([ms], device=dev)
     if world > 1:
@@ -426,22 +452,39 @@ def run_ep(args, world, rank, dev, tf_sus, barrier):
     for (_, a), (name, b) in zip(phases, phases[1:]):
         split[name] = a.elapsed_time(b)
     flops = 2.0 * K * EP_TOKENS * 3 * EP_D * EP_FFN
-    sent = sum(n for e, (_, n) in enumerate(plan.send) if e * world // E != rank)
-    return {
+    if impl == "peer":
+        ctx.close()
+        desc = ("peer-memory kernels over NVLink (dispatch = permutation gather with remote "
+                "stores; return fused into the down GEMM epilogue; epoch flags)"
+                if world > 1 else "none (G=1)")
+        # router, permute (count, scan, scatter), publish, dispatch, recv, up,
+        # fused-return down, wait, combine
+        launches = 11
+    else:
+        desc = ("nccl all_to_all (counts) + grouped send/recv (payload, outputs)"
+                if world > 1 else "none (G=1)")
+        launches = 9  # router, permute (4), up, down, combine + NCCL
+    out = {
         "workload": f"Mixtral-8x22B-shaped layer (d={EP_D}, ffn={EP_FFN}, E={E}, top-{K}), "
                     f"prefill {EP_TOKENS} tokens sharded {t_local}/rank, expert-parallel "
                     f"over {world} GPU(s) (BASELINE configs[4])",
+        "impl": impl,
         "value": EP_TOKENS / (ms / 1e3), "unit": "tokens/s", "ms_per_layer": ms,
         "scaling": "strong", "experts_per_gpu": E // world,
-        "collective": "nccl all_to_all (counts) + grouped send/recv (payload, outputs)"
-                      if world > 1 else "none (G=1)",
-        "rank0_phase_ms": split,
-        "rank0_rows_sent": sent, "rank0_payload_bytes_sent": sent * EP_D * 2,
+        "collective": desc,
         "roofline": {"bound": "tensor", "achieved_per_gpu": flops / world / (ms / 1e3) / 1e12,
                      "peak": tf_sus, "unit": "TFLOP/s",
                      "frac": flops / world / (ms / 1e3) / 1e12 / tf_sus,
                      "flops_per_layer": flops},
     }
+    if split:
+        out["rank0_phase_ms"] = split
+    if impl == "peer":
+        out["rank0_payload_bytes_sent"] = int(sent) * EP_D * 2
+    out["gpu_launches_per_layer"] = launches
+    del m
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():

@@ -204,6 +204,46 @@ int daop_expert_gemm_down(const uint16_t* d_act, int64_t rows, int32_t d, int32_
                           int32_t num_experts, float* d_y, int32_t group_m,
                           daop_stream_t stream);
 
+/* ------------------------------------------------ expert parallelism over peer memory
+ * Replaces the NCCL all-to-all dispatch / combine that SURVEY.md §8b
+ * proposes as "daop_ep_dispatch / daop_ep_combine" -- the reference has no
+ * devices; its only exchange is the priced expert-activation
+ * transfer, moesim/simulator.py:196-234.  One symmetric workspace per rank
+ * (daop_ep_ws_layout bytes, zeroed, shared with the peers by CUDA IPC);
+ * d_peers[G] = the G workspace bases as seen from this GPU.  Per layer, on
+ * one stream, no host sync: publish -> dispatch -> recv -> up GEMM ->
+ * daop_ep_expert_gemm_down -> wait_back -> daop_combine.  `epoch` increases
+ * by one per layer call and is identical on every rank. */
+int daop_ep_ws_layout(int32_t world, int32_t num_experts, int32_t d, int64_t cap_recv_rows,
+                      int64_t cap_send_rows, int64_t* h_total_bytes, int64_t* h_recv_off,
+                      int64_t* h_yback_off, int64_t* h_local_offsets_off);
+/* per-expert row counts of this rank's permutation -> every peer */
+int daop_ep_publish(const uint64_t* d_peers, int32_t rank, int32_t world, int32_t num_experts,
+                    const int64_t* d_offsets, uint32_t epoch, daop_stream_t stream);
+/* permutation gather fused with the all-to-all: x rows (token order) are
+ * stored straight into the owners' expert-major receive buffers */
+int daop_ep_dispatch(const uint64_t* d_peers, int32_t rank, int32_t world, int32_t num_experts,
+                     int32_t k, int32_t d, const uint16_t* d_x, const int32_t* d_perm,
+                     int64_t rows_cap, int64_t recv_off, uint32_t epoch, daop_stream_t stream);
+/* waits for every source's rows; writes the local expert offsets and the
+ * per-row return addresses into the workspace */
+int daop_ep_recv(const uint64_t* d_peers, int32_t rank, int32_t world, int32_t num_experts,
+                 int32_t d, int64_t yback_off, uint32_t epoch, daop_stream_t stream);
+/* down GEMM fused with the return all-to-all (outputs stored into the
+ * source ranks' y_back, tile by tile) */
+int daop_ep_expert_gemm_down(const uint16_t* d_act, int64_t rows_cap, int32_t d, int32_t ffn,
+                             const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
+                             const int32_t* d_slot_of, int32_t num_experts,
+                             const uint64_t* d_peers, void* d_ws, int32_t rank, int32_t world,
+                             uint32_t epoch, int32_t group_m, daop_stream_t stream);
+int daop_ep_wait_back(void* d_ws, int32_t world, uint32_t epoch, daop_stream_t stream);
+/* 1 if any wait of this workspace timed out (synchronous read) */
+int daop_ep_status(const void* d_ws, int32_t* h_err);
+/* CUDA IPC of a workspace: 64-byte handle + offset inside its allocation */
+int daop_ep_ipc_handle(const void* d_ptr, void* h_handle64, int64_t* h_offset);
+int daop_ep_ipc_open(const void* h_handle64, int64_t offset, void** h_base, void** h_ptr);
+int daop_ep_ipc_close(void* h_base);
+
 /* ------------------------------------------------ decode layer (b = 1)
  * One persistent cooperative launch: RMSNorm + gate + next-layer gate, the
  * selection (mode 0: true top-k -- Fiddler / l < start; mode 1: DAOP plan

@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "ep.cuh"
 #include "tcgen05.cuh"
 
 namespace daop {
@@ -61,7 +62,34 @@ struct GemmParams {
   const uint16_t* b_ptr;   // B base of slot 0 (rows x b_ld bf16)
   int64_t b_ld;
   int64_t b_slot_stride;   // elements
+  // expert-parallel return (down GEMM only, ep_p2p.cu): row r of the output
+  // is stored at the address row_dst[r] (the source rank's y_back row, over
+  // NVLink) instead of out + r * out_ld, and the CTA that finishes last
+  // flags y[sig_rank] = sig_epoch on every peer workspace
+  const uint64_t* row_dst;
+  unsigned* sig_done;
+  const uint64_t* sig_peers;
+  int sig_G, sig_rank;
+  unsigned sig_epoch;
 };
+
+// end-of-kernel EP signal: every thread fences its (remote) output stores,
+// the last CTA to arrive publishes the flags
+__device__ __forceinline__ void ep_gemm_signal_fence(const GemmParams& p) {
+  if (p.sig_done) __threadfence_system();
+}
+
+__device__ __forceinline__ void ep_gemm_signal(const GemmParams& p) {
+  if (p.sig_done && threadIdx.x == 0) {
+    if (atomicAdd(p.sig_done, 1u) == gridDim.x - 1) {
+      *p.sig_done = 0;
+      __threadfence_system();
+      for (int s = 0; s < p.sig_G; ++s)
+        st_release_sys(reinterpret_cast<unsigned*>(p.sig_peers[s] + EP_FLAGS_Y) + p.sig_rank,
+                       p.sig_epoch);
+    }
+  }
+}
 
 __device__ __forceinline__ void l2_demote_range(const void* p, int64_t bytes) {
   const char* c = static_cast<const char*>(p);
@@ -241,7 +269,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           }
         }
       } else {
-        float* out = static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
+        float* out = p.row_dst ? (valid ? reinterpret_cast<float*>(p.row_dst[grow]) + n * GB_N
+                                        : nullptr)
+                               : static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
 #pragma unroll 1
         for (int c = 0; c < GB_N; c += 32) {
           uint32_t v[32];
@@ -266,11 +296,13 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     }
   }
   tc_fence_before();
+  ep_gemm_signal_fence(p);
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
   }
+  ep_gemm_signal(p);
 }
 
 // ---------------------------------------------------------------- host side
@@ -530,7 +562,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
           }
         }
       } else {
-        float* out = static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
+        float* out = p.row_dst ? (valid ? reinterpret_cast<float*>(p.row_dst[grow]) + n * GB_N
+                                        : nullptr)
+                               : static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
 #pragma unroll 1
         for (int c = 0; c < GB_N; c += 32) {
           uint32_t v[32];
@@ -565,11 +599,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     }
   }
   tc_fence_before();
+  ep_gemm_signal_fence(p);
   cluster_sync_all();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_pair<512>(tmem_base);
   }
+  ep_gemm_signal(p);
 }
 
 static int g_gemm_mode = 0;    // 0: CTA pair (default), 1: single CTA
@@ -709,4 +745,43 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
                GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0,
                g_gemm_demote & 2, act, ffn, w2, ffn, slot_stride_elems};
   return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
+}
+
+// Expert-parallel down GEMM (ep_p2p.cu): rows of the expert-major receive
+// buffer (capacity rows_cap; the real extents come from the device offsets
+// the receive kernel wrote into the workspace), outputs stored through the
+// workspace's return table straight into the source ranks' y_back, then
+// y[rank] flagged on every peer.
+extern "C" int daop_ep_expert_gemm_down(const uint16_t* act, int64_t rows_cap, int32_t d,
+                                        int32_t ffn, const uint16_t* slab, int64_t n_slots,
+                                        int64_t slot_stride_elems, const int32_t* d_slot_of,
+                                        int32_t E, const uint64_t* d_peers, void* d_ws,
+                                        int32_t rank, int32_t G, uint32_t epoch, int32_t group_m,
+                                        daop_stream_t stream) {
+  int rc = check_ffn_shape(rows_cap, d, ffn, E);
+  if (rc) return rc;
+  if (G < 1 || G > EP_MAX_G || rank < 0 || rank >= G || rows_cap < 1) {
+    set_error("ep gemm: bad rank/world (%d/%d) or capacity %lld", rank, G,
+              static_cast<long long>(rows_cap));
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  uint8_t* ws = static_cast<uint8_t*>(d_ws);
+  CUtensorMap ta, tb;
+  const uint64_t adims[2] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(rows_cap)};
+  const uint64_t astr[1] = {static_cast<uint64_t>(ffn) * 2};
+  const uint32_t abox[2] = {GB_K, GB_M};
+  if ((rc = make_tmap_bf16(&ta, act, 2, adims, astr, abox))) return rc;
+  const uint64_t bdims[3] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(d),
+                             static_cast<uint64_t>(n_slots)};
+  const uint64_t bstr[2] = {static_cast<uint64_t>(ffn) * 2,
+                            static_cast<uint64_t>(slot_stride_elems) * 2};
+  const uint32_t bbox[3] = {GB_K, 128, 1};
+  const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
+  if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
+  GemmParams p{reinterpret_cast<const int64_t*>(ws + EP_LOCAL_OFF), d_slot_of, E, ffn / GB_K,
+               d / GB_N, group_m != 0 ? group_m : -8, GB_N, 128, nullptr, d, GB_N,
+               g_gemm_policy >= 0 ? g_gemm_policy : 2, 0, g_gemm_demote & 2, act, ffn, w2, ffn,
+               slot_stride_elems, reinterpret_cast<const uint64_t*>(ws + EP_ROWMAP),
+               reinterpret_cast<unsigned*>(ws + EP_DONE_GEMM), d_peers, G, rank, epoch};
+  return launch_gemm<false>(ta, tb, p, rows_cap, as_stream(stream));
 }

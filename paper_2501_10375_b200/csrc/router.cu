@@ -434,7 +434,7 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
   const int rows = wg_next ? 2 * E : E;
   const size_t smem_mma = static_cast<size_t>(16) * (d + 8) * 2 + static_cast<size_t>(d) * 2 +
                           2 * kMmaWarps * kTokTile * 4 + 2 * kMmaWarps * 16 * kTokTile * 4;
-  if (rows <= 16 && d % (16 * kMmaWarps) == 0 && smem_mma <= 220 * 1024) {
+  if (rows <= 16 && d % (16 * kMmaWarps) == 0 && smem_mma <= 232448) {
     const int64_t ntiles = (T + kTokTile - 1) / kTokTile;
     const int blocks = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
     DAOP_CUDA(cudaFuncSetAttribute(router_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -275,3 +275,166 @@ def ep_model(shape, d_model: int, d_ff: int, rank: int, world: int, layers=(0,),
         for e in mine:
             m.load_expert(l, e)
     return m
+
+
+# ------------------------------------------------------------------ peer-memory EP
+
+
+class PeerEP:
+    """Expert-parallel MoE layer over NVLink peer memory (csrc/ep_p2p.cu).
+
+    Replaces the NCCL exchanges of `ep_moe_layer` with kernels that store
+    straight into the peers' symmetric workspaces: the permutation gather IS
+    the dispatch (x rows go from token order to the owner's expert-major
+    receive buffer in one pass), and the down GEMM's epilogue IS the return
+    all-to-all (each fp32 output tile is stored into the source rank's
+    y_back as it leaves TMEM).  Ranks synchronise through epoch flags in the
+    workspaces; nothing on the path waits for the host, so a layer is one
+    stream of launches (graph-capturable).
+
+    `model` holds this rank's experts (ep_model); `t_cap` bounds the tokens
+    per rank per call.  With world > 1 the workspaces are exchanged by CUDA
+    IPC over the process group (one process per GPU)."""
+
+    def __init__(self, model, layer: int, t_cap: int, rank: int = 0, world: int = 1,
+                 group=None, _peer_table=None):
+        from . import _lib
+        self.m, self.layer_idx, self.rank, self.world = model, layer, rank, world
+        self.E, self.k, self.d, self.ffn = (model.shape.num_experts, model.shape.top_k,
+                                            model.d, model.ffn)
+        self.t_cap = t_cap
+        self.cap_send = t_cap * self.k
+        self.cap_recv = world * t_cap * self.k
+        out = [torch.zeros(1, dtype=torch.int64) for _ in range(4)]
+        _lib.call("daop_ep_ws_layout", world, self.E, self.d, self.cap_recv, self.cap_send,
+                  *[o.data_ptr() for o in out])
+        total, self.recv_off, self.yback_off, self.local_off = (int(o[0]) for o in out)
+        dev = model.device
+        self.ws = torch.zeros(total, dtype=torch.uint8, device=dev)
+        self.recv_x = self.ws[self.recv_off: self.recv_off + self.cap_recv * self.d * 2] \
+            .view(torch.bfloat16).view(self.cap_recv, self.d)
+        self.y_back = self.ws[self.yback_off: self.yback_off + self.cap_send * self.d * 4] \
+            .view(torch.float32).view(self.cap_send, self.d)
+        self.act = torch.empty((self.cap_recv, self.ffn), dtype=torch.bfloat16, device=dev)
+        self.epoch = 0
+        self._ipc_bases = []
+        if _peer_table is not None:
+            self.peers = _peer_table
+        elif world == 1:
+            self.peers = torch.tensor([self.ws.data_ptr()], dtype=torch.int64, device=dev)
+        else:
+            self.peers = self._open_peers(group)
+
+    def _open_peers(self, group):
+        import ctypes
+
+        from . import _lib
+        torch.cuda.synchronize()  # the zeroed workspace must exist before any peer flags it
+        handle = ctypes.create_string_buffer(64)
+        off = torch.zeros(1, dtype=torch.int64)
+        _lib.call("daop_ep_ipc_handle", self.ws.data_ptr(), ctypes.addressof(handle),
+                  off.data_ptr())
+        mine = (bytes(handle.raw), int(off[0]))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        ptrs = []
+        for s, (hb, o) in enumerate(allh):
+            if s == self.rank:
+                ptrs.append(self.ws.data_ptr())
+                continue
+            hbuf = ctypes.create_string_buffer(hb, 64)
+            base, ptr = ctypes.c_void_p(), ctypes.c_void_p()
+            _lib.call("daop_ep_ipc_open", ctypes.addressof(hbuf), o, ctypes.byref(base),
+                      ctypes.byref(ptr))
+            self._ipc_bases.append(base.value)
+            ptrs.append(ptr.value)
+        dist.barrier(group=group)
+        return torch.tensor(ptrs, dtype=torch.int64, device=self.ws.device)
+
+    @classmethod
+    def emulated(cls, models, layer: int, t_cap: int):
+        """G ranks in ONE process on one GPU (test harness): every rank's
+        peer table points at the G workspaces, so the kernels run the exact
+        multi-rank data movement; the caller interleaves the phases."""
+        G = len(models)
+        ranks = [cls(m, layer, t_cap, r, G, _peer_table=torch.zeros(1)) for r, m in
+                 enumerate(models)]
+        table = torch.tensor([c.ws.data_ptr() for c in ranks], dtype=torch.int64,
+                             device=models[0].device)
+        for c in ranks:
+            c.peers = table
+        return ranks
+
+    def close(self):
+        from . import _lib
+        for b in self._ipc_bases:
+            _lib.call("daop_ep_ipc_close", b)
+        self._ipc_bases = []
+
+    # -- phases (one layer = route, publish, dispatch, experts, finish) -----
+    def route(self, h):
+        from . import ops
+        m, l = self.m, self.layer_idx
+        t = h.shape[0]
+        if t > self.t_cap:
+            raise ValueError(f"{t} tokens exceed the workspace capacity {self.t_cap}")
+        nxt = m.gate[l + 1] if l + 1 < m.shape.num_layers else None
+        r = ops.router(h, m.norm[l], m.gate[l], nxt, self.k)
+        pr = ops.permute(r["topk_idx"], self.E)
+        self.epoch += 1
+        self._cur = dict(h=h, x=r["x"], sel=r["topk_idx"], w=r["topk_w"], perm=pr["perm"],
+                         inv=pr["inv"], offsets=pr["offsets"], t=t)
+        return self._cur
+
+    def publish(self):
+        from . import _lib, ops
+        _lib.call("daop_ep_publish", self.peers.data_ptr(), self.rank, self.world, self.E,
+                  self._cur["offsets"].data_ptr(), self.epoch, ops._s())
+
+    def dispatch(self):
+        from . import _lib, ops
+        c = self._cur
+        _lib.call("daop_ep_dispatch", self.peers.data_ptr(), self.rank, self.world, self.E,
+                  self.k, self.d, c["x"].data_ptr(), c["perm"].data_ptr(), c["t"] * self.k,
+                  self.recv_off, self.epoch, ops._s())
+
+    def experts(self):
+        from . import _lib, ops
+        m, l = self.m, self.layer_idx
+        s = ops._s()
+        _lib.call("daop_ep_recv", self.peers.data_ptr(), self.rank, self.world, self.E, self.d,
+                  self.yback_off, self.epoch, s)
+        _lib.call("daop_expert_gemm_up", self.recv_x.data_ptr(), self.cap_recv, self.d, self.ffn,
+                  m.slab.data_ptr(), m.n_slots, m.slot_elems, self.ws.data_ptr() + self.local_off,
+                  m.slot_of[l].data_ptr(), self.E, self.act.data_ptr(), 0, s)
+        _lib.call("daop_ep_expert_gemm_down", self.act.data_ptr(), self.cap_recv, self.d,
+                  self.ffn, m.slab.data_ptr(), m.n_slots, m.slot_elems, m.slot_of[l].data_ptr(),
+                  self.E, self.peers.data_ptr(), self.ws.data_ptr(), self.rank, self.world,
+                  self.epoch, 0, s)
+
+    def finish(self):
+        from . import _lib, ops
+        c = self._cur
+        _lib.call("daop_ep_wait_back", self.ws.data_ptr(), self.world, self.epoch, ops._s())
+        out = ops.combine(c["h"], self.y_back[: c["t"] * self.k], c["inv"], c["w"])
+        return out, c["sel"], c["w"]
+
+    def layer(self, h):
+        """One EP MoE layer on this rank's tokens: (h', sel, w)."""
+        self.route(h)
+        self.publish()
+        self.dispatch()
+        self.experts()
+        return self.finish()
+
+    def local_offsets(self):
+        return self.ws[self.local_off: self.local_off + 8 * (self.E + 1)].view(torch.int64)
+
+    def check(self):
+        """Raise if any cross-GPU wait of this workspace timed out."""
+        from . import _lib
+        from .errors import DeviceError
+        err = torch.zeros(1, dtype=torch.int32)
+        _lib.call("daop_ep_status", self.ws.data_ptr(), err.data_ptr())
+        if int(err[0]):
+            raise DeviceError("peer-memory EP: a cross-GPU wait timed out (peer not progressing)")

@@ -151,7 +151,8 @@ def test_device_planner_matches_golden(P, golden):
                 [x[0], x[2]] for x in exp["degraded"]]
 
 
-@pytest.mark.parametrize("d,E,k,T", [(256, 8, 2, 64), (4096, 8, 2, 300), (1024, 16, 2, 77)])
+@pytest.mark.parametrize("d,E,k,T", [(256, 8, 2, 64), (4096, 8, 2, 300), (1024, 16, 2, 77),
+                                     (6144, 8, 2, 4100)])  # 8x22B width: tensor-core path
 def test_router_parity(P, d, E, k, T):
     pkg, model_mod, ops = P
     om = N.OracleModel(3, E, k, d, 512, seed=4)
