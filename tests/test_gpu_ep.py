@@ -106,3 +106,64 @@ def test_peer_ep_emulated_ranks_equal_single_gpu(G):
         # every row was received exactly once by its owner
         total = sum(int(ranks[r].local_offsets()[-1]) for r in range(G))
         assert total == 2 * sum(tok)
+
+
+def _two_proc_worker(rank, port, q):
+    import os as _os
+    _os.environ["MASTER_ADDR"] = "127.0.0.1"
+    _os.environ["MASTER_PORT"] = str(port)
+    import torch as _t
+    import torch.distributed as dist
+    try:
+        import paper_2501_10375_b200 as P
+        from paper_2501_10375_b200.ep import PeerEP, ep_model
+        _t.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=2)
+        E, d, ffn = 8, 512, 1024
+        m, eng = _single_gpu_reference(P, E, d, ffn, 8)
+        me = ep_model(P.ModelShape(2, E, 2), d, ffn, rank, 2, seed=8)
+        ctx = PeerEP(me, 0, t_cap=300, rank=rank, world=2)
+        ok = True
+        for step, t in enumerate((300, 77)):
+            h = m.input_hidden(t, stream=40 + rank, step=step)
+            out, sel, _ = ctx.layer(h)
+            _t.cuda.synchronize()
+            ctx.check()
+            ref = eng.prefill(h, 0)
+            ok = ok and _t.equal(out, ref["out"]) and _t.equal(sel, ref["topk_idx"])
+        dist.barrier()
+        ctx.close()
+        dist.destroy_process_group()
+        q.put((rank, ok, ""))
+    except Exception as exc:  # report instead of hanging the parent
+        q.put((rank, False, repr(exc)))
+
+
+def test_peer_ep_two_processes_one_gpu():
+    """The real multi-process protocol on one GPU: two processes, CUDA IPC of
+    each other's workspace, kernels of both processes synchronising through
+    the epoch flags across contexts (gloo carries only the IPC handles)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_proc_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in range(2):
+            r, ok, err = q.get(timeout=240)
+            res[r] = (ok, err)
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert res[0][0] and res[1][0], res
