@@ -49,6 +49,14 @@ const char* daop_last_error(void);
 int daop_version(void);
 /* sm count and compute capability of the current device (fails without GPU) */
 int daop_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* one synchronous step of a captured CUDA graph (cudaGraphExec_t): copy
+ * `bytes` from h_src into the graph's pinned staging buffer, launch, wait.
+ * The end-to-end decode call (no reference analogue: the reference prices a
+ * decode step, simulator.py:289-391). */
+int daop_graph_step(void* graph_exec, daop_stream_t stream, const void* h_src, void* h_staging,
+                    int64_t bytes);
+/* completion wait of daop_graph_step: 0 = cudaStreamSynchronize (default), 1 = busy-poll */
+int daop_graph_step_mode(int32_t spin);
 
 /* ---------------------------------------------- operator table (_kernels.py)
  * Device replacements of the reference's module-level operator table,

@@ -23,6 +23,8 @@ I32, I64, U64, F32, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_doubl
 PROTOS = {
     "daop_version": [],
     "daop_device_info": [P, P, P],
+    "daop_graph_step": [P, P, P, P, I64],
+    "daop_graph_step_mode": [I32],
     "daop_topk_rows_f64": [P, I64, I32, I32, P, P],
     "daop_topk_rows_f32": [P, I64, I32, I32, P, P],
     "daop_activation_counts": [P, I64, I32, I32, I32, P, P],

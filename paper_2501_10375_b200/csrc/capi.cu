@@ -64,6 +64,36 @@ int daop_device_info(int* sms, int* major, int* minor) {
   return DAOP_OK;
 }
 
+// One synchronous host step of a captured graph: stage the caller's host
+// input into the graph's pinned source buffer, launch, wait.  The end-to-end
+// decode call (engine.decode_host) runs entirely here, with no Python between
+// the staging copy, the launch and the synchronisation.
+static int g_graph_step_spin = 0;
+int daop_graph_step_mode(int32_t spin) {
+  g_graph_step_spin = spin;
+  return DAOP_OK;
+}
+
+int daop_graph_step(void* graph_exec, daop_stream_t stream, const void* h_src, void* h_staging,
+                    int64_t bytes) {
+  if (!graph_exec) {
+    set_error("graph_step: null graph");
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (bytes > 0 && h_src && h_src != h_staging) memcpy(h_staging, h_src, static_cast<size_t>(bytes));
+  DAOP_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), as_stream(stream)));
+  if (g_graph_step_spin) {
+    // busy-poll: no sleep / yield between the kernel's last store and the return
+    cudaError_t e;
+    while ((e = cudaStreamQuery(as_stream(stream))) == cudaErrorNotReady) {
+    }
+    DAOP_CUDA(e);
+  } else {
+    DAOP_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  }
+  return DAOP_OK;
+}
+
 // placement.py:123-125 -- math.floor(ecr * L * E), left to right in double
 int daop_slot_budget(double ecr, int32_t L, int32_t E, int64_t* budget) {
   double v = (ecr * static_cast<double>(L)) * static_cast<double>(E);

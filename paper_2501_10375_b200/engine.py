@@ -20,11 +20,9 @@ daop.py.
 
 from __future__ import annotations
 
-import ctypes
-
 import torch
 
-from . import ops
+from . import _lib, ops
 from .model import MoEModel
 
 
@@ -63,20 +61,23 @@ class MoEBlockEngine:
         copy of h from a pinned staging buffer, then the decode launch, which
         writes the residual and the selection straight into pinned host memory
         over the bus (no D2H copy node).  The caller's h is copied into the
-        staging buffer on the host; one replay + one synchronize per call."""
+        staging buffer, the graph launched and the stream synchronised in one
+        native call (daop_graph_step)."""
+        c = self._host_graphs.get(layer) if self._out_host is not None else None
+        if c is not None and h_host.dtype is torch.float32 and not h_host.is_cuda and \
+                h_host.is_contiguous() and h_host.numel() == self.d:
+            # fast path: staging copy + launch + wait in one native call
+            rc = c[0](c[1], c[2], h_host.data_ptr(), c[3], c[4])
+            if rc:
+                _lib.check(rc, "daop_graph_step")
+            return self._out_host, self._sel_host
         if self._out_host is None:
             self._h_host = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
             self._out_host = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
             self._sel_host = torch.empty(self.k, dtype=torch.int32, pin_memory=True)
             self._host_graphs = {}
-        if h_host.data_ptr() != self._h_host.data_ptr():
-            if h_host.device.type == "cpu" and h_host.dtype == torch.float32 and \
-                    h_host.is_contiguous() and h_host.numel() == self.d:
-                ctypes.memmove(self._h_host.data_ptr(), h_host.data_ptr(), 4 * self.d)
-            else:
-                self._h_host.copy_(h_host)
-        g = self._host_graphs.get(layer)
-        if g is None:
+        self._h_host.copy_(h_host)
+        if layer not in self._host_graphs:
             def step():
                 self._h_dev.copy_(self._h_host, non_blocking=True)
                 self.decode(self._h_dev, layer, h_out=self._out_host, sel_out=self._sel_host)
@@ -90,9 +91,12 @@ class MoEBlockEngine:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 step()
-            self._host_graphs[layer] = g
-        g.replay()
-        torch.cuda.current_stream().synchronize()
+            self._graphs_keepalive = getattr(self, "_graphs_keepalive", []) + [g]
+            self._host_graphs[layer] = (_lib.LIB.daop_graph_step, g.raw_cuda_graph_exec(),
+                                        torch.cuda.current_stream().cuda_stream,
+                                        self._h_host.data_ptr(), 4 * self.d)
+        c = self._host_graphs[layer]
+        _lib.check(c[0](c[1], c[2], c[3], c[3], c[4]), "daop_graph_step")
         return self._out_host, self._sel_host
 
     @staticmethod
