@@ -245,6 +245,17 @@ int daop_ep_expert_gemm_down(const uint16_t* d_act, int64_t rows_cap, int32_t d,
                              const uint64_t* d_peers, void* d_ws, int32_t rank, int32_t world,
                              uint32_t epoch, int32_t group_m, daop_stream_t stream);
 int daop_ep_wait_back(void* d_ws, int32_t world, uint32_t epoch, daop_stream_t stream);
+/* decode b = 1 over G GPUs: the residual is replicated, every rank runs
+ * daop_decode_layer (mode 0) with its own experts as the resident set, then
+ * daop_ep_decode_share stores its picks' outputs (d_y rows where d_is_fast)
+ * into every peer's decode workspace (daop_ep_decode_ws_bytes, zeroed) slot
+ * [epoch & 1]; after daop_ep_decode_wait, daop_combine_dense on that slot
+ * gives every rank the same next residual. */
+int daop_ep_decode_ws_bytes(int32_t k, int32_t d, int64_t* h_bytes);
+int daop_ep_decode_share(const uint64_t* d_peers, int32_t rank, int32_t world, int32_t k,
+                         int32_t d, const float* d_y, const uint8_t* d_is_fast, uint32_t epoch,
+                         daop_stream_t stream);
+int daop_ep_decode_wait(void* d_ws, int32_t world, uint32_t epoch, daop_stream_t stream);
 /* 1 if any wait of this workspace timed out (synchronous read) */
 int daop_ep_status(const void* d_ws, int32_t* h_err);
 /* CUDA IPC of a workspace: 64-byte handle + offset inside its allocation */

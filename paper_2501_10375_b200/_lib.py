@@ -54,6 +54,9 @@ PROTOS = {
                                  C.c_uint32, I32, P],
     "daop_ep_wait_back": [P, I32, C.c_uint32, P],
     "daop_ep_status": [P, P],
+    "daop_ep_decode_ws_bytes": [I32, I32, P],
+    "daop_ep_decode_share": [P, I32, I32, I32, I32, P, P, C.c_uint32, P],
+    "daop_ep_decode_wait": [P, I32, C.c_uint32, P],
     "daop_ep_ipc_handle": [P, P, P],
     "daop_ep_ipc_open": [P, I64, P, P],
     "daop_ep_ipc_close": [P],

@@ -776,6 +776,14 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
     case 6: return launch_decode<12, 2, 6144>(a, grid, st);
     case 7: return launch_decode<16, 1, 8192>(a, grid, st);
     case 8: return launch_decode<10, 2, 7680>(a, grid, st);
-    default: return launch_decode<16, 1, 10240>(a, grid, st);
+    default: {
+      // largest ring that fits: Mixtral-8x22B (d = 6144, ffn = 16384) needs
+      // 64 KB of activations in shared memory and a 144 KB router stage
+      int rc = launch_decode<16, 1, 10240>(a, grid, st);
+      if (rc != DAOP_ERR_UNSUPPORTED) return rc;
+      rc = launch_decode<16, 1, 9216>(a, grid, st);
+      if (rc != DAOP_ERR_UNSUPPORTED) return rc;
+      return launch_decode<16, 1, 8192>(a, grid, st);
+    }
   }
 }

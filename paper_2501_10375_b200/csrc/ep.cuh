@@ -13,6 +13,9 @@ constexpr int64_t EP_FLAGS_Y = 128;        // u32 [EP_MAX_G]
 constexpr int64_t EP_ERR = 192;            // u32
 constexpr int64_t EP_DONE_DISPATCH = 196;  // u32
 constexpr int64_t EP_DONE_GEMM = 200;      // u32
+constexpr int64_t EP_DONE_SHARE = 204;     // u32 (decode workspace)
+constexpr int64_t EP_FLAGS_D = 256;        // u32 [EP_MAX_G] (decode workspace)
+constexpr int64_t EP_DEC_Y = 1024;         // f32 [2][k][d] gathered pick outputs (decode workspace)
 constexpr int64_t EP_COUNTS = 1024;        // i64 [2][EP_MAX_G][EP_MAX_E]
 constexpr int64_t EP_LOCAL_OFF = EP_COUNTS + 2 * EP_MAX_G * EP_MAX_E * 8;  // i64 [EP_MAX_E+1]
 constexpr int64_t EP_ROWMAP = 16384;       // u64 [cap_recv]

@@ -210,9 +210,72 @@ __global__ void ep_wait_back_kernel(uint8_t* ws, int G, unsigned epoch) {
   ep_wait_flags(ws, EP_FLAGS_Y, G, epoch);
 }
 
+// ---------------------------------------------------------------- decode (b = 1)
+//
+// The residual is replicated on every rank; each rank runs the decode kernel
+// with its own experts as the resident set (true top-k, identical decisions
+// everywhere), so each pick is streamed by exactly its owner.  share: the
+// owner stores its picks' fp32 outputs into slot [epoch&1][j] of EVERY
+// peer's decode workspace and flags; then every rank combines
+// h + sum_j w_j y_j in fixed j order (the single-GPU combine) -> the
+// replicated residual of the next layer.
+__global__ void ep_decode_share_kernel(const uint64_t* peers, int rank, int G, int k, int d,
+                                       const float* y, const uint8_t* is_fast, unsigned epoch) {
+  const int s = blockIdx.x / k, j = blockIdx.x - (blockIdx.x / k) * k;
+  if (is_fast[j]) {
+    float4* dst = reinterpret_cast<float4*>(ws_of(peers, s) + EP_DEC_Y) +
+                  (static_cast<int64_t>(epoch & 1) * k + j) * (d / 4);
+    const float4* src = reinterpret_cast<const float4*>(y) + static_cast<int64_t>(j) * (d / 4);
+    for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* done = reinterpret_cast<unsigned*>(ws_of(peers, rank) + EP_DONE_SHARE);
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *done = 0;
+      __threadfence_system();
+      for (int q = 0; q < G; ++q)
+        st_release_sys(reinterpret_cast<unsigned*>(ws_of(peers, q) + EP_FLAGS_D) + rank, epoch);
+    }
+  }
+}
+
+__global__ void ep_wait_kernel(uint8_t* ws, int64_t flags_off, int G, unsigned epoch) {
+  ep_wait_flags(ws, flags_off, G, epoch);
+}
+
 }  // namespace daop
 
 using namespace daop;
+
+extern "C" int daop_ep_decode_ws_bytes(int32_t k, int32_t d, int64_t* h_bytes) {
+  if (k < 1 || d % 4 != 0) {
+    set_error("ep decode: unsupported k=%d d=%d", k, d);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  *h_bytes = EP_DEC_Y + static_cast<int64_t>(2) * k * d * 4;
+  return DAOP_OK;
+}
+
+extern "C" int daop_ep_decode_share(const uint64_t* d_peers, int32_t rank, int32_t G, int32_t k,
+                                    int32_t d, const float* d_y, const uint8_t* d_is_fast,
+                                    uint32_t epoch, daop_stream_t st) {
+  if (G < 1 || G > EP_MAX_G || rank < 0 || rank >= G || k < 1 || d % 4 != 0) {
+    set_error("ep_decode_share: bad rank/world (%d/%d), k=%d or d=%d", rank, G, k, d);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  ep_decode_share_kernel<<<G * k, 256, 0, as_stream(st)>>>(d_peers, rank, G, k, d, d_y,
+                                                          d_is_fast, epoch);
+  DAOP_CHECK_LAUNCH("ep_decode_share");
+  return DAOP_OK;
+}
+
+extern "C" int daop_ep_decode_wait(void* d_ws, int32_t G, uint32_t epoch, daop_stream_t st) {
+  ep_wait_kernel<<<1, 1, 0, as_stream(st)>>>(static_cast<uint8_t*>(d_ws), EP_FLAGS_D, G, epoch);
+  DAOP_CHECK_LAUNCH("ep_decode_wait");
+  return DAOP_OK;
+}
 
 // ---------------------------------------------------------------- C ABI
 

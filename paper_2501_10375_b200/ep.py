@@ -277,6 +277,43 @@ def ep_model(shape, d_model: int, d_ff: int, rank: int, world: int, layers=(0,),
     return m
 
 
+def open_peer_table(ws: torch.Tensor, rank: int, world: int, group=None):
+    """Exchange this rank's workspace by CUDA IPC over the process group and
+    open every peer's: returns (device table of the G workspace addresses as
+    seen from this GPU, opened IPC bases to close)."""
+    import ctypes
+
+    from . import _lib
+    torch.cuda.synchronize()  # the zeroed workspace must exist before any peer flags it
+    handle = ctypes.create_string_buffer(64)
+    off = torch.zeros(1, dtype=torch.int64)
+    _lib.call("daop_ep_ipc_handle", ws.data_ptr(), ctypes.addressof(handle), off.data_ptr())
+    allh = [None] * world
+    dist.all_gather_object(allh, (bytes(handle.raw), int(off[0])), group=group)
+    ptrs, bases = [], []
+    for s, (hb, o) in enumerate(allh):
+        if s == rank:
+            ptrs.append(ws.data_ptr())
+            continue
+        hbuf = ctypes.create_string_buffer(hb, 64)
+        base, ptr = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.call("daop_ep_ipc_open", ctypes.addressof(hbuf), o, ctypes.byref(base),
+                  ctypes.byref(ptr))
+        bases.append(base.value)
+        ptrs.append(ptr.value)
+    dist.barrier(group=group)
+    return torch.tensor(ptrs, dtype=torch.int64, device=ws.device), bases
+
+
+def _check_ws(ws: torch.Tensor, what: str):
+    from . import _lib
+    from .errors import DeviceError
+    err = torch.zeros(1, dtype=torch.int32)
+    _lib.call("daop_ep_status", ws.data_ptr(), err.data_ptr())
+    if int(err[0]):
+        raise DeviceError(f"{what}: a cross-GPU wait timed out (peer not progressing)")
+
+
 # ------------------------------------------------------------------ peer-memory EP
 
 
@@ -326,30 +363,8 @@ class PeerEP:
             self.peers = self._open_peers(group)
 
     def _open_peers(self, group):
-        import ctypes
-
-        from . import _lib
-        torch.cuda.synchronize()  # the zeroed workspace must exist before any peer flags it
-        handle = ctypes.create_string_buffer(64)
-        off = torch.zeros(1, dtype=torch.int64)
-        _lib.call("daop_ep_ipc_handle", self.ws.data_ptr(), ctypes.addressof(handle),
-                  off.data_ptr())
-        mine = (bytes(handle.raw), int(off[0]))
-        allh = [None] * self.world
-        dist.all_gather_object(allh, mine, group=group)
-        ptrs = []
-        for s, (hb, o) in enumerate(allh):
-            if s == self.rank:
-                ptrs.append(self.ws.data_ptr())
-                continue
-            hbuf = ctypes.create_string_buffer(hb, 64)
-            base, ptr = ctypes.c_void_p(), ctypes.c_void_p()
-            _lib.call("daop_ep_ipc_open", ctypes.addressof(hbuf), o, ctypes.byref(base),
-                      ctypes.byref(ptr))
-            self._ipc_bases.append(base.value)
-            ptrs.append(ptr.value)
-        dist.barrier(group=group)
-        return torch.tensor(ptrs, dtype=torch.int64, device=self.ws.device)
+        table, self._ipc_bases = open_peer_table(self.ws, self.rank, self.world, group)
+        return table
 
     @classmethod
     def emulated(cls, models, layer: int, t_cap: int):
@@ -432,9 +447,86 @@ class PeerEP:
 
     def check(self):
         """Raise if any cross-GPU wait of this workspace timed out."""
+        _check_ws(self.ws, "peer-memory EP")
+
+
+class PeerEPDecode:
+    """Expert-parallel decode of one token (b = 1) over NVLink peer memory.
+
+    The residual stream is replicated on every rank.  Per layer each rank runs
+    the fused decode kernel (router + selection + HBM-streaming SwiGLU GEMV)
+    with ITS experts as the resident set -- the selection is the true top-k
+    and identical on every rank, and each pick is streamed by exactly one
+    GPU, so a token's 2 experts are read by 2 GPUs in parallel.  The owners
+    store their picks' outputs into every peer's decode workspace
+    (daop_ep_decode_share), and every rank combines h + sum_j w_j y_j in
+    fixed j order -- bit-identical to the single-GPU decode layer.  DAOP
+    PLAN mode (prediction-driven selection with degradation) is a
+    single-GPU / host-tier feature: here every expert is in some GPU's HBM."""
+
+    def __init__(self, model, rank: int = 0, world: int = 1, group=None, _peer_table=None):
+        from . import _lib, ops
+        self.m, self.rank, self.world = model, rank, world
+        self.E, self.k, self.d, self.ffn = (model.shape.num_experts, model.shape.top_k,
+                                            model.d, model.ffn)
+        nb = torch.zeros(1, dtype=torch.int64)
+        _lib.call("daop_ep_decode_ws_bytes", self.k, self.d, nb.data_ptr())
+        dev = model.device
+        self.ws = torch.zeros(int(nb[0]), dtype=torch.uint8, device=dev)
+        self.ygather = self.ws[1024:].view(torch.float32).view(2, self.k, self.d)
+        self.bufs = ops.DecodeBuffers(self.d, self.ffn, self.E, self.k, dev)
+        self.out = [torch.empty(self.d, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.epoch = 0
+        self._ipc_bases = []
+        if _peer_table is not None:
+            self.peers = _peer_table
+        elif world == 1:
+            self.peers = torch.tensor([self.ws.data_ptr()], dtype=torch.int64, device=dev)
+        else:
+            self.peers, self._ipc_bases = open_peer_table(self.ws, rank, world, group)
+
+    @classmethod
+    def emulated(cls, models):
+        """G ranks in one process on one GPU (test harness), see PeerEP.emulated."""
+        ranks = [cls(m, r, len(models), _peer_table=torch.zeros(1)) for r, m in enumerate(models)]
+        table = torch.tensor([c.ws.data_ptr() for c in ranks], dtype=torch.int64,
+                             device=models[0].device)
+        for c in ranks:
+            c.peers = table
+        return ranks
+
+    def close(self):
         from . import _lib
-        from .errors import DeviceError
-        err = torch.zeros(1, dtype=torch.int32)
-        _lib.call("daop_ep_status", self.ws.data_ptr(), err.data_ptr())
-        if int(err[0]):
-            raise DeviceError("peer-memory EP: a cross-GPU wait timed out (peer not progressing)")
+        for b in self._ipc_bases:
+            _lib.call("daop_ep_ipc_close", b)
+        self._ipc_bases = []
+
+    def stream(self, h: torch.Tensor, layer: int = 0):
+        """Decode kernel on this rank's experts + share of the local picks."""
+        from . import _lib, ops
+        m = self.m
+        self.epoch += 1
+        nxt = m.gate[layer + 1] if layer + 1 < m.shape.num_layers else None
+        ops.decode_layer(h, m.norm[layer], m.gate[layer], nxt, m.fast[layer], m.slot_of[layer],
+                         m.slab, m.slot_elems, self.d, self.ffn, self.k, self.bufs)
+        _lib.call("daop_ep_decode_share", self.peers.data_ptr(), self.rank, self.world, self.k,
+                  self.d, self.bufs.y.data_ptr(), self.bufs.is_fast.data_ptr(), self.epoch,
+                  ops._s())
+        self._h = h
+
+    def finish(self) -> torch.Tensor:
+        """Wait for every owner's outputs, combine -> the next residual."""
+        from . import _lib, ops
+        _lib.call("daop_ep_decode_wait", self.ws.data_ptr(), self.world, self.epoch, ops._s())
+        out = self.out[self.epoch & 1]
+        _lib.call("daop_combine_dense", self._h.data_ptr(),
+                  self.ygather[self.epoch & 1].data_ptr(), self.bufs.w.data_ptr(), self.k,
+                  self.d, out.data_ptr(), ops._s())
+        return out
+
+    def layer(self, h: torch.Tensor, layer: int = 0) -> torch.Tensor:
+        self.stream(h, layer)
+        return self.finish()
+
+    def check(self):
+        _check_ws(self.ws, "peer-memory EP decode")

@@ -131,7 +131,18 @@ def _two_proc_worker(rank, port, q):
             ctx.check()
             ref = eng.prefill(h, 0)
             ok = ok and _t.equal(out, ref["out"]) and _t.equal(sel, ref["topk_idx"])
+        # decode b = 1: replicated residual, each rank streams its own picks
+        from paper_2501_10375_b200.ep import PeerEPDecode
+        dec = PeerEPDecode(me, rank=rank, world=2)
+        for step in range(3):
+            h1 = m.input_hidden(1, stream=60, step=step)[0]
+            got = dec.layer(h1, 0)
+            _t.cuda.synchronize()
+            dec.check()
+            ref = eng.decode(h1, 0)
+            ok = ok and _t.equal(got, ref.h_out)
         dist.barrier()
+        dec.close()
         ctx.close()
         dist.destroy_process_group()
         q.put((rank, ok, ""))
@@ -167,3 +178,43 @@ def test_peer_ep_two_processes_one_gpu():
             if p.is_alive():
                 p.kill()
     assert res[0][0] and res[1][0], res
+
+
+def _decode_reference(P, E, d, ffn, seed, L=2):
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    from paper_2501_10375_b200.model import MoEModel
+    m = MoEModel(P.ModelShape(L, E, 2), d, ffn, seed=seed)
+    return m, MoEBlockEngine(m)
+
+
+@pytest.mark.parametrize("G,d,ffn", [(1, 512, 1024), (2, 512, 1024), (4, 512, 1024),
+                                     (8, 512, 1024), (2, 6144, 16384)])
+def test_peer_ep_decode_equals_single_gpu(G, d, ffn):
+    """Decode b = 1, experts sharded over G emulated ranks (one workspace
+    each, peer tables pointing at each other): every rank streams only its
+    own picks, shares their outputs through the peers' workspaces and
+    combines -- every rank's residual must equal the single-GPU decode layer
+    bit for bit, chained over 2 layers and 3 tokens.  (2, 6144, 16384) is
+    the Mixtral-8x22B shape."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.ep import PeerEPDecode, ep_model
+    E = 8
+    m, eng = _decode_reference(P, E, d, ffn, 11)
+    models = [ep_model(P.ModelShape(2, E, 2), d, ffn, r, G, layers=(0, 1), seed=11)
+              for r in range(G)]
+    ranks = PeerEPDecode.emulated(models)
+    for step in range(3):
+        h = m.input_hidden(1, stream=50, step=step)[0]
+        hs = [h] * G
+        for layer in range(2):
+            for r in range(G):
+                ranks[r].stream(hs[r], layer)
+            hs = [ranks[r].finish() for r in range(G)]
+            ref = eng.decode(h if layer == 0 else ref_h, layer)
+            torch.cuda.synchronize()
+            ref_h = ref.h_out.clone()
+            for r in range(G):
+                ranks[r].check()
+                assert torch.equal(hs[r], ref_h), (G, step, layer, r)

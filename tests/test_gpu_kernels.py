@@ -253,7 +253,8 @@ def test_grouped_gemm_parity(P, d, ffn, E, T, mode):
     hidden_close(out.cpu().numpy(), ref["out"], "layer output")
 
 
-@pytest.mark.parametrize("d,ffn,E,k", [(256, 512, 8, 2), (4096, 14336, 8, 2), (1024, 2816, 16, 4)])
+@pytest.mark.parametrize("d,ffn,E,k", [(256, 512, 8, 2), (4096, 14336, 8, 2), (1024, 2816, 16, 4),
+                                      (6144, 16384, 8, 2)])  # Mixtral-8x22B shape
 def test_decode_layer_parity(P, d, ffn, E, k):
     pkg, model_mod, ops = P
     m = model_mod.MoEModel(pkg.ModelShape(2, E, k), d, ffn, seed=1, resident_layers=[0])
