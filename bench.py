@@ -338,6 +338,12 @@ def run_b200(args, world, rank, local_rank):
     if not args.no_ep:
         del eng, model
         torch.cuda.empty_cache()
+        # decode first: the short HBM-bound run is not measured on a GPU left
+        # hot by the prefill GEMMs
+        try:
+            ep_dec = run_ep_decode(args, world, rank, dev, hbm_peak, barrier)
+        except Exception as exc:
+            ep_dec = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         try:
             ep = run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer")
         except Exception as exc:  # keep the headline line if this section fails
@@ -348,6 +354,8 @@ def run_b200(args, world, rank, local_rank):
             ep_nccl = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         if isinstance(ep, dict):
             ep["nccl_baseline"] = ep_nccl
+        if isinstance(ep, dict):
+            ep["decode"] = ep_dec
 
     # -------- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -486,6 +494,62 @@ def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer"):
     torch.cuda.empty_cache()
     return out
 
+
+def run_ep_decode(args, world, rank, dev, hbm_peak, barrier):
+    """Mixtral-8x22B-shaped layer, decode b=1, experts sharded E/G per rank
+    (ep.PeerEPDecode): the residual is replicated, every rank runs the fused
+    decode kernel on its own experts, so the token's 2 experts (2 x 604 MB)
+    are streamed by up to 2 GPUs in parallel; outputs are shared through
+    peer memory and combined in fixed order on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.ep import PeerEPDecode, ep_model
+
+    if world > 1 and not dist.is_initialized():
+        return None
+    m = ep_model(P.ModelShape(2, E, K), EP_D, EP_FFN, rank, world, seed=0, device=dev)
+    dec = PeerEPDecode(m, rank, world)
+    hs = [m.input_hidden(1, stream=400, step=i)[0] for i in range(32)]
+    for i in range(8):
+        dec.layer(hs[i % 32])
+    barrier()
+    torch.cuda.synchronize()
+    steps = max(50, min(args.steps, 1000))
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        dec.layer(hs[i % 32])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    dec.check()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    step_bytes = 2 * 3 * EP_D * EP_FFN * 2 + 2 * E * EP_D * 2  # 2 experts + 2 gates
+    active = min(world, K)  # b = 1: at most k GPUs hold a pick
+    dec.close()
+    del dec, m
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"Mixtral-8x22B-shaped layer, decode b=1, experts sharded {E // world}/GPU "
+                    f"over {world} GPU(s) (BASELINE configs[4])",
+        "value": 1e3 / ms, "unit": "tokens/s", "ms_per_step": ms, "steps": steps,
+        "scaling": "strong",
+        "collective": ("peer-memory share of the picks' outputs (NVLink stores + epoch flags)"
+                       if world > 1 else "none (G=1)"),
+        "roofline": {"bound": "hbm", "achieved": step_bytes / (ms / 1e3) / 1e9,
+                     "peak": hbm_peak * active if world > 1 else hbm_peak, "unit": "GB/s",
+                     "frac": step_bytes / (ms / 1e3) / 1e9 / (hbm_peak * (active if world > 1 else 1)),
+                     "bytes_per_step": step_bytes,
+                     "note": "b=1 touches 2 experts: at most 2 GPUs stream; peak = that many x HBM"},
+        "gpu_launches_per_step": 2,
+    }
 
 def main():
     ap = argparse.ArgumentParser()

@@ -256,6 +256,20 @@ int daop_ep_decode_share(const uint64_t* d_peers, int32_t rank, int32_t world, i
                          int32_t d, const float* d_y, const uint8_t* d_is_fast, uint32_t epoch,
                          daop_stream_t stream);
 int daop_ep_decode_wait(void* d_ws, int32_t world, uint32_t epoch, daop_stream_t stream);
+/* the fused form: daop_decode_layer (mode 0) whose phase-2 reduction also
+ * stores the local picks' outputs into every peer's slot and whose last CTA
+ * flags them; then daop_ep_decode_finish = wait + fixed-order combine */
+int daop_ep_decode_layer(const uint64_t* d_peers, int32_t rank, int32_t world, uint32_t epoch,
+                         const float* d_h, const uint16_t* d_gamma, const uint16_t* d_wg,
+                         const uint16_t* d_wg_next, const uint8_t* d_fast_row,
+                         const int32_t* d_slot_of, const uint16_t* d_slab,
+                         int64_t slot_stride_elems, int32_t d, int32_t ffn, int32_t num_experts,
+                         int32_t k, float eps, uint16_t* d_x_out, float* d_p_true,
+                         float* d_p_pred, int32_t* d_sel, float* d_w, uint8_t* d_is_fast,
+                         int32_t* d_deg, float* d_y, float* d_h_out, void* d_workspace,
+                         daop_stream_t stream);
+int daop_ep_decode_finish(void* d_ws, int32_t world, int32_t k, int32_t d, const float* d_h,
+                          const float* d_w, float* d_out, uint32_t epoch, daop_stream_t stream);
 /* 1 if any wait of this workspace timed out (synchronous read) */
 int daop_ep_status(const void* d_ws, int32_t* h_err);
 /* CUDA IPC of a workspace: 64-byte handle + offset inside its allocation */

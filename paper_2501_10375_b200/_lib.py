@@ -57,6 +57,9 @@ PROTOS = {
     "daop_ep_decode_ws_bytes": [I32, I32, P],
     "daop_ep_decode_share": [P, I32, I32, I32, I32, P, P, C.c_uint32, P],
     "daop_ep_decode_wait": [P, I32, C.c_uint32, P],
+    "daop_ep_decode_layer": [P, I32, I32, C.c_uint32, P, P, P, P, P, P, P, I64, I32, I32, I32,
+                             I32, F32, P, P, P, P, P, P, P, P, P, P, P],
+    "daop_ep_decode_finish": [P, I32, I32, I32, P, P, P, C.c_uint32, P],
     "daop_ep_ipc_handle": [P, P, P],
     "daop_ep_ipc_open": [P, I64, P, P],
     "daop_ep_ipc_close": [P],

@@ -32,6 +32,7 @@
 // 2 B of gates = 704,774,144 B -> HBM roofline.
 #include "common.cuh"
 #include "decide.cuh"
+#include "ep.cuh"
 
 namespace daop {
 
@@ -69,6 +70,12 @@ struct DecodeArgs {
   unsigned* ctr;           // [0] finished CTAs, [1] pred rows, [2..2+DK_MAX) rows per pick
   float* pred_logits;      // (E)
   uint16_t* act;           // (k, ffn) bf16 SwiGLU activations
+  // expert-parallel decode (ep_p2p.cu): the y rows of this GPU's picks are
+  // also stored into slot [ep_epoch & 1] of every peer's decode workspace,
+  // and the grid's last CTA flags them (null = single GPU)
+  const uint64_t* ep_peers;
+  int ep_G, ep_rank;
+  unsigned ep_epoch;
 };
 
 __device__ unsigned long long g_decode_timeline[1024][16];
@@ -655,12 +662,41 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
     }
   }
   publish();
+  int cta_done = 0;
   if (lane == 0) {
     if (tl) atomicMax(&g_decode_timeline[blockIdx.x][4], gtimer());
-    if (atomicAdd(&s.fin, 1) == DW - 1) {           // CTA done
-      if (atomicAdd(a.ctr, 1u) == gridDim.x - 1) {  // grid done: reset for the next call
-        for (int q = 0; q < DK_MAX; ++q) a.ctr[2 + q] = 0;
-        a.ctr[0] = 0;
+    if (a.ep_peers) __threadfence_block();          // this warp's y rows -> the CTA finisher
+    cta_done = atomicAdd(&s.fin, 1) == DW - 1;      // CTA done
+  }
+  cta_done = __shfl_sync(0xffffffffu, cta_done, 0);
+  if (cta_done && a.ep_peers) {
+    // expert parallelism: the finishing warp stores this CTA's block of y
+    // rows (every executed pick) into slot [epoch & 1] of every peer's
+    // decode workspace; one system fence before the grid-done count
+    __threadfence_block();
+    const int r1 = min(L.r0 + a.rows_per_cta, d);
+    for (int jj = 0; jj < L.n_exec; ++jj) {
+      const int q0 = s.exec_q[jj];
+      const float* src = a.y + static_cast<int64_t>(q0) * d;
+      for (int r = L.r0 + lane; r < r1; r += 32) {
+        const float v = __ldcg(src + r);
+        for (int g = 0; g < a.ep_G; ++g)
+          (reinterpret_cast<float*>(a.ep_peers[g] + EP_DEC_Y) +
+           (static_cast<int64_t>(a.ep_epoch & 1) * k + q0) * d)[r] = v;
+      }
+    }
+    __threadfence_system();
+    __syncwarp();
+  }
+  if (lane == 0 && cta_done) {
+    if (atomicAdd(a.ctr, 1u) == gridDim.x - 1) {  // grid done: reset for the next call
+      for (int q = 0; q < DK_MAX; ++q) a.ctr[2 + q] = 0;
+      a.ctr[0] = 0;
+      if (a.ep_peers) {                           // every peer: this GPU's picks landed
+        __threadfence_system();
+        for (int q = 0; q < a.ep_G; ++q)
+          st_release_sys(reinterpret_cast<unsigned*>(a.ep_peers[q] + EP_FLAGS_D) + a.ep_rank,
+                         a.ep_epoch);
       }
     }
   }
@@ -732,6 +768,10 @@ extern "C" int daop_decode_workspace(int32_t d, int32_t ffn, int32_t E, int32_t 
   return DAOP_OK;
 }
 
+static thread_local const uint64_t* t_ep_peers = nullptr;
+static thread_local int t_ep_G = 0, t_ep_rank = 0;
+static thread_local unsigned t_ep_epoch = 0;
+
 extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const uint16_t* wg,
                                  const uint16_t* wg_next, const float* pred_prev,
                                  const uint8_t* fast_row, const int32_t* slot_of,
@@ -757,6 +797,7 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
   a.weights_from_pred = weights_from_pred; a.eps = eps;
   a.x_out = x_out; a.p_true = p_true; a.p_pred = wg_next ? p_pred : nullptr; a.sel = sel;
   a.w = w; a.is_fast = is_fast; a.deg = deg; a.y = y; a.h_out = h_out;
+  a.ep_peers = t_ep_peers; a.ep_G = t_ep_G; a.ep_rank = t_ep_rank; a.ep_epoch = t_ep_epoch;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   a.ctr = reinterpret_cast<unsigned*>(ws);
   a.pred_logits = reinterpret_cast<float*>(ws + 128);
@@ -776,6 +817,11 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
     case 6: return launch_decode<12, 2, 6144>(a, grid, st);
     case 7: return launch_decode<16, 1, 8192>(a, grid, st);
     case 8: return launch_decode<10, 2, 7680>(a, grid, st);
+    // Mixtral-8x22B candidates (d = 6144: a W1/W3 row is 12 KB)
+    case 10: return launch_decode<12, 1, 12288>(a, grid, st);
+    case 11: return launch_decode<24, 1, 6144>(a, grid, st);
+    case 12: return launch_decode<8, 2, 9216>(a, grid, st);
+    case 13: return launch_decode<16, 1, 9216>(a, grid, st);
     default: {
       // largest ring that fits: Mixtral-8x22B (d = 6144, ffn = 16384) needs
       // 64 KB of activations in shared memory and a 144 KB router stage
@@ -786,4 +832,31 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
       return launch_decode<16, 1, 8192>(a, grid, st);
     }
   }
+}
+
+// Expert-parallel decode layer: daop_decode_layer whose kernel also stores
+// this GPU's picks' outputs into every peer's decode workspace and flags them
+// (ep_p2p.cu; the share is fused into the phase-2 reduction).
+extern "C" int daop_ep_decode_layer(const uint64_t* d_peers, int32_t rank, int32_t G,
+                                    uint32_t epoch, const float* h, const uint16_t* gamma,
+                                    const uint16_t* wg, const uint16_t* wg_next,
+                                    const uint8_t* fast_row, const int32_t* slot_of,
+                                    const uint16_t* slab, int64_t slot_stride, int32_t d,
+                                    int32_t ffn, int32_t E, int32_t k, float eps,
+                                    uint16_t* x_out, float* p_true, float* p_pred, int32_t* sel,
+                                    float* w, uint8_t* is_fast, int32_t* deg, float* y,
+                                    float* h_out, void* workspace, daop_stream_t stream) {
+  if (!d_peers || G < 1 || G > EP_MAX_G || rank < 0 || rank >= G || d % 4 != 0) {
+    set_error("ep_decode_layer: bad peers / rank %d / world %d", rank, G);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  t_ep_peers = d_peers;
+  t_ep_G = G;
+  t_ep_rank = rank;
+  t_ep_epoch = epoch;
+  const int rc = daop_decode_layer(h, gamma, wg, wg_next, nullptr, fast_row, slot_of, slab,
+                                   slot_stride, d, ffn, E, k, 0, 0, 0, eps, x_out, p_true,
+                                   p_pred, sel, w, is_fast, deg, y, h_out, workspace, 0, stream);
+  t_ep_peers = nullptr;
+  return rc;
 }

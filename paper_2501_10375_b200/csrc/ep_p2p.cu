@@ -245,6 +245,22 @@ __global__ void ep_wait_kernel(uint8_t* ws, int64_t flags_off, int G, unsigned e
   ep_wait_flags(ws, flags_off, G, epoch);
 }
 
+// wait for every owner's picks, then out = h + sum_j w_j y_j (fixed j order,
+// the combine_dense / fused-decode arithmetic)
+__global__ void ep_decode_finish_kernel(uint8_t* ws, int G, int k, int d, const float* h,
+                                        const float* w, float* out, unsigned epoch) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = ep_wait_flags(ws, EP_FLAGS_D, G, epoch);
+  __syncthreads();
+  const float* y = reinterpret_cast<const float*>(ws + EP_DEC_Y) +
+                   static_cast<int64_t>(epoch & 1) * k * d;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) {
+    float o = h[i];
+    for (int q = 0; q < k; ++q) o = fmaf(w[q], y[static_cast<int64_t>(q) * d + i], o);
+    out[i] = o;
+  }
+}
+
 }  // namespace daop
 
 using namespace daop;
@@ -394,5 +410,14 @@ extern "C" int daop_ep_ipc_open(const void* h_handle, int64_t offset, void** h_b
 
 extern "C" int daop_ep_ipc_close(void* h_base) {
   DAOP_CUDA(cudaIpcCloseMemHandle(h_base));
+  return DAOP_OK;
+}
+
+extern "C" int daop_ep_decode_finish(void* d_ws, int32_t G, int32_t k, int32_t d,
+                                     const float* d_h, const float* d_w, float* d_out,
+                                     uint32_t epoch, daop_stream_t st) {
+  ep_decode_finish_kernel<<<(d + 255) / 256, 256, 0, as_stream(st)>>>(
+      static_cast<uint8_t*>(d_ws), G, k, d, d_h, d_w, d_out, epoch);
+  DAOP_CHECK_LAUNCH("ep_decode_finish");
   return DAOP_OK;
 }

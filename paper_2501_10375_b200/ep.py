@@ -502,26 +502,30 @@ class PeerEPDecode:
         self._ipc_bases = []
 
     def stream(self, h: torch.Tensor, layer: int = 0):
-        """Decode kernel on this rank's experts + share of the local picks."""
+        """Decode kernel on this rank's experts; its phase-2 reduction stores
+        the local picks' outputs into every peer's workspace and its last CTA
+        flags them (daop_ep_decode_layer)."""
         from . import _lib, ops
-        m = self.m
+        m, b = self.m, self.bufs
         self.epoch += 1
         nxt = m.gate[layer + 1] if layer + 1 < m.shape.num_layers else None
-        ops.decode_layer(h, m.norm[layer], m.gate[layer], nxt, m.fast[layer], m.slot_of[layer],
-                         m.slab, m.slot_elems, self.d, self.ffn, self.k, self.bufs)
-        _lib.call("daop_ep_decode_share", self.peers.data_ptr(), self.rank, self.world, self.k,
-                  self.d, self.bufs.y.data_ptr(), self.bufs.is_fast.data_ptr(), self.epoch,
-                  ops._s())
+        _lib.call("daop_ep_decode_layer", self.peers.data_ptr(), self.rank, self.world,
+                  self.epoch, h.data_ptr(), m.norm[layer].data_ptr(), m.gate[layer].data_ptr(),
+                  0 if nxt is None else nxt.data_ptr(), m.fast[layer].data_ptr(),
+                  m.slot_of[layer].data_ptr(), m.slab.data_ptr(), m.slot_elems, self.d, self.ffn,
+                  self.E, self.k, float(ops.RMS_EPS), b.x.data_ptr(), b.p.data_ptr(),
+                  b.p_pred.data_ptr(), b.sel.data_ptr(), b.w.data_ptr(), b.is_fast.data_ptr(),
+                  b.deg.data_ptr(), b.y.data_ptr(), b.h_out.data_ptr(), b.ws.data_ptr(), ops._s())
         self._h = h
 
     def finish(self) -> torch.Tensor:
-        """Wait for every owner's outputs, combine -> the next residual."""
+        """Wait for every owner's outputs and combine (one kernel) -> the
+        next residual."""
         from . import _lib, ops
-        _lib.call("daop_ep_decode_wait", self.ws.data_ptr(), self.world, self.epoch, ops._s())
         out = self.out[self.epoch & 1]
-        _lib.call("daop_combine_dense", self._h.data_ptr(),
-                  self.ygather[self.epoch & 1].data_ptr(), self.bufs.w.data_ptr(), self.k,
-                  self.d, out.data_ptr(), ops._s())
+        _lib.call("daop_ep_decode_finish", self.ws.data_ptr(), self.world, self.k, self.d,
+                  self._h.data_ptr(), self.bufs.w.data_ptr(), out.data_ptr(), self.epoch,
+                  ops._s())
         return out
 
     def layer(self, h: torch.Tensor, layer: int = 0) -> torch.Tensor:
