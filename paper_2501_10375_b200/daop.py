@@ -108,6 +108,8 @@ class PrefillResult:
     pred_scores: np.ndarray           # (T, L, E) float64, zero on the last layer
     slow_executions: int
     ms: float
+    migration_ms: float = 0.0         # swap copies, serialised on the migration stream
+    migration_hidden_ms: float = 0.0  # of which overlapped with compute (simulator.py:495-502)
 
 
 @dataclass
@@ -157,8 +159,11 @@ class DaopEngine:
         self._lru = None  # LRU planner of the ondemand / prefetch engines (after prefill)
 
     # ------------------------------------------------------------ residency
-    def _migrate_in(self, layer: int, expert: int, slot: int):
-        """pinned host pool -> HBM slot on the migration stream; returns its event."""
+    def _migrate_in(self, layer: int, expert: int, slot: int, wait: bool = True):
+        """pinned host pool -> HBM slot on the migration stream; returns its
+        event.  wait=False leaves the compute stream free to run other experts
+        while the copy lands (the caller orders the expert's first use after
+        the event; prefill's swapped-in experts, simulator.py:457-471)."""
         m = self.model
         if slot in m._free:
             m._free.remove(slot)
@@ -166,20 +171,27 @@ class DaopEngine:
         self.mig_stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.mig_stream):
             m.slab[slot].copy_(self.pool.slot(layer, expert), non_blocking=True)
-            ev = torch.cuda.Event()
+            ev = torch.cuda.Event(enable_timing=True)
             ev.record(self.mig_stream)
-        torch.cuda.current_stream().wait_event(ev)  # table update ordered after the copy
+        if wait:
+            torch.cuda.current_stream().wait_event(ev)  # table update ordered after the copy
         m._bind(layer, expert, slot)
         self.migrations_done += 1
         return ev
 
     def _apply_swaps(self, layer: int, events):
-        evs = []
+        """Alg. 1's swaps of one layer, serialised on the migration stream
+        (the reference's single interconnect lane, simulator.py:446-456).
+        Returns (start event, per-swap completion events)."""
         m = self.model
+        self.mig_stream.wait_stream(torch.cuda.current_stream())
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(self.mig_stream)
+        evs = []
         for ev in events:
             slot = m.evict(layer, ev.swapped_out)
-            evs.append(self._migrate_in(layer, ev.swapped_in, slot))
-        return evs
+            evs.append(self._migrate_in(layer, ev.swapped_in, slot, wait=False))
+        return start, evs
 
     # ------------------------------------------------------------ prefill
     def prefill(self, h: torch.Tensor) -> PrefillResult:
@@ -193,10 +205,12 @@ class DaopEngine:
         swaps_all = []
         new_sets = [set(s) for s in self.placement0.on_fast]
         slow_execs = 0
+        mig_timing = []  # per layer: (migration start, copies done, resident GEMMs done)
         for l in range(L):
             nxt = m.gate[l + 1] if l + 1 < L else None
             r = ops.router(h, m.norm[l], m.gate[l], nxt, k, hist=hist[:, l], tokens_per_seq=T,
                            hist_seq_stride=L * E)
+            swapped_in, mig_evs = [], []
             if self.config.engine == "daop":
                 # only DAOP reallocates (experiment.py:158-163): Alg. 1 for this
                 # layer right after its gate (placement.py:188-237)
@@ -208,24 +222,56 @@ class DaopEngine:
                        for e in ev1]
                 swaps_all.extend(evs)
                 new_sets[l] = set(after.on_fast[0])
-                self._apply_swaps(l, evs)
-            # experts at the post-swap residence
+                if evs:
+                    mig_start, mig_evs = self._apply_swaps(l, evs)
+                    swapped_in = [e.swapped_in for e in evs]
             pr = ops.permute(r["topk_idx"], E, r["x"])
-            slot_of = m.slot_of[l]
-            act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_of, m.slab, m.n_slots,
-                                     m.slot_elems, d, m.ffn)
-            y = ops.expert_gemm_down(act, pr["offsets"], slot_of, m.slab, m.n_slots,
-                                     m.slot_elems, d, m.ffn)
             off = pr["offsets"].cpu().numpy()
-            resident = m.resident_mask()[l]
-            for e in range(E):
-                a, b = int(off[e]), int(off[e + 1])
-                if a == b or resident[e]:
-                    continue
-                xs = pr["x_perm"][a:b].view(torch.int16).cpu().numpy().view(np.uint16)
-                ys = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
-                y[a:b].copy_(torch.from_numpy(ys))
-                slow_execs += 1
+            resident = m.resident_mask()[l]  # post-swap residence
+            slow = [e for e in range(E) if off[e + 1] > off[e] and not resident[e]]
+            # slow experts' rows -> pinned host memory BEFORE the GEMMs are queued,
+            # so the host tier runs while the GPU computes
+            xs_host = {}
+            for e in slow:
+                a_, b_ = int(off[e]), int(off[e + 1])
+                xs_host[e] = torch.empty((b_ - a_, d), dtype=torch.bfloat16, pin_memory=True)
+                xs_host[e].copy_(pr["x_perm"][a_:b_], non_blocking=True)
+            x_ready = torch.cuda.Event()
+            x_ready.record()
+            # experts at the post-swap residence: first every expert whose weights
+            # are already in HBM, then the swapped-in ones, each after its copy
+            # lands (simulator.py:457-471)
+            slot_now = m.slot_of[l]
+            if swapped_in:
+                slot_now = slot_now.clone()
+                slot_now[swapped_in] = -1
+            rows = pr["x_perm"].shape[0]
+            act = torch.empty((rows, m.ffn), dtype=torch.bfloat16, device=m.device)
+            y = torch.empty((rows, d), dtype=torch.float32, device=m.device)
+            ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_now, m.slab, m.n_slots,
+                               m.slot_elems, d, m.ffn, out=act)
+            ops.expert_gemm_down(act, pr["offsets"], slot_now, m.slab, m.n_slots,
+                                 m.slot_elems, d, m.ffn, out=y)
+            if swapped_in:
+                g1 = torch.cuda.Event(enable_timing=True)
+                g1.record()
+                mig_timing.append((mig_start, mig_evs[-1], g1))
+                for ev in mig_evs:
+                    torch.cuda.current_stream().wait_event(ev)
+                slot_mig = torch.full_like(slot_now, -1)
+                slot_mig[swapped_in] = m.slot_of[l][swapped_in]
+                ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_mig, m.slab, m.n_slots,
+                                   m.slot_elems, d, m.ffn, out=act)
+                ops.expert_gemm_down(act, pr["offsets"], slot_mig, m.slab, m.n_slots,
+                                     m.slot_elems, d, m.ffn, out=y)
+            if slow:
+                x_ready.synchronize()
+                for e in slow:
+                    a_, b_ = int(off[e]), int(off[e + 1])
+                    xs = xs_host[e].view(torch.int16).numpy().view(np.uint16)
+                    ys = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
+                    y[a_:b_].copy_(torch.from_numpy(ys), non_blocking=False)
+                    slow_execs += 1
             out = ops.combine(h, y, pr["inv"], r["topk_w"])
             true_sc[:, l, :] = r["p"].cpu().numpy()
             if nxt is not None:
@@ -236,8 +282,19 @@ class DaopEngine:
         if self.config.engine in ("ondemand", "prefetch"):
             self._lru = make_planner(self.placement, self.config)
         counts = hist[0].to(torch.int64).cpu().numpy()
+        # migration time hidden under compute, measured the way the reference
+        # prices it (simulator.py:495-502): total copy time minus the time the
+        # compute stream actually waited for the copies after its resident
+        # experts were done
+        mig_total = mig_hidden = 0.0
+        for st, done, g1 in mig_timing:
+            tot = st.elapsed_time(done)
+            stall = max(0.0, g1.elapsed_time(done))
+            mig_total += tot
+            mig_hidden += min(max(tot - stall, 0.0), tot)
         return PrefillResult(h, counts, self.placement0, self.placement, swaps_all, true_sc,
-                             pred_sc, slow_execs, 1e3 * (time.perf_counter() - t0))
+                             pred_sc, slow_execs, 1e3 * (time.perf_counter() - t0),
+                             mig_total, mig_hidden)
 
     # ------------------------------------------------------------ decode
     def _host_views(self):

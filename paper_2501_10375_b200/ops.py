@@ -99,20 +99,25 @@ def set_gemm_mode(mode: int) -> None:
     _lib.call("daop_set_gemm_mode", int(mode))
 
 
-def expert_gemm_up(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, group_m=0):
-    _dev(x_perm, offsets, slot_of, slab)
+def expert_gemm_up(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, group_m=0,
+                   out=None):
+    """act rows of every expert with an HBM slot in `slot_of` (experts with
+    slot -1 get no tiles: their rows of `out` are left untouched)."""
+    _dev(x_perm, offsets, slot_of, slab, out)
     rows = x_perm.shape[0]
-    act = torch.empty((rows, ffn), dtype=torch.bfloat16, device=x_perm.device)
+    act = torch.empty((rows, ffn), dtype=torch.bfloat16, device=x_perm.device) if out is None \
+        else out
     _lib.call("daop_expert_gemm_up", x_perm.data_ptr(), rows, d, ffn, slab.data_ptr(), n_slots,
               slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
               act.data_ptr(), group_m, _s())
     return act
 
 
-def expert_gemm_down(act, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, group_m=0):
-    _dev(act, offsets, slot_of, slab)
+def expert_gemm_down(act, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, group_m=0,
+                     out=None):
+    _dev(act, offsets, slot_of, slab, out)
     rows = act.shape[0]
-    y = torch.empty((rows, d), dtype=torch.float32, device=act.device)
+    y = torch.empty((rows, d), dtype=torch.float32, device=act.device) if out is None else out
     _lib.call("daop_expert_gemm_down", act.data_ptr(), rows, d, ffn, slab.data_ptr(), n_slots,
               slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
               y.data_ptr(), group_m, _s())

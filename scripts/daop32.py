@@ -84,6 +84,8 @@ def main():
             "prefill_ms": rec.prefill.ms,
             "prefill_tokens_per_s": a.prompt / (rec.prefill.ms / 1e3),
             "swaps": len(rec.prefill.swaps),
+            "prefill_migration_ms": rec.prefill.migration_ms,
+            "prefill_migration_hidden_ms": rec.prefill.migration_hidden_ms,
             "prefill_slow_expert_batches": rec.prefill.slow_executions,
             "counts": rec.counts,
             "slow_executions_per_token": rec.counts["slow_executions"] / n,

@@ -49,8 +49,9 @@ w13 = [m.slab[m.slot(0, e)][: 2 * ffn * d].view(2 * ffn, d) for e in range(E)]
 w2 = [m.slab[m.slot(0, e)][2 * ffn * d:].view(d, ffn) for e in range(E)]
 
 for cfg in CONFIGS:
-    which, pol, grp = cfg.split(":")
-    ops.set_gemm_mode(int(pol) << 4)
+    which, pol, grp = cfg.split(":")[:3]
+    extra = int(cfg.split(":")[3]) if cfg.count(":") >= 3 else 0  # demote | persist-off bits
+    ops.set_gemm_mode((int(pol) << 4) | (extra << 8))
     grp = int(grp)
 
     def run():

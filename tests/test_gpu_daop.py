@@ -58,6 +58,13 @@ def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
     assert [(s.layer, s.swapped_in, s.swapped_out, s.hot_tokens, s.cold_tokens)
             for s in rec.prefill.swaps] == evs
     assert [set(s) for s in rec.prefill.placement.on_fast] == sets
+    # (a11) swap copies overlap the resident experts' GEMMs; the hidden part is
+    # measured like simulator.py:495-502 prices it
+    pf = rec.prefill
+    if evs:
+        assert pf.migration_ms > 0 and 0.0 <= pf.migration_hidden_ms <= pf.migration_ms
+    else:
+        assert pf.migration_ms == 0.0 and pf.migration_hidden_ms == 0.0
     # the HBM slot table follows the placement (LRU engines move it during decode)
     if engine in ("daop", "fiddler"):
         assert np.array_equal(eng.model.resident_mask(), rec.prefill.placement.mask())
