@@ -147,6 +147,7 @@ class DaopEngine:
                               n_slots=self.placement0.slot_budget, resident_layers=[])
         self.pool = host_pool or HostExpertPool(shape, d_model, d_ff, seed)
         self.mig_stream = torch.cuda.Stream(device=self.model.device)
+        self.h2d_stream = torch.cuda.Stream(device=self.model.device)
         self.migrations_done = 0
         for l, s in enumerate(self.placement0.on_fast):
             for e in sorted(s):
@@ -255,7 +256,7 @@ class DaopEngine:
             if swapped_in:
                 g1 = torch.cuda.Event(enable_timing=True)
                 g1.record()
-                mig_timing.append((mig_start, mig_evs[-1], g1))
+                mig_timing.append([mig_start, mig_evs[-1], g1, None])
                 for ev in mig_evs:
                     torch.cuda.current_stream().wait_event(ev)
                 slot_mig = torch.full_like(slot_now, -1)
@@ -266,12 +267,21 @@ class DaopEngine:
                                      m.slot_elems, d, m.ffn, out=y)
             if slow:
                 x_ready.synchronize()
-                for e in slow:
-                    a_, b_ = int(off[e]), int(off[e + 1])
-                    xs = xs_host[e].view(torch.int16).numpy().view(np.uint16)
-                    ys = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
-                    y[a_:b_].copy_(torch.from_numpy(ys), non_blocking=False)
-                    slow_execs += 1
+                # the host tier's results go up on their own stream, so the GPU
+                # clock records when the slow experts finished (for the hidden-
+                # migration measurement) independently of the GEMM queue
+                with torch.cuda.stream(self.h2d_stream):
+                    for e in slow:
+                        a_, b_ = int(off[e]), int(off[e + 1])
+                        xs = xs_host[e].view(torch.int16).numpy().view(np.uint16)
+                        ys = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
+                        y[a_:b_].copy_(torch.from_numpy(ys), non_blocking=False)
+                        slow_execs += 1
+                    hev = torch.cuda.Event(enable_timing=True)
+                    hev.record(self.h2d_stream)
+                torch.cuda.current_stream().wait_event(hev)
+                if swapped_in:
+                    mig_timing[-1][3] = hev
             out = ops.combine(h, y, pr["inv"], r["topk_w"])
             true_sc[:, l, :] = r["p"].cpu().numpy()
             if nxt is not None:
@@ -284,12 +294,15 @@ class DaopEngine:
         counts = hist[0].to(torch.int64).cpu().numpy()
         # migration time hidden under compute, measured the way the reference
         # prices it (simulator.py:495-502): total copy time minus the time the
-        # compute stream actually waited for the copies after its resident
-        # experts were done
+        # compute stream actually waited for the copies once its resident
+        # experts and the layer's slow (host-tier) experts were done
         mig_total = mig_hidden = 0.0
-        for st, done, g1 in mig_timing:
+        for st, done, g1, hev in mig_timing:
             tot = st.elapsed_time(done)
-            stall = max(0.0, g1.elapsed_time(done))
+            other = st.elapsed_time(g1)  # resident experts' GEMMs done
+            if hev is not None:          # the layer also waits for its slow experts
+                other = max(other, st.elapsed_time(hev))
+            stall = max(0.0, tot - other)
             mig_total += tot
             mig_hidden += min(max(tot - stall, 0.0), tot)
         return PrefillResult(h, counts, self.placement0, self.placement, swaps_all, true_sc,
