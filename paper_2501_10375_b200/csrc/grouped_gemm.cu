@@ -361,6 +361,23 @@ constexpr int P_A_BYTES = 128 * GB_K * 2;                 // 16 KB per CTA
 constexpr int P_B_BYTES = 128 * GB_K * 2;                 // 16 KB per CTA
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;      // 32 KB
 constexpr uint32_t P_IDESC = umma_idesc_bf16_f32(P_M, GB_N);
+// TWO_M variant: 512-row pair tile = two M=256 MMAs per k-step sharing the
+// B box (each CTA holds 256 A rows: two 128-row boxes), so every B byte
+// brought into shared memory feeds twice the MMA work and the operand
+// traffic per FLOP drops by a quarter (the tile shape cuBLAS picks here);
+// the two accumulators fill all 512 TMEM columns (no double buffering).
+constexpr int P2_M = 512;
+constexpr int P2_STAGES = 4;
+constexpr int P2_STAGE_BYTES = 2 * P_A_BYTES + P_B_BYTES; // 48 KB
+
+template <bool TWO_M>
+struct PairCfg {
+  static constexpr int M = TWO_M ? P2_M : P_M;
+  static constexpr int STAGES = TWO_M ? P2_STAGES : P_STAGES;
+  static constexpr int STAGE_BYTES = TWO_M ? P2_STAGE_BYTES : P_STAGE_BYTES;
+  static constexpr int A_BYTES = TWO_M ? 2 * P_A_BYTES : P_A_BYTES;
+  static constexpr int NACC = TWO_M ? 1 : 2;  // TMEM accumulator buffers
+};
 
 struct PairSmem {
   uint64_t full[P_STAGES];
@@ -400,14 +417,15 @@ __device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, 
   return true;
 }
 
-template <bool SWIGLU>
+template <bool SWIGLU, bool TWO_M = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  using C = PairCfg<TWO_M>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
-  PairSmem& s = *reinterpret_cast<PairSmem*>(tiles + P_STAGES * P_STAGE_BYTES);
+  PairSmem& s = *reinterpret_cast<PairSmem*>(tiles + C::STAGES * C::STAGE_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -417,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int i = 0; i < P_STAGES; ++i) {
+    for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&s.full[i], 2);   // leader: own expect_tx arrive + follower's remote arrive
       mbar_init(&s.empty[i], 1);  // multicast commit
     }
@@ -431,7 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     for (int e = 0; e <= E; ++e) s.off[e] = p.offsets[e];
     for (int e = 0; e < E; ++e) {
       const int64_t me = p.slot_of[e] >= 0 ? s.off[e + 1] - s.off[e] : 0;
-      s.mt[e] = static_cast<int>((me + P_M - 1) / P_M);
+      s.mt[e] = static_cast<int>((me + C::M - 1) / C::M);
       acc += s.mt[e] * p.n_tiles;
       s.prefix[e + 1] = acc;
     }
@@ -466,17 +484,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       uint32_t phase = 0;
       int e, m, n;
       for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
-        const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * P_M) + rank * 128;
+        const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * C::M) + rank * 128;
         const int slot = p.slot_of[e];
         const int brow = n * p.b_tile_rows + (leader ? 0 : p.b_half2);
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
-          uint8_t* st = tiles + stage * P_STAGE_BYTES;
-          if (leader) mbar_arrive_expect_tx(&s.full[stage], 2 * P_STAGE_BYTES);
+          uint8_t* st = tiles + stage * C::STAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&s.full[stage], 2 * C::STAGE_BYTES);
           else mbar_arrive_cluster(&s.full[stage], 0);
           tma_load_2d_pair(st, &tmA, &s.full[stage], kb * GB_K, row0, pol_a);
-          tma_load_3d_pair(st + P_A_BYTES, &tmB, &s.full[stage], kb * GB_K, brow, slot, pol_b);
-          if (++stage == P_STAGES) {
+          if constexpr (TWO_M)  // second M=256 half: tile rows 256 + rank * 128
+            tma_load_2d_pair(st + P_A_BYTES, &tmA, &s.full[stage], kb * GB_K, row0 + 256, pol_a);
+          tma_load_3d_pair(st + C::A_BYTES, &tmB, &s.full[stage], kb * GB_K, brow, slot, pol_b);
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -496,29 +516,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&s.full[stage], phase);
           tc_fence_after();
-          uint8_t* st = tiles + stage * P_STAGE_BYTES;
+          uint8_t* st = tiles + stage * C::STAGE_BYTES;
           const uint64_t adesc = umma_desc_sw128(smem_u32(st));
-          const uint64_t bdesc = umma_desc_sw128(smem_u32(st + P_A_BYTES));
+          const uint64_t bdesc = umma_desc_sw128(smem_u32(st + C::A_BYTES));
 #pragma unroll
-          for (int k = 0; k < GB_K / 16; ++k)
+          for (int k = 0; k < GB_K / 16; ++k) {
             umma_bf16_pair(tmem_d, adesc + 2 * k, bdesc + 2 * k, P_IDESC, (kb | k) != 0);
+            if constexpr (TWO_M) {  // same B, second A half -> TMEM columns 256..511
+              const uint64_t adesc1 = umma_desc_sw128(smem_u32(st + P_A_BYTES));
+              umma_bf16_pair(tmem_d + GB_N, adesc1 + 2 * k, bdesc + 2 * k, P_IDESC,
+                             (kb | k) != 0);
+            }
+          }
           umma_commit_pair(&s.empty[stage], 0x3);
-          if (++stage == P_STAGES) {
+          if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
         umma_commit_pair(&s.tfull[acc], 0x3);
         ++iters;
-        if (++acc == 2) {
+        if (++acc == C::NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
       // drain: wait until both epilogues released the last accumulator(s)
-      for (int i = 0; i < 2 && i < iters; ++i) {
+      for (int i = 0; i < C::NACC && i < iters; ++i) {
         mbar_wait(&s.tempty[acc], acc_phase ^ 1);
-        if (++acc == 2) {
+        if (++acc == C::NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -533,11 +559,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
-      const int row_in_tile = rank * 128 + q * 32 + lane;
       const int64_t me = s.off[e + 1] - s.off[e];
-      const bool valid = static_cast<int64_t>(m) * P_M + row_in_tile < me;
-      const int64_t grow = s.off[e] + static_cast<int64_t>(m) * P_M + row_in_tile;
-      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * GB_N;
+#pragma unroll 1
+      for (int half = 0; half < (TWO_M ? 2 : 1); ++half) {
+      const int row_in_tile = half * 256 + rank * 128 + q * 32 + lane;
+      const bool valid = static_cast<int64_t>(m) * C::M + row_in_tile < me;
+      const int64_t grow = s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * GB_N +
+                          half * GB_N;
       if constexpr (SWIGLU) {
         uint16_t* out = static_cast<uint16_t*>(p.out) + grow * p.out_ld + n * 128;
 #pragma unroll 1
@@ -579,10 +608,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
           }
         }
       }
+      }  // half
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&s.tempty[acc], 0);
-      if (p.demote) {
+      if (p.demote && !TWO_M) {
+        const int row_in_tile = rank * 128 + q * 32 + lane;
+        const bool valid = static_cast<int64_t>(m) * C::M + row_in_tile < me;
+        const int64_t grow = s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile;
         if ((p.demote & 1) && p.raster == 0 && n == nt - 1 && valid)  // A m-tile done
           l2_demote_range(p.a_ptr + grow * p.a_ld, p.a_ld * 2);
         if ((p.demote & 2) && p.raster == 1 && m == s.mt[e] - 1) {     // B n-tile done
@@ -592,7 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
                           p.b_ld * 2);
         }
       }
-      if (++acc == 2) {
+      if (++acc == C::NACC) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -613,7 +646,41 @@ static int g_gemm_policy = -1;  // L2 hint set override (tuning); -1 = per-GEMM 
 static int g_gemm_demote = 0;   // bit 0: demote A (up), bit 1: demote B (down)
 
 static size_t gemm_smem_bytes() { return 1024 + G_STAGES * G_STAGE_BYTES + sizeof(GemmSmem); }
-static size_t pair_smem_bytes() { return 1024 + P_STAGES * P_STAGE_BYTES + sizeof(PairSmem); }
+// bit 0: up GEMM, bit 1: down GEMM use the 512-row pair tile.  Default: down
+// only (sustained 5.6-5.8 vs 6.2-6.7 ms on 8 x 4096 tokens, DRAM 13 vs 28 GB,
+// profiles/r01/gemm_two_m.txt); the up GEMM's SwiGLU epilogue cannot overlap
+// the next tile's MMAs without a second accumulator, so it keeps 256 rows
+static int g_gemm_two_m = 2;
+static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
+
+template <bool TWO_M>
+static size_t pair_smem_bytes() {
+  return 1024 + PairCfg<TWO_M>::STAGES * PairCfg<TWO_M>::STAGE_BYTES + sizeof(PairSmem);
+}
+
+template <bool SWIGLU, bool TWO_M>
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                       int64_t rows_total, cudaStream_t st) {
+  using C = PairCfg<TWO_M>;
+  const size_t smem = pair_smem_bytes<TWO_M>();
+  auto kern = grouped_gemm_pair_kernel<SWIGLU, TWO_M>;
+  DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  const int64_t max_tiles = (rows_total / C::M + p.E) * static_cast<int64_t>(p.n_tiles);
+  int clusters = sm_count() / 2;
+  if (max_tiles < clusters) clusters = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
+  GemmParams pp = p;
+  if (p.group_m < 0) {  // negative group = n-grouped raster of |group| weight tiles
+    pp.raster = 1;
+    pp.group_m = -p.group_m;
+  } else {              // group counted in 128-row units -> pair tiles of C::M rows
+    pp.raster = 0;
+    pp.group_m = p.group_m > C::M / 128 ? p.group_m / (C::M / 128) : 1;
+  }
+  kern<<<2 * clusters, G_THREADS, smem, st>>>(ta, tb, pp);
+  DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
+  return DAOP_OK;
+}
 
 template <bool SWIGLU>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
@@ -621,37 +688,31 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
   {
     // L2::evict_last (the A operand, re-read by every n-tile of its group) is
     // only honoured inside the persisting L2 set-aside, which defaults to 0
-    static bool done[64] = {false};
+    // (tuning bit: g_gemm_persist_off leaves / resets it to 0)
+    static int applied[64];
+    static bool init = false;
+    if (!init) {
+      for (int i = 0; i < 64; ++i) applied[i] = -1;
+      init = true;
+    }
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev >= 0 && dev < 64 && !done[dev]) {
-      int max_persist = 0;
-      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-      if (max_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist);
-      cudaGetLastError();
-      done[dev] = true;
+    if (dev >= 0 && dev < 64) {
+      int want = 0;
+      if (!g_gemm_persist_off)
+        cudaDeviceGetAttribute(&want, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      if (applied[dev] != want) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        cudaGetLastError();
+        applied[dev] = want;
+      }
     }
   }
   if (g_gemm_demote & 4) cudaCtxResetPersistingL2Cache();  // tuning: start from a clean set-aside
   if (g_gemm_mode == 0) {
-    const size_t smem = pair_smem_bytes();
-    DAOP_CUDA(cudaFuncSetAttribute(grouped_gemm_pair_kernel<SWIGLU>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    const int64_t max_tiles = (rows_total / P_M + p.E) * static_cast<int64_t>(p.n_tiles);
-    int clusters = sm_count() / 2;
-    if (max_tiles < clusters) clusters = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
-    GemmParams pp = p;
-    if (p.group_m < 0) {  // negative group = n-grouped raster of |group| weight tiles
-      pp.raster = 1;
-      pp.group_m = -p.group_m;
-    } else {
-      pp.raster = 0;
-      pp.group_m = p.group_m > 1 ? p.group_m / 2 : 1;  // group counted in 256-row tiles
-    }
-    grouped_gemm_pair_kernel<SWIGLU><<<2 * clusters, G_THREADS, smem, st>>>(ta, tb, pp);
-    DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
-    return DAOP_OK;
+    const bool two = (g_gemm_two_m >> (SWIGLU ? 0 : 1)) & 1;
+    return two ? launch_pair<SWIGLU, true>(ta, tb, p, rows_total, st)
+               : launch_pair<SWIGLU, false>(ta, tb, p, rows_total, st);
   }
   const size_t smem = gemm_smem_bytes();
   DAOP_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<SWIGLU>,
@@ -691,6 +752,8 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_mode = mode & 15;
   g_gemm_policy = ((mode >> 4) & 15) ? ((mode >> 4) & 15) : -1;
   g_gemm_demote = (mode >> 8) & 7;
+  g_gemm_persist_off = (mode >> 11) & 1;
+  g_gemm_two_m = ((mode >> 12) & 3) ^ 2;  // mode bits flip the default (tuning)
   return DAOP_OK;
 }
 
@@ -739,9 +802,10 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
   const uint32_t bbox[3] = {GB_K, 128, 1};
   const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
   if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
-  // default: n-grouped raster, 8 weight n-tiles per group (DRAM 20 GB vs 25 GB
-  // for m-groups on 8 x 4096 tokens; profiles/r01/gemm_sweep.txt)
-  GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, group_m != 0 ? group_m : -8,
+  // default: n-grouped raster, 16 weight n-tiles per group with the 512-row
+  // tile (8 with the 256-row one); profiles/r01/gemm_two_m.txt, gemm_sweep.txt
+  const int grp = group_m != 0 ? group_m : ((g_gemm_two_m & 2) ? -16 : -8);
+  GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, grp,
                GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0,
                g_gemm_demote & 2, act, ffn, w2, ffn, slot_stride_elems};
   return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
@@ -779,7 +843,8 @@ extern "C" int daop_ep_expert_gemm_down(const uint16_t* act, int64_t rows_cap, i
   const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
   if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
   GemmParams p{reinterpret_cast<const int64_t*>(ws + EP_LOCAL_OFF), d_slot_of, E, ffn / GB_K,
-               d / GB_N, group_m != 0 ? group_m : -8, GB_N, 128, nullptr, d, GB_N,
+               d / GB_N, group_m != 0 ? group_m : ((g_gemm_two_m & 2) ? -16 : -8), GB_N, 128,
+               nullptr, d, GB_N,
                g_gemm_policy >= 0 ? g_gemm_policy : 2, 0, g_gemm_demote & 2, act, ffn, w2, ffn,
                slot_stride_elems, reinterpret_cast<const uint64_t*>(ws + EP_ROWMAP),
                reinterpret_cast<unsigned*>(ws + EP_DONE_GEMM), d_peers, G, rank, epoch};

@@ -41,6 +41,9 @@ def clocks(stop, out):
         time.sleep(0.005)
 
 
+from paper_2501_10375_b200.engine import MoEBlockEngine  # noqa: E402
+eng = MoEBlockEngine(m)
+
 # cuBLAS reference on the same per-expert shapes (bf16 out, no SwiGLU)
 off = pr["offsets"].tolist()
 xs = [pr["x_perm"][off[e]:off[e + 1]] for e in range(E)]
@@ -61,6 +64,8 @@ for cfg in CONFIGS:
         elif which == "cublas_down":
             for e in range(E):
                 torch.matmul(acts[e], w2[e].t())
+        elif which == "prefill":  # the whole layer through the engine, default groups
+            eng.prefill(h, 0)
         elif which == "up":
             ops.expert_gemm_up(pr["x_perm"], pr["offsets"], m.slot_of[0], m.slab, m.n_slots,
                                m.slot_elems, d, ffn, grp)
@@ -83,7 +88,7 @@ for cfg in CONFIGS:
     stop.set()
     th.join()
     ms = e0.elapsed_time(e1) / N
-    fl = 2.0 * T * k * d * ffn * (2 if which.endswith("up") else 1)
+    fl = 2.0 * T * k * d * ffn * (2 if which.endswith("up") else 3 if which == "prefill" else 1)
     print(f"{cfg:12s} {ms:7.3f} ms  {fl / ms / 1e9:7.1f} TF/s  sm {statistics.median(samples):.0f} MHz",
           flush=True)
 ops.set_gemm_mode(0)

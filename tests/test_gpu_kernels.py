@@ -219,7 +219,7 @@ def _gemm_case(P, d, ffn, E, T, k, seed=0):
     return m, om, h, r, pr, act, y, out
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 0x3000])  # pair, single CTA, 512-row pair tiles
 @pytest.mark.parametrize("d,ffn,E,T", [(256, 512, 8, 64), (512, 1024, 8, 700), (4096, 14336, 8, 256)])
 def test_grouped_gemm_parity(P, d, ffn, E, T, mode):
     P[2].set_gemm_mode(mode)
@@ -345,3 +345,21 @@ def test_decode_and_router_nan_input_selects_valid_ids(P):
     torch.cuda.synchronize()
     idx = r["topk_idx"].cpu().numpy()
     assert ((idx >= 0) & (idx < E)).all()
+
+
+@pytest.mark.parametrize("d,ffn,E,T", [(512, 1024, 8, 700), (1024, 2048, 8, 3000)])
+def test_grouped_gemm_two_m_bitexact(P, d, ffn, E, T):
+    """The 512-row pair tile (two M=256 MMAs sharing B) accumulates every
+    output element in the same K order as the 256-row tile: bit-identical."""
+    outs = []
+    for mode in (0, 0x3000):
+        P[2].set_gemm_mode(mode)
+        try:
+            _, _, _, _, pr, act, y, out = _gemm_case(P, d, ffn, E, T, 2)
+        finally:
+            P[2].set_gemm_mode(0)
+        off = pr["offsets"][-1].item()
+        outs.append((act[:off].clone(), y[:off].clone(), out.clone()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert torch.equal(outs[0][2], outs[1][2])
