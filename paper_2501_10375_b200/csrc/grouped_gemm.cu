@@ -37,6 +37,10 @@ constexpr int G_THREADS = 192;
 constexpr int G_MAX_EXPERTS = 64;
 constexpr uint32_t G_IDESC = umma_idesc_bf16_f32(GB_M, GB_N);
 
+// SwiGLU of the GEMM epilogues: hardware ex2 / fast divide (a few ulp in fp32,
+// far below the bf16 rounding of act; the decode GEMV keeps silu_f32)
+__device__ __forceinline__ float silu_fast(float a) { return __fdividef(a, 1.0f + __expf(-a)); }
+
 struct GemmParams {
   const int64_t* offsets;  // [E+1] expert row offsets (device)
   const int32_t* slot_of;  // [E] HBM slot of each expert (device)
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           for (int i = 0; i < 16; ++i) {
             const float a0 = __uint_as_float(g[2 * i]), a1 = __uint_as_float(g[2 * i + 1]);
             const float b0 = __uint_as_float(u[2 * i]), b1 = __uint_as_float(u[2 * i + 1]);
-            const float h0 = silu_f32(a0) * b0, h1 = silu_f32(a1) * b1;
+            const float h0 = silu_fast(a0) * b0, h1 = silu_fast(a1) * b1;
             packed[i] = static_cast<uint32_t>(f32_to_bf16_bits(h0)) |
                         (static_cast<uint32_t>(f32_to_bf16_bits(h1)) << 16);
           }
@@ -377,7 +381,13 @@ struct PairCfg {
   static constexpr int STAGE_BYTES = TWO_M ? P2_STAGE_BYTES : P_STAGE_BYTES;
   static constexpr int A_BYTES = TWO_M ? 2 * P_A_BYTES : P_A_BYTES;
   static constexpr int NACC = TWO_M ? 1 : 2;  // TMEM accumulator buffers
+  // TWO_M: 8 epilogue warps (two per TMEM lane quarter, one per accumulator
+  // half) drain the single accumulator twice as fast -- the MMAs of the next
+  // tile wait for it
+  static constexpr int EPI_WARPS = TWO_M ? 8 : 4;
+  static constexpr int THREADS = (2 + EPI_WARPS) * 32;
 };
+
 
 struct PairSmem {
   uint64_t full[P_STAGES];
@@ -418,7 +428,7 @@ __device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, 
 }
 
 template <bool SWIGLU, bool TWO_M = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THREADS, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   using C = PairCfg<TWO_M>;
@@ -441,7 +451,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s.tfull[i], 1);   // multicast commit
-      mbar_init(&s.tempty[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      mbar_init(&s.tempty[i], 2 * C::EPI_WARPS);  // epilogue warps x 2 CTAs (leader's copy)
     }
     fence_mbar_init();
     int acc = 0;
@@ -560,8 +570,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t me = s.off[e + 1] - s.off[e];
-#pragma unroll 1
-      for (int half = 0; half < (TWO_M ? 2 : 1); ++half) {
+      const int half = TWO_M ? (warp - 2) >> 2 : 0;  // this warp's accumulator half
+      {
       const int row_in_tile = half * 256 + rank * 128 + q * 32 + lane;
       const bool valid = static_cast<int64_t>(m) * C::M + row_in_tile < me;
       const int64_t grow = s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile;
@@ -578,8 +588,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float h0 = silu_f32(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
-            const float h1 = silu_f32(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+            const float h0 = silu_fast(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+            const float h1 = silu_fast(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
             packed[i] = static_cast<uint32_t>(f32_to_bf16_bits(h0)) |
                         (static_cast<uint32_t>(f32_to_bf16_bits(h1)) << 16);
           }
@@ -608,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
           }
         }
       }
-      }  // half
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&s.tempty[acc], 0);
@@ -646,11 +656,11 @@ static int g_gemm_policy = -1;  // L2 hint set override (tuning); -1 = per-GEMM 
 static int g_gemm_demote = 0;   // bit 0: demote A (up), bit 1: demote B (down)
 
 static size_t gemm_smem_bytes() { return 1024 + G_STAGES * G_STAGE_BYTES + sizeof(GemmSmem); }
-// bit 0: up GEMM, bit 1: down GEMM use the 512-row pair tile.  Default: down
-// only (sustained 5.6-5.8 vs 6.2-6.7 ms on 8 x 4096 tokens, DRAM 13 vs 28 GB,
-// profiles/r01/gemm_two_m.txt); the up GEMM's SwiGLU epilogue cannot overlap
-// the next tile's MMAs without a second accumulator, so it keeps 256 rows
-static int g_gemm_two_m = 2;
+// bit 0: up GEMM, bit 1: down GEMM use the 512-row pair tile.  Default: both
+// (down: sustained 5.6-6.0 vs 6.2-6.7 ms on 8 x 4096 tokens, DRAM 13 vs 28 GB;
+// up, with 8 epilogue warps and the fast SwiGLU: 11.8 vs 12.0 ms; whole layer
+// 19.2 vs 19.6 ms -- profiles/r01/gemm_two_m.txt)
+static int g_gemm_two_m = 3;
 static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
 
 template <bool TWO_M>
@@ -677,7 +687,7 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
     pp.raster = 0;
     pp.group_m = p.group_m > C::M / 128 ? p.group_m / (C::M / 128) : 1;
   }
-  kern<<<2 * clusters, G_THREADS, smem, st>>>(ta, tb, pp);
+  kern<<<2 * clusters, C::THREADS, smem, st>>>(ta, tb, pp);
   DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
   return DAOP_OK;
 }
@@ -753,7 +763,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_policy = ((mode >> 4) & 15) ? ((mode >> 4) & 15) : -1;
   g_gemm_demote = (mode >> 8) & 7;
   g_gemm_persist_off = (mode >> 11) & 1;
-  g_gemm_two_m = ((mode >> 12) & 3) ^ 2;  // mode bits flip the default (tuning)
+  g_gemm_two_m = ((mode >> 12) & 3) ^ 3;  // mode bits flip the default (tuning)
   return DAOP_OK;
 }
 

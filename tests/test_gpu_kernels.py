@@ -219,7 +219,7 @@ def _gemm_case(P, d, ffn, E, T, k, seed=0):
     return m, om, h, r, pr, act, y, out
 
 
-@pytest.mark.parametrize("mode", [0, 1, 0x3000])  # pair, single CTA, 512-row pair tiles
+@pytest.mark.parametrize("mode", [0, 1, 0x3000])  # 512-row pair tiles, single CTA, 256-row pair tiles
 @pytest.mark.parametrize("d,ffn,E,T", [(256, 512, 8, 64), (512, 1024, 8, 700), (4096, 14336, 8, 256)])
 def test_grouped_gemm_parity(P, d, ffn, E, T, mode):
     P[2].set_gemm_mode(mode)
