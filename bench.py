@@ -297,6 +297,28 @@ def run_b200(args, world, rank, local_rank):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = world * ne / float(te.item())
 
+    # -------- the same calls through the persistent decode server (no launch,
+    # no stream synchronisation per call; MoEBlockEngine.decode_server)
+    e2e_server = None
+    try:
+        with eng.decode_server() as srv:
+            for i in range(min(args.warmup, 20)):
+                srv.step(hh[i % 8])
+            t0 = time.perf_counter()
+            for i in range(ne):
+                srv.step(hh[i % 8])
+            wall_s = time.perf_counter() - t0
+        ts = torch.tensor([wall_s], device=dev)
+        if world > 1:
+            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        e2e_server = {"value": world * ne / float(ts.item()), "unit": "tokens/s",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                      "api": "MoEBlockEngine.decode_server().step (persistent kernel, "
+                             "host doorbell, result in pinned host memory)"}
+    except Exception as exc:
+        e2e_server = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    torch.cuda.synchronize()
+
     # -------- 32-layer decode token (BASELINE configs[2], ECR 1.0: all experts in HBM)
     decode32 = None
     if not args.no_decode32:
@@ -389,7 +411,8 @@ def run_b200(args, world, rank, local_rank):
                      "frac_of_8tbs": achieved / 8000.0},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "api": "MoEBlockEngine.decode_host"},
+        "e2e_server": e2e_server,
         "gpu_launches": args.steps,
         "clocks": clocks,
         "prefill": prefill,

@@ -305,6 +305,28 @@ int daop_decode_layer(const float* d_h, const uint16_t* d_gamma, const uint16_t*
 /* variant: ring geometry (warps x stages x stage bytes); 0 = default
  * (16 x 1 x 10 KB), 1..9 = tuning alternatives.  num_experts <= 16. */
 
+/* ------------------------------------------------ persistent decode server (b = 1)
+ * The end-to-end decode call without a launch or a stream synchronisation
+ * per call: daop_server_start launches ONE persistent cooperative kernel for
+ * a layer (mode 0; arguments as daop_decode_layer, d_h_out / d_sel normally
+ * pinned host memory); each daop_server_step copies h into pinned memory,
+ * rings a doorbell the kernel polls, and spins until the kernel has written
+ * the residual and the selection to the host.  The kernel holds every SM
+ * until daop_server_stop, or exits by itself after idle_ms without a call.
+ * (The reference's decode step is priced, not executed: simulator.py:289-391.) */
+int daop_server_start(const uint16_t* d_gamma, const uint16_t* d_wg, const uint16_t* d_wg_next,
+                      const uint8_t* d_fast_row, const int32_t* d_slot_of,
+                      const uint16_t* d_slab, int64_t slot_stride_elems, int32_t d, int32_t ffn,
+                      int32_t num_experts, int32_t k, float eps, uint16_t* d_x_out,
+                      float* d_p_true, float* d_p_pred, int32_t* sel, float* d_w,
+                      uint8_t* d_is_fast, int32_t* d_deg, float* d_y, float* h_out,
+                      void* d_workspace, double idle_ms, daop_stream_t stream, void** handle);
+int daop_server_step(void* handle, const float* h_in, double timeout_ms);
+int daop_server_stop(void* handle);
+/* profiling aid: per-call GPU timestamps of servers started afterwards
+ * (d_buf [cap][4] u64 zeroed: doorbell seen, input released, body done) */
+int daop_server_trace(uint64_t* d_buf, int32_t cap);
+
 /* ------------------------------------------------ trace files (moesim JSONL)
  * Formats one phase's token records of a RoutingTrace exactly as
  * moesim/trace.py:328-362 save_trace does ("%.17g" scores, "null" where the

@@ -25,6 +25,11 @@ PROTOS = {
     "daop_device_info": [P, P, P],
     "daop_graph_step": [P, P, P, P, I64],
     "daop_graph_step_mode": [I32],
+    "daop_server_start": [P, P, P, P, P, P, I64, I32, I32, I32, I32, F32, P, P, P, P, P, P, P,
+                          P, P, P, F64, P, P],
+    "daop_server_step": [P, P, F64],
+    "daop_server_stop": [P],
+    "daop_server_trace": [P, I32],
     "daop_topk_rows_f64": [P, I64, I32, I32, P, P],
     "daop_topk_rows_f32": [P, I64, I32, I32, P, P],
     "daop_activation_counts": [P, I64, I32, I32, I32, P, P],

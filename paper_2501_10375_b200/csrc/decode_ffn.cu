@@ -30,6 +30,10 @@
 // (DS stages x DSB bytes, L2 evict_first).  Bytes per call (Mixtral-8x7B,
 // 2 resident picks): 2 x 3 x 4096 x 14336 x 2 B of weights + 2 x 8 x 4096 x
 // 2 B of gates = 704,774,144 B -> HBM roofline.
+#include <atomic>
+#include <chrono>
+#include <cstring>
+
 #include "common.cuh"
 #include "decide.cuh"
 #include "ep.cuh"
@@ -76,6 +80,12 @@ struct DecodeArgs {
   const uint64_t* ep_peers;
   int ep_G, ep_rank;
   unsigned ep_epoch;
+  // persistent decode server (daop_server_*): the grid's last CTA publishes
+  // host_seq into this pinned host word once h_out / sel are in host memory
+  unsigned* host_done;
+  unsigned host_seq;
+  float* host_out;         // pinned host copies of h_out / sel (server mode)
+  int32_t* host_sel;
 };
 
 __device__ unsigned long long g_decode_timeline[1024][16];
@@ -84,6 +94,12 @@ __device__ int g_decode_timeline_on;
 // SM cycle counter (per-SM; phases are compared within one CTA).  %globaltimer
 // was too coarse to resolve the sub-microsecond phase-0 steps.
 __device__ __forceinline__ unsigned long long gtimer() { return clock64(); }
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct Piece {   // what one ring stage holds
   int kind;      // 1 = W1/W3 piece, 2 = W2 piece, 0 = end of stream
@@ -160,7 +176,7 @@ __device__ __forceinline__ int degrade_smem(const float* s, int E, int* sel, int
 }
 
 template <int DW, int DS, int DSB>
-__global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) {
+__device__ __forceinline__ void decode_body(const DecodeArgs a) {
   constexpr int NT = DW * 32;
   extern __shared__ __align__(128) uint8_t smem[];
   const int d = a.d, E = a.E, k = a.k;
@@ -176,6 +192,7 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool tl = g_decode_timeline_on != 0 && blockIdx.x < 1024;
   const bool pred_row = a.wg_next && blockIdx.x < static_cast<unsigned>(E);
+  bool wrote_out = false;  // this thread stored part of the result (host memory in server mode)
 
   // staging of the router inputs in the (still idle) ring area, mode 0 only
   float* h_s = reinterpret_cast<float*>(ring);
@@ -563,6 +580,7 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
       if (lane < E) a.p_true[lane] = s.p[lane];
       if (lane < k) {
         a.sel[lane] = s.sel[lane];
+        wrote_out = true;
         a.w[lane] = s.wsel[lane];
         a.is_fast[lane] = s.fast[lane];
         a.deg[lane] = lane < s.nd ? s.drop[lane] : -1;
@@ -656,12 +674,18 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
             a.y[static_cast<int64_t>(s.exec_q[jj]) * d + pc.row] = yv;
             o = fmaf(s.wsel[s.exec_q[jj]], yv, o);
           }
-          if (all_fast) a.h_out[pc.row] = o;
+          if (all_fast) {
+            a.h_out[pc.row] = o;
+            wrote_out = true;
+          }
         }
       }
     }
   }
   publish();
+  // decode server: this thread's result stores (h_out rows, the selection, in
+  // HBM) are visible to the grid's last warp, which ships them to the host
+  if (a.host_done && wrote_out) __threadfence();
   int cta_done = 0;
   if (lane == 0) {
     if (tl) atomicMax(&g_decode_timeline[blockIdx.x][4], gtimer());
@@ -688,8 +712,11 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
     __threadfence_system();
     __syncwarp();
   }
-  if (lane == 0 && cta_done) {
-    if (atomicAdd(a.ctr, 1u) == gridDim.x - 1) {  // grid done: reset for the next call
+  int grid_done = 0;
+  if (lane == 0 && cta_done) grid_done = atomicAdd(a.ctr, 1u) == gridDim.x - 1;
+  grid_done = __shfl_sync(0xffffffffu, grid_done, 0);
+  if (grid_done) {  // the grid's last warp: reset for the next call, publish
+    if (lane == 0) {
       for (int q = 0; q < DK_MAX; ++q) a.ctr[2 + q] = 0;
       a.ctr[0] = 0;
       if (a.ep_peers) {                           // every peer: this GPU's picks landed
@@ -699,11 +726,137 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
                          a.ep_epoch);
       }
     }
+    if (a.host_done) {
+      // decode server: the result (written to HBM by every CTA) leaves for
+      // pinned host memory in 16-byte stores from this one warp -- a few
+      // hundred large PCIe writes instead of d scattered 4-byte ones
+      // (two bulk DMAs through this CTA's now idle ring: HBM -> smem -> host)
+      __threadfence();
+      if (lane == 0) {
+        if (a.host_out && all_fast) {
+          uint64_t* bar = &s.bar[0][0];  // re-armed below for the next call's init
+          mbar_init(bar, 1);
+          fence_mbar_init();
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // h_out rows: generic -> bulk
+          mbar_arrive_expect_tx(bar, d * 4);
+          bulk_g2s_plain(ring, a.h_out, d * 4, bar);
+          mbar_wait(bar, 0);
+          asm volatile(
+              "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+              "cp.async.bulk.commit_group;\n\t"
+              "cp.async.bulk.wait_group 0;" ::"l"(a.host_out), "r"(smem_u32(ring)), "r"(d * 4)
+              : "memory");
+          asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+        }
+        if (a.host_sel)
+          for (int q = 0; q < k; ++q) a.host_sel[q] = __ldcg(a.sel + q);
+        __threadfence_system();
+        st_release_sys(a.host_done, a.host_seq);
+      }
+      __syncwarp();
+    }
   }
 }
 
 template <int DW, int DS, int DSB>
-static int launch_decode(DecodeArgs a, int grid, cudaStream_t st) {
+__global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) {
+  decode_body<DW, DS, DSB>(a);
+}
+
+// ---------------------------------------------------------------- decode server
+//
+// A persistent cooperative launch that serves decode calls from the host
+// without a kernel launch or a stream synchronisation per call: the host
+// writes h into pinned memory and rings a doorbell word; CTA 0 sees it (PCIe
+// poll), pulls h into HBM and releases the grid through a device flag; the
+// grid runs the decode layer (decode_body, unchanged), writing the residual
+// and the selection straight into pinned host memory; the last CTA fences
+// and publishes the call's sequence number to a pinned `done` word the host
+// spins on.  Idle longer than idle_ns (or doorbell = ~0u) ends the kernel.
+struct ServerArgs {
+  const unsigned* doorbell;  // pinned host: sequence number of the requested call, ~0u = stop
+  const float* h_host;       // pinned host: the call's residual (d floats)
+  unsigned* go;              // device: sequence released to the grid (~0u = stop)
+  unsigned long long idle_ns;
+  unsigned long long* trace;  // optional [calls][4] globaltimer: seen, released, body done, -
+  int trace_cap;
+};
+
+// the doorbell is written by the CPU: acquire at system scope, so the h the
+// host stored before ringing is what the following loads see
+__device__ __forceinline__ unsigned ld_doorbell(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int DW, int DS, int DSB>
+__global__ void __launch_bounds__(DW * 32, 1) decode_server_kernel(DecodeArgs a, ServerArgs sv) {
+  // (no static shared memory here: the 8x7B layer uses all 227 KB dynamically)
+  for (unsigned seq = 1;; ++seq) {
+    unsigned v = 0;
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = globaltimer_ns();
+      if (blockIdx.x == 0) {
+        while ((v = ld_doorbell(sv.doorbell)) != seq && v != ~0u) {
+          if (globaltimer_ns() - t0 > sv.idle_ns) {
+            v = ~0u;
+            break;
+          }
+        }
+        if (sv.trace && seq <= static_cast<unsigned>(sv.trace_cap))
+          sv.trace[(seq - 1) * 4] = globaltimer_ns();
+      } else {
+        while ((v = ld_acquire_gpu(sv.go)) != seq && v != ~0u) {
+          if (globaltimer_ns() - t0 > sv.idle_ns + 1000000000ull) {
+            v = ~0u;
+            break;
+          }
+        }
+      }
+    }
+    if (__syncthreads_or(threadIdx.x == 0 && v == ~0u)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) st_release_gpu(sv.go, ~0u);
+      return;
+    }
+    if (blockIdx.x == 0) {  // h: pinned host -> (one bulk DMA) smem -> HBM, release the grid
+      extern __shared__ __align__(128) uint8_t smem_s[];
+      uint64_t* bar = reinterpret_cast<uint64_t*>(smem_s + a.d * 4);
+      if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, a.d * 4);
+        bulk_g2s_plain(smem_s, sv.h_host, a.d * 4, bar);
+      }
+      __syncthreads();
+      mbar_wait(bar, 0);
+      __syncthreads();
+      if (threadIdx.x == 0)  // the barrier's bytes become ring space for the body
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+      const float4* src = reinterpret_cast<const float4*>(smem_s);
+      float4* dst = reinterpret_cast<float4*>(const_cast<float*>(a.h));
+      for (int i = threadIdx.x; i < a.d / 4; i += DW * 32) dst[i] = src[i];
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        st_release_gpu(sv.go, seq);
+        if (sv.trace && seq <= static_cast<unsigned>(sv.trace_cap))
+          sv.trace[(seq - 1) * 4 + 1] = globaltimer_ns();
+      }
+    }
+    if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // h -> bulk copies
+    __syncthreads();
+    DecodeArgs b = a;
+    b.host_seq = seq;
+    decode_body<DW, DS, DSB>(b);
+    __syncthreads();  // shared state is re-initialised by the next call
+    if (sv.trace && threadIdx.x == 0 && seq <= static_cast<unsigned>(sv.trace_cap))
+      atomicMax(&sv.trace[(seq - 1) * 4 + 2], globaltimer_ns());
+  }
+}
+
+template <int DW, int DS, int DSB>
+static int launch_decode(DecodeArgs a, int grid, cudaStream_t st, const ServerArgs* sv = nullptr) {
   a.rows_per_cta = (a.d + grid - 1) / grid;
   const int npc2 = (a.ffn * 2 + DSB - 1) / DSB;
   if (npc2 > kMaxChunks) {
@@ -726,7 +879,10 @@ static int launch_decode(DecodeArgs a, int grid, cudaStream_t st) {
     return DAOP_ERR_UNSUPPORTED;
   }
   auto kern = decode_layer_kernel<DW, DS, DSB>;
-  DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto skern = decode_server_kernel<DW, DS, DSB>;
+  DAOP_CUDA(cudaFuncSetAttribute(sv ? reinterpret_cast<const void*>(skern)
+                                    : reinterpret_cast<const void*>(kern),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -738,7 +894,8 @@ static int launch_decode(DecodeArgs a, int grid, cudaStream_t st) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DAOP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  if (sv) DAOP_CUDA(cudaLaunchKernelEx(&cfg, skern, a, *sv));
+  else DAOP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   return DAOP_OK;
 }
 
@@ -790,7 +947,7 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
     set_error("decode_layer: PLAN mode needs the previous layer's prediction");
     return DAOP_ERR_PREDICTION_MISSING;
   }
-  DecodeArgs a;
+  DecodeArgs a{};  // value-initialised: optional pointers (EP, server) stay null
   a.h = h; a.gamma = gamma; a.wg = wg; a.wg_next = wg_next; a.pred_prev = pred_prev;
   a.fast_row = fast_row; a.slot_of = slot_of; a.slab = slab; a.slot_stride = slot_stride;
   a.d = d; a.ffn = ffn; a.E = E; a.k = k; a.mode = mode; a.graceful = graceful;
@@ -859,4 +1016,145 @@ extern "C" int daop_ep_decode_layer(const uint64_t* d_peers, int32_t rank, int32
                                    p_pred, sel, w, is_fast, deg, y, h_out, workspace, 0, stream);
   t_ep_peers = nullptr;
   return rc;
+}
+
+// ---------------------------------------------------------------- decode server C ABI
+
+static unsigned long long* g_server_trace = nullptr;  // profiling aid (daop_server_trace)
+static int g_server_trace_cap = 0;
+
+// profiling aid: per-call GPU timestamps of the next server started
+// ([seq][4]: doorbell seen, h released to the grid, body done; device memory)
+extern "C" int daop_server_trace(uint64_t* d_buf, int32_t cap) {
+  g_server_trace = reinterpret_cast<unsigned long long*>(d_buf);
+  g_server_trace_cap = cap;
+  return DAOP_OK;
+}
+
+namespace {
+struct DecodeServer {
+  unsigned* doorbell = nullptr;  // pinned host
+  unsigned* done = nullptr;      // pinned host
+  float* h_host = nullptr;       // pinned host staging of the input residual
+  unsigned* go = nullptr;        // device
+  float* h_dev = nullptr;        // device copy of the input
+  float* out_dev = nullptr;      // device residual out (shipped to the host by the last warp)
+  int32_t* sel_dev = nullptr;
+  unsigned seq = 0;
+  int d = 0;
+  cudaStream_t stream = nullptr;
+};
+}  // namespace
+
+static void server_free(DecodeServer* s) {
+  if (s->doorbell) cudaFreeHost(s->doorbell);
+  if (s->h_host) cudaFreeHost(s->h_host);
+  if (s->go) cudaFree(s->go);
+  if (s->h_dev) cudaFree(s->h_dev);
+  if (s->out_dev) cudaFree(s->out_dev);
+  if (s->sel_dev) cudaFree(s->sel_dev);
+  delete s;
+}
+
+// Start a persistent decode server for one MoE layer (mode 0, all arguments
+// as daop_decode_layer; d_h_out and d_sel should be pinned host memory --
+// the kernel writes the result there).  The server kernel occupies every SM
+// until daop_server_stop or idle_ms without a call.
+extern "C" int daop_server_start(const uint16_t* gamma, const uint16_t* wg,
+                                 const uint16_t* wg_next, const uint8_t* fast_row,
+                                 const int32_t* slot_of, const uint16_t* slab,
+                                 int64_t slot_stride, int32_t d, int32_t ffn, int32_t E,
+                                 int32_t k, float eps, uint16_t* x_out, float* p_true,
+                                 float* p_pred, int32_t* sel, float* w, uint8_t* is_fast,
+                                 int32_t* deg, float* y, float* h_out, void* workspace,
+                                 double idle_ms, daop_stream_t stream, void** handle) {
+  if (E < 2 || E > DE_MAX || k < 1 || k > DK_MAX || k > E || d % 8 || ffn % 8) {
+    set_error("decode server: unsupported shape (E=%d k=%d d=%d ffn=%d)", E, k, d, ffn);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  auto* s = new DecodeServer();
+  s->d = d;
+  s->stream = as_stream(stream);
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&s->doorbell), 256, cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&s->h_host), d * 4,
+                                          cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&s->go), 256);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&s->h_dev), d * 4);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&s->out_dev), d * 4);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&s->sel_dev), 64);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->go, 0, 256, s->stream);
+  if (e != cudaSuccess) {
+    server_free(s);
+    return cuda_fail(e, "decode server allocation");
+  }
+  s->done = s->doorbell + 32;  // separate 128-byte line
+  *reinterpret_cast<volatile unsigned*>(s->doorbell) = 0;
+  *reinterpret_cast<volatile unsigned*>(s->done) = 0;
+  DecodeArgs a{};
+  a.h = s->h_dev; a.gamma = gamma; a.wg = wg; a.wg_next = wg_next; a.pred_prev = nullptr;
+  a.fast_row = fast_row; a.slot_of = slot_of; a.slab = slab; a.slot_stride = slot_stride;
+  a.d = d; a.ffn = ffn; a.E = E; a.k = k; a.mode = 0; a.graceful = 0;
+  a.weights_from_pred = 0; a.eps = eps;
+  a.x_out = x_out; a.p_true = p_true; a.p_pred = wg_next ? p_pred : nullptr;
+  a.w = w; a.is_fast = is_fast; a.deg = deg; a.y = y;
+  a.h_out = s->out_dev;  // every CTA writes HBM; the last warp ships it to the host
+  a.sel = s->sel_dev;
+  a.host_out = h_out;
+  a.host_sel = sel;
+  a.ep_peers = nullptr;
+  a.host_done = s->done;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  a.ctr = reinterpret_cast<unsigned*>(ws);
+  a.pred_logits = reinterpret_cast<float*>(ws + 128);
+  a.act = reinterpret_cast<uint16_t*>(ws + 128 + (static_cast<int64_t>(E) * 4 + 255) / 256 * 256);
+  ServerArgs sv{s->doorbell, s->h_host, s->go,
+                static_cast<unsigned long long>(idle_ms * 1e6), g_server_trace,
+                g_server_trace_cap};
+  int grid = sm_count();
+  if (grid < E) grid = E;
+  int rc = launch_decode<16, 1, 10240>(a, grid, s->stream, &sv);
+  if (rc == DAOP_ERR_UNSUPPORTED) rc = launch_decode<16, 1, 9216>(a, grid, s->stream, &sv);
+  if (rc == DAOP_ERR_UNSUPPORTED) rc = launch_decode<16, 1, 8192>(a, grid, s->stream, &sv);
+  if (rc) {
+    server_free(s);
+    return rc;
+  }
+  *handle = s;
+  return DAOP_OK;
+}
+
+// One call: h (d floats, any host memory) -> the server; returns once the
+// residual and the selection are in the pinned host buffers given at start.
+extern "C" int daop_server_step(void* handle, const float* h_src, double timeout_ms) {
+  auto* s = static_cast<DecodeServer*>(handle);
+  memcpy(s->h_host, h_src, static_cast<size_t>(s->d) * 4);
+  const unsigned seq = ++s->seq;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *reinterpret_cast<volatile unsigned*>(s->doorbell) = seq;
+  const auto t0 = std::chrono::steady_clock::now();
+  unsigned spins = 0;
+  while (*reinterpret_cast<volatile unsigned*>(s->done) != seq) {
+    if ((++spins & 1023) == 0) {
+      const double ms = std::chrono::duration<double, std::milli>(
+          std::chrono::steady_clock::now() - t0).count();
+      if (ms > timeout_ms) {
+        const cudaError_t q = cudaStreamQuery(s->stream);
+        set_error("decode server: call %u not answered in %.0f ms (server %s)", seq, ms,
+                  q == cudaSuccess ? "exited (idle timeout?)" : "running");
+        return DAOP_ERR_CUDA;
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  return DAOP_OK;
+}
+
+extern "C" int daop_server_stop(void* handle) {
+  auto* s = static_cast<DecodeServer*>(handle);
+  *reinterpret_cast<volatile unsigned*>(s->doorbell) = ~0u;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  const cudaError_t e = cudaStreamSynchronize(s->stream);
+  server_free(s);
+  DAOP_CUDA(e);
+  return DAOP_OK;
 }

@@ -99,6 +99,15 @@ class MoEBlockEngine:
         _lib.check(c[0](c[1], c[2], c[3], c[3], c[4]), "daop_graph_step")
         return self._out_host, self._sel_host
 
+    def decode_server(self, layer: int = 0, idle_ms: float = 5000.0):
+        """Persistent serving mode of `decode_host` (daop_server_*): one
+        resident kernel answers every call -- h is read from pinned host
+        memory when the host rings, the residual and the selection are written
+        back to pinned host memory -- so a call costs no launch and no stream
+        synchronisation.  The kernel holds every SM: use it as a context
+        manager and run no other GPU work while it is open."""
+        return DecodeServer(self, layer, idle_ms)
+
     @staticmethod
     def host_bytes(d: int, k: int):
         """(h2d, d2h) bytes of one decode_host call: h in; the residual and
@@ -168,3 +177,59 @@ class MoEBlockEngine:
         """Kernel launches of one prefill layer: router, permute (count, scan,
         scatter, gather), up GEMM, down GEMM, combine."""
         return 8
+
+
+class DecodeServer:
+    """See MoEBlockEngine.decode_server."""
+
+    def __init__(self, eng: MoEBlockEngine, layer: int, idle_ms: float):
+        import ctypes
+        m = eng.model
+        self.eng = eng
+        self.d, self.k = eng.d, eng.k
+        self.out = torch.empty(self.d, dtype=torch.float32, pin_memory=True)
+        self.sel = torch.empty(self.k, dtype=torch.int32, pin_memory=True)
+        self.bufs = ops.DecodeBuffers(eng.d, eng.ffn, eng.E, eng.k, eng.device)
+        self.stream = torch.cuda.Stream(eng.device)
+        nxt = m.gate[layer + 1] if layer + 1 < m.shape.num_layers else None
+        b = self.bufs
+        self._h = ctypes.c_void_p()
+        torch.cuda.synchronize(eng.device)  # weights and buffers ready before the kernel starts
+        _lib.call("daop_server_start", m.norm[layer].data_ptr(), m.gate[layer].data_ptr(),
+                  0 if nxt is None else nxt.data_ptr(), m.fast[layer].data_ptr(),
+                  m.slot_of[layer].data_ptr(), m.slab.data_ptr(), m.slot_elems, eng.d, eng.ffn,
+                  eng.E, eng.k, float(ops.RMS_EPS), b.x.data_ptr(), b.p.data_ptr(),
+                  b.p_pred.data_ptr(), self.sel.data_ptr(), b.w.data_ptr(),
+                  b.is_fast.data_ptr(), b.deg.data_ptr(), b.y.data_ptr(), self.out.data_ptr(),
+                  b.ws.data_ptr(), float(idle_ms), self.stream.cuda_stream, ctypes.byref(self._h))
+        self._step = _lib.LIB.daop_server_step
+
+    def step(self, h_host: torch.Tensor, timeout_ms: float = 5000.0):
+        """One decode call: h (d,) fp32 in host memory -> (residual, selection)
+        in pinned host memory (valid until the next call)."""
+        if self._h is None:
+            raise RuntimeError("decode server is closed")
+        if h_host.dtype is not torch.float32 or h_host.is_cuda or not h_host.is_contiguous() \
+                or h_host.numel() != self.d:
+            h_host = h_host.to(device="cpu", dtype=torch.float32).contiguous().view(-1)
+        rc = self._step(self._h, h_host.data_ptr(), float(timeout_ms))
+        if rc:
+            _lib.check(rc, "daop_server_step")
+        return self.out, self.sel
+
+    def close(self):
+        if self._h is not None:
+            h, self._h = self._h, None
+            _lib.call("daop_server_stop", h)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

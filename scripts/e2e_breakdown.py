@@ -61,3 +61,29 @@ with torch.cuda.graph(g3):
 def empty():
     g3.replay(); torch.cuda.current_stream().synchronize()
 print("empty graph replay + sync us", wall(empty))
+
+# persistent decode server: no launch, no stream sync per call
+# (no torch.cuda.synchronize() while it is open: the server kernel only ends
+# when closed or idle)
+with eng.decode_server() as srv:
+    for _ in range(20):
+        srv.step(hh)
+    t = time.perf_counter()
+    for _ in range(1000):
+        srv.step(hh)
+    print("decode server us/step", (time.perf_counter() - t) / 1000 * 1e6)
+
+# where the server's per-call time goes (GPU globaltimer stamps)
+tr = torch.zeros((1200, 4), dtype=torch.int64, device="cuda")
+_lib.call("daop_server_trace", tr.data_ptr(), 1200)
+with eng.decode_server() as srv:
+    for _ in range(1100):
+        srv.step(hh)
+_lib.call("daop_server_trace", 0, 0)
+torch.cuda.synchronize()
+t = tr[100:1100].cpu().double()
+import numpy as np
+seen, rel, done = t[:, 0], t[:, 1], t[:, 2]
+print("server: doorbell->released %.2f us, released->body done %.2f us, call period %.2f us" % (
+    float((rel - seen).median()) / 1e3, float((done - rel).median()) / 1e3,
+    float((seen[1:] - seen[:-1]).median()) / 1e3))

@@ -363,3 +363,44 @@ def test_grouped_gemm_two_m_bitexact(P, d, ffn, E, T):
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
     assert torch.equal(outs[0][2], outs[1][2])
+
+
+@pytest.mark.parametrize("d,ffn", [(512, 1024), (4096, 14336)])
+def test_decode_server_matches_host_call(P, d, ffn):
+    """The persistent decode server answers each call exactly like the
+    launch-per-call end-to-end path (same kernel body): residual and selection
+    bit-identical over several calls; stop returns the GPU."""
+    pkg, model_mod, ops = P
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    E, k = 8, 2
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, k), d, ffn, seed=2, resident_layers=[0])
+    eng = MoEBlockEngine(m)
+    hs = [m.input_hidden(1, stream=70, step=i)[0].cpu().contiguous() for i in range(6)]
+    ref = []
+    for h in hs:
+        out, sel = eng.decode_host(h)
+        ref.append((out.clone(), sel.clone()))
+    with eng.decode_server() as srv:
+        for i, h in enumerate(hs):
+            out, sel = srv.step(h)
+            assert torch.equal(out, ref[i][0]), i
+            assert torch.equal(sel, ref[i][1]), i
+    torch.cuda.synchronize()
+    # the GPU is free again: an ordinary launch still works and agrees
+    out, sel = eng.decode_host(hs[0])
+    assert torch.equal(out, ref[0][0])
+
+
+def test_decode_server_idle_exit(P):
+    """A server nobody calls ends by itself (no GPU left spinning)."""
+    pkg, model_mod, ops = P
+    import time
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    m = model_mod.MoEModel(pkg.ModelShape(2, 8, 2), 256, 512, seed=2, resident_layers=[0])
+    eng = MoEBlockEngine(m)
+    srv = eng.decode_server(idle_ms=200.0)
+    time.sleep(1.5)
+    assert srv.stream.query()  # kernel exited on its idle timeout
+    with pytest.raises(Exception):
+        srv.step(torch.zeros(256), timeout_ms=300.0)
+    srv.close()
