@@ -301,6 +301,8 @@ def run_b200(args, world, rank, local_rank):
     # no stream synchronisation per call; MoEBlockEngine.decode_server)
     e2e_server = None
     try:
+        if args.no_server:
+            raise RuntimeError("skipped (--no-server)")
         with eng.decode_server() as srv:
             for i in range(min(args.warmup, 20)):
                 srv.step(hh[i % 8])
@@ -584,6 +586,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode32", action="store_true")
     ap.add_argument("--no-ep", action="store_true")
+    ap.add_argument("--no-server", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
