@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(EP_WARPS * 32)
       const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
       uint4* dst = reinterpret_cast<uint4*>(ws_of(peers, o) + recv_off) +
                    (L.dst_row[e] + (i - L.own_off[e])) * n16;
+#pragma unroll 8
       for (int c = lane; c < n16; c += 32) dst[c] = __ldg(src + c);
     }
   }

@@ -12,6 +12,8 @@
 //             warp totals prefix-summed in shared memory
 //   gather  : one warp per sorted row, 16-byte coalesced row copy
 //   combine : h'[t] = h[t] + sum_{j=0..k-1} w[t,j] * y[inv[t,j]]  (fixed j order)
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace daop {
@@ -91,16 +93,33 @@ __global__ void perm_scatter_kernel(const int32_t* __restrict__ ids, int64_t n, 
   }
 }
 
-__global__ void perm_gather_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ perm,
-                                   int64_t rows, int k, int n16, uint4* __restrict__ x_perm) {
+// token-major gather: a warp reads token t's x row ONCE and stores it at its
+// k sorted positions inv[t, j] (reading in permuted order would fetch every
+// row k times, far apart in time)
+template <int K>
+__global__ void perm_gather_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ inv,
+                                   int64_t T, int k_rt, int n16, uint4* __restrict__ x_perm) {
   const int lane = threadIdx.x & 31;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < rows;
-       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t src = perm[r] / k;
-    const uint4* s = x + src * n16;
-    uint4* d = x_perm + r * n16;
-#pragma unroll 8
-    for (int c = lane; c < n16; c += 32) d[c] = __ldcs(s + c);
+  const int k = K > 0 ? K : k_rt;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint4* s = x + t * n16;
+    if constexpr (K > 0) {
+      uint4* d[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) d[j] = x_perm + static_cast<int64_t>(inv[t * K + j]) * n16;
+#pragma unroll 4
+      for (int c = lane; c < n16; c += 32) {
+        const uint4 v = __ldcs(s + c);
+#pragma unroll
+        for (int j = 0; j < K; ++j) d[j][c] = v;
+      }
+    } else {
+      for (int c = lane; c < n16; c += 32) {
+        const uint4 v = __ldcs(s + c);
+        for (int j = 0; j < k; ++j) x_perm[static_cast<int64_t>(inv[t * k + j]) * n16 + c] = v;
+      }
+    }
   }
 }
 
@@ -155,6 +174,130 @@ __global__ void combine_kernel(const float* __restrict__ h, const float* __restr
   }
 }
 
+// ---------------------------------------------------------------- bulk-DMA pipelines
+//
+// Row-streaming kernels for the big prefill passes: one CTA per SM, a ring of
+// shared-memory stages filled by cp.async.bulk (one DMA per row) and drained
+// by cp.async.bulk stores, so each SM keeps ~200 KB in flight with a handful
+// of instructions (the register-staged versions above stall on memory
+// latency at ~55 % occupancy: ncu 2.5-3.4 TB/s).
+
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// out[t] = h[t] + sum_j w[t,j] * y[inv[t,j]]  (fixed j order, fmaf: the same
+// arithmetic as combine_kernel).  Stage = [h row | y rows of the k picks].
+template <int K>
+__global__ void __launch_bounds__(256, 1)
+    combine_bulk_kernel(const float* __restrict__ h, const float* __restrict__ y,
+                        const int32_t* __restrict__ inv, const float* __restrict__ w, int64_t T,
+                        int d, int stages, float* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t row = static_cast<uint32_t>(d) * 4;
+  const uint32_t stage_bytes = row * (K + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * stage_bytes);
+  const int64_t n_my = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto issue = [&](int64_t i) {  // thread 0: loads of my i-th token into stage i % stages
+    const int st = static_cast<int>(i % stages);
+    const int64_t t = blockIdx.x + i * gridDim.x;
+    uint8_t* sb = smem + static_cast<size_t>(st) * stage_bytes;
+    mbar_arrive_expect_tx(&full[st], stage_bytes);
+    bulk_g2s_plain(sb, h + t * d, row, &full[st]);
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      bulk_g2s_plain(sb + (j + 1) * row, y + static_cast<int64_t>(inv[t * K + j]) * d, row,
+                     &full[st]);
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < stages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+    for (int64_t i = 0; i < n_my && i < stages; ++i) issue(i);
+  }
+  __syncthreads();
+  for (int64_t i = 0; i < n_my; ++i) {
+    const int st = static_cast<int>(i % stages);
+    const int64_t t = blockIdx.x + i * gridDim.x;
+    float* sb = reinterpret_cast<float*>(smem + static_cast<size_t>(st) * stage_bytes);
+    mbar_wait(&full[st], static_cast<uint32_t>((i / stages) & 1));
+    float wj[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) wj[j] = w[t * K + j];
+    for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+      float4 acc = reinterpret_cast<const float4*>(sb)[c];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const float4 v = reinterpret_cast<const float4*>(sb + (j + 1) * d)[c];
+        acc.x = fmaf(wj[j], v.x, acc.x);
+        acc.y = fmaf(wj[j], v.y, acc.y);
+        acc.z = fmaf(wj[j], v.z, acc.z);
+        acc.w = fmaf(wj[j], v.w, acc.w);
+      }
+      reinterpret_cast<float4*>(sb)[c] = acc;  // result in place of h
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(out + t * d, sb, row);
+      bulk_commit();
+      // refill the stage stored one iteration ago (this store stays in flight)
+      if (i >= 1 && i - 1 + stages < n_my) {
+        asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
+        issue(i - 1 + stages);
+      }
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+// token-major gather with bulk DMAs: x row -> smem -> its k sorted positions
+__global__ void __launch_bounds__(32, 1)
+    gather_bulk_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ inv,
+                       int64_t T, int k, int d, int stages, uint16_t* __restrict__ x_perm) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t row = static_cast<uint32_t>(d) * 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * row);
+  if (threadIdx.x != 0) return;
+  const int64_t n_my = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  for (int st = 0; st < stages; ++st) mbar_init(&full[st], 1);
+  fence_mbar_init();
+  auto issue = [&](int64_t i) {
+    const int st = static_cast<int>(i % stages);
+    const int64_t t = blockIdx.x + i * gridDim.x;
+    mbar_arrive_expect_tx(&full[st], row);
+    bulk_g2s_plain(smem + static_cast<size_t>(st) * row, x + t * d, row, &full[st]);
+  };
+  // the first refill happens at iteration 1: prime stages - 1 loads plus one
+  for (int64_t i = 0; i < n_my && i < stages; ++i) issue(i);
+  for (int64_t i = 0; i < n_my; ++i) {
+    const int st = static_cast<int>(i % stages);
+    const int64_t t = blockIdx.x + i * gridDim.x;
+    mbar_wait(&full[st], static_cast<uint32_t>((i / stages) & 1));
+    for (int j = 0; j < k; ++j)
+      bulk_s2g(x_perm + static_cast<int64_t>(inv[t * k + j]) * d,
+               smem + static_cast<size_t>(st) * row, row);
+    bulk_commit();
+    // refill the stage stored one iteration ago (its stores have had a whole
+    // iteration to read it; this one's stay in flight)
+    if (i >= 1 && i - 1 + stages < n_my) {
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(1) : "memory");
+      issue(i - 1 + stages);
+    }
+  }
+  bulk_wait_all();
+}
+
 // decode-side combine when some picks ran on the host tier:
 // out[i] = h[i] + sum_{q<k} w[q] * y[q, i]   (fixed q order, like the fused path)
 __global__ void combine_dense_kernel(const float* __restrict__ h, const float* __restrict__ y,
@@ -205,11 +348,22 @@ int daop_permute(const int32_t* ids, int64_t T, int32_t k, int32_t E, const uint
   if (n > 0) perm_scatter_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts, offsets, perm, inv);
   DAOP_CHECK_LAUNCH("permute");
   if (x_perm && n > 0) {
-    int64_t blocks = (n * 32 + 255) / 256;
+    int64_t blocks = (T * 32 + 255) / 256;
     const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
     if (blocks > cap) blocks = cap;
-    perm_gather_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(
-        reinterpret_cast<const uint4*>(x), perm, n, k, d / 8, reinterpret_cast<uint4*>(x_perm));
+    const uint4* xs = reinterpret_cast<const uint4*>(x);
+    uint4* xp = reinterpret_cast<uint4*>(x_perm);
+    const size_t row = static_cast<size_t>(d) * 2;
+    if (T >= 4 * sm_count() && row % 16 == 0 && row <= 16 * 1024) {
+      const int stages = static_cast<int>(std::min<size_t>(16, (48 * 1024) / row));
+      const size_t smem = row * stages + 16 * 8 + 64;
+      DAOP_CUDA(cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      gather_bulk_kernel<<<4 * sm_count(), 32, smem, st>>>(x, inv, T, k, d, stages, x_perm);
+    } else if (k == 2)
+      perm_gather_kernel<2><<<static_cast<int>(blocks), 256, 0, st>>>(xs, inv, T, k, d / 8, xp);
+    else
+      perm_gather_kernel<0><<<static_cast<int>(blocks), 256, 0, st>>>(xs, inv, T, k, d / 8, xp);
     DAOP_CHECK_LAUNCH("permute_gather");
   }
   return DAOP_OK;
@@ -229,6 +383,20 @@ int daop_combine(const float* h, const float* y_sorted, const int32_t* inv, cons
     kern<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(h, y_sorted, inv, w, T, k, d / 4,
                                                                   out);
   };
+  if (k == 2 && d % 4 == 0 && T >= sm_count()) {
+    const size_t stage = static_cast<size_t>(d) * 4 * 3;
+    const int stages = static_cast<int>(std::min<size_t>(4, (200 * 1024) / stage));
+    if (stages >= 2) {
+      const size_t smem = stage * stages + 64;
+      DAOP_CUDA(cudaFuncSetAttribute(combine_bulk_kernel<2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      combine_bulk_kernel<2><<<sm_count(), 256, smem, as_stream(stream)>>>(
+          h, y_sorted, inv, w, T, d, stages, out);
+      DAOP_CHECK_LAUNCH("combine_bulk");
+      return DAOP_OK;
+    }
+  }
   if (k == 1) launch(combine_kernel<1>);
   else if (k == 2) launch(combine_kernel<2>);
   else if (k == 4) launch(combine_kernel<4>);
