@@ -305,6 +305,20 @@ int daop_decode_layer(const float* d_h, const uint16_t* d_gamma, const uint16_t*
 /* variant: ring geometry (warps x stages x stage bytes); 0 = default
  * (16 x 1 x 10 KB), 1..9 = tuning alternatives.  num_experts <= 16. */
 
+/* ------------------------------------------------ non-MoE block: attention (decode, b = 1)
+ * The caller of the MoE block (priced by
+ * the reference as t_nonmoe, simulator.py:291): RMSNorm -> QKV GEMV -> RoPE
+ * (theta) -> append to the layer's KV cache (n_kv, max_seq, 128) bf16 at
+ * `pos` -> GQA flash-decoding over positions 0..pos -> O-proj GEMV ->
+ * d_h_out = d_h + o Wo^T.  head_dim 128; Wqkv (q + 2 kv, d), Wo (d, q) bf16.
+ * d_workspace: daop_attn_workspace() bytes. */
+int daop_attn_workspace(int32_t n_heads, int32_t n_kv, int32_t max_seq, int64_t* h_bytes);
+int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const uint16_t* d_wqkv,
+                     const uint16_t* d_wo, uint16_t* d_k_cache, uint16_t* d_v_cache, int32_t d,
+                     int32_t n_heads, int32_t n_kv, int32_t max_seq, int32_t pos, float eps,
+                     float theta, uint16_t* d_xa_out, float* d_h_out, void* d_workspace,
+                     daop_stream_t stream);
+
 /* ------------------------------------------------ persistent decode server (b = 1)
  * The end-to-end decode call without a launch or a stream synchronisation
  * per call: daop_server_start launches ONE persistent cooperative kernel for

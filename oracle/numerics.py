@@ -195,3 +195,72 @@ def daop_decode_token(model: OracleModel, h: np.ndarray, sel_per_layer, start: i
             out = out + w[j] * expert_ffn(xin, model.w1(l, e), model.w3(l, e), model.w2(l, e))
         h, x_prev, ph_prev = out, x, ph
     return h[0]
+
+
+# ------------------------------------------------------------------ non-MoE block (attention)
+# Builder-defined restatement of csrc/attention.cu (the reference prices this
+# block as t_nonmoe, moesim/simulator.py:291).  Parity is
+# within tolerance (fp32 reductions in a different order).
+
+KIND_ATTN = 5
+NORM_LAYER_OFFSET = 4096
+HEAD_DIM = 128
+
+
+class OracleAttention:
+    def __init__(self, d, n_heads=32, n_kv=8, theta=1e6, seed=0):
+        self.d, self.n_heads, self.n_kv, self.theta, self.seed = d, n_heads, n_kv, theta, seed
+        self.q_dim, self.kv_dim = n_heads * HEAD_DIM, n_kv * HEAD_DIM
+        self.s_in = float(np.float32(1.0 / np.sqrt(d)))
+        self.s_o = float(np.float32(1.0 / np.sqrt(self.q_dim)))
+
+    def norm(self, layer):
+        return rng.norm_weight(self.seed, layer + NORM_LAYER_OFFSET, self.d)
+
+    def wqkv(self, layer):
+        return rng.tensor_bf16(self.seed, rng.make_tag(KIND_ATTN, layer, 0, 0),
+                               (self.q_dim + 2 * self.kv_dim, self.d), self.s_in)
+
+    def wo(self, layer):
+        return rng.tensor_bf16(self.seed, rng.make_tag(KIND_ATTN, layer, 0, 1),
+                               (self.d, self.q_dim), self.s_o)
+
+
+def rope(x: np.ndarray, pos: int, theta: float) -> np.ndarray:
+    """Rotate-half RoPE of (..., 128) fp32 vectors at position pos."""
+    half = HEAD_DIM // 2
+    i = np.arange(half, dtype=np.float32)
+    inv = (np.float32(1.0) / np.power(np.float32(theta), (2 * i) / np.float32(HEAD_DIM))).astype(np.float32)
+    ang = (np.float32(pos) * inv).astype(np.float32)
+    c, s = np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+    a, b = x[..., :half], x[..., half:]
+    return np.concatenate([a * c - b * s, b * c + a * s], axis=-1).astype(np.float32)
+
+
+def attention_decode(att: OracleAttention, layer: int, h: np.ndarray, pos: int,
+                     k_cache: np.ndarray, v_cache: np.ndarray):
+    """One decode token; k_cache / v_cache (n_kv, >= pos+1, 128) float32 views
+    of the bf16 cache (entries < pos used as given; pos is written here).
+    Returns (h_out, xa, k_cache, v_cache)."""
+    xa = rmsnorm(h[None, :], att.norm(layer))[0]
+    qkv = (att.wqkv(layer).astype(np.float64) @ xa.astype(np.float64)).astype(np.float32)
+    q = qkv[: att.q_dim].reshape(att.n_heads, HEAD_DIM)
+    k = qkv[att.q_dim: att.q_dim + att.kv_dim].reshape(att.n_kv, HEAD_DIM)
+    v = qkv[att.q_dim + att.kv_dim:].reshape(att.n_kv, HEAD_DIM)
+    q = rope(q, pos, att.theta)
+    k = rope(k, pos, att.theta)
+    k_cache = k_cache.copy()
+    v_cache = v_cache.copy()
+    k_cache[:, pos] = rng.round_bf16(k)
+    v_cache[:, pos] = rng.round_bf16(v)
+    group = att.n_heads // att.n_kv
+    o = np.zeros((att.n_heads, HEAD_DIM), dtype=np.float64)
+    for hd in range(att.n_heads):
+        g = hd // group
+        sc = (k_cache[g, : pos + 1].astype(np.float64) @ q[hd].astype(np.float64)) / np.sqrt(HEAD_DIM)
+        p = np.exp(sc - sc.max())
+        p /= p.sum()
+        o[hd] = p @ v_cache[g, : pos + 1].astype(np.float64)
+    o_b = rng.round_bf16(o.reshape(-1).astype(np.float32))
+    y = (att.wo(layer).astype(np.float64) @ o_b.astype(np.float64)).astype(np.float32)
+    return h.astype(np.float32) + y, xa, k_cache, v_cache
