@@ -357,6 +357,14 @@ def run_b200(args, world, rank, local_rank):
             "gpu_launches": nt * 32,
         }
 
+    # -------- full decoder layers: attention with a KV cache + MoE (32 layers)
+    decoder32 = None
+    if not args.no_decode32:
+        try:
+            decoder32 = run_decoder32(args, world, dev, eng, model, hs, hbm_peak, barrier)
+        except Exception as exc:
+            decoder32 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # -------- expert parallelism (BASELINE configs[4]: Mixtral-8x22B shape)
     ep = None
     if not args.no_ep:
@@ -419,10 +427,68 @@ def run_b200(args, world, rank, local_rank):
         "clocks": clocks,
         "prefill": prefill,
         "decode32": decode32,
+        "decoder32": decoder32,
         "ep": ep,
     }
     return line
 
+
+DEC_CTX = 512  # context position of the decoder32 measurement
+
+
+def run_decoder32(args, world, dev, eng, model, hs, hbm_peak, barrier):
+    """BASELINE configs[2] with the non-MoE block executed: 32 Mixtral-8x7B
+    decoder layers per token = attention with a KV cache (RMSNorm, QKV GEMV,
+    RoPE, GQA flash-decoding over DEC_CTX cached positions, O-proj + residual)
+    then the MoE block (DAOP plans from layer 4, all experts in HBM)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_10375_b200.attention import AttentionStack
+
+    L = model.shape.num_layers
+    att = AttentionStack(L, D, 32, 8, max_seq=DEC_CTX + 256, seed=0, device=dev)
+    # a filled history: the cache rows before DEC_CTX are random bf16 values
+    g = torch.Generator(device=dev).manual_seed(7)
+    att.k_cache[:, :, :DEC_CTX].copy_(torch.randn(att.k_cache[:, :, :DEC_CTX].shape,
+                                                  generator=g, device=dev))
+    att.v_cache[:, :, :DEC_CTX].copy_(torch.randn(att.v_cache[:, :, :DEC_CTX].shape,
+                                                  generator=g, device=dev))
+    h_in = torch.empty(D, dtype=torch.float32, device=dev)
+    for i in range(3):
+        h_in.copy_(hs[i])
+        eng.decode_token(h_in, start=4, daop=True, attn=att, pos=DEC_CTX + i)
+    barrier()
+    torch.cuda.synchronize()
+    nt = max(10, min(100, args.steps // 20))
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(nt):
+        h_in.copy_(hs[i % len(hs)])
+        eng.decode_token(h_in, start=4, daop=True, attn=att, pos=DEC_CTX + 3 + i % 200)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    tok_ms = e0.elapsed_time(e1) / nt
+    t = torch.tensor([tok_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tok_ms = float(t.item())
+    ctx = DEC_CTX + 3 + nt // 2
+    bytes_tok = 32 * DECODE_BYTES - 2 * E * D + L * att.bytes_per_token_layer(ctx)
+    del att
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"decode b=1 through 32 full Mixtral-8x7B decoder layers (attention with a "
+                    f"KV cache at context ~{DEC_CTX}, 32 q / 8 kv heads, then the MoE block; "
+                    f"DAOP plans from layer 4, all experts in HBM)",
+        "value": world * 1e3 / tok_ms, "unit": "tokens/s", "ms_per_token": tok_ms,
+        "roofline": {"bound": "hbm", "achieved": bytes_tok / (tok_ms / 1e3) / 1e9,
+                     "peak": hbm_peak, "unit": "GB/s",
+                     "frac": bytes_tok / (tok_ms / 1e3) / 1e9 / hbm_peak,
+                     "bytes_per_token": bytes_tok},
+        "gpu_launches": nt * L * 5,
+    }
 
 EP_D, EP_FFN, EP_TOKENS = 6144, 16384, 8 * 4096
 

@@ -10,13 +10,16 @@
 //   o_h  = softmax_p(q_h . k_p / sqrt(hd)) . v_p  over p <= pos, GQA (head h uses kv h / group)
 //   h'   = h + bf16(o) . Wo^T                  fp32
 //
-// Four launches, each HBM-bound on what it streams:
-//   attn_qkv_kernel      RMSNorm in every CTA + warp-per-row GEMV over Wqkv (50 MB at 8x7B)
-//   attn_decode_kernel   flash-decoding: CTA = (kv head, position split), a thread per
-//                        position for the scores of the group's q heads (k read once),
-//                        a thread per head dim for P.V, online softmax across tiles
-//   attn_combine_kernel  per q head, the splits merged in fixed order -> bf16 o
-//   attn_oproj_kernel    warp-per-row GEMV over Wo (33.5 MB) + residual
+// Three launches, each HBM-bound on what it streams:
+//   attn_qkv_kernel      warp-per-row GEMV over Wqkv (50 MB at 8x7B); every CTA first
+//                        prefetches its rows into L2, then computes the RMSNorm
+//   attn_decode_kernel   flash-decoding: CTA = (kv head, 64-position split); K and V
+//                        tiles arrive by bulk copy; scores thread = (head, position),
+//                        P.V thread = (head, dim pair); (m, l, acc) per split
+//   attn_oproj_kernel    every CTA merges the split partials in fixed order (bf16 o
+//                        in smem), then warp-per-row GEMV over Wo (33.5 MB) + residual
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace daop {
@@ -26,70 +29,107 @@ constexpr int AT_HD = 128;      // head dim (Mixtral / Llama)
 constexpr int AT_TILE = 128;    // positions per attention tile (one per thread)
 constexpr int AT_MAX_GROUP = 8; // q heads per kv head
 
-// dot of one bf16 row (K elements, K % 256 == 0) with x (bf16, smem), lane-
-// strided 16-byte pieces in fixed order, then a butterfly warp sum
-__device__ __forceinline__ float row_dot(const uint16_t* __restrict__ w, const uint4* x_s, int K,
-                                         int lane) {
-  const uint4* wr = reinterpret_cast<const uint4*>(w);
-  const int n16 = K / 8;
-  float acc = 0.f;
-  for (int c0 = 0; c0 < n16; c0 += 32 * 8) {
-    uint4 v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int c = c0 + i * 32 + lane;
-      v[i] = c < n16 ? ldg_nc_v4(wr + c) : make_uint4(0, 0, 0, 0);
+// Bulk-streamed GEMV over this CTA's block of rows: warp AT_WARPS (lane 0)
+// is the producer -- one cp.async.bulk per row into a ring of S = AT_WARPS
+// row stages, issued from the first cycle of the kernel (the weights do not
+// depend on x) -- and warps 0..AT_WARPS-1 consume rows round-robin (row i:
+// stage and warp i % AT_WARPS, so each stage's phases are consumed in order
+// by one warp): dot with x (smem) in a fixed lane-strided order + butterfly
+// sum, then free the stage.
+struct RowRing {
+  uint8_t* ring;     // S x row_bytes
+  uint64_t* full;    // S
+  uint64_t* empty;   // S
+  int S;
+};
+
+__device__ __forceinline__ void ring_init(RowRing& R) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < R.S; ++i) {
+      mbar_init(&R.full[i], 1);
+      mbar_init(&R.empty[i], 1);
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int c = c0 + i * 32 + lane;
-      if (c < n16) acc = dot8(x_s[c], v[i], acc);
-    }
+    fence_mbar_init();
   }
-  return warp_sum(acc);
 }
 
-// every CTA: xa = bf16(rmsnorm(h) * gamma) into shared memory (fixed-order
-// block reduction -> identical in every CTA); CTA 0 also writes it out
-__device__ void rmsnorm_to_smem(const float* __restrict__ h, const uint16_t* __restrict__ gamma,
-                                int d, float eps, uint16_t* xs, float* red, uint16_t* x_out) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ void ring_produce(const RowRing& R, const uint16_t* W, int r0, int n,
+                                             int K) {
+  const uint32_t rb = static_cast<uint32_t>(K) * 2;
+  for (int i = 0; i < n; ++i) {
+    const int st = i % R.S;
+    mbar_wait(&R.empty[st], ((i / R.S) & 1) ^ 1);
+    mbar_arrive_expect_tx(&R.full[st], rb);
+    bulk_g2s_plain(R.ring + static_cast<size_t>(st) * rb, W + static_cast<int64_t>(r0 + i) * K,
+                   rb, &R.full[st]);
+  }
+}
+
+template <class Epi>
+__device__ __forceinline__ void ring_consume(const RowRing& R, int r0, int n, int K,
+                                             const uint4* x_s, int warp, int lane, Epi epi) {
+  const uint32_t rb = static_cast<uint32_t>(K) * 2;
+  const int n16 = K / 8;
+  for (int i = warp; i < n; i += AT_WARPS) {
+    const int st = i % R.S;
+    mbar_wait(&R.full[st], (i / R.S) & 1);
+    const uint4* wr = reinterpret_cast<const uint4*>(R.ring + static_cast<size_t>(st) * rb);
+    float acc = 0.f;
+    for (int c = lane; c < n16; c += 32) acc = dot8(x_s[c], wr[c], acc);
+    acc = warp_sum(acc);
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&R.empty[st]);
+      epi(r0 + i, acc);
+    }
+  }
+}
+
+__global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
+    attn_qkv_kernel(const float* __restrict__ h, const uint16_t* __restrict__ gamma,
+                    const uint16_t* __restrict__ wqkv, int d, int rows, int rows_per_cta,
+                    int stages, float eps, uint16_t* __restrict__ xa_out,
+                    float* __restrict__ qkv) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  RowRing R;
+  R.S = stages;
+  R.ring = smem;
+  uint16_t* xs = reinterpret_cast<uint16_t*>(smem + static_cast<size_t>(stages) * d * 2);
+  float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xs) + d * 2);
+  R.full = reinterpret_cast<uint64_t*>(red + 40);
+  R.empty = R.full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int n = max(0, min(rows, r0 + rows_per_cta) - r0);
+  ring_init(R);
+  __syncthreads();
+  if (warp == AT_WARPS) {  // producer warp: stream the rows while the others normalise
+    if (lane == 0) ring_produce(R, wqkv, r0, n, d);
+    return;
+  }
+  // RMSNorm by the consumer warps (named barrier: the producer is not waited for)
+  const int nt = AT_WARPS * 32;
   float ss = 0.f;
-  for (int i = tid; i < d; i += nt) ss = fmaf(h[i], h[i], ss);
+  for (int i = threadIdx.x; i < d; i += nt) ss = fmaf(h[i], h[i], ss);
   ss = warp_sum(ss);
   if (lane == 0) red[warp] = ss;
-  __syncthreads();
-  if (tid == 0) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nt));
+  if (threadIdx.x == 0) {
     float t = 0.f;
-    for (int w = 0; w < nt / 32; ++w) t += red[w];
+    for (int w = 0; w < AT_WARPS; ++w) t += red[w];
     red[32] = 1.0f / sqrtf(t / static_cast<float>(d) + eps);
   }
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"r"(nt));
   const float r = red[32];
-  for (int i = tid; i < d; i += nt) {
-    const uint16_t g = gamma[i];
-    const float x = __fmul_rn(__fmul_rn(h[i], r), __uint_as_float(static_cast<uint32_t>(g) << 16));
+  for (int i = threadIdx.x; i < d; i += nt) {
+    const float x = __fmul_rn(__fmul_rn(h[i], r),
+                              __uint_as_float(static_cast<uint32_t>(gamma[i]) << 16));
     xs[i] = f32_to_bf16_bits(x);
-    if (x_out && blockIdx.x == 0) x_out[i] = xs[i];
+    if (xa_out && blockIdx.x == 0) xa_out[i] = xs[i];
   }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(AT_WARPS * 32, 1)
-    attn_qkv_kernel(const float* __restrict__ h, const uint16_t* __restrict__ gamma,
-                    const uint16_t* __restrict__ wqkv, int d, int rows, float eps,
-                    uint16_t* __restrict__ xa_out, float* __restrict__ qkv) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
-  float* red = reinterpret_cast<float*>(smem + static_cast<size_t>(d) * 2);
-  rmsnorm_to_smem(h, gamma, d, eps, xs, red, xa_out);
-  const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * AT_WARPS + (threadIdx.x >> 5), nw = gridDim.x * AT_WARPS;
-  for (int r = gw; r < rows; r += nw) {
-    const float v = row_dot(wqkv + static_cast<int64_t>(r) * d, reinterpret_cast<const uint4*>(xs),
-                            d, lane);
-    if (lane == 0) qkv[r] = v;
-  }
+  asm volatile("bar.sync 1, %0;" ::"r"(nt));
+  ring_consume(R, r0, n, d, reinterpret_cast<const uint4*>(xs), warp, lane,
+               [&](int row, float v) { qkv[row] = v; });
 }
 
 // RoPE of one head vector held as hd floats in smem (pairs (i, i + hd/2))
@@ -108,21 +148,48 @@ struct AttnArgs {
   const float* qkv;       // raw projections: q (n_heads*hd) | k (n_kv*hd) | v (n_kv*hd)
   uint16_t* k_cache;      // (n_kv, max_seq, hd) bf16, this layer
   uint16_t* v_cache;
-  int n_heads, n_kv, max_seq, pos, splits, per_split;
+  int n_heads, n_kv, max_seq, pos, splits;
   float theta, scale;
   float* part;            // (n_kv, splits, group, 2 + hd): m, l, acc[hd]
+  unsigned* counter;      // (n_kv) finished splits, self-resetting
+  uint16_t* o;            // (n_heads * hd) bf16 attention output
 };
 
-__global__ void __launch_bounds__(AT_TILE, 1) attn_decode_kernel(AttnArgs a) {
+constexpr int AT_SPLIT = 64;  // positions per CTA (one K tile + one V tile, 16 KB each)
+
+// CTA = (kv head g, split of AT_SPLIT positions), 256 threads.  The split's K
+// and V rows (contiguous in the cache) arrive by two bulk copies while the
+// CTA applies RoPE to its group's q heads; scores: thread = (head, position);
+// P.V: thread = (head, 2 head dims).  The split's (m, l, acc) go to `part`.
+// The CTA whose split holds `pos` first appends the new k (RoPE) and v.
+__global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
+  __shared__ __align__(128) uint16_t k_s[AT_SPLIT * AT_HD];
+  __shared__ __align__(128) uint16_t v_s[AT_SPLIT * AT_HD];
   __shared__ float q_s[AT_MAX_GROUP][AT_HD];
-  __shared__ float p_s[AT_MAX_GROUP][AT_TILE];
-  __shared__ float red[AT_MAX_GROUP][AT_TILE / 32];
-  __shared__ float m_s[AT_MAX_GROUP], l_s[AT_MAX_GROUP], corr_s[AT_MAX_GROUP];
-  const int g = blockIdx.x, split = blockIdx.y, tid = threadIdx.x, lane = tid & 31,
-            warp = tid >> 5;
+  __shared__ float p_s[AT_MAX_GROUP][AT_SPLIT];
+  __shared__ float ml_s[AT_MAX_GROUP][2];
+  __shared__ uint64_t bar;
+  const int g = blockIdx.x, split = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   const int group = a.n_heads / a.n_kv;
   const int q_dim = a.n_heads * AT_HD, kv_dim = a.n_kv * AT_HD;
-  // q of the group's heads with RoPE (redundant per CTA: 4 x 128 floats)
+  const int p0 = split * AT_SPLIT;
+  const int n = min(a.pos + 1, p0 + AT_SPLIT) - p0;  // positions of this split (>= 1)
+  uint16_t* kc = a.k_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
+  uint16_t* vc = a.v_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
+  const bool owns_new = a.pos >= p0 && a.pos < p0 + AT_SPLIT;
+  const int n_load = owns_new ? n - 1 : n;  // rows already in the cache
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    if (n_load > 0) {
+      mbar_arrive_expect_tx(&bar, 2 * n_load * AT_HD * 2);
+      bulk_g2s_plain(k_s, kc + static_cast<int64_t>(p0) * AT_HD, n_load * AT_HD * 2, &bar);
+      bulk_g2s_plain(v_s, vc + static_cast<int64_t>(p0) * AT_HD, n_load * AT_HD * 2, &bar);
+    } else {
+      mbar_arrive_expect_tx(&bar, 0);
+    }
+  }
+  // q of the group's heads with RoPE
   for (int i = tid; i < group * (AT_HD / 2); i += blockDim.x) {
     const int hh = i / (AT_HD / 2), j = i - hh * (AT_HD / 2);
     float x0 = a.qkv[(g * group + hh) * AT_HD + j];
@@ -131,150 +198,142 @@ __global__ void __launch_bounds__(AT_TILE, 1) attn_decode_kernel(AttnArgs a) {
     q_s[hh][j] = x0;
     q_s[hh][j + AT_HD / 2] = x1;
   }
-  const int p0 = split * a.per_split;
-  const int p1 = min(a.pos + 1, p0 + a.per_split);
-  uint16_t* kc = a.k_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
-  uint16_t* vc = a.v_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
-  if (a.pos >= p0 && a.pos < p1) {  // this split holds the new position: append k, v
+  if (owns_new) {  // new k (RoPE) and v -> the cache and this CTA's tile
+    const int r = a.pos - p0;
     for (int j = tid; j < AT_HD / 2; j += blockDim.x) {
       float k0 = a.qkv[q_dim + g * AT_HD + j];
       float k1 = a.qkv[q_dim + g * AT_HD + j + AT_HD / 2];
       rope_pair(k0, k1, j, a.pos, a.theta);
-      kc[static_cast<int64_t>(a.pos) * AT_HD + j] = f32_to_bf16_bits(k0);
-      kc[static_cast<int64_t>(a.pos) * AT_HD + j + AT_HD / 2] = f32_to_bf16_bits(k1);
+      const uint16_t b0 = f32_to_bf16_bits(k0), b1 = f32_to_bf16_bits(k1);
+      kc[static_cast<int64_t>(a.pos) * AT_HD + j] = b0;
+      kc[static_cast<int64_t>(a.pos) * AT_HD + j + AT_HD / 2] = b1;
+      k_s[r * AT_HD + j] = b0;
+      k_s[r * AT_HD + j + AT_HD / 2] = b1;
     }
-    for (int j = tid; j < AT_HD; j += blockDim.x)
-      vc[static_cast<int64_t>(a.pos) * AT_HD + j] =
-          f32_to_bf16_bits(a.qkv[q_dim + kv_dim + g * AT_HD + j]);
-    __threadfence_block();
-  }
-  if (tid < group) {
-    m_s[tid] = -INFINITY;
-    l_s[tid] = 0.f;
+    for (int j = tid; j < AT_HD; j += blockDim.x) {
+      const uint16_t bv = f32_to_bf16_bits(a.qkv[q_dim + kv_dim + g * AT_HD + j]);
+      vc[static_cast<int64_t>(a.pos) * AT_HD + j] = bv;
+      v_s[r * AT_HD + j] = bv;
+    }
   }
   __syncthreads();
-  float acc[AT_MAX_GROUP];  // thread tid owns head dim tid of every group head
+  mbar_wait(&bar, 0);
+  // scores: thread = (head hh, position i); group * AT_SPLIT <= 512 -> two passes max
+  for (int t = tid; t < group * AT_SPLIT; t += blockDim.x) {
+    const int hh = t / AT_SPLIT, i = t - hh * AT_SPLIT;
+    float sc = -INFINITY;
+    if (i < n) {
+      const uint4* kr = reinterpret_cast<const uint4*>(k_s + i * AT_HD);
+      float acc = 0.f;
 #pragma unroll
-  for (int hh = 0; hh < AT_MAX_GROUP; ++hh) acc[hh] = 0.f;
-  for (int t0 = p0; t0 < p1; t0 += AT_TILE) {
-    const int p = t0 + tid;
-    // scores: thread = position, k row read once for the whole group
-    float sc[AT_MAX_GROUP];
-#pragma unroll
-    for (int hh = 0; hh < AT_MAX_GROUP; ++hh) sc[hh] = -INFINITY;
-    if (p < p1) {
-      const uint4* kr = reinterpret_cast<const uint4*>(kc + static_cast<int64_t>(p) * AT_HD);
-      float s[AT_MAX_GROUP];
-#pragma unroll
-      for (int hh = 0; hh < AT_MAX_GROUP; ++hh) s[hh] = 0.f;
-#pragma unroll 4
       for (int c = 0; c < AT_HD / 8; ++c) {
-        const uint4 kv = kr[c];
-        const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
-#pragma unroll
-          for (int hh = 0; hh < AT_MAX_GROUP; ++hh)
-            if (hh < group) {
-              s[hh] = fmaf(q_s[hh][c * 8 + 2 * e], lo, s[hh]);
-              s[hh] = fmaf(q_s[hh][c * 8 + 2 * e + 1], hi, s[hh]);
-            }
-        }
+        const uint4 kv = kr[(c + i) & (AT_HD / 8 - 1)];  // rotated start: no bank conflicts
+        const int cc = ((c + i) & (AT_HD / 8 - 1)) * 8;
+        acc = fmaf(q_s[hh][cc + 0], bf16lo(kv.x), acc);
+        acc = fmaf(q_s[hh][cc + 1], bf16hi(kv.x), acc);
+        acc = fmaf(q_s[hh][cc + 2], bf16lo(kv.y), acc);
+        acc = fmaf(q_s[hh][cc + 3], bf16hi(kv.y), acc);
+        acc = fmaf(q_s[hh][cc + 4], bf16lo(kv.z), acc);
+        acc = fmaf(q_s[hh][cc + 5], bf16hi(kv.z), acc);
+        acc = fmaf(q_s[hh][cc + 6], bf16lo(kv.w), acc);
+        acc = fmaf(q_s[hh][cc + 7], bf16hi(kv.w), acc);
       }
-#pragma unroll
-      for (int hh = 0; hh < AT_MAX_GROUP; ++hh) sc[hh] = s[hh] * a.scale;
+      sc = acc * a.scale;
     }
-    // tile max per head (fixed-order block reduction)
-#pragma unroll
-    for (int hh = 0; hh < AT_MAX_GROUP; ++hh) {
-      if (hh >= group) break;
-      float mx = sc[hh];
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) red[hh][warp] = mx;
+    p_s[hh][i] = sc;
+  }
+  __syncthreads();
+  // per head: max and exp-sum over the split (one warp per head, fixed order)
+  const int warp = tid >> 5;
+  for (int hh = warp; hh < group; hh += blockDim.x / 32) {
+    float mx = fmaxf(p_s[hh][lane], p_s[hh][lane + 32]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float e0 = lane < n ? expf(p_s[hh][lane] - mx) : 0.f;
+    const float e1 = lane + 32 < n ? expf(p_s[hh][lane + 32] - mx) : 0.f;
+    p_s[hh][lane] = e0;
+    p_s[hh][lane + 32] = e1;
+    const float se = warp_sum(e0 + e1);
+    if (lane == 0) {
+      ml_s[hh][0] = mx;
+      ml_s[hh][1] = se;
     }
-    __syncthreads();
-    if (tid < group) {
-      float mx = -INFINITY;
-      for (int w = 0; w < AT_TILE / 32; ++w) mx = fmaxf(mx, red[tid][w]);
-      const float mnew = fmaxf(m_s[tid], mx);
-      corr_s[tid] = expf(m_s[tid] - mnew);  // 0 on the first tile (m = -inf)
-      m_s[tid] = mnew;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int hh = 0; hh < AT_MAX_GROUP; ++hh) {
-      if (hh >= group) break;
-      const float e = p < p1 ? expf(sc[hh] - m_s[hh]) : 0.f;
-      p_s[hh][tid] = e;
-      const float se = warp_sum(e);
-      if (lane == 0) red[hh][warp] = se;
-    }
-    __syncthreads();
-    if (tid < group) {
-      float se = 0.f;
-      for (int w = 0; w < AT_TILE / 32; ++w) se += red[tid][w];
-      l_s[tid] = l_s[tid] * corr_s[tid] + se;
-    }
-    // P.V: thread = head dim; v rows read coalesced (256 B per position)
-#pragma unroll
-    for (int hh = 0; hh < AT_MAX_GROUP; ++hh) acc[hh] *= (hh < group ? corr_s[hh] : 1.f);
-    const int n = min(AT_TILE, p1 - t0);
-#pragma unroll 8
+  }
+  __syncthreads();
+  // P.V: thread = (head hh, dims 2c, 2c + 1)
+  for (int t = tid; t < group * (AT_HD / 2); t += blockDim.x) {
+    const int hh = t / (AT_HD / 2), c = t - hh * (AT_HD / 2);
+    float a0 = 0.f, a1 = 0.f;
     for (int i = 0; i < n; ++i) {
-      const float v = __uint_as_float(static_cast<uint32_t>(
-                          vc[static_cast<int64_t>(t0 + i) * AT_HD + tid]) << 16);
-#pragma unroll
-      for (int hh = 0; hh < AT_MAX_GROUP; ++hh)
-        if (hh < group) acc[hh] = fmaf(p_s[hh][i], v, acc[hh]);
+      const uint32_t vv = *reinterpret_cast<const uint32_t*>(v_s + i * AT_HD + 2 * c);
+      a0 = fmaf(p_s[hh][i], bf16lo(vv), a0);
+      a1 = fmaf(p_s[hh][i], bf16hi(vv), a1);
     }
-    __syncthreads();
-  }
-  // partial of this split: (m, l, acc)
-  for (int hh = 0; hh < group; ++hh) {
     float* pr = a.part + ((static_cast<int64_t>(g) * a.splits + split) * group + hh) * (2 + AT_HD);
-    if (tid == 0) {
-      pr[0] = m_s[hh];
-      pr[1] = l_s[hh];
+    pr[2 + 2 * c] = a0;
+    pr[2 + 2 * c + 1] = a1;
+    if (c == 0) {
+      pr[0] = ml_s[hh][0];
+      pr[1] = ml_s[hh][1];
     }
-    pr[2 + tid] = acc[hh];
   }
-}
-
-// per q head: merge the splits in fixed order -> o (bf16)
-__global__ void attn_combine_kernel(const float* __restrict__ part, int n_heads, int n_kv,
-                                    int splits, int used, uint16_t* __restrict__ o) {
-  const int head = blockIdx.x, tid = threadIdx.x;
-  const int group = n_heads / n_kv, g = head / group, hh = head - g * group;
-  float m = -INFINITY;
-  for (int s = 0; s < used; ++s)
-    m = fmaxf(m, part[((static_cast<int64_t>(g) * splits + s) * group + hh) * (2 + AT_HD)]);
-  float l = 0.f, acc = 0.f;
-  for (int s = 0; s < used; ++s) {
-    const float* pr = part + ((static_cast<int64_t>(g) * splits + s) * group + hh) * (2 + AT_HD);
-    const float c = expf(pr[0] - m);
-    l = fmaf(pr[1], c, l);
-    acc = fmaf(pr[2 + tid], c, acc);
+  // the kv head's last split to finish merges all of them (fixed split order)
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (tid == 0) {
+    last = atomicAdd(a.counter + g, 1u) == static_cast<unsigned>(gridDim.y) - 1;
+    if (last) a.counter[g] = 0;  // self-resetting for the next call
   }
-  o[head * AT_HD + tid] = f32_to_bf16_bits(acc / l);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int used = gridDim.y;
+  for (int t = tid; t < group * (AT_HD / 2); t += blockDim.x) {
+    const int hh = t / (AT_HD / 2), c = t - hh * (AT_HD / 2);
+    const float* base = a.part + (static_cast<int64_t>(g) * a.splits * group + hh) * (2 + AT_HD);
+    const int64_t stride = static_cast<int64_t>(group) * (2 + AT_HD);
+    float m = -INFINITY;
+    for (int s2 = 0; s2 < used; ++s2) m = fmaxf(m, __ldcg(base + s2 * stride));
+    float l = 0.f, o0 = 0.f, o1 = 0.f;
+    for (int s2 = 0; s2 < used; ++s2) {
+      const float* pr = base + s2 * stride;
+      const float cf = expf(__ldcg(pr) - m);
+      l = fmaf(__ldcg(pr + 1), cf, l);
+      o0 = fmaf(__ldcg(pr + 2 + 2 * c), cf, o0);
+      o1 = fmaf(__ldcg(pr + 3 + 2 * c), cf, o1);
+    }
+    const int head = g * group + hh;
+    a.o[head * AT_HD + 2 * c] = f32_to_bf16_bits(o0 / l);
+    a.o[head * AT_HD + 2 * c + 1] = f32_to_bf16_bits(o1 / l);
+  }
 }
 
 // h' = h + o . Wo^T  (rows of Wo are output dims; o bf16 (q_dim) in smem)
-__global__ void __launch_bounds__(AT_WARPS * 32, 1)
+__global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
     attn_oproj_kernel(const float* __restrict__ h, const uint16_t* __restrict__ o,
-                      const uint16_t* __restrict__ wo, int d, int q_dim,
-                      float* __restrict__ h_out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint4* os = reinterpret_cast<uint4*>(smem);
-  for (int i = threadIdx.x; i < q_dim / 8; i += blockDim.x)
-    os[i] = reinterpret_cast<const uint4*>(o)[i];
+                      const uint16_t* __restrict__ wo, int d, int q_dim, int rows_per_cta,
+                      int stages, float* __restrict__ h_out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  RowRing R;
+  R.S = stages;
+  R.ring = smem;
+  uint4* os = reinterpret_cast<uint4*>(smem + static_cast<size_t>(stages) * q_dim * 2);
+  R.full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(os) + q_dim * 2);
+  R.empty = R.full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int n = max(0, min(d, r0 + rows_per_cta) - r0);
+  ring_init(R);
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * AT_WARPS + (threadIdx.x >> 5), nw = gridDim.x * AT_WARPS;
-  for (int r = gw; r < d; r += nw) {
-    const float v = row_dot(wo + static_cast<int64_t>(r) * q_dim, os, q_dim, lane);
-    if (lane == 0) h_out[r] = h[r] + v;
+  if (warp == AT_WARPS) {
+    if (lane == 0) ring_produce(R, wo, r0, n, q_dim);
+    return;
   }
+  for (int i = threadIdx.x; i < q_dim / 8; i += AT_WARPS * 32)
+    os[i] = reinterpret_cast<const uint4*>(o)[i];
+  asm volatile("bar.sync 1, %0;" ::"r"(AT_WARPS * 32));
+  ring_consume(R, r0, n, q_dim, os, warp, lane,
+               [&](int row, float v) { h_out[row] = h[row] + v; });
 }
 
 }  // namespace daop
@@ -287,7 +346,7 @@ extern "C" int daop_attn_workspace(int32_t n_heads, int32_t n_kv, int32_t max_se
   const int64_t q_dim = static_cast<int64_t>(n_heads) * AT_HD;
   const int64_t kv_dim = static_cast<int64_t>(n_kv) * AT_HD;
   const int64_t part = static_cast<int64_t>(n_kv) * 64 * (n_heads / n_kv) * (2 + AT_HD) * 4;
-  *h_bytes = (q_dim + 2 * kv_dim) * 4 + part + q_dim * 2 + 256;
+  *h_bytes = (q_dim + 2 * kv_dim) * 4 + part + q_dim * 2 + 4 * n_kv + 256;
   (void)max_seq;
   return DAOP_OK;
 }
@@ -313,32 +372,44 @@ extern "C" int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const
   uint16_t* o = reinterpret_cast<uint16_t*>(part + static_cast<int64_t>(n_kv) * 64 * group *
                                                        (2 + AT_HD));
   const int sms = sm_count();
-  const size_t smem_qkv = static_cast<size_t>(d) * 2 + 33 * 4;
-  DAOP_CUDA(cudaFuncSetAttribute(attn_qkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem_qkv)));
-  attn_qkv_kernel<<<sms, AT_WARPS * 32, smem_qkv, st>>>(d_h, d_gamma, d_wqkv, d,
-                                                        q_dim + 2 * kv_dim, eps, d_xa_out, qkv);
-  DAOP_CHECK_LAUNCH("attn_qkv");
-  // position splits: enough CTAs to cover the SMs, at least one tile each
+  unsigned* counter = reinterpret_cast<unsigned*>(o + q_dim);
+  {
+    const int rows = q_dim + 2 * kv_dim;
+    const int rpc = (rows + sms - 1) / sms;
+    // one stage per consumer warp: row i lives in stage i % AT_WARPS and is
+    // consumed by warp i % AT_WARPS, so no warp can wait on a stage a whole
+    // ring cycle ahead of its data (a shared ring would let it)
+    const int stages = AT_WARPS;
+    const size_t smem = static_cast<size_t>(stages) * d * 2 + static_cast<size_t>(d) * 2 + 40 * 4 +
+                        2 * stages * 8;
+    DAOP_CUDA(cudaFuncSetAttribute(attn_qkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    attn_qkv_kernel<<<sms, (AT_WARPS + 1) * 32, smem, st>>>(d_h, d_gamma, d_wqkv, d, rows, rpc,
+                                                            stages, eps, d_xa_out, qkv);
+    DAOP_CHECK_LAUNCH("attn_qkv");
+  }
+  // position splits of AT_SPLIT positions (<= 64 splits: max_seq <= 4096)
   const int ctx = pos + 1;
-  int splits = (sms + n_kv - 1) / n_kv;
-  const int max_splits = (ctx + AT_TILE - 1) / AT_TILE;
-  if (splits > max_splits) splits = max_splits;
-  if (splits > 64) splits = 64;
-  if (splits < 1) splits = 1;
-  int per_split = (ctx + splits - 1) / splits;
-  per_split = (per_split + AT_TILE - 1) / AT_TILE * AT_TILE;
-  const int used = (ctx + per_split - 1) / per_split;
-  AttnArgs a{qkv, d_k_cache, d_v_cache, n_heads, n_kv, max_seq, pos, splits, per_split,
-             theta, 1.0f / sqrtf(static_cast<float>(AT_HD)), part};
-  attn_decode_kernel<<<dim3(n_kv, used), AT_TILE, 0, st>>>(a);
+  const int used = (ctx + AT_SPLIT - 1) / AT_SPLIT;
+  const int splits = 64;
+  if (used > splits) {
+    set_error("attention: context %d exceeds %d positions", ctx, splits * AT_SPLIT);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  AttnArgs a{qkv, d_k_cache, d_v_cache, n_heads, n_kv, max_seq, pos, splits,
+             theta, 1.0f / sqrtf(static_cast<float>(AT_HD)), part, counter, o};
+  attn_decode_kernel<<<dim3(n_kv, used), 256, 0, st>>>(a);
   DAOP_CHECK_LAUNCH("attn_decode");
-  attn_combine_kernel<<<n_heads, AT_HD, 0, st>>>(part, n_heads, n_kv, splits, used, o);
-  DAOP_CHECK_LAUNCH("attn_combine");
-  const size_t smem_o = static_cast<size_t>(q_dim) * 2;
-  DAOP_CUDA(cudaFuncSetAttribute(attn_oproj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem_o)));
-  attn_oproj_kernel<<<sms, AT_WARPS * 32, smem_o, st>>>(d_h, o, d_wo, d, q_dim, d_h_out);
-  DAOP_CHECK_LAUNCH("attn_oproj");
+  {
+    const int rpc = (d + sms - 1) / sms;
+    const int stages = AT_WARPS;  // one stage per consumer warp (see above)
+    const size_t smem = static_cast<size_t>(stages) * q_dim * 2 + static_cast<size_t>(q_dim) * 2 +
+                        2 * stages * 8;
+    DAOP_CUDA(cudaFuncSetAttribute(attn_oproj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    attn_oproj_kernel<<<sms, (AT_WARPS + 1) * 32, smem, st>>>(d_h, o, d_wo, d, q_dim, rpc, stages,
+                                                              d_h_out);
+    DAOP_CHECK_LAUNCH("attn_oproj");
+  }
   return DAOP_OK;
 }

@@ -116,19 +116,26 @@ class MoEBlockEngine:
 
     # ------------------------------------------------------------ full decode token
     def decode_token(self, h: torch.Tensor, *, start: int = 4, daop: bool = True,
-                     weights_from_pred: bool = True) -> torch.Tensor:
+                     weights_from_pred: bool = True, attn=None, pos: int = 0) -> torch.Tensor:
         """One decode token through every layer, all experts HBM-resident:
         layer l < start (or fiddler) selects by its own gate, layer l >= start
         by the DAOP plan on the prediction carried by layer l-1 -- known when
         the launch starts, so its weight stream starts before its router runs.
-        Returns the final residual (a view into a ping-pong buffer)."""
+        With `attn` (an AttentionStack) every layer is a full decoder layer:
+        h <- h + Attention(RMSNorm(h)) at position `pos` (KV cache append),
+        then the MoE block.  Returns the final residual (a view into a
+        ping-pong buffer)."""
         m = self.model
         L = m.shape.num_layers
         if not hasattr(self, "_pp"):
             self._pp = [ops.DecodeBuffers(self.d, self.ffn, self.E, self.k, self.device)
                         for _ in range(2)]
+        if attn is not None and not hasattr(self, "_ha"):
+            self._ha = torch.empty(self.d, dtype=torch.float32, device=self.device)
         cur = h
         for l in range(L):
+            if attn is not None:
+                cur = attn.decode(cur, l, pos, out=self._ha)
             b = self._pp[l % 2]
             mode = 1 if (daop and l >= start) else 0
             nxt = m.gate[l + 1] if l + 1 < L else None
