@@ -170,17 +170,20 @@ def moe_layer(model: OracleModel, layer: int, h: np.ndarray, sel=None, w=None,
 
 
 def daop_decode_token(model: OracleModel, h: np.ndarray, sel_per_layer, start: int,
-                      weights_from_pred: bool = True, engine: str = "daop"):
+                      weights_from_pred: bool = True, engine: str = "daop", pre=None):
     """One decode token through all layers with the engine's decisions injected
     (teacher forcing).  Below `start` (or for fiddler) picks run on the current
     x_l with true-gate weights; from `start` on (daop) weights come from the
     prediction carried on layer l-1 and slow picks -- flagged by the caller --
     use the stale x_{l-1} (policies.py:325-330).
 
-    sel_per_layer: list of (experts, slow_flags) per layer.  Returns h'."""
+    sel_per_layer: list of (experts, slow_flags) per layer; pre(h, l) (optional)
+    is the non-MoE block applied before layer l's MoE block.  Returns h'."""
     h = h.astype(np.float32)[None, :]
     x_prev, ph_prev = None, None
     for l in range(model.L):
+        if pre is not None:
+            h = pre(h[0], l)[None, :].astype(np.float32)
         x = rmsnorm(h, model.norm(l))
         wg_next = model.gate(l + 1) if l + 1 < model.L else None
         p, ph = router(x, model.gate(l), wg_next)

@@ -136,7 +136,8 @@ class DaopEngine:
     def __init__(self, shape: ModelShape, d_model: int, d_ff: int, calib, ecr: float,
                  config: PolicyConfig | None = None, seed: int = 0, device="cuda",
                  swap_in_out: float = SWAP_IN_OUT_DEFAULT, weights_from_pred: bool = True,
-                 host_pool: HostExpertPool | None = None, host_threads: int = 0):
+                 host_pool: HostExpertPool | None = None, host_threads: int = 0,
+                 attention: bool = False, max_seq: int = 1024):
         self.config = config or PolicyConfig("daop")
         self.shape = shape
         self.placement0 = init_from_calibration(calib, ecr, shape)
@@ -157,6 +158,16 @@ class DaopEngine:
         self.migrations_done = 0
         E, k = shape.num_experts, shape.top_k
         self.bufs = [ops.DecodeBuffers(d_model, d_ff, E, k, self.model.device) for _ in range(2)]
+        # the non-MoE block: attention with a KV cache or,
+        # without it, the residual stream goes straight into the MoE block
+        self.attn = None
+        self.pos = 0
+        if attention:
+            from .attention import AttentionStack
+            heads = d_model // 128
+            self.attn = AttentionStack(shape.num_layers, d_model, heads, max(1, heads // 4),
+                                       max_seq=max_seq, seed=seed, device=self.model.device)
+            self._h_attn = torch.empty(d_model, dtype=torch.float32, device=self.model.device)
         self._lru = None  # LRU planner of the ondemand / prefetch engines (after prefill)
 
     # ------------------------------------------------------------ residency
@@ -194,6 +205,24 @@ class DaopEngine:
             evs.append(self._migrate_in(layer, ev.swapped_in, slot, wait=False))
         return start, evs
 
+    # ------------------------------------------------------------ non-MoE block
+    def _non_moe(self, h: torch.Tensor, layer: int, pos: int) -> torch.Tensor:
+        """h + Attention(RMSNorm(h)) at position pos (decode, one token)."""
+        if self.attn is None:
+            return h
+        return self.attn.decode(h, layer, pos, out=self._h_attn)
+
+    def _non_moe_prefill(self, h: torch.Tensor, layer: int) -> torch.Tensor:
+        """Causal attention over the prompt, token by token (each token's
+        layer-l attention reads the layer-l keys / values of the tokens before
+        it, which are in the cache by then)."""
+        if self.attn is None:
+            return h
+        out = torch.empty_like(h)
+        for t in range(h.shape[0]):
+            self.attn.decode(h[t], layer, t, out=out[t])
+        return out
+
     # ------------------------------------------------------------ prefill
     def prefill(self, h: torch.Tensor) -> PrefillResult:
         m = self.model
@@ -208,6 +237,7 @@ class DaopEngine:
         slow_execs = 0
         mig_timing = []  # per layer: (migration start, copies done, resident GEMMs done)
         for l in range(L):
+            h = self._non_moe_prefill(h, l)
             nxt = m.gate[l + 1] if l + 1 < L else None
             r = ops.router(h, m.norm[l], m.gate[l], nxt, k, hist=hist[:, l], tokens_per_seq=T,
                            hist_seq_stride=L * E)
@@ -289,6 +319,7 @@ class DaopEngine:
             h = out
         torch.cuda.synchronize()
         self.placement = ExpertPlacement(self.shape, new_sets, self.placement0.slot_budget)
+        self.pos = T  # the first decode token's position
         if self.config.engine in ("ondemand", "prefetch"):
             self._lru = make_planner(self.placement, self.config)
         counts = hist[0].to(torch.int64).cpu().numpy()
@@ -382,7 +413,9 @@ class DaopEngine:
         true_sc = np.zeros((L, E))
         pred_sc = np.zeros((L, E))
         prev_b, prev_v = None, None
+        pos = self.pos
         for l in range(L):
+            h = self._non_moe(h, l, pos)
             b = self.bufs[l % 2]
             ht, v = mh[l % 2]
             mode = 1 if (daop and l >= start) else 0
@@ -432,6 +465,7 @@ class DaopEngine:
             prev_b, prev_v = b, v
         torch.cuda.synchronize()
         h = h.clone()
+        self.pos += 1
         plans = plans_from_arrays(sel, fast, drop, sub, nd, pred_sc, cfg)
         return DecodeResult(h, plans, true_sc, pred_sc, 1e3 * (time.perf_counter() - t0))
 
@@ -456,7 +490,9 @@ class DaopEngine:
         true_sc = np.zeros((L, E))
         pred_sc = np.zeros((L, E))
         plans = []
+        pos = self.pos
         for l in range(L):
+            h = self._non_moe(h, l, pos)
             b = self.bufs[l % 2]
             nxt = m.gate[l + 1] if l + 1 < L else None
 
@@ -484,6 +520,7 @@ class DaopEngine:
                                    migrations=dec.migrations,
                                    prefetch_issues=dec.prefetch_issues))
         torch.cuda.synchronize()
+        self.pos += 1
         return DecodeResult(h, plans, true_sc, pred_sc, 1e3 * (time.perf_counter() - t0))
 
     # ------------------------------------------------------------ sequence

@@ -38,12 +38,15 @@ def main():
     ap.add_argument("--ecr", type=float, nargs="+", default=[0.75, 0.5, 0.25])
     ap.add_argument("--out", default="")
     ap.add_argument("--trace-dir", default="", help="save each run's routing trace (moesim JSONL)")
+    ap.add_argument("--attention", action="store_true",
+                    help="full decoder layers: attention with a KV cache before each MoE block")
     a = ap.parse_args()
     shape = P.ModelShape(a.layers, 8, 2)
     t0 = time.perf_counter()
     pool = HostExpertPool(shape, a.d, a.ffn, seed=0)
     res = {"config": {"layers": a.layers, "d": a.d, "ffn": a.ffn, "experts": 8, "top_k": 2,
-                      "prompt_tokens": a.prompt, "decode_tokens": a.decode},
+                      "prompt_tokens": a.prompt, "decode_tokens": a.decode,
+                      "attention": a.attention},
            "host_pool_gb": pool.buf.numel() * 2 / 1e9,
            "host_pool_setup_s": time.perf_counter() - t0}
     caps = np.zeros(2, dtype=np.int32)
@@ -65,7 +68,8 @@ def main():
     runs = []
     for ecr in a.ecr:
         eng = DaopEngine(shape, a.d, a.ffn, calib, ecr, P.PolicyConfig("daop"), seed=0,
-                         host_pool=pool)
+                         host_pool=pool, attention=a.attention,
+                         max_seq=a.prompt + a.decode + 64)
         prompt = eng.model.input_hidden(a.prompt, stream=400)
         toks = [eng.model.input_hidden(1, stream=401, step=i)[0] for i in range(a.decode)]
         torch.cuda.synchronize()

@@ -24,10 +24,12 @@ def _calib(L, E, k, seed):
     return c
 
 
-@pytest.mark.parametrize("engine,ecr,start", [("daop", 0.5, 4), ("daop", 0.25, 2),
-                                              ("fiddler", 0.5, 4), ("daop", 1.0, 4),
-                                              ("ondemand", 0.5, 4), ("prefetch", 0.25, 2)])
-def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
+@pytest.mark.parametrize("engine,ecr,start,attention", [
+    ("daop", 0.5, 4, False), ("daop", 0.25, 2, False), ("fiddler", 0.5, 4, False),
+    ("daop", 1.0, 4, False), ("ondemand", 0.5, 4, False), ("prefetch", 0.25, 2, False),
+    # full decoder layers: attention with a KV cache before every MoE block
+    ("daop", 0.5, 4, True), ("ondemand", 0.5, 4, True)])
+def test_daop_sequence_matches_reference_decisions(engine, ecr, start, attention):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_2501_10375_b200 as P
@@ -37,7 +39,8 @@ def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
     shape = P.ModelShape(L, E, k)
     calib = _calib(L, E, k, 5)
     cfg = P.PolicyConfig(engine, prediction_start_layer=start)
-    eng = DaopEngine(shape, d, ffn, calib, ecr, cfg, seed=0, device="cuda")
+    eng = DaopEngine(shape, d, ffn, calib, ecr, cfg, seed=0, device="cuda",
+                     attention=attention, max_seq=128)
     prompt = eng.model.input_hidden(64, stream=11)
     toks = [eng.model.input_hidden(1, stream=12, step=i)[0] for i in range(10)]
     rec = eng.run_sequence(prompt, toks, "s0")
@@ -102,7 +105,16 @@ def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
     om = N.OracleModel(L, E, k, d, ffn, seed=0)
     h = prompt.cpu().numpy()
     ptop = D.topk_rows(tr.prefill_true.reshape(-1, E), k).reshape(64, L, k)
+    if attention:
+        oatt = N.OracleAttention(d, d // 128, max(1, d // 512), theta=eng.attn.theta, seed=0)
+        caches = {}
     for l in range(L):
+        if attention:  # causal attention over the prompt (the oracle keeps its own cache)
+            kc = np.zeros((oatt.n_kv, 128, 128), dtype=np.float32)
+            vc = np.zeros_like(kc)
+            for t in range(64):
+                h[t], _, kc, vc = N.attention_decode(oatt, l, h[t], t, kc, vc)
+            caches[l] = [kc, vc]
         p = tr.prefill_true[:, l, :].astype(np.float32)
         sel = ptop[:, l, :]
         h = N.moe_layer(om, l, h, sel=sel, w=N.renorm_weights(p, sel))["out"]
@@ -114,8 +126,14 @@ def test_daop_sequence_matches_reference_decisions(engine, ecr, start):
         plans = rec.decode[t].plans
         sel = [([x.expert for x in p.executed], [x.device == "slow" for x in p.executed])
                for p in plans]
+        pre = None
+        if attention:
+            def pre(hv, l, pos=64 + t):
+                out, _, caches[l][0], caches[l][1] = N.attention_decode(
+                    oatt, l, hv, pos, caches[l][0], caches[l][1])
+                return out
         ref = N.daop_decode_token(om, toks[t].cpu().numpy(), sel, start, True,
-                                  engine if engine in ("daop", "fiddler") else "fiddler")
+                                  engine if engine in ("daop", "fiddler") else "fiddler", pre=pre)
         got = rec.decode[t].out.cpu().numpy()
         rms = float(np.sqrt(np.mean(ref.astype(np.float64) ** 2)))
         assert np.abs(got - ref).max() <= 5e-3 * rms + 2e-3 * np.abs(ref).max(), t
