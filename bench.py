@@ -12,8 +12,10 @@ takes a fresh token, so the picked experts change step to step; the 2.8 GB
 of expert weights exceed the 126 MB L2, so no L2 flush is needed.
 
   value  tokens/s with the token already in HBM (device clock, max over ranks)
-  e2e    tokens/s through the public host API (MoEBlockEngine.decode_host):
-         pinned h -> H2D -> decode -> D2H of (h_out, picks) -> sync, per step
+  e2e    tokens/s through the public host API with host buffers every step:
+         MoEBlockEngine.decode_server().step (persistent kernel: h pulled from
+         pinned memory on a doorbell, residual + picks written back to pinned
+         memory) -- e2e_launch is the launch-per-call MoEBlockEngine.decode_host
   roofline  HBM: algorithmic bytes per launch / CUDA-event launch duration,
             against MEASURED_PEAKS.json hbm_gbs (driver-measured copy peak)
   prefill   BASELINE configs[3]: 8 sequences x 4096 tokens through the same
@@ -403,6 +405,9 @@ def run_b200(args, world, rank, local_rank):
 
     if rank != 0:
         return None
+    e2e_launch = {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                  "d2h_bytes_per_step": d2h,
+                  "api": "MoEBlockEngine.decode_host (one CUDA graph launch + sync per call)"}
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -420,8 +425,10 @@ def run_b200(args, world, rank, local_rank):
                      "launch_us_p50": launch_ms[len(launch_ms) // 2] * 1e3,
                      "frac_of_8tbs": achieved / 8000.0},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": "MoEBlockEngine.decode_host"},
+        # headline end-to-end: the serving call (persistent kernel), when it ran;
+        # the launch-per-call host API beside it
+        "e2e": (dict(e2e_server) if e2e_server and "value" in e2e_server else e2e_launch),
+        "e2e_launch": e2e_launch,
         "e2e_server": e2e_server,
         "gpu_launches": args.steps,
         "clocks": clocks,
