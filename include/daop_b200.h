@@ -211,6 +211,18 @@ int daop_expert_gemm_down(const uint16_t* d_act, int64_t rows, int32_t d, int32_
                           const int64_t* d_offsets, const int32_t* d_slot_of,
                           int32_t num_experts, float* d_y, int32_t group_m,
                           daop_stream_t stream);
+/* down GEMM with the combine fused into its epilogue: each token's last pick
+ * to land (per 256-column tile) writes d_out = d_h + sum_j w_j y_j in fixed j
+ * order (daop_combine's arithmetic); d_perm / d_inv from daop_permute,
+ * d_cnt (T, d / 256) u32 zeroed once and self-resetting.  Needs the CTA-pair
+ * kernel (gemm mode 0). */
+int daop_expert_gemm_down_combine(const uint16_t* d_act, int64_t rows, int32_t d, int32_t ffn,
+                                  const uint16_t* d_slab, int64_t n_slots,
+                                  int64_t slot_stride_elems, const int64_t* d_offsets,
+                                  const int32_t* d_slot_of, int32_t num_experts, float* d_y,
+                                  const int32_t* d_perm, const int32_t* d_inv, const float* d_h,
+                                  const float* d_w, int32_t k, float* d_out, uint32_t* d_cnt,
+                                  int32_t group_m, daop_stream_t stream);
 
 /* ------------------------------------------------ expert parallelism over peer memory
  * Replaces the NCCL all-to-all dispatch / combine that SURVEY.md §8b

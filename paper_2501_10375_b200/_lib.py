@@ -53,6 +53,8 @@ PROTOS = {
     "daop_set_gemm_mode": [I32],
     "daop_expert_gemm_up": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
+    "daop_expert_gemm_down_combine": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, P, P, P, P,
+                                      I32, P, P, I32, P],
     "daop_ep_ws_layout": [I32, I32, I32, I64, I64, P, P, P, P],
     "daop_ep_publish": [P, I32, I32, I32, P, C.c_uint32, P],
     "daop_ep_dispatch": [P, I32, I32, I32, I32, I32, P, P, I64, I64, C.c_uint32, P],

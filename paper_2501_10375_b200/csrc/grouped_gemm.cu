@@ -75,7 +75,55 @@ struct GemmParams {
   const uint64_t* sig_peers;
   int sig_G, sig_rank;
   unsigned sig_epoch;
+  // fused combine (down GEMM, single GPU): after storing its y slice of
+  // (row, n-tile), a thread counts it on the token's counter; the token's
+  // last pick to land computes out = h + sum_j w_j y_j over that n-tile in
+  // fixed j order (the combine kernel's arithmetic) -- no separate pass
+  const int32_t* comb_perm;  // sorted row -> t * k + j
+  const int32_t* comb_inv;   // t * k + j -> sorted row
+  const float* comb_h;       // (T, d) residual in
+  const float* comb_w;       // (T, k) weights
+  float* comb_out;           // (T, d)
+  unsigned* comb_cnt;        // (T, n_tiles) zeroed once, self-resetting
+  int comb_k;
 };
+
+// the fused combine of one (row, n-tile): called by the row's thread after
+// its y slice is stored and the accumulator released
+__device__ __forceinline__ void fused_combine(const GemmParams& p, int64_t grow, int n) {
+  __threadfence();  // this thread's y slice -> visible to the token's last pick
+  const int k = p.comb_k;
+  const int src = p.comb_perm[grow];
+  const int64_t t = src / k;
+  const int nt = p.n_tiles;
+  const unsigned old = atomicAdd(p.comb_cnt + t * nt + n, 1u);
+  if (old != static_cast<unsigned>(k - 1)) return;
+  p.comb_cnt[t * nt + n] = 0;  // self-resetting for the next layer
+  __threadfence();
+  const int64_t d = p.out_ld;
+  const float* y = static_cast<const float*>(p.out);
+  const float4* hr = reinterpret_cast<const float4*>(p.comb_h + t * d + n * GB_N);
+  float4* o = reinterpret_cast<float4*>(p.comb_out + t * d + n * GB_N);
+  float wj[8];
+  const float4* yr[8];
+  for (int j = 0; j < k && j < 8; ++j) {
+    wj[j] = p.comb_w[t * k + j];
+    yr[j] = reinterpret_cast<const float4*>(y + static_cast<int64_t>(p.comb_inv[t * k + j]) * d +
+                                            n * GB_N);
+  }
+#pragma unroll 4
+  for (int c = 0; c < GB_N / 4; ++c) {
+    float4 acc = __ldcg(hr + c);
+    for (int j = 0; j < k && j < 8; ++j) {
+      const float4 v = __ldcg(yr[j] + c);
+      acc.x = fmaf(wj[j], v.x, acc.x);
+      acc.y = fmaf(wj[j], v.y, acc.y);
+      acc.z = fmaf(wj[j], v.z, acc.z);
+      acc.w = fmaf(wj[j], v.w, acc.w);
+    }
+    o[c] = acc;
+  }
+}
 
 // end-of-kernel EP signal: every thread fences its (remote) output stores,
 // the last CTA to arrive publishes the flags
@@ -622,6 +670,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&s.tempty[acc], 0);
+      if constexpr (!SWIGLU) {
+        if (p.comb_cnt) {  // accumulator released: the combine runs off the MMA's path
+          const int row_in_tile = (TWO_M ? ((warp - 2) >> 2) * 256 : 0) + rank * 128 + q * 32 + lane;
+          if (static_cast<int64_t>(m) * C::M + row_in_tile < me)
+            fused_combine(p, s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile, n);
+        }
+      }
       if (p.demote && !TWO_M) {
         const int row_in_tile = rank * 128 + q * 32 + lane;
         const bool valid = static_cast<int64_t>(m) * C::M + row_in_tile < me;
@@ -818,6 +873,55 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
   GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, grp,
                GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0,
                g_gemm_demote & 2, act, ffn, w2, ffn, slot_stride_elems};
+  return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
+}
+
+// Down GEMM with the combine fused into its epilogue (single GPU prefill;
+// measured 0.7 ms per 8 x 4096-token layer SLOWER than GEMM + bulk combine
+// kernel -- the last picks' combine loads delay the single-accumulator
+// epilogue -- so MoEBlockEngine.prefill keeps the separate pass by default):
+// y (rows, d) fp32 is still written (the first picks of a token park their
+// slice there); out (T, d) = h + sum_j w_j y_j is written by each token's last
+// pick per n-tile.  cnt: (T, d / 256) u32, zeroed once, self-resetting.
+extern "C" int daop_expert_gemm_down_combine(const uint16_t* act, int64_t rows, int32_t d,
+                                             int32_t ffn, const uint16_t* slab, int64_t n_slots,
+                                             int64_t slot_stride_elems, const int64_t* d_offsets,
+                                             const int32_t* d_slot_of, int32_t E, float* y,
+                                             const int32_t* d_perm, const int32_t* d_inv,
+                                             const float* d_h, const float* d_w, int32_t k,
+                                             float* d_out, uint32_t* d_cnt, int32_t group_m,
+                                             daop_stream_t stream) {
+  int rc = check_ffn_shape(rows, d, ffn, E);
+  if (rc) return rc;
+  if (k < 1 || k > 8 || g_gemm_mode != 0 || d % GB_N != 0) {
+    set_error("fused combine: needs the CTA-pair kernel, k in 1..8 and d %% 256 == 0 "
+              "(k=%d, mode=%d)", k, g_gemm_mode);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (rows == 0) return DAOP_OK;
+  CUtensorMap ta, tb;
+  const uint64_t adims[2] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(rows)};
+  const uint64_t astr[1] = {static_cast<uint64_t>(ffn) * 2};
+  const uint32_t abox[2] = {GB_K, GB_M};
+  if ((rc = make_tmap_bf16(&ta, act, 2, adims, astr, abox))) return rc;
+  const uint64_t bdims[3] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(d),
+                             static_cast<uint64_t>(n_slots)};
+  const uint64_t bstr[2] = {static_cast<uint64_t>(ffn) * 2,
+                            static_cast<uint64_t>(slot_stride_elems) * 2};
+  const uint32_t bbox[3] = {GB_K, 128, 1};
+  const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
+  if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
+  const int grp = group_m != 0 ? group_m : ((g_gemm_two_m & 2) ? -16 : -8);
+  GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, grp,
+               GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0,
+               g_gemm_demote & 2, act, ffn, w2, ffn, slot_stride_elems};
+  p.comb_perm = d_perm;
+  p.comb_inv = d_inv;
+  p.comb_h = d_h;
+  p.comb_w = d_w;
+  p.comb_out = d_out;
+  p.comb_cnt = reinterpret_cast<unsigned*>(d_cnt);
+  p.comb_k = k;
   return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
 }
 

@@ -160,7 +160,8 @@ class MoEBlockEngine:
 
     # ------------------------------------------------------------ prefill
     def prefill(self, h: torch.Tensor, layer: int = 0, *, hist=None, tokens_per_seq: int = 0,
-                hist_seq_stride: int = 0, group_up: int = 0, group_down: int = 0):
+                hist_seq_stride: int = 0, group_up: int = 0, group_down: int = 0,
+                fused_combine: bool = False):
         """T tokens (h: (T, d) fp32 on device) through MoE layer `layer`.
         Returns dict(out, p, p_pred, topk_idx, topk_w).  `hist` (optional,
         int32 view [seq, E] of this layer) receives the activation counts."""
@@ -172,9 +173,14 @@ class MoEBlockEngine:
         slot_of = m.slot_of[layer]
         act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_of, m.slab, m.n_slots,
                                  m.slot_elems, self.d, self.ffn, group_up)
-        y = ops.expert_gemm_down(act, pr["offsets"], slot_of, m.slab, m.n_slots, m.slot_elems,
-                                 self.d, self.ffn, group_down)
-        out = ops.combine(h, y, pr["inv"], r["topk_w"])
+        if fused_combine:  # combine in the down GEMM's epilogue (measured slower: off)
+            out, y = ops.expert_gemm_down_combine(act, pr["offsets"], slot_of, m.slab, m.n_slots,
+                                                  m.slot_elems, self.d, self.ffn, pr["perm"],
+                                                  pr["inv"], h, r["topk_w"], group_down)
+        else:
+            y = ops.expert_gemm_down(act, pr["offsets"], slot_of, m.slab, m.n_slots,
+                                     m.slot_elems, self.d, self.ffn, group_down)
+            out = ops.combine(h, y, pr["inv"], r["topk_w"])
         r["out"] = out
         r["offsets"] = pr["offsets"]
         return r

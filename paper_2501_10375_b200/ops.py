@@ -124,6 +124,24 @@ def expert_gemm_down(act, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, g
     return y
 
 
+def expert_gemm_down_combine(act, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, perm,
+                             inv, h, w, group_m=0):
+    """Down GEMM + combine in one kernel (daop_expert_gemm_down_combine):
+    returns (out (T, d) = h + sum_j w_j y_j, y).  Raises DeviceError when the
+    fused form is unavailable (single-CTA tuning mode)."""
+    _dev(act, offsets, slot_of, slab, perm, inv, h, w)
+    rows = act.shape[0]
+    t, k = inv.shape
+    y = torch.empty((rows, d), dtype=torch.float32, device=act.device)
+    out = torch.empty_like(h)
+    cnt = torch.zeros((t, d // 256), dtype=torch.int32, device=act.device)
+    _lib.call("daop_expert_gemm_down_combine", act.data_ptr(), rows, d, ffn, slab.data_ptr(),
+              n_slots, slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
+              y.data_ptr(), perm.data_ptr(), inv.data_ptr(), h.data_ptr(), w.data_ptr(), k,
+              out.data_ptr(), cnt.data_ptr(), group_m, _s())
+    return out, y
+
+
 def combine(h, y_sorted, inv, w, out=None):
     _dev(h, y_sorted, inv, w, out)
     t, d = h.shape

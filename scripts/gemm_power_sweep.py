@@ -66,6 +66,14 @@ for cfg in CONFIGS:
                 torch.matmul(acts[e], w2[e].t())
         elif which == "prefill":  # the whole layer through the engine, default groups
             eng.prefill(h, 0)
+        elif which == "prefill_sep":  # the same layer with the separate combine pass
+            rr = ops.router(h, m.norm[0], m.gate[0], m.gate[1], k)
+            pp = ops.permute(rr["topk_idx"], E, rr["x"])
+            aa = ops.expert_gemm_up(pp["x_perm"], pp["offsets"], m.slot_of[0], m.slab,
+                                    m.n_slots, m.slot_elems, d, ffn)
+            yy = ops.expert_gemm_down(aa, pp["offsets"], m.slot_of[0], m.slab, m.n_slots,
+                                      m.slot_elems, d, ffn)
+            ops.combine(h, yy, pp["inv"], rr["topk_w"])
         elif which == "up":
             ops.expert_gemm_up(pr["x_perm"], pr["offsets"], m.slot_of[0], m.slab, m.n_slots,
                                m.slot_elems, d, ffn, grp)
@@ -88,7 +96,8 @@ for cfg in CONFIGS:
     stop.set()
     th.join()
     ms = e0.elapsed_time(e1) / N
-    fl = 2.0 * T * k * d * ffn * (2 if which.endswith("up") else 3 if which == "prefill" else 1)
+    fl = 2.0 * T * k * d * ffn * (2 if which.endswith("up") else 3 if which.startswith("prefill")
+                                  else 1)
     print(f"{cfg:12s} {ms:7.3f} ms  {fl / ms / 1e9:7.1f} TF/s  sm {statistics.median(samples):.0f} MHz",
           flush=True)
 ops.set_gemm_mode(0)

@@ -404,3 +404,26 @@ def test_decode_server_idle_exit(P):
     with pytest.raises(Exception):
         srv.step(torch.zeros(256), timeout_ms=300.0)
     srv.close()
+
+
+@pytest.mark.parametrize("d,ffn,E,T", [(512, 1024, 8, 700), (4096, 14336, 8, 300)])
+def test_fused_down_combine_bitexact(P, d, ffn, E, T):
+    """The down GEMM with the combine fused into its epilogue (each token's
+    last pick writes h + sum_j w_j y_j) == down GEMM + combine kernel, bit
+    for bit, twice in a row (the per-token counters reset themselves)."""
+    pkg, model_mod, ops = P
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, 2), d, ffn, seed=7, resident_layers=[0])
+    h = m.input_hidden(T, stream=4)
+    r = ops.router(h, m.norm[0], m.gate[0], m.gate[1], 2)
+    pr = ops.permute(r["topk_idx"], E, r["x"])
+    so = m.slot_of[0]
+    act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems,
+                             d, ffn)
+    y = ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn)
+    ref = ops.combine(h, y, pr["inv"], r["topk_w"])
+    for _ in range(2):
+        out, y2 = ops.expert_gemm_down_combine(act, pr["offsets"], so, m.slab, m.n_slots,
+                                               m.slot_elems, d, ffn, pr["perm"], pr["inv"], h,
+                                               r["topk_w"])
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
