@@ -7,7 +7,7 @@ timeout 900 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; e
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json
 timeout 600 python bench.py --impl reference --steps 50 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json
 if [ "$1" == "ncu" ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"decode_layer|router|perm_|grouped_gemm|combine" -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-ep --no-server > gpurun_out/ncu_bench.log 2>&1; echo "ncu list rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"decode_layer|router|perm_|gather|grouped_gemm|combine" -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-ep --no-server > gpurun_out/ncu_bench.log 2>&1; echo "ncu list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_layer -s 3 -c 1 -o gpurun_out/prof_decode -f python scripts/profile_target.py decode > gpurun_out/ncu_decode.log 2>&1; echo "ncu decode rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -s 2 -c 2 -o gpurun_out/prof_gemm -f python scripts/profile_target.py prefill > gpurun_out/ncu_gemm.log 2>&1; echo "ncu gemm rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:router -s 1 -c 1 -o gpurun_out/prof_router -f python scripts/profile_target.py prefill > gpurun_out/ncu_router.log 2>&1; echo "ncu router rc=$?"
