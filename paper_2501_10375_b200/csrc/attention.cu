@@ -26,7 +26,6 @@ namespace daop {
 
 constexpr int AT_WARPS = 16;    // GEMV CTAs
 constexpr int AT_HD = 128;      // head dim (Mixtral / Llama)
-constexpr int AT_TILE = 128;    // positions per attention tile (one per thread)
 constexpr int AT_MAX_GROUP = 8; // q heads per kv head
 
 // Bulk-streamed GEMV over this CTA's block of rows: warp AT_WARPS (lane 0)
