@@ -625,6 +625,28 @@ def run_ep_decode(args, world, rank, dev, hbm_peak, barrier):
     barrier()
     dec.check()
     ms = e0.elapsed_time(e1) / steps
+    # NCCL baseline of the same step (decode kernel + all_reduce of the picks' outputs)
+    from paper_2501_10375_b200 import ops as _ops
+    from paper_2501_10375_b200.ep import nccl_ep_decode_layer
+    nb = _ops.DecodeBuffers(EP_D, EP_FFN, E, K, dev)
+    y_sum = torch.empty((K, EP_D), dtype=torch.float32, device=dev)
+    o_n = torch.empty(EP_D, dtype=torch.float32, device=dev)
+    for i in range(8):
+        nccl_ep_decode_layer(m, 0, hs[i % 32], nb, y_sum, o_n)
+    barrier()
+    torch.cuda.synchronize()
+    n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0.record(stream)
+    for i in range(steps):
+        nccl_ep_decode_layer(m, 0, hs[i % 32], nb, y_sum, o_n)
+    n1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_n = n0.elapsed_time(n1) / steps
+    tn = torch.tensor([ms_n], device=dev)
+    if world > 1:
+        dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+    ms_n = float(tn.item())
     t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -647,6 +669,9 @@ def run_ep_decode(args, world, rank, dev, hbm_peak, barrier):
                      "bytes_per_step": step_bytes,
                      "note": "b=1 touches 2 experts: at most 2 GPUs stream; peak = that many x HBM"},
         "gpu_launches_per_step": 2,
+        "nccl_baseline": {"value": 1e3 / ms_n, "unit": "tokens/s", "ms_per_step": ms_n,
+                          "collective": "nccl all_reduce of the k x d pick outputs"
+                                        if world > 1 else "none (G=1)"},
     }
 
 def main():

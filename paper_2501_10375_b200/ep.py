@@ -534,3 +534,23 @@ class PeerEPDecode:
 
     def check(self):
         _check_ws(self.ws, "peer-memory EP decode")
+
+
+def nccl_ep_decode_layer(model, layer: int, h: torch.Tensor, bufs, y_sum: torch.Tensor,
+                         out: torch.Tensor, group=None):
+    """Baseline of PeerEPDecode with a collective: every rank runs the decode
+    kernel on its own experts, zeroes the outputs of picks it does not own,
+    and an all_reduce (NCCL over NVLink) sums the k x d outputs -- each pick
+    has exactly one non-zero contribution, so the sum is exact -- then the
+    fixed-order combine.  Bit-identical to the single-GPU decode layer."""
+    from . import _lib, ops
+    m = model
+    nxt = m.gate[layer + 1] if layer + 1 < m.shape.num_layers else None
+    ops.decode_layer(h, m.norm[layer], m.gate[layer], nxt, m.fast[layer], m.slot_of[layer],
+                     m.slab, m.slot_elems, m.d, m.ffn, m.shape.top_k, bufs)
+    torch.mul(bufs.y, bufs.is_fast.view(-1, 1).to(torch.float32), out=y_sum)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(y_sum, group=group)
+    _lib.call("daop_combine_dense", h.data_ptr(), y_sum.data_ptr(), bufs.w.data_ptr(),
+              m.shape.top_k, m.d, out.data_ptr(), ops._s())
+    return out

@@ -141,6 +141,18 @@ def _two_proc_worker(rank, port, q):
             dec.check()
             ref = eng.decode(h1, 0)
             ok = ok and _t.equal(got, ref.h_out)
+        # the collective baseline of the same step (all_reduce of the pick outputs)
+        from paper_2501_10375_b200 import ops as _ops
+        from paper_2501_10375_b200.ep import nccl_ep_decode_layer
+        nb = _ops.DecodeBuffers(d, ffn, E, 2, "cuda")
+        y_sum = _t.empty((2, d), dtype=_t.float32, device="cuda")
+        o_n = _t.empty(d, dtype=_t.float32, device="cuda")
+        for step in range(2):
+            h1 = m.input_hidden(1, stream=61, step=step)[0]
+            got = nccl_ep_decode_layer(me, 0, h1, nb, y_sum, o_n)
+            _t.cuda.synchronize()
+            ref = eng.decode(h1, 0)
+            ok = ok and _t.equal(got, ref.h_out)
         dist.barrier()
         dec.close()
         ctx.close()
