@@ -290,27 +290,56 @@ def open_peer_table(ws: torch.Tensor, rank: int, world: int, group=None):
     _lib.call("daop_ep_ipc_handle", ws.data_ptr(), ctypes.addressof(handle), off.data_ptr())
     allh = [None] * world
     dist.all_gather_object(allh, (bytes(handle.raw), int(off[0])), group=group)
-    ptrs, bases = [], []
+    ptrs, bases, err = [], [], ""
     for s, (hb, o) in enumerate(allh):
         if s == rank:
             ptrs.append(ws.data_ptr())
             continue
         hbuf = ctypes.create_string_buffer(hb, 64)
         base, ptr = ctypes.c_void_p(), ctypes.c_void_p()
-        _lib.call("daop_ep_ipc_open", ctypes.addressof(hbuf), o, ctypes.byref(base),
-                  ctypes.byref(ptr))
+        try:
+            _lib.call("daop_ep_ipc_open", ctypes.addressof(hbuf), o, ctypes.byref(base),
+                      ctypes.byref(ptr))
+        except Exception as exc:  # every rank must learn about it (no half-open group)
+            err = f"rank {rank}: peer {s}: {exc}"
+            break
         bases.append(base.value)
         ptrs.append(ptr.value)
-    dist.barrier(group=group)
+    _all_ok(not err, group, err or "a peer could not open this rank's workspace", bases)
     return torch.tensor(ptrs, dtype=torch.int64, device=ws.device), bases
 
 
-def _check_ws(ws: torch.Tensor, what: str):
+def _all_ok(ok: bool, group, what: str, bases=()):
+    """Collective success check: every rank raises if any rank failed, so the
+    ranks never diverge into mismatched collectives."""
+    from . import _lib
+    from .errors import DeviceError
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                        device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 0:
+        for b in bases:
+            try:
+                _lib.call("daop_ep_ipc_close", b)
+            except Exception:
+                pass
+        raise DeviceError(f"peer-memory EP setup failed: {what}")
+
+
+def _check_ws(ws: torch.Tensor, what: str, world: int = 1, group=None):
+    """Raise if any cross-GPU wait of this workspace timed out -- on every
+    rank when world > 1 (the flag is reduced over the group)."""
     from . import _lib
     from .errors import DeviceError
     err = torch.zeros(1, dtype=torch.int32)
     _lib.call("daop_ep_status", ws.data_ptr(), err.data_ptr())
-    if int(err[0]):
+    bad = int(err[0])
+    if world > 1 and dist.is_available() and dist.is_initialized():
+        flag = torch.tensor([bad], dtype=torch.int32,
+                            device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+        bad = int(flag.item())
+    if bad:
         raise DeviceError(f"{what}: a cross-GPU wait timed out (peer not progressing)")
 
 
@@ -355,6 +384,7 @@ class PeerEP:
         self.act = torch.empty((self.cap_recv, self.ffn), dtype=torch.bfloat16, device=dev)
         self.epoch = 0
         self._ipc_bases = []
+        self._group = group
         if _peer_table is not None:
             self.peers = _peer_table
         elif world == 1:
@@ -446,8 +476,8 @@ class PeerEP:
         return self.ws[self.local_off: self.local_off + 8 * (self.E + 1)].view(torch.int64)
 
     def check(self):
-        """Raise if any cross-GPU wait of this workspace timed out."""
-        _check_ws(self.ws, "peer-memory EP")
+        """Raise (on every rank) if any cross-GPU wait timed out."""
+        _check_ws(self.ws, "peer-memory EP", self.world, self._group)
 
 
 class PeerEPDecode:
@@ -478,6 +508,7 @@ class PeerEPDecode:
         self.out = [torch.empty(self.d, dtype=torch.float32, device=dev) for _ in range(2)]
         self.epoch = 0
         self._ipc_bases = []
+        self._group = group
         if _peer_table is not None:
             self.peers = _peer_table
         elif world == 1:
@@ -533,7 +564,7 @@ class PeerEPDecode:
         return self.finish()
 
     def check(self):
-        _check_ws(self.ws, "peer-memory EP decode")
+        _check_ws(self.ws, "peer-memory EP decode", self.world, self._group)
 
 
 def nccl_ep_decode_layer(model, layer: int, h: torch.Tensor, bufs, y_sum: torch.Tensor,
