@@ -205,6 +205,10 @@ class DecodeServer:
         self.bufs = ops.DecodeBuffers(eng.d, eng.ffn, eng.E, eng.k, eng.device)
         self.stream = torch.cuda.Stream(eng.device)
         nxt = m.gate[layer + 1] if layer + 1 < m.shape.num_layers else None
+        if not bool(m.fast[layer].all()):
+            from .errors import ConfigError
+            raise ConfigError("decode_server needs every expert of the layer in HBM "
+                              "(the slow tier is host work between kernel phases)")
         b = self.bufs
         self._h = ctypes.c_void_p()
         torch.cuda.synchronize(eng.device)  # weights and buffers ready before the kernel starts
