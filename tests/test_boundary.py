@@ -71,3 +71,32 @@ def test_routing_trace_validation_matches_reference_rules():
     t = P.RoutingTrace.from_token_lists(shape, "y", [[P.TokenRouting(good, good),
                                                      P.TokenRouting(good)]])
     assert t.num_prefill_tokens == 1 and t.prefill_mask.tolist() == [[True, False]]
+
+
+def test_ep_workspace_layout_host_rules():
+    """The symmetric EP workspace layout is host arithmetic: offsets are
+    aligned, the receive buffer and y_back fit, bad worlds are refused."""
+    import torch
+    from paper_2501_10375_b200 import _lib
+    from paper_2501_10375_b200.errors import DeviceError
+    out = [torch.zeros(1, dtype=torch.int64) for _ in range(4)]
+    ptrs = [o.data_ptr() for o in out]
+    _lib.call("daop_ep_ws_layout", 4, 8, 4096, 1000, 500, *ptrs)
+    total, recv_off, yback_off, local_off = (int(o[0]) for o in out)
+    assert recv_off % 4096 == 0 and yback_off % 4096 == 0 and total % 4096 == 0
+    assert yback_off >= recv_off + 1000 * 4096 * 2
+    assert total >= yback_off + 500 * 4096 * 4
+    assert local_off < 16384  # local offsets live in the header, before the row table
+    for bad in [(3, 8), (16, 16), (2, 65)]:  # E % G != 0, G > 8, E > 64
+        with pytest.raises(DeviceError):
+            _lib.call("daop_ep_ws_layout", bad[0], bad[1], 4096, 10, 10, *ptrs)
+
+
+def test_attention_workspace_size():
+    import torch
+    from paper_2501_10375_b200 import _lib
+    nb = torch.zeros(1, dtype=torch.int64)
+    _lib.call("daop_attn_workspace", 32, 8, 4096, nb.data_ptr())
+    q, kv = 32 * 128, 8 * 128
+    # qkv fp32 + split partials (8 kv heads x 64 splits x 4 heads x 130) + o bf16 + counters
+    assert int(nb[0]) >= (q + 2 * kv) * 4 + 8 * 64 * 4 * 130 * 4 + q * 2 + 4 * 8
