@@ -116,3 +116,40 @@ def test_plan_exchange_expert_major():
     assert plan.recv == {(0, 2): (0, 5), (1, 2): (5, 1), (0, 3): (6, 7), (1, 3): (13, 0)}
     assert plan.local_offsets == [0, 0, 0, 6, 13]
     assert plan.recv_rows == 13
+
+
+def test_plan_exchange_properties():
+    """Random count matrices: every source segment is sent once, every owner
+    receives exactly the rows addressed to its experts, receive segments tile
+    [0, recv_rows) expert-major without gaps, and non-local experts are empty."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+    from paper_2501_10375_b200.ep import local_experts, plan_exchange
+
+    @settings(max_examples=200, deadline=None)
+    @given(st.sampled_from([(1, 8), (2, 8), (4, 8), (8, 8), (2, 4), (4, 16)]),
+           st.data())
+    def check(ge, data):
+        G, E = ge
+        counts = [[data.draw(st.integers(0, 50)) for _ in range(E)] for _ in range(G)]
+        for r in range(G):
+            offs = [0]
+            for e in range(E):
+                offs.append(offs[-1] + counts[r][e])
+            mine = local_experts(r, E, G)
+            recv = [[counts[s][e] for e in mine] for s in range(G)]
+            plan = plan_exchange(offs, recv, r, G, E)
+            assert [n for _, n in plan.send] == counts[r]
+            assert plan.recv_rows == sum(counts[s][e] for s in range(G) for e in mine)
+            pos = 0
+            for e in range(E):
+                assert plan.local_offsets[e] == pos
+                if e in mine:
+                    for s in range(G):
+                        a, n = plan.recv[(s, e)]
+                        assert a == pos and n == counts[s][e]
+                        pos += n
+                assert plan.local_offsets[e + 1] == pos
+            assert pos == plan.recv_rows
+
+    check()
