@@ -206,6 +206,14 @@ int daop_expert_gemm_up(const uint16_t* d_x_perm, int64_t rows, int32_t d, int32
                         const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
                         const int64_t* d_offsets, const int32_t* d_slot_of, int32_t num_experts,
                         uint16_t* d_act, int32_t group_m, daop_stream_t stream);
+/* up GEMM with its A rows gathered by TMA straight from the token matrix
+ * d_x (src_rows, d): sorted row r reads token d_perm[r] / k (no x_perm). */
+int daop_expert_gemm_up_gather(const uint16_t* d_x, int64_t src_rows, const int32_t* d_perm,
+                               int32_t k, int64_t rows, int32_t d, int32_t ffn,
+                               const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
+                               const int64_t* d_offsets, const int32_t* d_slot_of,
+                               int32_t num_experts, uint16_t* d_act, int32_t group_m,
+                               daop_stream_t stream);
 int daop_expert_gemm_down(const uint16_t* d_act, int64_t rows, int32_t d, int32_t ffn,
                           const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
                           const int64_t* d_offsets, const int32_t* d_slot_of,

@@ -52,6 +52,8 @@ PROTOS = {
     "daop_combine": [P, P, P, P, I64, I32, I32, P, P],
     "daop_set_gemm_mode": [I32],
     "daop_expert_gemm_up": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
+    "daop_expert_gemm_up_gather": [P, I64, P, I32, I64, I32, I32, P, I64, I64, P, P, I32, P, I32,
+                                   P],
     "daop_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_expert_gemm_down_combine": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, P, P, P, P,
                                       I32, P, P, I32, P],

@@ -79,6 +79,12 @@ struct GemmParams {
   // (row, n-tile), a thread counts it on the token's counter; the token's
   // last pick to land computes out = h + sum_j w_j y_j over that n-tile in
   // fixed j order (the combine kernel's arithmetic) -- no separate pass
+  // A rows gathered by TMA (up GEMM, single GPU): sorted row r reads row
+  // a_perm[r] / a_k of the token matrix (the permutation never materialises
+  // x_perm); null = dense A rows
+  const int32_t* a_perm;
+  int a_k;
+  int a_src_rows;
   const int32_t* comb_perm;  // sorted row -> t * k + j
   const int32_t* comb_inv;   // t * k + j -> sorted row
   const float* comb_h;       // (T, d) residual in
@@ -520,7 +526,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
   const int nt = p.n_tiles, G = p.group_m;
 
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer (both CTAs)
+    if (p.a_perm || lane == 0) {  // TMA producer (both CTAs; all lanes when gathering A)
       uint64_t pol_a = l2_evict_last_policy();
       uint64_t pol_b = l2_evict_normal_policy();  // shared by the wave's m-tiles
       if (p.policy == 1) pol_a = l2_evict_normal_policy();
@@ -545,15 +551,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
         const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * C::M) + rank * 128;
         const int slot = p.slot_of[e];
         const int brow = n * p.b_tile_rows + (leader ? 0 : p.b_half2);
+        // gathered A: lane L fetches rows 4L .. 4L+3 of each 128-row box; the
+        // token indices stay in registers for the whole tile (rows past the
+        // matrix repeat a valid row; the epilogue never stores them)
+        int gi[2][4];
+        if (p.a_perm) {
+          const int last = s.off[E] > 0 ? static_cast<int>(s.off[E]) - 1 : 0;
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              const int r = min(row0 + b * 256 + 4 * lane + q2, last);
+              gi[b][q2] = p.a_perm[r] / p.a_k;
+            }
+        }
         for (int kb = 0; kb < p.k_blocks; ++kb) {
-          mbar_wait(&s.empty[stage], phase ^ 1);
+          if (lane == 0) mbar_wait(&s.empty[stage], phase ^ 1);
+          if (p.a_perm) __syncwarp();  // (dense A: lane 0 runs this loop alone)
           uint8_t* st = tiles + stage * C::STAGE_BYTES;
-          if (leader) mbar_arrive_expect_tx(&s.full[stage], 2 * C::STAGE_BYTES);
-          else mbar_arrive_cluster(&s.full[stage], 0);
-          tma_load_2d_pair(st, &tmA, &s.full[stage], kb * GB_K, row0, pol_a);
-          if constexpr (TWO_M)  // second M=256 half: tile rows 256 + rank * 128
-            tma_load_2d_pair(st + P_A_BYTES, &tmA, &s.full[stage], kb * GB_K, row0 + 256, pol_a);
-          tma_load_3d_pair(st + C::A_BYTES, &tmB, &s.full[stage], kb * GB_K, brow, slot, pol_b);
+          if (lane == 0) {
+            if (leader) mbar_arrive_expect_tx(&s.full[stage], 2 * C::STAGE_BYTES);
+            else mbar_arrive_cluster(&s.full[stage], 0);
+          }
+          if (p.a_perm) {
+            __syncwarp();  // the expect_tx precedes every lane's gather
+            tma_gather4_pair(st + lane * 4 * GB_K * 2, &tmA, &s.full[stage], kb * GB_K,
+                             gi[0][0], gi[0][1], gi[0][2], gi[0][3], pol_a);
+            if constexpr (TWO_M)
+              tma_gather4_pair(st + P_A_BYTES + lane * 4 * GB_K * 2, &tmA, &s.full[stage],
+                               kb * GB_K, gi[1][0], gi[1][1], gi[1][2], gi[1][3], pol_a);
+          } else if (lane == 0) {
+            tma_load_2d_pair(st, &tmA, &s.full[stage], kb * GB_K, row0, pol_a);
+            if constexpr (TWO_M)  // second M=256 half: tile rows 256 + rank * 128
+              tma_load_2d_pair(st + P_A_BYTES, &tmA, &s.full[stage], kb * GB_K, row0 + 256, pol_a);
+          }
+          if (lane == 0)
+            tma_load_3d_pair(st + C::A_BYTES, &tmB, &s.full[stage], kb * GB_K, brow, slot, pol_b);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -844,6 +877,44 @@ extern "C" int daop_expert_gemm_up(const uint16_t* x_perm, int64_t rows, int32_t
   GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : 64,
                128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0, 0,
                g_gemm_demote & 1, x_perm, d, slab, d, slot_stride_elems};
+  return launch_gemm<true>(ta, tb, p, rows, as_stream(stream));
+}
+
+// Up GEMM reading its A rows straight from the token matrix x (T_src, d)
+// through TMA row gathers (sorted row r = token perm[r] / k): the
+// permutation's gather pass and x_perm disappear from the prefill.
+extern "C" int daop_expert_gemm_up_gather(const uint16_t* x, int64_t src_rows,
+                                          const int32_t* d_perm, int32_t k, int64_t rows,
+                                          int32_t d, int32_t ffn, const uint16_t* slab,
+                                          int64_t n_slots, int64_t slot_stride_elems,
+                                          const int64_t* d_offsets, const int32_t* d_slot_of,
+                                          int32_t E, uint16_t* act, int32_t group_m,
+                                          daop_stream_t stream) {
+  int rc = check_ffn_shape(rows, d, ffn, E);
+  if (rc) return rc;
+  if (g_gemm_mode != 0 || k < 1 || src_rows < 1) {
+    set_error("gathered up GEMM: needs the CTA-pair kernel (mode %d), k >= 1, rows >= 1",
+              g_gemm_mode);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (rows == 0) return DAOP_OK;
+  CUtensorMap ta, tb;
+  const uint64_t adims[2] = {static_cast<uint64_t>(d), static_cast<uint64_t>(src_rows)};
+  const uint64_t astr[1] = {static_cast<uint64_t>(d) * 2};
+  const uint32_t abox[2] = {GB_K, 1};  // gather4: 4 rows of one 64-element box each
+  if ((rc = make_tmap_bf16(&ta, x, 2, adims, astr, abox))) return rc;
+  const uint64_t bdims[3] = {static_cast<uint64_t>(d), static_cast<uint64_t>(2 * ffn),
+                             static_cast<uint64_t>(n_slots)};
+  const uint64_t bstr[2] = {static_cast<uint64_t>(d) * 2,
+                            static_cast<uint64_t>(slot_stride_elems) * 2};
+  const uint32_t bbox[3] = {GB_K, 128, 1};
+  if ((rc = make_tmap_bf16(&tb, slab, 3, bdims, bstr, bbox))) return rc;
+  GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : 64,
+               128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0, 0,
+               g_gemm_demote & 1, x, d, slab, d, slot_stride_elems};
+  p.a_perm = d_perm;
+  p.a_k = k;
+  p.a_src_rows = static_cast<int>(src_rows);
   return launch_gemm<true>(ta, tb, p, rows, as_stream(stream));
 }
 

@@ -113,6 +113,20 @@ def expert_gemm_up(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, 
     return act
 
 
+def expert_gemm_up_gather(x, perm, k, offsets, slot_of, slab, n_slots, slot_elems, d, ffn,
+                          group_m=0):
+    """Up GEMM whose A rows are TMA-gathered from x (T, d) by the permutation
+    (sorted row r = token perm[r] // k): no x_perm.  Raises DeviceError in the
+    single-CTA tuning mode."""
+    _dev(x, perm, offsets, slot_of, slab)
+    rows = perm.numel()
+    act = torch.empty((rows, ffn), dtype=torch.bfloat16, device=x.device)
+    _lib.call("daop_expert_gemm_up_gather", x.data_ptr(), x.shape[0], perm.data_ptr(), k, rows, d,
+              ffn, slab.data_ptr(), n_slots, slot_elems, offsets.data_ptr(), slot_of.data_ptr(),
+              offsets.numel() - 1, act.data_ptr(), group_m, _s())
+    return act
+
+
 def expert_gemm_down(act, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, group_m=0,
                      out=None):
     _dev(act, offsets, slot_of, slab, out)

@@ -68,7 +68,7 @@ for cfg in CONFIGS:
             eng.prefill(h, 0)
         elif which == "prefill_sep":  # the same layer with the separate combine pass
             rr = ops.router(h, m.norm[0], m.gate[0], m.gate[1], k)
-            pp = ops.permute(rr["topk_idx"], E, rr["x"])
+            pp = ops.permute(rr["topk_idx"], E, rr["x"])  # dense: materialised x_perm
             aa = ops.expert_gemm_up(pp["x_perm"], pp["offsets"], m.slot_of[0], m.slab,
                                     m.n_slots, m.slot_elems, d, ffn)
             yy = ops.expert_gemm_down(aa, pp["offsets"], m.slot_of[0], m.slab, m.n_slots,

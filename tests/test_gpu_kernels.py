@@ -427,3 +427,23 @@ def test_fused_down_combine_bitexact(P, d, ffn, E, T):
                                                r["topk_w"])
         torch.cuda.synchronize()
         assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("d,ffn,E,T", [(512, 1024, 8, 700), (4096, 14336, 8, 300),
+                                       (1024, 2048, 8, 3001)])
+def test_up_gemm_gather_bitexact(P, d, ffn, E, T):
+    """TMA row gathers (tile::gather4, straight from x by the permutation) ==
+    the dense up GEMM on the gathered x_perm, bit for bit (ragged experts)."""
+    pkg, model_mod, ops = P
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, 2), d, ffn, seed=8, resident_layers=[0])
+    h = m.input_hidden(T, stream=5)
+    r = ops.router(h, m.norm[0], m.gate[0], m.gate[1], 2)
+    pr = ops.permute(r["topk_idx"], E, r["x"])
+    so = m.slot_of[0]
+    ref = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems,
+                             d, ffn)
+    got = ops.expert_gemm_up_gather(r["x"], pr["perm"], 2, pr["offsets"], so, m.slab, m.n_slots,
+                                    m.slot_elems, d, ffn)
+    torch.cuda.synchronize()
+    n = int(pr["offsets"][-1])
+    assert torch.equal(got[:n], ref[:n])
