@@ -206,6 +206,19 @@ int daop_expert_gemm_up(const uint16_t* d_x_perm, int64_t rows, int32_t d, int32
                         const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
                         const int64_t* d_offsets, const int32_t* d_slot_of, int32_t num_experts,
                         uint16_t* d_act, int32_t group_m, daop_stream_t stream);
+/* the same two GEMMs for SMALL token counts (batched decode): weights are the
+ * M side (128-row tiles), the expert's tokens the N side (nt = 32 or 64 per
+ * block), so each expert's weights stream once per block of nt tokens. */
+int daop_expert_gemm_up_skinny(const uint16_t* d_x_perm, int64_t rows, int32_t d, int32_t ffn,
+                               const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
+                               const int64_t* d_offsets, const int32_t* d_slot_of,
+                               int32_t num_experts, uint16_t* d_act, int32_t nt,
+                               daop_stream_t stream);
+int daop_expert_gemm_down_skinny(const uint16_t* d_act, int64_t rows, int32_t d, int32_t ffn,
+                                 const uint16_t* d_slab, int64_t n_slots,
+                                 int64_t slot_stride_elems, const int64_t* d_offsets,
+                                 const int32_t* d_slot_of, int32_t num_experts, float* d_y,
+                                 int32_t nt, daop_stream_t stream);
 /* up GEMM with its A rows gathered by TMA straight from the token matrix
  * d_x (src_rows, d): sorted row r reads token d_perm[r] / k (no x_perm). */
 int daop_expert_gemm_up_gather(const uint16_t* d_x, int64_t src_rows, const int32_t* d_perm,

@@ -1,0 +1,320 @@
+// Grouped SwiGLU expert FFN for SMALL token counts (batched decode, b <= ~128):
+// the "swap-AB" form of grouped_gemm.cu.  With a handful of tokens per expert
+// the X . W^T tiles of the prefill GEMM waste the tensor pipe (M = 256/512
+// rows of which a few are real) and the layer becomes compute-bound on empty
+// rows (~2.7 TB/s of weights at b = 64).  Here the WEIGHTS are the M side:
+//
+//   up  : D1 = W1[rows] . X^T, D3 = W3[rows] . X^T   (M = 128 weight rows,
+//         N = NT token columns, K = d), act[t, row] = bf16(silu(D1) * D3)
+//   down: D = W2[rows] . act^T                        (K = ffn), y[t, row] fp32
+//
+// so a tile costs 128 x NT x K MACs and the kernel streams each expert's
+// weights once per block of NT tokens -- HBM-bound like the b = 1 decode GEMV.
+// One CTA per SM, persistent, warp-specialised like grouped_gemm.cu: warp 0
+// TMA producer (weight box(es) 128 x 64 + token box NT x 64 per stage), warp 1
+// tcgen05.mma.cta_group::1 issuer (M 128, N NT, K 16), warps 2-5 epilogue
+// (thread = weight row, tcgen05.ld 32x32b.x32 over the token columns; stores
+// for one token are 32 consecutive rows per warp).  Tile = (expert, token
+// block, 128-row weight tile), weight tiles fastest.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+namespace daop {
+
+constexpr int SK_K = 64;                      // K per stage (one 128-byte swizzle row)
+constexpr int SK_W_BYTES = 128 * SK_K * 2;    // one 128-row weight box, 16 KB
+constexpr int SK_MAX_E = 64;
+
+int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                   const uint64_t* strides_bytes, const uint32_t* box);
+
+struct SkinnyParams {
+  const int64_t* offsets;   // [E+1] token row offsets (device)
+  const int32_t* slot_of;   // [E]
+  int E;
+  int k_blocks;             // K / 64
+  int row_tiles;            // weight rows / 128 (per matrix)
+  int w_half2;              // SWIGLU: row offset of W3 (= ffn)
+  void* out;                // up: bf16 act (rows, ffn); down: fp32 y (rows, d)
+  int64_t out_ld;
+};
+
+template <int NT>
+struct SkinnySmem {
+  static constexpr int STAGES = 5;
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  int32_t prefix[SK_MAX_E + 1];
+  int32_t blocks[SK_MAX_E];
+  int64_t off[SK_MAX_E + 1];
+};
+
+template <bool SWIGLU, int NT>
+struct SkinnyCfg {
+  static constexpr int STAGES = SkinnySmem<NT>::STAGES;
+  static constexpr int W_BYTES = SWIGLU ? 2 * SK_W_BYTES : SK_W_BYTES;
+  static constexpr int X_BYTES = NT * SK_K * 2;
+  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
+  static constexpr int ACC_COLS = SWIGLU ? 2 * NT : NT;  // per accumulator buffer
+  static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : 2 * ACC_COLS <= 64 ? 64
+                                   : 2 * ACC_COLS <= 128 ? 128 : 256;
+  static constexpr uint32_t IDESC = umma_idesc_bf16_f32(128, NT);
+};
+
+template <int NT>
+__device__ __forceinline__ bool skinny_tile(const SkinnySmem<NT>& s, int E, int rt, int t, int& e,
+                                            int& blk, int& r) {
+  if (t >= s.prefix[E]) return false;
+  e = 0;
+  while (s.prefix[e + 1] <= t) ++e;
+  const int u = t - s.prefix[e];
+  blk = u / rt;
+  r = u - blk * rt;
+  return true;
+}
+
+template <bool SWIGLU, int NT>
+__global__ void __launch_bounds__(192, 1)
+    skinny_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
+                       const __grid_constant__ CUtensorMap tmX, SkinnyParams p) {
+  using C = SkinnyCfg<SWIGLU, NT>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = smem_u32(smem_raw);
+  uint8_t* tiles = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+  SkinnySmem<NT>& s = *reinterpret_cast<SkinnySmem<NT>*>(tiles + C::STAGES * C::STAGE_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int E = p.E, rt = p.row_tiles;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s.tfull[i], 1);
+      mbar_init(&s.tempty[i], 4);
+    }
+    fence_mbar_init();
+    int acc = 0;
+    s.prefix[0] = 0;
+    for (int e = 0; e <= E; ++e) s.off[e] = p.offsets[e];
+    for (int e = 0; e < E; ++e) {
+      const int64_t me = p.slot_of[e] >= 0 ? s.off[e + 1] - s.off[e] : 0;
+      s.blocks[e] = static_cast<int>((me + NT - 1) / NT);
+      acc += s.blocks[e] * rt;
+      s.prefix[e + 1] = acc;
+    }
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(&s.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = s.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      const uint64_t pol_w = l2_evict_first_policy();  // weights: streamed once
+      const uint64_t pol_x = l2_evict_last_policy();   // tokens: re-read by every row tile
+      int stage = 0;
+      uint32_t phase = 0;
+      int e, blk, r;
+      for (int t = blockIdx.x; skinny_tile(s, E, rt, t, e, blk, r); t += gridDim.x) {
+        const int slot = p.slot_of[e];
+        const int xrow = static_cast<int>(s.off[e]) + blk * NT;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&s.empty[stage], phase ^ 1);
+          uint8_t* st = tiles + stage * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&s.full[stage], C::STAGE_BYTES);
+          tma_load_3d(st, &tmW, &s.full[stage], kb * SK_K, r * 128, slot, pol_w);
+          if constexpr (SWIGLU)
+            tma_load_3d(st + SK_W_BYTES, &tmW, &s.full[stage], kb * SK_K, r * 128 + p.w_half2,
+                        slot, pol_w);
+          tma_load_2d(st + C::W_BYTES, &tmX, &s.full[stage], kb * SK_K, xrow, pol_x);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      int e, blk, r;
+      for (int t = blockIdx.x; skinny_tile(s, E, rt, t, e, blk, r); t += gridDim.x) {
+        mbar_wait(&s.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * C::ACC_COLS;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&s.full[stage], phase);
+          tc_fence_after();
+          uint8_t* st = tiles + stage * C::STAGE_BYTES;
+          const uint64_t wdesc = umma_desc_sw128(smem_u32(st));
+          const uint64_t xdesc = umma_desc_sw128(smem_u32(st + C::W_BYTES));
+#pragma unroll
+          for (int k = 0; k < SK_K / 16; ++k) {
+            umma_bf16(d0, wdesc + 2 * k, xdesc + 2 * k, C::IDESC, (kb | k) != 0);
+            if constexpr (SWIGLU) {
+              const uint64_t w3desc = umma_desc_sw128(smem_u32(st + SK_W_BYTES));
+              umma_bf16(d0 + NT, w3desc + 2 * k, xdesc + 2 * k, C::IDESC, (kb | k) != 0);
+            }
+          }
+          umma_commit(&s.empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&s.tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {  // epilogue: thread = weight row of the tile, columns = tokens
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int e, blk, r;
+    for (int t = blockIdx.x; skinny_tile(s, E, rt, t, e, blk, r); t += gridDim.x) {
+      mbar_wait(&s.tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = r * 128 + q * 32 + lane;
+      const int64_t t0 = s.off[e] + static_cast<int64_t>(blk) * NT;
+      const int64_t rem = s.off[e + 1] - t0;
+      const int nvalid = rem < NT ? static_cast<int>(rem) : NT;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::ACC_COLS;
+#pragma unroll 1
+      for (int c = 0; c < NT; c += 32) {
+        uint32_t g[32];
+        tmem_ld32(tb + c, g);
+        if constexpr (SWIGLU) {
+          uint32_t u[32];
+          tmem_ld32(tb + NT + c, u);
+          tmem_ld_wait();
+          uint16_t* out = static_cast<uint16_t*>(p.out);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c + j < nvalid)
+              out[(t0 + c + j) * p.out_ld + row] = f32_to_bf16_bits(
+                  __fdividef(__uint_as_float(g[j]), 1.0f + __expf(-__uint_as_float(g[j]))) *
+                  __uint_as_float(u[j]));  // the prefill GEMM's SwiGLU (silu_fast)
+        } else {
+          tmem_ld_wait();
+          float* out = static_cast<float*>(p.out);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c + j < nvalid) out[(t0 + c + j) * p.out_ld + row] = __uint_as_float(g[j]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+template <bool SWIGLU, int NT>
+static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const SkinnyParams& p,
+                         int64_t rows_total, cudaStream_t st) {
+  using C = SkinnyCfg<SWIGLU, NT>;
+  const size_t smem = 1024 + C::STAGES * C::STAGE_BYTES + sizeof(SkinnySmem<NT>);
+  auto kern = skinny_gemm_kernel<SWIGLU, NT>;
+  DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  const int64_t max_tiles = (rows_total / NT + p.E) * static_cast<int64_t>(p.row_tiles);
+  int grid = sm_count();
+  if (max_tiles < grid) grid = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
+  kern<<<grid, 192, smem, st>>>(tw, tx, p);
+  DAOP_CHECK_LAUNCH(SWIGLU ? "skinny_gemm_up" : "skinny_gemm_down");
+  return DAOP_OK;
+}
+
+template <bool SWIGLU>
+static int skinny_dispatch(const CUtensorMap& tw, const CUtensorMap& tx, const SkinnyParams& p,
+                           int64_t rows, int32_t nt, cudaStream_t st) {
+  if (nt == 32) return launch_skinny<SWIGLU, 32>(tw, tx, p, rows, st);
+  return launch_skinny<SWIGLU, 64>(tw, tx, p, rows, st);
+}
+
+}  // namespace daop
+
+using namespace daop;
+
+static int check_skinny(int64_t rows, int32_t d, int32_t ffn, int32_t E, int32_t nt) {
+  if (E < 1 || E > SK_MAX_E || d % 128 != 0 || ffn % 128 != 0 || d % 64 != 0 ||
+      (nt != 32 && nt != 64) || rows < 0 || rows >= (1ll << 31)) {
+    set_error("skinny expert GEMM: unsupported shape (rows=%lld d=%d ffn=%d E=%d nt=%d)",
+              static_cast<long long>(rows), d, ffn, E, nt);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  return DAOP_OK;
+}
+
+extern "C" int daop_expert_gemm_up_skinny(const uint16_t* x_perm, int64_t rows, int32_t d,
+                                          int32_t ffn, const uint16_t* slab, int64_t n_slots,
+                                          int64_t slot_stride_elems, const int64_t* d_offsets,
+                                          const int32_t* d_slot_of, int32_t E, uint16_t* act,
+                                          int32_t nt, daop_stream_t stream) {
+  int rc = check_skinny(rows, d, ffn, E, nt);
+  if (rc) return rc;
+  if (rows == 0) return DAOP_OK;
+  CUtensorMap tw, tx;
+  const uint64_t wdims[3] = {static_cast<uint64_t>(d), static_cast<uint64_t>(2 * ffn),
+                             static_cast<uint64_t>(n_slots)};
+  const uint64_t wstr[2] = {static_cast<uint64_t>(d) * 2,
+                            static_cast<uint64_t>(slot_stride_elems) * 2};
+  const uint32_t wbox[3] = {SK_K, 128, 1};
+  if ((rc = make_tmap_bf16(&tw, slab, 3, wdims, wstr, wbox))) return rc;
+  const uint64_t xdims[2] = {static_cast<uint64_t>(d), static_cast<uint64_t>(rows)};
+  const uint64_t xstr[1] = {static_cast<uint64_t>(d) * 2};
+  const uint32_t xbox[2] = {SK_K, static_cast<uint32_t>(nt)};
+  if ((rc = make_tmap_bf16(&tx, x_perm, 2, xdims, xstr, xbox))) return rc;
+  SkinnyParams p{d_offsets, d_slot_of, E, d / SK_K, ffn / 128, ffn, act, ffn};
+  return skinny_dispatch<true>(tw, tx, p, rows, nt, as_stream(stream));
+}
+
+extern "C" int daop_expert_gemm_down_skinny(const uint16_t* act, int64_t rows, int32_t d,
+                                            int32_t ffn, const uint16_t* slab, int64_t n_slots,
+                                            int64_t slot_stride_elems, const int64_t* d_offsets,
+                                            const int32_t* d_slot_of, int32_t E, float* y,
+                                            int32_t nt, daop_stream_t stream) {
+  int rc = check_skinny(rows, d, ffn, E, nt);
+  if (rc) return rc;
+  if (rows == 0) return DAOP_OK;
+  CUtensorMap tw, tx;
+  const uint64_t wdims[3] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(d),
+                             static_cast<uint64_t>(n_slots)};
+  const uint64_t wstr[2] = {static_cast<uint64_t>(ffn) * 2,
+                            static_cast<uint64_t>(slot_stride_elems) * 2};
+  const uint32_t wbox[3] = {SK_K, 128, 1};
+  const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
+  if ((rc = make_tmap_bf16(&tw, w2, 3, wdims, wstr, wbox))) return rc;
+  const uint64_t xdims[2] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(rows)};
+  const uint64_t xstr[1] = {static_cast<uint64_t>(ffn) * 2};
+  const uint32_t xbox[2] = {SK_K, static_cast<uint32_t>(nt)};
+  if ((rc = make_tmap_bf16(&tx, act, 2, xdims, xstr, xbox))) return rc;
+  SkinnyParams p{d_offsets, d_slot_of, E, ffn / SK_K, d / 128, 0, y, d};
+  return skinny_dispatch<false>(tw, tx, p, rows, nt, as_stream(stream));
+}

@@ -26,6 +26,11 @@ from . import _lib, ops
 from .model import MoEModel
 
 
+# up to this many permuted rows (T * k) the layer runs the skinny (swap-AB)
+# GEMMs of batched decode: below it the prefill GEMM tiles are mostly empty
+SKINNY_MAX_ROWS = 256
+
+
 class MoEBlockEngine:
     def __init__(self, model: MoEModel, device=None):
         self.model = model
@@ -171,6 +176,16 @@ class MoEBlockEngine:
                        tokens_per_seq=tokens_per_seq, hist_seq_stride=hist_seq_stride)
         pr = ops.permute(r["topk_idx"], self.E, r["x"])
         slot_of = m.slot_of[layer]
+        rows = pr["x_perm"].shape[0]
+        if rows <= SKINNY_MAX_ROWS and not fused_combine:
+            # batched decode: weights are the M side, tokens the N side
+            act = ops.expert_gemm_up_skinny(pr["x_perm"], pr["offsets"], slot_of, m.slab,
+                                            m.n_slots, m.slot_elems, self.d, self.ffn)
+            y = ops.expert_gemm_down_skinny(act, pr["offsets"], slot_of, m.slab, m.n_slots,
+                                            m.slot_elems, self.d, self.ffn)
+            r["out"] = ops.combine(h, y, pr["inv"], r["topk_w"])
+            r["offsets"] = pr["offsets"]
+            return r
         act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_of, m.slab, m.n_slots,
                                  m.slot_elems, self.d, self.ffn, group_up)
         if fused_combine:  # combine in the down GEMM's epilogue (measured slower: off)

@@ -447,3 +447,30 @@ def test_up_gemm_gather_bitexact(P, d, ffn, E, T):
     torch.cuda.synchronize()
     n = int(pr["offsets"][-1])
     assert torch.equal(got[:n], ref[:n])
+
+
+@pytest.mark.parametrize("d,ffn,E,T", [(512, 1024, 8, 1), (512, 1024, 8, 13), (4096, 14336, 8, 64),
+                                       (1024, 2048, 16, 100)])
+def test_skinny_gemm_matches_dense(P, d, ffn, E, T):
+    """Batched-decode GEMMs (weights as the M side, tokens as N) == the
+    prefill GEMMs on the same permuted rows, bit for bit (the tensor cores
+    accumulate each element in the same K order either way); ragged and
+    empty experts, several token blocks."""
+    pkg, model_mod, ops = P
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, 2), d, ffn, seed=9, resident_layers=[0])
+    h = m.input_hidden(T, stream=3)
+    r = ops.router(h, m.norm[0], m.gate[0], m.gate[1], 2)
+    pr = ops.permute(r["topk_idx"], E, r["x"])
+    so = m.slot_of[0]
+    act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems,
+                             d, ffn)
+    y = ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn)
+    for nt in (32, 64):
+        act2 = ops.expert_gemm_up_skinny(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots,
+                                         m.slot_elems, d, ffn, nt)
+        y2 = ops.expert_gemm_down_skinny(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems,
+                                         d, ffn, nt)
+        torch.cuda.synchronize()
+        n = int(pr["offsets"][-1])
+        assert torch.equal(act2[:n], act[:n]), nt
+        assert torch.equal(y2[:n], y[:n]), nt
