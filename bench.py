@@ -276,6 +276,45 @@ def run_b200(args, world, rank, local_rank):
         }
         del hp
 
+    # -------- batched decode: 64 sequences' next tokens through the same layer
+    # (router -> permutation -> skinny tcgen05 GEMMs -> combine)
+    decode_b64 = None
+    try:
+        B = 64
+        hb = model.input_hidden(B, stream=500 + rank)
+        for _ in range(3):
+            rb = eng.prefill(hb, 0)
+        torch.cuda.synchronize()
+        active = int((rb["offsets"][1:] - rb["offsets"][:-1] > 0).sum())
+        nb_ = 50
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(nb_):
+            eng.prefill(hb, 0)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1) / nb_
+        tb_ = torch.tensor([bms], device=dev)
+        if world > 1:
+            dist.all_reduce(tb_, op=dist.ReduceOp.MAX)
+        bms = float(tb_.item())
+        wbytes = active * 3 * D * FFN * 2 + 2 * E * D * 2
+        decode_b64 = {
+            "workload": "decode step of 64 sequences (b=64) through one Mixtral-8x7B MoE layer: "
+                        "router, permutation, skinny tcgen05 grouped GEMMs (weights as the M "
+                        "side), combine",
+            "value": world * B / (bms / 1e3), "unit": "tokens/s", "ms_per_step": bms,
+            "active_experts": active,
+            "roofline": {"bound": "hbm", "achieved": wbytes / (bms / 1e3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s",
+                         "frac": wbytes / (bms / 1e3) / 1e9 / hbm_peak,
+                         "bytes_per_step": wbytes},
+            "gpu_launches_per_step": MoEBlockEngine.prefill_kernels(),
+        }
+        del hb, rb
+    except Exception as exc:
+        decode_b64 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # -------- end-to-end through the host API (value measured with host buffers)
     hh = [torch.empty(D, dtype=torch.float32, pin_memory=True) for _ in range(8)]
     for i, h in enumerate(hh):
@@ -433,6 +472,7 @@ def run_b200(args, world, rank, local_rank):
         "gpu_launches": args.steps,
         "clocks": clocks,
         "prefill": prefill,
+        "decode_b64": decode_b64,
         "decode32": decode32,
         "decoder32": decoder32,
         "ep": ep,

@@ -44,7 +44,7 @@ struct SkinnyParams {
 
 template <int NT>
 struct SkinnySmem {
-  static constexpr int STAGES = 5;
+  static constexpr int STAGES = 8;  // upper bound; the kernel uses SkinnyCfg::STAGES
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
   uint64_t tfull[2];
@@ -57,10 +57,12 @@ struct SkinnySmem {
 
 template <bool SWIGLU, int NT>
 struct SkinnyCfg {
-  static constexpr int STAGES = SkinnySmem<NT>::STAGES;
   static constexpr int W_BYTES = SWIGLU ? 2 * SK_W_BYTES : SK_W_BYTES;
   static constexpr int X_BYTES = NT * SK_K * 2;
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
+  // as many stages as fit in ~200 KB (up, NT 64: 5 x 40 KB; down: 8 x 24 KB)
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < SkinnySmem<NT>::STAGES
+                                    ? (200 * 1024) / STAGE_BYTES : SkinnySmem<NT>::STAGES;
   static constexpr int ACC_COLS = SWIGLU ? 2 * NT : NT;  // per accumulator buffer
   static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : 2 * ACC_COLS <= 64 ? 64
                                    : 2 * ACC_COLS <= 128 ? 128 : 256;
