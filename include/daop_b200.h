@@ -277,6 +277,13 @@ int daop_ep_expert_gemm_down(const uint16_t* d_act, int64_t rows_cap, int32_t d,
                              const int32_t* d_slot_of, int32_t num_experts,
                              const uint64_t* d_peers, void* d_ws, int32_t rank, int32_t world,
                              uint32_t epoch, int32_t group_m, daop_stream_t stream);
+/* the skinny (batched-decode) form of the fused-return down GEMM */
+int daop_ep_expert_gemm_down_skinny(const uint16_t* d_act, int64_t rows_cap, int32_t d,
+                                    int32_t ffn, const uint16_t* d_slab, int64_t n_slots,
+                                    int64_t slot_stride_elems, const int32_t* d_slot_of,
+                                    int32_t num_experts, const uint64_t* d_peers, void* d_ws,
+                                    int32_t rank, int32_t world, uint32_t epoch, int32_t nt,
+                                    daop_stream_t stream);
 int daop_ep_wait_back(void* d_ws, int32_t world, uint32_t epoch, daop_stream_t stream);
 /* decode b = 1 over G GPUs: the residual is replicated, every rank runs
  * daop_decode_layer (mode 0) with its own experts as the resident set, then

@@ -66,6 +66,8 @@ PROTOS = {
     "daop_ep_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, I32, P, P, I32, I32,
                                  C.c_uint32, I32, P],
     "daop_ep_wait_back": [P, I32, C.c_uint32, P],
+    "daop_ep_expert_gemm_down_skinny": [P, I64, I32, I32, P, I64, I64, P, I32, P, P, I32, I32,
+                                        C.c_uint32, I32, P],
     "daop_ep_status": [P, P],
     "daop_ep_decode_ws_bytes": [I32, I32, P],
     "daop_ep_decode_share": [P, I32, I32, I32, I32, P, P, C.c_uint32, P],

@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "ep.cuh"
 #include "tcgen05.cuh"
 
 namespace daop {
@@ -40,6 +41,14 @@ struct SkinnyParams {
   int w_half2;              // SWIGLU: row offset of W3 (= ffn)
   void* out;                // up: bf16 act (rows, ffn); down: fp32 y (rows, d)
   int64_t out_ld;
+  // expert-parallel return (down only, ep_p2p.cu): row t of the output goes
+  // to the address row_dst[t] (the source GPU's y_back row) and the last CTA
+  // flags y[sig_rank] = sig_epoch on every peer
+  const uint64_t* row_dst;
+  unsigned* sig_done;
+  const uint64_t* sig_peers;
+  int sig_G, sig_rank;
+  unsigned sig_epoch;
 };
 
 template <int NT>
@@ -217,7 +226,11 @@ __global__ void __launch_bounds__(192, 1)
           float* out = static_cast<float*>(p.out);
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (c + j < nvalid) out[(t0 + c + j) * p.out_ld + row] = __uint_as_float(g[j]);
+            if (c + j < nvalid) {
+              float* dst = p.row_dst ? reinterpret_cast<float*>(p.row_dst[t0 + c + j]) + row
+                                     : out + (t0 + c + j) * p.out_ld + row;
+              *dst = __uint_as_float(g[j]);
+            }
         }
       }
       tc_fence_before();
@@ -230,10 +243,18 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
   tc_fence_before();
+  if (p.sig_done) __threadfence_system();  // this thread's (remote) output rows
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+  if (p.sig_done && threadIdx.x == 0 && atomicAdd(p.sig_done, 1u) == gridDim.x - 1) {
+    *p.sig_done = 0;
+    __threadfence_system();
+    for (int q = 0; q < p.sig_G; ++q)
+      st_release_sys(reinterpret_cast<unsigned*>(p.sig_peers[q] + EP_FLAGS_Y) + p.sig_rank,
+                     p.sig_epoch);
   }
 }
 
@@ -319,4 +340,39 @@ extern "C" int daop_expert_gemm_down_skinny(const uint16_t* act, int64_t rows, i
   if ((rc = make_tmap_bf16(&tx, act, 2, xdims, xstr, xbox))) return rc;
   SkinnyParams p{d_offsets, d_slot_of, E, ffn / SK_K, d / 128, 0, y, d};
   return skinny_dispatch<false>(tw, tx, p, rows, nt, as_stream(stream));
+}
+
+// Expert-parallel down GEMM for small receive buffers (batched decode over
+// several GPUs): the skinny kernel with the return table and the peer flags
+// of daop_ep_expert_gemm_down.
+extern "C" int daop_ep_expert_gemm_down_skinny(const uint16_t* act, int64_t rows_cap, int32_t d,
+                                               int32_t ffn, const uint16_t* slab, int64_t n_slots,
+                                               int64_t slot_stride_elems,
+                                               const int32_t* d_slot_of, int32_t E,
+                                               const uint64_t* d_peers, void* d_ws, int32_t rank,
+                                               int32_t G, uint32_t epoch, int32_t nt,
+                                               daop_stream_t stream) {
+  int rc = check_skinny(rows_cap, d, ffn, E, nt);
+  if (rc) return rc;
+  if (G < 1 || G > EP_MAX_G || rank < 0 || rank >= G || rows_cap < 1) {
+    set_error("ep skinny gemm: bad rank/world (%d/%d) or capacity", rank, G);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  uint8_t* ws = static_cast<uint8_t*>(d_ws);
+  CUtensorMap tw, tx;
+  const uint64_t wdims[3] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(d),
+                             static_cast<uint64_t>(n_slots)};
+  const uint64_t wstr[2] = {static_cast<uint64_t>(ffn) * 2,
+                            static_cast<uint64_t>(slot_stride_elems) * 2};
+  const uint32_t wbox[3] = {SK_K, 128, 1};
+  const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
+  if ((rc = make_tmap_bf16(&tw, w2, 3, wdims, wstr, wbox))) return rc;
+  const uint64_t xdims[2] = {static_cast<uint64_t>(ffn), static_cast<uint64_t>(rows_cap)};
+  const uint64_t xstr[1] = {static_cast<uint64_t>(ffn) * 2};
+  const uint32_t xbox[2] = {SK_K, static_cast<uint32_t>(nt)};
+  if ((rc = make_tmap_bf16(&tx, act, 2, xdims, xstr, xbox))) return rc;
+  SkinnyParams p{reinterpret_cast<const int64_t*>(ws + EP_LOCAL_OFF), d_slot_of, E, ffn / SK_K,
+                 d / 128, 0, nullptr, d, reinterpret_cast<const uint64_t*>(ws + EP_ROWMAP),
+                 reinterpret_cast<unsigned*>(ws + EP_DONE_GEMM), d_peers, G, rank, epoch};
+  return skinny_dispatch<false>(tw, tx, p, rows_cap, nt, as_stream(stream));
 }

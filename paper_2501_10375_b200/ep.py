@@ -37,6 +37,8 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
+SKINNY_MAX_ROWS = 256  # receive capacity up to which the skinny (batched-decode) GEMMs run
+
 
 def owner_of(expert: torch.Tensor, num_experts: int, world: int) -> torch.Tensor:
     return (expert * world) // num_experts
@@ -449,6 +451,17 @@ class PeerEP:
         s = ops._s()
         _lib.call("daop_ep_recv", self.peers.data_ptr(), self.rank, self.world, self.E, self.d,
                   self.yback_off, self.epoch, s)
+        if self.cap_recv <= SKINNY_MAX_ROWS:  # batched decode: weights as the M side
+            nt = ops.skinny_nt(self.cap_recv)
+            _lib.call("daop_expert_gemm_up_skinny", self.recv_x.data_ptr(), self.cap_recv, self.d,
+                      self.ffn, m.slab.data_ptr(), m.n_slots, m.slot_elems,
+                      self.ws.data_ptr() + self.local_off, m.slot_of[l].data_ptr(), self.E,
+                      self.act.data_ptr(), nt, s)
+            _lib.call("daop_ep_expert_gemm_down_skinny", self.act.data_ptr(), self.cap_recv,
+                      self.d, self.ffn, m.slab.data_ptr(), m.n_slots, m.slot_elems,
+                      m.slot_of[l].data_ptr(), self.E, self.peers.data_ptr(), self.ws.data_ptr(),
+                      self.rank, self.world, self.epoch, nt, s)
+            return
         _lib.call("daop_expert_gemm_up", self.recv_x.data_ptr(), self.cap_recv, self.d, self.ffn,
                   m.slab.data_ptr(), m.n_slots, m.slot_elems, self.ws.data_ptr() + self.local_off,
                   m.slot_of[l].data_ptr(), self.E, self.act.data_ptr(), 0, s)

@@ -230,3 +230,36 @@ def test_peer_ep_decode_equals_single_gpu(G, d, ffn):
             for r in range(G):
                 ranks[r].check()
                 assert torch.equal(hs[r], ref_h), (G, step, layer, r)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_peer_ep_small_batch_skinny(G):
+    """Batched decode over G emulated ranks (<= 16 tokens per rank: the
+    receive capacity selects the skinny GEMMs and the skinny fused-return down
+    GEMM): every rank's output equals the single-GPU layer bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.ep import PeerEP, ep_model
+    E, d, ffn = 8, 512, 1024
+    m, eng = _single_gpu_reference(P, E, d, ffn, 12)
+    models = [ep_model(P.ModelShape(2, E, 2), d, ffn, r, G, seed=12) for r in range(G)]
+    ranks = PeerEP.emulated(models, 0, t_cap=16)
+    assert ranks[0].cap_recv <= 256
+    tok = [16, 1, 9, 16, 3, 12, 16, 7][:G]
+    for step in range(3):
+        hs = [m.input_hidden(tok[r], stream=80 + r, step=step) for r in range(G)]
+        for r in range(G):
+            ranks[r].route(hs[r])
+        for r in range(G):
+            ranks[r].publish()
+        for r in range(G):
+            ranks[r].dispatch()
+        for r in range(G):
+            ranks[r].experts()
+        outs = [ranks[r].finish() for r in range(G)]
+        torch.cuda.synchronize()
+        for r in range(G):
+            ranks[r].check()
+            ref = eng.prefill(hs[r], 0)
+            assert torch.equal(outs[r][0], ref["out"]), (G, step, r)
