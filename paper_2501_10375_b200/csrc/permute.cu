@@ -298,6 +298,46 @@ __global__ void __launch_bounds__(32, 1)
   bulk_wait_all();
 }
 
+// small batches (decode): one CTA per token, every thread a few float4 of
+// the row -- one memory round trip instead of a warp walking 16 KB
+template <int K>
+__global__ void combine_small_kernel(const float* __restrict__ h, const float* __restrict__ y,
+                                     const int32_t* __restrict__ inv, const float* __restrict__ w,
+                                     int d4, float* __restrict__ out) {
+  const int64_t t = blockIdx.x;
+  const float4* hr = reinterpret_cast<const float4*>(h) + t * d4;
+  float4* o = reinterpret_cast<float4*>(out) + t * d4;
+  const float4* yr[K];
+  float wj[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    yr[j] = reinterpret_cast<const float4*>(y) + static_cast<int64_t>(inv[t * K + j]) * d4;
+    wj[j] = w[t * K + j];
+  }
+  for (int c = threadIdx.x; c < d4; c += blockDim.x) {
+    float4 acc = hr[c];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const float4 v = yr[j][c];
+      acc.x = fmaf(wj[j], v.x, acc.x);
+      acc.y = fmaf(wj[j], v.y, acc.y);
+      acc.z = fmaf(wj[j], v.z, acc.z);
+      acc.w = fmaf(wj[j], v.w, acc.w);
+    }
+    o[c] = acc;
+  }
+}
+
+// small batches: one CTA per token row of x, stored at its k sorted positions
+__global__ void gather_small_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ inv,
+                                    int k, int n16, uint4* __restrict__ x_perm) {
+  const int64_t t = blockIdx.x;
+  for (int c = threadIdx.x; c < n16; c += blockDim.x) {
+    const uint4 v = x[t * n16 + c];
+    for (int j = 0; j < k; ++j) x_perm[static_cast<int64_t>(inv[t * k + j]) * n16 + c] = v;
+  }
+}
+
 // decode-side combine when some picks ran on the host tier:
 // out[i] = h[i] + sum_{q<k} w[q] * y[q, i]   (fixed q order, like the fused path)
 __global__ void combine_dense_kernel(const float* __restrict__ h, const float* __restrict__ y,
@@ -354,7 +394,9 @@ int daop_permute(const int32_t* ids, int64_t T, int32_t k, int32_t E, const uint
     const uint4* xs = reinterpret_cast<const uint4*>(x);
     uint4* xp = reinterpret_cast<uint4*>(x_perm);
     const size_t row = static_cast<size_t>(d) * 2;
-    if (T >= 4 * sm_count() && row % 16 == 0 && row <= 16 * 1024) {
+    if (T < 2 * sm_count()) {  // decode-sized batches
+      gather_small_kernel<<<static_cast<int>(T), 256, 0, st>>>(xs, inv, k, d / 8, xp);
+    } else if (T >= 4 * sm_count() && row % 16 == 0 && row <= 16 * 1024) {
       const int stages = static_cast<int>(std::min<size_t>(16, (48 * 1024) / row));
       const size_t smem = row * stages + 16 * 8 + 64;
       DAOP_CUDA(cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -383,6 +425,12 @@ int daop_combine(const float* h, const float* y_sorted, const int32_t* inv, cons
     kern<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(h, y_sorted, inv, w, T, k, d / 4,
                                                                   out);
   };
+  if (k == 2 && T < 2 * sm_count()) {  // decode-sized batches
+    combine_small_kernel<2><<<static_cast<int>(T), 256, 0, as_stream(stream)>>>(
+        h, y_sorted, inv, w, d / 4, out);
+    DAOP_CHECK_LAUNCH("combine_small");
+    return DAOP_OK;
+  }
   if (k == 2 && d % 4 == 0 && T >= sm_count()) {
     const size_t stage = static_cast<size_t>(d) * 4 * 3;
     const int stages = static_cast<int>(std::min<size_t>(4, (200 * 1024) / stage));

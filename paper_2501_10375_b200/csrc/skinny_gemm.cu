@@ -69,9 +69,13 @@ struct SkinnyCfg {
   static constexpr int W_BYTES = SWIGLU ? 2 * SK_W_BYTES : SK_W_BYTES;
   static constexpr int X_BYTES = NT * SK_K * 2;
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  // as many stages as fit in ~200 KB (up, NT 64: 5 x 40 KB; down: 8 x 24 KB)
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < SkinnySmem<NT>::STAGES
-                                    ? (200 * 1024) / STAGE_BYTES : SkinnySmem<NT>::STAGES;
+  // up (NT 64): 5 x 40 KB stages, one CTA per SM; down: 4 x 24 KB stages so
+  // TWO CTAs share an SM -- its d / 128 row tiles per expert (256 at b = 64)
+  // then fill one wave of 2 x 148 CTAs instead of leaving half a second wave
+  static constexpr int CTAS_PER_SM = SWIGLU ? 1 : 2;
+  static constexpr int BUDGET = SWIGLU ? 200 * 1024 : 96 * 1024;
+  static constexpr int STAGES = BUDGET / STAGE_BYTES < SkinnySmem<NT>::STAGES
+                                    ? BUDGET / STAGE_BYTES : SkinnySmem<NT>::STAGES;
   static constexpr int ACC_COLS = SWIGLU ? 2 * NT : NT;  // per accumulator buffer
   static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : 2 * ACC_COLS <= 64 ? 64
                                    : 2 * ACC_COLS <= 128 ? 128 : 256;
@@ -267,7 +271,7 @@ static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const Ski
   DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int64_t max_tiles = (rows_total / NT + p.E) * static_cast<int64_t>(p.row_tiles);
-  int grid = sm_count();
+  int grid = sm_count() * C::CTAS_PER_SM;
   if (max_tiles < grid) grid = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
   kern<<<grid, 192, smem, st>>>(tw, tx, p);
   DAOP_CHECK_LAUNCH(SWIGLU ? "skinny_gemm_up" : "skinny_gemm_down");
