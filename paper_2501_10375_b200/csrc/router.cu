@@ -410,6 +410,120 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
   }
 }
 
+// ---------------------------------------------------------------------------
+// Decode-sized batches (T <= 128): one CTA per token, 16 warps splitting d.
+// The tensor-core router above amortises its 128 KB gate staging over many
+// 8-token tiles; with a handful of tokens it would run a few CTAs through
+// long dependent chains.  Here every token gets an SM: RMSNorm by a block
+// reduction, the 2E gate dot products as per-warp partials reduced in fixed
+// warp order, then the same softmax / top-k / renormalisation / counter as
+// router_kernel (lane-parallel, ties -> lower id).
+constexpr int kSmallWarps = 16;
+
+__global__ void __launch_bounds__(kSmallWarps * 32, 1) router_small_kernel(RouterArgs a) {
+  const int d = a.d, E = a.E, k = a.k;
+  const int rows = a.wg_next ? 2 * E : E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  const int64_t t = blockIdx.x;
+  __shared__ float red[kSmallWarps];
+  __shared__ float part[kSmallWarps][kMaxGateRows];
+  const float* hrow = a.h + t * d;
+  const int n8 = d / 8;  // 8-element chunks, thread-strided
+  float ss = 0.f;
+  for (int c = tid; c < n8; c += blockDim.x) {
+    const float4 u = reinterpret_cast<const float4*>(hrow)[2 * c];
+    const float4 v = reinterpret_cast<const float4*>(hrow)[2 * c + 1];
+    ss = fmaf(u.x, u.x, ss); ss = fmaf(u.y, u.y, ss); ss = fmaf(u.z, u.z, ss); ss = fmaf(u.w, u.w, ss);
+    ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < kSmallWarps; ++w) tot += red[w];
+  const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + a.eps);
+  float acc[kMaxGateRows];
+#pragma unroll
+  for (int q = 0; q < kMaxGateRows; ++q) acc[q] = 0.f;
+  for (int c = tid; c < n8; c += blockDim.x) {
+    const float4 u = reinterpret_cast<const float4*>(hrow)[2 * c];
+    const float4 v = reinterpret_cast<const float4*>(hrow)[2 * c + 1];
+    const uint4 gm = reinterpret_cast<const uint4*>(a.gamma)[c];
+    const float hv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+    const uint32_t gw[4] = {gm.x, gm.y, gm.z, gm.w};
+    uint32_t xw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x0 = __fmul_rn(__fmul_rn(hv[2 * q], r), bf16lo(gw[q]));
+      const float x1 = __fmul_rn(__fmul_rn(hv[2 * q + 1], r), bf16hi(gw[q]));
+      xw[q] = static_cast<uint32_t>(f32_to_bf16_bits(x0)) |
+              (static_cast<uint32_t>(f32_to_bf16_bits(x1)) << 16);
+    }
+    const uint4 x8 = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+    if (a.x_out) reinterpret_cast<uint4*>(a.x_out + t * d)[c] = x8;
+#pragma unroll
+    for (int q = 0; q < kMaxGateRows; ++q)
+      if (q < rows) {
+        const uint16_t* grow = q < E ? a.wg + static_cast<size_t>(q) * d
+                                     : a.wg_next + static_cast<size_t>(q - E) * d;
+        acc[q] = dot8(x8, reinterpret_cast<const uint4*>(grow)[c], acc[q]);
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < kMaxGateRows; ++q)
+    if (q < rows) {
+      const float z = warp_sum(acc[q]);
+      if (lane == 0) part[warp][q] = z;
+    }
+  __syncthreads();
+  if (warp != 0) return;
+  float zt = 0.f, zp = 0.f;
+  if (lane < E)
+    for (int w = 0; w < kSmallWarps; ++w) {
+      zt += part[w][lane];
+      if (a.wg_next) zp += part[w][E + lane];
+    }
+  const float p = lane_softmax(zt, lane, E);
+  if (lane < E) a.p_true[t * E + lane] = p;
+  if (a.wg_next) {
+    const float ph = lane_softmax(zp, lane, E);
+    if (lane < E) a.p_pred[t * E + lane] = ph;
+  }
+  bool taken = lane >= E;
+  int my_sel = -1;
+  float my_p = 0.f, den = 0.f;
+  for (int j = 0; j < k; ++j) {
+    float bv = taken ? -INFINITY : p;
+    int bi = taken ? 0x7fffffff : lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    bi = __shfl_sync(0xffffffffu, bi, 0);
+    bv = __shfl_sync(0xffffffffu, bv, 0);
+    if (bi >= E) {  // NaN scores never compare: first untaken id (topk_scan rule)
+      bi = __ffs(__ballot_sync(0xffffffffu, !taken)) - 1;
+      bv = __shfl_sync(0xffffffffu, p, bi);
+    }
+    den += bv;
+    if (lane == j) {
+      my_sel = bi;
+      my_p = bv;
+    }
+    if (lane == bi) taken = true;
+  }
+  if (lane < k) {
+    a.topk_idx[t * k + lane] = my_sel;
+    a.topk_w[t * k + lane] = my_p / den;
+    if (a.hist) atomicAdd(a.hist + (t / a.tokens_per_seq) * a.hist_seq_stride + my_sel, 1);
+  }
+}
+
 }  // namespace daop
 
 using namespace daop;
@@ -432,6 +546,11 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
   RouterArgs a{h, gamma, wg, wg_next, T, d, E, k, eps, x_out, p_true, p_pred,
                topk_idx, topk_w, hist, tokens_per_seq, hist_seq_stride};
   const int rows = wg_next ? 2 * E : E;
+  if (T <= 128 && d % 8 == 0) {  // decode-sized batch: a CTA per token
+    router_small_kernel<<<static_cast<int>(T), kSmallWarps * 32, 0, as_stream(st)>>>(a);
+    DAOP_CHECK_LAUNCH("router_small");
+    return DAOP_OK;
+  }
   const size_t smem_mma = static_cast<size_t>(16) * (d + 8) * 2 + static_cast<size_t>(d) * 2 +
                           2 * kMmaWarps * kTokTile * 4 + 2 * kMmaWarps * 16 * kTokTile * 4;
   if (rows <= 16 && d % (16 * kMmaWarps) == 0 && smem_mma <= 232448) {
