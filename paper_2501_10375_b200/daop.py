@@ -342,12 +342,14 @@ class DaopEngine:
 
     # ------------------------------------------------------------ decode
     def _host_views(self):
-        """Pinned mirrors of the two decode buffers' decision prefix, with
-        numpy views (one D2H copy per layer)."""
+        """Pinned mirrors of the decode buffers' decision prefix, one per
+        layer, with numpy views (one D2H copy per layer; a layer whose
+        decisions are read only at the end of the token keeps its own)."""
         if getattr(self, "_mh", None) is None:
             E, k, d = self.shape.num_experts, self.shape.top_k, self.model.d
             self._mh = []
-            for b in self.bufs:
+            for l in range(self.shape.num_layers):
+                b = self.bufs[l % 2]
                 t = torch.empty(b.decisions_bytes, dtype=torch.uint8, pin_memory=True)
                 a = t.numpy()
                 o = b.offsets
@@ -394,7 +396,12 @@ class DaopEngine:
         start layer on (DAOP), the plan is known before the launch (it only
         depends on layer l-1's prediction), so the host tier computes the
         slow picks on the stale x_{l-1} while the GPU streams the resident
-        picks -- the pre-calculation overlap of PAPER.md:317-339."""
+        picks -- the pre-calculation overlap of PAPER.md:317-339.
+
+        A layer with every expert in HBM needs nothing from the host: when
+        the next layer does not need its prediction on the host either, its
+        synchronisation is skipped and its decisions are read after the
+        token (at ECR 1.0 the whole token runs without a host round trip)."""
         if self.config.engine in ("ondemand", "prefetch"):
             return self._decode_lru(h)
         m = self.model
@@ -412,12 +419,25 @@ class DaopEngine:
         nd = np.zeros(L, dtype=np.int32)
         true_sc = np.zeros((L, E))
         pred_sc = np.zeros((L, E))
+
+        def read(l, v):  # one layer's decisions out of its pinned mirror
+            dg = v["deg"]
+            sel[l], fast[l] = v["sel"], v["is_fast"]
+            nd[l] = dg[2 * k]
+            drop[l, : nd[l]] = dg[: nd[l]]
+            sub[l, : nd[l]] = dg[k: k + nd[l]]
+            true_sc[l] = v["p"]
+            if l + 1 < L:
+                pred_sc[l] = v["p_pred"]
+
         prev_b, prev_v = None, None
         pos = self.pos
+        full = m.resident_mask().all(axis=1)
+        deferred = []
         for l in range(L):
             h = self._non_moe(h, l, pos)
             b = self.bufs[l % 2]
-            ht, v = mh[l % 2]
+            ht, v = mh[l]
             mode = 1 if (daop and l >= start) else 0
             nxt = m.gate[l + 1] if l + 1 < L else None
             ops.decode_layer(h, m.norm[l], m.gate[l], nxt, m.fast[l], m.slot_of[l], m.slab,
@@ -426,8 +446,14 @@ class DaopEngine:
                              graceful=cfg.graceful_degradation,
                              weights_from_pred=self.weights_from_pred and mode == 1)
             ht.copy_(b.meta[: b.decisions_bytes], non_blocking=True)
+            if full[l] and (l + 1 == L or full[l + 1]):
+                deferred.append(l)  # all picks resident: no host work, read later
+                h = b.h_out
+                prev_b, prev_v = b, v
+                continue
             ys = {}
-            if mode == 1:
+            plan_on_host = mode == 1 and not full[l]
+            if plan_on_host:
                 # pre-calculation on the host while the GPU streams the layer
                 hs, hf = self._host_plan(l, prev_v["p_pred"].astype(np.float64))
                 xs = prev_v["x"][None, :]
@@ -436,16 +462,9 @@ class DaopEngine:
                         ys[q] = host_expert_ffn(self.pool, l, int(hs[q]), xs, self.host_threads)
             stream.synchronize()
             s_l, f_l = v["sel"].copy(), v["is_fast"].copy()
-            if mode == 1 and (s_l.tolist() != hs.tolist() or f_l.tolist() != hf.tolist()):
+            if plan_on_host and (s_l.tolist() != hs.tolist() or f_l.tolist() != hf.tolist()):
                 raise ShapeMismatchError(f"layer {l}: host plan differs from the device plan")
-            dg = v["deg"]
-            sel[l], fast[l] = s_l, f_l
-            nd[l] = dg[2 * k]
-            drop[l, : nd[l]] = dg[: nd[l]]
-            sub[l, : nd[l]] = dg[k: k + nd[l]]
-            true_sc[l] = v["p"]
-            if nxt is not None:
-                pred_sc[l] = v["p_pred"]
+            read(l, v)
             if not f_l.all():
                 if mode == 0:  # Fiddler rule: current x_l, after the router
                     xs = v["x"][None, :]
@@ -464,6 +483,8 @@ class DaopEngine:
                 h = b.h_out
             prev_b, prev_v = b, v
         torch.cuda.synchronize()
+        for l in deferred:
+            read(l, mh[l][1])
         h = h.clone()
         self.pos += 1
         plans = plans_from_arrays(sel, fast, drop, sub, nd, pred_sc, cfg)
