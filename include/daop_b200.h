@@ -188,6 +188,11 @@ int daop_host_expert_ffn(const uint16_t* h_x, int64_t n, const uint16_t* h_w1,
                          const uint16_t* h_w3, const uint16_t* h_w2, int32_t d, int32_t ffn,
                          float* h_y, uint16_t* h_act_scratch, int32_t threads);
 int daop_host_caps(int32_t* avx512_bf16, int32_t* hw_threads);
+
+/* Host-tier scheduling: rows per work chunk of the up / down GEMV phases
+ * (0 = one contiguous share per worker).  Tuning knob; no reference
+ * counterpart (the reference only prices t_expert_slow, simulator.py:49). */
+int daop_host_set_grain(int64_t up_rows, int64_t down_rows);
 /* profiling aid: stream-read `bytes` of host memory on the slow tier's thread
  * pool (the bandwidth ceiling of its GEMV); *checksum defeats elision */
 int daop_host_stream_read(const void* h_buf, int64_t bytes, int32_t threads, double* checksum);

@@ -83,6 +83,7 @@ PROTOS = {
     "daop_combine_dense": [P, P, P, I32, I32, P, P],
     "daop_host_expert_ffn": [P, I64, P, P, P, I32, I32, P, P, I32],
     "daop_host_caps": [P, P],
+    "daop_host_set_grain": [I64, I64],
     "daop_host_stream_read": [P, I64, I32, P],
     "daop_lru_plan_layer": [I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P, P, P, P],
     "daop_trace_format_phase": [P, P, P, I64, I32, I32, I32, P, I64, P],

@@ -295,13 +295,19 @@ class Pool {
     for (auto& t : th_) t.join();
   }
   int size() const { return n_; }
-  // run fn(worker, begin, end) over [0, total) split in n_ contiguous parts
-  void run(int64_t total, const std::function<void(int, int64_t, int64_t)>& fn) {
+  // run fn(worker, begin, end) over [0, total): split in n_ contiguous parts
+  // (grain 0), or in `grain`-sized chunks claimed from a shared counter, so a
+  // worker the OS delays (the caller's thread, driver threads share the
+  // cores) costs one chunk rather than a whole 1/n_ share
+  void run(int64_t total, const std::function<void(int, int64_t, int64_t)>& fn,
+           int64_t grain = 0) {
     std::unique_lock<std::mutex> lk(run_m_);
     {
       std::lock_guard<std::mutex> g(m_);
       fn_ = &fn;
       total_ = total;
+      grain_ = grain;
+      next_.store(0, std::memory_order_relaxed);
       pending_ = n_;
       ++gen_;
     }
@@ -315,7 +321,7 @@ class Pool {
     uint64_t seen = 0;
     while (true) {
       const std::function<void(int, int64_t, int64_t)>* fn;
-      int64_t total;
+      int64_t total, grain;
       {
         std::unique_lock<std::mutex> g(m_);
         cv_.wait(g, [&] { return gen_ != seen; });
@@ -323,9 +329,15 @@ class Pool {
         if (stop_) return;
         fn = fn_;
         total = total_;
+        grain = grain_;
       }
-      const int64_t a = total * id / n_, b = total * (id + 1) / n_;
-      if (a < b) (*fn)(id, a, b);
+      if (grain > 0) {
+        for (int64_t a; (a = next_.fetch_add(grain, std::memory_order_relaxed)) < total;)
+          (*fn)(id, a, std::min(a + grain, total));
+      } else {
+        const int64_t a = total * id / n_, b = total * (id + 1) / n_;
+        if (a < b) (*fn)(id, a, b);
+      }
       {
         std::lock_guard<std::mutex> g(m_);
         if (--pending_ == 0) done_cv_.notify_all();
@@ -337,7 +349,8 @@ class Pool {
   std::mutex m_, run_m_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int, int64_t, int64_t)>* fn_ = nullptr;
-  int64_t total_ = 0;
+  int64_t total_ = 0, grain_ = 0;
+  std::atomic<int64_t> next_{0};
   int pending_ = 0;
   uint64_t gen_ = 0;
   bool stop_ = false;
@@ -359,6 +372,16 @@ static Pool* pool_for(int threads) {
 
 using namespace daop;
 
+// chunk sizes of the GEMV phases (rows; 0 = static split): ~0.5-1 MB of
+// weights per claim.  Settable for sweeps (daop_host_set_grain).
+static int64_t g_grain_up = 32, g_grain_down = 16;
+
+extern "C" int daop_host_set_grain(int64_t up, int64_t down) {
+  g_grain_up = up < 0 ? 0 : up;
+  g_grain_down = down < 0 ? 0 : down;
+  return DAOP_OK;
+}
+
 extern "C" int daop_host_expert_ffn(const uint16_t* x, int64_t n, const uint16_t* w1,
                                     const uint16_t* w3, const uint16_t* w2, int32_t d,
                                     int32_t ffn, float* y, uint16_t* act_scratch,
@@ -368,10 +391,10 @@ extern "C" int daop_host_expert_ffn(const uint16_t* x, int64_t n, const uint16_t
     return DAOP_ERR_SHAPE;
   }
   if (n == 0) return DAOP_OK;
-  // default: two workers per hardware thread -- more outstanding misses per
-  // core (measured 2.64-2.73 ms vs 2.93 ms per 8x7B expert on 16 cores)
-  if (threads < 1)
-    threads = 2 * static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  // default: one worker per hardware thread, rows claimed in chunks
+  // (scripts/host_threads_probe.py, 16 cores, 8x7B expert: 1.90 ms = 185 GB/s,
+  // vs 2.2-2.9 ms with static shares, where one delayed worker stalls all)
+  if (threads < 1) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   host::Pool* pool = host::pool_for(threads);
   if (n >= 16 && d % 32 == 0 && ffn % 32 == 0 && host::amx_usable()) {
     // batched experts on AMX tiles (prefill slow tier)
@@ -424,14 +447,14 @@ extern "C" int daop_host_expert_ffn(const uint16_t* x, int64_t n, const uint16_t
         act[t * ffn + i] = host::f2bf(s * u);
       }
     }
-  });
+  }, g_grain_up);
   // down: rows j of W2
   pool->run(d, [&](int, int64_t a, int64_t b) {
     for (int64_t j = a; j < b; ++j) {
       const uint16_t* r2 = w2 + j * ffn;
       for (int64_t t = 0; t < n; ++t) y[t * d + j] = host::dot_long(act + t * ffn, r2, ffn);
     }
-  });
+  }, g_grain_down);
   return DAOP_OK;
 }
 

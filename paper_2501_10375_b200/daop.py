@@ -41,6 +41,7 @@ from __future__ import annotations
 
 import os
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -144,6 +145,8 @@ class DaopEngine:
         self.swap_in_out = swap_in_out
         self.weights_from_pred = weights_from_pred
         self.host_threads = host_threads
+        self.host_ms = 0.0  # decode: wall time inside host-tier expert calls
+        self._host_exec = None  # one thread feeding the host tier (decode pre-calculation)
         self.model = MoEModel(shape, d_model, d_ff, seed=seed, device=device,
                               n_slots=self.placement0.slot_budget, resident_layers=[])
         self.pool = host_pool or HostExpertPool(shape, d_model, d_ff, seed)
@@ -434,6 +437,23 @@ class DaopEngine:
         pos = self.pos
         full = m.resident_mask().all(axis=1)
         deferred = []
+        queued = {}  # layer -> (sel, is_fast, {pick: Future}) of its host pre-calculation
+        if self._host_exec is None:
+            self._host_exec = ThreadPoolExecutor(max_workers=1, thread_name_prefix="daop-host")
+
+        def host_job(l, e, xs):  # one slow expert on the host tier (GIL released)
+            th0 = time.perf_counter()
+            y = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
+            self.host_ms += 1e3 * (time.perf_counter() - th0)
+            return y
+
+        def queue_precalc(l, pv):  # DAOP plan of l from layer l-1's mirror pv
+            hs, hf = self._host_plan(l, pv["p_pred"].astype(np.float64))
+            xs = pv["x"][None, :]
+            futs = {q: self._host_exec.submit(host_job, l, int(hs[q]), xs)
+                    for q in range(k) if not hf[q]}
+            queued[l] = (hs, hf, futs)
+
         for l in range(L):
             h = self._non_moe(h, l, pos)
             b = self.bufs[l % 2]
@@ -451,27 +471,29 @@ class DaopEngine:
                 h = b.h_out
                 prev_b, prev_v = b, v
                 continue
-            ys = {}
             plan_on_host = mode == 1 and not full[l]
-            if plan_on_host:
+            if plan_on_host and l not in queued:
                 # pre-calculation on the host while the GPU streams the layer
-                hs, hf = self._host_plan(l, prev_v["p_pred"].astype(np.float64))
-                xs = prev_v["x"][None, :]
-                for q in range(k):
-                    if not hf[q]:
-                        ys[q] = host_expert_ffn(self.pool, l, int(hs[q]), xs, self.host_threads)
+                queue_precalc(l, prev_v)
             stream.synchronize()
             s_l, f_l = v["sel"].copy(), v["is_fast"].copy()
-            if plan_on_host and (s_l.tolist() != hs.tolist() or f_l.tolist() != hf.tolist()):
-                raise ShapeMismatchError(f"layer {l}: host plan differs from the device plan")
+            if plan_on_host:
+                hs, hf, _ = queued[l]
+                if s_l.tolist() != hs.tolist() or f_l.tolist() != hf.tolist():
+                    raise ShapeMismatchError(f"layer {l}: host plan differs from the device plan")
             read(l, v)
+            # layer l+1's plan and stale input are known now: queue its
+            # pre-calculation behind this layer's, so the host tier runs back to
+            # back while this thread combines and launches
+            if daop and start <= l + 1 < L and not full[l + 1]:
+                queue_precalc(l + 1, v)
+            ys = {q: f.result() for q, f in queued[l][2].items()} if plan_on_host else {}
             if not f_l.all():
                 if mode == 0:  # Fiddler rule: current x_l, after the router
                     xs = v["x"][None, :]
                     for q in range(k):
                         if not f_l[q]:
-                            ys[q] = host_expert_ffn(self.pool, l, int(s_l[q]), xs,
-                                                    self.host_threads)
+                            ys[q] = host_job(l, int(s_l[q]), xs)
                 for q, yq in ys.items():
                     self._y_host[q].copy_(torch.from_numpy(yq[0]))
                     b.y[q].copy_(self._y_host[q], non_blocking=True)

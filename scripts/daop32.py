@@ -85,6 +85,7 @@ def main():
             "hbm_expert_gb": eng.placement0.slot_budget * 3 * a.d * a.ffn * 2 / 1e9,
             "decode_tokens_per_s": rec.tokens_per_second,
             "decode_ms_per_token": [round(r.ms, 2) for r in rec.decode],
+            "decode_host_tier_ms_per_token": eng.host_ms / n,
             "prefill_ms": rec.prefill.ms,
             "prefill_tokens_per_s": a.prompt / (rec.prefill.ms / 1e3),
             "swaps": len(rec.prefill.swaps),
