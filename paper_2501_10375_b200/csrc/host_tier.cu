@@ -411,14 +411,14 @@ extern "C" int daop_host_expert_ffn(const uint16_t* x, int64_t n, const uint16_t
       for (int64_t blk = a; blk < b; ++blk)
         host::amx_up_block(w1, w3, d, ffn, blk * 16, xp.data(), ntb, actp.data(), n);
       host::amx_release();
-    });
+    }, g_grain_up > 0 ? 4 : 0);
     pool->run(d / 16, [&](int, int64_t a, int64_t b) {
       if (a >= b) return;
       host::amx_config();
       for (int64_t blk = a; blk < b; ++blk)
         host::amx_down_block(w2, d, ffn, blk * 16, actp.data(), ntb, y, n);
       host::amx_release();
-    });
+    }, g_grain_down > 0 ? 2 : 0);
     if (act_scratch) {  // unpack act for callers that asked for it
       for (int64_t t = 0; t < n; ++t)
         for (int i = 0; i < ffn; ++i) {

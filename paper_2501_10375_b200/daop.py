@@ -146,6 +146,7 @@ class DaopEngine:
         self.weights_from_pred = weights_from_pred
         self.host_threads = host_threads
         self.host_ms = 0.0  # decode: wall time inside host-tier expert calls
+        self.prefill_host_ms = 0.0  # prefill: the same for the slow experts' token batches
         self._host_exec = None  # one thread feeding the host tier (decode pre-calculation)
         self.model = MoEModel(shape, d_model, d_ff, seed=seed, device=device,
                               n_slots=self.placement0.slot_budget, resident_layers=[])
@@ -307,7 +308,9 @@ class DaopEngine:
                     for e in slow:
                         a_, b_ = int(off[e]), int(off[e + 1])
                         xs = xs_host[e].view(torch.int16).numpy().view(np.uint16)
+                        th0 = time.perf_counter()
                         ys = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
+                        self.prefill_host_ms += 1e3 * (time.perf_counter() - th0)
                         y[a_:b_].copy_(torch.from_numpy(ys), non_blocking=False)
                         slow_execs += 1
                     hev = torch.cuda.Event(enable_timing=True)

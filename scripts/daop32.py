@@ -86,6 +86,7 @@ def main():
             "decode_tokens_per_s": rec.tokens_per_second,
             "decode_ms_per_token": [round(r.ms, 2) for r in rec.decode],
             "decode_host_tier_ms_per_token": eng.host_ms / n,
+            "prefill_host_tier_ms": eng.prefill_host_ms,
             "prefill_ms": rec.prefill.ms,
             "prefill_tokens_per_s": a.prompt / (rec.prefill.ms / 1e3),
             "swaps": len(rec.prefill.swaps),

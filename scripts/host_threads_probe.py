@@ -34,3 +34,18 @@ for gu, gd in grains:
     med = statistics.median(ts) * 1e3
     print("  threads %2d: %.3f ms  %.1f GB/s  (min %.3f max %.3f)" %
           (th, med, 352.3 / med, min(ts) * 1e3, max(ts) * 1e3))
+
+# batched experts (prefill slow tier, AMX tiles when n >= 16)
+for gu, gd in ((0, 0), (32, 16)):
+    _lib.call("daop_host_set_grain", gu, gd)
+    for n in (16, 64, 256):
+        xb = np.random.default_rng(1).integers(0, 1 << 14, (n, d)).astype(np.uint16)
+        host_expert_ffn(pool, 0, 0, xb)
+        ts = []
+        for i in range(8):
+            a = time.perf_counter()
+            host_expert_ffn(pool, 0, i % 8, xb)
+            ts.append(time.perf_counter() - a)
+        med = statistics.median(ts) * 1e3
+        print("grain %s n %3d: %.3f ms  %.1f TFLOP/s" %
+              ("chunked" if gu else "static ", n, med, 6 * n * d * ffn / med / 1e9))
