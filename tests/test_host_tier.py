@@ -43,3 +43,25 @@ def test_host_caps_reports():
     t = np.zeros(1, dtype=np.int32)
     _lib.call("daop_host_caps", a.ctypes.data, t.ctypes.data)
     assert t[0] >= 1
+
+
+@pytest.mark.parametrize("n", [1, 5, 16, 40])
+@pytest.mark.parametrize("threads", [1, 3, 7])
+def test_chunked_schedule_is_bit_identical(n, threads):
+    """Rows claimed in chunks (default) vs one contiguous share per worker:
+    every output row is computed by one worker in a fixed order either way,
+    so the results are bit-identical for any thread count."""
+    d, ffn = 256, 1024
+    rng = np.random.default_rng(n * 10 + threads)
+    mk = lambda *s: np.ascontiguousarray(  # noqa: E731
+        R.f32_to_bf16_bits(rng.uniform(-0.06, 0.06, size=s).astype(np.float32)))
+    b1, b3, b2, xb = mk(ffn, d), mk(ffn, d), mk(d, ffn), mk(n, d)
+    out = []
+    for grain in ((0, 0), (32, 16), (3, 5)):
+        _lib.call("daop_host_set_grain", *grain)
+        y = np.empty((n, d), dtype=np.float32)
+        _lib.call("daop_host_expert_ffn", xb.ctypes.data, n, b1.ctypes.data, b3.ctypes.data,
+                  b2.ctypes.data, d, ffn, y.ctypes.data, 0, threads)
+        out.append(y)
+    _lib.call("daop_host_set_grain", 32, 16)
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
