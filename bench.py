@@ -309,7 +309,7 @@ def run_b200(args, world, rank, local_rank):
                          "peak": hbm_peak, "unit": "GB/s",
                          "frac": wbytes / (bms / 1e3) / 1e9 / hbm_peak,
                          "bytes_per_step": wbytes},
-            "gpu_launches_per_step": MoEBlockEngine.prefill_kernels(),
+            "gpu_launches_per_step": MoEBlockEngine.prefill_kernels(B),
         }
         del hb, rb
     except Exception as exc:

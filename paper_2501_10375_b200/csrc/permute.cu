@@ -93,6 +93,56 @@ __global__ void perm_scatter_kernel(const int32_t* __restrict__ ids, int64_t n, 
   }
 }
 
+// n <= one chunk (decode-sized batches, prefill up to 4096 rows): count, scan
+// and the stable scatter of the three kernels above in ONE CTA -- the same
+// order (rows by expert, then by i), one launch instead of three
+__global__ void __launch_bounds__(P_THREADS, 1)
+    perm_single_kernel(const int32_t* __restrict__ ids, int64_t n, int E,
+                       int64_t* __restrict__ offsets, int32_t* __restrict__ perm,
+                       int32_t* __restrict__ inv) {
+  __shared__ int32_t cnt[P_MAX_E];
+  __shared__ int32_t run[P_MAX_E];
+  __shared__ int64_t off[P_MAX_E];
+  __shared__ int32_t wtot[P_THREADS / 32][P_MAX_E];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) cnt[i] = run[i] = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[ids[i]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t s = 0;
+    for (int e = 0; e < E; ++e) {
+      off[e] = offsets[e] = s;
+      s += cnt[e];
+    }
+    offsets[E] = s;
+  }
+  for (int64_t base = 0; base < n; base += P_THREADS) {
+    for (int i = threadIdx.x; i < (P_THREADS / 32) * E; i += blockDim.x) wtot[i / E][i % E] = 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    const bool ok = i < n;
+    const int e = ok ? ids[i] : -1 - lane;  // distinct dummies never match real ids
+    const unsigned same = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(same & ((1u << lane) - 1u));
+    if (ok && rank == 0) wtot[warp][e] = __popc(same);
+    __syncthreads();
+    if (ok) {
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += wtot[w][e];
+      const int64_t pos = off[e] + run[e] + before + rank;
+      perm[pos] = static_cast<int32_t>(i);
+      inv[i] = static_cast<int32_t>(pos);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < E; x += blockDim.x) {
+      int s = 0;
+      for (int w = 0; w < P_THREADS / 32; ++w) s += wtot[w][x];
+      run[x] += s;
+    }
+  }
+}
+
 // token-major gather: a warp reads token t's x row ONCE and stores it at its
 // k sorted positions inv[t, j] (reading in permuted order would fetch every
 // row k times, far apart in time)
@@ -383,9 +433,14 @@ int daop_permute(const int32_t* ids, int64_t T, int32_t k, int32_t E, const uint
   int nchunks = static_cast<int>((n + chunk - 1) / chunk);
   if (nchunks < 1) nchunks = 1;
   int32_t* counts = static_cast<int32_t*>(workspace);
-  perm_count_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts);
-  perm_scan_kernel<<<1, 256, 0, st>>>(counts, nchunks, E, offsets);
-  if (n > 0) perm_scatter_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts, offsets, perm, inv);
+  if (nchunks == 1) {
+    perm_single_kernel<<<1, P_THREADS, 0, st>>>(ids, n, E, offsets, perm, inv);
+  } else {
+    perm_count_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts);
+    perm_scan_kernel<<<1, 256, 0, st>>>(counts, nchunks, E, offsets);
+    perm_scatter_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts, offsets, perm,
+                                                       inv);
+  }
   DAOP_CHECK_LAUNCH("permute");
   if (x_perm && n > 0) {
     int64_t blocks = (T * 32 + 255) / 256;

@@ -201,10 +201,11 @@ class MoEBlockEngine:
         return r
 
     @staticmethod
-    def prefill_kernels() -> int:
-        """Kernel launches of one prefill layer: router, permute (count, scan,
-        scatter, gather), up GEMM, down GEMM, combine."""
-        return 8
+    def prefill_kernels(tokens: int = 1 << 20, k: int = 2) -> int:
+        """Kernel launches of one prefill layer of `tokens` tokens: router,
+        permute (count, scan, scatter -- one fused kernel when tokens * k fits
+        one 4096-row chunk -- then gather), up GEMM, down GEMM, combine."""
+        return 6 if tokens * k <= 4096 else 8
 
 
 class DecodeServer:

@@ -152,7 +152,10 @@ def test_device_planner_matches_golden(P, golden):
 
 
 @pytest.mark.parametrize("d,E,k,T", [(256, 8, 2, 64), (4096, 8, 2, 300), (1024, 16, 2, 77),
-                                     (6144, 8, 2, 4100)])  # 8x22B width: tensor-core path
+                                     (6144, 8, 2, 4100),  # 8x22B width: tensor-core path
+                                     # T <= 128: CTA-per-token kernel; 129: tensor-core path
+                                     (4096, 8, 2, 1), (4096, 8, 2, 128), (4096, 8, 2, 129),
+                                     (512, 4, 1, 5), (256, 2, 1, 3), (6144, 8, 2, 64)])
 def test_router_parity(P, d, E, k, T):
     pkg, model_mod, ops = P
     om = N.OracleModel(3, E, k, d, 512, seed=4)
@@ -184,6 +187,20 @@ def test_router_parity(P, d, E, k, T):
             counts[t // S, sel[t, j]] += 1
     assert np.array_equal(hist[:, 1].cpu().numpy(), counts)
     assert hist[:, 0].sum().item() == 0 and hist[:, 2].sum().item() == 0
+
+
+@pytest.mark.parametrize("T", [1, 64, 300])
+def test_router_last_layer_without_prediction(P, T):
+    """wg_next = None (the last layer): no p_pred, same decisions as with it."""
+    pkg, model_mod, ops = P
+    d, E, k = 1024, 8, 2
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, k), d, 512, seed=6, resident_layers=[])
+    h = m.input_hidden(T, stream=3)
+    r0 = ops.router(h, m.norm[1], m.gate[1], None, k)
+    r1 = ops.router(h, m.norm[1], m.gate[1], m.gate[0], k)
+    assert r0["p_pred"] is None
+    for key in ("x", "p", "topk_idx", "topk_w"):
+        assert torch.equal(r0[key], r1[key]), key
 
 
 @pytest.mark.parametrize("T,k,E", [(1, 2, 8), (1000, 2, 8), (4099, 2, 8), (777, 4, 16), (20000, 2, 8)])
