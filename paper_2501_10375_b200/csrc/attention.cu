@@ -106,10 +106,28 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
     if (lane == 0) ring_produce(R, wqkv, r0, n, d);
     return;
   }
-  // RMSNorm by the consumer warps (named barrier: the producer is not waited for)
-  const int nt = AT_WARPS * 32;
+  // RMSNorm by the consumer warps (named barrier: the producer is not waited
+  // for).  Chunks of 8: h (2 x float4) and gamma (uint4) loaded once, up front;
+  // <= 2 chunks per thread in registers (d <= 16 * AT_WARPS * 32), else reload.
+  const int nt = AT_WARPS * 32, n8 = d / 8, tid = threadIdx.x;
+  const float4* h4 = reinterpret_cast<const float4*>(h);
+  const uint4* g4 = reinterpret_cast<const uint4*>(gamma);
+  const bool regs = n8 <= 2 * nt;
+  const int c0 = tid, c1 = tid + nt;
+  float4 ha = make_float4(0.f, 0.f, 0.f, 0.f), hb = ha, hc = ha, hd = ha;
+  uint4 ga = make_uint4(0u, 0u, 0u, 0u), gb = ga;
+  if (regs && c0 < n8) { ha = h4[2 * c0]; hb = h4[2 * c0 + 1]; ga = g4[c0]; }
+  if (regs && c1 < n8) { hc = h4[2 * c1]; hd = h4[2 * c1 + 1]; gb = g4[c1]; }
+  auto sq4 = [](float4 v, float a) {
+    a = fmaf(v.x, v.x, a); a = fmaf(v.y, v.y, a); a = fmaf(v.z, v.z, a);
+    return fmaf(v.w, v.w, a);
+  };
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += nt) ss = fmaf(h[i], h[i], ss);
+  if (regs) {
+    ss = sq4(hd, sq4(hc, sq4(hb, sq4(ha, ss))));
+  } else {
+    for (int i = tid; i < d; i += nt) ss = fmaf(h[i], h[i], ss);
+  }
   ss = warp_sum(ss);
   if (lane == 0) red[warp] = ss;
   asm volatile("bar.sync 1, %0;" ::"r"(nt));
@@ -120,11 +138,26 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nt));
   const float r = red[32];
-  for (int i = threadIdx.x; i < d; i += nt) {
-    const float x = __fmul_rn(__fmul_rn(h[i], r),
-                              __uint_as_float(static_cast<uint32_t>(gamma[i]) << 16));
-    xs[i] = f32_to_bf16_bits(x);
-    if (xa_out && blockIdx.x == 0) xa_out[i] = xs[i];
+  auto norm8 = [&](int c, float4 u, float4 v, uint4 g) {
+    const float hv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+    const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+    uint32_t xw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x0 = __fmul_rn(__fmul_rn(hv[2 * q], r), __uint_as_float(gw[q] << 16));
+      const float x1 = __fmul_rn(__fmul_rn(hv[2 * q + 1], r), __uint_as_float(gw[q] & 0xffff0000u));
+      xw[q] = static_cast<uint32_t>(f32_to_bf16_bits(x0)) |
+              (static_cast<uint32_t>(f32_to_bf16_bits(x1)) << 16);
+    }
+    const uint4 x8 = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+    reinterpret_cast<uint4*>(xs)[c] = x8;
+    if (xa_out && blockIdx.x == 0) reinterpret_cast<uint4*>(xa_out)[c] = x8;
+  };
+  if (regs) {
+    if (c0 < n8) norm8(c0, ha, hb, ga);
+    if (c1 < n8) norm8(c1, hc, hd, gb);
+  } else {
+    for (int c = tid; c < n8; c += nt) norm8(c, h4[2 * c], h4[2 * c + 1], g4[c]);
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nt));
   ring_consume(R, r0, n, d, reinterpret_cast<const uint4*>(xs), warp, lane,

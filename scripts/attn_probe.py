@@ -15,11 +15,24 @@ for i in range(5):
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 n = 200
-e0.record()
-for i in range(n):
-    att.decode(h, i % 2, ctx, out=out)
-e1.record()
-torch.cuda.synchronize()
-us = e0.elapsed_time(e1) / n * 1e3
 b = att.bytes_per_token_layer(ctx + 1)
-print(f"attention decode layer at ctx {ctx}: {us:.1f} us, {b / us / 1e3:.0f} GB/s")
+for graph in (False, True):
+    if graph:  # launch-cost free: the layers back to back in one graph
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(20):
+                att.decode(h, i % 2, ctx, out=out)
+        g.replay()
+        torch.cuda.synchronize()
+    e0.record()
+    if graph:
+        for _ in range(n // 20):
+            g.replay()
+    else:
+        for i in range(n):
+            att.decode(h, i % 2, ctx, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / n * 1e3
+    print(f"attention decode layer at ctx {ctx} ({'graph' if graph else 'eager'}): {us:.1f} us, "
+          f"{b / us / 1e3:.0f} GB/s")
