@@ -364,6 +364,21 @@ int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const uint16_t* 
                      float theta, uint16_t* d_xa_out, float* d_h_out, void* d_workspace,
                      daop_stream_t stream);
 
+/* Prefill of T prompt tokens through the same attention block, positions
+ * pos0 .. pos0 + T - 1 (the calls DaopEngine.prefill makes per layer; the
+ * reference prices this as the prefill t_nonmoe, simulator.py:438-441).  The
+ * two projections are plain GEMMs the caller runs (cuBLAS, fp32 output):
+ *   daop_attn_norm_rows: d_xa (T, d) bf16 = rmsnorm(d_h (T, d) fp32) * gamma
+ *   qkv = xa . Wqkv^T  (T, q + 2 kv) fp32                        [caller]
+ *   daop_attn_prefill:   k (RoPE), v of every token -> the cache, then causal
+ *                        attention per token -> d_o (T, q) bf16
+ *   h' = h + o . Wo^T                                              [caller] */
+int daop_attn_norm_rows(const float* d_h, int64_t T, const uint16_t* d_gamma, int32_t d, float eps,
+                        uint16_t* d_xa, daop_stream_t stream);
+int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, uint16_t* d_k_cache,
+                      uint16_t* d_v_cache, int32_t n_heads, int32_t n_kv, int32_t max_seq,
+                      float theta, uint16_t* d_o, daop_stream_t stream);
+
 /* ------------------------------------------------ persistent decode server (b = 1)
  * The end-to-end decode call without a launch or a stream synchronisation
  * per call: daop_server_start launches ONE persistent cooperative kernel for

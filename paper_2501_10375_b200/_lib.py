@@ -30,6 +30,8 @@ PROTOS = {
     "daop_server_step": [P, P, F64],
     "daop_server_stop": [P],
     "daop_attn_workspace": [I32, I32, I32, P],
+    "daop_attn_norm_rows": [P, I64, P, I32, F32, P, P],
+    "daop_attn_prefill": [P, I64, I32, P, P, I32, I32, I32, F32, P, P],
     "daop_attn_decode": [P, P, P, P, P, P, I32, I32, I32, I32, I32, F32, F32, P, P, P, P],
     "daop_server_trace": [P, I32],
     "daop_topk_rows_f64": [P, I64, I32, I32, P, P],

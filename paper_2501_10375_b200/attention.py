@@ -8,7 +8,9 @@ QKV projection [Wq; Wk; Wv] (q + 2 kv, d), the output projection Wo (d, q)
 -- bf16, random-init from the counter generator like the experts -- and a
 bf16 KV cache (n_kv, max_seq, 128).  `decode(h, layer, pos)` runs one token
 through csrc/attention.cu (daop_attn_decode: RMSNorm -> QKV GEMV -> RoPE ->
-cache append -> GQA flash-decoding -> O-proj GEMV + residual).  Mixtral-8x7B:
+cache append -> GQA flash-decoding -> O-proj GEMV + residual); `prefill(h,
+layer, pos0)` runs a whole prompt causally (cuBLAS projections over its T
+rows + daop_attn_norm_rows / daop_attn_prefill).  Mixtral-8x7B:
 d 4096, 32 query heads, 8 KV heads, head dim 128, rope theta 1e6.
 """
 
@@ -17,6 +19,7 @@ from __future__ import annotations
 import torch
 
 from . import _lib, ops
+from .errors import ShapeMismatchError
 from .model import make_tag
 
 KIND_ATTN = 5      # matrix 0 = Wqkv (q + 2 kv, d), 1 = Wo (d, q)
@@ -63,6 +66,32 @@ class AttentionStack:
                   float(self.theta), self.xa.data_ptr(), out.data_ptr(), self.ws.data_ptr(),
                   ops._s())
         return out
+
+    def prefill(self, h: torch.Tensor, layer: int, pos0: int = 0,
+                out: torch.Tensor | None = None):
+        """h (T, d) fp32 on the device: T prompt tokens at positions pos0 ..
+        pos0 + T - 1 -> h + Attention(RMSNorm(h)) (T, d) fp32, causal; appends
+        every token's k, v to the layer's cache.  The two projections are plain
+        GEMMs (cuBLAS, bf16 in, fp32 out); RMSNorm, RoPE, the cache append and
+        the attention are the library's kernels (daop_attn_norm_rows /
+        daop_attn_prefill)."""
+        ops._dev(h)
+        T, d = h.shape
+        if pos0 < 0 or pos0 + T > self.max_seq:
+            raise ShapeMismatchError(f"prefill positions {pos0}..{pos0 + T - 1} exceed max_seq "
+                                     f"{self.max_seq}")
+        xa = torch.empty((T, d), dtype=torch.bfloat16, device=h.device)
+        _lib.call("daop_attn_norm_rows", h.data_ptr(), T, self.norm[layer].data_ptr(), d,
+                  float(ops.RMS_EPS), xa.data_ptr(), ops._s())
+        qkv = torch.mm(xa, self.wqkv[layer].t(), out_dtype=torch.float32)
+        o = torch.empty((T, self.q_dim), dtype=torch.bfloat16, device=h.device)
+        _lib.call("daop_attn_prefill", qkv.data_ptr(), T, int(pos0),
+                  self.k_cache[layer].data_ptr(), self.v_cache[layer].data_ptr(), self.n_heads,
+                  self.n_kv, self.max_seq, float(self.theta), o.data_ptr(), ops._s())
+        y = torch.mm(o, self.wo[layer].t(), out_dtype=torch.float32)
+        if out is None:
+            return h + y
+        return torch.add(h, y, out=out)
 
     def bytes_per_token_layer(self, ctx: int) -> int:
         """Algorithmic HBM bytes of one decode step of one layer at context

@@ -368,9 +368,232 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
                [&](int row, float v) { h_out[row] = h[row] + v; });
 }
 
+// ---------------------------------------------------------------------------
+// Prefill: T prompt tokens of one layer at positions pos0 .. pos0 + T - 1.
+// The projections are plain GEMMs over the T rows (the caller's cuBLAS calls:
+// xa . Wqkv^T and o . Wo^T with fp32 output); these kernels do the rest.
+
+// xa[t] = bf16(rmsnorm(h[t]) * gamma): one CTA per token
+__global__ void __launch_bounds__(256) attn_norm_rows_kernel(const float* __restrict__ h,
+                                                             const uint16_t* __restrict__ gamma,
+                                                             int d, float eps,
+                                                             uint16_t* __restrict__ xa) {
+  __shared__ float red[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n8 = d / 8;
+  const float4* h4 = reinterpret_cast<const float4*>(h + static_cast<int64_t>(blockIdx.x) * d);
+  const uint4* g4 = reinterpret_cast<const uint4*>(gamma);
+  float ss = 0.f;
+  for (int c = tid; c < n8; c += blockDim.x) {
+    const float4 u = h4[2 * c], v = h4[2 * c + 1];
+    ss = fmaf(u.x, u.x, ss); ss = fmaf(u.y, u.y, ss); ss = fmaf(u.z, u.z, ss); ss = fmaf(u.w, u.w, ss);
+    ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + eps);
+  uint4* x4 = reinterpret_cast<uint4*>(xa + static_cast<int64_t>(blockIdx.x) * d);
+  for (int c = tid; c < n8; c += blockDim.x) {
+    const float4 u = h4[2 * c], v = h4[2 * c + 1];
+    const uint4 g = g4[c];
+    const float hv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+    const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+    uint32_t xw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float x0 = __fmul_rn(__fmul_rn(hv[2 * q], r), __uint_as_float(gw[q] << 16));
+      const float x1 = __fmul_rn(__fmul_rn(hv[2 * q + 1], r), __uint_as_float(gw[q] & 0xffff0000u));
+      xw[q] = static_cast<uint32_t>(f32_to_bf16_bits(x0)) |
+              (static_cast<uint32_t>(f32_to_bf16_bits(x1)) << 16);
+    }
+    x4[c] = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+  }
+}
+
+struct PrefillArgs {
+  const float* qkv;   // (T, q_dim + 2 kv_dim) fp32, unrotated
+  uint16_t* k_cache;  // (n_kv, max_seq, hd) bf16, this layer
+  uint16_t* v_cache;
+  int n_heads, n_kv, max_seq, pos0;
+  float theta, scale;
+  uint16_t* o;        // (T, n_heads * hd) bf16
+};
+
+// k (RoPE) and v of every prompt token -> the cache (before any attention
+// reads it): CTA = token
+__global__ void __launch_bounds__(128) attn_prefill_append_kernel(PrefillArgs a) {
+  const int t = blockIdx.x, p = a.pos0 + t;
+  const int q_dim = a.n_heads * AT_HD, kv_dim = a.n_kv * AT_HD;
+  const float* row = a.qkv + static_cast<int64_t>(t) * (q_dim + 2 * kv_dim);
+  for (int i = threadIdx.x; i < a.n_kv * (AT_HD / 2); i += blockDim.x) {
+    const int g = i / (AT_HD / 2), j = i - g * (AT_HD / 2);
+    float k0 = row[q_dim + g * AT_HD + j], k1 = row[q_dim + g * AT_HD + j + AT_HD / 2];
+    rope_pair(k0, k1, j, p, a.theta);
+    uint16_t* kc = a.k_cache + (static_cast<int64_t>(g) * a.max_seq + p) * AT_HD;
+    kc[j] = f32_to_bf16_bits(k0);
+    kc[j + AT_HD / 2] = f32_to_bf16_bits(k1);
+  }
+  for (int i = threadIdx.x; i < kv_dim; i += blockDim.x) {
+    const int g = i / AT_HD, j = i - g * AT_HD;
+    a.v_cache[(static_cast<int64_t>(g) * a.max_seq + p) * AT_HD + j] =
+        f32_to_bf16_bits(row[q_dim + kv_dim + i]);
+  }
+}
+
+// causal attention of query token t (position pos0 + t) over positions
+// 0 .. pos0 + t: CTA = (kv head g, token t); 64-position K / V tiles by bulk
+// copy; per tile the same scores / exp / P.V as attn_decode_kernel's split,
+// folded into running (m, l, acc) with the usual rescaling
+__global__ void __launch_bounds__(256, 2) attn_prefill_kernel(PrefillArgs a) {
+  __shared__ __align__(128) uint16_t k_s[AT_SPLIT * AT_HD];
+  __shared__ __align__(128) uint16_t v_s[AT_SPLIT * AT_HD];
+  __shared__ float q_s[AT_MAX_GROUP][AT_HD];
+  __shared__ float p_s[AT_MAX_GROUP][AT_SPLIT];
+  __shared__ float ml_s[AT_MAX_GROUP][2];
+  __shared__ uint64_t bar;
+  const int g = blockIdx.x, t = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+  const int p = a.pos0 + t;
+  const int group = a.n_heads / a.n_kv;
+  const int q_dim = a.n_heads * AT_HD, kv_dim = a.n_kv * AT_HD;
+  const float* row = a.qkv + static_cast<int64_t>(t) * (q_dim + 2 * kv_dim);
+  const uint16_t* kc = a.k_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
+  const uint16_t* vc = a.v_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < group * (AT_HD / 2); i += blockDim.x) {
+    const int hh = i / (AT_HD / 2), j = i - hh * (AT_HD / 2);
+    float x0 = row[(g * group + hh) * AT_HD + j];
+    float x1 = row[(g * group + hh) * AT_HD + j + AT_HD / 2];
+    rope_pair(x0, x1, j, p, a.theta);
+    q_s[hh][j] = x0;
+    q_s[hh][j + AT_HD / 2] = x1;
+  }
+  // running state of this thread's (head, dim pair) items (<= 2: group <= 8)
+  constexpr int MAXI = AT_MAX_GROUP * (AT_HD / 2) / 256;
+  float rm[MAXI], rl[MAXI], o0[MAXI], o1[MAXI];
+#pragma unroll
+  for (int q = 0; q < MAXI; ++q) rm[q] = -INFINITY, rl[q] = o0[q] = o1[q] = 0.f;
+  const int tiles = p / AT_SPLIT + 1;
+  for (int s = 0; s < tiles; ++s) {
+    const int p0 = s * AT_SPLIT;
+    const int n = min(p + 1, p0 + AT_SPLIT) - p0;
+    __syncthreads();  // the previous tile is fully consumed (and q_s / bar are ready)
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar, 2 * n * AT_HD * 2);
+      bulk_g2s_plain(k_s, kc + static_cast<int64_t>(p0) * AT_HD, n * AT_HD * 2, &bar);
+      bulk_g2s_plain(v_s, vc + static_cast<int64_t>(p0) * AT_HD, n * AT_HD * 2, &bar);
+    }
+    mbar_wait(&bar, s & 1);
+    for (int u = tid; u < group * AT_SPLIT; u += blockDim.x) {
+      const int hh = u / AT_SPLIT, i = u - hh * AT_SPLIT;
+      float sc = -INFINITY;
+      if (i < n) {
+        const uint4* kr = reinterpret_cast<const uint4*>(k_s + i * AT_HD);
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < AT_HD / 8; ++c) {
+          const uint4 kv = kr[(c + i) & (AT_HD / 8 - 1)];
+          const int cc = ((c + i) & (AT_HD / 8 - 1)) * 8;
+          acc = fmaf(q_s[hh][cc + 0], bf16lo(kv.x), acc);
+          acc = fmaf(q_s[hh][cc + 1], bf16hi(kv.x), acc);
+          acc = fmaf(q_s[hh][cc + 2], bf16lo(kv.y), acc);
+          acc = fmaf(q_s[hh][cc + 3], bf16hi(kv.y), acc);
+          acc = fmaf(q_s[hh][cc + 4], bf16lo(kv.z), acc);
+          acc = fmaf(q_s[hh][cc + 5], bf16hi(kv.z), acc);
+          acc = fmaf(q_s[hh][cc + 6], bf16lo(kv.w), acc);
+          acc = fmaf(q_s[hh][cc + 7], bf16hi(kv.w), acc);
+        }
+        sc = acc * a.scale;
+      }
+      p_s[hh][i] = sc;
+    }
+    __syncthreads();
+    const int warp = tid >> 5;
+    for (int hh = warp; hh < group; hh += blockDim.x / 32) {
+      float mx = fmaxf(p_s[hh][lane], p_s[hh][lane + 32]);
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float e0 = lane < n ? expf(p_s[hh][lane] - mx) : 0.f;
+      const float e1 = lane + 32 < n ? expf(p_s[hh][lane + 32] - mx) : 0.f;
+      p_s[hh][lane] = e0;
+      p_s[hh][lane + 32] = e1;
+      const float se = warp_sum(e0 + e1);
+      if (lane == 0) {
+        ml_s[hh][0] = mx;
+        ml_s[hh][1] = se;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < MAXI; ++q) {
+      const int u = tid + q * blockDim.x;
+      if (u >= group * (AT_HD / 2)) break;
+      const int hh = u / (AT_HD / 2), c = u - hh * (AT_HD / 2);
+      float a0 = 0.f, a1 = 0.f;
+      for (int i = 0; i < n; ++i) {
+        const uint32_t vv = *reinterpret_cast<const uint32_t*>(v_s + i * AT_HD + 2 * c);
+        a0 = fmaf(p_s[hh][i], bf16lo(vv), a0);
+        a1 = fmaf(p_s[hh][i], bf16hi(vv), a1);
+      }
+      const float ms = ml_s[hh][0], mn = fmaxf(rm[q], ms);
+      const float co = expf(rm[q] - mn), cs = expf(ms - mn);  // rm = -inf -> co = 0
+      rl[q] = fmaf(rl[q], co, ml_s[hh][1] * cs);
+      o0[q] = fmaf(o0[q], co, a0 * cs);
+      o1[q] = fmaf(o1[q], co, a1 * cs);
+      rm[q] = mn;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MAXI; ++q) {
+    const int u = tid + q * blockDim.x;
+    if (u >= group * (AT_HD / 2)) break;
+    const int hh = u / (AT_HD / 2), c = u - hh * (AT_HD / 2);
+    uint16_t* orow = a.o + static_cast<int64_t>(t) * q_dim + (g * group + hh) * AT_HD;
+    orow[2 * c] = f32_to_bf16_bits(o0[q] / rl[q]);
+    orow[2 * c + 1] = f32_to_bf16_bits(o1[q] / rl[q]);
+  }
+}
+
 }  // namespace daop
 
 using namespace daop;
+
+extern "C" int daop_attn_norm_rows(const float* d_h, int64_t T, const uint16_t* d_gamma, int32_t d,
+                                   float eps, uint16_t* d_xa, daop_stream_t stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0) {
+    set_error("attn_norm_rows: unsupported shape (T=%lld, d=%d)", (long long)T, d);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (T == 0) return DAOP_OK;
+  attn_norm_rows_kernel<<<static_cast<unsigned>(T), 256, 0, as_stream(stream)>>>(d_h, d_gamma, d,
+                                                                                 eps, d_xa);
+  DAOP_CHECK_LAUNCH("attn_norm_rows");
+  return DAOP_OK;
+}
+
+extern "C" int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, uint16_t* d_k_cache,
+                                 uint16_t* d_v_cache, int32_t n_heads, int32_t n_kv,
+                                 int32_t max_seq, float theta, uint16_t* d_o,
+                                 daop_stream_t stream) {
+  if (n_kv < 1 || n_heads % n_kv != 0 || n_heads / n_kv > AT_MAX_GROUP || T < 0 || pos0 < 0 ||
+      pos0 + T > max_seq || T > 65535) {
+    set_error("attn_prefill: unsupported (heads=%d kv=%d pos0=%d T=%lld max_seq=%d)", n_heads,
+              n_kv, pos0, (long long)T, max_seq);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (T == 0) return DAOP_OK;
+  cudaStream_t st = as_stream(stream);
+  PrefillArgs a{d_qkv, d_k_cache, d_v_cache, n_heads, n_kv, max_seq, pos0,
+                theta, 1.0f / sqrtf(static_cast<float>(AT_HD)), d_o};
+  attn_prefill_append_kernel<<<static_cast<unsigned>(T), 128, 0, st>>>(a);
+  DAOP_CHECK_LAUNCH("attn_prefill_append");
+  attn_prefill_kernel<<<dim3(n_kv, static_cast<unsigned>(T)), 256, 0, st>>>(a);
+  DAOP_CHECK_LAUNCH("attn_prefill");
+  return DAOP_OK;
+}
 
 extern "C" int daop_attn_workspace(int32_t n_heads, int32_t n_kv, int32_t max_seq,
                                    int64_t* h_bytes) {

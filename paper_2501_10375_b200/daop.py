@@ -217,15 +217,11 @@ class DaopEngine:
         return self.attn.decode(h, layer, pos, out=self._h_attn)
 
     def _non_moe_prefill(self, h: torch.Tensor, layer: int) -> torch.Tensor:
-        """Causal attention over the prompt, token by token (each token's
-        layer-l attention reads the layer-l keys / values of the tokens before
-        it, which are in the cache by then)."""
+        """Causal attention over the whole prompt at positions 0 .. T-1 (its
+        keys / values land in the layer's cache for the decode tokens)."""
         if self.attn is None:
             return h
-        out = torch.empty_like(h)
-        for t in range(h.shape[0]):
-            self.attn.decode(h[t], layer, t, out=out[t])
-        return out
+        return self.attn.prefill(h, layer, 0)
 
     # ------------------------------------------------------------ prefill
     def prefill(self, h: torch.Tensor) -> PrefillResult:

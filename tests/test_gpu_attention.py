@@ -71,3 +71,52 @@ def test_attention_bad_position(P):
     h = torch.zeros(1024, device="cuda")
     with pytest.raises(pkg.errors.DeviceError):
         att.decode(h, 0, 64)
+
+
+@pytest.mark.parametrize("d,heads,kv,pos0,T", [
+    (1024, 8, 2, 0, 5),          # a fresh prompt inside one tile
+    (1024, 8, 2, 70, 130),       # history + a prompt spanning several tiles
+    (4096, 32, 8, 0, 64),        # Mixtral-8x7B attention shape
+])
+def test_attention_prefill_parity(P, d, heads, kv, pos0, T):
+    """Batched causal prefill (cuBLAS projections + daop_attn_norm_rows /
+    daop_attn_prefill) vs the oracle run position by position, and vs the
+    decode kernels run token by token: outputs within the hidden-state bar,
+    cache rows within one bf16 ulp (the GEMM's summation order differs)."""
+    pkg, A = P
+    att = A.AttentionStack(2, d, heads, kv, max_seq=512, seed=5)
+    dec = A.AttentionStack(2, d, heads, kv, max_seq=512, seed=5)
+    oatt = N.OracleAttention(d, heads, kv, theta=att.theta, seed=5)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    hist_k = torch.randn(att.k_cache[1].shape, generator=g, device="cuda")
+    hist_v = torch.randn(att.v_cache[1].shape, generator=g, device="cuda")
+    for a in (att, dec):  # the same history before pos0, nothing after
+        a.k_cache[1].copy_(hist_k)
+        a.v_cache[1].copy_(hist_v)
+        a.k_cache[1][:, pos0:].zero_()
+        a.v_cache[1][:, pos0:].zero_()
+    h = torch.empty((T, d), dtype=torch.float32, device="cuda")
+    A.ops.fill_uniform_f32(h, 5, (4 << 56) | (11 << 32), float(np.float32(np.sqrt(3))))
+    kc, vc = bf16_f32(att.k_cache[1]), bf16_f32(att.v_cache[1])
+    out = att.prefill(h, 1, pos0)
+    ref_dec = torch.stack([dec.decode(h[t], 1, pos0 + t) for t in range(T)])
+    torch.cuda.synchronize()
+    hn = h.cpu().numpy()
+    for t in range(T):
+        ref, _, kc, vc = N.attention_decode(oatt, 1, hn[t], pos0 + t, kc, vc)
+        close(out[t].cpu().numpy(), ref, f"token {t} vs oracle")
+    close(out.cpu().numpy(), ref_dec.cpu().numpy(), "prefill vs decode path")
+    span = slice(pos0, pos0 + T)
+    for mine, want in ((att.k_cache[1], kc), (att.v_cache[1], vc)):
+        m = bf16_f32(mine)[:, span]
+        w = want[:, span]
+        assert np.all(np.abs(m - w) <= np.abs(w) * 2 ** -7 + 1e-3 * np.abs(w).max())
+    assert att.k_cache[0].abs().sum().item() == 0  # layer 0 untouched
+
+
+def test_attention_prefill_bounds(P):
+    pkg, A = P
+    att = A.AttentionStack(1, 1024, 8, 2, max_seq=64, seed=3)
+    h = torch.zeros((10, 1024), device="cuda")
+    with pytest.raises(pkg.ShapeMismatchError):
+        att.prefill(h, 0, 60)
