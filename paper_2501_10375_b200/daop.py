@@ -49,6 +49,7 @@ import torch
 
 from . import _lib, ops
 from .errors import ConfigError, ShapeMismatchError
+from .engine import SKINNY_MAX_ROWS
 from .model import KIND_EXPERT, MoEModel, make_tag
 from .placement import (SWAP_IN_OUT_DEFAULT, ExpertPlacement, SwapEvent,
                         allocate_for_sequence, init_from_calibration)
@@ -172,6 +173,9 @@ class DaopEngine:
             self.attn = AttentionStack(shape.num_layers, d_model, heads, max(1, heads // 4),
                                        max_seq=max_seq, seed=seed, device=self.model.device)
             self._h_attn = torch.empty(d_model, dtype=torch.float32, device=self.model.device)
+            # one-time cuBLAS / kernel setup of the prompt attention here, not in the
+            # first timed prefill (position 0 of layer 0 is rewritten by every prefill)
+            self.attn.prefill(torch.zeros((1, d_model), device=self.model.device), 0, 0)
         self._lru = None  # LRU planner of the ondemand / prefetch engines (after prefill)
 
     # ------------------------------------------------------------ residency
@@ -279,10 +283,12 @@ class DaopEngine:
             rows = pr["x_perm"].shape[0]
             act = torch.empty((rows, m.ffn), dtype=torch.bfloat16, device=m.device)
             y = torch.empty((rows, d), dtype=torch.float32, device=m.device)
-            ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_now, m.slab, m.n_slots,
-                               m.slot_elems, d, m.ffn, out=act)
-            ops.expert_gemm_down(act, pr["offsets"], slot_now, m.slab, m.n_slots,
-                                 m.slot_elems, d, m.ffn, out=y)
+            skinny = rows <= SKINNY_MAX_ROWS  # weights as the M side (engine.py)
+            up = ops.expert_gemm_up_skinny if skinny else ops.expert_gemm_up
+            down = ops.expert_gemm_down_skinny if skinny else ops.expert_gemm_down
+            up(pr["x_perm"], pr["offsets"], slot_now, m.slab, m.n_slots, m.slot_elems, d, m.ffn,
+               out=act)
+            down(act, pr["offsets"], slot_now, m.slab, m.n_slots, m.slot_elems, d, m.ffn, out=y)
             if swapped_in:
                 g1 = torch.cuda.Event(enable_timing=True)
                 g1.record()
@@ -291,10 +297,10 @@ class DaopEngine:
                     torch.cuda.current_stream().wait_event(ev)
                 slot_mig = torch.full_like(slot_now, -1)
                 slot_mig[swapped_in] = m.slot_of[l][swapped_in]
-                ops.expert_gemm_up(pr["x_perm"], pr["offsets"], slot_mig, m.slab, m.n_slots,
-                                   m.slot_elems, d, m.ffn, out=act)
-                ops.expert_gemm_down(act, pr["offsets"], slot_mig, m.slab, m.n_slots,
-                                     m.slot_elems, d, m.ffn, out=y)
+                up(pr["x_perm"], pr["offsets"], slot_mig, m.slab, m.n_slots, m.slot_elems, d,
+                   m.ffn, out=act)
+                down(act, pr["offsets"], slot_mig, m.slab, m.n_slots, m.slot_elems, d, m.ffn,
+                     out=y)
             if slow:
                 x_ready.synchronize()
                 # the host tier's results go up on their own stream, so the GPU

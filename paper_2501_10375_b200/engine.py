@@ -27,8 +27,10 @@ from .model import MoEModel
 
 
 # up to this many permuted rows (T * k) the layer runs the skinny (swap-AB)
-# GEMMs of batched decode: below it the prefill GEMM tiles are mostly empty
-SKINNY_MAX_ROWS = 256
+# GEMMs of batched decode: below it the prefill GEMM tiles are mostly empty.
+# scripts/skinny_crossover.py (8x7B layer, up + down): T 256 0.63 vs 0.96 ms,
+# T 384 0.92 vs 1.03, T 512 1.17 vs 1.09 (skinny vs 512-row pair tiles)
+SKINNY_MAX_ROWS = 768
 
 
 class MoEBlockEngine:

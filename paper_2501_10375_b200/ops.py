@@ -132,21 +132,25 @@ def skinny_nt(rows: int) -> int:
     return 32 if rows <= 32 else 64
 
 
-def expert_gemm_up_skinny(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, nt=0):
-    """Up GEMM for small token counts (weights as the M side)."""
-    _dev(x_perm, offsets, slot_of, slab)
+def expert_gemm_up_skinny(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, nt=0,
+                          out=None):
+    """Up GEMM for small token counts (weights as the M side); like
+    expert_gemm_up, rows of experts with slot -1 in `out` are left untouched."""
+    _dev(x_perm, offsets, slot_of, slab, out)
     rows = x_perm.shape[0]
-    act = torch.empty((rows, ffn), dtype=torch.bfloat16, device=x_perm.device)
+    act = torch.empty((rows, ffn), dtype=torch.bfloat16, device=x_perm.device) if out is None \
+        else out
     _lib.call("daop_expert_gemm_up_skinny", x_perm.data_ptr(), rows, d, ffn, slab.data_ptr(),
               n_slots, slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
               act.data_ptr(), nt or skinny_nt(rows), _s())
     return act
 
 
-def expert_gemm_down_skinny(act, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, nt=0):
-    _dev(act, offsets, slot_of, slab)
+def expert_gemm_down_skinny(act, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, nt=0,
+                            out=None):
+    _dev(act, offsets, slot_of, slab, out)
     rows = act.shape[0]
-    y = torch.empty((rows, d), dtype=torch.float32, device=act.device)
+    y = torch.empty((rows, d), dtype=torch.float32, device=act.device) if out is None else out
     _lib.call("daop_expert_gemm_down_skinny", act.data_ptr(), rows, d, ffn, slab.data_ptr(),
               n_slots, slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
               y.data_ptr(), nt or skinny_nt(rows), _s())

@@ -467,7 +467,8 @@ def test_up_gemm_gather_bitexact(P, d, ffn, E, T):
 
 
 @pytest.mark.parametrize("d,ffn,E,T", [(512, 1024, 8, 1), (512, 1024, 8, 13), (4096, 14336, 8, 64),
-                                       (1024, 2048, 16, 100)])
+                                       (1024, 2048, 16, 100),
+                                       (4096, 14336, 8, 384)])  # prefill-sized: up to 768 rows
 def test_skinny_gemm_matches_dense(P, d, ffn, E, T):
     """Batched-decode GEMMs (weights as the M side, tokens as N) == the
     prefill GEMMs on the same permuted rows, bit for bit (the tensor cores
@@ -491,3 +492,16 @@ def test_skinny_gemm_matches_dense(P, d, ffn, E, T):
         n = int(pr["offsets"][-1])
         assert torch.equal(act2[:n], act[:n]), nt
         assert torch.equal(y2[:n], y[:n]), nt
+    # out=: rows of experts without a slot are left as they were
+    so_half = so.clone()
+    so_half[::2] = -1
+    keep = torch.full_like(act, 7)
+    ops.expert_gemm_up_skinny(pr["x_perm"], pr["offsets"], so_half, m.slab, m.n_slots,
+                              m.slot_elems, d, ffn, out=keep)
+    off = pr["offsets"].tolist()
+    for e in range(E):
+        blk = keep[off[e]:off[e + 1]]
+        if e % 2 == 0:
+            assert bool((blk == 7).all()), e
+        else:
+            assert torch.equal(blk, act[off[e]:off[e + 1]]), e
