@@ -505,3 +505,32 @@ def test_skinny_gemm_matches_dense(P, d, ffn, E, T):
             assert bool((blk == 7).all()), e
         else:
             assert torch.equal(blk, act[off[e]:off[e + 1]]), e
+
+
+@pytest.mark.parametrize("B", [16, 64, 256])
+def test_batched_decode_graph_replay_bitexact(P, B):
+    """The batched decode step (router, permutation, skinny GEMMs, combine)
+    captured as one CUDA graph -- as bench.py times it -- replays to the same
+    bits as the eager step, for fresh inputs copied into the captured buffer."""
+    pkg, model_mod, ops = P
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    d, ffn, E = 512, 1024, 8
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, 2), d, ffn, seed=12, resident_layers=[0])
+    eng = MoEBlockEngine(m)
+    h_in = m.input_hidden(B, stream=1)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        eng.prefill(h_in, 0)
+        with torch.cuda.graph(g):
+            r = eng.prefill(h_in, 0)
+    torch.cuda.current_stream().wait_stream(side)
+    for step in range(3):
+        h_new = m.input_hidden(B, stream=2, step=step)
+        want = eng.prefill(h_new, 0)
+        h_in.copy_(h_new)
+        g.replay()
+        torch.cuda.synchronize()
+        for key in ("out", "topk_idx", "topk_w", "p", "offsets"):
+            assert torch.equal(r[key], want[key]), (step, key)
