@@ -350,24 +350,28 @@ class DaopEngine:
 
     # ------------------------------------------------------------ decode
     def _host_views(self):
-        """Pinned mirrors of the decode buffers' decision prefix, one per
-        layer, with numpy views (one D2H copy per layer; a layer whose
-        decisions are read only at the end of the token keeps its own)."""
+        """Pinned mirrors of the decode buffers' decision prefix: one row per
+        layer of one pinned buffer (one D2H copy per layer), with per-layer
+        numpy views and whole-buffer (L, ...) views for reading every deferred
+        layer at once at the end of a token."""
         if getattr(self, "_mh", None) is None:
-            E, k, d = self.shape.num_experts, self.shape.top_k, self.model.d
-            self._mh = []
-            for l in range(self.shape.num_layers):
-                b = self.bufs[l % 2]
-                t = torch.empty(b.decisions_bytes, dtype=torch.uint8, pin_memory=True)
-                a = t.numpy()
-                o = b.offsets
-                v = {"x": a[o["x"]: o["x"] + 2 * d].view(np.uint16),
-                     "p": a[o["p"]: o["p"] + 4 * E].view(np.float32),
-                     "p_pred": a[o["p_pred"]: o["p_pred"] + 4 * E].view(np.float32),
-                     "deg": a[o["deg"]: o["deg"] + 4 * (2 * k + 1)].view(np.int32),
-                     "is_fast": a[o["is_fast"]: o["is_fast"] + k],
-                     "sel": a[o["sel"]: o["sel"] + 4 * k].view(np.int32)}
-                self._mh.append((t, v))
+            L, E, k, d = (self.shape.num_layers, self.shape.num_experts, self.shape.top_k,
+                          self.model.d)
+            b0 = self.bufs[0]
+            o = b0.offsets
+            self._mh_buf = torch.empty((L, b0.decisions_bytes), dtype=torch.uint8,
+                                       pin_memory=True)
+            big = self._mh_buf.numpy()
+
+            def fields(a):  # a: (..., decisions_bytes) uint8
+                return {"x": a[..., o["x"]: o["x"] + 2 * d].view(np.uint16),
+                        "p": a[..., o["p"]: o["p"] + 4 * E].view(np.float32),
+                        "p_pred": a[..., o["p_pred"]: o["p_pred"] + 4 * E].view(np.float32),
+                        "deg": a[..., o["deg"]: o["deg"] + 4 * (2 * k + 1)].view(np.int32),
+                        "is_fast": a[..., o["is_fast"]: o["is_fast"] + k],
+                        "sel": a[..., o["sel"]: o["sel"] + 4 * k].view(np.int32)}
+            self._mh = [(self._mh_buf[l], fields(big[l])) for l in range(L)]
+            self._mh_all = fields(big)
             self._y_host = torch.empty((k, d), dtype=torch.float32, pin_memory=True)
             self._h_pp = [torch.empty(d, dtype=torch.float32, device=self.model.device)
                           for _ in range(2)]
@@ -510,8 +514,14 @@ class DaopEngine:
                 h = b.h_out
             prev_b, prev_v = b, v
         torch.cuda.synchronize()
-        for l in deferred:
-            read(l, mh[l][1])
+        if deferred:  # every picked expert resident: no degradations to read
+            dl = np.asarray(deferred)
+            va = self._mh_all
+            sel[dl], fast[dl] = va["sel"][dl], va["is_fast"][dl]
+            nd[dl] = va["deg"][dl, 2 * k]
+            true_sc[dl] = va["p"][dl]
+            dp = dl[dl + 1 < L]
+            pred_sc[dp] = va["p_pred"][dp]
         h = h.clone()
         self.pos += 1
         plans = plans_from_arrays(sel, fast, drop, sub, nd, pred_sc, cfg)

@@ -145,31 +145,38 @@ class _NativePlanner:
         return plans_from_arrays(sel, fast, drop, sub, nd, pred, self.config)
 
 
+_EXECUTED = {}  # (expert, kind) -> ExecutedExpert; the values are frozen, so shared
+
+
+def _executed(e: int, kind: int) -> ExecutedExpert:
+    """kind 0: fast / current, 1: slow / stale / precalc, 2: slow / current."""
+    x = _EXECUTED.get((e, kind))
+    if x is None:
+        x = (ExecutedExpert(e, "fast", "current"), ExecutedExpert(e, "slow", "stale", precalc=True),
+             ExecutedExpert(e, "slow", "current"))[kind]
+        _EXECUTED[(e, kind)] = x
+    return x
+
+
 def plans_from_arrays(sel, fast, drop, sub, nd, pred_scores, config: PolicyConfig) -> list:
     """Build LayerPlans from the native planner's arrays (host or device).
 
     pred_scores (L, E): predictions carried on each layer (row l-1 scores the
-    degradation at layer l)."""
+    degradation at layer l).  Runs once per decode token, so the arrays are
+    read as Python lists and the (immutable) ExecutedExpert values are shared."""
     daop = config.engine == "daop"
     start = config.prediction_start_layer
+    sel_l, fast_l, nd_l = sel.tolist(), fast.tolist(), nd.tolist()
     plans = []
-    for l in range(sel.shape[0]):
-        precalc_layer = daop and l >= start
-        executed = []
-        for q in range(sel.shape[1]):
-            e = int(sel[l, q])
-            if fast[l, q]:
-                executed.append(ExecutedExpert(e, "fast", "current"))
-            elif precalc_layer:
-                executed.append(ExecutedExpert(e, "slow", "stale", precalc=True))
-            else:
-                executed.append(ExecutedExpert(e, "slow", "current"))
+    for l, (row, frow) in enumerate(zip(sel_l, fast_l)):
+        slow_kind = 1 if daop and l >= start else 2
+        executed = tuple(_executed(e, 0 if f else slow_kind) for e, f in zip(row, frow))
         deg = ()
-        if nd[l]:
+        if nd_l[l]:
             sc = pred_scores[l - 1]
             deg = tuple(Degradation(int(drop[l, i]), float(sc[drop[l, i]]), int(sub[l, i]),
-                                    float(sc[sub[l, i]])) for i in range(int(nd[l])))
-        plans.append(LayerPlan(layer=l, executed=tuple(executed), degraded=deg))
+                                    float(sc[sub[l, i]])) for i in range(nd_l[l]))
+        plans.append(LayerPlan(layer=l, executed=executed, degraded=deg))
     return plans
 
 
