@@ -37,7 +37,9 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
-SKINNY_MAX_ROWS = 256  # receive capacity up to which the skinny (batched-decode) GEMMs run
+# SKINNY_MAX_ROWS: receive capacity up to which the skinny (weights-as-M) GEMMs
+# run -- the single-GPU crossover (scripts/skinny_crossover.py)
+from .engine import SKINNY_MAX_ROWS
 
 
 def owner_of(expert: torch.Tensor, num_experts: int, world: int) -> torch.Tensor:
