@@ -24,18 +24,21 @@ def _calib(L, E, k, seed):
     return c
 
 
-@pytest.mark.parametrize("engine,ecr,start,attention", [
-    ("daop", 0.5, 4, False), ("daop", 0.25, 2, False), ("fiddler", 0.5, 4, False),
-    ("daop", 1.0, 4, False), ("ondemand", 0.5, 4, False), ("prefetch", 0.25, 2, False),
+@pytest.mark.parametrize("engine,ecr,start,attention,E,k", [
+    ("daop", 0.5, 4, False, 8, 2), ("daop", 0.25, 2, False, 8, 2),
+    ("fiddler", 0.5, 4, False, 8, 2), ("daop", 1.0, 4, False, 8, 2),
+    ("ondemand", 0.5, 4, False, 8, 2), ("prefetch", 0.25, 2, False, 8, 2),
     # full decoder layers: attention with a KV cache before every MoE block
-    ("daop", 0.5, 4, True), ("ondemand", 0.5, 4, True)])
-def test_daop_sequence_matches_reference_decisions(engine, ecr, start, attention):
+    ("daop", 0.5, 4, True, 8, 2), ("ondemand", 0.5, 4, True, 8, 2),
+    # the widest shape the decode kernel takes (E <= 16), top-4
+    ("daop", 0.5, 3, False, 16, 4)])
+def test_daop_sequence_matches_reference_decisions(engine, ecr, start, attention, E, k):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_2501_10375_b200 as P
     from paper_2501_10375_b200.daop import DaopEngine
 
-    L, E, k, d, ffn = 8, 8, 2, 256, 512
+    L, d, ffn = 8, 256, 512
     shape = P.ModelShape(L, E, k)
     calib = _calib(L, E, k, 5)
     cfg = P.PolicyConfig(engine, prediction_start_layer=start)
