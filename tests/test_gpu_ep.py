@@ -69,8 +69,8 @@ def test_peer_ep_world1_equals_single_gpu():
         assert ctx.local_offsets().tolist() == ref["offsets"].tolist()
 
 
-@pytest.mark.parametrize("G", [2, 4, 8])
-def test_peer_ep_emulated_ranks_equal_single_gpu(G):
+@pytest.mark.parametrize("G,E", [(2, 8), (4, 8), (8, 8), (4, 16), (8, 16)])
+def test_peer_ep_emulated_ranks_equal_single_gpu(G, E):
     """G ranks in one process on one GPU, each with its own workspace, its
     own E/G experts and its own tokens; the peer tables point at each
     other's workspaces, so dispatch (remote row stores), the expert-major
@@ -81,7 +81,7 @@ def test_peer_ep_emulated_ranks_equal_single_gpu(G):
         pytest.skip("needs a CUDA device")
     import paper_2501_10375_b200 as P
     from paper_2501_10375_b200.ep import PeerEP, ep_model
-    E, d, ffn = 8, 512, 1024
+    d, ffn = 512, 1024
     m, eng = _single_gpu_reference(P, E, d, ffn, 6)
     models = [ep_model(P.ModelShape(2, E, 2), d, ffn, r, G, seed=6) for r in range(G)]
     ranks = PeerEP.emulated(models, 0, t_cap=400)
