@@ -13,7 +13,8 @@ d, ffn, E, k = 4096, 14336, 8, 2
 m = MoEModel(P.ModelShape(2, E, k), d, ffn, seed=0, resident_layers=[0])
 eng = MoEBlockEngine(m)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for b in (1, 8, 16, 32, 64, 128, 256):
+sizes = [int(a) for a in sys.argv[1:]] or [1, 8, 16, 32, 64, 128, 256]
+for b in sizes:
     h = m.input_hidden(b, stream=9)
     for _ in range(3):
         r = eng.prefill(h, 0)
