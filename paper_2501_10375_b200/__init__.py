@@ -18,7 +18,8 @@ from .trace import (MIXTRAL_SHAPE, PHI_SHAPE, SCORE_SUM_TOL, ModelShape,
 from . import kernels as _kernels
 from .metrics import (ActivationMatrix, activation_matrix, expert_counts,
                       mean_prediction_accuracy, pooled_decode_probabilities,
-                      prediction_accuracy, routing_fidelity)
+                      prediction_accuracy, routing_fidelity, row_cosines,
+                      similarity)
 from .placement import (SWAP_IN_OUT_DEFAULT, ExpertPlacement, SwapEvent,
                         allocate_for_sequence, init_from_calibration,
                         slot_budget_for_ecr)
@@ -29,7 +30,9 @@ from .policies import (ENGINES, PREDICTION_START_LAYER_DEFAULT, DaopPlanner,
                        plan_token_daop, plan_token_fiddler, plan_token_ondemand,
                        plan_token_prefetch, plan_trace_decode)
 
-__version__ = "0.1.0"
+from .experiment import CSV_SCHEMA_VERSION, TimelineResult, run_single
+
+__version__ = "0.2.0"
 
 __all__ = [
     "BudgetError", "ConfigError", "DeviceError", "EmptyPhaseError",
@@ -46,5 +49,6 @@ __all__ = [
     "ExecutedExpert", "FiddlerPlanner", "LayerPlan", "PolicyConfig",
     "decode_counters", "degrade_selection", "make_planner", "plan_token_daop",
     "plan_token_fiddler", "plan_trace_decode", "OnDemandPlanner", "PrefetchPlanner",
-    "plan_token_ondemand", "plan_token_prefetch",
+    "plan_token_ondemand", "plan_token_prefetch", "row_cosines", "similarity",
+    "CSV_SCHEMA_VERSION", "TimelineResult", "run_single",
 ]

@@ -14,6 +14,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -356,14 +357,15 @@ class Pool {
   bool stop_ = false;
 };
 
+// one pool per thread count, created on first use and never destroyed: a
+// caller asking for another size can never free a pool another thread is
+// running on (pools are few -- one per distinct `threads` value)
 static Pool* pool_for(int threads) {
   static std::mutex m;
-  static Pool* p = nullptr;
+  static std::map<int, Pool*>* pools = new std::map<int, Pool*>();
   std::lock_guard<std::mutex> g(m);
-  if (!p || p->size() != threads) {
-    delete p;
-    p = new Pool(threads);
-  }
+  Pool*& p = (*pools)[threads];
+  if (!p) p = new Pool(threads);
   return p;
 }
 

@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(P_THREADS, 1)
       for (int w = 0; w < P_THREADS / 32; ++w) s += wtot[w][x];
       run[x] += s;
     }
+    __syncthreads();  // run[] complete before the next tile zeroes wtot / reads run
   }
 }
 

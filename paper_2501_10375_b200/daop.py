@@ -40,6 +40,7 @@ slow tier its inputs); the decision path is fully on device.
 from __future__ import annotations
 
 import os
+import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -143,12 +144,14 @@ class DaopEngine:
         self.config = config or PolicyConfig("daop")
         self.shape = shape
         self.placement0 = init_from_calibration(calib, ecr, shape)
+        self.ecr = ecr
         self.swap_in_out = swap_in_out
         self.weights_from_pred = weights_from_pred
         self.host_threads = host_threads
         self.host_ms = 0.0  # decode: wall time inside host-tier expert calls
         self.prefill_host_ms = 0.0  # prefill: the same for the slow experts' token batches
         self._host_exec = None  # one thread feeding the host tier (decode pre-calculation)
+        self._host_ms_lock = threading.Lock()
         self.model = MoEModel(shape, d_model, d_ff, seed=seed, device=device,
                               n_slots=self.placement0.slot_budget, resident_layers=[])
         self.pool = host_pool or HostExpertPool(shape, d_model, d_ff, seed)
@@ -234,8 +237,9 @@ class DaopEngine:
         T, d = h.shape
         t0 = time.perf_counter()
         hist = torch.zeros((1, L, E), dtype=torch.int32, device=m.device)
-        true_sc = np.zeros((T, L, E))
-        pred_sc = np.zeros((T, L, E))
+        # the exported trace's scores: async D2H into one pinned buffer per
+        # phase, read once after the last layer (no per-layer host sync)
+        p_host = torch.zeros((2, L, T, E), dtype=torch.float32, pin_memory=True)
         swaps_all = []
         new_sets = [set(s) for s in self.placement0.on_fast]
         slow_execs = 0
@@ -246,7 +250,9 @@ class DaopEngine:
             r = ops.router(h, m.norm[l], m.gate[l], nxt, k, hist=hist[:, l], tokens_per_seq=T,
                            hist_seq_stride=L * E)
             swapped_in, mig_evs = [], []
-            if self.config.engine == "daop":
+            # a layer whose every expert is cached has no uncached (hot)
+            # candidate, so Alg. 1 cannot swap there: no host round trip
+            if self.config.engine == "daop" and len(self.placement0.on_fast[l]) < E:
                 # only DAOP reallocates (experiment.py:158-163): Alg. 1 for this
                 # layer right after its gate (placement.py:188-237)
                 counts_l = hist[0, l].to(torch.int64).cpu().numpy()
@@ -261,9 +267,11 @@ class DaopEngine:
                     mig_start, mig_evs = self._apply_swaps(l, evs)
                     swapped_in = [e.swapped_in for e in evs]
             pr = ops.permute(r["topk_idx"], E, r["x"])
-            off = pr["offsets"].cpu().numpy()
             resident = m.resident_mask()[l]  # post-swap residence
-            slow = [e for e in range(E) if off[e + 1] > off[e] and not resident[e]]
+            slow = []
+            if not resident.all():  # only then does the host need the expert offsets
+                off = pr["offsets"].cpu().numpy()
+                slow = [e for e in range(E) if off[e + 1] > off[e] and not resident[e]]
             # slow experts' rows -> pinned host memory BEFORE the GEMMs are queued,
             # so the host tier runs while the GPU computes
             xs_host = {}
@@ -321,11 +329,13 @@ class DaopEngine:
                 if swapped_in:
                     mig_timing[-1][3] = hev
             out = ops.combine(h, y, pr["inv"], r["topk_w"])
-            true_sc[:, l, :] = r["p"].cpu().numpy()
+            p_host[0, l].copy_(r["p"], non_blocking=True)
             if nxt is not None:
-                pred_sc[:, l, :] = r["p_pred"].cpu().numpy()
+                p_host[1, l].copy_(r["p_pred"], non_blocking=True)
             h = out
         torch.cuda.synchronize()
+        true_sc = np.ascontiguousarray(p_host[0].numpy().transpose(1, 0, 2), dtype=np.float64)
+        pred_sc = np.ascontiguousarray(p_host[1].numpy().transpose(1, 0, 2), dtype=np.float64)
         self.placement = ExpertPlacement(self.shape, new_sets, self.placement0.slot_budget)
         self.pos = T  # the first decode token's position
         if self.config.engine in ("ondemand", "prefetch"):
@@ -453,7 +463,8 @@ class DaopEngine:
         def host_job(l, e, xs):  # one slow expert on the host tier (GIL released)
             th0 = time.perf_counter()
             y = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
-            self.host_ms += 1e3 * (time.perf_counter() - th0)
+            with self._host_ms_lock:
+                self.host_ms += 1e3 * (time.perf_counter() - th0)
             return y
 
         def queue_precalc(l, pv):  # DAOP plan of l from layer l-1's mirror pv
@@ -491,18 +502,21 @@ class DaopEngine:
                 if s_l.tolist() != hs.tolist() or f_l.tolist() != hf.tolist():
                     raise ShapeMismatchError(f"layer {l}: host plan differs from the device plan")
             read(l, v)
+            futs = dict(queued[l][2]) if plan_on_host else {}
+            if mode == 0 and not f_l.all():
+                # Fiddler rule: current x_l, after the router -- on the host
+                # tier's queue AHEAD of layer l+1's pre-calculation
+                xs = v["x"][None, :].copy()
+                for q in range(k):
+                    if not f_l[q]:
+                        futs[q] = self._host_exec.submit(host_job, l, int(s_l[q]), xs)
             # layer l+1's plan and stale input are known now: queue its
             # pre-calculation behind this layer's, so the host tier runs back to
             # back while this thread combines and launches
             if daop and start <= l + 1 < L and not full[l + 1]:
                 queue_precalc(l + 1, v)
-            ys = {q: f.result() for q, f in queued[l][2].items()} if plan_on_host else {}
+            ys = {q: f.result() for q, f in futs.items()}
             if not f_l.all():
-                if mode == 0:  # Fiddler rule: current x_l, after the router
-                    xs = v["x"][None, :]
-                    for q in range(k):
-                        if not f_l[q]:
-                            ys[q] = host_job(l, int(s_l[q]), xs)
                 for q, yq in ys.items():
                     self._y_host[q].copy_(torch.from_numpy(yq[0]))
                     b.y[q].copy_(self._y_host[q], non_blocking=True)
@@ -605,3 +619,32 @@ class DaopEngine:
         rec.counts = decode_counters([r.plans for r in rec.decode], self.config)
         rec.tokens_per_second = 1e3 * n / lat if lat > 0 else float("nan")
         return rec
+
+    def run_single(self, h_prompt: torch.Tensor, decode_inputs, sequence_id: str = "seq",
+                   seed: int = 0) -> dict:
+        """experiment.run_single (moesim/experiment.py:145-211) EXECUTED:
+        prefill + decode of one sequence on the B200, returned as the
+        reference's flat run record.  Decision fields (placements, swaps,
+        counters, set_fidelity, score_mass, similarity_prefill_decode,
+        swap_count) come from the kernels' own decisions; the timing fields
+        are measured (per-token wall latency, tokens/s, prefill latency,
+        hidden migration time).  Extra keys: ``_trace`` (the exported
+        RoutingTrace: re-running the reference's run_single on it with the
+        same calibration reproduces every decision field), ``_sequence``."""
+        from .experiment import make_record
+        rec = self.run_sequence(h_prompt, decode_inputs, sequence_id)
+        pre = rec.prefill
+        lat = [d.ms for d in rec.decode]
+        total = pre.ms + sum(lat)
+        out = make_record(rec.trace, self.ecr, self.config.engine, seed, pre.placement_initial,
+                          pre.placement, pre.swaps, [d.plans for d in rec.decode], self.config,
+                          per_token_latency_ms=lat, prefill_latency_ms=pre.ms,
+                          prefill_hidden_migration_ms=pre.migration_hidden_ms,
+                          busy_fraction={"host_tier": (self.host_ms / sum(lat)) if lat else 0.0,
+                                         "host_tier_prefill": (self.prefill_host_ms / total)
+                                         if total else 0.0})
+        out["_prefill_result"] = pre
+        out["_trace"] = rec.trace
+        out["_sequence"] = rec
+        return out
+

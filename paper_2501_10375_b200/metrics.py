@@ -123,3 +123,31 @@ def pooled_decode_probabilities(traces) -> np.ndarray:
     if tokens == 0:
         raise ConfigError("calibration traces contain no decode tokens")
     return total / tokens
+
+
+def _as_matrix(m) -> np.ndarray:
+    if isinstance(m, ActivationMatrix):
+        return m.values
+    arr = np.asarray(m, dtype=np.float64)
+    if arr.ndim != 2:
+        raise ShapeMismatchError("similarity expects 2-D matrices")
+    return arr
+
+
+def row_cosines(p, d) -> tuple:
+    """Per-layer cosine of two L x E matrices plus the degenerate-row mask
+    (moesim/metrics.py:94-111): a zero row on either side scores 0."""
+    pv, dv = _as_matrix(p), _as_matrix(d)
+    if pv.shape != dv.shape:
+        raise ShapeMismatchError(f"matrix dimensions differ: {pv.shape} vs {dv.shape}")
+    num = (pv * dv).sum(axis=1)
+    n_p, n_d = np.linalg.norm(pv, axis=1), np.linalg.norm(dv, axis=1)
+    degenerate = (n_p == 0.0) | (n_d == 0.0)
+    cows = np.where(degenerate, 0.0, num / np.where(degenerate, 1.0, n_p * n_d))
+    return cows, degenerate
+
+
+def similarity(p, d) -> float:
+    """Eq. 1 of the paper: mean over layers of the row cosines
+    (moesim/metrics.py:114-117)."""
+    return float(row_cosines(p, d)[0].mean())

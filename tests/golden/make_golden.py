@@ -275,7 +275,38 @@ def main():
                     "counts": {k2: int(v) for k2, v in dec.counts.items()},
                     "executed": [[list(map(int, ex)) for ex in tok] for tok in dec.executed],
                     "set_fidelity": rec["set_fidelity"],
+                    # the rest of the flat record's decision fields (experiment.py:178-210)
+                    "record": {key: rec[key] for key in (
+                        "schema_version", "trace_id", "ecr", "engine", "seed",
+                        "num_prefill_tokens", "num_decode_tokens", "migrations", "prefetches",
+                        "wasted_prefetches", "slow_executions", "degradations", "stale_inputs",
+                        "set_fidelity", "score_mass", "swap_count",
+                        "similarity_prefill_decode")},
                 })
+        if shape.num_layers == 8:
+            # calibration + fidelity metrics (experiment.py:132-142,
+            # metrics.py:74-82,114-117,177-215) on the same traces
+            from moesim import activation_matrix, routing_fidelity, similarity
+            rng = np.random.default_rng(5)
+            execs = []
+            for _ in range(3):  # random executed sets (k distinct experts per layer)
+                execs.append([[sorted(rng.choice(shape.num_experts, shape.top_k,
+                                                 replace=False).tolist())
+                               for _ in range(shape.num_layers)]
+                              for _ in range(trace.num_decode_tokens)])
+            g["metrics"] = {
+                "shape": [shape.num_layers, shape.num_experts, shape.top_k],
+                "calib_decode_true": [t.decode_true.tolist() for t in calib_traces],
+                "calib_prefill_true": [t.prefill_true.tolist() for t in calib_traces],
+                "pooled_decode_probabilities": calib.tolist(),
+                "trace": len(traces) - 1,
+                "activation_prefill": activation_matrix(trace, "prefill").values.tolist(),
+                "activation_decode": activation_matrix(trace, "decode").values.tolist(),
+                "similarity": similarity(activation_matrix(trace, "prefill"),
+                                         activation_matrix(trace, "decode")),
+                "executed": execs,
+                "routing_fidelity": [list(routing_fidelity(trace, ex)) for ex in execs],
+            }
     g["run_single"] = {"traces": traces, "cases": cases}
 
     OUT.write_text(json.dumps(g, separators=(",", ":")))
