@@ -135,7 +135,7 @@ def ncu_traffic():
 
 def cpu_decode_layer():
     from oracle.baseline import CpuMoELayer
-    return CpuMoELayer(2, E, K, D, FFN, seed=0, layer=0)
+    return CpuMoELayer(2, E, K, D, FFN, seed=0, layer=0, with_bf16=True)
 
 
 def cpu_inputs(n, rank=0):
@@ -143,29 +143,77 @@ def cpu_inputs(n, rank=0):
     return [N.input_hidden(0, 100 + rank, i, 1, D)[0] for i in range(n)]
 
 
+def cpu_arm(layer, xs, steps, warmup, budget_s, fns=None, tokens_per_step=1,
+            what="decode tokens through one Mixtral-8x7B layer"):
+    """Time the CPU path: the faster of the oracle's numpy fp32 restatement and
+    the torch-CPU bf16 (oneDNN, fp32 accumulation) deployment of the same
+    block, each on all host cores (decided on 2 calibration steps); both
+    numbers are reported."""
+    from oracle.baseline import blas_threads, cpu_model, time_steps
+    cand = fns or {"numpy_f32": layer.decode_step, "torch_bf16": layer.decode_step_bf16}
+    probe = {}
+    for name, fn in cand.items():
+        n, sec = time_steps(fn, xs, budget_s=5.0, max_steps=2, warmup=1)
+        probe[name] = tokens_per_step * n / sec
+    best = max(probe, key=probe.get)
+    n, sec = time_steps(cand[best], xs, budget_s=budget_s, max_steps=steps, warmup=warmup)
+    desc = {"numpy_f32": "oracle numpy fp32 on bf16-valued weights",
+            "torch_bf16": "torch-CPU bf16 weights/activations, oneDNN fp32 accumulation"}[best]
+    return {"value": tokens_per_step * n / sec, "unit": "tokens/s", "cores": blas_threads(),
+            "kind": "port", "cpu_model": cpu_model(), "variant": best,
+            "variants_tok_s": {k: round(v, 2) for k, v in probe.items()},
+            "sample": f"{n} steps of {tokens_per_step} x {what} ({desc}, {sec:.1f} s)",
+            "steps": n, "seconds": sec}
+
+
+def workload_config(world):
+    """The config dict both arms print (same workload, same keys)."""
+    if world > 1:
+        return {"workload": f"Mixtral-8x22B-shaped MoE layer (d={EP_D}, ffn={EP_FFN}, E={E}, "
+                            f"top-{K}), prefill {EP_TOKENS} tokens sharded over {world} GPUs, "
+                            f"expert-parallel (BASELINE configs[4])",
+                "d_model": EP_D, "d_ff": EP_FFN, "experts": E, "top_k": K,
+                "global_batch": EP_TOKENS, "parallelism": f"ep{world}",
+                "l2": "inputs larger than L2 (4.8 GB of experts per layer)"}
+    return {"workload": "decode b=1, one Mixtral-8x7B MoE layer (BASELINE configs[1])",
+            "d_model": D, "d_ff": FFN, "experts": E, "top_k": K, "global_batch": 1,
+            "parallelism": "single",
+            "l2": "inputs larger than L2 (2.8 GB of experts, 704.8 MB streamed per step)"}
+
+
 def run_reference(args, world, rank):
-    import numpy as np  # noqa: F401
-    from oracle.baseline import blas_threads, time_steps
     if rank != 0:
         return None
-    layer = cpu_decode_layer()
-    xs = cpu_inputs(16)
-    warm = max(1, min(args.warmup, 3))
-    n, sec = time_steps(layer.decode_step, xs, budget_s=60.0, max_steps=args.steps, warmup=warm)
-    v = n / sec
-    cores = blas_threads()
+    if world > 1:
+        # our arm's N > 1 workload: the Mixtral-8x22B layer's prefill; the CPU
+        # runs a bounded sample of it (64 prompt tokens per step)
+        from oracle.baseline import CpuMoELayer
+        from oracle import numerics as N
+        layer = CpuMoELayer(2, E, K, EP_D, EP_FFN, seed=0, layer=0, with_bf16=True)
+        xs = [N.input_hidden(0, 300, i, 64, EP_D) for i in range(2)]
+        cb = cpu_arm(layer, xs, steps=args.steps, warmup=args.warmup, budget_s=90.0,
+                     fns={"numpy_f32": layer.prefill, "torch_bf16": layer.prefill_bf16},
+                     tokens_per_step=64, what="64 prompt tokens through one Mixtral-8x22B layer")
+    else:
+        layer = cpu_decode_layer()
+        xs = cpu_inputs(16)
+        cb = cpu_arm(layer, xs, steps=args.steps, warmup=args.warmup, budget_s=60.0)
+    v = cb["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
-        "n_gpus": world, "steps": n, "warmup": warm, "ms_per_step": 1e3 * sec / n,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "n_gpus": world, "steps": cb["steps"], "warmup": args.warmup,
+        "ms_per_step": 1e3 * cb["seconds"] / cb["steps"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if cb["variant"] == "torch_bf16" else "f32",
         "data": "synthetic (counter-RNG random-init weights and tokens)",
-        "config": {"workload": "decode b=1, one Mixtral-8x7B MoE layer (BASELINE configs[1])",
-                   "d_model": D, "d_ff": FFN, "experts": E, "top_k": K,
-                   "parallelism": "replicas" if world > 1 else "single"},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} decode tokens through one layer (oracle numpy, fp32)"},
+        "config": workload_config(world),
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "cpu_model",
+                                              "variant", "variants_tok_s", "sample")},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if world > 1:
+        line["scaling"] = "strong"
+        line["note"] = "rank 0 alone runs the host CPU path; the other ranks exit without work"
     return line
 
 
@@ -196,6 +244,13 @@ def run_b200(args, world, rank, local_rank):
     def barrier():
         if world > 1:
             dist.barrier()
+
+    # decisions of the first tokens, for the free-running routing agreement
+    # the cpu_baseline leg reports (untimed)
+    dec_sel = []
+    for i in range(n_in):
+        dec_sel.append(eng.decode(hs[i]).sel.clone())
+    dec_sel = torch.stack(dec_sel).cpu().numpy()
 
     # -------- device-resident timed loop (value)
     for i in range(args.warmup):
@@ -236,12 +291,19 @@ def run_b200(args, world, rank, local_rank):
 
     # -------- prefill (BASELINE configs[3]: 8 x 4096 tokens)
     prefill = None
+    pf_sample = None
     if not args.no_prefill:
         T = PREFILL_SEQS * PREFILL_LEN
         hp = model.input_hidden(T, stream=200 + rank)
         hist = torch.zeros((PREFILL_SEQS, n_layers, E), dtype=torch.int32, device=dev)
         for _ in range(2):
-            eng.prefill(hp, 0, hist=hist[:, 0], tokens_per_seq=PREFILL_LEN, hist_seq_stride=n_layers * E)
+            rp = eng.prefill(hp, 0, hist=hist[:, 0], tokens_per_seq=PREFILL_LEN,
+                             hist_seq_stride=n_layers * E)
+        # one sequence's routing, for the free-running agreement (untimed)
+        pf_sample = {"h": hp[:PREFILL_LEN].cpu().numpy(),
+                     "sel": rp["topk_idx"][:PREFILL_LEN].cpu().numpy(),
+                     "x": rp["x"][:PREFILL_LEN].float().cpu().numpy()}
+        del rp
         barrier()
         torch.cuda.synchronize()
         kp = max(3, min(10, args.steps // 200))
@@ -449,16 +511,25 @@ def run_b200(args, world, rank, local_rank):
         if isinstance(ep, dict):
             ep["decode_b64"] = ep_b64
 
-    # -------- CPU baseline (rank 0, N = 1 only)
+    # -------- DAOP at ECR < 1 (BASELINE configs[2]): 32 layers, slow tier on the host
+    daop = None
+    if not args.no_daop:
+        try:
+            daop = run_daop(args, dev, rank)
+        except Exception as exc:
+            daop = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        torch.cuda.empty_cache()
+
+    # -------- CPU baseline (rank 0, N = 1 only) + free-running routing agreement
     cpu = None
+    agreement = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle.baseline import blas_threads, time_steps
         layer = cpu_decode_layer()
         xs = cpu_inputs(16)
-        n, sec = time_steps(layer.decode_step, xs, budget_s=20.0, max_steps=200, warmup=1)
-        cpu = {"value": n / sec, "unit": "tokens/s", "cores": blas_threads(), "kind": "port",
-               "sample": f"{n} decode tokens through one Mixtral-8x7B layer "
-                         f"(oracle numpy fp32, {sec:.1f} s)"}
+        cpu = cpu_arm(layer, xs, steps=200, warmup=1, budget_s=20.0)
+        for key in ("steps", "seconds"):
+            cpu.pop(key)
+        agreement = routing_agreement(layer, [h.cpu().numpy() for h in hs], dec_sel, pf_sample)
         del layer
 
     if rank != 0:
@@ -472,10 +543,7 @@ def run_b200(args, world, rank, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (counter-RNG random-init weights and tokens)",
-        "config": {"workload": "decode b=1, one Mixtral-8x7B MoE layer (BASELINE configs[1])",
-                   "d_model": D, "d_ff": FFN, "experts": E, "top_k": K, "global_batch": world,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (2.8 GB of experts, 704.8 MB streamed per step)"},
+        "config": workload_config(1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": ncu_traffic(),
                      "peak_kind": peak_kind, "bytes_per_launch": DECODE_BYTES,
@@ -495,8 +563,140 @@ def run_b200(args, world, rank, local_rank):
         "decode32": decode32,
         "decoder32": decoder32,
         "ep": ep,
+        "daop": daop,
+        "routing_agreement": agreement,
     }
+    line["summary"] = summarize(line)  # last key: survives a truncated stdout tail
     return line
+
+
+def _g(d, *path):
+    for p in path:
+        if not isinstance(d, dict) or p not in d:
+            return None
+        d = d[p]
+    return round(d, 4) if isinstance(d, float) else d
+
+
+def summarize(line):
+    """Compact copy of every section's headline number."""
+    dr = _g(line, "daop", "runs") or []
+    return {
+        "decode_tok_s": _g(line, "value"), "decode_frac": _g(line, "roofline", "frac"),
+        "e2e_tok_s": _g(line, "e2e", "value"), "cpu_tok_s": _g(line, "cpu_baseline", "value"),
+        "prefill_ms_layer": _g(line, "prefill", "ms_per_layer"),
+        "prefill_frac_sustained": _g(line, "prefill", "roofline", "frac"),
+        "prefill_frac_burst": _g(line, "prefill", "roofline", "frac_of_burst"),
+        "decode_b64_ms": _g(line, "decode_b64", "ms_per_step"),
+        "decode_b64_frac": _g(line, "decode_b64", "roofline", "frac"),
+        "decode32_tok_s": _g(line, "decode32", "value"),
+        "decode32_frac": _g(line, "decode32", "roofline", "frac"),
+        "decoder32_tok_s": _g(line, "decoder32", "value"),
+        "decoder32_frac": _g(line, "decoder32", "roofline", "frac"),
+        "ep_prefill_ms": _g(line, "ep", "ms_per_layer"),
+        "ep_prefill_frac": _g(line, "ep", "roofline", "frac"),
+        "ep_decode_b64_ms": _g(line, "ep", "decode_b64", "ms_per_step"),
+        "ep_decode_b1_ms": _g(line, "ep", "decode", "ms_per_step"),
+        "daop": [{"ecr": r.get("ecr"), "tok_s": _g(r, "tokens_per_second"),
+                  "slow_per_tok": _g(r, "slow_executions_per_token"),
+                  "prefill_ms": _g(r, "prefill_latency_ms")} for r in dr],
+        "routing_agreement": {k: _g(line, "routing_agreement", k, "agree_frac")
+                              for k in ("decode", "prefill")},
+    }
+
+
+def routing_agreement(layer, hs, dec_sel, pf_sample):
+    """Free-running routing of the GPU vs the CPU oracle on the same h
+    (moesim/_kernels.py:63-79 tie rule): the oracle computes x = RMSNorm(h),
+    p and top-k from h alone.  Disagreeing rows are reported, split into
+    near ties (oracle top-(k+1) gap < 1e-5) and the rest (should be 0)."""
+    import numpy as np
+    from oracle import decisions as Dd
+    from oracle import numerics as N
+
+    def rows(h, sel_gpu, x_gpu=None):
+        x = N.rmsnorm(h, layer.norm)
+        p, _ = N.router(x, layer.gate, layer.gate_next)
+        sel = Dd.topk_rows(p.astype(np.float64), K)
+        srt = -np.sort(-p.astype(np.float64), axis=1)[:, : K + 1]
+        gap = np.min(srt[:, :-1] - srt[:, 1:], axis=1)
+        diff = np.any(sel != sel_gpu, axis=1)
+        out = {"rows": int(len(diff)), "agree_frac": float(1.0 - diff.mean()),
+               "near_tie_exempt": int((diff & (gap < 1e-5)).sum()),
+               "mismatch_non_tie": int((diff & (gap >= 1e-5)).sum())}
+        if x_gpu is not None:
+            out["x_bits_equal_frac"] = float((x_gpu == x).mean())
+        return out
+
+    res = {"decode": rows(np.stack(hs), dec_sel.astype(np.int64))}
+    if pf_sample is not None:
+        res["prefill"] = rows(pf_sample["h"], pf_sample["sel"].astype(np.int64), pf_sample["x"])
+    return res
+
+
+def run_daop(args, dev, rank):
+    """BASELINE configs[2]: Mixtral-8x7B-shaped 32-layer DAOP sequence at ECR
+    < 1 (default 0.5): calibration sequence at ECR 1.0 -> init_from_calibration
+    -> 256-token prefill (device activation counter, Alg. 1 swaps as pinned-host
+    -> HBM copies on a side stream, slow experts on the host tier) -> decode
+    tokens with DAOP plans, graceful degradation and the stale-input
+    pre-calculation on the host tier.  Returned as the reference's run_single
+    record (moesim/experiment.py:178-210), timings measured."""
+    import numpy as np
+    import torch
+
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.daop import DaopEngine, HostExpertPool
+
+    if rank != 0 and not args.daop_all_ranks:
+        return None
+    L, n_pre, n_dec = 32, 256, args.daop_tokens
+    shape = P.ModelShape(L, E, K)
+    t0 = time.perf_counter()
+    pool = HostExpertPool(shape, D, FFN, seed=0, device=dev)
+    setup_s = time.perf_counter() - t0
+    cal = DaopEngine(shape, D, FFN, np.full((L, E), K / E), 1.0, P.PolicyConfig("daop"), seed=0,
+                     host_pool=pool)
+    crec = cal.run_sequence(cal.model.input_hidden(64, stream=300),
+                            [cal.model.input_hidden(1, stream=301, step=i)[0] for i in range(16)],
+                            "calib")
+    calib = P.pooled_decode_probabilities([crec.trace])
+    del cal, crec
+    torch.cuda.empty_cache()
+    runs = []
+    for ecr in args.daop_ecr:
+        # the calibration run above already loaded every kernel in this process
+        eng_run = DaopEngine(shape, D, FFN, calib, ecr, P.PolicyConfig("daop"), seed=0,
+                             host_pool=pool)
+        prompt = eng_run.model.input_hidden(n_pre, stream=400)
+        toks = [eng_run.model.input_hidden(1, stream=401, step=i)[0] for i in range(n_dec)]
+        torch.cuda.synchronize()
+        rec = eng_run.run_single(prompt, toks, f"daop_ecr{ecr}")
+        n = rec["num_decode_tokens"]
+        runs.append({
+            "ecr": ecr, "slot_budget": eng_run.placement0.slot_budget,
+            "tokens_per_second": rec["tokens_per_second"],
+            "mean_token_latency_ms": rec["mean_token_latency_ms"],
+            "prefill_latency_ms": rec["prefill_latency_ms"],
+            "prefill_hidden_migration_ms": rec["prefill_hidden_migration_ms"],
+            "swap_count": rec["swap_count"],
+            "slow_executions_per_token": rec["slow_executions"] / n,
+            "degradations_per_token": rec["degradations"] / n,
+            "stale_inputs_per_token": rec["stale_inputs"] / n,
+            "host_tier_ms_per_token": eng_run.host_ms / n,
+            "set_fidelity": rec["set_fidelity"], "score_mass": rec["score_mass"],
+            "similarity_prefill_decode": rec["similarity_prefill_decode"],
+            "prediction_accuracy": P.mean_prediction_accuracy(rec["_trace"]),
+        })
+        del eng_run, rec
+        torch.cuda.empty_cache()
+    del pool
+    return {"workload": f"32 Mixtral-8x7B MoE layers, {n_pre}-token prompt + {n_dec} decode "
+                        f"tokens per ECR, DAOP (prediction from layer 4, graceful degradation), "
+                        f"slow experts on the host tier (BASELINE configs[2]); the reference's "
+                        f"run_single record, timings measured",
+            "host_pool_gb": L * E * 3 * D * FFN * 2 / 1e9, "host_pool_setup_s": setup_s,
+            "runs": runs}
 
 
 DEC_CTX = 512  # context position of the decoder32 measurement
@@ -559,7 +759,8 @@ def run_decoder32(args, world, dev, eng, model, hs, hbm_peak, barrier):
 EP_D, EP_FFN, EP_TOKENS = 6144, 16384, 8 * 4096
 
 
-def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", tokens=None, hbm_peak=None):
+def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", tokens=None, hbm_peak=None,
+           steps=None, warmup=2, e2e=False):
     """Mixtral-8x22B-shaped MoE layer (d=6144, ffn=16384, E=8, top-2),
     prefill 8 x 4096 tokens sharded T/G per rank, experts sharded E/G per
     rank, expert-parallel over the ranks.  Total work is fixed as G grows
@@ -592,19 +793,50 @@ def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", tokens=None, hb
     else:
         def step(record=False):
             return gpu_ep_layer(m, 0, h, timings=phases if record else None)[:3]
-    for _ in range(2):
+    for _ in range(warmup):
         step()
     barrier()
     torch.cuda.synchronize()
-    kp = 5 if tokens is None else 50
+    kp = steps or (5 if tokens is None else 50)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(kp):
-        step(record=i == kp - 1)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(dev.index or 0) as clk:
+        e0.record(stream)
+        for i in range(kp):
+            step(record=i == kp - 1)
+        e1.record(stream)
+        torch.cuda.synchronize()
     barrier()
+    e2e_res = None
+    if e2e and impl == "peer":
+        # the same layer through the public call with HOST buffers: this rank's
+        # tokens copied in from pinned memory and the output copied back, every step
+        h_host = torch.empty(h.shape, dtype=h.dtype, pin_memory=True)
+        h_host.copy_(h)
+        o_host = torch.empty(h.shape, dtype=torch.float32, pin_memory=True)
+        h_dev = torch.empty_like(h)
+        for _ in range(warmup):
+            h_dev.copy_(h_host, non_blocking=True)
+            o_host.copy_(ctx.layer(h_dev)[0], non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        q0.record(stream)
+        for _ in range(kp):
+            h_dev.copy_(h_host, non_blocking=True)
+            o_host.copy_(ctx.layer(h_dev)[0], non_blocking=True)
+        q1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        te = torch.tensor([max(q0.elapsed_time(q1) / 1e3, wall)], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_res = {"value": total * kp / float(te.item()), "unit": "tokens/s",
+                   "h2d_bytes_per_step": int(h.numel() * 4), "d2h_bytes_per_step": int(h.numel() * 4),
+                   "api": "PeerEP.layer with this rank's tokens from pinned host memory, output "
+                          "copied back every step"}
+        barrier()
     if impl == "peer":
         ctx.check()
         off = ctx._cur["offsets"].tolist()
@@ -661,6 +893,10 @@ def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", tokens=None, hb
                      "frac": flops / world / (ms / 1e3) / 1e12 / tf_sus,
                      "flops_per_layer": flops},
     }
+    out["steps"] = kp
+    out["clocks"] = clk.summary()
+    if e2e_res:
+        out["e2e"] = e2e_res
     if split:
         out["rank0_phase_ms"] = split
     if impl == "peer":
@@ -669,6 +905,67 @@ def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", tokens=None, hb
     del m
     torch.cuda.empty_cache()
     return out
+
+
+def run_b200_ep(args, world, rank, local_rank):
+    """--gpus N > 1: the headline is expert parallelism (BASELINE configs[4]):
+    one Mixtral-8x22B-shaped layer, a prefill of 8 x 4096 tokens sharded
+    T/N per rank, experts sharded E/N per rank, the product peer-memory path
+    (ep.PeerEP: dispatch = permutation gather with NVLink stores, return fused
+    into the down-GEMM epilogue).  value = whole-job tokens/s over the max
+    rank time of exactly K steps; e2e = the same call with host buffers.
+    The NCCL-collective path and the EP decode steps are reported beside it."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    hbm_peak, tf_peak, tf_sus, peak_kind = peaks()
+
+    def barrier():
+        dist.barrier()
+
+    head = run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", steps=args.steps,
+                  warmup=args.warmup, e2e=True)
+    try:
+        nccl = run_ep(args, world, rank, dev, tf_sus, barrier, impl="nccl")
+    except Exception as exc:
+        nccl = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    try:
+        dec = run_ep_decode(args, world, rank, dev, hbm_peak, barrier)
+    except Exception as exc:
+        dec = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    try:
+        b64 = run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", tokens=64,
+                     hbm_peak=hbm_peak)
+    except Exception as exc:
+        b64 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    if rank != 0:
+        return None
+    ms = head["ms_per_layer"]
+    line = {
+        "metric": METRIC, "value": head["value"], "unit": "tokens/s", "n_gpus": world,
+        "steps": head["steps"], "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (counter-RNG random-init weights and tokens)",
+        "config": workload_config(world),
+        "roofline": {"bound": "tensor", "achieved": head["roofline"]["achieved_per_gpu"],
+                     "peak": tf_sus, "unit": "TFLOP/s", "frac": head["roofline"]["frac"],
+                     "peak_kind": f"{peak_kind} sustained", "traffic": None,
+                     "flops_per_launch": head["roofline"]["flops_per_layer"] / world},
+        "cpu_baseline": None,
+        "e2e": head.get("e2e"),
+        "gpu_launches": head["gpu_launches_per_layer"] * head["steps"],
+        "clocks": head.get("clocks"),
+        "ep": {"peer": head, "nccl_baseline": nccl, "decode": dec, "decode_b64": b64},
+    }
+    line["summary"] = {"ep_prefill_tok_s": _g(head, "value"), "ep_prefill_ms": _g(head, "ms_per_layer"),
+                       "ep_prefill_frac": _g(head, "roofline", "frac"),
+                       "nccl_prefill_ms": _g(nccl, "ms_per_layer"),
+                       "ep_decode_b1_ms": _g(dec, "ms_per_step"),
+                       "ep_decode_b64_ms": _g(b64, "ms_per_step"),
+                       "e2e_tok_s": _g(head, "e2e", "value")}
+    return line
 
 
 def run_ep_decode(args, world, rank, dev, hbm_peak, barrier):
@@ -763,6 +1060,10 @@ def main():
     ap.add_argument("--no-decode32", action="store_true")
     ap.add_argument("--no-ep", action="store_true")
     ap.add_argument("--no-server", action="store_true")
+    ap.add_argument("--no-daop", action="store_true")
+    ap.add_argument("--daop-ecr", type=float, nargs="+", default=[0.5])
+    ap.add_argument("--daop-tokens", type=int, default=16)
+    ap.add_argument("--daop-all-ranks", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -776,7 +1077,7 @@ def main():
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        line = run_b200(args, world, rank, local_rank)
+        line = (run_b200_ep if world > 1 else run_b200)(args, world, rank, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

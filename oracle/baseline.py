@@ -1,11 +1,16 @@
 """Oracle (TEST / BASELINE INFRASTRUCTURE ONLY): the CPU path timed beside the
 GPU in bench.py (`cpu_baseline` and `--impl reference`).
 
-It executes the MoE block exactly as restated in oracle/numerics.py and the
-decisions exactly as restated in oracle/decisions.py (the reference's own
-algorithm, pinned to its golden vectors) -- numpy, fp32 arithmetic on
-bf16-valued weights, all host cores through the BLAS thread pool.  Weights
-come from the oracle generator (oracle/rng.py), generated in parallel threads
+`CpuMoELayer` executes the MoE block exactly as restated in
+oracle/numerics.py and the decisions exactly as restated in
+oracle/decisions.py (the reference's own algorithm, pinned to its golden
+vectors) -- numpy, fp32 arithmetic on bf16-valued weights, all host cores
+through the BLAS thread pool.  `CpuMoELayerBf16` is the same block the way a
+CPU deployment would run it: bf16 weights and activations
+through torch-CPU (oneDNN, fp32 accumulation, AVX-512 BF16 where the host
+has it), all host cores -- half the weight bytes of the fp32 port, so it is
+the faster, fairer CPU baseline and the one bench.py reports.  Weights come
+from the oracle generator (oracle/rng.py), generated in parallel threads
 (numpy releases the GIL), so nothing from the product package is used.
 """
 
@@ -33,19 +38,70 @@ def blas_threads() -> int:
 
 
 class CpuMoELayer:
-    """One MoE layer (all experts) on the host, weights as fp32 arrays."""
+    """One MoE layer (all experts) on the host, weights as fp32 arrays (and,
+    with_bf16, as torch bf16 tensors for the bf16 variant)."""
 
-    def __init__(self, num_layers, num_experts, top_k, d, ffn, seed=0, layer=0, threads=None):
+    def __init__(self, num_layers, num_experts, top_k, d, ffn, seed=0, layer=0, threads=None,
+                 with_bf16=False):
         self.om = N.OracleModel(num_layers, num_experts, top_k, d, ffn, seed)
-        self.layer, self.E, self.k = layer, num_experts, top_k
+        self.layer, self.E, self.k, self.d, self.ffn = layer, num_experts, top_k, d, ffn
+        self.threads = threads or len(os.sched_getaffinity(0))
         jobs = [(e, m) for e in range(num_experts) for m in range(3)]
         fns = {0: self.om.w1, 1: self.om.w3, 2: self.om.w2}
-        with ThreadPoolExecutor(threads or len(os.sched_getaffinity(0))) as ex:
+        with ThreadPoolExecutor(self.threads) as ex:
             mats = list(ex.map(lambda em: fns[em[1]](layer, em[0]), jobs))
         self.w = {(e, m): mats[i] for i, (e, m) in enumerate(jobs)}
         self.gate = self.om.gate(layer)
         self.gate_next = self.om.gate(layer + 1) if layer + 1 < num_layers else None
         self.norm = self.om.norm(layer)
+        self.torch = None
+        if with_bf16:
+            import torch
+            torch.set_num_threads(self.threads)
+            self.torch = torch
+            # the weights are bf16-valued, so the conversion is exact
+            self.w13 = [torch.cat([torch.from_numpy(self.w[(e, 0)]),
+                                   torch.from_numpy(self.w[(e, 1)])]).to(torch.bfloat16)
+                        for e in range(num_experts)]
+            self.w2b = [torch.from_numpy(self.w[(e, 2)]).to(torch.bfloat16)
+                        for e in range(num_experts)]
+
+    def _expert_bf16(self, e, x_bf16):
+        """torch-CPU bf16: [W1; W3] in one GEMM (oneDNN, fp32 accumulation,
+        bf16 outputs), SwiGLU in fp32 -> bf16 act, W2 GEMM -> fp32."""
+        F = self.torch.nn.functional
+        gu = F.linear(x_bf16, self.w13[e]).float()
+        act = (F.silu(gu[:, : self.ffn]) * gu[:, self.ffn:]).to(self.torch.bfloat16)
+        return F.linear(act, self.w2b[e]).float()
+
+    def decode_step_bf16(self, h: np.ndarray):
+        """decode_step with the experts in torch-CPU bf16."""
+        torch = self.torch
+        x = N.rmsnorm(h[None, :], self.norm)
+        p, _ = N.router(x, self.gate, self.gate_next)
+        sel = D.topk_rows(p.astype(np.float64), self.k)
+        w = N.renorm_weights(p, sel)
+        xb = torch.from_numpy(x).to(torch.bfloat16)
+        out = torch.from_numpy(h.astype(np.float32))
+        for j, e in enumerate(sel[0]):
+            out = out + float(w[0, j]) * self._expert_bf16(int(e), xb)[0]
+        return out.numpy(), sel[0]
+
+    def prefill_bf16(self, h: np.ndarray):
+        torch = self.torch
+        x = N.rmsnorm(h, self.norm)
+        p, _ = N.router(x, self.gate, self.gate_next)
+        sel = D.topk_rows(p.astype(np.float64), self.k)
+        w = N.renorm_weights(p, sel)
+        off, perm, inv = N.permutation(sel, self.E)
+        y = np.zeros((sel.size, h.shape[1]), dtype=np.float32)
+        xb = torch.from_numpy(x).to(torch.bfloat16)
+        for e in range(self.E):
+            a, b = int(off[e]), int(off[e + 1])
+            if a < b:
+                rows = torch.from_numpy(perm[a:b] // self.k)
+                y[a:b] = self._expert_bf16(e, xb[rows]).numpy()
+        return N.combine(h, y, inv, w)
 
     def decode_step(self, h: np.ndarray):
         """One token (d,) through the layer: router -> top-k -> SwiGLU experts
@@ -73,6 +129,16 @@ class CpuMoELayer:
                 rows = perm[a:b] // self.k
                 y[a:b] = N.expert_ffn(x[rows], self.w[(e, 0)], self.w[(e, 1)], self.w[(e, 2)])
         return N.combine(h, y, inv, w)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:  # pragma: no cover
+        pass
+    return "unknown"
 
 
 def time_steps(fn, inputs, budget_s: float, max_steps: int, warmup: int = 1):

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   R.S = stages;
   R.ring = smem;
   uint16_t* xs = reinterpret_cast<uint16_t*>(smem + static_cast<size_t>(stages) * d * 2);
-  float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xs) + d * 2);
+  double* red = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(xs) + d * 2);
   R.full = reinterpret_cast<uint64_t*>(red + 40);
   R.empty = R.full + stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,26 +118,22 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   uint4 ga = make_uint4(0u, 0u, 0u, 0u), gb = ga;
   if (regs && c0 < n8) { ha = h4[2 * c0]; hb = h4[2 * c0 + 1]; ga = g4[c0]; }
   if (regs && c1 < n8) { hc = h4[2 * c1]; hd = h4[2 * c1 + 1]; gb = g4[c1]; }
-  auto sq4 = [](float4 v, float a) {
-    a = fmaf(v.x, v.x, a); a = fmaf(v.y, v.y, a); a = fmaf(v.z, v.z, a);
-    return fmaf(v.w, v.w, a);
-  };
-  float ss = 0.f;
+  double ss = 0.0;  // fp64 squares: common.cuh rms_scale
   if (regs) {
-    ss = sq4(hd, sq4(hc, sq4(hb, sq4(ha, ss))));
+    ss = sq_acc4(hd, sq_acc4(hc, sq_acc4(hb, sq_acc4(ha, ss))));
   } else {
-    for (int i = tid; i < d; i += nt) ss = fmaf(h[i], h[i], ss);
+    for (int i = tid; i < d; i += nt) ss = sq_acc(h[i], ss);
   }
   ss = warp_sum(ss);
   if (lane == 0) red[warp] = ss;
   asm volatile("bar.sync 1, %0;" ::"r"(nt));
   if (threadIdx.x == 0) {
-    float t = 0.f;
+    double t = 0.0;
     for (int w = 0; w < AT_WARPS; ++w) t += red[w];
-    red[32] = 1.0f / sqrtf(t / static_cast<float>(d) + eps);
+    red[32] = rms_scale(t, d, eps);
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nt));
-  const float r = red[32];
+  const float r = static_cast<float>(red[32]);
   auto norm8 = [&](int c, float4 u, float4 v, uint4 g) {
     const float hv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
     const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
@@ -378,22 +374,18 @@ __global__ void __launch_bounds__(256) attn_norm_rows_kernel(const float* __rest
                                                              const uint16_t* __restrict__ gamma,
                                                              int d, float eps,
                                                              uint16_t* __restrict__ xa) {
-  __shared__ float red[8];
+  __shared__ double red[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n8 = d / 8;
   const float4* h4 = reinterpret_cast<const float4*>(h + static_cast<int64_t>(blockIdx.x) * d);
   const uint4* g4 = reinterpret_cast<const uint4*>(gamma);
-  float ss = 0.f;
-  for (int c = tid; c < n8; c += blockDim.x) {
-    const float4 u = h4[2 * c], v = h4[2 * c + 1];
-    ss = fmaf(u.x, u.x, ss); ss = fmaf(u.y, u.y, ss); ss = fmaf(u.z, u.z, ss); ss = fmaf(u.w, u.w, ss);
-    ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
-  }
+  double ss = 0.0;  // fp64 squares: common.cuh rms_scale
+  for (int c = tid; c < n8; c += blockDim.x) ss = sq_acc4(h4[2 * c + 1], sq_acc4(h4[2 * c], ss));
   ss = warp_sum(ss);
   if (lane == 0) red[warp] = ss;
   __syncthreads();
-  float tot = 0.f;
+  double tot = 0.0;
   for (int w = 0; w < 8; ++w) tot += red[w];
-  const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + eps);
+  const float r = rms_scale(tot, d, eps);
   uint4* x4 = reinterpret_cast<uint4*>(xa + static_cast<int64_t>(blockIdx.x) * d);
   for (int c = tid; c < n8; c += blockDim.x) {
     const float4 u = h4[2 * c], v = h4[2 * c + 1];
@@ -635,7 +627,7 @@ extern "C" int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const
     // consumed by warp i % AT_WARPS, so no warp can wait on a stage a whole
     // ring cycle ahead of its data (a shared ring would let it)
     const int stages = AT_WARPS;
-    const size_t smem = static_cast<size_t>(stages) * d * 2 + static_cast<size_t>(d) * 2 + 40 * 4 +
+    const size_t smem = static_cast<size_t>(stages) * d * 2 + static_cast<size_t>(d) * 2 + 40 * 8 +
                         2 * stages * 8;
     DAOP_CUDA(cudaFuncSetAttribute(attn_qkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));

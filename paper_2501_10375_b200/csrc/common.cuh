@@ -174,6 +174,29 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// RMSNorm, bit-compatible with oracle/numerics.rmsnorm:
+// squares accumulated in fp64 (h*h is exact in fp64, so only the order of the
+// additions differs -- far below the one rounding to f32 that follows), the
+// mean rounded to f32 once, then +eps, sqrt and 1/x in IEEE f32.  x =
+// bf16((h * r) * gamma) is then the oracle's value for all but astronomically
+// rare double-rounding ties, so free-running routing matches the CPU path.
+__device__ __forceinline__ double sq_acc(float v, double a) {
+  return fma(static_cast<double>(v), static_cast<double>(v), a);
+}
+__device__ __forceinline__ double sq_acc4(float4 v, double a) {
+  return sq_acc(v.w, sq_acc(v.z, sq_acc(v.y, sq_acc(v.x, a))));
+}
+__device__ __forceinline__ float rms_scale(double ss, int d, float eps) {
+  const float ms = static_cast<float>(ss / static_cast<double>(d));
+  return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, eps)));
+}
+
 __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
   __nv_bfloat16 b = __float2bfloat16_rn(f);
   return *reinterpret_cast<uint16_t*>(&b);

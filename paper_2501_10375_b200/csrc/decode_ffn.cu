@@ -106,17 +106,33 @@ struct Piece {   // what one ring stage holds
   int j, row, c; // pick (executed index), row, piece within the unit
 };
 
+// a Piece packed into 32 bits for the per-stage record in shared memory
+// (kind 2 b | j 4 b | c 8 b | row 18 b): the decode kernel's smem is at the
+// 227 KB limit for Mixtral-8x7B, so every byte of the control block counts
+__device__ __forceinline__ uint32_t pack_piece(const Piece& p) {
+  return static_cast<uint32_t>(p.kind) | (static_cast<uint32_t>(p.j) << 2) |
+         (static_cast<uint32_t>(p.c) << 6) | (static_cast<uint32_t>(p.row) << 14);
+}
+__device__ __forceinline__ Piece unpack_piece(uint32_t v) {
+  Piece p;
+  p.kind = static_cast<int>(v & 3u);
+  p.j = static_cast<int>((v >> 2) & 15u);
+  p.c = static_cast<int>((v >> 6) & 255u);
+  p.row = static_cast<int>(v >> 14);
+  return p;
+}
+
 template <int DW, int DS>
 struct DecodeSmem {
   uint64_t bar[DW][DS];
   uint64_t act_bar[DK_MAX];
   uint64_t in_bar;   // h + gamma
   uint64_t in_bar2;  // gate rows (+ next-layer row)
-  Piece rec[DW][DS];
+  uint32_t rec[DW][DS];  // pack_piece
   int act_req[DK_MAX];
   int p1_next, p2_next, fin;
   int done1[DK_MAX];
-  float red[DW];
+  double red[DW];         // per-warp sums of squares (fp64, common.cuh rms_scale)
   float zpart[DW][DE_MAX];  // per-warp partial gate logits
   float zpp[DW];            // per-warp partial next-layer logit
   float p[DE_MAX];
@@ -332,7 +348,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     next_piece(pc);
     const int stg = issued % DS;
     if (lane == 0) {
-      s.rec[warp][stg] = pc;
+      s.rec[warp][stg] = pack_piece(pc);
       if (pc.kind) {
         int elems, voff;
         const uint16_t* src = piece_src(L, pc, elems, voff);
@@ -386,7 +402,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     __syncwarp();
   };
 
-  float ss = 0.f;
+  double ss = 0.0;
   if (a.mode == 1) {
     // ---------------------------------------------------- PLAN: stream first
     if (warp == 0) {
@@ -397,17 +413,13 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     }
     __syncthreads();
     start_stream();
-    for (int i = threadIdx.x; i < d / 4; i += NT) {  // router inputs from global
-      const float4 v = reinterpret_cast<const float4*>(a.h)[i];
-      ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
-    }
+    for (int i = threadIdx.x; i < d / 4; i += NT)  // router inputs from global
+      ss = sq_acc4(reinterpret_cast<const float4*>(a.h)[i], ss);
   } else {
     // ---------------------------------------------------- TRUE: router first
     mbar_wait(&s.in_bar, 0);
-    for (int i = threadIdx.x; i < d / 4; i += NT) {
-      const float4 v = reinterpret_cast<const float4*>(h_s)[i];
-      ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
-    }
+    for (int i = threadIdx.x; i < d / 4; i += NT)
+      ss = sq_acc4(reinterpret_cast<const float4*>(h_s)[i], ss);
   }
   ss = warp_sum(ss);
   if (lane == 0) s.red[warp] = ss;
@@ -424,9 +436,9 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   const bool lazy_gates = a.mode == 1 && a.weights_from_pred;
   const int n16 = d / 8;
   {
-    float tot = 0.f;
+    double tot = 0.0;
     for (int w = 0; w < DW; ++w) tot += s.red[w];
-    const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + a.eps);
+    const float r = rms_scale(tot, d, a.eps);
     const float4* hsrc = reinterpret_cast<const float4*>(mode0 ? h_s : a.h);
     const uint4* gmsrc = reinterpret_cast<const uint4*>(mode0 ? gm_s : a.gamma);
     const uint16_t* gsrc = mode0 ? g_s : a.wg;
@@ -612,7 +624,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   for (int p = 0;; ++p) {
     const int stg = p % DS;
     __syncwarp();
-    const Piece pc = s.rec[warp][stg];
+    const Piece pc = unpack_piece(s.rec[warp][stg]);
     if (pc.kind == 0) break;
     int elems, voff;
     piece_src(L, pc, elems, voff);

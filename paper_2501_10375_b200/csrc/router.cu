@@ -87,16 +87,15 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
   for (int64_t t = blockIdx.x * (int64_t)kRouterWarps + warp; t < a.T;
        t += (int64_t)gridDim.x * kRouterWarps) {
     const float* hrow = a.h + t * d;
-    // pass 1: sum of squares
-    float ss = 0.f;
+    // pass 1: sum of squares (fp64, common.cuh rms_scale)
+    double ss = 0.0;
     for (int c = lane; c < nchunk; c += 32) {
       const float4 u = reinterpret_cast<const float4*>(hrow)[2 * c];
       const float4 v = reinterpret_cast<const float4*>(hrow)[2 * c + 1];
-      ss = fmaf(u.x, u.x, ss); ss = fmaf(u.y, u.y, ss); ss = fmaf(u.z, u.z, ss); ss = fmaf(u.w, u.w, ss);
-      ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+      ss = sq_acc4(v, sq_acc4(u, ss));
     }
     ss = warp_sum(ss);
-    const float r = 1.0f / sqrtf(ss / static_cast<float>(d) + a.eps);
+    const float r = rms_scale(ss, d, a.eps);
     // pass 2: normalise, store x, dot with the gate rows
     float acc[kMaxGateRows];
 #pragma unroll
@@ -231,8 +230,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
   const int ld = d + 8;  // padded gate row (bf16): conflict-free fragment loads
   uint16_t* gs = reinterpret_cast<uint16_t*>(smem);                 // 16 x ld
   uint16_t* gam = gs + 16 * ld;                                       // d
-  float* sspart = reinterpret_cast<float*>(gam + d);                  // [2][kMmaWarps][8]
-  float* zpart = sspart + 2 * kMmaWarps * kTokTile;                   // [2][kMmaWarps][16][8]
+  double* sspart = reinterpret_cast<double*>(gam + d);                // [2][kMmaWarps][8]
+  float* zpart = reinterpret_cast<float*>(sspart + 2 * kMmaWarps * kTokTile);  // [2][kMmaWarps][16][8]
 
   for (int i = threadIdx.x; i < 16 * (d / 8); i += blockDim.x) {
     const int r = i / (d / 8), c = i - r * (d / 8);
@@ -264,7 +263,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
     for (int i = 0; i < PF; ++i) prefetch_tile(blockIdx.x + static_cast<int64_t>(i) * gridDim.x);
   // software pipeline over this CTA's tiles: the x/MMA pass of tile i and the
   // sum-of-squares pass of tile i+1 share one batch of loads and one barrier
-  auto ss_partial = [&](float ssv) {  // sum over the 4 lanes of a token
+  auto ss_partial = [&](double ssv) {  // sum over the 4 lanes of a token
     ssv += __shfl_xor_sync(0xffffffffu, ssv, 1);
     ssv += __shfl_xor_sync(0xffffffffu, ssv, 2);
     return ssv;
@@ -272,7 +271,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
   int buf = 0;
   {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * kTokTile + g;
-    float ss = 0.f;
+    double ss = 0.0;
     if (blockIdx.x < ntiles && t < a.T) {
       const float* hrow = a.h + t * d;
 #pragma unroll 16
@@ -280,8 +279,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
         const int k = k0w + ks * 16 + c2;
         const float2 u = __ldg(reinterpret_cast<const float2*>(hrow + k));
         const float2 v = __ldg(reinterpret_cast<const float2*>(hrow + k + 8));
-        ss = fmaf(u.x, u.x, ss); ss = fmaf(u.y, u.y, ss);
-        ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss);
+        ss = sq_acc(v.y, sq_acc(v.x, sq_acc(u.y, sq_acc(u.x, ss))));
       }
     }
     ss = ss_partial(ss);
@@ -296,12 +294,12 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
     const int64_t t1 = t + static_cast<int64_t>(gridDim.x) * kTokTile;  // next tile, same lane
     const bool live1 = t1 < a.T;
     const float* hrow1 = a.h + (live1 ? t1 : 0) * d;
-    const float* ssb = sspart + buf * kMmaWarps * kTokTile;
-    float tot = 0.f;
+    const double* ssb = sspart + buf * kMmaWarps * kTokTile;
+    double tot = 0.0;
     for (int w = 0; w < kMmaWarps; ++w) tot += ssb[w * kTokTile + g];
-    const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + a.eps);
+    const float r = rms_scale(tot, d, a.eps);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    float ss1 = 0.f;
+    double ss1 = 0.0;
     uint16_t* xrow = a.x_out ? a.x_out + (live ? t : 0) * d : nullptr;
     // batches of 4 k-steps: every h load of the batch (this tile's reload and
     // the next tile's first read) is issued before the x stores, which the
@@ -325,8 +323,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        ss1 = fmaf(u1[i].x, u1[i].x, ss1); ss1 = fmaf(u1[i].y, u1[i].y, ss1);
-        ss1 = fmaf(v1[i].x, v1[i].x, ss1); ss1 = fmaf(v1[i].y, v1[i].y, ss1);
+        ss1 = sq_acc(v1[i].y, sq_acc(v1[i].x, sq_acc(u1[i].y, sq_acc(u1[i].x, ss1))));
         if (ks0 + i < ksteps) {
           const int k = k0w + (ks0 + i) * 16 + c2;
           const uint32_t b0 = pack_x2(u[i].x, u[i].y, r, *reinterpret_cast<const uint32_t*>(gam + k));
@@ -425,23 +422,22 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) router_small_kernel(Route
   const int rows = a.wg_next ? 2 * E : E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
   const int64_t t = blockIdx.x;
-  __shared__ float red[kSmallWarps];
+  __shared__ double red[kSmallWarps];
   __shared__ float part[kSmallWarps][kMaxGateRows];
   const float* hrow = a.h + t * d;
   const int n8 = d / 8;  // 8-element chunks, thread-strided
-  float ss = 0.f;
+  double ss = 0.0;
   for (int c = tid; c < n8; c += blockDim.x) {
     const float4 u = reinterpret_cast<const float4*>(hrow)[2 * c];
     const float4 v = reinterpret_cast<const float4*>(hrow)[2 * c + 1];
-    ss = fmaf(u.x, u.x, ss); ss = fmaf(u.y, u.y, ss); ss = fmaf(u.z, u.z, ss); ss = fmaf(u.w, u.w, ss);
-    ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+    ss = sq_acc4(v, sq_acc4(u, ss));
   }
   ss = warp_sum(ss);
   if (lane == 0) red[warp] = ss;
   __syncthreads();
-  float tot = 0.f;
+  double tot = 0.0;
   for (int w = 0; w < kSmallWarps; ++w) tot += red[w];
-  const float r = 1.0f / sqrtf(tot / static_cast<float>(d) + a.eps);
+  const float r = rms_scale(tot, d, a.eps);
   float acc[kMaxGateRows];
 #pragma unroll
   for (int q = 0; q < kMaxGateRows; ++q) acc[q] = 0.f;
@@ -552,7 +548,7 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
     return DAOP_OK;
   }
   const size_t smem_mma = static_cast<size_t>(16) * (d + 8) * 2 + static_cast<size_t>(d) * 2 +
-                          2 * kMmaWarps * kTokTile * 4 + 2 * kMmaWarps * 16 * kTokTile * 4;
+                          2 * kMmaWarps * kTokTile * 8 + 2 * kMmaWarps * 16 * kTokTile * 4;
   if (rows <= 16 && d % (16 * kMmaWarps) == 0 && smem_mma <= 232448) {
     const int64_t ntiles = (T + kTokTile - 1) / kTokTile;
     const int blocks = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());

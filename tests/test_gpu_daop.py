@@ -192,3 +192,16 @@ def test_decode_host_graph_matches_device_decode():
             torch.cuda.synchronize()
             assert torch.equal(out, eng.bufs.h_out.cpu()), (t, layer)
             assert torch.equal(sel, eng.bufs.sel.cpu()), (t, layer)
+
+
+def test_host_pool_device_fill_matches_host_fill():
+    """HostExpertPool generated on the GPU (bench / daop32 fast path) is bit-
+    identical to the host generator's pool."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.daop import HostExpertPool
+    shape = P.ModelShape(2, 4, 2)
+    a = HostExpertPool(shape, 256, 512, seed=9)
+    b = HostExpertPool(shape, 256, 512, seed=9, device="cuda")
+    assert torch.equal(a.buf.view(torch.int16), b.buf.view(torch.int16))
