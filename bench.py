@@ -150,7 +150,8 @@ def cpu_arm(layer, xs, steps, warmup, budget_s, fns=None, tokens_per_step=1,
     block, each on all host cores (decided on 2 calibration steps); both
     numbers are reported."""
     from oracle.baseline import blas_threads, cpu_model, time_steps
-    cand = fns or {"numpy_f32": layer.decode_step, "torch_bf16": layer.decode_step_bf16}
+    cand = fns or {"numpy_f32": layer.decode_step, "torch_bf16": layer.decode_step_bf16,
+                   "c_bf16": layer.decode_step_c}
     probe = {}
     for name, fn in cand.items():
         n, sec = time_steps(fn, xs, budget_s=5.0, max_steps=2, warmup=1)
@@ -158,8 +159,11 @@ def cpu_arm(layer, xs, steps, warmup, budget_s, fns=None, tokens_per_step=1,
     best = max(probe, key=probe.get)
     n, sec = time_steps(cand[best], xs, budget_s=budget_s, max_steps=steps, warmup=warmup)
     desc = {"numpy_f32": "oracle numpy fp32 on bf16-valued weights",
-            "torch_bf16": "torch-CPU bf16 weights/activations, oneDNN fp32 accumulation"}[best]
-    return {"value": tokens_per_step * n / sec, "unit": "tokens/s", "cores": blas_threads(),
+            "torch_bf16": "torch-CPU bf16 weights/activations, oneDNN fp32 accumulation",
+            "c_bf16": "oracle C (oracle/cpu_moe.c) on bf16 weights, fp32 accumulation, "
+                      "OpenMP"}[best]
+    cores = layer.c_threads() if best == "c_bf16" else blas_threads()
+    return {"value": tokens_per_step * n / sec, "unit": "tokens/s", "cores": cores,
             "kind": "port", "cpu_model": cpu_model(), "variant": best,
             "variants_tok_s": {k: round(v, 2) for k, v in probe.items()},
             "sample": f"{n} steps of {tokens_per_step} x {what} ({desc}, {sec:.1f} s)",
@@ -192,7 +196,8 @@ def run_reference(args, world, rank):
         layer = CpuMoELayer(2, E, K, EP_D, EP_FFN, seed=0, layer=0, with_bf16=True)
         xs = [N.input_hidden(0, 300, i, 64, EP_D) for i in range(2)]
         cb = cpu_arm(layer, xs, steps=args.steps, warmup=args.warmup, budget_s=90.0,
-                     fns={"numpy_f32": layer.prefill, "torch_bf16": layer.prefill_bf16},
+                     fns={"numpy_f32": layer.prefill, "torch_bf16": layer.prefill_bf16,
+                          "c_bf16": layer.prefill_c},
                      tokens_per_step=64, what="64 prompt tokens through one Mixtral-8x22B layer")
     else:
         layer = cpu_decode_layer()
@@ -204,7 +209,7 @@ def run_reference(args, world, rank):
         "n_gpus": world, "steps": cb["steps"], "warmup": args.warmup,
         "ms_per_step": 1e3 * cb["seconds"] / cb["steps"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16" if cb["variant"] == "torch_bf16" else "f32",
+        "dtype": "f32" if cb["variant"] == "numpy_f32" else "bf16",
         "data": "synthetic (counter-RNG random-init weights and tokens)",
         "config": workload_config(world),
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "cpu_model",
@@ -306,7 +311,9 @@ def run_b200(args, world, rank, local_rank):
         del rp
         barrier()
         torch.cuda.synchronize()
-        kp = max(3, min(10, args.steps // 200))
+        # 10 back-to-back layers (~170 ms): the power-capped regime the
+        # sustained bf16 peak is measured in, whatever --steps is
+        kp = 10
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(local_rank) as pclk:
             p0.record(stream)

@@ -366,13 +366,17 @@ int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const uint16_t* 
 
 /* Prefill of T prompt tokens through the same attention block, positions
  * pos0 .. pos0 + T - 1 (the calls DaopEngine.prefill makes per layer; the
- * reference prices this as the prefill t_nonmoe, simulator.py:438-441).  The
- * two projections are plain GEMMs the caller runs (cuBLAS, fp32 output):
+ * reference prices this as the prefill t_nonmoe, simulator.py:438-441):
  *   daop_attn_norm_rows: d_xa (T, d) bf16 = rmsnorm(d_h (T, d) fp32) * gamma
- *   qkv = xa . Wqkv^T  (T, q + 2 kv) fp32                        [caller]
+ *   daop_gemm_bf16_f32:  qkv = xa . Wqkv^T  (T, q + 2 kv) fp32   (tcgen05)
  *   daop_attn_prefill:   k (RoPE), v of every token -> the cache, then causal
- *                        attention per token -> d_o (T, q) bf16
- *   h' = h + o . Wo^T                                              [caller] */
+ *                        flash attention on the tensor cores -> d_o (T, q) bf16
+ *   daop_gemm_bf16_f32:  h' = h + o . Wo^T  (residual in the epilogue) */
+/* Dense projection on the grouped-GEMM tcgen05 pipeline: d_out (M, N) fp32 =
+ * d_a (M, K) bf16 . d_w^T (d_w (N, K) bf16 row-major) [+ d_resid (M, N) fp32,
+ * may alias d_out, NULL for none].  K % 64 == 0, N % 256 == 0. */
+int daop_gemm_bf16_f32(const uint16_t* d_a, int64_t M, int32_t K, const uint16_t* d_w, int32_t N,
+                       const float* d_resid, float* d_out, daop_stream_t stream);
 int daop_attn_norm_rows(const float* d_h, int64_t T, const uint16_t* d_gamma, int32_t d, float eps,
                         uint16_t* d_xa, daop_stream_t stream);
 int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, uint16_t* d_k_cache,

@@ -4,12 +4,12 @@ GPU in bench.py (`cpu_baseline` and `--impl reference`).
 `CpuMoELayer` executes the MoE block exactly as restated in
 oracle/numerics.py and the decisions exactly as restated in
 oracle/decisions.py (the reference's own algorithm, pinned to its golden
-vectors) -- numpy, fp32 arithmetic on bf16-valued weights, all host cores
-through the BLAS thread pool.  `CpuMoELayerBf16` is the same block the way a
-CPU deployment would run it: bf16 weights and activations
-through torch-CPU (oneDNN, fp32 accumulation, AVX-512 BF16 where the host
-has it), all host cores -- half the weight bytes of the fp32 port, so it is
-the faster, fairer CPU baseline and the one bench.py reports.  Weights come
+vectors) in three variants, all on every host core: numpy fp32 on the
+bf16-valued weights (BLAS thread pool); torch-CPU bf16 (oneDNN, fp32
+accumulation); and plain C on the bf16 weights as stored (oracle/cpu_moe.c,
+OpenMP, fp32 accumulation -- half the weight bytes of the fp32 port).
+bench.py times all three and reports the fastest as the CPU baseline
+(BASELINE.md §3 asked for bf16 weights with fp32 accumulation).  Weights come
 from the oracle generator (oracle/rng.py), generated in parallel threads
 (numpy releases the GIL), so nothing from the product package is used.
 """
@@ -65,6 +65,61 @@ class CpuMoELayer:
                         for e in range(num_experts)]
             self.w2b = [torch.from_numpy(self.w[(e, 2)]).to(torch.bfloat16)
                         for e in range(num_experts)]
+
+    # ---- plain-C bf16 variant (oracle/cpu_moe.c): bf16 weights as stored,
+    # fp32 accumulation, OpenMP over every host core
+    def _c(self):
+        if getattr(self, "_lib", None) is None:
+            import ctypes
+            from .build import build
+            lib = ctypes.CDLL(str(build()))
+            lib.oracle_expert_ffn.argtypes = [ctypes.c_void_p, ctypes.c_int] + \
+                [ctypes.c_void_p] * 3 + [ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                         ctypes.c_void_p]
+            lib.oracle_threads.restype = ctypes.c_int
+            self._lib = lib
+            # the weights are bf16-valued fp32: their top 16 bits are the bf16
+            self.wb = {key: np.ascontiguousarray((w.view(np.uint32) >> 16).astype(np.uint16))
+                       for key, w in self.w.items()}
+        return self._lib
+
+    def _expert_c(self, e, x):
+        lib = self._c()
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        n = x.shape[0]
+        act = np.empty((n, self.ffn), dtype=np.float32)
+        y = np.empty((n, self.d), dtype=np.float32)
+        lib.oracle_expert_ffn(x.ctypes.data, n, self.wb[(e, 0)].ctypes.data,
+                              self.wb[(e, 1)].ctypes.data, self.wb[(e, 2)].ctypes.data, self.d,
+                              self.ffn, act.ctypes.data, y.ctypes.data)
+        return y
+
+    def c_threads(self) -> int:
+        return int(self._c().oracle_threads())
+
+    def decode_step_c(self, h: np.ndarray):
+        """decode_step with the experts in plain C on bf16 weights."""
+        x = N.rmsnorm(h[None, :], self.norm)
+        p, _ = N.router(x, self.gate, self.gate_next)
+        sel = D.topk_rows(p.astype(np.float64), self.k)
+        w = N.renorm_weights(p, sel)
+        out = h.astype(np.float32).copy()
+        for j, e in enumerate(sel[0]):
+            out = out + w[0, j] * self._expert_c(int(e), x)[0]
+        return out, sel[0]
+
+    def prefill_c(self, h: np.ndarray):
+        x = N.rmsnorm(h, self.norm)
+        p, _ = N.router(x, self.gate, self.gate_next)
+        sel = D.topk_rows(p.astype(np.float64), self.k)
+        w = N.renorm_weights(p, sel)
+        off, perm, inv = N.permutation(sel, self.E)
+        y = np.zeros((sel.size, h.shape[1]), dtype=np.float32)
+        for e in range(self.E):
+            a, b = int(off[e]), int(off[e + 1])
+            if a < b:
+                y[a:b] = self._expert_c(e, x[perm[a:b] // self.k])
+        return N.combine(h, y, inv, w)
 
     def _expert_bf16(self, e, x_bf16):
         """torch-CPU bf16: [W1; W3] in one GEMM (oneDNN, fp32 accumulation,

@@ -57,6 +57,7 @@ PROTOS = {
     "daop_expert_gemm_up_gather": [P, I64, P, I32, I64, I32, I32, P, I64, I64, P, P, I32, P, I32,
                                    P],
     "daop_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
+    "daop_gemm_bf16_f32": [P, I64, I32, P, I32, P, P, P],
     "daop_expert_gemm_up_skinny": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_expert_gemm_down_skinny": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_expert_gemm_down_combine": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, P, P, P, P,

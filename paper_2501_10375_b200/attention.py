@@ -9,8 +9,11 @@ QKV projection [Wq; Wk; Wv] (q + 2 kv, d), the output projection Wo (d, q)
 bf16 KV cache (n_kv, max_seq, 128).  `decode(h, layer, pos)` runs one token
 through csrc/attention.cu (daop_attn_decode: RMSNorm -> QKV GEMV -> RoPE ->
 cache append -> GQA flash-decoding -> O-proj GEMV + residual); `prefill(h,
-layer, pos0)` runs a whole prompt causally (cuBLAS projections over its T
-rows + daop_attn_norm_rows / daop_attn_prefill).  Mixtral-8x7B:
+layer, pos0)` runs a whole prompt causally: RMSNorm rows, the QKV projection
+on the tcgen05 GEMM pipeline (daop_gemm_bf16_f32), RoPE + cache append,
+FlashAttention-style causal attention on the tensor cores
+(daop_attn_prefill), and the O projection with the residual added in the
+GEMM epilogue.  Mixtral-8x7B:
 d 4096, 32 query heads, 8 KV heads, head dim 128, rope theta 1e6.
 """
 
@@ -71,10 +74,10 @@ class AttentionStack:
                 out: torch.Tensor | None = None):
         """h (T, d) fp32 on the device: T prompt tokens at positions pos0 ..
         pos0 + T - 1 -> h + Attention(RMSNorm(h)) (T, d) fp32, causal; appends
-        every token's k, v to the layer's cache.  The two projections are plain
-        GEMMs (cuBLAS, bf16 in, fp32 out); RMSNorm, RoPE, the cache append and
-        the attention are the library's kernels (daop_attn_norm_rows /
-        daop_attn_prefill)."""
+        every token's k, v to the layer's cache.  Every step is a library kernel:
+        daop_attn_norm_rows, daop_gemm_bf16_f32 (QKV, tcgen05), daop_attn_prefill
+        (RoPE + append, tensor-core flash attention), daop_gemm_bf16_f32 (O-proj
+        + residual, tcgen05)."""
         ops._dev(h)
         T, d = h.shape
         if pos0 < 0 or pos0 + T > self.max_seq:
@@ -83,15 +86,13 @@ class AttentionStack:
         xa = torch.empty((T, d), dtype=torch.bfloat16, device=h.device)
         _lib.call("daop_attn_norm_rows", h.data_ptr(), T, self.norm[layer].data_ptr(), d,
                   float(ops.RMS_EPS), xa.data_ptr(), ops._s())
-        qkv = torch.mm(xa, self.wqkv[layer].t(), out_dtype=torch.float32)
+        qkv = ops.gemm_bf16_f32(xa, self.wqkv[layer])
         o = torch.empty((T, self.q_dim), dtype=torch.bfloat16, device=h.device)
         _lib.call("daop_attn_prefill", qkv.data_ptr(), T, int(pos0),
                   self.k_cache[layer].data_ptr(), self.v_cache[layer].data_ptr(), self.n_heads,
                   self.n_kv, self.max_seq, float(self.theta), o.data_ptr(), ops._s())
-        y = torch.mm(o, self.wo[layer].t(), out_dtype=torch.float32)
-        if out is None:
-            return h + y
-        return torch.add(h, y, out=out)
+        # O projection with the residual added in the GEMM epilogue
+        return ops.gemm_bf16_f32(o, self.wo[layer], resid=h, out=out)
 
     def bytes_per_token_layer(self, ctx: int) -> int:
         """Algorithmic HBM bytes of one decode step of one layer at context

@@ -549,6 +549,231 @@ __global__ void __launch_bounds__(256, 2) attn_prefill_kernel(PrefillArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Causal prompt attention on the tensor cores (FlashAttention-2 style).
+// CTA = (kv head g, 16 query tokens); warp w = query head g * group + w, so
+// the GQA group's heads share every K / V tile the CTA stages.  Per warp:
+//   Q (16 x 128) = bf16(RoPE(q)) held as m16n8k16 A fragments (32 regs);
+//   per 64-position tile: S = Q K^T (ldmatrix B fragments from the padded
+//   K tile), causal mask, online softmax in fp32 (running max / sum per row,
+//   the accumulator rescaled), P = bf16(exp(S - m)) reused in registers as
+//   the A operand of O += P V (V fragments by ldmatrix.trans);
+//   o = bf16(O / l).
+// K / V tiles (64 x 128 bf16, rows padded to 136 elements: conflict-free
+// ldmatrix) are double-buffered with cp.async.  Numerics vs the oracle
+// (oracle/numerics.attention_decode): q and P are rounded to bf16 for the
+// MMAs (fp32 accumulation); within the hidden-state tolerance (tests).
+constexpr int FA_TOK = 16;            // query tokens per CTA (MMA M)
+constexpr int FA_KV = 64;             // positions per K / V tile
+constexpr int FA_LD = AT_HD + 8;      // padded smem row (bf16 elements)
+constexpr int FA_TILE = FA_KV * FA_LD;  // elements of one K (or V) tile
+
+__device__ __forceinline__ void mma_bf16_16816_acc(float (&d)[4], uint32_t a0, uint32_t a1,
+                                                   uint32_t a2, uint32_t a3, uint32_t b0,
+                                                   uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  // invalid rows are zero-filled (src-size 0): masked positions never read garbage
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)),
+               "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  return static_cast<uint32_t>(f32_to_bf16_bits(lo)) |
+         (static_cast<uint32_t>(f32_to_bf16_bits(hi)) << 16);
+}
+
+__global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(PrefillArgs a, int T) {
+  extern __shared__ __align__(128) uint16_t fa_smem[];  // [2 stages][K | V] tiles
+  const int g = blockIdx.x, t0 = blockIdx.y * FA_TOK;
+  const int group = a.n_heads / a.n_kv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = group * 32;
+  const int gr = lane >> 2, c4 = lane & 3;  // fragment row / column pair
+  const int q_dim = a.n_heads * AT_HD, kv_dim = a.n_kv * AT_HD, ld = q_dim + 2 * kv_dim;
+  const int hh = g * group + warp;  // this warp's query head
+  const uint16_t* kc = a.k_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
+  const uint16_t* vc = a.v_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
+  const int t_last = min(T, t0 + FA_TOK) - 1;
+  const int n_pos = a.pos0 + t_last + 1;  // positions any row of this CTA attends to
+  const int n_tiles = (n_pos + FA_KV - 1) / FA_KV;
+
+  auto load_tile = [&](int s) {  // positions [s * 64, s * 64 + 64) -> stage s & 1
+    uint16_t* ks = fa_smem + (s & 1) * 2 * FA_TILE;
+    uint16_t* vs = ks + FA_TILE;
+    const int p0 = s * FA_KV;
+    for (int i = threadIdx.x; i < FA_KV * (AT_HD / 8); i += nthr) {
+      const int r = i >> 4, c = (i & 15) * 8;
+      const bool ok = p0 + r < n_pos;
+      const int64_t src = static_cast<int64_t>(ok ? p0 + r : 0) * AT_HD + c;
+      cp_async16(ks + r * FA_LD + c, kc + src, ok);
+      cp_async16(vs + r * FA_LD + c, vc + src, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  load_tile(0);
+
+  // Q fragments: rows gr / gr + 8 = tokens t0 + gr / t0 + gr + 8; k-step ks
+  // covers dims 16 ks .. 16 ks + 15; RoPE pairs (j, j + 64) = (ks, ks + 4)
+  uint32_t qf[8][4];
+  {
+    float qv[2][8][4];  // [row half][ks][0..3] = dims 16ks + 2c4 + {0, 1, 8, 9}
+#pragma unroll
+    for (int rh = 0; rh < 2; ++rh) {
+      const int t = min(t0 + gr + 8 * rh, T - 1);
+      const float* q = a.qkv + static_cast<int64_t>(t) * ld + hh * AT_HD;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = 16 * ks + 2 * c4 + (e & 1) + 8 * (e >> 1);  // j < 64
+          float x0 = q[j], x1 = q[j + AT_HD / 2];
+          rope_pair(x0, x1, j, a.pos0 + t, a.theta);
+          qv[rh][ks][e] = x0;
+          qv[rh][ks + 4][e] = x1;
+        }
+    }
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      qf[ks][0] = pack_bf16x2(qv[0][ks][0], qv[0][ks][1]);
+      qf[ks][1] = pack_bf16x2(qv[1][ks][0], qv[1][ks][1]);
+      qf[ks][2] = pack_bf16x2(qv[0][ks][2], qv[0][ks][3]);
+      qf[ks][3] = pack_bf16x2(qv[1][ks][2], qv[1][ks][3]);
+    }
+  }
+  const int lim0 = a.pos0 + min(t0 + gr, T - 1);      // last position row gr may see
+  const int lim1 = a.pos0 + min(t0 + gr + 8, T - 1);  // ... row gr + 8
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  for (int s = 0; s < n_tiles; ++s) {
+    if (s + 1 < n_tiles) {
+      load_tile(s + 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const uint16_t* ks_ = fa_smem + (s & 1) * 2 * FA_TILE;
+    const uint16_t* vs_ = ks_ + FA_TILE;
+    const int p0 = s * FA_KV;
+    // ---- S = Q K^T (16 x 64)
+    float sc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int ks = 0; ks < 8; ks += 2) {
+        const int mi = lane >> 3;
+        const uint32_t addr = smem_u32(ks_ + (8 * j + (lane & 7)) * FA_LD + 16 * ks + 8 * mi);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(addr, b0, b1, b2, b3);
+        mma_bf16_16816_acc(sc[j], qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3], b0, b1);
+        mma_bf16_16816_acc(sc[j], qf[ks + 1][0], qf[ks + 1][1], qf[ks + 1][2], qf[ks + 1][3], b2,
+                           b3);
+      }
+    }
+    // ---- scale, causal mask, online softmax (rows gr, gr + 8; a quad owns a row)
+    float mx0 = m0, mx1 = m1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int pos = p0 + 8 * j + 2 * c4 + e;
+        sc[j][e] = pos <= lim0 ? sc[j][e] * a.scale : -INFINITY;
+        sc[j][2 + e] = pos <= lim1 ? sc[j][2 + e] * a.scale : -INFINITY;
+        mx0 = fmaxf(mx0, sc[j][e]);
+        mx1 = fmaxf(mx1, sc[j][2 + e]);
+      }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    // every row sees position 0 in its first tile, so mx is finite from tile 0
+    const float al0 = expf(m0 - mx0), al1 = expf(m1 - mx1);
+    m0 = mx0;
+    m1 = mx1;
+    float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        sc[j][e] = expf(sc[j][e] - m0);
+        sc[j][2 + e] = expf(sc[j][2 + e] - m1);
+        rs0 += sc[j][e];
+        rs1 += sc[j][2 + e];
+      }
+    rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
+    rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
+    rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
+    rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
+    l0 = l0 * al0 + rs0;
+    l1 = l1 * al1 + rs1;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      o[i][0] *= al0;
+      o[i][1] *= al0;
+      o[i][2] *= al1;
+      o[i][3] *= al1;
+    }
+    // ---- O += P V: k-step kk = positions 16 kk .. 16 kk + 15 = S tiles 2kk, 2kk+1
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint32_t pa0 = pack_bf16x2(sc[2 * kk][0], sc[2 * kk][1]);
+      const uint32_t pa1 = pack_bf16x2(sc[2 * kk][2], sc[2 * kk][3]);
+      const uint32_t pa2 = pack_bf16x2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+      const uint32_t pa3 = pack_bf16x2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+#pragma unroll
+      for (int dn = 0; dn < 16; dn += 2) {
+        const int mi = lane >> 3;
+        const uint32_t addr =
+            smem_u32(vs_ + (16 * kk + 8 * (mi & 1) + (lane & 7)) * FA_LD + 8 * (dn + (mi >> 1)));
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(addr, b0, b1, b2, b3);
+        mma_bf16_16816_acc(o[dn], pa0, pa1, pa2, pa3, b0, b1);
+        mma_bf16_16816_acc(o[dn + 1], pa0, pa1, pa2, pa3, b2, b3);
+      }
+    }
+    __syncthreads();  // this stage is refilled two iterations from now
+  }
+  // ---- o = bf16(O / l) -> (T, q_dim) at this head's 128 columns
+  const float inv0 = 1.0f / l0, inv1 = 1.0f / l1;
+  const int ta = t0 + gr, tb = t0 + gr + 8;
+#pragma unroll
+  for (int dn = 0; dn < 16; ++dn) {
+    const int col = hh * AT_HD + 8 * dn + 2 * c4;
+    if (ta < T)
+      *reinterpret_cast<uint32_t*>(a.o + static_cast<int64_t>(ta) * q_dim + col) =
+          pack_bf16x2(o[dn][0] * inv0, o[dn][1] * inv0);
+    if (tb < T)
+      *reinterpret_cast<uint32_t*>(a.o + static_cast<int64_t>(tb) * q_dim + col) =
+          pack_bf16x2(o[dn][2] * inv1, o[dn][3] * inv1);
+  }
+}
+
 }  // namespace daop
 
 using namespace daop;
@@ -582,7 +807,13 @@ extern "C" int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, ui
                 theta, 1.0f / sqrtf(static_cast<float>(AT_HD)), d_o};
   attn_prefill_append_kernel<<<static_cast<unsigned>(T), 128, 0, st>>>(a);
   DAOP_CHECK_LAUNCH("attn_prefill_append");
-  attn_prefill_kernel<<<dim3(n_kv, static_cast<unsigned>(T)), 256, 0, st>>>(a);
+  const size_t smem = 2 * 2 * static_cast<size_t>(FA_TILE) * 2;  // 2 stages x (K, V)
+  DAOP_CUDA(cudaFuncSetAttribute(attn_prefill_mma_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  const unsigned tok_tiles = static_cast<unsigned>((T + FA_TOK - 1) / FA_TOK);
+  attn_prefill_mma_kernel<<<dim3(n_kv, tok_tiles), (n_heads / n_kv) * 32, smem, st>>>(
+      a, static_cast<int>(T));
   DAOP_CHECK_LAUNCH("attn_prefill");
   return DAOP_OK;
 }

@@ -92,7 +92,38 @@ struct GemmParams {
   float* comb_out;           // (T, d)
   unsigned* comb_cnt;        // (T, n_tiles) zeroed once, self-resetting
   int comb_k;
+  // dense GEMM (daop_gemm_bf16_f32: one "expert" of dense_rows rows, weight
+  // slot 0, no device offset / slot tables) and an optional fp32 residual
+  // added in the down epilogue: out = resid + A . B^T (resid may alias out)
+  int64_t dense_rows;
+  const float* resid;
 };
+
+__device__ __forceinline__ int64_t off_at(const GemmParams& p, int e) {
+  return p.offsets ? p.offsets[e] : (e == 0 ? 0 : p.dense_rows);
+}
+__device__ __forceinline__ int slot_at(const GemmParams& p, int e) {
+  return p.slot_of ? p.slot_of[e] : 0;
+}
+
+// 32 accumulator columns -> fp32 row slice (+ the residual when given)
+__device__ __forceinline__ void store_f32x32(float* out, const float* res, const uint32_t (&v)[32]) {
+  float4* o = reinterpret_cast<float4*>(out);
+  const float4* r = reinterpret_cast<const float4*>(res);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float4 a = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                           __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+    if (res) {
+      const float4 b = r[i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    o[i] = a;
+  }
+}
 
 // the fused combine of one (row, n-tile): called by the row's thread after
 // its y slice is stored and the accumulator released
@@ -207,11 +238,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     fence_mbar_init();
     int acc = 0;
     s.prefix[0] = 0;
-    for (int e = 0; e <= E; ++e) s.off[e] = p.offsets[e];
+    for (int e = 0; e <= E; ++e) s.off[e] = off_at(p, e);
     for (int e = 0; e < E; ++e) {
       // experts without an HBM slot (slow tier) get no tiles: their rows are
       // computed by the host tier and written into the output by the caller
-      const int64_t me = p.slot_of[e] >= 0 ? s.off[e + 1] - s.off[e] : 0;
+      const int64_t me = slot_at(p, e) >= 0 ? s.off[e + 1] - s.off[e] : 0;
       s.mt[e] = static_cast<int>((me + GB_M - 1) / GB_M);
       acc += s.mt[e] * p.n_tiles;
       s.prefix[e + 1] = acc;
@@ -237,7 +268,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       int e, m, n;
       for (int t = blockIdx.x; map_tile(s, E, nt, G, t, e, m, n); t += gridDim.x) {
         const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * GB_M);
-        const int slot = p.slot_of[e];
+        const int slot = slot_at(p, e);
         const int brow = n * p.b_tile_rows;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
@@ -335,13 +366,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           uint32_t v[32];
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
-          if (valid) {
-            float4* o = reinterpret_cast<float4*>(out + c);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              o[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-          }
+          if (valid)
+            store_f32x32(out + c, p.resid ? p.resid + grow * p.out_ld + n * GB_N + c : nullptr, v);
         }
       }
       tc_fence_before();
@@ -510,9 +536,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
     fence_mbar_init();
     int acc = 0;
     s.prefix[0] = 0;
-    for (int e = 0; e <= E; ++e) s.off[e] = p.offsets[e];
+    for (int e = 0; e <= E; ++e) s.off[e] = off_at(p, e);
     for (int e = 0; e < E; ++e) {
-      const int64_t me = p.slot_of[e] >= 0 ? s.off[e + 1] - s.off[e] : 0;
+      const int64_t me = slot_at(p, e) >= 0 ? s.off[e + 1] - s.off[e] : 0;
       s.mt[e] = static_cast<int>((me + C::M - 1) / C::M);
       acc += s.mt[e] * p.n_tiles;
       s.prefix[e + 1] = acc;
@@ -549,7 +575,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
       int e, m, n;
       for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
         const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * C::M) + rank * 128;
-        const int slot = p.slot_of[e];
+        const int slot = slot_at(p, e);
         const int brow = n * p.b_tile_rows + (leader ? 0 : p.b_half2);
         // gathered A: lane L fetches rows 4L .. 4L+3 of each 128-row box; the
         // token indices stay in registers for the whole tile (rows past the
@@ -690,13 +716,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
           uint32_t v[32];
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
-          if (valid) {
-            float4* o = reinterpret_cast<float4*>(out + c);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              o[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-          }
+          if (valid)
+            store_f32x32(out + c, p.resid ? p.resid + grow * p.out_ld + n * GB_N + c : nullptr, v);
         }
       }
       }
@@ -718,7 +739,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
           l2_demote_range(p.a_ptr + grow * p.a_ld, p.a_ld * 2);
         if ((p.demote & 2) && p.raster == 1 && m == s.mt[e] - 1) {     // B n-tile done
           const int brow = n * p.b_tile_rows + (rank == 0 ? 0 : p.b_half2) + q * 32 + lane;
-          l2_demote_range(p.b_ptr + static_cast<int64_t>(p.slot_of[e]) * p.b_slot_stride +
+          l2_demote_range(p.b_ptr + static_cast<int64_t>(slot_at(p, e)) * p.b_slot_stride +
                               static_cast<int64_t>(brow) * p.b_ld,
                           p.b_ld * 2);
         }
@@ -945,6 +966,38 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
                GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0,
                g_gemm_demote & 2, act, ffn, w2, ffn, slot_stride_elems};
   return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
+}
+
+// Dense projection on the same tcgen05 pipeline (the prompt attention's QKV
+// and O projections, attention.py): out (M, N) fp32 = A (M, K) bf16 . W^T,
+// W (N, K) bf16 row-major, optionally + resid (M, N) fp32 (may alias out).
+// One "expert" of M rows without device tables; N % 256 == 0, K % 64 == 0.
+extern "C" int daop_gemm_bf16_f32(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w,
+                                  int32_t N, const float* resid, float* out,
+                                  daop_stream_t stream) {
+  if (M < 0 || M >= (1ll << 31) || K < 64 || K % GB_K != 0 || N < GB_N || N % GB_N != 0) {
+    set_error("dense GEMM: unsupported shape (M=%lld K=%d N=%d): needs K %% 64 == 0, "
+              "N %% 256 == 0", static_cast<long long>(M), K, N);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (M == 0) return DAOP_OK;
+  CUtensorMap ta, tb;
+  int rc;
+  const uint64_t adims[2] = {static_cast<uint64_t>(K), static_cast<uint64_t>(M)};
+  const uint64_t astr[1] = {static_cast<uint64_t>(K) * 2};
+  const uint32_t abox[2] = {GB_K, GB_M};
+  if ((rc = make_tmap_bf16(&ta, a, 2, adims, astr, abox))) return rc;
+  const uint64_t bdims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), 1};
+  const uint64_t bstr[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K) * N * 2};
+  const uint32_t bbox[3] = {GB_K, 128, 1};
+  if ((rc = make_tmap_bf16(&tb, w, 3, bdims, bstr, bbox))) return rc;
+  const int grp = (g_gemm_two_m & 2) ? -16 : -8;
+  GemmParams p{nullptr, nullptr, 1, K / GB_K, N / GB_N, grp, GB_N, 128, out, N,
+               GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0, 0, a, K, w, K,
+               static_cast<int64_t>(K) * N};
+  p.dense_rows = M;
+  p.resid = resid;
+  return launch_gemm<false>(ta, tb, p, M, as_stream(stream));
 }
 
 // Down GEMM with the combine fused into its epilogue (single GPU prefill;

@@ -94,6 +94,20 @@ def permute(topk_idx, num_experts, x=None):
     return {"offsets": offsets, "perm": perm, "inv": inv.view(t, k), "x_perm": x_perm}
 
 
+def gemm_bf16_f32(a, w, resid=None, out=None):
+    """out (M, N) fp32 = a (M, K) bf16 . w (N, K)^T [+ resid (M, N) fp32] on the
+    tcgen05 GEMM pipeline (daop_gemm_bf16_f32); N % 256 == 0, K % 64 == 0."""
+    _dev(a, w, resid, out)
+    m, k = a.shape
+    n = w.shape[0]
+    if w.shape[1] != k or (resid is not None and tuple(resid.shape) != (m, n)):
+        raise ShapeMismatchError(f"gemm: a {tuple(a.shape)}, w {tuple(w.shape)}")
+    out = torch.empty((m, n), dtype=torch.float32, device=a.device) if out is None else out
+    _lib.call("daop_gemm_bf16_f32", a.data_ptr(), m, k, w.data_ptr(), n, _p(resid),
+              out.data_ptr(), _s())
+    return out
+
+
 def set_gemm_mode(mode: int) -> None:
     """0: tcgen05 CTA-pair grouped GEMM (default), 1: single-CTA kernel."""
     _lib.call("daop_set_gemm_mode", int(mode))

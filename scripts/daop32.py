@@ -40,10 +40,17 @@ def main():
     ap.add_argument("--trace-dir", default="", help="save each run's routing trace (moesim JSONL)")
     ap.add_argument("--attention", action="store_true",
                     help="full decoder layers: attention with a KV cache before each MoE block")
+    ap.add_argument("--export-dir", default="",
+                    help="write the calibration, each run's trace (gzipped moesim JSONL) and the "
+                         "engine's decisions for the reference parity test "
+                         "(tests/golden/make_daop32_golden.py)")
+    ap.add_argument("--host-fill", action="store_true",
+                    help="generate the pinned pool with the host generator (default: on the GPU)")
     a = ap.parse_args()
     shape = P.ModelShape(a.layers, 8, 2)
     t0 = time.perf_counter()
-    pool = HostExpertPool(shape, a.d, a.ffn, seed=0)
+    pool = HostExpertPool(shape, a.d, a.ffn, seed=0,
+                          device=None if a.host_fill else torch.device("cuda"))
     res = {"config": {"layers": a.layers, "d": a.d, "ffn": a.ffn, "experts": 8, "top_k": 2,
                       "prompt_tokens": a.prompt, "decode_tokens": a.decode,
                       "attention": a.attention},
@@ -61,6 +68,10 @@ def main():
                             [cal.model.input_hidden(1, stream=301, step=i)[0] for i in range(16)],
                             "calib")
     calib = P.pooled_decode_probabilities([crec.trace])
+    exp = Path(a.export_dir) if a.export_dir else None
+    if exp:
+        exp.mkdir(parents=True, exist_ok=True)
+        (exp / "calib.json").write_text(json.dumps({"calib": calib.tolist()}))
     res["calibration_prediction_accuracy"] = P.mean_prediction_accuracy(crec.trace)
     del cal, crec
     torch.cuda.empty_cache()
@@ -79,6 +90,27 @@ def main():
             Path(a.trace_dir).mkdir(parents=True, exist_ok=True)
             P.save_trace(tr, Path(a.trace_dir) / f"daop_ecr{ecr}.jsonl")
         n = tr.num_decode_tokens
+        if exp:
+            import gzip
+            import tempfile
+            with tempfile.NamedTemporaryFile(suffix=".jsonl") as f:
+                P.save_trace(tr, f.name)
+                (exp / f"trace_ecr{ecr}.jsonl.gz").write_bytes(gzip.compress(Path(f.name).read_bytes()))
+            pre = rec.prefill
+            (exp / f"engine_ecr{ecr}.json").write_text(json.dumps({
+                "ecr": ecr, "engine": "daop", "prediction_start_layer": 4,
+                "placement_initial": [sorted(x) for x in pre.placement_initial.on_fast],
+                "placement_final": [sorted(x) for x in pre.placement.on_fast],
+                "swaps": [[e.layer, e.swapped_in, e.swapped_out, e.hot_tokens, e.cold_tokens]
+                          for e in pre.swaps],
+                "device_counts": pre.counts.tolist(),
+                "executed": [[[int(x) for x in p.executed_experts()] for p in r.plans]
+                             for r in rec.decode],
+                "devices": [[[x.device for x in p.executed] for p in r.plans] for r in rec.decode],
+                "degraded": [[[[dg.dropped_expert, dg.substitute_expert] for dg in p.degraded]
+                               for p in r.plans]
+                             for r in rec.decode],
+                "counts": rec.counts}))
         runs.append({
             "ecr": ecr,
             "slot_budget": eng.placement0.slot_budget,

@@ -77,12 +77,15 @@ def test_attention_bad_position(P):
     (1024, 8, 2, 0, 5),          # a fresh prompt inside one tile
     (1024, 8, 2, 70, 130),       # history + a prompt spanning several tiles
     (4096, 32, 8, 0, 64),        # Mixtral-8x7B attention shape
+    (4096, 32, 8, 0, 256),       # configs[2]'s 256-token prompt: 4 K/V tiles, 16 token tiles
+    (1024, 8, 1, 3, 37),         # MQA-style group 8, ragged token tile
 ])
 def test_attention_prefill_parity(P, d, heads, kv, pos0, T):
-    """Batched causal prefill (cuBLAS projections + daop_attn_norm_rows /
-    daop_attn_prefill) vs the oracle run position by position, and vs the
-    decode kernels run token by token: outputs within the hidden-state bar,
-    cache rows within one bf16 ulp (the GEMM's summation order differs)."""
+    """Batched causal prefill (tcgen05 projections, tensor-core flash
+    attention with bf16 q / P operands) vs the oracle run position by
+    position, and vs the decode kernels run token by token: outputs within
+    the hidden-state bar, cache rows within one bf16 ulp (the GEMM's
+    summation order differs)."""
     pkg, A = P
     att = A.AttentionStack(2, d, heads, kv, max_seq=512, seed=5)
     dec = A.AttentionStack(2, d, heads, kv, max_seq=512, seed=5)
@@ -120,3 +123,26 @@ def test_attention_prefill_bounds(P):
     h = torch.zeros((10, 1024), device="cuda")
     with pytest.raises(pkg.ShapeMismatchError):
         att.prefill(h, 0, 60)
+
+
+@pytest.mark.parametrize("M,K,N,resid", [(1, 512, 256, False), (5, 512, 1024, True),
+                                         (256, 4096, 6144, False), (700, 4096, 4096, True),
+                                         (1100, 1024, 512, True)])
+def test_dense_gemm_parity(P, M, K, N, resid):
+    """daop_gemm_bf16_f32 (the prompt attention's projections on the tcgen05
+    pipeline) vs a float64 numpy product of the same bf16 operands."""
+    pkg, A = P
+    g = torch.Generator(device="cuda").manual_seed(M + K + N)
+    a = torch.randn((M, K), generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.rand((N, K), generator=g, device="cuda") - 0.5).to(torch.bfloat16)
+    r = torch.randn((M, N), generator=g, device="cuda") if resid else None
+    out = A.ops.gemm_bf16_f32(a, w, resid=r)
+    ref = a.double().cpu().numpy() @ w.double().cpu().numpy().T
+    if resid:
+        ref = ref + r.double().cpu().numpy()
+        # in place: the residual buffer receives the result
+        r2 = r.clone()
+        A.ops.gemm_bf16_f32(a, w, resid=r2, out=r2)
+        assert torch.equal(r2, out)
+    torch.cuda.synchronize()
+    close(out.cpu().numpy(), ref, f"gemm {M}x{K}x{N}")
