@@ -222,6 +222,53 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
                : "memory");
 }
 
+// softmax / top-k / renormalisation / activation counter of token tt from
+// its gate logits (zt own gate, zp next layer's), one expert per lane, shuffles
+// over the P2 >= E lanes; ties -> lower id (topk_scan, moesim/_kernels.py:63-79)
+__device__ __forceinline__ void token_finish(const RouterArgs& a, int64_t tt, int lane, float zt,
+                                             float zp, int P2) {
+  const int E = a.E;
+  const float p = lane_softmax_p2(zt, lane, E, P2);
+  if (lane < E) a.p_true[tt * E + lane] = p;
+  if (a.wg_next) {
+    const float ph = lane_softmax_p2(zp, lane, E, P2);
+    if (lane < E) a.p_pred[tt * E + lane] = ph;
+  }
+  bool taken = lane >= E;
+  int my_sel = -1;
+  float my_p = 0.f, den = 0.f;
+  for (int j = 0; j < a.k; ++j) {
+    float bv = taken ? -INFINITY : p;
+    int bi = taken ? 0x7fffffff : lane;
+#pragma unroll
+    for (int o = P2 >> 1; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    bi = __shfl_sync(0xffffffffu, bi, 0);
+    bv = __shfl_sync(0xffffffffu, bv, 0);
+    if (bi >= E) {  // NaN scores never compare: first untaken id
+      bi = __ffs(__ballot_sync(0xffffffffu, !taken)) - 1;
+      bv = __shfl_sync(0xffffffffu, p, bi);
+    }
+    den += bv;
+    if (lane == j) {
+      my_sel = bi;
+      my_p = bv;
+    }
+    if (lane == bi) taken = true;
+  }
+  if (lane < a.k) {
+    a.topk_idx[tt * a.k + lane] = my_sel;
+    a.topk_w[tt * a.k + lane] = my_p / den;
+    if (a.hist) atomicAdd(a.hist + (tt / a.tokens_per_seq) * a.hist_seq_stride + my_sel, 1);
+  }
+}
+
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int d = a.d, E = a.E;
@@ -363,45 +410,115 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
             if (a.wg_next) zp += z0[(w * 16 + E + lane) * kTokTile + warp];
           }
         }
-        const float p = lane_softmax_p2(zt, lane, E, P2);
-        if (lane < E) a.p_true[tt * E + lane] = p;
-        if (a.wg_next) {
-          const float ph = lane_softmax_p2(zp, lane, E, P2);
-          if (lane < E) a.p_pred[tt * E + lane] = ph;
-        }
-        bool taken = lane >= E;
-        int my_sel = -1;
-        float my_p = 0.f, den = 0.f;
-        for (int j = 0; j < a.k; ++j) {
-          float bv = taken ? -INFINITY : p;
-          int bi = taken ? 0x7fffffff : lane;
+        token_finish(a, tt, lane, zt, zp, P2);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Single-pass tensor-core router (d = 256 * KS, KS <= 16: every Mixtral-8x7B
+// sized model).  Same tile / fragment scheme as router_mma_kernel, but each
+// lane keeps its token's h slice (KS x 4 floats) in registers from the one
+// read that feeds both the sum of squares and the x / MMA pass: h crosses
+// HBM once (L2 prefetch of the tiles PF grid-strides ahead) and L2 once,
+// instead of L2 twice.  Two CTA barriers per tile: the RMS partials, then
+// the logit partials; warps 8..15 start the next tile while 0..7 finish the
+// tokens of this one.
+template <int KS>
+__global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma1_kernel(RouterArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int d = a.d, E = a.E;
+  const int rows = a.wg_next ? 2 * E : E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ld = d + 8;
+  uint16_t* gs = reinterpret_cast<uint16_t*>(smem);                  // 16 x ld
+  uint16_t* gam = gs + 16 * ld;                                        // d
+  double* sspart = reinterpret_cast<double*>(gam + d);                 // [kMmaWarps][8]
+  float* zpart = reinterpret_cast<float*>(sspart + kMmaWarps * kTokTile);  // [kMmaWarps][16][8]
+  for (int i = threadIdx.x; i < 16 * (d / 8); i += blockDim.x) {
+    const int r = i / (d / 8), c = i - r * (d / 8);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < E) v = reinterpret_cast<const uint4*>(a.wg + static_cast<size_t>(r) * d)[c];
+    else if (r < rows) v = reinterpret_cast<const uint4*>(a.wg_next + static_cast<size_t>(r - E) * d)[c];
+    *reinterpret_cast<uint4*>(gs + static_cast<size_t>(r) * ld + c * 8) = v;
+  }
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x)
+    reinterpret_cast<uint4*>(gam)[i] = reinterpret_cast<const uint4*>(a.gamma)[i];
+  __syncthreads();
+
+  const int g = lane >> 2, c2 = (lane & 3) * 2;
+  int P2 = 1;
+  while (P2 < E) P2 <<= 1;
+  const int k0w = warp * KS * 16;
+  const int64_t ntiles = (a.T + kTokTile - 1) / kTokTile;
+  constexpr int PF = 3;
+  auto prefetch_tile = [&](int64_t tl) {
+    if (tl >= ntiles) return;
+    const int64_t t0 = tl * kTokTile;
+    const int64_t n = (a.T - t0 < kTokTile ? a.T - t0 : kTokTile);
+    bulk_prefetch_l2(a.h + t0 * d, static_cast<uint32_t>(n * d * 4));  // rows are contiguous
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < PF; ++i) prefetch_tile(blockIdx.x + static_cast<int64_t>(i) * gridDim.x);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (threadIdx.x == 0) prefetch_tile(tile + static_cast<int64_t>(PF) * gridDim.x);
+    const int64_t t = tile * kTokTile + g;
+    const bool live = t < a.T;
+    const float* hrow = a.h + (live ? t : 0) * d;
+    float2 u[KS], v[KS];
 #pragma unroll
-          for (int o = P2 >> 1; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ov > bv || (ov == bv && oi < bi)) {
-              bv = ov;
-              bi = oi;
-            }
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = k0w + ks * 16 + c2;
+      u[ks] = live ? __ldg(reinterpret_cast<const float2*>(hrow + k)) : make_float2(0.f, 0.f);
+      v[ks] = live ? __ldg(reinterpret_cast<const float2*>(hrow + k + 8)) : make_float2(0.f, 0.f);
+    }
+    double ss = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+      ss = sq_acc(v[ks].y, sq_acc(v[ks].x, sq_acc(u[ks].y, sq_acc(u[ks].x, ss))));
+    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+    if ((lane & 3) == 0) sspart[warp * kTokTile + g] = ss;
+    __syncthreads();
+    double tot = 0.0;
+    for (int w = 0; w < kMmaWarps; ++w) tot += sspart[w * kTokTile + g];
+    const float r = rms_scale(tot, d, a.eps);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint16_t* xrow = a.x_out ? a.x_out + (live ? t : 0) * d : nullptr;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = k0w + ks * 16 + c2;
+      const uint32_t b0 = pack_x2(u[ks].x, u[ks].y, r, *reinterpret_cast<const uint32_t*>(gam + k));
+      const uint32_t b1 = pack_x2(v[ks].x, v[ks].y, r, *reinterpret_cast<const uint32_t*>(gam + k + 8));
+      if (live && xrow) {
+        *reinterpret_cast<uint32_t*>(xrow + k) = b0;
+        *reinterpret_cast<uint32_t*>(xrow + k + 8) = b1;
+      }
+      uint32_t af[4];
+      af[0] = *reinterpret_cast<const uint32_t*>(gs + g * ld + k);
+      af[1] = *reinterpret_cast<const uint32_t*>(gs + (g + 8) * ld + k);
+      af[2] = *reinterpret_cast<const uint32_t*>(gs + g * ld + k + 8);
+      af[3] = *reinterpret_cast<const uint32_t*>(gs + (g + 8) * ld + k + 8);
+      mma_bf16_16816(acc, af, b0, b1);
+    }
+    float* zb = zpart + warp * 16 * kTokTile;
+    zb[g * kTokTile + c2] = acc[0];
+    zb[g * kTokTile + c2 + 1] = acc[1];
+    zb[(g + 8) * kTokTile + c2] = acc[2];
+    zb[(g + 8) * kTokTile + c2 + 1] = acc[3];
+    __syncthreads();
+    if (warp < kTokTile) {
+      const int64_t tt = tile * kTokTile + warp;
+      if (tt < a.T) {
+        float zt = 0.f, zp = 0.f;
+        if (lane < E) {
+          for (int w = 0; w < kMmaWarps; ++w) {
+            zt += zpart[(w * 16 + lane) * kTokTile + warp];
+            if (a.wg_next) zp += zpart[(w * 16 + E + lane) * kTokTile + warp];
           }
-          bi = __shfl_sync(0xffffffffu, bi, 0);
-          bv = __shfl_sync(0xffffffffu, bv, 0);
-          if (bi >= E) {  // NaN scores never compare: first untaken id
-            bi = __ffs(__ballot_sync(0xffffffffu, !taken)) - 1;
-            bv = __shfl_sync(0xffffffffu, p, bi);
-          }
-          den += bv;
-          if (lane == j) {
-            my_sel = bi;
-            my_p = bv;
-          }
-          if (lane == bi) taken = true;
         }
-        if (lane < a.k) {
-          a.topk_idx[tt * a.k + lane] = my_sel;
-          a.topk_w[tt * a.k + lane] = my_p / den;
-          if (a.hist) atomicAdd(a.hist + (tt / a.tokens_per_seq) * a.hist_seq_stride + my_sel, 1);
-        }
+        token_finish(a, tt, lane, zt, zp, P2);
       }
     }
   }
@@ -524,6 +641,14 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) router_small_kernel(Route
 
 using namespace daop;
 
+// tuning switch (daop_set_router_mode): 1 = single-pass router where it applies
+static int g_router_single_pass = 1;
+
+extern "C" int daop_set_router_mode(int32_t single_pass) {
+  g_router_single_pass = single_pass != 0;
+  return DAOP_OK;
+}
+
 extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t* wg,
                            const uint16_t* wg_next, int64_t T, int32_t d, int32_t E, int32_t k,
                            float eps, uint16_t* x_out, float* p_true, float* p_pred,
@@ -545,6 +670,25 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
   if (T <= 128 && d % 8 == 0) {  // decode-sized batch: a CTA per token
     router_small_kernel<<<static_cast<int>(T), kSmallWarps * 32, 0, as_stream(st)>>>(a);
     DAOP_CHECK_LAUNCH("router_small");
+    return DAOP_OK;
+  }
+  // single-pass router: d = 256 * KS with KS in {4, 8, 12, 16} (h slice in registers)
+  const int ks1 = d % (16 * kMmaWarps) == 0 ? d / (16 * kMmaWarps) : 0;
+  if (rows <= 16 && g_router_single_pass && (ks1 == 4 || ks1 == 8 || ks1 == 12 || ks1 == 16)) {
+    const size_t smem1 = static_cast<size_t>(16) * (d + 8) * 2 + static_cast<size_t>(d) * 2 +
+                         kMmaWarps * kTokTile * 8 + kMmaWarps * 16 * kTokTile * 4;
+    const int64_t ntiles = (T + kTokTile - 1) / kTokTile;
+    const int blocks = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
+    auto launch1 = [&](auto kern) {
+      DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem1)));
+      kern<<<blocks, kMmaWarps * 32, smem1, as_stream(st)>>>(a);
+      return DAOP_OK;
+    };
+    int rc = ks1 == 4 ? launch1(router_mma1_kernel<4>) : ks1 == 8 ? launch1(router_mma1_kernel<8>)
+             : ks1 == 12 ? launch1(router_mma1_kernel<12>) : launch1(router_mma1_kernel<16>);
+    if (rc) return rc;
+    DAOP_CHECK_LAUNCH("router_single_pass");
     return DAOP_OK;
   }
   const size_t smem_mma = static_cast<size_t>(16) * (d + 8) * 2 + static_cast<size_t>(d) * 2 +

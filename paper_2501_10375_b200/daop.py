@@ -52,6 +52,7 @@ from . import _lib, ops
 from .errors import ConfigError, ShapeMismatchError
 from .engine import SKINNY_MAX_ROWS
 from .model import KIND_EXPERT, MoEModel, make_tag
+from .nvtx import nvtx_pop, nvtx_push, nvtx_range
 from .placement import (SWAP_IN_OUT_DEFAULT, ExpertPlacement, SwapEvent,
                         allocate_for_sequence, init_from_calibration)
 from .policies import (ExecutedExpert, LayerPlan, PolicyConfig, decode_counters, make_planner,
@@ -261,10 +262,13 @@ class DaopEngine:
         slow_execs = 0
         mig_timing = []  # per layer: (migration start, copies done, resident GEMMs done)
         for l in range(L):
-            h = self._non_moe_prefill(h, l)
+            nvtx_push(f"prefill/L{l}")
+            with nvtx_range("attention"):
+                h = self._non_moe_prefill(h, l)
             nxt = m.gate[l + 1] if l + 1 < L else None
-            r = ops.router(h, m.norm[l], m.gate[l], nxt, k, hist=hist[:, l], tokens_per_seq=T,
-                           hist_seq_stride=L * E)
+            with nvtx_range("router"):
+                r = ops.router(h, m.norm[l], m.gate[l], nxt, k, hist=hist[:, l],
+                               tokens_per_seq=T, hist_seq_stride=L * E)
             swapped_in, mig_evs = [], []
             # a layer whose every expert is cached has no uncached (hot)
             # candidate, so Alg. 1 cannot swap there: no host round trip
@@ -310,9 +314,11 @@ class DaopEngine:
             skinny = rows <= SKINNY_MAX_ROWS  # weights as the M side (engine.py)
             up = ops.expert_gemm_up_skinny if skinny else ops.expert_gemm_up
             down = ops.expert_gemm_down_skinny if skinny else ops.expert_gemm_down
-            up(pr["x_perm"], pr["offsets"], slot_now, m.slab, m.n_slots, m.slot_elems, d, m.ffn,
-               out=act)
-            down(act, pr["offsets"], slot_now, m.slab, m.n_slots, m.slot_elems, d, m.ffn, out=y)
+            with nvtx_range("experts/resident"):
+                up(pr["x_perm"], pr["offsets"], slot_now, m.slab, m.n_slots, m.slot_elems, d,
+                   m.ffn, out=act)
+                down(act, pr["offsets"], slot_now, m.slab, m.n_slots, m.slot_elems, d, m.ffn,
+                     out=y)
             if swapped_in:
                 g1 = torch.cuda.Event(enable_timing=True)
                 g1.record()
@@ -326,6 +332,7 @@ class DaopEngine:
                 down(act, pr["offsets"], slot_mig, m.slab, m.n_slots, m.slot_elems, d, m.ffn,
                      out=y)
             if slow:
+                nvtx_push("experts/host_tier")
                 x_ready.synchronize()
                 # the host tier's results go up on their own stream, so the GPU
                 # clock records when the slow experts finished (for the hidden-
@@ -344,11 +351,13 @@ class DaopEngine:
                 torch.cuda.current_stream().wait_event(hev)
                 if swapped_in:
                     mig_timing[-1][3] = hev
+                nvtx_pop()
             out = ops.combine(h, y, pr["inv"], r["topk_w"])
             p_host[0, l].copy_(r["p"], non_blocking=True)
             if nxt is not None:
                 p_host[1, l].copy_(r["p_pred"], non_blocking=True)
             h = out
+            nvtx_pop()
         torch.cuda.synchronize()
         true_sc = np.ascontiguousarray(p_host[0].numpy().transpose(1, 0, 2), dtype=np.float64)
         pred_sc = np.ascontiguousarray(p_host[1].numpy().transpose(1, 0, 2), dtype=np.float64)
@@ -491,6 +500,7 @@ class DaopEngine:
             queued[l] = (hs, hf, futs)
 
         for l in range(L):
+            nvtx_push(f"decode/L{l}")
             h = self._non_moe(h, l, pos)
             b = self.bufs[l % 2]
             ht, v = mh[l]
@@ -506,6 +516,7 @@ class DaopEngine:
                 deferred.append(l)  # all picks resident: no host work, read later
                 h = b.h_out
                 prev_b, prev_v = b, v
+                nvtx_pop()
                 continue
             plan_on_host = mode == 1 and not full[l]
             if plan_on_host and l not in queued:
@@ -543,6 +554,7 @@ class DaopEngine:
             else:
                 h = b.h_out
             prev_b, prev_v = b, v
+            nvtx_pop()
         torch.cuda.synchronize()
         if deferred:  # every picked expert resident: no degradations to read
             dl = np.asarray(deferred)

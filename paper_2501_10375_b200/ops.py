@@ -72,6 +72,11 @@ def router(h, gamma, wg, wg_next, k, *, hist=None, tokens_per_seq=0, hist_seq_st
     return {"x": x, "p": p, "p_pred": pp, "topk_idx": idx, "topk_w": w}
 
 
+def set_router_mode(single_pass: bool) -> None:
+    """Tuning switch: single-pass tensor-core router (default) or two-pass."""
+    _lib.call("daop_set_router_mode", int(bool(single_pass)))
+
+
 def permute(topk_idx, num_experts, x=None):
     """Stable (expert, token, j) permutation; gathers x rows when given."""
     _dev(topk_idx, x)

@@ -29,13 +29,15 @@ def test_reference_api_names_present():
 
 
 def test_error_codes_map_to_reference_classes():
-    with pytest.raises(P.BudgetError):
+    with pytest.raises(P.BudgetError) as ei:
         P.init_from_calibration(np.ones((4, 4)), 0.1, P.ModelShape(4, 4, 2))
+    # the native code's message is carried into the raised exception
+    msg = _lib.LIB.daop_last_error().decode()
+    assert "budget" in msg.lower() and msg in str(ei.value)
     with pytest.raises(P.BudgetError):
         P.init_from_calibration(np.ones((4, 4)), float("nan"), P.ModelShape(4, 4, 2))
     with pytest.raises(P.ShapeMismatchError):
         P.init_from_calibration(np.ones((2, 4)), 0.5, P.ModelShape(3, 4, 2))
-    assert "budget" in _lib.LIB.daop_last_error().decode().lower() or True
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")

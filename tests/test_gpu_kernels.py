@@ -534,3 +534,25 @@ def test_batched_decode_graph_replay_bitexact(P, B):
         torch.cuda.synchronize()
         for key in ("out", "topk_idx", "topk_w", "p", "offsets"):
             assert torch.equal(r[key], want[key]), (step, key)
+
+
+@pytest.mark.parametrize("d,T", [(1024, 129), (4096, 1000), (4096, 4099), (6144, 300), (3072, 777)])
+def test_router_single_pass_equals_two_pass(P, d, T):
+    """The single-pass router (h slice in registers) and the two-pass one
+    (L2 re-read) produce identical bits: x, p, p_pred, top-k, weights, counts."""
+    pkg, model_mod, ops = P
+    E, k = 8, 2
+    m = model_mod.MoEModel(pkg.ModelShape(2, E, k), d, 512, seed=2, resident_layers=[])
+    h = m.input_hidden(T, stream=8)
+    outs = []
+    for mode in (1, 0):
+        ops.set_router_mode(mode)
+        hist = torch.zeros((2, E), dtype=torch.int32, device="cuda")
+        r = ops.router(h, m.norm[0], m.gate[0], m.gate[1], k, hist=hist, tokens_per_seq=(T + 1) // 2,
+                       hist_seq_stride=E)
+        outs.append((r, hist))
+    ops.set_router_mode(1)
+    (r1, h1), (r0, h0) = outs
+    for key in ("x", "p", "p_pred", "topk_idx", "topk_w"):
+        assert torch.equal(r1[key], r0[key]), key
+    assert torch.equal(h1, h0)
