@@ -191,6 +191,12 @@ int daop_combine_dense(const float* d_h, const float* d_y, const float* d_w, int
 int daop_host_expert_ffn(const uint16_t* h_x, int64_t n, const uint16_t* h_w1,
                          const uint16_t* h_w3, const uint16_t* h_w2, int32_t d, int32_t ffn,
                          float* h_y, uint16_t* h_act_scratch, int32_t threads);
+/* Pinned host memory for the expert pool (the slow tier and the migration
+ * source): mmap + transparent huge pages, parallel first touch on `threads`
+ * cores (<= 0: all), cudaHostRegister (*h_registered = 1; 0 when the host has
+ * no CUDA device, e.g. a build machine).  Free with daop_host_pool_free. */
+int daop_host_pool_alloc(int64_t bytes, int32_t threads, void** h_out, int32_t* h_registered);
+int daop_host_pool_free(void* h_ptr, int64_t bytes, int32_t registered);
 int daop_host_caps(int32_t* avx512_bf16, int32_t* hw_threads);
 
 /* Host-tier scheduling: rows per work chunk of the up / down GEMV phases

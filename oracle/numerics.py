@@ -220,13 +220,20 @@ class OracleAttention:
     def norm(self, layer):
         return rng.norm_weight(self.seed, layer + NORM_LAYER_OFFSET, self.d)
 
-    def wqkv(self, layer):
-        return rng.tensor_bf16(self.seed, rng.make_tag(KIND_ATTN, layer, 0, 0),
-                               (self.q_dim + 2 * self.kv_dim, self.d), self.s_in)
+    def _cached(self, key, make):
+        cache = self.__dict__.setdefault("_cache", {})
+        if key not in cache:
+            cache[key] = make()
+        return cache[key]
+
+    def wqkv(self, layer):  # generated once per layer (token-by-token oracle runs)
+        return self._cached(("qkv", layer), lambda: rng.tensor_bf16(
+            self.seed, rng.make_tag(KIND_ATTN, layer, 0, 0),
+            (self.q_dim + 2 * self.kv_dim, self.d), self.s_in))
 
     def wo(self, layer):
-        return rng.tensor_bf16(self.seed, rng.make_tag(KIND_ATTN, layer, 0, 1),
-                               (self.d, self.q_dim), self.s_o)
+        return self._cached(("o", layer), lambda: rng.tensor_bf16(
+            self.seed, rng.make_tag(KIND_ATTN, layer, 0, 1), (self.d, self.q_dim), self.s_o))
 
 
 def rope(x: np.ndarray, pos: int, theta: float) -> np.ndarray:
@@ -246,7 +253,8 @@ def attention_decode(att: OracleAttention, layer: int, h: np.ndarray, pos: int,
     of the bf16 cache (entries < pos used as given; pos is written here).
     Returns (h_out, xa, k_cache, v_cache)."""
     xa = rmsnorm(h[None, :], att.norm(layer))[0]
-    qkv = (att.wqkv(layer).astype(np.float64) @ xa.astype(np.float64)).astype(np.float32)
+    w64 = att._cached(("qkv64", layer), lambda: att.wqkv(layer).astype(np.float64))
+    qkv = (w64 @ xa.astype(np.float64)).astype(np.float32)
     q = qkv[: att.q_dim].reshape(att.n_heads, HEAD_DIM)
     k = qkv[att.q_dim: att.q_dim + att.kv_dim].reshape(att.n_kv, HEAD_DIM)
     v = qkv[att.q_dim + att.kv_dim:].reshape(att.n_kv, HEAD_DIM)
@@ -265,5 +273,6 @@ def attention_decode(att: OracleAttention, layer: int, h: np.ndarray, pos: int,
         p /= p.sum()
         o[hd] = p @ v_cache[g, : pos + 1].astype(np.float64)
     o_b = rng.round_bf16(o.reshape(-1).astype(np.float32))
-    y = (att.wo(layer).astype(np.float64) @ o_b.astype(np.float64)).astype(np.float32)
+    wo64 = att._cached(("o64", layer), lambda: att.wo(layer).astype(np.float64))
+    y = (wo64 @ o_b.astype(np.float64)).astype(np.float32)
     return h.astype(np.float32) + y, xa, k_cache, v_cache

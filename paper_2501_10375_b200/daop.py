@@ -39,6 +39,7 @@ slow tier its inputs); the decision path is fully on device.
 
 from __future__ import annotations
 
+import ctypes
 import os
 import threading
 import time
@@ -69,7 +70,15 @@ class HostExpertPool:
         self.shape, self.d, self.ffn, self.seed = shape, d, ffn, seed
         L, E = shape.num_layers, shape.num_experts
         self.slot_elems = 3 * ffn * d
-        self.buf = torch.empty((L * E, self.slot_elems), dtype=torch.bfloat16, pin_memory=True)
+        # pinned by the library: mmap + huge pages + parallel first touch +
+        # cudaHostRegister (~5x faster than cudaHostAlloc for 90 GB)
+        self._nbytes = L * E * self.slot_elems * 2
+        ptr, reg = ctypes.c_void_p(), ctypes.c_int32(0)
+        _lib.call("daop_host_pool_alloc", self._nbytes, 0, ctypes.addressof(ptr),
+                  ctypes.addressof(reg))
+        self._ptr, self.pinned = ptr.value, bool(reg.value)
+        arr = np.ctypeslib.as_array((ctypes.c_int16 * (self._nbytes // 2)).from_address(self._ptr))
+        self.buf = torch.from_numpy(arr).view(torch.bfloat16).view(L * E, self.slot_elems)
         sc_in = float(np.float32(1.0 / np.sqrt(d)))
         sc_ff = float(np.float32(1.0 / np.sqrt(ffn)))
         mats = ((0, ffn * d, sc_in), (ffn * d, ffn * d, sc_in), (2 * ffn * d, d * ffn, sc_ff))
@@ -95,6 +104,18 @@ class HostExpertPool:
                 for mtx, (off, n, sc) in enumerate(mats):
                     _lib.call("daop_fill_uniform_bf16_host", base + off * 2, n, seed,
                               make_tag(KIND_EXPERT, l, e, mtx), sc, 0, th)
+
+    def close(self):
+        if getattr(self, "_ptr", None):
+            self.buf = None
+            _lib.call("daop_host_pool_free", self._ptr, self._nbytes, int(self.pinned))
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
 
     def slot(self, layer: int, expert: int) -> torch.Tensor:
         return self.buf[layer * self.shape.num_experts + expert]

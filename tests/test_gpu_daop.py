@@ -205,3 +205,5 @@ def test_host_pool_device_fill_matches_host_fill():
     a = HostExpertPool(shape, 256, 512, seed=9)
     b = HostExpertPool(shape, 256, 512, seed=9, device="cuda")
     assert torch.equal(a.buf.view(torch.int16), b.buf.view(torch.int16))
+    # registered with the driver: copies from it are true async DMAs
+    assert b.pinned and b.buf.is_pinned()
