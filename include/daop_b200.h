@@ -153,10 +153,16 @@ int daop_fill_uniform_bf16_host(uint16_t* h_dst, int64_t n, uint64_t seed, uint6
  * lower id (_kernels.py:63-79), renormalised weights, and the per-sequence
  * activation counter d_hist[(t / tokens_per_seq) * hist_seq_stride + e] += 1
  * (metrics.expert_counts, metrics.py:64-71) when d_hist != NULL. */
-/* tuning: 1 (default) = single-pass tensor-core router where d = 256 * {4, 8,
- * 12, 16} (h slice held in registers: one HBM + one L2 read of h), 0 = the
- * two-pass variant; the two are bit-identical (tests). */
-int daop_set_router_mode(int32_t single_pass);
+/* tuning: bit 0 = 1 (default) single-pass tensor-core router where d = 256 *
+ * {4, 8, 12, 16} (h slice held in registers), 0 = the two-pass variant (the
+ * two are bit-identical, tests); bits 4..7 = 1 + the single-pass kernel's L2
+ * prefetch distance in grid-strides (0 = keep). */
+int daop_set_router_mode(int32_t mode);
+/* tuning: gather / combine kernel variants (0 = default bulk-DMA kernels for
+ * large T, 1 = warp-per-token register kernels), bulk gather CTAs per SM and
+ * combine ring stages (<= 0 keeps the current value). */
+int daop_set_stream_mode(int32_t gather, int32_t combine, int32_t gather_ctas_per_sm,
+                         int32_t combine_stages);
 int daop_router(const float* d_h, const uint16_t* d_gamma, const uint16_t* d_wg,
                 const uint16_t* d_wg_next, int64_t t, int32_t d, int32_t num_experts, int32_t k,
                 float eps, uint16_t* d_x, float* d_p_true, float* d_p_pred, int32_t* d_topk_idx,

@@ -405,7 +405,21 @@ __global__ void combine_dense_kernel(const float* __restrict__ h, const float* _
 
 using namespace daop;
 
+// tuning (daop_set_stream_mode): gather 0 = auto (bulk DMA rows for large T),
+// 1 = warp-per-token registers; combine 0 = auto (bulk), 1 = warp-per-token
+static int g_gather_variant = 0, g_combine_variant = 0;
+static int g_bulk_ctas_per_sm = 4, g_combine_stages = 4;
+
 extern "C" {
+
+int daop_set_stream_mode(int32_t gather, int32_t combine, int32_t gather_ctas_per_sm,
+                         int32_t combine_stages) {
+  g_gather_variant = gather;
+  g_combine_variant = combine;
+  if (gather_ctas_per_sm > 0) g_bulk_ctas_per_sm = gather_ctas_per_sm;
+  if (combine_stages > 0) g_combine_stages = combine_stages;
+  return DAOP_OK;
+}
 
 int daop_permute_workspace(int64_t T, int32_t k, int32_t E, int64_t* bytes) {
   const int64_t n = T * k;
@@ -452,12 +466,13 @@ int daop_permute(const int32_t* ids, int64_t T, int32_t k, int32_t E, const uint
     const size_t row = static_cast<size_t>(d) * 2;
     if (T < 2 * sm_count()) {  // decode-sized batches
       gather_small_kernel<<<static_cast<int>(T), 256, 0, st>>>(xs, inv, k, d / 8, xp);
-    } else if (T >= 4 * sm_count() && row % 16 == 0 && row <= 16 * 1024) {
+    } else if (g_gather_variant == 0 && T >= 4 * sm_count() && row % 16 == 0 && row <= 16 * 1024) {
       const int stages = static_cast<int>(std::min<size_t>(16, (48 * 1024) / row));
       const size_t smem = row * stages + 16 * 8 + 64;
       DAOP_CUDA(cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-      gather_bulk_kernel<<<4 * sm_count(), 32, smem, st>>>(x, inv, T, k, d, stages, x_perm);
+      gather_bulk_kernel<<<g_bulk_ctas_per_sm * sm_count(), 32, smem, st>>>(x, inv, T, k, d,
+                                                                         stages, x_perm);
     } else if (k == 2)
       perm_gather_kernel<2><<<static_cast<int>(blocks), 256, 0, st>>>(xs, inv, T, k, d / 8, xp);
     else
@@ -487,9 +502,9 @@ int daop_combine(const float* h, const float* y_sorted, const int32_t* inv, cons
     DAOP_CHECK_LAUNCH("combine_small");
     return DAOP_OK;
   }
-  if (k == 2 && d % 4 == 0 && T >= sm_count()) {
+  if (g_combine_variant == 0 && k == 2 && d % 4 == 0 && T >= sm_count()) {
     const size_t stage = static_cast<size_t>(d) * 4 * 3;
-    const int stages = static_cast<int>(std::min<size_t>(4, (200 * 1024) / stage));
+    const int stages = static_cast<int>(std::min<size_t>(g_combine_stages, (200 * 1024) / stage));
     if (stages >= 2) {
       const size_t smem = stage * stages + 64;
       DAOP_CUDA(cudaFuncSetAttribute(combine_bulk_kernel<2>,

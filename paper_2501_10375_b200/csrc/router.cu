@@ -39,6 +39,7 @@ struct RouterArgs {
   int32_t* hist;  // per layer slice base or null
   int64_t tokens_per_seq;
   int64_t hist_seq_stride;
+  int prefetch_tiles;  // single-pass router: L2 prefetch distance in grid-strides (0: none)
 };
 
 // softmax over E <= 32 logits held one per lane (max-subtracted, fp32)
@@ -452,9 +453,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma1_kernel(RouterAr
   while (P2 < E) P2 <<= 1;
   const int k0w = warp * KS * 16;
   const int64_t ntiles = (a.T + kTokTile - 1) / kTokTile;
-  constexpr int PF = 3;
+  const int PF = a.prefetch_tiles;
   auto prefetch_tile = [&](int64_t tl) {
-    if (tl >= ntiles) return;
+    if (PF <= 0 || tl >= ntiles) return;
     const int64_t t0 = tl * kTokTile;
     const int64_t n = (a.T - t0 < kTokTile ? a.T - t0 : kTokTile);
     bulk_prefetch_l2(a.h + t0 * d, static_cast<uint32_t>(n * d * 4));  // rows are contiguous
@@ -643,9 +644,13 @@ using namespace daop;
 
 // tuning switch (daop_set_router_mode): 1 = single-pass router where it applies
 static int g_router_single_pass = 1;
+static int g_router_prefetch = 1;
 
-extern "C" int daop_set_router_mode(int32_t single_pass) {
-  g_router_single_pass = single_pass != 0;
+// bit 0: single pass; bits 4..7: + 1 = L2 prefetch distance of the single-pass
+// kernel in grid-strides (0 in those bits keeps the current distance)
+extern "C" int daop_set_router_mode(int32_t mode) {
+  g_router_single_pass = mode & 1;
+  if ((mode >> 4) & 15) g_router_prefetch = ((mode >> 4) & 15) - 1;
   return DAOP_OK;
 }
 
@@ -665,7 +670,7 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
   if (T == 0) return DAOP_OK;
   if (hist && tokens_per_seq <= 0) tokens_per_seq = T;
   RouterArgs a{h, gamma, wg, wg_next, T, d, E, k, eps, x_out, p_true, p_pred,
-               topk_idx, topk_w, hist, tokens_per_seq, hist_seq_stride};
+               topk_idx, topk_w, hist, tokens_per_seq, hist_seq_stride, g_router_prefetch};
   const int rows = wg_next ? 2 * E : E;
   if (T <= 128 && d % 8 == 0) {  // decode-sized batch: a CTA per token
     router_small_kernel<<<static_cast<int>(T), kSmallWarps * 32, 0, as_stream(st)>>>(a);

@@ -72,9 +72,17 @@ def router(h, gamma, wg, wg_next, k, *, hist=None, tokens_per_seq=0, hist_seq_st
     return {"x": x, "p": p, "p_pred": pp, "topk_idx": idx, "topk_w": w}
 
 
-def set_router_mode(single_pass: bool) -> None:
-    """Tuning switch: single-pass tensor-core router (default) or two-pass."""
-    _lib.call("daop_set_router_mode", int(bool(single_pass)))
+def set_router_mode(single_pass: bool, prefetch: int = -1) -> None:
+    """Tuning switch: single-pass tensor-core router (default) or two-pass;
+    prefetch >= 0 sets the single-pass kernel's L2 prefetch distance."""
+    mode = int(bool(single_pass)) | ((prefetch + 1) << 4 if prefetch >= 0 else 0)
+    _lib.call("daop_set_router_mode", mode)
+
+
+def set_stream_mode(gather: int = 0, combine: int = 0, gather_ctas_per_sm: int = 0,
+                    combine_stages: int = 0) -> None:
+    """Tuning switch for the gather / combine kernels (daop_set_stream_mode)."""
+    _lib.call("daop_set_stream_mode", gather, combine, gather_ctas_per_sm, combine_stages)
 
 
 def permute(topk_idx, num_experts, x=None):

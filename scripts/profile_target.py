@@ -13,7 +13,13 @@ ops.set_gemm_mode(int(os.environ.get("DAOP_GEMM_MODE", "0")))
 d, ffn, E, k = 4096, 14336, 8, 2
 m = MoEModel(P.ModelShape(2, E, k), d, ffn, seed=0, resident_layers=[0])
 eng = MoEBlockEngine(m)
-if what == "decode":
+if what == "attn_prefill":  # 256-token prompt through one attention layer (tcgen05 + mma.sync)
+    from paper_2501_10375_b200.attention import AttentionStack
+    att = AttentionStack(1, d, 32, 8, max_seq=512)
+    hp = m.input_hidden(256, stream=6)
+    for _ in range(3):
+        att.prefill(hp, 0, 0)
+elif what == "decode":
     hs = [m.input_hidden(1, stream=9, step=i)[0] for i in range(8)]
     for i in range(8):
         eng.decode(hs[i])

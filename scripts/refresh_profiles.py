@@ -34,7 +34,7 @@ def main():
     dst = ROOT / "profiles" / rnd
     dst.mkdir(parents=True, exist_ok=True)
     full = {}
-    for name in ("decode", "gemm", "router", "skinny", "attention", "ep"):
+    for name in ("decode", "gemm", "router", "attn_prefill", "skinny", "attention", "ep"):
         rep = OUT / f"prof_{name}.ncu-rep"
         if rep.exists():
             full[name] = summarise(str(rep))
