@@ -735,14 +735,21 @@ def run_decoder32(args, world, dev, eng, model, hs, hbm_peak, barrier):
     torch.cuda.synchronize()
     nt = max(10, min(100, args.steps // 20))
     stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(nt):
-        h_in.copy_(hs[i % len(hs)])
-        eng.decode_token(h_in, start=4, daop=True, attn=att, pos=DEC_CTX + 3 + i % 200)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    tok_ms = e0.elapsed_time(e1) / nt
+
+    def run(prefetch):
+        eng.attn_prefetch = prefetch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(nt):
+            h_in.copy_(hs[i % len(hs)])
+            eng.decode_token(h_in, start=4, daop=True, attn=att, pos=DEC_CTX + 3 + i % 200)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / nt
+
+    no_pf_ms = run(False)  # attention weights streamed by the attention GEMVs
+    tok_ms = run(True)     # default: next layer's attention weights prefetched into L2
+    eng.attn_prefetch = True
     t = torch.tensor([tok_ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -760,7 +767,8 @@ def run_decoder32(args, world, dev, eng, model, hs, hbm_peak, barrier):
                      "peak": hbm_peak, "unit": "GB/s",
                      "frac": bytes_tok / (tok_ms / 1e3) / 1e9 / hbm_peak,
                      "bytes_per_token": bytes_tok},
-        "gpu_launches": nt * L * 5,
+        "without_attn_l2_prefetch": {"tokens_per_s": 1e3 / no_pf_ms, "ms_per_token": no_pf_ms},
+        "gpu_launches": nt * L * 6,
     }
 
 EP_D, EP_FFN, EP_TOKENS = 6144, 16384, 8 * 4096
@@ -930,7 +938,8 @@ def run_b200_ep(args, world, rank, local_rank):
     hbm_peak, tf_peak, tf_sus, peak_kind = peaks()
 
     def barrier():
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
 
     head = run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", steps=args.steps,
                   warmup=args.warmup, e2e=True)
@@ -1071,6 +1080,8 @@ def main():
     ap.add_argument("--daop-ecr", type=float, nargs="+", default=[0.5])
     ap.add_argument("--daop-tokens", type=int, default=16)
     ap.add_argument("--daop-all-ranks", action="store_true")
+    ap.add_argument("--ep-headline", action="store_true",
+                    help="N = 1: run the N > 1 expert-parallel headline path (exercises it on one GPU)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -1084,7 +1095,8 @@ def main():
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        line = (run_b200_ep if world > 1 else run_b200)(args, world, rank, local_rank)
+        ep_head = world > 1 or args.ep_headline
+        line = (run_b200_ep if ep_head else run_b200)(args, world, rank, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

@@ -380,6 +380,12 @@ int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const uint16_t* 
                      float theta, uint16_t* d_xa_out, float* d_h_out, void* d_workspace,
                      daop_stream_t stream);
 
+/* L2 prefetch of up to two byte ranges on `stream` (fire and forget): the
+ * decode loop issues the next layer's Wqkv / Wo before this layer's MoE
+ * decode kernel, whose expert stream is L2::evict_first. */
+int daop_l2_prefetch(const void* d_p0, int64_t n0, const void* d_p1, int64_t n1,
+                     daop_stream_t stream);
+
 /* Prefill of T prompt tokens through the same attention block, positions
  * pos0 .. pos0 + T - 1 (the calls DaopEngine.prefill makes per layer; the
  * reference prices this as the prefill t_nonmoe, simulator.py:438-441):

@@ -94,6 +94,16 @@ class AttentionStack:
         # O projection with the residual added in the GEMM epilogue
         return ops.gemm_bf16_f32(o, self.wo[layer], resid=h, out=out)
 
+    def prefetch_l2(self, layer: int) -> None:
+        """Queue an L2 prefetch of `layer`'s Wqkv and Wo (84 MB at the
+        Mixtral-8x7B shape) on the current stream (daop_l2_prefetch): issued
+        before the previous layer's MoE decode kernel, it is in L2 when this
+        layer's attention GEMVs run."""
+        if 0 <= layer < self.L:
+            a, b = self.wqkv[layer], self.wo[layer]
+            _lib.call("daop_l2_prefetch", a.data_ptr(), a.numel() * 2, b.data_ptr(),
+                      b.numel() * 2, ops._s())
+
     def bytes_per_token_layer(self, ctx: int) -> int:
         """Algorithmic HBM bytes of one decode step of one layer at context
         length ctx: Wqkv + Wo + the k, v rows read (bf16)."""

@@ -774,6 +774,25 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
   }
 }
 
+// L2 prefetch of up to two byte ranges (the next layer's attention weights,
+// issued just before this layer's MoE decode kernel): the MoE kernel streams
+// its experts with L2::evict_first, so the prefetched lines survive it and
+// the next QKV / O-proj GEMVs read L2 instead of ramping up on HBM
+constexpr int64_t PF_CHUNK = 32 * 1024;
+__global__ void l2_prefetch_kernel(const uint8_t* __restrict__ p0, int64_t n0,
+                                   const uint8_t* __restrict__ p1, int64_t n1) {
+  const int64_t c0 = (n0 + PF_CHUNK - 1) / PF_CHUNK, c1 = (n1 + PF_CHUNK - 1) / PF_CHUNK;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < c0 + c1;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint8_t* p = c < c0 ? p0 + c * PF_CHUNK : p1 + (c - c0) * PF_CHUNK;
+    const int64_t rem = c < c0 ? n0 - c * PF_CHUNK : n1 - (c - c0) * PF_CHUNK;
+    const uint32_t bytes = static_cast<uint32_t>(rem < PF_CHUNK ? rem : PF_CHUNK);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)),
+                 "r"(bytes)
+                 : "memory");
+  }
+}
+
 }  // namespace daop
 
 using namespace daop;
@@ -889,5 +908,19 @@ extern "C" int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const
                                                               d_h_out);
     DAOP_CHECK_LAUNCH("attn_oproj");
   }
+  return DAOP_OK;
+}
+
+extern "C" int daop_l2_prefetch(const void* d_p0, int64_t n0, const void* d_p1, int64_t n1,
+                                daop_stream_t stream) {
+  if (n0 < 0 || n1 < 0 || (n0 % 16) || (n1 % 16) ||
+      (reinterpret_cast<uintptr_t>(d_p0) % 16) || (reinterpret_cast<uintptr_t>(d_p1) % 16)) {
+    set_error("l2_prefetch: ranges must be 16-byte aligned multiples of 16 bytes");
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (n0 + n1 == 0) return DAOP_OK;
+  l2_prefetch_kernel<<<sm_count(), 32, 0, as_stream(stream)>>>(
+      static_cast<const uint8_t*>(d_p0), n0, static_cast<const uint8_t*>(d_p1), n1);
+  DAOP_CHECK_LAUNCH("l2_prefetch");
   return DAOP_OK;
 }

@@ -44,6 +44,9 @@ class MoEBlockEngine:
         self._h_host = None
         self._out_host = None
         self._sel_host = None
+        # full decoder layers: prefetch layer l+1's attention weights into L2
+        # while layer l's MoE kernel streams its experts (tuning switch)
+        self.attn_prefetch = True
 
     # ------------------------------------------------------------ decode
     def decode(self, h: torch.Tensor, layer: int = 0, *, pred_prev=None, mode: int = 0,
@@ -143,6 +146,8 @@ class MoEBlockEngine:
         for l in range(L):
             if attn is not None:
                 cur = attn.decode(cur, l, pos, out=self._ha)
+                if self.attn_prefetch:
+                    attn.prefetch_l2(l + 1)  # streams beside this layer's MoE kernel
             b = self._pp[l % 2]
             mode = 1 if (daop and l >= start) else 0
             nxt = m.gate[l + 1] if l + 1 < L else None

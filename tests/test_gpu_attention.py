@@ -146,3 +146,24 @@ def test_dense_gemm_parity(P, M, K, N, resid):
         assert torch.equal(r2, out)
     torch.cuda.synchronize()
     close(out.cpu().numpy(), ref, f"gemm {M}x{K}x{N}")
+
+
+def test_decode_token_with_attention_l2_prefetch_is_bit_identical(P):
+    """The next layer's attention weights prefetched into L2 during the MoE
+    kernel (daop_l2_prefetch) is a cache hint: bit-identical results."""
+    pkg, A = P
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    from paper_2501_10375_b200.model import MoEModel
+    L, d = 3, 1024
+    m = MoEModel(pkg.ModelShape(L, 8, 2), d, 1024, seed=2)
+    outs = []
+    for pf in (False, True):
+        att = A.AttentionStack(L, d, 8, 2, max_seq=64, seed=2)
+        eng = MoEBlockEngine(m)
+        eng.attn_prefetch = pf
+        h = m.input_hidden(1, stream=3)[0]
+        for pos in range(3):
+            h = eng.decode_token(h, start=1, attn=att, pos=pos).clone()
+        outs.append(h)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
