@@ -97,6 +97,10 @@ struct GemmParams {
   // added in the down epilogue: out = resid + A . B^T (resid may alias out)
   int64_t dense_rows;
   const float* resid;
+  // epilogue stores as streaming (st.global.cs: evict-first in L2) so the
+  // 1.9 GB act / 1.1 GB y output streams do not push the re-read A / B
+  // operand tiles out of L2 (tuning bit, daop_set_gemm_mode bit 14)
+  int store_cs;
 };
 
 __device__ __forceinline__ int64_t off_at(const GemmParams& p, int e) {
@@ -107,7 +111,8 @@ __device__ __forceinline__ int slot_at(const GemmParams& p, int e) {
 }
 
 // 32 accumulator columns -> fp32 row slice (+ the residual when given)
-__device__ __forceinline__ void store_f32x32(float* out, const float* res, const uint32_t (&v)[32]) {
+__device__ __forceinline__ void store_f32x32(float* out, const float* res, const uint32_t (&v)[32],
+                                             bool cs) {
   float4* o = reinterpret_cast<float4*>(out);
   const float4* r = reinterpret_cast<const float4*>(res);
 #pragma unroll
@@ -121,7 +126,8 @@ __device__ __forceinline__ void store_f32x32(float* out, const float* res, const
       a.z += b.z;
       a.w += b.w;
     }
-    o[i] = a;
+    if (cs) __stcs(o + i, a);
+    else o[i] = a;
   }
 }
 
@@ -354,7 +360,12 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             uint4* o = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              o[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+            {
+              const uint4 pk = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                                          packed[4 * i + 3]);
+              if (p.store_cs) __stcs(o + i, pk);
+              else o[i] = pk;
+            }
           }
         }
       } else {
@@ -367,7 +378,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
           if (valid)
-            store_f32x32(out + c, p.resid ? p.resid + grow * p.out_ld + n * GB_N + c : nullptr, v);
+            store_f32x32(out + c, p.resid ? p.resid + grow * p.out_ld + n * GB_N + c : nullptr, v,
+                         p.store_cs);
         }
       }
       tc_fence_before();
@@ -704,7 +716,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
             uint4* o = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              o[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+            {
+              const uint4 pk = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                                          packed[4 * i + 3]);
+              if (p.store_cs) __stcs(o + i, pk);
+              else o[i] = pk;
+            }
           }
         }
       } else {
@@ -717,7 +734,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
           if (valid)
-            store_f32x32(out + c, p.resid ? p.resid + grow * p.out_ld + n * GB_N + c : nullptr, v);
+            store_f32x32(out + c, p.resid ? p.resid + grow * p.out_ld + n * GB_N + c : nullptr, v,
+                         p.store_cs);
         }
       }
       }
@@ -770,6 +788,7 @@ static size_t gemm_smem_bytes() { return 1024 + G_STAGES * G_STAGE_BYTES + sizeo
 // up, with 8 epilogue warps and the fast SwiGLU: 11.8 vs 12.0 ms; whole layer
 // 19.2 vs 19.6 ms -- profiles/r01/gemm_two_m.txt)
 static int g_gemm_two_m = 3;
+static int g_gemm_store_cs = 0;  // epilogue streaming stores (tuning)
 static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
 
 template <bool TWO_M>
@@ -789,6 +808,7 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
   int clusters = sm_count() / 2;
   if (max_tiles < clusters) clusters = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
   GemmParams pp = p;
+  pp.store_cs = g_gemm_store_cs;
   if (p.group_m < 0) {  // negative group = n-grouped raster of |group| weight tiles
     pp.raster = 1;
     pp.group_m = -p.group_m;
@@ -873,6 +893,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_demote = (mode >> 8) & 7;
   g_gemm_persist_off = (mode >> 11) & 1;
   g_gemm_two_m = ((mode >> 12) & 3) ^ 3;  // mode bits flip the default (tuning)
+  g_gemm_store_cs = (mode >> 14) & 1;
   return DAOP_OK;
 }
 
