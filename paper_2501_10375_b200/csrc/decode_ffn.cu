@@ -124,10 +124,9 @@ __device__ __forceinline__ Piece unpack_piece(uint32_t v) {
 
 struct WarpSel {
   const uint16_t* base[DK_MAX];  // slab slot base of each executed pick
-  float p[DE_MAX];               // this layer's gate probabilities
   float wsel[DK_MAX];            // combine weights, pick order
   int sel[DK_MAX];
-  int exec_q[DK_MAX];            // executed index -> pick
+  uint8_t exec_q[DK_MAX];        // executed index -> pick
   uint8_t fast[DK_MAX];
   int n_exec;
 };
@@ -277,8 +276,10 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   // (summed in pick order, like the reference renormalisation)
   // selsrc: the picks (any copy, read-only here); wsrc: weight source or
   // null; result into copy `dst` (this warp's own, or [DW] for the plan)
-  int cw = warp;  // the selection copy this warp streams / combines with
-  auto finish_selection = [&](const int* selsrc, const float* wsrc, int dst) {
+  int cw = warp;     // the selection copy this warp streams / combines with
+  float my_p = 0.f;  // this layer's gate probability of expert `lane` (registers)
+  // wsrc: 0 no weights, 1 from the carried prediction (s.pp), 2 from my_p
+  auto finish_selection = [&](const int* selsrc, int wsrc, int dst) {
     __syncwarp();
     WarpSel& o = s.ws[dst];
     int e = 0, slot = 0;
@@ -295,12 +296,13 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
       if (f) {
         const int pos = __popc(fm & ((1u << lane) - 1u));
         o.base[pos] = a.slab + static_cast<int64_t>(slot) * a.slot_stride;
-        o.exec_q[pos] = lane;
+        o.exec_q[pos] = static_cast<uint8_t>(lane);
       }
     }
     if (lane == 0) o.n_exec = __popc(fm);
     if (wsrc) {
-      const float v = lane < k ? wsrc[e] : 0.f;
+      const float pe = __shfl_sync(0xffffffffu, my_p, e);  // every lane: uniform shuffle
+      const float v = lane < k ? (wsrc == 1 ? s.pp[e] : pe) : 0.f;
       float den = 0.f;
       for (int q = 0; q < k; ++q) den += __shfl_sync(0xffffffffu, v, q);
       if (lane < k) o.wsel[lane] = v / den;
@@ -423,7 +425,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
       lane_topk(lane < E ? s.pp[lane] : 0.f, plan);
       if (lane == 0) s.nd = a.graceful ? degrade_smem(s.pp, E, plan, k, s.fast_row, s.drop, s.sub) : 0;
       __syncwarp();
-      finish_selection(plan, a.weights_from_pred ? s.pp : nullptr, DW);
+      finish_selection(plan, a.weights_from_pred ? 1 : 0, DW);
     }
     __syncthreads();
     cw = DW;  // the plan copy, read-only from here on
@@ -554,8 +556,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
         }
       __syncwarp();
       __threadfence_block();
-      const float p = lane_softmax(lane < E ? zfull[lane] : 0.f);
-      if (lane < E) s.ws[0].p[lane] = p;  // warp 0's copy: exported below
+      my_p = lane_softmax(lane < E ? zfull[lane] : 0.f);  // exported below
       __syncwarp();
     }
   }
@@ -565,23 +566,22 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     if (lane < E)
       for (int w = 0; w < DW; ++w) z += s.zpart[w][lane];
     if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][7] = gtimer();
-    const float p = lane_softmax(z);
+    my_p = lane_softmax(z);  // every warp computes the same probabilities
     WarpSel& me = s.ws[warp];
-    if (lane < E) me.p[lane] = p;  // this warp's copy (every warp computes the same)
     if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][9] = gtimer();
     if (mode0) {
-      lane_topk(p, me.sel);
+      lane_topk(my_p, me.sel);
       if (lane == 0 && warp == 0) s.nd = 0;
       __syncwarp();
       if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][10] = gtimer();
-      finish_selection(me.sel, me.p, warp);
+      finish_selection(me.sel, 2, warp);
       cw = warp;
       if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][11] = gtimer();
       start_stream();
     } else if (!a.weights_from_pred) {
       // PLAN mode, weights from this layer's own gate: the plan's picks
       // (read-only copy [DW]) re-weighted into this warp's copy
-      finish_selection(s.ws[DW].sel, me.p, warp);
+      finish_selection(s.ws[DW].sel, 2, warp);
       cw = warp;
     }
   }
@@ -610,7 +610,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   if (blockIdx.x == 0) {
     if (warp == 0) {
       const WarpSel& ex = s.ws[cw];  // warp 0's selection copy
-      if (lane < E) a.p_true[lane] = s.ws[0].p[lane];
+      if (lane < E) a.p_true[lane] = my_p;
       if (lane < k) {
         a.sel[lane] = ex.sel[lane];
         wrote_out = true;
