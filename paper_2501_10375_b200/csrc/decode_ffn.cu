@@ -636,8 +636,14 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     if (cur_j >= 0 && cur_cnt > 0 && lane == 0) {
       __threadfence();          // this warp's act rows -> visible GPU-wide
       const int tot_j = count_mod(cur_j * a.ffn, (cur_j + 1) * a.ffn, L.cta, L.G);
-      if (atomicAdd(&s.done1[cur_j], cur_cnt) + cur_cnt == tot_j)
+      if (atomicAdd(&s.done1[cur_j], cur_cnt) + cur_cnt == tot_j) {
+        // cumulativity: the other warps' act rows this warp observed through
+        // done1 are ordered before the grid-wide count (a consumer CTA then
+        // bulk-reads act_j; without this fence a fast consumer could pull a
+        // row of the previous token -- seen as a rare mismatch in server mode)
+        __threadfence();
         atomicAdd(a.ctr + 2 + cur_j, static_cast<unsigned>(tot_j));
+      }
     }
     cur_cnt = 0;
   };
@@ -746,7 +752,10 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     __syncwarp();
   }
   int grid_done = 0;
-  if (lane == 0 && cta_done) grid_done = atomicAdd(a.ctr, 1u) == gridDim.x - 1;
+  if (lane == 0 && cta_done) {
+    __threadfence();  // the CTA's result rows (other warps' stores + fences) before the count
+    grid_done = atomicAdd(a.ctr, 1u) == gridDim.x - 1;
+  }
   grid_done = __shfl_sync(0xffffffffu, grid_done, 0);
   if (grid_done) {  // the grid's last warp: reset for the next call, publish
     if (lane == 0) {

@@ -789,6 +789,7 @@ static size_t gemm_smem_bytes() { return 1024 + G_STAGES * G_STAGE_BYTES + sizeo
 // 19.2 vs 19.6 ms -- profiles/r01/gemm_two_m.txt)
 static int g_gemm_two_m = 3;
 static int g_gemm_store_cs = 0;  // epilogue streaming stores (tuning)
+static int g_gemm_dense_skinny = 1;  // tuning: small-M dense GEMMs on the skinny kernel
 static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
 
 template <bool TWO_M>
@@ -894,6 +895,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_persist_off = (mode >> 11) & 1;
   g_gemm_two_m = ((mode >> 12) & 3) ^ 3;  // mode bits flip the default (tuning)
   g_gemm_store_cs = (mode >> 14) & 1;
+  g_gemm_dense_skinny = !((mode >> 15) & 1);
   return DAOP_OK;
 }
 
@@ -989,6 +991,9 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
   return launch_gemm<false>(ta, tb, p, rows, as_stream(stream));
 }
 
+int skinny_dense_gemm(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w, int32_t N,
+                      const float* resid, float* out, cudaStream_t st);
+
 // Dense projection on the same tcgen05 pipeline (the prompt attention's QKV
 // and O projections, attention.py): out (M, N) fp32 = A (M, K) bf16 . W^T,
 // W (N, K) bf16 row-major, optionally + resid (M, N) fp32 (may alias out).
@@ -1002,6 +1007,10 @@ extern "C" int daop_gemm_bf16_f32(const uint16_t* a, int64_t M, int32_t K, const
     return DAOP_ERR_UNSUPPORTED;
   }
   if (M == 0) return DAOP_OK;
+  // prompt-sized M: the swap-AB skinny kernel (weights as the MMA M side), so
+  // the weight tiles spread over every SM instead of N / 256 CTA pairs
+  if (M <= 768 && g_gemm_dense_skinny)
+    return skinny_dense_gemm(a, M, K, w, N, resid, out, as_stream(stream));
   CUtensorMap ta, tb;
   int rc;
   const uint64_t adims[2] = {static_cast<uint64_t>(K), static_cast<uint64_t>(M)};

@@ -49,7 +49,21 @@ struct SkinnyParams {
   const uint64_t* sig_peers;
   int sig_G, sig_rank;
   unsigned sig_epoch;
+  // dense GEMM (daop_gemm_bf16_f32 for M <= 768): no offset / slot tables,
+  // one "expert" of dense_rows token rows, weight slot 0; down only: the
+  // residual added in the epilogue (may alias out); weights kept in L2
+  // (evict_normal) because every token block re-reads them
+  int64_t dense_rows;
+  const float* resid;
+  int w_keep;
 };
+
+__device__ __forceinline__ int64_t sk_off(const SkinnyParams& p, int e) {
+  return p.offsets ? p.offsets[e] : (e == 0 ? 0 : p.dense_rows);
+}
+__device__ __forceinline__ int sk_slot(const SkinnyParams& p, int e) {
+  return p.slot_of ? p.slot_of[e] : 0;
+}
 
 template <int NT>
 struct SkinnySmem {
@@ -119,9 +133,9 @@ __global__ void __launch_bounds__(192, 1)
     fence_mbar_init();
     int acc = 0;
     s.prefix[0] = 0;
-    for (int e = 0; e <= E; ++e) s.off[e] = p.offsets[e];
+    for (int e = 0; e <= E; ++e) s.off[e] = sk_off(p, e);
     for (int e = 0; e < E; ++e) {
-      const int64_t me = p.slot_of[e] >= 0 ? s.off[e + 1] - s.off[e] : 0;
+      const int64_t me = sk_slot(p, e) >= 0 ? s.off[e + 1] - s.off[e] : 0;
       s.blocks[e] = static_cast<int>((me + NT - 1) / NT);
       acc += s.blocks[e] * rt;
       s.prefix[e + 1] = acc;
@@ -135,13 +149,14 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      const uint64_t pol_w = l2_evict_first_policy();  // weights: streamed once
+      const uint64_t pol_w = p.w_keep ? l2_evict_normal_policy()   // re-read per token block
+                                      : l2_evict_first_policy();  // weights: streamed once
       const uint64_t pol_x = l2_evict_last_policy();   // tokens: re-read by every row tile
       int stage = 0;
       uint32_t phase = 0;
       int e, blk, r;
       for (int t = blockIdx.x; skinny_tile(s, E, rt, t, e, blk, r); t += gridDim.x) {
-        const int slot = p.slot_of[e];
+        const int slot = sk_slot(p, e);
         const int xrow = static_cast<int>(s.off[e]) + blk * NT;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
@@ -233,7 +248,8 @@ __global__ void __launch_bounds__(192, 1)
             if (c + j < nvalid) {
               float* dst = p.row_dst ? reinterpret_cast<float*>(p.row_dst[t0 + c + j]) + row
                                      : out + (t0 + c + j) * p.out_ld + row;
-              *dst = __uint_as_float(g[j]);
+              const float v = __uint_as_float(g[j]);
+              *dst = p.resid ? v + p.resid[(t0 + c + j) * p.out_ld + row] : v;
             }
         }
       }
@@ -379,4 +395,25 @@ extern "C" int daop_ep_expert_gemm_down_skinny(const uint16_t* act, int64_t rows
                  d / 128, 0, nullptr, d, reinterpret_cast<const uint64_t*>(ws + EP_ROWMAP),
                  reinterpret_cast<unsigned*>(ws + EP_DONE_GEMM), d_peers, G, rank, epoch};
   return skinny_dispatch<false>(tw, tx, p, rows_cap, nt, as_stream(stream));
+}
+
+// the dense projection entry's small-M path (grouped_gemm.cu daop_gemm_bf16_f32)
+int skinny_dense_gemm(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w, int32_t N,
+                      const float* resid, float* out, cudaStream_t st) {
+  int rc;
+  CUtensorMap tw, tx;
+  const uint64_t wdims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), 1};
+  const uint64_t wstr[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K) * N * 2};
+  const uint32_t wbox[3] = {SK_K, 128, 1};
+  if ((rc = make_tmap_bf16(&tw, w, 3, wdims, wstr, wbox))) return rc;
+  const int nt = M <= 32 ? 32 : 64;
+  const uint64_t xdims[2] = {static_cast<uint64_t>(K), static_cast<uint64_t>(M)};
+  const uint64_t xstr[1] = {static_cast<uint64_t>(K) * 2};
+  const uint32_t xbox[2] = {SK_K, static_cast<uint32_t>(nt)};
+  if ((rc = make_tmap_bf16(&tx, a, 2, xdims, xstr, xbox))) return rc;
+  SkinnyParams p{nullptr, nullptr, 1, K / SK_K, N / 128, 0, out, N};
+  p.dense_rows = M;
+  p.resid = resid;
+  p.w_keep = M > nt;
+  return skinny_dispatch<false>(tw, tx, p, M, nt, st);
 }

@@ -125,24 +125,34 @@ def test_attention_prefill_bounds(P):
         att.prefill(h, 0, 60)
 
 
+@pytest.mark.parametrize("pair", [False, True])  # M <= 768: skinny (default) or forced CTA-pair
 @pytest.mark.parametrize("M,K,N,resid", [(1, 512, 256, False), (5, 512, 1024, True),
                                          (256, 4096, 6144, False), (700, 4096, 4096, True),
                                          (1100, 1024, 512, True)])
-def test_dense_gemm_parity(P, M, K, N, resid):
+def test_dense_gemm_parity(P, M, K, N, resid, pair):
     """daop_gemm_bf16_f32 (the prompt attention's projections on the tcgen05
-    pipeline) vs a float64 numpy product of the same bf16 operands."""
+    pipeline: the swap-AB skinny kernel for prompt-sized M, the CTA-pair
+    kernel above) vs a float64 numpy product of the same bf16 operands."""
     pkg, A = P
     g = torch.Generator(device="cuda").manual_seed(M + K + N)
     a = torch.randn((M, K), generator=g, device="cuda").to(torch.bfloat16)
     w = (torch.rand((N, K), generator=g, device="cuda") - 0.5).to(torch.bfloat16)
     r = torch.randn((M, N), generator=g, device="cuda") if resid else None
-    out = A.ops.gemm_bf16_f32(a, w, resid=r)
+    A.ops.set_gemm_mode(1 << 15 if pair else 0)
+    try:
+        out = A.ops.gemm_bf16_f32(a, w, resid=r)
+    finally:
+        A.ops.set_gemm_mode(0)
     ref = a.double().cpu().numpy() @ w.double().cpu().numpy().T
     if resid:
         ref = ref + r.double().cpu().numpy()
         # in place: the residual buffer receives the result
         r2 = r.clone()
-        A.ops.gemm_bf16_f32(a, w, resid=r2, out=r2)
+        A.ops.set_gemm_mode(1 << 15 if pair else 0)
+        try:
+            A.ops.gemm_bf16_f32(a, w, resid=r2, out=r2)
+        finally:
+            A.ops.set_gemm_mode(0)
         assert torch.equal(r2, out)
     torch.cuda.synchronize()
     close(out.cpu().numpy(), ref, f"gemm {M}x{K}x{N}")

@@ -392,7 +392,7 @@ def test_decode_server_matches_host_call(P, d, ffn):
     E, k = 8, 2
     m = model_mod.MoEModel(pkg.ModelShape(2, E, k), d, ffn, seed=2, resident_layers=[0])
     eng = MoEBlockEngine(m)
-    hs = [m.input_hidden(1, stream=70, step=i)[0].cpu().contiguous() for i in range(6)]
+    hs = [m.input_hidden(1, stream=70, step=i)[0].cpu().contiguous() for i in range(16)]
     ref = []
     for h in hs:
         out, sel = eng.decode_host(h)
