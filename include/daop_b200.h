@@ -223,6 +223,9 @@ int daop_host_stream_read(const void* h_buf, int64_t bytes, int32_t threads, dou
 /* tuning switch: 0 = tcgen05.mma.cta_group::2 CTA-pair kernel (default),
  * 1 = single-CTA kernel */
 int daop_set_gemm_mode(int32_t mode);
+/* device-wide GEMM setup (persisting-L2 limit); call before capturing GEMMs
+ * into a CUDA graph (the launch path does it lazily otherwise). */
+int daop_gemm_prepare(void);
 int daop_expert_gemm_up(const uint16_t* d_x_perm, int64_t rows, int32_t d, int32_t ffn,
                         const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,
                         const int64_t* d_offsets, const int32_t* d_slot_of, int32_t num_experts,

@@ -61,6 +61,7 @@ PROTOS = {
     "daop_set_router_mode": [I32],
     "daop_set_stream_mode": [I32, I32, I32, I32],
     "daop_l2_prefetch": [P, I64, P, I64, P],
+    "daop_gemm_prepare": [],
     "daop_host_pool_alloc": [I64, I32, P, P],
     "daop_host_pool_free": [P, I64, I32],
     "daop_expert_gemm_up_skinny": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],

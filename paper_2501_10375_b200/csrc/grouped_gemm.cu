@@ -822,9 +822,7 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
   return DAOP_OK;
 }
 
-template <bool SWIGLU>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                       int64_t rows_total, cudaStream_t st) {
+static void apply_persisting_l2() {
   {
     // L2::evict_last (the A operand, re-read by every n-tile of its group) is
     // only honoured inside the persisting L2 set-aside, which defaults to 0
@@ -848,6 +846,12 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
       }
     }
   }
+}
+
+template <bool SWIGLU>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                       int64_t rows_total, cudaStream_t st) {
+  apply_persisting_l2();
   if (g_gemm_demote & 4) cudaCtxResetPersistingL2Cache();  // tuning: start from a clean set-aside
   if (g_gemm_mode == 0) {
     const bool two = (g_gemm_two_m >> (SWIGLU ? 0 : 1)) & 1;
@@ -880,6 +884,13 @@ static int check_ffn_shape(int64_t rows, int32_t d, int32_t ffn, int32_t E) {
               static_cast<long long>(rows), d, ffn, E, G_MAX_EXPERTS);
     return DAOP_ERR_UNSUPPORTED;
   }
+  return DAOP_OK;
+}
+
+// device-wide GEMM setup (the persisting-L2 limit) outside any stream
+// capture: a CUDA graph that captures the GEMMs calls this first
+extern "C" int daop_gemm_prepare() {
+  apply_persisting_l2();
   return DAOP_OK;
 }
 

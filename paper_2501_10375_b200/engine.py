@@ -45,8 +45,9 @@ class MoEBlockEngine:
         self._out_host = None
         self._sel_host = None
         # full decoder layers: prefetch layer l+1's attention weights into L2
-        # while layer l's MoE kernel streams its experts (tuning switch)
-        self.attn_prefetch = True
+        # while layer l's MoE kernel streams its experts.  Measured slower
+        # (decoder32 192.7 vs 206.4 tok/s, DESIGN §6 tried and rejected): off
+        self.attn_prefetch = False
 
     # ------------------------------------------------------------ decode
     def decode(self, h: torch.Tensor, layer: int = 0, *, pred_prev=None, mode: int = 0,

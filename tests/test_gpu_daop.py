@@ -207,3 +207,33 @@ def test_host_pool_device_fill_matches_host_fill():
     assert torch.equal(a.buf.view(torch.int16), b.buf.view(torch.int16))
     # registered with the driver: copies from it are true async DMAs
     assert b.pinned and b.buf.is_pinned()
+
+
+@pytest.mark.parametrize("attention", [False, True])
+def test_resident_prefill_graph_equals_eager(attention):
+    """A fully resident model's prefill replays as one CUDA graph per prompt
+    length: bit-identical output, counts and exported scores to the eager
+    per-layer loop, also when the graph is replayed for a second prompt."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.daop import DaopEngine, HostExpertPool
+    L, E, k, d, ffn = 4, 8, 2, 256, 512
+    shape = P.ModelShape(L, E, k)
+    pool = HostExpertPool(shape, d, ffn, seed=3)
+    res = {}
+    for graphs in (False, True):
+        eng = DaopEngine(shape, d, ffn, np.full((L, E), 0.25), 1.0, P.PolicyConfig("daop"),
+                         seed=3, host_pool=pool, attention=attention, max_seq=128)
+        eng.prefill_graphs = graphs
+        outs = []
+        for s_ in (0, 1):
+            pre = eng.prefill(eng.model.input_hidden(40, stream=500 + s_))
+            outs.append((pre.out.clone(), pre.counts.copy(), pre.true_scores.copy(),
+                         pre.pred_scores.copy()))
+        res[graphs] = outs
+        assert len(eng._pf_graphs) == (1 if graphs else 0)
+    for a, b in zip(res[False], res[True]):
+        assert torch.equal(a[0], b[0])
+        for x, y in zip(a[1:], b[1:]):
+            assert np.array_equal(x, y)
