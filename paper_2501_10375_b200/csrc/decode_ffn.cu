@@ -239,8 +239,13 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     *reinterpret_cast<int*>(&s.zpart[1][0]) = 0;  // lazy-gates counter (zpart unused then)
     fence_mbar_init();
     if (a.mode == 0) {  // h + gamma (RMSNorm starts on them), then the gate rows
-      mbar_arrive_expect_tx(&s.in_bar, d * 4 + d * 2);
-      bulk_g2s_plain(h_s, a.h, d * 4, &s.in_bar);
+      // server mode: h was just written by block 0 with generic stores and
+      // handed over through an acquire; it is read with generic loads below
+      // (a bulk copy here read a stale h in some CTAs: the async proxy is not
+      // ordered by that acquire)
+      const bool h_bulk = a.host_seq == 0;
+      mbar_arrive_expect_tx(&s.in_bar, (h_bulk ? d * 4 : 0) + d * 2);
+      if (h_bulk) bulk_g2s_plain(h_s, a.h, d * 4, &s.in_bar);
       bulk_g2s_plain(gm_s, a.gamma, d * 2, &s.in_bar);
       mbar_arrive_expect_tx(&s.in_bar2, E * d * 2 + (pred_row ? d * 2 : 0));
       bulk_g2s_plain(g_s, a.wg, E * d * 2, &s.in_bar2);
@@ -434,9 +439,18 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
       ss = sq_acc4(reinterpret_cast<const float4*>(a.h)[i], ss);
   } else {
     // ---------------------------------------------------- TRUE: router first
-    mbar_wait(&s.in_bar, 0);
-    for (int i = threadIdx.x; i < d / 4; i += NT)
-      ss = sq_acc4(reinterpret_cast<const float4*>(h_s)[i], ss);
+    if (a.host_seq != 0) {  // server mode: generic loads of h (each thread the elements it sums)
+      for (int i = threadIdx.x; i < d / 4; i += NT) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.h) + i);
+        reinterpret_cast<float4*>(h_s)[i] = v;
+        ss = sq_acc4(v, ss);
+      }
+      mbar_wait(&s.in_bar, 0);  // gamma
+    } else {
+      mbar_wait(&s.in_bar, 0);
+      for (int i = threadIdx.x; i < d / 4; i += NT)
+        ss = sq_acc4(reinterpret_cast<const float4*>(h_s)[i], ss);
+    }
   }
   ss = warp_sum(ss);
   if (lane == 0) s.red[warp] = ss;

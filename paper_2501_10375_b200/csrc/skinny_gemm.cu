@@ -103,8 +103,13 @@ __device__ __forceinline__ bool skinny_tile(const SkinnySmem<NT>& s, int E, int 
   e = 0;
   while (s.prefix[e + 1] <= t) ++e;
   const int u = t - s.prefix[e];
-  blk = u / rt;
-  r = u - blk * rt;
+  // token blocks fastest within a weight tile: an expert with more than NT
+  // rows (a prompt) has its blocks of one weight tile on neighbouring CTAs at
+  // the same time, so the tile crosses HBM once and the rest hit L2
+  const int nb = s.blocks[e];
+  r = u / nb;
+  blk = u - r * nb;
+  (void)rt;
   return true;
 }
 
@@ -149,8 +154,8 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
-      const uint64_t pol_w = p.w_keep ? l2_evict_normal_policy()   // re-read per token block
-                                      : l2_evict_first_policy();  // weights: streamed once
+      const uint64_t pol_once = l2_evict_first_policy();   // weights read by one token block
+      const uint64_t pol_reuse = l2_evict_normal_policy();  // ... by several (neighbour CTAs)
       const uint64_t pol_x = l2_evict_last_policy();   // tokens: re-read by every row tile
       int stage = 0;
       uint32_t phase = 0;
@@ -158,6 +163,7 @@ __global__ void __launch_bounds__(192, 1)
       for (int t = blockIdx.x; skinny_tile(s, E, rt, t, e, blk, r); t += gridDim.x) {
         const int slot = sk_slot(p, e);
         const int xrow = static_cast<int>(s.off[e]) + blk * NT;
+        const uint64_t pol_w = (p.w_keep || s.blocks[e] > 1) ? pol_reuse : pol_once;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
           uint8_t* st = tiles + stage * C::STAGE_BYTES;
