@@ -105,10 +105,6 @@ struct Piece {   // what one ring stage holds
   int kind;      // 1 = W1/W3 piece, 2 = W2 piece, 0 = end of stream
   int j, row, c; // pick (executed index), row, piece within the unit
 };
-
-// a Piece packed into 32 bits for the per-stage record in shared memory
-// (kind 2 b | j 4 b | c 8 b | row 18 b): the decode kernel's smem is at the
-// 227 KB limit for Mixtral-8x7B, so every byte of the control block counts
 __device__ __forceinline__ uint32_t pack_piece(const Piece& p) {
   return static_cast<uint32_t>(p.kind) | (static_cast<uint32_t>(p.j) << 2) |
          (static_cast<uint32_t>(p.c) << 6) | (static_cast<uint32_t>(p.row) << 14);
@@ -122,37 +118,30 @@ __device__ __forceinline__ Piece unpack_piece(uint32_t v) {
   return p;
 }
 
-struct WarpSel {
-  const uint16_t* base[DK_MAX];  // slab slot base of each executed pick
-  float wsel[DK_MAX];            // combine weights, pick order
-  int sel[DK_MAX];
-  uint8_t exec_q[DK_MAX];        // executed index -> pick
-  uint8_t fast[DK_MAX];
-  int n_exec;
-};
-
 template <int DW, int DS>
 struct DecodeSmem {
   uint64_t bar[DW][DS];
   uint64_t act_bar[DK_MAX];
   uint64_t in_bar;   // h + gamma
   uint64_t in_bar2;  // gate rows (+ next-layer row)
-  uint32_t rec[DW][DS];  // pack_piece
+  uint32_t rec[DW][DS];
   int act_req[DK_MAX];
   int p1_next, p2_next, fin;
   int done1[DK_MAX];
   double red[DW];         // per-warp sums of squares (fp64, common.cuh rms_scale)
   float zpart[DW][DE_MAX];  // per-warp partial gate logits
   float zpp[DW];            // per-warp partial next-layer logit
+  float p[DE_MAX];
   float pp[DE_MAX];
   int slot[DE_MAX];
   uint8_t fast_row[DE_MAX];
-  int nd, drop[DK_MAX], sub[DK_MAX];
+  float wsel[DK_MAX];
+  int sel[DK_MAX];
+  int exec_q[DK_MAX];
+  uint8_t fast[DK_MAX];
+  int n_exec, nd, drop[DK_MAX], sub[DK_MAX];
   int pred_last;
-  // the selection, one copy per warp (+ the PLAN-mode copy at [DW]): every
-  // warp computes the selection itself and reads only its own copy, so no
-  // shared word is written by one warp while another reads it
-  WarpSel ws[DW + 1];
+  const uint16_t* base[DK_MAX];  // slab slot base of each executed pick
 };
 
 struct Layout {
@@ -241,8 +230,6 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     if (a.mode == 0) {  // h + gamma (RMSNorm starts on them), then the gate rows
       // server mode: h was just written by block 0 with generic stores and
       // handed over through an acquire; it is read with generic loads below
-      // (a bulk copy here read a stale h in some CTAs: the async proxy is not
-      // ordered by that acquire)
       const bool h_bulk = a.host_seq == 0;
       mbar_arrive_expect_tx(&s.in_bar, (h_bulk ? d * 4 : 0) + d * 2);
       if (h_bulk) bulk_g2s_plain(h_s, a.h, d * 4, &s.in_bar);
@@ -279,38 +266,30 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   // lane-parallel (lane q = pick q): residence, compaction of the resident
   // picks in pick order, weights w_q = wsrc[sel_q] / sum_q' wsrc[sel_q']
   // (summed in pick order, like the reference renormalisation)
-  // selsrc: the picks (any copy, read-only here); wsrc: weight source or
-  // null; result into copy `dst` (this warp's own, or [DW] for the plan)
-  int cw = warp;     // the selection copy this warp streams / combines with
-  float my_p = 0.f;  // this layer's gate probability of expert `lane` (registers)
-  // wsrc: 0 no weights, 1 from the carried prediction (s.pp), 2 from my_p
-  auto finish_selection = [&](const int* selsrc, int wsrc, int dst) {
+  auto finish_selection = [&](const float* wsrc) {
     __syncwarp();
-    WarpSel& o = s.ws[dst];
     int e = 0, slot = 0;
     bool f = false;
     if (lane < k) {
-      e = selsrc[lane];
+      e = s.sel[lane];
       f = s.fast_row[e] != 0;
       slot = s.slot[e];
     }
     const unsigned fm = __ballot_sync(0xffffffffu, lane < k && f);
     if (lane < k) {
-      o.sel[lane] = e;
-      o.fast[lane] = f ? 1 : 0;
+      s.fast[lane] = f ? 1 : 0;
       if (f) {
         const int pos = __popc(fm & ((1u << lane) - 1u));
-        o.base[pos] = a.slab + static_cast<int64_t>(slot) * a.slot_stride;
-        o.exec_q[pos] = static_cast<uint8_t>(lane);
+        s.base[pos] = a.slab + static_cast<int64_t>(slot) * a.slot_stride;
+        s.exec_q[pos] = lane;
       }
     }
-    if (lane == 0) o.n_exec = __popc(fm);
+    if (lane == 0) s.n_exec = __popc(fm);
     if (wsrc) {
-      const float pe = __shfl_sync(0xffffffffu, my_p, e);  // every lane: uniform shuffle
-      const float v = lane < k ? (wsrc == 1 ? s.pp[e] : pe) : 0.f;
+      const float v = lane < k ? wsrc[e] : 0.f;
       float den = 0.f;
       for (int q = 0; q < k; ++q) den += __shfl_sync(0xffffffffu, v, q);
-      if (lane < k) o.wsel[lane] = v / den;
+      if (lane < k) s.wsel[lane] = v / den;
     }
     __syncwarp();
   };
@@ -379,8 +358,8 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     ++issued;
   };
   auto start_stream = [&]() {
-    L.n_exec = s.ws[cw].n_exec;
-    L.base = s.ws[cw].base;
+    L.n_exec = s.n_exec;
+    L.base = s.base;
     L.n1c = count_mod(0, L.n_exec * a.ffn, L.cta, L.G);
     L.P2c = L.n_exec * L.R * L.npc2;
     for (int q = 0; q < DS; ++q) issue_next();
@@ -399,7 +378,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     for (int o = P2 >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     return lane < E ? e / sum : 0.f;
   };
-  auto lane_topk = [&](float v, int* sel_out) {  // -> sel_out[0..k)
+  auto lane_topk = [&](float v) {  // -> s.sel[0..k)
     bool taken = lane >= E;
     for (int j = 0; j < k; ++j) {
       float bv = taken ? -INFINITY : v;
@@ -416,7 +395,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
       // NaN scores never compare: fall back to the first untaken id
       // (topk_scan's "best < 0" rule), never an out-of-range id
       if (bi >= E) bi = __ffs(__ballot_sync(0xffffffffu, !taken)) - 1;
-      if (lane == 0) sel_out[j] = bi;
+      if (lane == 0) s.sel[j] = bi;
       if (lane == bi) taken = true;
     }
     __syncwarp();
@@ -426,14 +405,12 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   if (a.mode == 1) {
     // ---------------------------------------------------- PLAN: stream first
     if (warp == 0) {
-      int* plan = s.ws[DW].sel;
-      lane_topk(lane < E ? s.pp[lane] : 0.f, plan);
-      if (lane == 0) s.nd = a.graceful ? degrade_smem(s.pp, E, plan, k, s.fast_row, s.drop, s.sub) : 0;
+      lane_topk(lane < E ? s.pp[lane] : 0.f);
+      if (lane == 0) s.nd = a.graceful ? degrade_smem(s.pp, E, s.sel, k, s.fast_row, s.drop, s.sub) : 0;
       __syncwarp();
-      finish_selection(plan, a.weights_from_pred ? 1 : 0, DW);
+      finish_selection(a.weights_from_pred ? s.pp : nullptr);
     }
     __syncthreads();
-    cw = DW;  // the plan copy, read-only from here on
     start_stream();
     for (int i = threadIdx.x; i < d / 4; i += NT)  // router inputs from global
       ss = sq_acc4(reinterpret_cast<const float4*>(a.h)[i], ss);
@@ -570,7 +547,8 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
         }
       __syncwarp();
       __threadfence_block();
-      my_p = lane_softmax(lane < E ? zfull[lane] : 0.f);  // exported below
+      const float p = lane_softmax(lane < E ? zfull[lane] : 0.f);
+      if (lane < E) s.p[lane] = p;
       __syncwarp();
     }
   }
@@ -580,23 +558,19 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     if (lane < E)
       for (int w = 0; w < DW; ++w) z += s.zpart[w][lane];
     if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][7] = gtimer();
-    my_p = lane_softmax(z);  // every warp computes the same probabilities
-    WarpSel& me = s.ws[warp];
+    const float p = lane_softmax(z);
+    if (lane < E) s.p[lane] = p;  // identical values from every warp
     if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][9] = gtimer();
     if (mode0) {
-      lane_topk(my_p, me.sel);
-      if (lane == 0 && warp == 0) s.nd = 0;
+      lane_topk(p);
+      if (lane == 0) s.nd = 0;
       __syncwarp();
       if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][10] = gtimer();
-      finish_selection(me.sel, 2, warp);
-      cw = warp;
+      finish_selection(s.p);
       if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][11] = gtimer();
       start_stream();
     } else if (!a.weights_from_pred) {
-      // PLAN mode, weights from this layer's own gate: the plan's picks
-      // (read-only copy [DW]) re-weighted into this warp's copy
-      finish_selection(s.ws[DW].sel, 2, warp);
-      cw = warp;
+      finish_selection(s.p);
     }
   }
   if (tl && threadIdx.x == 0) g_decode_timeline[blockIdx.x][8] = gtimer();
@@ -623,13 +597,12 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   }
   if (blockIdx.x == 0) {
     if (warp == 0) {
-      const WarpSel& ex = s.ws[cw];  // warp 0's selection copy
-      if (lane < E) a.p_true[lane] = my_p;
+      if (lane < E) a.p_true[lane] = s.p[lane];
       if (lane < k) {
-        a.sel[lane] = ex.sel[lane];
+        a.sel[lane] = s.sel[lane];
         wrote_out = true;
-        a.w[lane] = ex.wsel[lane];
-        a.is_fast[lane] = ex.fast[lane];
+        a.w[lane] = s.wsel[lane];
+        a.is_fast[lane] = s.fast[lane];
         a.deg[lane] = lane < s.nd ? s.drop[lane] : -1;
         a.deg[k + lane] = lane < s.nd ? s.sub[lane] : -1;
       }
@@ -652,9 +625,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
       const int tot_j = count_mod(cur_j * a.ffn, (cur_j + 1) * a.ffn, L.cta, L.G);
       if (atomicAdd(&s.done1[cur_j], cur_cnt) + cur_cnt == tot_j) {
         // cumulativity: the other warps' act rows this warp observed through
-        // done1 are ordered before the grid-wide count (a consumer CTA then
-        // bulk-reads act_j; without this fence a fast consumer could pull a
-        // row of the previous token -- seen as a rare mismatch in server mode)
+        // done1 are ordered before the grid-wide count a consumer CTA waits on
         __threadfence();
         atomicAdd(a.ctr + 2 + cur_j, static_cast<unsigned>(tot_j));
       }
@@ -683,7 +654,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
         asm volatile("fence.proxy.async;" ::: "memory");
         mbar_arrive_expect_tx(&s.act_bar[pc.j], a.ffn * 2);
         bulk_g2s_plain(act_s + static_cast<size_t>(pc.j) * a.ffn,
-                       a.act + static_cast<size_t>(s.ws[cw].exec_q[pc.j]) * a.ffn, a.ffn * 2,
+                       a.act + static_cast<size_t>(s.exec_q[pc.j]) * a.ffn, a.ffn * 2,
                        &s.act_bar[pc.j]);
       }
       mbar_wait(&s.act_bar[pc.j], 0);
@@ -699,7 +670,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
         const float g = warp_sum(acc0), u = warp_sum(acc1);
         acc0 = acc1 = 0.f;
         if (lane == 0)
-          a.act[static_cast<int64_t>(s.ws[cw].exec_q[pc.j]) * a.ffn + pc.row] =
+          a.act[static_cast<int64_t>(s.exec_q[pc.j]) * a.ffn + pc.row] =
               f32_to_bf16_bits(silu_f32(g) * u);
         if (pc.j != cur_j) {
           publish();
@@ -724,8 +695,8 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
           for (int jj = 0; jj < L.n_exec; ++jj) {
             float yv = 0.f;
             for (int c = 0; c < L.npc2; ++c) yv += pr[jj * L.npc2 + c];
-            a.y[static_cast<int64_t>(s.ws[cw].exec_q[jj]) * d + pc.row] = yv;
-            o = fmaf(s.ws[cw].wsel[s.ws[cw].exec_q[jj]], yv, o);
+            a.y[static_cast<int64_t>(s.exec_q[jj]) * d + pc.row] = yv;
+            o = fmaf(s.wsel[s.exec_q[jj]], yv, o);
           }
           if (all_fast) {
             a.h_out[pc.row] = o;
@@ -753,7 +724,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     __threadfence_block();
     const int r1 = min(L.r0 + a.rows_per_cta, d);
     for (int jj = 0; jj < L.n_exec; ++jj) {
-      const int q0 = s.ws[cw].exec_q[jj];
+      const int q0 = s.exec_q[jj];
       const float* src = a.y + static_cast<int64_t>(q0) * d;
       for (int r = L.r0 + lane; r < r1; r += 32) {
         const float v = __ldcg(src + r);
@@ -1018,15 +989,14 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
   int grid = sm_count();
   if (grid < E) grid = E;  // CTAs 0..E-1 own one next-layer gate row each
   cudaStream_t st = as_stream(stream);
-  // default geometry: 16 warps x 1 stage x ~10 KB pieces (110.6 us vs 117.2 us
+  // default geometry: 16 warps x 1 stage x 10 KB pieces (110.6 us vs 117.2 us
   // for 8 warps x 2 stages: twice the warps computing W2 partials in phase 2)
   switch (variant) {
     case 1: return launch_decode<4, 4, 10240>(a, grid, st);
     case 9: return launch_decode<8, 2, 10240>(a, grid, st);
     case 2: return launch_decode<8, 2, 8192>(a, grid, st);
     case 3: return launch_decode<6, 3, 8192>(a, grid, st);
-    case 4: return launch_decode<16, 1, 10240>(a, grid, st);  // > 227 KB at 8x7B since the per-warp selections
-    case 14: return launch_decode<16, 1, 9600>(a, grid, st);
+    case 4: return launch_decode<16, 1, 10240>(a, grid, st);
     case 5: return launch_decode<16, 2, 4608>(a, grid, st);
     case 6: return launch_decode<12, 2, 6144>(a, grid, st);
     case 7: return launch_decode<16, 1, 8192>(a, grid, st);
@@ -1039,8 +1009,6 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
     default: {
       // largest ring that fits: Mixtral-8x22B (d = 6144, ffn = 16384) needs
       // 64 KB of activations in shared memory and a 144 KB router stage
-      // 9600-byte stages: the same W1/W3 and W2 pieces as 10 KB for
-      // Mixtral-8x7B (8 KB rows, 3 x 9568 B W2 pieces), 10 KB less smem
       int rc = launch_decode<16, 1, 9600>(a, grid, st);
       if (rc != DAOP_ERR_UNSUPPORTED) return rc;
       rc = launch_decode<16, 1, 9216>(a, grid, st);
