@@ -408,7 +408,7 @@ using namespace daop;
 // tuning (daop_set_stream_mode): gather 0 = auto (bulk DMA rows for large T),
 // 1 = warp-per-token registers; combine 0 = auto (bulk), 1 = warp-per-token
 static int g_gather_variant = 0, g_combine_variant = 0;
-static int g_bulk_ctas_per_sm = 4, g_combine_stages = 4;
+static int g_bulk_ctas_per_sm = 2, g_combine_stages = 4;  // profiles/r02/stream_kernels.json
 
 extern "C" {
 

@@ -52,15 +52,15 @@ r = ops.router(h, m.norm[0], m.gate[0], m.gate[1], k)
 x, idx, w = r["x"], r["topk_idx"], r["topk_w"]
 res["permute_only"] = (timed(lambda: ops.permute(idx, E)), T * k * 16)
 for var, ctas in ((0, 2), (0, 4), (0, 8), (1, 0)):
-    ops.set_stream_mode(gather=var, gather_ctas_per_sm=ctas or 4)
+    ops.set_stream_mode(gather=var, gather_ctas_per_sm=ctas or 2)
     res[f"permute+gather_v{var}_c{ctas}"] = (timed(lambda: ops.permute(idx, E, x)), T * d * 2 * 3)
-ops.set_stream_mode(0, 0, 4, 4)
+ops.set_stream_mode(0, 0, 2, 4)
 pr = ops.permute(idx, E, x)
 y = torch.randn((T * k, d), device="cuda")
 for var, st in ((0, 2), (0, 3), (0, 4), (1, 0)):
-    ops.set_stream_mode(combine=var, combine_stages=st or 4, gather_ctas_per_sm=4)
+    ops.set_stream_mode(combine=var, combine_stages=st or 4, gather_ctas_per_sm=2)
     res[f"combine_v{var}_s{st}"] = (timed(lambda: ops.combine(h, y, pr["inv"], w)), T * d * 4 * 4)
-ops.set_stream_mode(0, 0, 4, 4)
+ops.set_stream_mode(0, 0, 2, 4)
 out = {}
 for key, (ts, nbytes) in res.items():
     med = statistics.median(ts)
