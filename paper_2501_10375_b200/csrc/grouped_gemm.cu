@@ -133,14 +133,16 @@ __device__ __forceinline__ void store_f32x32(float* out, const float* res, const
 
 // the fused combine of one (row, n-tile): called by the row's thread after
 // its y slice is stored and the accumulator released
-__device__ __forceinline__ void fused_combine(const GemmParams& p, int64_t grow, int n) {
+__device__ __forceinline__ void fused_combine(const GemmParams& p, int64_t grow, int n,
+                                              int parts) {
   __threadfence();  // this thread's y slice -> visible to the token's last pick
   const int k = p.comb_k;
   const int src = p.comb_perm[grow];
   const int64_t t = src / k;
   const int nt = p.n_tiles;
+  // every pick's (row, n-tile) slice is stored in `parts` column pieces
   const unsigned old = atomicAdd(p.comb_cnt + t * nt + n, 1u);
-  if (old != static_cast<unsigned>(k - 1)) return;
+  if (old != static_cast<unsigned>(k * parts - 1)) return;
   p.comb_cnt[t * nt + n] = 0;  // self-resetting for the next layer
   __threadfence();
   const int64_t d = p.out_ld;
@@ -466,17 +468,19 @@ constexpr int P2_M = 512;
 constexpr int P2_STAGES = 4;
 constexpr int P2_STAGE_BYTES = 2 * P_A_BYTES + P_B_BYTES; // 48 KB
 
-template <bool TWO_M>
+template <bool TWO_M, int EW = 8>
 struct PairCfg {
   static constexpr int M = TWO_M ? P2_M : P_M;
   static constexpr int STAGES = TWO_M ? P2_STAGES : P_STAGES;
   static constexpr int STAGE_BYTES = TWO_M ? P2_STAGE_BYTES : P_STAGE_BYTES;
   static constexpr int A_BYTES = TWO_M ? 2 * P_A_BYTES : P_A_BYTES;
   static constexpr int NACC = TWO_M ? 1 : 2;  // TMEM accumulator buffers
-  // TWO_M: 8 epilogue warps (two per TMEM lane quarter, one per accumulator
-  // half) drain the single accumulator twice as fast -- the MMAs of the next
-  // tile wait for it
-  static constexpr int EPI_WARPS = TWO_M ? 8 : 4;
+  // TWO_M: EW = 8 or 16 epilogue warps (2 or 4 per TMEM lane quarter; each
+  // drains one accumulator half, or a quarter of the columns) -- the MMAs of
+  // the next tile wait for the single accumulator, so a faster drain is
+  // tensor-pipe time
+  static constexpr int EPI_WARPS = TWO_M ? EW : 4;
+  static constexpr int GROUPS_PER_HALF = TWO_M ? EW / 8 : 1;  // warps per (quarter, half)
   static constexpr int THREADS = (2 + EPI_WARPS) * 32;
 };
 
@@ -519,11 +523,11 @@ __device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, 
   return true;
 }
 
-template <bool SWIGLU, bool TWO_M = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THREADS, 1)
+template <bool SWIGLU, bool TWO_M = false, int EW = 8>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::THREADS, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, GemmParams p) {
-  using C = PairCfg<TWO_M>;
+  using C = PairCfg<TWO_M, EW>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
@@ -689,7 +693,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t me = s.off[e + 1] - s.off[e];
-      const int half = TWO_M ? (warp - 2) >> 2 : 0;  // this warp's accumulator half
+      const int grp = (warp - 2) >> 2;  // 0 .. EPI_WARPS / 4 - 1
+      const int half = TWO_M ? grp / C::GROUPS_PER_HALF : 0;  // this warp's accumulator half
+      const int sub = TWO_M ? grp % C::GROUPS_PER_HALF : 0;   // its share of the half's columns
       {
       const int row_in_tile = half * 256 + rank * 128 + q * 32 + lane;
       const bool valid = static_cast<int64_t>(m) * C::M + row_in_tile < me;
@@ -699,7 +705,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
       if constexpr (SWIGLU) {
         uint16_t* out = static_cast<uint16_t*>(p.out) + grow * p.out_ld + n * 128;
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = sub * (128 / C::GROUPS_PER_HALF); c < (sub + 1) * (128 / C::GROUPS_PER_HALF);
+             c += 32) {
           uint32_t g[32], u[32];
           tmem_ld32(tb + c, g);
           tmem_ld32(tb + 128 + c, u);
@@ -729,7 +736,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
                                         : nullptr)
                                : static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
 #pragma unroll 1
-        for (int c = 0; c < GB_N; c += 32) {
+        for (int c = sub * (GB_N / C::GROUPS_PER_HALF); c < (sub + 1) * (GB_N / C::GROUPS_PER_HALF);
+             c += 32) {
           uint32_t v[32];
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
@@ -744,9 +752,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M>::THRE
       if (lane == 0) mbar_arrive_cluster(&s.tempty[acc], 0);
       if constexpr (!SWIGLU) {
         if (p.comb_cnt) {  // accumulator released: the combine runs off the MMA's path
-          const int row_in_tile = (TWO_M ? ((warp - 2) >> 2) * 256 : 0) + rank * 128 + q * 32 + lane;
+          const int row_in_tile = half * 256 + rank * 128 + q * 32 + lane;
           if (static_cast<int64_t>(m) * C::M + row_in_tile < me)
-            fused_combine(p, s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile, n);
+            fused_combine(p, s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile, n,
+                          C::GROUPS_PER_HALF);
         }
       }
       if (p.demote && !TWO_M) {
@@ -790,6 +799,7 @@ static size_t gemm_smem_bytes() { return 1024 + G_STAGES * G_STAGE_BYTES + sizeo
 static int g_gemm_two_m = 3;
 static int g_gemm_store_cs = 0;  // epilogue streaming stores (tuning)
 static int g_gemm_dense_skinny = 1;  // tuning: small-M dense GEMMs on the skinny kernel
+static int g_gemm_epi16 = 0;  // tuning: 16 epilogue warps for the 512-row pair tile
 static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
 
 template <bool TWO_M>
@@ -797,12 +807,12 @@ static size_t pair_smem_bytes() {
   return 1024 + PairCfg<TWO_M>::STAGES * PairCfg<TWO_M>::STAGE_BYTES + sizeof(PairSmem);
 }
 
-template <bool SWIGLU, bool TWO_M>
-static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                       int64_t rows_total, cudaStream_t st) {
-  using C = PairCfg<TWO_M>;
+template <bool SWIGLU, bool TWO_M, int EW>
+static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                          int64_t rows_total, cudaStream_t st) {
+  using C = PairCfg<TWO_M, EW>;
   const size_t smem = pair_smem_bytes<TWO_M>();
-  auto kern = grouped_gemm_pair_kernel<SWIGLU, TWO_M>;
+  auto kern = grouped_gemm_pair_kernel<SWIGLU, TWO_M, EW>;
   DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const int64_t max_tiles = (rows_total / C::M + p.E) * static_cast<int64_t>(p.n_tiles);
@@ -820,6 +830,13 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
   kern<<<2 * clusters, C::THREADS, smem, st>>>(ta, tb, pp);
   DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
   return DAOP_OK;
+}
+
+template <bool SWIGLU, bool TWO_M>
+static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                       int64_t rows_total, cudaStream_t st) {
+  if (TWO_M && g_gemm_epi16) return launch_pair_ew<SWIGLU, TWO_M, 16>(ta, tb, p, rows_total, st);
+  return launch_pair_ew<SWIGLU, TWO_M, 8>(ta, tb, p, rows_total, st);
 }
 
 static void apply_persisting_l2() {
@@ -907,6 +924,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_two_m = ((mode >> 12) & 3) ^ 3;  // mode bits flip the default (tuning)
   g_gemm_store_cs = (mode >> 14) & 1;
   g_gemm_dense_skinny = !((mode >> 15) & 1);
+  g_gemm_epi16 = (mode >> 16) & 1;
   return DAOP_OK;
 }
 

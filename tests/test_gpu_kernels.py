@@ -236,7 +236,8 @@ def _gemm_case(P, d, ffn, E, T, k, seed=0):
     return m, om, h, r, pr, act, y, out
 
 
-@pytest.mark.parametrize("mode", [0, 1, 0x3000])  # 512-row pair tiles, single CTA, 256-row pair tiles
+# 512-row pair tiles, single CTA, 256-row pair tiles, 512-row tiles with 16 epilogue warps
+@pytest.mark.parametrize("mode", [0, 1, 0x3000, 0x10000])
 @pytest.mark.parametrize("d,ffn,E,T", [(256, 512, 8, 64), (512, 1024, 8, 700), (4096, 14336, 8, 256)])
 def test_grouped_gemm_parity(P, d, ffn, E, T, mode):
     P[2].set_gemm_mode(mode)
@@ -369,7 +370,7 @@ def test_grouped_gemm_two_m_bitexact(P, d, ffn, E, T):
     """The 512-row pair tile (two M=256 MMAs sharing B) accumulates every
     output element in the same K order as the 256-row tile: bit-identical."""
     outs = []
-    for mode in (0, 0x3000):
+    for mode in (0, 0x3000, 0x10000):
         P[2].set_gemm_mode(mode)
         try:
             _, _, _, _, pr, act, y, out = _gemm_case(P, d, ffn, E, T, 2)
@@ -377,9 +378,10 @@ def test_grouped_gemm_two_m_bitexact(P, d, ffn, E, T):
             P[2].set_gemm_mode(0)
         off = pr["offsets"][-1].item()
         outs.append((act[:off].clone(), y[:off].clone(), out.clone()))
-    assert torch.equal(outs[0][0], outs[1][0])
-    assert torch.equal(outs[0][1], outs[1][1])
-    assert torch.equal(outs[0][2], outs[1][2])
+    for o in outs[1:]:
+        assert torch.equal(outs[0][0], o[0])
+        assert torch.equal(outs[0][1], o[1])
+        assert torch.equal(outs[0][2], o[2])
 
 
 @pytest.mark.parametrize("d,ffn", [(512, 1024), (4096, 14336)])
@@ -423,8 +425,9 @@ def test_decode_server_idle_exit(P):
     srv.close()
 
 
+@pytest.mark.parametrize("mode", [0, 0x10000])  # 8 / 16 epilogue warps
 @pytest.mark.parametrize("d,ffn,E,T", [(512, 1024, 8, 700), (4096, 14336, 8, 300)])
-def test_fused_down_combine_bitexact(P, d, ffn, E, T):
+def test_fused_down_combine_bitexact(P, d, ffn, E, T, mode):
     """The down GEMM with the combine fused into its epilogue (each token's
     last pick writes h + sum_j w_j y_j) == down GEMM + combine kernel, bit
     for bit, twice in a row (the per-token counters reset themselves)."""
@@ -438,12 +441,16 @@ def test_fused_down_combine_bitexact(P, d, ffn, E, T):
                              d, ffn)
     y = ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn)
     ref = ops.combine(h, y, pr["inv"], r["topk_w"])
-    for _ in range(2):
-        out, y2 = ops.expert_gemm_down_combine(act, pr["offsets"], so, m.slab, m.n_slots,
-                                               m.slot_elems, d, ffn, pr["perm"], pr["inv"], h,
-                                               r["topk_w"])
-        torch.cuda.synchronize()
-        assert torch.equal(out, ref)
+    ops.set_gemm_mode(mode)
+    try:
+        for _ in range(2):
+            out, y2 = ops.expert_gemm_down_combine(act, pr["offsets"], so, m.slab, m.n_slots,
+                                                   m.slot_elems, d, ffn, pr["perm"], pr["inv"], h,
+                                                   r["topk_w"])
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref)
+    finally:
+        ops.set_gemm_mode(0)
 
 
 @pytest.mark.parametrize("d,ffn,E,T", [(512, 1024, 8, 700), (4096, 14336, 8, 300),
