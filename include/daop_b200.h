@@ -231,7 +231,7 @@ int daop_expert_gemm_up(const uint16_t* d_x_perm, int64_t rows, int32_t d, int32
                         const int64_t* d_offsets, const int32_t* d_slot_of, int32_t num_experts,
                         uint16_t* d_act, int32_t group_m, daop_stream_t stream);
 /* the same two GEMMs for SMALL token counts (batched decode): weights are the
- * M side (128-row tiles), the expert's tokens the N side (nt = 32 or 64 per
+ * M side (128-row tiles), the expert's tokens the N side (nt = 32, 64 or 128 per
  * block), so each expert's weights stream once per block of nt tokens. */
 int daop_expert_gemm_up_skinny(const uint16_t* d_x_perm, int64_t rows, int32_t d, int32_t ffn,
                                const uint16_t* d_slab, int64_t n_slots, int64_t slot_stride_elems,

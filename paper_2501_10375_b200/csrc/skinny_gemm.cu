@@ -92,7 +92,7 @@ struct SkinnyCfg {
                                     ? BUDGET / STAGE_BYTES : SkinnySmem<NT>::STAGES;
   static constexpr int ACC_COLS = SWIGLU ? 2 * NT : NT;  // per accumulator buffer
   static constexpr int TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : 2 * ACC_COLS <= 64 ? 64
-                                   : 2 * ACC_COLS <= 128 ? 128 : 256;
+                                   : 2 * ACC_COLS <= 128 ? 128 : 2 * ACC_COLS <= 256 ? 256 : 512;
   static constexpr uint32_t IDESC = umma_idesc_bf16_f32(128, NT);
 };
 
@@ -304,6 +304,7 @@ template <bool SWIGLU>
 static int skinny_dispatch(const CUtensorMap& tw, const CUtensorMap& tx, const SkinnyParams& p,
                            int64_t rows, int32_t nt, cudaStream_t st) {
   if (nt == 32) return launch_skinny<SWIGLU, 32>(tw, tx, p, rows, st);
+  if (nt == 128) return launch_skinny<SWIGLU, 128>(tw, tx, p, rows, st);
   return launch_skinny<SWIGLU, 64>(tw, tx, p, rows, st);
 }
 
@@ -313,7 +314,7 @@ using namespace daop;
 
 static int check_skinny(int64_t rows, int32_t d, int32_t ffn, int32_t E, int32_t nt) {
   if (E < 1 || E > SK_MAX_E || d % 128 != 0 || ffn % 128 != 0 || d % 64 != 0 ||
-      (nt != 32 && nt != 64) || rows < 0 || rows >= (1ll << 31)) {
+      (nt != 32 && nt != 64 && nt != 128) || rows < 0 || rows >= (1ll << 31)) {
     set_error("skinny expert GEMM: unsupported shape (rows=%lld d=%d ffn=%d E=%d nt=%d)",
               static_cast<long long>(rows), d, ffn, E, nt);
     return DAOP_ERR_UNSUPPORTED;

@@ -155,8 +155,13 @@ def expert_gemm_up_gather(x, perm, k, offsets, slot_of, slab, n_slots, slot_elem
 
 
 def skinny_nt(rows: int) -> int:
-    """Token block of the skinny GEMMs for `rows` permuted rows (T * k)."""
-    return 32 if rows <= 32 else 64
+    """Token block of the skinny GEMMs for `rows` permuted rows (T * k):
+    prompts (> 384 rows, ~48+ per expert) take 128-token blocks so an expert's
+    weight tile is multiplied by all its tokens at once."""
+    return 32 if rows <= 32 else 64 if rows <= SKINNY_NT128_ROWS else 128
+
+
+SKINNY_NT128_ROWS = 384
 
 
 def expert_gemm_up_skinny(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d, ffn, nt=0,
