@@ -218,8 +218,10 @@ class DaopEngine:
             # first timed prefill (position 0 of layer 0 is rewritten by every prefill)
             self.attn.prefill(torch.zeros((1, d_model), device=self.model.device), 0, 0)
         self._lru = None  # LRU planner of the ondemand / prefetch engines (after prefill)
-        # fully resident prefill as one CUDA graph per prompt length (switch for A/B runs)
-        self.prefill_graphs = True
+        # fully resident prefill as one CUDA graph per prompt length: bit-identical,
+        # but measured no faster (the 256-token layer is GPU-bound, 0.59 ms either
+        # way) and the first prompt of a length pays the capture: off by default
+        self.prefill_graphs = False
         self._pf_graphs = {}
 
     # ------------------------------------------------------------ residency

@@ -225,7 +225,7 @@ def test_resident_prefill_graph_equals_eager(attention):
     for graphs in (False, True):
         eng = DaopEngine(shape, d, ffn, np.full((L, E), 0.25), 1.0, P.PolicyConfig("daop"),
                          seed=3, host_pool=pool, attention=attention, max_seq=128)
-        eng.prefill_graphs = graphs
+        eng.prefill_graphs = graphs  # the switch, both ways
         outs = []
         for s_ in (0, 1):
             pre = eng.prefill(eng.model.input_hidden(40, stream=500 + s_))
