@@ -56,3 +56,15 @@ t("down_pair", lambda: ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_
 off = pr["offsets"].tolist()
 print("rows per expert", [off[i + 1] - off[i] for i in range(E)])
 print(res, "moe sum (router..combine)", round(sum(res[x] for x in ("router", "permute+gather", "up_skinny", "down_skinny", "combine")), 1))
+# attention sub-ops
+from paper_2501_10375_b200 import _lib
+xa = torch.empty((T, d), dtype=torch.bfloat16, device="cuda")
+t("attn_norm_rows", lambda: _lib.call("daop_attn_norm_rows", h.data_ptr(), T, att.norm[0].data_ptr(), d,
+                                      float(ops.RMS_EPS), xa.data_ptr(), ops._s()))
+qkv = t("attn_qkv_gemm", lambda: ops.gemm_bf16_f32(xa, att.wqkv[0]))
+o = torch.empty((T, att.q_dim), dtype=torch.bfloat16, device="cuda")
+t("attn_core", lambda: _lib.call("daop_attn_prefill", qkv.data_ptr(), T, 0, att.k_cache[0].data_ptr(),
+                                 att.v_cache[0].data_ptr(), 32, 8, att.max_seq, float(att.theta),
+                                 o.data_ptr(), ops._s()))
+t("attn_o_gemm", lambda: ops.gemm_bf16_f32(o, att.wo[0], resid=h))
+print({k: v for k, v in res.items() if k.startswith("attn")})
