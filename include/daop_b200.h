@@ -397,16 +397,11 @@ int daop_l2_prefetch(const void* d_p0, int64_t n0, const void* d_p1, int64_t n1,
  *   daop_attn_prefill:   k (RoPE), v of every token -> the cache, then causal
  *                        flash attention on the tensor cores -> d_o (T, q) bf16
  *   daop_gemm_bf16_f32:  h' = h + o . Wo^T  (residual in the epilogue) */
-/* Dense projection on the tcgen05 pipeline: d_out (M, N) fp32 = d_a (M, K)
- * bf16 . d_w^T (d_w (N, K) bf16 row-major) [+ d_resid (M, N) fp32, may alias
- * d_out, NULL for none].  K % 64 == 0, N % 256 == 0.  M <= 768 runs on the
- * swap-AB skinny kernel, split over K (deterministic reduction) when
- * d_workspace holds daop_gemm_workspace() bytes whose counters were zeroed
- * once (NULL: no split); larger M on the CTA-pair kernel. */
-int daop_gemm_workspace(int64_t M, int32_t K, int32_t N, int64_t* h_bytes);
+/* Dense projection on the grouped-GEMM tcgen05 pipeline: d_out (M, N) fp32 =
+ * d_a (M, K) bf16 . d_w^T (d_w (N, K) bf16 row-major) [+ d_resid (M, N) fp32,
+ * may alias d_out, NULL for none].  K % 64 == 0, N % 256 == 0. */
 int daop_gemm_bf16_f32(const uint16_t* d_a, int64_t M, int32_t K, const uint16_t* d_w, int32_t N,
-                       const float* d_resid, float* d_out, void* d_workspace, int64_t ws_bytes,
-                       daop_stream_t stream);
+                       const float* d_resid, float* d_out, daop_stream_t stream);
 int daop_attn_norm_rows(const float* d_h, int64_t T, const uint16_t* d_gamma, int32_t d, float eps,
                         uint16_t* d_xa, daop_stream_t stream);
 int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, uint16_t* d_k_cache,

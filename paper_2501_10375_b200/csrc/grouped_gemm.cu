@@ -1021,25 +1021,15 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
 }
 
 int skinny_dense_gemm(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w, int32_t N,
-                      const float* resid, float* out, void* ws, int64_t ws_bytes,
-                      cudaStream_t st);
-int skinny_dense_workspace(int64_t M, int32_t K, int32_t N);
-
-// workspace of daop_gemm_bf16_f32 for split-K on prompt-sized M (0 = none
-// needed); the first bytes are counters that must be zero once (the kernel
-// leaves them zero again)
-extern "C" int daop_gemm_workspace(int64_t M, int32_t K, int32_t N, int64_t* bytes) {
-  *bytes = (M > 0 && M <= 768 && K % 64 == 0 && N % 128 == 0) ? skinny_dense_workspace(M, K, N) : 0;
-  return DAOP_OK;
-}
+                      const float* resid, float* out, cudaStream_t st);
 
 // Dense projection on the same tcgen05 pipeline (the prompt attention's QKV
 // and O projections, attention.py): out (M, N) fp32 = A (M, K) bf16 . W^T,
 // W (N, K) bf16 row-major, optionally + resid (M, N) fp32 (may alias out).
 // One "expert" of M rows without device tables; N % 256 == 0, K % 64 == 0.
 extern "C" int daop_gemm_bf16_f32(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w,
-                                  int32_t N, const float* resid, float* out, void* workspace,
-                                  int64_t ws_bytes, daop_stream_t stream) {
+                                  int32_t N, const float* resid, float* out,
+                                  daop_stream_t stream) {
   if (M < 0 || M >= (1ll << 31) || K < 64 || K % GB_K != 0 || N < GB_N || N % GB_N != 0) {
     set_error("dense GEMM: unsupported shape (M=%lld K=%d N=%d): needs K %% 64 == 0, "
               "N %% 256 == 0", static_cast<long long>(M), K, N);
@@ -1049,7 +1039,7 @@ extern "C" int daop_gemm_bf16_f32(const uint16_t* a, int64_t M, int32_t K, const
   // prompt-sized M: the swap-AB skinny kernel (weights as the MMA M side), so
   // the weight tiles spread over every SM instead of N / 256 CTA pairs
   if (M <= 768 && g_gemm_dense_skinny)
-    return skinny_dense_gemm(a, M, K, w, N, resid, out, workspace, ws_bytes, as_stream(stream));
+    return skinny_dense_gemm(a, M, K, w, N, resid, out, as_stream(stream));
   CUtensorMap ta, tb;
   int rc;
   const uint64_t adims[2] = {static_cast<uint64_t>(K), static_cast<uint64_t>(M)};

@@ -56,13 +56,6 @@ struct SkinnyParams {
   int64_t dense_rows;
   const float* resid;
   int w_keep;
-  // split-K (dense path, down form only): tile = (row tile, K slice, token
-  // block); each slice writes an fp32 partial into part (ksplit, M, N) and the
-  // last slice to finish a (tile, lane quarter) sums the partials in slice
-  // order (+ resid) -- deterministic; cnt (tiles x 4) zeroed once, self-resetting
-  int ksplit;
-  float* part;
-  unsigned* cnt;
 };
 
 __device__ __forceinline__ int64_t sk_off(const SkinnyParams& p, int e) {
@@ -104,20 +97,18 @@ struct SkinnyCfg {
 };
 
 template <int NT>
-__device__ __forceinline__ bool skinny_tile(const SkinnySmem<NT>& s, int E, int rt, int ks_n,
-                                            int t, int& e, int& blk, int& r, int& ks) {
+__device__ __forceinline__ bool skinny_tile(const SkinnySmem<NT>& s, int E, int rt, int t, int& e,
+                                            int& blk, int& r) {
   if (t >= s.prefix[E]) return false;
   e = 0;
   while (s.prefix[e + 1] <= t) ++e;
   const int u = t - s.prefix[e];
-  // token blocks fastest within a weight tile (slice): an expert with more
-  // than NT rows (a prompt) has its blocks of one weight tile on neighbouring
-  // CTAs at the same time, so the tile crosses HBM once and the rest hit L2
+  // token blocks fastest within a weight tile: an expert with more than NT
+  // rows (a prompt) has its blocks of one weight tile on neighbouring CTAs at
+  // the same time, so the tile crosses HBM once and the rest hit L2
   const int nb = s.blocks[e];
-  const int rk = u / nb;
-  blk = u - rk * nb;
-  r = rk / ks_n;
-  ks = rk - r * ks_n;
+  r = u / nb;
+  blk = u - r * nb;
   (void)rt;
   return true;
 }
@@ -151,7 +142,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int e = 0; e < E; ++e) {
       const int64_t me = sk_slot(p, e) >= 0 ? s.off[e + 1] - s.off[e] : 0;
       s.blocks[e] = static_cast<int>((me + NT - 1) / NT);
-      acc += s.blocks[e] * rt * p.ksplit;
+      acc += s.blocks[e] * rt;
       s.prefix[e + 1] = acc;
     }
   }
@@ -168,13 +159,12 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t pol_x = l2_evict_last_policy();   // tokens: re-read by every row tile
       int stage = 0;
       uint32_t phase = 0;
-      int e, blk, r, ks;
-      const int kb_per = p.k_blocks / p.ksplit;
-      for (int t = blockIdx.x; skinny_tile(s, E, rt, p.ksplit, t, e, blk, r, ks); t += gridDim.x) {
+      int e, blk, r;
+      for (int t = blockIdx.x; skinny_tile(s, E, rt, t, e, blk, r); t += gridDim.x) {
         const int slot = sk_slot(p, e);
         const int xrow = static_cast<int>(s.off[e]) + blk * NT;
         const uint64_t pol_w = (p.w_keep || s.blocks[e] > 1) ? pol_reuse : pol_once;
-        for (int kb = ks * kb_per; kb < (ks + 1) * kb_per; ++kb) {
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&s.empty[stage], phase ^ 1);
           uint8_t* st = tiles + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&s.full[stage], C::STAGE_BYTES);
@@ -195,13 +185,12 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // MMA issuer
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      int e, blk, r, ks;
-      const int kb_per = p.k_blocks / p.ksplit;
-      for (int t = blockIdx.x; skinny_tile(s, E, rt, p.ksplit, t, e, blk, r, ks); t += gridDim.x) {
+      int e, blk, r;
+      for (int t = blockIdx.x; skinny_tile(s, E, rt, t, e, blk, r); t += gridDim.x) {
         mbar_wait(&s.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * C::ACC_COLS;
-        for (int kb = 0; kb < kb_per; ++kb) {
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&s.full[stage], phase);
           tc_fence_after();
           uint8_t* st = tiles + stage * C::STAGE_BYTES;
@@ -233,8 +222,8 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    int e, blk, r, ks;
-    for (int t = blockIdx.x; skinny_tile(s, E, rt, p.ksplit, t, e, blk, r, ks); t += gridDim.x) {
+    int e, blk, r;
+    for (int t = blockIdx.x; skinny_tile(s, E, rt, t, e, blk, r); t += gridDim.x) {
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
       const int row = r * 128 + q * 32 + lane;
@@ -260,51 +249,19 @@ __global__ void __launch_bounds__(192, 1)
         } else {
           tmem_ld_wait();
           float* out = static_cast<float*>(p.out);
-          if (p.ksplit > 1) {  // this slice's partial (no residual yet)
-            float* part = p.part + static_cast<int64_t>(ks) * p.dense_rows * p.out_ld;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c + j < nvalid) part[(t0 + c + j) * p.out_ld + row] = __uint_as_float(g[j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c + j < nvalid) {
-                float* dst = p.row_dst ? reinterpret_cast<float*>(p.row_dst[t0 + c + j]) + row
-                                       : out + (t0 + c + j) * p.out_ld + row;
-                const float v = __uint_as_float(g[j]);
-                *dst = p.resid ? v + p.resid[(t0 + c + j) * p.out_ld + row] : v;
-              }
-          }
+          for (int j = 0; j < 32; ++j)
+            if (c + j < nvalid) {
+              float* dst = p.row_dst ? reinterpret_cast<float*>(p.row_dst[t0 + c + j]) + row
+                                     : out + (t0 + c + j) * p.out_ld + row;
+              const float v = __uint_as_float(g[j]);
+              *dst = p.resid ? v + p.resid[(t0 + c + j) * p.out_ld + row] : v;
+            }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s.tempty[acc]);
-      if constexpr (!SWIGLU) {
-        if (p.ksplit > 1) {
-          // the last K slice of this (tile, lane quarter) reduces the slices in
-          // order; the counter resets itself for the next call
-          __threadfence();
-          __syncwarp();
-          unsigned last = 0;
-          unsigned* c_ = p.cnt + (static_cast<int64_t>(r) * s.blocks[e] + blk) * 4 + q;
-          if (lane == 0) last = atomicAdd(c_, 1u) == static_cast<unsigned>(p.ksplit - 1);
-          last = __shfl_sync(0xffffffffu, last, 0);
-          if (last) {
-            __threadfence();
-            if (lane == 0) *c_ = 0;
-            float* out = static_cast<float*>(p.out);
-            for (int j = 0; j < nvalid; ++j) {
-              const int64_t o = (t0 + j) * p.out_ld + row;
-              float v = p.resid ? p.resid[o] : 0.f;
-              float acc_ = 0.f;
-              for (int k2 = 0; k2 < p.ksplit; ++k2)
-                acc_ += __ldcg(p.part + static_cast<int64_t>(k2) * p.dense_rows * p.out_ld + o);
-              out[o] = p.resid ? v + acc_ : acc_;
-            }
-          }
-        }
-      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -385,7 +342,6 @@ extern "C" int daop_expert_gemm_up_skinny(const uint16_t* x_perm, int64_t rows, 
   const uint32_t xbox[2] = {SK_K, static_cast<uint32_t>(nt)};
   if ((rc = make_tmap_bf16(&tx, x_perm, 2, xdims, xstr, xbox))) return rc;
   SkinnyParams p{d_offsets, d_slot_of, E, d / SK_K, ffn / 128, ffn, act, ffn};
-  p.ksplit = 1;
   return skinny_dispatch<true>(tw, tx, p, rows, nt, as_stream(stream));
 }
 
@@ -410,7 +366,6 @@ extern "C" int daop_expert_gemm_down_skinny(const uint16_t* act, int64_t rows, i
   const uint32_t xbox[2] = {SK_K, static_cast<uint32_t>(nt)};
   if ((rc = make_tmap_bf16(&tx, act, 2, xdims, xstr, xbox))) return rc;
   SkinnyParams p{d_offsets, d_slot_of, E, ffn / SK_K, d / 128, 0, y, d};
-  p.ksplit = 1;
   return skinny_dispatch<false>(tw, tx, p, rows, nt, as_stream(stream));
 }
 
@@ -446,32 +401,12 @@ extern "C" int daop_ep_expert_gemm_down_skinny(const uint16_t* act, int64_t rows
   SkinnyParams p{reinterpret_cast<const int64_t*>(ws + EP_LOCAL_OFF), d_slot_of, E, ffn / SK_K,
                  d / 128, 0, nullptr, d, reinterpret_cast<const uint64_t*>(ws + EP_ROWMAP),
                  reinterpret_cast<unsigned*>(ws + EP_DONE_GEMM), d_peers, G, rank, epoch};
-  p.ksplit = 1;
   return skinny_dispatch<false>(tw, tx, p, rows_cap, nt, as_stream(stream));
-}
-
-// split-K factor of the dense small-M path: enough tiles for two CTAs per SM
-static int dense_ksplit(int64_t M, int32_t K, int32_t N) {
-  const int nt = M <= 32 ? 32 : 64;
-  const int64_t tiles = (N / 128) * ((M + nt - 1) / nt);
-  int S = 1;
-  while (S < 8 && tiles * S < 2 * sm_count() && (K / SK_K) % (2 * S) == 0 && K / (2 * S) >= 512)
-    S *= 2;
-  return S;
-}
-
-int skinny_dense_workspace(int64_t M, int32_t K, int32_t N) {
-  const int S = dense_ksplit(M, K, N);
-  if (S == 1) return 0;
-  const int nt = M <= 32 ? 32 : 64;
-  const int64_t tiles = (N / 128) * ((M + nt - 1) / nt);
-  return static_cast<int>(((tiles * 4 * 4 + 255) / 256) * 256 + S * M * N * 4);
 }
 
 // the dense projection entry's small-M path (grouped_gemm.cu daop_gemm_bf16_f32)
 int skinny_dense_gemm(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w, int32_t N,
-                      const float* resid, float* out, void* ws, int64_t ws_bytes,
-                      cudaStream_t st) {
+                      const float* resid, float* out, cudaStream_t st) {
   int rc;
   CUtensorMap tw, tx;
   const uint64_t wdims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), 1};
@@ -487,14 +422,5 @@ int skinny_dense_gemm(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w
   p.dense_rows = M;
   p.resid = resid;
   p.w_keep = M > nt;
-  p.ksplit = 1;
-  const int S = dense_ksplit(M, K, N);
-  const int need = skinny_dense_workspace(M, K, N);
-  if (S > 1 && ws && ws_bytes >= need) {
-    const int64_t tiles = (N / 128) * ((M + nt - 1) / nt);
-    p.ksplit = S;
-    p.cnt = static_cast<unsigned*>(ws);
-    p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ((tiles * 16 + 255) / 256) * 256);
-  }
-  return skinny_dispatch<false>(tw, tx, p, M * p.ksplit, nt, st);
+  return skinny_dispatch<false>(tw, tx, p, M, nt, st);
 }

@@ -116,27 +116,9 @@ def gemm_bf16_f32(a, w, resid=None, out=None):
     if w.shape[1] != k or (resid is not None and tuple(resid.shape) != (m, n)):
         raise ShapeMismatchError(f"gemm: a {tuple(a.shape)}, w {tuple(w.shape)}")
     out = torch.empty((m, n), dtype=torch.float32, device=a.device) if out is None else out
-    nb = torch.zeros(1, dtype=torch.int64)
-    _lib.call("daop_gemm_workspace", m, k, n, nb.data_ptr())
-    ws = _gemm_workspace(a.device, int(nb[0]))
     _lib.call("daop_gemm_bf16_f32", a.data_ptr(), m, k, w.data_ptr(), n, _p(resid),
-              out.data_ptr(), _p(ws), 0 if ws is None else ws.numel(), _s())
+              out.data_ptr(), _s())
     return out
-
-
-_GEMM_WS = {}
-
-
-def _gemm_workspace(device, nbytes: int):
-    """Per-device split-K workspace, zeroed when (re)allocated; the kernel
-    leaves its counters zero, so calls on one stream can share it."""
-    if nbytes <= 0:
-        return None
-    ws = _GEMM_WS.get(device)
-    if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-        _GEMM_WS[device] = ws
-    return ws
 
 
 def set_gemm_mode(mode: int) -> None:
