@@ -16,6 +16,7 @@
 // (thread = weight row, tcgen05.ld 32x32b.x32 over the token columns; stores
 // for one token are 32 consecutive rows per warp).  Tile = (expert, token
 // block, 128-row weight tile), weight tiles fastest.
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -413,7 +414,18 @@ int skinny_dense_gemm(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w
   const uint64_t wstr[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K) * N * 2};
   const uint32_t wbox[3] = {SK_K, 128, 1};
   if ((rc = make_tmap_bf16(&tw, w, 3, wdims, wstr, wbox))) return rc;
-  const int nt = M <= 32 ? 32 : 64;
+  // token block (tuning override: DAOP_DENSE_NT environment variable)
+  static const int nt_env = [] {
+    const char* v = getenv("DAOP_DENSE_NT");
+    return v ? atoi(v) : 0;
+  }();
+  // default: 64-token blocks unless they leave SMs without a weight tile
+  // (256-token prompt: O-proj 128 tiles -> 32-token blocks, 56 vs 71 us;
+  // QKV 192 tiles -> 64, 43 vs 60 us)
+  const int64_t tiles64 = (N / 128) * ((M + 63) / 64);
+  const int nt = nt_env == 32 || nt_env == 64 || nt_env == 128
+                     ? nt_env
+                     : (M <= 32 || tiles64 < sm_count() ? 32 : 64);
   const uint64_t xdims[2] = {static_cast<uint64_t>(K), static_cast<uint64_t>(M)};
   const uint64_t xstr[1] = {static_cast<uint64_t>(K) * 2};
   const uint32_t xbox[2] = {SK_K, static_cast<uint32_t>(nt)};
