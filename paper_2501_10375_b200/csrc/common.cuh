@@ -121,6 +121,32 @@ __device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint3
       : "memory");
 }
 
+// 1-D bulk copy this CTA's shared memory -> global (bulk async-group)
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// four 8x8 b16 matrices from shared memory in mma fragment layout (lane l
+// supplies the address of row l % 8 of matrix l / 8)
+__device__ __forceinline__ uint4 ldmatrix_x4(const void* p) {
+  uint4 r;
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+
 // non-coherent 16-byte global load issued exactly here (volatile: the
 // compiler may not sink it to the first use)
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
@@ -200,6 +226,14 @@ __device__ __forceinline__ float rms_scale(double ss, int d, float eps) {
 __device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
   __nv_bfloat16 b = __float2bfloat16_rn(f);
   return *reinterpret_cast<uint16_t*>(&b);
+}
+
+// two f32 -> one bf16x2 word (lo in bits 0..15), round to nearest even: one
+// cvt instead of two + a permute; same bits as two f32_to_bf16_bits calls
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
 }
 
 __device__ __forceinline__ float silu_f32(float a) { return a / (1.0f + expf(-a)); }

@@ -233,20 +233,6 @@ __global__ void combine_kernel(const float* __restrict__ h, const float* __restr
 // of instructions (the register-staged versions above stall on memory
 // latency at ~55 % occupancy: ncu 2.5-3.4 TB/s).
 
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read_all() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
 
 // out[t] = h[t] + sum_j w[t,j] * y[inv[t,j]]  (fixed j order, fmaf: the same
 // arithmetic as combine_kernel).  Stage = [h row | y rows of the k picks].

@@ -526,6 +526,312 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma1_kernel(RouterAr
 }
 
 // ---------------------------------------------------------------------------
+// Bulk-copy router (d = 256 * KS, KS in {8, 16}; 2E <= 16): the default for
+// prompt-sized T.  The register-resident kernel above issues a tile's h loads
+// only after the previous tile's logits are done, so HBM idles through every
+// RMS / MMA / top-k phase (3.0 TB/s).  Here thread 0 streams 4-token tiles
+// (4 contiguous rows, one cp.async.bulk of 4 * d * 4 B, L2 evict_first) into
+// a ring of `stages` shared-memory stages (3 x 64 KB at d = 4096; a stage is
+// refilled right after the barrier that ends its tile), so two tiles are in
+// flight while the 16 warps work on the third.  (A dedicated producer warp
+// would cap the 17-warp CTA at 96 registers and spill.)  The gate rows do not
+// live in shared memory: warp w owns the d-slice [w S, (w + 1) S), S = 16 KS,
+// and keeps its A fragments (rows g, g + 8 of the slice) in registers.
+// Per tile, two CTA barriers:
+//   pass 1  warps 0..14: fp64 sums of squares, float4s lane-strided over the
+//           whole row (doubles assembled with integer ops: F2F.F64 is issued
+//           through MIO and was the pass's bottleneck); a transposed butterfly
+//           leaves token (lane >> 3)'s sum in lanes 0, 8, 16, 24; the last
+//           warp to arrive (shared-memory counter) turns the 15 partials into
+//           r in fixed warp order.  Warp 15 meanwhile finishes the PREVIOUS
+//           tile's 4 tokens (lane = token * 8 + expert: segmented softmax of
+//           both gates, top-k, renormalisation, counter).
+//   -- barrier A --
+//   pass 2  every warp: x = bf16(h * r * gamma) of its slice, in place in the
+//           stage (row tok shifted by tok * 16 B) and to x_out (8-byte
+//           coalesced stores); the slice's m16n8k16 chain with B fragments by
+//           ldmatrix.x4 (tokens 0..3 = columns 0..3; rows 4..7 repeat 0..3
+//           and their columns are discarded); partial logits -> zpart
+//   -- barrier B --  stage refill
+// The logits are the same MMA chains over the same 16-column k-steps as
+// router_mma1_kernel<KS>, summed over warps in the same order.
+// Measured (profiles/r02/stream_kernels.json, ncu_router_bulk.json): 32,768 tokens x d = 4096 in
+// ~164 us = 4.9 TB/s of algorithmic bytes (register-resident: 269 us).
+constexpr int kTmaTok = 4;
+constexpr int kPass1Warps = kMmaWarps - 1;
+
+// |v| as a double built with integer ops (the ALU pipe) instead of
+// F2F.F64.F32 (MIO-issued, the pass-1 bottleneck): exact for normal floats;
+// zeros / subnormals become values below 2^-126 whose squares (< 2^-252)
+// vanish in any fp64 sum that matters and underflow the f32 mean otherwise;
+// Inf / NaN become finite values >= 2^128 (squares >= 2^256, an f32 mean of
+// Inf -> r = 0 exactly as for Inf); NaN is restored by the caller from `mx`.
+__device__ __forceinline__ double abs_f32_as_f64(float v, uint32_t& mx) {
+  const uint32_t t = __float_as_uint(v) << 1;  // |v| bits, shifted left once
+  mx = max(mx, t);
+  return __hiloint2double((t >> 4) + 0x38000000u, __float_as_uint(v) << 29);
+}
+
+__device__ __forceinline__ double sq_acc4_int(float4 v, double a, uint32_t& mx) {
+  double x = abs_f32_as_f64(v.x, mx);
+  a = fma(x, x, a);
+  x = abs_f32_as_f64(v.y, mx);
+  a = fma(x, x, a);
+  x = abs_f32_as_f64(v.z, mx);
+  a = fma(x, x, a);
+  x = abs_f32_as_f64(v.w, mx);
+  return fma(x, x, a);
+}
+
+// finish 4 tokens of a tile in one warp: lane = tok * 8 + e (E <= 8)
+__device__ __forceinline__ void tile_finish(const RouterArgs& a, int64_t t0, int n, int lane,
+                                            const float* zpart) {
+  const int E = a.E, tok = lane >> 3, e = lane & 7;
+  const bool ex = e < E;
+  float zt = 0.f, zp = 0.f;
+  if (ex) {
+#pragma unroll
+    for (int w = 0; w < kMmaWarps; ++w) {
+      zt += zpart[(w * 16 + e) * kTmaTok + tok];
+      if (a.wg_next) zp += zpart[(w * 16 + E + e) * kTmaTok + tok];
+    }
+  }
+  // segmented softmax over the 8 lanes of the token (== lane_softmax_p2: the
+  // extra lanes contribute -inf to the max and +0 to the sum)
+  float m = ex ? zt : -INFINITY, mp = ex ? zp : -INFINITY;
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    mp = fmaxf(mp, __shfl_xor_sync(0xffffffffu, mp, o));
+  }
+  const float et = ex ? expf(zt - m) : 0.f, ep = ex ? expf(zp - mp) : 0.f;
+  float st = et, sp = ep;
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    st += __shfl_xor_sync(0xffffffffu, st, o);
+    sp += __shfl_xor_sync(0xffffffffu, sp, o);
+  }
+  const float p = ex ? et / st : 0.f;
+  const bool live = tok < n;
+  const int64_t tt = t0 + tok;
+  if (live && ex) {
+    a.p_true[tt * E + e] = p;
+    if (a.wg_next) a.p_pred[tt * E + e] = ep / sp;
+  }
+  const int seg = lane & ~7;
+  bool taken = !ex;
+  int my_sel = -1;
+  float my_p = 0.f, den = 0.f;
+  for (int j = 0; j < a.k; ++j) {
+    float bv = taken ? -INFINITY : p;
+    int bi = taken ? 0x7fffffff : e;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    bi = __shfl_sync(0xffffffffu, bi, seg);
+    bv = __shfl_sync(0xffffffffu, bv, seg);
+    if (bi >= E) {  // NaN scores never compare: first untaken id (topk_scan rule)
+      const unsigned free_ = (__ballot_sync(0xffffffffu, !taken) >> seg) & 0xffu;
+      bi = __ffs(free_) - 1;
+      bv = __shfl_sync(0xffffffffu, p, seg + bi);
+    }
+    den += bv;
+    if (e == j) {
+      my_sel = bi;
+      my_p = bv;
+    }
+    if (e == bi) taken = true;
+  }
+  if (live && e < a.k) {
+    a.topk_idx[tt * a.k + e] = my_sel;
+    a.topk_w[tt * a.k + e] = my_p / den;
+    if (a.hist) atomicAdd(a.hist + (tt / a.tokens_per_seq) * a.hist_seq_stride + my_sel, 1);
+  }
+}
+
+template <int KS>
+__global__ void __launch_bounds__(kMmaWarps * 32, 1) router_tma_kernel(RouterArgs a, int stages) {
+  constexpr int TOK = kTmaTok;
+  constexpr int S = KS * 16;                   // d-slice per warp
+  constexpr int NV4 = KS / 8;                  // float4s per lane per token row of the slice
+  constexpr int NV4ROW = KS * 64;              // float4s per row (d / 4)
+  constexpr int P1 = kPass1Warps * 32;         // pass-1 lanes
+  constexpr int P1FULL = NV4ROW / P1, P1REM = NV4ROW % P1;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int d = a.d, E = a.E;
+  const int rows = a.wg_next ? 2 * E : E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t stage_bytes = static_cast<uint32_t>(TOK) * d * 4;
+  uint8_t* ring = smem;
+  double* sspart = reinterpret_cast<double*>(smem + static_cast<size_t>(stages) * stage_bytes);
+  float* zpart = reinterpret_cast<float*>(sspart + kMmaWarps * TOK);  // [warp][16 rows][TOK]
+  float* rs = zpart + kMmaWarps * 16 * TOK;                           // [TOK]
+  unsigned* arrived = reinterpret_cast<unsigned*>(rs + TOK);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rs + 8);
+  const int64_t ntiles = (a.T + TOK - 1) / TOK;
+  uint64_t pol = 0;
+  // thread 0 issues tile i's copy into stage i % stages: the first `stages`
+  // tiles here, tile i + stages right after the barrier that ends tile i
+  auto issue = [&](int64_t tile, int s) {
+    if (tile >= ntiles) return;
+    const int64_t t0 = tile * TOK;
+    const int64_t n = a.T - t0 < TOK ? a.T - t0 : TOK;
+    const uint32_t bytes = static_cast<uint32_t>(n * d * 4);
+    mbar_arrive_expect_tx(&full[s], bytes);
+    bulk_g2s(ring + static_cast<size_t>(s) * stage_bytes, a.h + t0 * d, bytes, &full[s], pol);
+  };
+  if (threadIdx.x == 0) {
+    pol = l2_evict_first_policy();
+    *arrived = 0;
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < stages; ++s) issue(blockIdx.x + static_cast<int64_t>(s) * gridDim.x, s);
+  }
+  __syncthreads();
+
+  const int g = lane >> 2, c = lane & 3, c2 = c * 2;
+  const int base = warp * S;
+  uint32_t af[KS][4];
+  {
+    const uint16_t* r0 = g < E ? a.wg + static_cast<size_t>(g) * d
+                               : (g < rows ? a.wg_next + static_cast<size_t>(g - E) * d : nullptr);
+    const int g8 = g + 8;
+    const uint16_t* r1 = g8 < E ? a.wg + static_cast<size_t>(g8) * d
+                                : (g8 < rows ? a.wg_next + static_cast<size_t>(g8 - E) * d : nullptr);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = base + ks * 16 + c2;
+      af[ks][0] = r0 ? __ldg(reinterpret_cast<const uint32_t*>(r0 + k)) : 0u;
+      af[ks][1] = r1 ? __ldg(reinterpret_cast<const uint32_t*>(r1 + k)) : 0u;
+      af[ks][2] = r0 ? __ldg(reinterpret_cast<const uint32_t*>(r0 + k + 8)) : 0u;
+      af[ks][3] = r1 ? __ldg(reinterpret_cast<const uint32_t*>(r1 + k + 8)) : 0u;
+    }
+  }
+  uint2 gm[NV4];
+#pragma unroll
+  for (int j = 0; j < NV4; ++j)
+    gm[j] = *reinterpret_cast<const uint2*>(a.gamma + base + j * 128 + lane * 4);
+  const bool hi16 = lane & 16, hi8 = lane & 8;
+  const int p1 = warp * 32 + lane;                    // pass-1 lane id (warps 0..14)
+  const double inv_d = 1.0 / static_cast<double>(d);  // d = 2^11 / 2^12: exact
+  int64_t prev_t0 = -1;
+  int prev_n = 0;
+  int s = 0;
+  uint32_t phase = 0;  // parity of stage s's current fill
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint8_t* st = ring + static_cast<size_t>(s) * stage_bytes;
+    const int64_t t0 = tile * TOK;
+    const int n = static_cast<int>(a.T - t0 < TOK ? a.T - t0 : TOK);
+    if (warp < kPass1Warps) {
+      // pass 1: fp64 sums of squares of the 4 rows, lane-strided float4s
+      mbar_wait(&full[s], phase);
+      double ss[TOK];
+#pragma unroll
+      for (int tok = 0; tok < TOK; ++tok) {
+        const float4* hrow = reinterpret_cast<const float4*>(st) + tok * NV4ROW + p1;
+        double v = 0.0;
+        uint32_t mx = 0;
+#pragma unroll
+        for (int j = 0; j < P1FULL; ++j) v = sq_acc4_int(hrow[j * P1], v, mx);
+        if (p1 < P1REM) v = sq_acc4_int(hrow[P1FULL * P1], v, mx);
+        ss[tok] = mx > 0xff000000u ? __longlong_as_double(0x7ff8000000000000ll) : v;  // NaN in
+      }
+      const double s0 = __shfl_xor_sync(0xffffffffu, hi16 ? ss[0] : ss[2], 16);
+      const double s1 = __shfl_xor_sync(0xffffffffu, hi16 ? ss[1] : ss[3], 16);
+      const double k0 = (hi16 ? ss[2] : ss[0]) + s0;
+      const double k1 = (hi16 ? ss[3] : ss[1]) + s1;
+      const double s2 = __shfl_xor_sync(0xffffffffu, hi8 ? k0 : k1, 8);
+      double v = (hi8 ? k1 : k0) + s2;
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if ((lane & 7) == 0) sspart[warp * TOK + (lane >> 3)] = v;
+      // the last pass-1 warp turns the partials into r (fixed warp order)
+      __threadfence_block();
+      __syncwarp();
+      unsigned last = 0;
+      if (lane == 0) last = atomicAdd(arrived, 1u) == kPass1Warps - 1;
+      if (__shfl_sync(0xffffffffu, last, 0)) {
+        __threadfence_block();
+        if (lane < TOK) {
+          double tot = 0.0;
+#pragma unroll
+          for (int w = 0; w < kPass1Warps; ++w) tot += sspart[w * TOK + lane];
+          const float ms = static_cast<float>(tot * inv_d);
+          rs[lane] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.eps)));
+        }
+        if (lane == 0) *arrived = 0;
+      }
+    } else {
+      if (prev_t0 >= 0) tile_finish(a, prev_t0, prev_n, lane, zpart);
+      mbar_wait(&full[s], phase);
+    }
+    __syncthreads();  // A
+    // pass 2: x in place (row tok of the slice shifted by tok * 16 B) and to
+    // x_out, then the slice's MMA chain
+#pragma unroll
+    for (int tok = 0; tok < TOK; ++tok) {
+      const float r = rs[tok];
+      const float* hrow = reinterpret_cast<const float*>(st) + static_cast<size_t>(tok) * d + base;
+      float4 hv[NV4];
+#pragma unroll
+      for (int j = 0; j < NV4; ++j) hv[j] = *reinterpret_cast<const float4*>(hrow + j * 128 + lane * 4);
+      __syncwarp();
+      uint8_t* xs = st + static_cast<size_t>(tok) * d * 4 + static_cast<size_t>(base) * 4 + tok * 16;
+#pragma unroll
+      for (int j = 0; j < NV4; ++j) {
+        uint2 xw;
+        xw.x = cvt_bf16x2(__fmul_rn(__fmul_rn(hv[j].x, r), bf16lo(gm[j].x)),
+                          __fmul_rn(__fmul_rn(hv[j].y, r), bf16hi(gm[j].x)));
+        xw.y = cvt_bf16x2(__fmul_rn(__fmul_rn(hv[j].z, r), bf16lo(gm[j].y)),
+                          __fmul_rn(__fmul_rn(hv[j].w, r), bf16hi(gm[j].y)));
+        *reinterpret_cast<uint2*>(xs + (j * 128 + lane * 4) * 2) = xw;
+        if (a.x_out && tok < n)
+          *reinterpret_cast<uint2*>(a.x_out + (t0 + tok) * d + base + j * 128 + lane * 4) = xw;
+      }
+    }
+    __syncwarp();
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      // ldmatrix row = token (lane & 3; rows 4..7 repeat 0..3, their columns
+      // are discarded), matrix = 8-column quarter of the k-step pair
+      const int rt = lane & 3, q = lane >> 3;
+      const uint8_t* xr = st + static_cast<size_t>(rt) * d * 4 + static_cast<size_t>(base) * 4 +
+                          rt * 16 + q * 16;
+#pragma unroll
+      for (int pp = 0; pp < KS / 2; ++pp) {
+          const uint4 b = ldmatrix_x4(xr + pp * 64);
+        mma_bf16_16816(acc, af[2 * pp], b.x, b.y);
+        mma_bf16_16816(acc, af[2 * pp + 1], b.z, b.w);
+      }
+    }
+    fence_proxy_async();  // this warp's generic smem traffic before the stage's refill
+    float* zb = zpart + warp * 16 * TOK;
+    if (c2 < TOK) {
+      zb[g * TOK + c2] = acc[0];
+      zb[g * TOK + c2 + 1] = acc[1];
+      zb[(g + 8) * TOK + c2] = acc[2];
+      zb[(g + 8) * TOK + c2 + 1] = acc[3];
+    }
+    __syncthreads();  // B
+    if (threadIdx.x == 0) issue(tile + static_cast<int64_t>(stages) * gridDim.x, s);
+    prev_t0 = t0;
+    prev_n = n;
+    if (++s == stages) {
+      s = 0;
+      phase ^= 1u;
+    }
+  }
+  if (warp == kMmaWarps - 1 && prev_t0 >= 0) tile_finish(a, prev_t0, prev_n, lane, zpart);
+}
+
+// ---------------------------------------------------------------------------
 // Decode-sized batches (T <= 128): one CTA per token, 16 warps splitting d.
 // The tensor-core router above amortises its 128 KB gate staging over many
 // 8-token tiles; with a handful of tokens it would run a few CTAs through
@@ -645,11 +951,14 @@ using namespace daop;
 // tuning switch (daop_set_router_mode): 1 = single-pass router where it applies
 static int g_router_single_pass = 1;
 static int g_router_prefetch = 1;
+static int g_router_tma = 1;
 
-// bit 0: single pass; bits 4..7: + 1 = L2 prefetch distance of the single-pass
-// kernel in grid-strides (0 in those bits keeps the current distance)
+// bit 0: single pass; bit 2: bulk-copy router OFF; bits 4..7: + 1 = L2
+// prefetch distance of the single-pass kernel in grid-strides (0 in those
+// bits keeps the current distance)
 extern "C" int daop_set_router_mode(int32_t mode) {
   g_router_single_pass = mode & 1;
+  g_router_tma = (mode & 4) ? 0 : 1;
   if ((mode >> 4) & 15) g_router_prefetch = ((mode >> 4) & 15) - 1;
   return DAOP_OK;
 }
@@ -677,8 +986,28 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
     DAOP_CHECK_LAUNCH("router_small");
     return DAOP_OK;
   }
-  // single-pass router: d = 256 * KS with KS in {4, 8, 12, 16} (h slice in registers)
   const int ks1 = d % (16 * kMmaWarps) == 0 ? d / (16 * kMmaWarps) : 0;
+  // bulk-copy router: d = 256 * KS with KS in {8, 16}, E <= 8 (one finisher warp)
+  if (rows <= 16 && E <= 8 && g_router_single_pass && g_router_tma && (ks1 == 8 || ks1 == 16)) {
+    const size_t stage = static_cast<size_t>(kTmaTok) * d * 4;
+    const size_t fixed = kMmaWarps * kTmaTok * 8 + kMmaWarps * 16 * kTmaTok * 4 + 8 * 4 + 8 * 8;
+    int stages = static_cast<int>((232448 - fixed) / stage);
+    if (stages > 6) stages = 6;
+    const size_t smem = stages * stage + fixed;
+    const int64_t ntiles = (T + kTmaTok - 1) / kTmaTok;
+    const int blocks = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
+    auto launch = [&](auto kern) {
+      DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      kern<<<blocks, kMmaWarps * 32, smem, as_stream(st)>>>(a, stages);
+      return DAOP_OK;
+    };
+    const int rc = ks1 == 8 ? launch(router_tma_kernel<8>) : launch(router_tma_kernel<16>);
+    if (rc) return rc;
+    DAOP_CHECK_LAUNCH("router_tma");
+    return DAOP_OK;
+  }
+  // single-pass router: d = 256 * KS with KS in {4, 8, 12, 16} (h slice in registers)
   if (rows <= 16 && g_router_single_pass && (ks1 == 4 || ks1 == 8 || ks1 == 12 || ks1 == 16)) {
     const size_t smem1 = static_cast<size_t>(16) * (d + 8) * 2 + static_cast<size_t>(d) * 2 +
                          kMmaWarps * kTokTile * 8 + kMmaWarps * 16 * kTokTile * 4;

@@ -72,10 +72,13 @@ def router(h, gamma, wg, wg_next, k, *, hist=None, tokens_per_seq=0, hist_seq_st
     return {"x": x, "p": p, "p_pred": pp, "topk_idx": idx, "topk_w": w}
 
 
-def set_router_mode(single_pass: bool, prefetch: int = -1) -> None:
+def set_router_mode(single_pass: bool, prefetch: int = -1, bulk: bool = True) -> None:
     """Tuning switch: single-pass tensor-core router (default) or two-pass;
-    prefetch >= 0 sets the single-pass kernel's L2 prefetch distance."""
-    mode = int(bool(single_pass)) | ((prefetch + 1) << 4 if prefetch >= 0 else 0)
+    prefetch >= 0 sets the register-resident single-pass kernel's L2 prefetch
+    distance; bulk=False turns the bulk-copy (shared-memory ring) router off,
+    leaving the register-resident single-pass kernel."""
+    mode = (int(bool(single_pass)) | (0 if bulk else 4)
+            | ((prefetch + 1) << 4 if prefetch >= 0 else 0))
     _lib.call("daop_set_router_mode", mode)
 
 

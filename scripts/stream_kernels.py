@@ -40,14 +40,16 @@ def timed(fn):
 
 
 res = {}
-for pf in (0, 1, 2, 3):
-    ops.set_router_mode(True, prefetch=pf)
+ops.set_router_mode(True, bulk=True)
+res["router_bulk"] = (timed(lambda: ops.router(h, m.norm[0], m.gate[0], m.gate[1], k)), T * d * 6)
+for pf in (0, 1):
+    ops.set_router_mode(True, prefetch=pf, bulk=False)
     res[f"router_single_pf{pf}"] = (timed(lambda: ops.router(h, m.norm[0], m.gate[0], m.gate[1],
                                                              k)), T * d * 6)
 ops.set_router_mode(False)
 res["router_two_pass"] = (timed(lambda: ops.router(h, m.norm[0], m.gate[0], m.gate[1], k)),
                           T * d * 6)
-ops.set_router_mode(True, prefetch=int(os.environ.get("DAOP_PF", "1")))
+ops.set_router_mode(True, prefetch=int(os.environ.get("DAOP_PF", "1")), bulk=True)
 r = ops.router(h, m.norm[0], m.gate[0], m.gate[1], k)
 x, idx, w = r["x"], r["topk_idx"], r["topk_w"]
 res["permute_only"] = (timed(lambda: ops.permute(idx, E)), T * k * 16)

@@ -155,7 +155,9 @@ def test_device_planner_matches_golden(P, golden):
                                      (6144, 8, 2, 4100),  # 8x22B width: tensor-core path
                                      # T <= 128: CTA-per-token kernel; 129: tensor-core path
                                      (4096, 8, 2, 1), (4096, 8, 2, 128), (4096, 8, 2, 129),
-                                     (512, 4, 1, 5), (256, 2, 1, 3), (6144, 8, 2, 64)])
+                                     (512, 4, 1, 5), (256, 2, 1, 3), (6144, 8, 2, 64),
+                                     # bulk-copy router: partial last tile, E = 4 (zero rows)
+                                     (2048, 8, 2, 1003), (4096, 4, 1, 517)])
 def test_router_parity(P, d, E, k, T):
     pkg, model_mod, ops = P
     om = N.OracleModel(3, E, k, d, 512, seed=4)
@@ -543,23 +545,27 @@ def test_batched_decode_graph_replay_bitexact(P, B):
             assert torch.equal(r[key], want[key]), (step, key)
 
 
-@pytest.mark.parametrize("d,T", [(1024, 129), (4096, 1000), (4096, 4099), (6144, 300), (3072, 777)])
+@pytest.mark.parametrize("d,T", [(1024, 129), (4096, 1000), (4096, 4099), (6144, 300), (3072, 777),
+                                 (2048, 130), (2048, 5003), (4096, 32771)])
 def test_router_single_pass_equals_two_pass(P, d, T):
-    """The single-pass router (h slice in registers) and the two-pass one
-    (L2 re-read) produce identical bits: x, p, p_pred, top-k, weights, counts."""
+    """The bulk-copy router (shared-memory ring, d = 2048 / 4096), the
+    register-resident single-pass router and the two-pass one (L2 re-read)
+    produce identical bits: x, p, p_pred, top-k, weights, counts."""
     pkg, model_mod, ops = P
     E, k = 8, 2
     m = model_mod.MoEModel(pkg.ModelShape(2, E, k), d, 512, seed=2, resident_layers=[])
     h = m.input_hidden(T, stream=8)
     outs = []
-    for mode in (1, 0):
-        ops.set_router_mode(mode)
+    for mode in (1, 1 | 4, 0):
+        ops.set_router_mode(bool(mode & 1), bulk=not (mode & 4))
         hist = torch.zeros((2, E), dtype=torch.int32, device="cuda")
         r = ops.router(h, m.norm[0], m.gate[0], m.gate[1], k, hist=hist, tokens_per_seq=(T + 1) // 2,
                        hist_seq_stride=E)
         outs.append((r, hist))
-    ops.set_router_mode(1)
-    (r1, h1), (r0, h0) = outs
+    ops.set_router_mode(True)
+    (r1, h1), (rr, hr), (r0, h0) = outs
     for key in ("x", "p", "p_pred", "topk_idx", "topk_w"):
         assert torch.equal(r1[key], r0[key]), key
+        assert torch.equal(rr[key], r0[key]), key
+    assert torch.equal(hr, h0)
     assert torch.equal(h1, h0)
