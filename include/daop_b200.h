@@ -402,6 +402,14 @@ int daop_l2_prefetch(const void* d_p0, int64_t n0, const void* d_p1, int64_t n1,
  * may alias d_out, NULL for none].  K % 64 == 0, N % 256 == 0. */
 int daop_gemm_bf16_f32(const uint16_t* d_a, int64_t M, int32_t K, const uint16_t* d_w, int32_t N,
                        const float* d_resid, float* d_out, daop_stream_t stream);
+/* Same product with a caller-owned fp32 workspace d_ws (ws_bytes): prompt-sized
+ * M (<= 256 rows, whose N / 256 CTA-pair tiles leave most SMs idle) splits K
+ * over the idle SM pairs into ksplit fp32 partials in d_ws (ksplit x M x N x 4
+ * bytes, ksplit <= 8) and sums them in fixed order [+ d_resid] into d_out.
+ * Without room in d_ws, or for larger M, it is daop_gemm_bf16_f32. */
+int daop_gemm_bf16_f32_ws(const uint16_t* d_a, int64_t M, int32_t K, const uint16_t* d_w,
+                          int32_t N, const float* d_resid, float* d_out, float* d_ws,
+                          int64_t ws_bytes, daop_stream_t stream);
 int daop_attn_norm_rows(const float* d_h, int64_t T, const uint16_t* d_gamma, int32_t d, float eps,
                         uint16_t* d_xa, daop_stream_t stream);
 int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, uint16_t* d_k_cache,

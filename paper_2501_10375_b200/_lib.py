@@ -58,6 +58,7 @@ PROTOS = {
                                    P],
     "daop_expert_gemm_down": [P, I64, I32, I32, P, I64, I64, P, P, I32, P, I32, P],
     "daop_gemm_bf16_f32": [P, I64, I32, P, I32, P, P, P],
+    "daop_gemm_bf16_f32_ws": [P, I64, I32, P, I32, P, P, P, I64, P],
     "daop_set_router_mode": [I32],
     "daop_set_stream_mode": [I32, I32, I32, I32],
     "daop_l2_prefetch": [P, I64, P, I64, P],

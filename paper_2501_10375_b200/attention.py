@@ -35,6 +35,7 @@ class AttentionStack:
                  max_seq: int = 4096, theta: float = 1e6, seed: int = 0, device="cuda"):
         self.L, self.d, self.n_heads, self.n_kv = num_layers, d_model, n_heads, n_kv
         self.max_seq, self.theta, self.seed = max_seq, theta, seed
+        self.split_k = True  # prompt projections: split-K path (daop_gemm_bf16_f32_ws)
         self.device = torch.device(device)
         self.q_dim, self.kv_dim = n_heads * HEAD_DIM, n_kv * HEAD_DIM
         rows = self.q_dim + 2 * self.kv_dim
@@ -86,13 +87,14 @@ class AttentionStack:
         xa = torch.empty((T, d), dtype=torch.bfloat16, device=h.device)
         _lib.call("daop_attn_norm_rows", h.data_ptr(), T, self.norm[layer].data_ptr(), d,
                   float(ops.RMS_EPS), xa.data_ptr(), ops._s())
-        qkv = ops.gemm_bf16_f32(xa, self.wqkv[layer])
+        ws = True if self.split_k else None  # split-K over idle SMs for short prompts
+        qkv = ops.gemm_bf16_f32(xa, self.wqkv[layer], ws=ws)
         o = torch.empty((T, self.q_dim), dtype=torch.bfloat16, device=h.device)
         _lib.call("daop_attn_prefill", qkv.data_ptr(), T, int(pos0),
                   self.k_cache[layer].data_ptr(), self.v_cache[layer].data_ptr(), self.n_heads,
                   self.n_kv, self.max_seq, float(self.theta), o.data_ptr(), ops._s())
         # O projection with the residual added in the GEMM epilogue
-        return ops.gemm_bf16_f32(o, self.wo[layer], resid=h, out=out)
+        return ops.gemm_bf16_f32(o, self.wo[layer], resid=h, out=out, ws=ws)
 
     def prefetch_l2(self, layer: int) -> None:
         """Queue an L2 prefetch of `layer`'s Wqkv and Wo (84 MB at the

@@ -97,6 +97,13 @@ struct GemmParams {
   // added in the down epilogue: out = resid + A . B^T (resid may alias out)
   int64_t dense_rows;
   const float* resid;
+  // split-K (dense GEMM, 256-row pair tile only): n_tiles counts ksplit x the
+  // real n-tiles (tile n_eff -> k-slice n_eff / n_real, n-tile n_eff % n_real);
+  // slice ks covers k-blocks [ks K / ksplit, (ks + 1) K / ksplit) and stores
+  // its fp32 partial at out + ks * part_stride (resid is added by the
+  // fixed-order reduction, dense_splitk_reduce_kernel)
+  int ksplit;
+  int64_t part_stride;
   // epilogue stores as streaming (st.global.cs: evict-first in L2) so the
   // 1.9 GB act / 1.1 GB y output streams do not push the re-read A / B
   // operand tiles out of L2 (tuning bit, daop_set_gemm_mode bit 14)
@@ -374,13 +381,14 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         float* out = p.row_dst ? (valid ? reinterpret_cast<float*>(p.row_dst[grow]) + n * GB_N
                                         : nullptr)
                                : static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
+        const float* resid = p.resid;  // (no split-K on the single-CTA kernel)
 #pragma unroll 1
         for (int c = 0; c < GB_N; c += 32) {
           uint32_t v[32];
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
           if (valid)
-            store_f32x32(out + c, p.resid ? p.resid + grow * p.out_ld + n * GB_N + c : nullptr, v,
+            store_f32x32(out + c, resid ? resid + grow * p.out_ld + n * GB_N + c : nullptr, v,
                          p.store_cs);
         }
       }
@@ -523,6 +531,23 @@ __device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, 
   return true;
 }
 
+// split-K decode of a tile's n index (GemmParams::ksplit)
+__device__ __forceinline__ void split_tile(const GemmParams& p, int n_eff, int& n, int& ks, int& kb0,
+                                           int& kb1) {
+  if (p.ksplit <= 1) {
+    n = n_eff;
+    ks = 0;
+    kb0 = 0;
+    kb1 = p.k_blocks;
+    return;
+  }
+  const int nr = p.n_tiles / p.ksplit;
+  ks = n_eff / nr;
+  n = n_eff - ks * nr;
+  kb0 = ks * p.k_blocks / p.ksplit;
+  kb1 = (ks + 1) * p.k_blocks / p.ksplit;
+}
+
 template <bool SWIGLU, bool TWO_M = false, int EW = 8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::THREADS, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -590,6 +615,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
       uint32_t phase = 0;
       int e, m, n;
       for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+        int ks, kb0, kb1;
+        split_tile(p, n, n, ks, kb0, kb1);
         const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * C::M) + rank * 128;
         const int slot = slot_at(p, e);
         const int brow = n * p.b_tile_rows + (leader ? 0 : p.b_half2);
@@ -607,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
               gi[b][q2] = p.a_perm[r] / p.a_k;
             }
         }
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           if (lane == 0) mbar_wait(&s.empty[stage], phase ^ 1);
           if (p.a_perm) __syncwarp();  // (dense A: lane 0 runs this loop alone)
           uint8_t* st = tiles + stage * C::STAGE_BYTES;
@@ -643,10 +670,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
       uint32_t phase = 0, acc_phase = 0;
       int e, m, n;
       for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+        int ks, kb0, kb1;
+        split_tile(p, n, n, ks, kb0, kb1);
         mbar_wait(&s.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * GB_N;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&s.full[stage], phase);
           tc_fence_after();
           uint8_t* st = tiles + stage * C::STAGE_BYTES;
@@ -654,11 +683,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
           const uint64_t bdesc = umma_desc_sw128(smem_u32(st + C::A_BYTES));
 #pragma unroll
           for (int k = 0; k < GB_K / 16; ++k) {
-            umma_bf16_pair(tmem_d, adesc + 2 * k, bdesc + 2 * k, P_IDESC, (kb | k) != 0);
+            umma_bf16_pair(tmem_d, adesc + 2 * k, bdesc + 2 * k, P_IDESC, ((kb - kb0) | k) != 0);
             if constexpr (TWO_M) {  // same B, second A half -> TMEM columns 256..511
               const uint64_t adesc1 = umma_desc_sw128(smem_u32(st + P_A_BYTES));
               umma_bf16_pair(tmem_d + GB_N, adesc1 + 2 * k, bdesc + 2 * k, P_IDESC,
-                             (kb | k) != 0);
+                             ((kb - kb0) | k) != 0);
             }
           }
           umma_commit_pair(&s.empty[stage], 0x3);
@@ -690,6 +719,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
     uint32_t acc_phase = 0;
     int e, m, n;
     for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+      int ks, kb0, kb1;
+      split_tile(p, n, n, ks, kb0, kb1);
       mbar_wait(&s.tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t me = s.off[e + 1] - s.off[e];
@@ -734,7 +765,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
       } else {
         float* out = p.row_dst ? (valid ? reinterpret_cast<float*>(p.row_dst[grow]) + n * GB_N
                                         : nullptr)
-                               : static_cast<float*>(p.out) + grow * p.out_ld + n * GB_N;
+                               : static_cast<float*>(p.out) + ks * p.part_stride +
+                                     grow * p.out_ld + n * GB_N;
+        const float* resid = p.ksplit > 1 ? nullptr : p.resid;
 #pragma unroll 1
         for (int c = sub * (GB_N / C::GROUPS_PER_HALF); c < (sub + 1) * (GB_N / C::GROUPS_PER_HALF);
              c += 32) {
@@ -742,7 +775,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
           if (valid)
-            store_f32x32(out + c, p.resid ? p.resid + grow * p.out_ld + n * GB_N + c : nullptr, v,
+            store_f32x32(out + c, resid ? resid + grow * p.out_ld + n * GB_N + c : nullptr, v,
                          p.store_cs);
         }
       }
@@ -801,6 +834,7 @@ static int g_gemm_store_cs = 0;  // epilogue streaming stores (tuning)
 static int g_gemm_dense_skinny = 1;  // tuning: small-M dense GEMMs on the skinny kernel
 static int g_gemm_epi16 = 0;  // tuning: 16 epilogue warps for the 512-row pair tile
 static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
+static int g_gemm_splitk = 1;  // tuning: split-K for prompt-sized dense projections (_ws entry)
 
 template <bool TWO_M>
 static size_t pair_smem_bytes() {
@@ -925,6 +959,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_store_cs = (mode >> 14) & 1;
   g_gemm_dense_skinny = !((mode >> 15) & 1);
   g_gemm_epi16 = (mode >> 16) & 1;
+  g_gemm_splitk = !((mode >> 17) & 1);
   return DAOP_OK;
 }
 
@@ -1057,6 +1092,74 @@ extern "C" int daop_gemm_bf16_f32(const uint16_t* a, int64_t M, int32_t K, const
   p.dense_rows = M;
   p.resid = resid;
   return launch_gemm<false>(ta, tb, p, M, as_stream(stream));
+}
+
+// fixed-order reduction of the split-K partials: out = [resid +] p_0 + p_1 + ...
+__global__ void __launch_bounds__(256) dense_splitk_reduce_kernel(const float4* parts, int ksplit,
+                                                                  int64_t stride4,
+                                                                  const float4* resid,
+                                                                  float4* out, int64_t n4) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 a = resid ? resid[i] : parts[i];
+    for (int ks = resid ? 0 : 1; ks < ksplit; ++ks) {
+      const float4 b = parts[ks * stride4 + i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    out[i] = a;
+  }
+}
+
+// Prompt-sized dense projections (M <= 256 rows: one 256-row CTA-pair tile
+// of N / 256 n-tiles, fewer than the SM pairs): split K over the idle pairs,
+// fp32 partials into the caller's workspace, then one fixed-order reduction
+// pass (+ the residual).  Otherwise daop_gemm_bf16_f32.
+extern "C" int daop_gemm_bf16_f32_ws(const uint16_t* a, int64_t M, int32_t K, const uint16_t* w,
+                                     int32_t N, const float* resid, float* out, float* ws,
+                                     int64_t ws_bytes, daop_stream_t stream) {
+  if (M < 0 || M >= (1ll << 31) || K < 64 || K % GB_K != 0 || N < GB_N || N % GB_N != 0) {
+    set_error("dense GEMM: unsupported shape (M=%lld K=%d N=%d): needs K %% 64 == 0, "
+              "N %% 256 == 0", static_cast<long long>(M), K, N);
+    return DAOP_ERR_UNSUPPORTED;
+  }
+  if (M == 0) return DAOP_OK;
+  const int n_real = N / GB_N, kb = K / GB_K;
+  int ksplit = M <= P_M ? (sm_count() / 2) / n_real : 1;
+  if (ksplit > 8) ksplit = 8;
+  if (ksplit > kb / 4) ksplit = kb / 4;
+  if (ksplit < 2 || g_gemm_mode != 0 || !g_gemm_splitk || !ws ||
+      ws_bytes < static_cast<int64_t>(ksplit) * M * N * 4)
+    return daop_gemm_bf16_f32(a, M, K, w, N, resid, out, stream);
+  CUtensorMap ta, tb;
+  int rc;
+  const uint64_t adims[2] = {static_cast<uint64_t>(K), static_cast<uint64_t>(M)};
+  const uint64_t astr[1] = {static_cast<uint64_t>(K) * 2};
+  const uint32_t abox[2] = {GB_K, GB_M};
+  if ((rc = make_tmap_bf16(&ta, a, 2, adims, astr, abox))) return rc;
+  const uint64_t bdims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), 1};
+  const uint64_t bstr[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K) * N * 2};
+  const uint32_t bbox[3] = {GB_K, 128, 1};
+  if ((rc = make_tmap_bf16(&tb, w, 3, bdims, bstr, bbox))) return rc;
+  GemmParams p{nullptr, nullptr, 1, kb, n_real * ksplit, -16, GB_N, 128, ws, N,
+               GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0, 0, a, K, w, K,
+               static_cast<int64_t>(K) * N};
+  p.dense_rows = M;
+  p.ksplit = ksplit;
+  p.part_stride = M * static_cast<int64_t>(N);
+  apply_persisting_l2();
+  cudaStream_t st = as_stream(stream);
+  if ((rc = launch_pair<false, false>(ta, tb, p, M, st))) return rc;
+  const int64_t n4 = M * static_cast<int64_t>(N) / 4;
+  int64_t blocks = (n4 + 255) / 256;
+  if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
+  dense_splitk_reduce_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(
+      reinterpret_cast<const float4*>(ws), ksplit, p.part_stride / 4,
+      reinterpret_cast<const float4*>(resid), reinterpret_cast<float4*>(out), n4);
+  DAOP_CHECK_LAUNCH("dense_splitk_reduce");
+  return DAOP_OK;
 }
 
 // Down GEMM with the combine fused into its epilogue (single GPU prefill;

@@ -88,7 +88,7 @@ struct SkinnyCfg {
   // TWO CTAs share an SM -- its d / 128 row tiles per expert (256 at b = 64)
   // then fill one wave of 2 x 148 CTAs instead of leaving half a second wave
   static constexpr int CTAS_PER_SM = SWIGLU ? 1 : 2;
-  static constexpr int BUDGET = SWIGLU ? 200 * 1024 : 96 * 1024;
+  static constexpr int BUDGET = SWIGLU ? 200 * 1024 : 108 * 1024;
   static constexpr int STAGES = BUDGET / STAGE_BYTES < SkinnySmem<NT>::STAGES
                                     ? BUDGET / STAGE_BYTES : SkinnySmem<NT>::STAGES;
   static constexpr int ACC_COLS = SWIGLU ? 2 * NT : NT;  // per accumulator buffer
@@ -115,7 +115,7 @@ __device__ __forceinline__ bool skinny_tile(const SkinnySmem<NT>& s, int E, int 
 }
 
 template <bool SWIGLU, int NT>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, SkinnyCfg<SWIGLU, NT>::CTAS_PER_SM)
     skinny_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
                        const __grid_constant__ CUtensorMap tmX, SkinnyParams p) {
   using C = SkinnyCfg<SWIGLU, NT>;
@@ -240,24 +240,36 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t u[32];
           tmem_ld32(tb + NT + c, u);
           tmem_ld_wait();
-          uint16_t* out = static_cast<uint16_t*>(p.out);
+          const int nj = nvalid - c < 32 ? nvalid - c : 32;
+          uint16_t* o = static_cast<uint16_t*>(p.out) + (t0 + c) * p.out_ld + row;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c + j < nvalid)
-              out[(t0 + c + j) * p.out_ld + row] = f32_to_bf16_bits(
+          for (int j = 0; j < 32; ++j) {
+            if (j < nj)
+              *o = f32_to_bf16_bits(
                   __fdividef(__uint_as_float(g[j]), 1.0f + __expf(-__uint_as_float(g[j]))) *
                   __uint_as_float(u[j]));  // the prefill GEMM's SwiGLU (silu_fast)
+            o += p.out_ld;
+          }
         } else {
           tmem_ld_wait();
-          float* out = static_cast<float*>(p.out);
+          const int nj = nvalid - c < 32 ? nvalid - c : 32;
+          if (p.row_dst) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c + j < nvalid) {
-              float* dst = p.row_dst ? reinterpret_cast<float*>(p.row_dst[t0 + c + j]) + row
-                                     : out + (t0 + c + j) * p.out_ld + row;
-              const float v = __uint_as_float(g[j]);
-              *dst = p.resid ? v + p.resid[(t0 + c + j) * p.out_ld + row] : v;
+            for (int j = 0; j < 32; ++j)
+              if (j < nj) reinterpret_cast<float*>(p.row_dst[t0 + c + j])[row] = __uint_as_float(g[j]);
+          } else {
+            // one running pointer per stream (precomputed per-token addresses
+            // cost 2 x 32 registers and spilled for NT > 64)
+            const int64_t off = (t0 + c) * p.out_ld + row;
+            float* o = static_cast<float*>(p.out) + off;
+            const float* rr = p.resid ? p.resid + off : nullptr;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < nj) *o = rr ? __uint_as_float(g[j]) + *rr : __uint_as_float(g[j]);
+              o += p.out_ld;
+              if (rr) rr += p.out_ld;
             }
+          }
         }
       }
       tc_fence_before();
@@ -301,12 +313,21 @@ static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const Ski
   return DAOP_OK;
 }
 
+// token block NT = the MMA's N: any multiple of 16 works for M = 128; these
+// cover decode batches (32), prompts of ~100-400 tokens per layer (48..128:
+// the caller sizes NT to the expected rows per expert so one block holds an
+// expert's tokens without streaming mostly-empty token rows)
 template <bool SWIGLU>
 static int skinny_dispatch(const CUtensorMap& tw, const CUtensorMap& tx, const SkinnyParams& p,
                            int64_t rows, int32_t nt, cudaStream_t st) {
-  if (nt == 32) return launch_skinny<SWIGLU, 32>(tw, tx, p, rows, st);
-  if (nt == 128) return launch_skinny<SWIGLU, 128>(tw, tx, p, rows, st);
-  return launch_skinny<SWIGLU, 64>(tw, tx, p, rows, st);
+  switch (nt) {
+    case 32: return launch_skinny<SWIGLU, 32>(tw, tx, p, rows, st);
+    case 48: return launch_skinny<SWIGLU, 48>(tw, tx, p, rows, st);
+    case 80: return launch_skinny<SWIGLU, 80>(tw, tx, p, rows, st);
+    case 96: return launch_skinny<SWIGLU, 96>(tw, tx, p, rows, st);
+    case 128: return launch_skinny<SWIGLU, 128>(tw, tx, p, rows, st);
+    default: return launch_skinny<SWIGLU, 64>(tw, tx, p, rows, st);
+  }
 }
 
 }  // namespace daop
@@ -315,7 +336,8 @@ using namespace daop;
 
 static int check_skinny(int64_t rows, int32_t d, int32_t ffn, int32_t E, int32_t nt) {
   if (E < 1 || E > SK_MAX_E || d % 128 != 0 || ffn % 128 != 0 || d % 64 != 0 ||
-      (nt != 32 && nt != 64 && nt != 128) || rows < 0 || rows >= (1ll << 31)) {
+      (nt != 32 && nt != 48 && nt != 64 && nt != 80 && nt != 96 && nt != 128) || rows < 0 ||
+      rows >= (1ll << 31)) {
     set_error("skinny expert GEMM: unsupported shape (rows=%lld d=%d ffn=%d E=%d nt=%d)",
               static_cast<long long>(rows), d, ffn, E, nt);
     return DAOP_ERR_UNSUPPORTED;

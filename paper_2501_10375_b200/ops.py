@@ -110,17 +110,39 @@ def permute(topk_idx, num_experts, x=None):
     return {"offsets": offsets, "perm": perm, "inv": inv.view(t, k), "x_perm": x_perm}
 
 
-def gemm_bf16_f32(a, w, resid=None, out=None):
+SPLITK_MAX = 8
+
+
+def splitk_parts(m: int, k: int, n: int) -> int:
+    """The K split daop_gemm_bf16_f32_ws uses for an (m, k) x (n, k)^T product
+    (1 = none): the idle SM pairs over the n / 256 tiles of a <= 256-row M."""
+    if m > 256:
+        return 1
+    pairs = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count // 2
+    return max(1, min(SPLITK_MAX, pairs // (n // 256), (k // 64) // 4))
+
+
+def gemm_bf16_f32(a, w, resid=None, out=None, ws=None):
     """out (M, N) fp32 = a (M, K) bf16 . w (N, K)^T [+ resid (M, N) fp32] on the
-    tcgen05 GEMM pipeline (daop_gemm_bf16_f32); N % 256 == 0, K % 64 == 0."""
+    tcgen05 GEMM pipeline (daop_gemm_bf16_f32); N % 256 == 0, K % 64 == 0.
+    ws: fp32 workspace for the split-K path of prompt-sized M
+    (daop_gemm_bf16_f32_ws; True = allocate splitk_parts x M x N)."""
     _dev(a, w, resid, out)
     m, k = a.shape
     n = w.shape[0]
     if w.shape[1] != k or (resid is not None and tuple(resid.shape) != (m, n)):
         raise ShapeMismatchError(f"gemm: a {tuple(a.shape)}, w {tuple(w.shape)}")
     out = torch.empty((m, n), dtype=torch.float32, device=a.device) if out is None else out
-    _lib.call("daop_gemm_bf16_f32", a.data_ptr(), m, k, w.data_ptr(), n, _p(resid),
-              out.data_ptr(), _s())
+    if ws is None:
+        _lib.call("daop_gemm_bf16_f32", a.data_ptr(), m, k, w.data_ptr(), n, _p(resid),
+                  out.data_ptr(), _s())
+        return out
+    if ws is True:
+        ws = torch.empty(max(1, splitk_parts(m, k, n)) * m * n, dtype=torch.float32,
+                         device=a.device)
+    _dev(ws)
+    _lib.call("daop_gemm_bf16_f32_ws", a.data_ptr(), m, k, w.data_ptr(), n, _p(resid),
+              out.data_ptr(), ws.data_ptr(), ws.numel() * 4, _s())
     return out
 
 
@@ -157,11 +179,19 @@ def expert_gemm_up_gather(x, perm, k, offsets, slot_of, slab, n_slots, slot_elem
     return act
 
 
-def skinny_nt(rows: int) -> int:
-    """Token block of the skinny GEMMs for `rows` permuted rows (T * k):
-    prompts (> 384 rows, ~48+ per expert) take 128-token blocks so an expert's
-    weight tile is multiplied by all its tokens at once."""
-    return 32 if rows <= 32 else 64 if rows <= SKINNY_NT128_ROWS else 128
+SKINNY_NTS = (32, 48, 64, 80, 96, 128)
+
+
+def skinny_nt(rows: int, experts: int = 0) -> int:
+    """Token block (the MMA's N) of the skinny GEMMs for `rows` permuted rows
+    (T * k) over `experts` experts: the smallest instantiated block holding
+    1.25x the mean rows per expert, so one block usually covers an expert's
+    tokens and the stages stream few empty token rows (256-token prompt:
+    64 rows per expert -> 80).  experts = 0: by rows alone (32 / 64 / 128)."""
+    if experts <= 0:
+        return 32 if rows <= 32 else 64 if rows <= SKINNY_NT128_ROWS else 128
+    want = -(-5 * rows // (4 * experts))
+    return next((nt for nt in SKINNY_NTS if nt >= want), 128)
 
 
 SKINNY_NT128_ROWS = 384
@@ -177,7 +207,7 @@ def expert_gemm_up_skinny(x_perm, offsets, slot_of, slab, n_slots, slot_elems, d
         else out
     _lib.call("daop_expert_gemm_up_skinny", x_perm.data_ptr(), rows, d, ffn, slab.data_ptr(),
               n_slots, slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
-              act.data_ptr(), nt or skinny_nt(rows), _s())
+              act.data_ptr(), nt or skinny_nt(rows, offsets.numel() - 1), _s())
     return act
 
 
@@ -188,7 +218,7 @@ def expert_gemm_down_skinny(act, offsets, slot_of, slab, n_slots, slot_elems, d,
     y = torch.empty((rows, d), dtype=torch.float32, device=act.device) if out is None else out
     _lib.call("daop_expert_gemm_down_skinny", act.data_ptr(), rows, d, ffn, slab.data_ptr(),
               n_slots, slot_elems, offsets.data_ptr(), slot_of.data_ptr(), offsets.numel() - 1,
-              y.data_ptr(), nt or skinny_nt(rows), _s())
+              y.data_ptr(), nt or skinny_nt(rows, offsets.numel() - 1), _s())
     return y
 
 

@@ -43,7 +43,7 @@ act = t("up_skinny", lambda: ops.expert_gemm_up_skinny(pr["x_perm"], pr["offsets
 y = t("down_skinny", lambda: ops.expert_gemm_down_skinny(act, pr["offsets"], so, m.slab,
                                                           m.n_slots, m.slot_elems, d, ffn))
 t("combine", lambda: ops.combine(h, y, pr["inv"], r["topk_w"]))
-for nt in (64, 128):
+for nt in (32, 48, 64, 80, 96, 128):
     t(f"up_skinny_nt{nt}", lambda: ops.expert_gemm_up_skinny(pr["x_perm"], pr["offsets"], so, m.slab,
                                                               m.n_slots, m.slot_elems, d, ffn, nt))
     t(f"down_skinny_nt{nt}", lambda: ops.expert_gemm_down_skinny(act, pr["offsets"], so, m.slab,
@@ -67,4 +67,6 @@ t("attn_core", lambda: _lib.call("daop_attn_prefill", qkv.data_ptr(), T, 0, att.
                                  att.v_cache[0].data_ptr(), 32, 8, att.max_seq, float(att.theta),
                                  o.data_ptr(), ops._s()))
 t("attn_o_gemm", lambda: ops.gemm_bf16_f32(o, att.wo[0], resid=h))
+t("attn_qkv_gemm_splitk", lambda: ops.gemm_bf16_f32(xa, att.wqkv[0], ws=True))
+t("attn_o_gemm_splitk", lambda: ops.gemm_bf16_f32(o, att.wo[0], resid=h, ws=True))
 print({k: v for k, v in res.items() if k.startswith("attn")})

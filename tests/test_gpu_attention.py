@@ -177,3 +177,30 @@ def test_decode_token_with_attention_l2_prefetch_is_bit_identical(P):
         outs.append(h)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("M,K,N,resid", [(256, 4096, 6144, False), (256, 4096, 4096, True),
+                                         (100, 1024, 512, True), (37, 4096, 256, False),
+                                         (300, 1024, 512, True)])  # > 256 rows: no split
+def test_dense_gemm_splitk_parity(P, M, K, N, resid):
+    """daop_gemm_bf16_f32_ws (split-K over idle SM pairs + fixed-order
+    reduction) vs a float64 product; deterministic, and in place on resid."""
+    pkg, A = P
+    ops = A.ops
+    g = torch.Generator(device="cuda").manual_seed(3 * M + K + N)
+    a = torch.randn((M, K), generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.rand((N, K), generator=g, device="cuda") - 0.5).to(torch.bfloat16)
+    r = torch.randn((M, N), generator=g, device="cuda") if resid else None
+    parts = ops.splitk_parts(M, K, N)
+    assert (parts > 1) == (M <= 256 and N // 256 <= 37)
+    out = ops.gemm_bf16_f32(a, w, resid=r, ws=True)
+    again = ops.gemm_bf16_f32(a, w, resid=r, ws=True)
+    assert torch.equal(out, again)
+    ref = a.double().cpu().numpy() @ w.double().cpu().numpy().T
+    if resid:
+        ref = ref + r.double().cpu().numpy()
+        r2 = r.clone()
+        ops.gemm_bf16_f32(a, w, resid=r2, out=r2, ws=True)
+        assert torch.equal(r2, out)
+    torch.cuda.synchronize()
+    close(out.cpu().numpy(), ref, f"split-K gemm {M}x{K}x{N}")
