@@ -20,6 +20,8 @@
 //              epilogue.
 // Tiles are (expert, m-tile, n-tile), rasterised in groups of G m-tiles so
 // the weight tile is shared in L2 by the CTAs working on the same group.
+#include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -108,6 +110,11 @@ struct GemmParams {
   // 1.9 GB act / 1.1 GB y output streams do not push the re-read A / B
   // operand tiles out of L2 (tuning bit, daop_set_gemm_mode bit 14)
   int store_cs;
+  // diagnostic bits (daop_set_gemm_mode bits 20..22; results are WRONG with
+  // any set): 1 epilogue skips TMEM -> global, 2 producer skips the TMA loads
+  // (MMAs on stale smem), 4 producer reloads 4 L2-hot k-blocks of one tile.
+  // They split a GEMM's time into MMA / operand feed / epilogue.
+  int exp;
 };
 
 __device__ __forceinline__ int64_t off_at(const GemmParams& p, int e) {
@@ -548,27 +555,40 @@ __device__ __forceinline__ void split_tile(const GemmParams& p, int n_eff, int& 
   kb1 = (ks + 1) * p.k_blocks / p.ksplit;
 }
 
-template <bool SWIGLU, bool TWO_M = false, int EW = 8>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::THREADS, 1)
+// QUAD (TWO_M only; tuning, off): a 4-CTA cluster = two CTA pairs on the same
+// 512-row m-tile and neighbouring n-tiles (pair q takes n = 2 j + q).  Each A
+// box is loaded once and multicast to the matching CTA of both pairs, so a CTA
+// requests 16 KB of A + 16 KB of B per stage instead of 32 + 16 (L2 reads
+// -33 %).  A stage is refilled only after BOTH pairs' MMAs released it.
+// Measured: no gain -- only 33 four-CTA clusters fit the GPCs (132 SMs), and
+// with L2-hot operands the per-SM feed is as slow as without multicast (the
+// limit is the SM's ingress, ~36 B/clk, not L2 output).
+template <bool SWIGLU, bool TWO_M = false, int EW = 8, bool QUAD = false>
+__global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::THREADS, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  static_assert(!QUAD || TWO_M, "QUAD multicast needs the 512-row pair tile");
   using C = PairCfg<TWO_M, EW>;
+  constexpr int CL = QUAD ? 4 : 2;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
   PairSmem& s = *reinterpret_cast<PairSmem*>(tiles + C::STAGES * C::STAGE_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1;            // rank within the CTA pair
+  const int pairq = static_cast<int>(crank >> 1);  // QUAD: which pair of the cluster
+  const uint32_t lead_cta = crank & ~1u;      // this pair's leader CTA
   const bool leader = rank == 0;
   const int E = p.E;
-  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int cluster = blockIdx.x / CL, nclusters = gridDim.x / CL;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&s.full[i], 2);   // leader: own expect_tx arrive + follower's remote arrive
-      mbar_init(&s.empty[i], 1);  // multicast commit
+      mbar_init(&s.empty[i], QUAD ? 2 : 1);  // multicast commit (QUAD: from both pairs)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s.tfull[i], 1);   // multicast commit
@@ -581,7 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
     for (int e = 0; e < E; ++e) {
       const int64_t me = slot_at(p, e) >= 0 ? s.off[e + 1] - s.off[e] : 0;
       s.mt[e] = static_cast<int>((me + C::M - 1) / C::M);
-      acc += s.mt[e] * p.n_tiles;
+      acc += s.mt[e] * (QUAD ? p.n_tiles / 2 : p.n_tiles);
       s.prefix[e + 1] = acc;
     }
   }
@@ -590,7 +610,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = s.tmem_base;
-  const int nt = p.n_tiles, G = p.group_m;
+  const int nt = QUAD ? p.n_tiles / 2 : p.n_tiles, G = p.group_m;
 
   if (warp == 0) {
     if (p.a_perm || lane == 0) {  // TMA producer (both CTAs; all lanes when gathering A)
@@ -615,6 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
       uint32_t phase = 0;
       int e, m, n;
       for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+        if (QUAD) n = 2 * n + pairq;
         int ks, kb0, kb1;
         split_tile(p, n, n, ks, kb0, kb1);
         const int row0 = static_cast<int>(s.off[e] + static_cast<int64_t>(m) * C::M) + rank * 128;
@@ -638,9 +659,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
           if (lane == 0) mbar_wait(&s.empty[stage], phase ^ 1);
           if (p.a_perm) __syncwarp();  // (dense A: lane 0 runs this loop alone)
           uint8_t* st = tiles + stage * C::STAGE_BYTES;
+          if (p.exp & 2) {
+            if (lane == 0) {
+              if (leader) mbar_arrive(&s.full[stage]);
+              else mbar_arrive_cluster(&s.full[stage], lead_cta);
+            }
+            if (++stage == C::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (lane == 0) {
             if (leader) mbar_arrive_expect_tx(&s.full[stage], 2 * C::STAGE_BYTES);
-            else mbar_arrive_cluster(&s.full[stage], 0);
+            else mbar_arrive_cluster(&s.full[stage], lead_cta);
           }
           if (p.a_perm) {
             __syncwarp();  // the expect_tx precedes every lane's gather
@@ -650,12 +682,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
               tma_gather4_pair(st + P_A_BYTES + lane * 4 * GB_K * 2, &tmA, &s.full[stage],
                                kb * GB_K, gi[1][0], gi[1][1], gi[1][2], gi[1][3], pol_a);
           } else if (lane == 0) {
-            tma_load_2d_pair(st, &tmA, &s.full[stage], kb * GB_K, row0, pol_a);
-            if constexpr (TWO_M)  // second M=256 half: tile rows 256 + rank * 128
-              tma_load_2d_pair(st + P_A_BYTES, &tmA, &s.full[stage], kb * GB_K, row0 + 256, pol_a);
+            const int kx = (p.exp & 4) ? (kb & 3) * GB_K : kb * GB_K;  // EXPERIMENT: L2-hot operands
+            const int ra = (p.exp & 4) ? rank * 128 : row0;
+            if constexpr (QUAD) {  // box `pairq` for this CTA and its twin in the other pair
+              tma_load_2d_pair_mc(st + pairq * P_A_BYTES, &tmA, &s.full[stage], kx,
+                                  ra + pairq * 256, static_cast<uint16_t>(0x5u << rank), pol_a);
+            } else {
+              tma_load_2d_pair(st, &tmA, &s.full[stage], kx, ra, pol_a);
+              if constexpr (TWO_M)  // second M=256 half: tile rows 256 + rank * 128
+                tma_load_2d_pair(st + P_A_BYTES, &tmA, &s.full[stage], kx, ra + 256, pol_a);
+            }
           }
           if (lane == 0)
-            tma_load_3d_pair(st + C::A_BYTES, &tmB, &s.full[stage], kb * GB_K, brow, slot, pol_b);
+            tma_load_3d_pair(st + C::A_BYTES, &tmB, &s.full[stage], (p.exp & 4) ? (kb & 3) * GB_K : kb * GB_K,
+                             (p.exp & 4) ? (leader ? 0 : p.b_half2) : brow, slot, pol_b);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -670,6 +710,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
       uint32_t phase = 0, acc_phase = 0;
       int e, m, n;
       for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+        if (QUAD) n = 2 * n + pairq;
         int ks, kb0, kb1;
         split_tile(p, n, n, ks, kb0, kb1);
         mbar_wait(&s.tempty[acc], acc_phase ^ 1);
@@ -690,13 +731,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
                              ((kb - kb0) | k) != 0);
             }
           }
-          umma_commit_pair(&s.empty[stage], 0x3);
+          umma_commit_pair(&s.empty[stage], QUAD ? 0xF : 0x3);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(&s.tfull[acc], 0x3);
+        umma_commit_pair(&s.tfull[acc], static_cast<uint16_t>(0x3u << (2 * pairq)));
         ++iters;
         if (++acc == C::NACC) {
           acc = 0;
@@ -719,6 +760,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
     uint32_t acc_phase = 0;
     int e, m, n;
     for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+      if (QUAD) n = 2 * n + pairq;
       int ks, kb0, kb1;
       split_tile(p, n, n, ks, kb0, kb1);
       mbar_wait(&s.tfull[acc], acc_phase);
@@ -729,15 +771,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
       const int sub = TWO_M ? grp % C::GROUPS_PER_HALF : 0;   // its share of the half's columns
       {
       const int row_in_tile = half * 256 + rank * 128 + q * 32 + lane;
-      const bool valid = static_cast<int64_t>(m) * C::M + row_in_tile < me;
+      const bool valid = static_cast<int64_t>(m) * C::M + row_in_tile < me && !(p.exp & 1);
       const int64_t grow = s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile;
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * GB_N +
                           half * GB_N;
       if constexpr (SWIGLU) {
         uint16_t* out = static_cast<uint16_t*>(p.out) + grow * p.out_ld + n * 128;
 #pragma unroll 1
-        for (int c = sub * (128 / C::GROUPS_PER_HALF); c < (sub + 1) * (128 / C::GROUPS_PER_HALF);
-             c += 32) {
+        for (int c = sub * (128 / C::GROUPS_PER_HALF);
+             c < (sub + 1) * (128 / C::GROUPS_PER_HALF) && !(p.exp & 1); c += 32) {
           uint32_t g[32], u[32];
           tmem_ld32(tb + c, g);
           tmem_ld32(tb + 128 + c, u);
@@ -769,8 +811,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
                                      grow * p.out_ld + n * GB_N;
         const float* resid = p.ksplit > 1 ? nullptr : p.resid;
 #pragma unroll 1
-        for (int c = sub * (GB_N / C::GROUPS_PER_HALF); c < (sub + 1) * (GB_N / C::GROUPS_PER_HALF);
-             c += 32) {
+        for (int c = sub * (GB_N / C::GROUPS_PER_HALF);
+             c < (sub + 1) * (GB_N / C::GROUPS_PER_HALF) && !(p.exp & 1); c += 32) {
           uint32_t v[32];
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
@@ -782,7 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&s.tempty[acc], 0);
+      if (lane == 0) mbar_arrive_cluster(&s.tempty[acc], lead_cta);
       if constexpr (!SWIGLU) {
         if (p.comb_cnt) {  // accumulator released: the combine runs off the MMA's path
           const int row_in_tile = half * 256 + rank * 128 + q * 32 + lane;
@@ -834,34 +876,65 @@ static int g_gemm_store_cs = 0;  // epilogue streaming stores (tuning)
 static int g_gemm_dense_skinny = 1;  // tuning: small-M dense GEMMs on the skinny kernel
 static int g_gemm_epi16 = 0;  // tuning: 16 epilogue warps for the 512-row pair tile
 static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
-static int g_gemm_splitk = 1;  // tuning: split-K for prompt-sized dense projections (_ws entry)
+static int g_gemm_splitk = 1;
+static int g_gemm_exp = 0;  // EXPERIMENT bits (GemmParams::exp)
+static int g_gemm_quad = 0;  // tuning: 4-CTA multicast clusters for the 512-row pair tile (mode bit 18)  // tuning: split-K for prompt-sized dense projections (_ws entry)
 
 template <bool TWO_M>
 static size_t pair_smem_bytes() {
   return 1024 + PairCfg<TWO_M>::STAGES * PairCfg<TWO_M>::STAGE_BYTES + sizeof(PairSmem);
 }
 
-template <bool SWIGLU, bool TWO_M, int EW>
+template <bool SWIGLU, bool TWO_M, int EW, bool QUAD = false>
 static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                           int64_t rows_total, cudaStream_t st) {
   using C = PairCfg<TWO_M, EW>;
+  constexpr int CL = QUAD ? 4 : 2;
   const size_t smem = pair_smem_bytes<TWO_M>();
-  auto kern = grouped_gemm_pair_kernel<SWIGLU, TWO_M, EW>;
+  auto kern = grouped_gemm_pair_kernel<SWIGLU, TWO_M, EW, QUAD>;
   DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-  const int64_t max_tiles = (rows_total / C::M + p.E) * static_cast<int64_t>(p.n_tiles);
-  int clusters = sm_count() / 2;
+  const int64_t max_tiles =
+      (rows_total / C::M + p.E) * static_cast<int64_t>(QUAD ? p.n_tiles / 2 : p.n_tiles);
+  int clusters = sm_count() / CL;
+  if (QUAD) {
+    // 4-CTA clusters must fit inside a GPC: launch only the co-resident ones
+    // (a persistent grid with a second wave of clusters doubles the tail)
+    static int max_active = 0;
+    if (!max_active) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CL * clusters);
+      cfg.blockDim = dim3(C::THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = CL;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+        (void)cudaGetLastError();
+        n = clusters;
+      }
+      max_active = n;
+      if (getenv("DAOP_GEMM_VERBOSE")) fprintf(stderr, "quad gemm: %d co-resident 4-CTA clusters\n", n);
+    }
+    if (max_active < clusters) clusters = max_active;
+  }
   if (max_tiles < clusters) clusters = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
   GemmParams pp = p;
   pp.store_cs = g_gemm_store_cs;
+  pp.exp = g_gemm_exp;
   if (p.group_m < 0) {  // negative group = n-grouped raster of |group| weight tiles
     pp.raster = 1;
-    pp.group_m = -p.group_m;
+    pp.group_m = QUAD ? (-p.group_m > 1 ? -p.group_m / 2 : 1) : -p.group_m;  // (QUAD: n-pairs)
   } else {              // group counted in 128-row units -> pair tiles of C::M rows
     pp.raster = 0;
     pp.group_m = p.group_m > C::M / 128 ? p.group_m / (C::M / 128) : 1;
   }
-  kern<<<2 * clusters, C::THREADS, smem, st>>>(ta, tb, pp);
+  kern<<<CL * clusters, C::THREADS, smem, st>>>(ta, tb, pp);
   DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
   return DAOP_OK;
 }
@@ -869,7 +942,16 @@ static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
 template <bool SWIGLU, bool TWO_M>
 static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                        int64_t rows_total, cudaStream_t st) {
-  if (TWO_M && g_gemm_epi16) return launch_pair_ew<SWIGLU, TWO_M, 16>(ta, tb, p, rows_total, st);
+  if constexpr (TWO_M) {
+    // 4-CTA clusters with A multicast across two pairs (plain prefill GEMMs)
+    const bool quad = g_gemm_quad && p.n_tiles % 2 == 0 && !p.a_perm && !p.row_dst &&
+                      !p.comb_cnt && p.ksplit <= 1;
+    if (quad) {
+      if (g_gemm_epi16) return launch_pair_ew<SWIGLU, TWO_M, 16, true>(ta, tb, p, rows_total, st);
+      return launch_pair_ew<SWIGLU, TWO_M, 8, true>(ta, tb, p, rows_total, st);
+    }
+    if (g_gemm_epi16) return launch_pair_ew<SWIGLU, TWO_M, 16>(ta, tb, p, rows_total, st);
+  }
   return launch_pair_ew<SWIGLU, TWO_M, 8>(ta, tb, p, rows_total, st);
 }
 
@@ -960,6 +1042,8 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_dense_skinny = !((mode >> 15) & 1);
   g_gemm_epi16 = (mode >> 16) & 1;
   g_gemm_splitk = !((mode >> 17) & 1);
+  g_gemm_exp = (mode >> 20) & 7;
+  g_gemm_quad = (mode >> 18) & 1;
   return DAOP_OK;
 }
 

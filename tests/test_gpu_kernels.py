@@ -238,8 +238,9 @@ def _gemm_case(P, d, ffn, E, T, k, seed=0):
     return m, om, h, r, pr, act, y, out
 
 
-# 512-row pair tiles, single CTA, 256-row pair tiles, 512-row tiles with 16 epilogue warps
-@pytest.mark.parametrize("mode", [0, 1, 0x3000, 0x10000])
+# 512-row pair tiles, single CTA, 256-row pair tiles, 512-row tiles with 16
+# epilogue warps, 4-CTA clusters with A multicast (QUAD, tuning)
+@pytest.mark.parametrize("mode", [0, 1, 0x3000, 0x10000, 1 << 18])
 @pytest.mark.parametrize("d,ffn,E,T", [(256, 512, 8, 64), (512, 1024, 8, 700), (4096, 14336, 8, 256)])
 def test_grouped_gemm_parity(P, d, ffn, E, T, mode):
     P[2].set_gemm_mode(mode)
@@ -370,9 +371,10 @@ def test_decode_and_router_nan_input_selects_valid_ids(P):
 @pytest.mark.parametrize("d,ffn,E,T", [(512, 1024, 8, 700), (1024, 2048, 8, 3000)])
 def test_grouped_gemm_two_m_bitexact(P, d, ffn, E, T):
     """The 512-row pair tile (two M=256 MMAs sharing B) accumulates every
-    output element in the same K order as the 256-row tile: bit-identical."""
+    output element in the same K order as the 256-row tile: bit-identical;
+    so do the 16-epilogue-warp and the 4-CTA multicast (QUAD) variants."""
     outs = []
-    for mode in (0, 0x3000, 0x10000):
+    for mode in (0, 0x3000, 0x10000, 1 << 18):
         P[2].set_gemm_mode(mode)
         try:
             _, _, _, _, pr, act, y, out = _gemm_case(P, d, ffn, E, T, 2)
