@@ -320,15 +320,38 @@ __global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
     const int hh = t / (AT_HD / 2), c = t - hh * (AT_HD / 2);
     const float* base = a.part + (static_cast<int64_t>(g) * a.splits * group + hh) * (2 + AT_HD);
     const int64_t stride = static_cast<int64_t>(group) * (2 + AT_HD);
+    // the partials are read in batches of 8 splits with every load of a batch
+    // issued before the first use (one L2 round trip per batch, not per split)
+    constexpr int MB = 8;
     float m = -INFINITY;
-    for (int s2 = 0; s2 < used; ++s2) m = fmaxf(m, __ldcg(base + s2 * stride));
+    for (int s0 = 0; s0 < used; s0 += MB) {
+      float mv[MB];
+#pragma unroll
+      for (int j = 0; j < MB; ++j) mv[j] = s0 + j < used ? __ldcg(base + (s0 + j) * stride) : -INFINITY;
+#pragma unroll
+      for (int j = 0; j < MB; ++j) m = fmaxf(m, mv[j]);
+    }
     float l = 0.f, o0 = 0.f, o1 = 0.f;
-    for (int s2 = 0; s2 < used; ++s2) {
-      const float* pr = base + s2 * stride;
-      const float cf = expf(__ldcg(pr) - m);
-      l = fmaf(__ldcg(pr + 1), cf, l);
-      o0 = fmaf(__ldcg(pr + 2 + 2 * c), cf, o0);
-      o1 = fmaf(__ldcg(pr + 3 + 2 * c), cf, o1);
+    for (int s0 = 0; s0 < used; s0 += MB) {
+      float mv[MB], lv[MB], a0[MB], a1[MB];
+#pragma unroll
+      for (int j = 0; j < MB; ++j) {
+        const bool ok = s0 + j < used;
+        const float* pr = base + (s0 + j) * stride;
+        mv[j] = ok ? __ldcg(pr) : -INFINITY;
+        lv[j] = ok ? __ldcg(pr + 1) : 0.f;
+        a0[j] = ok ? __ldcg(pr + 2 + 2 * c) : 0.f;
+        a1[j] = ok ? __ldcg(pr + 3 + 2 * c) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < MB; ++j) {  // fixed split order, as before
+        if (s0 + j < used) {
+          const float cf = expf(mv[j] - m);
+          l = fmaf(lv[j], cf, l);
+          o0 = fmaf(a0[j], cf, o0);
+          o1 = fmaf(a1[j], cf, o1);
+        }
+      }
     }
     const int head = g * group + hh;
     a.o[head * AT_HD + 2 * c] = f32_to_bf16_bits(o0 / l);
