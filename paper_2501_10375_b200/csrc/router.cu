@@ -850,8 +850,26 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) router_small_kernel(Route
   __shared__ float part[kSmallWarps][kMaxGateRows];
   const float* hrow = a.h + t * d;
   const int n8 = d / 8;  // 8-element chunks, thread-strided
-  double ss = 0.0;
-  for (int c = tid; c < n8; c += blockDim.x) {
+  auto gate_chunk = [&](int q, int c) {
+    const uint16_t* grow = q < E ? a.wg + static_cast<size_t>(q) * d
+                                 : a.wg_next + static_cast<size_t>(q - E) * d;
+    return ldg_nc_v4(reinterpret_cast<const uint4*>(grow) + c);
+  };
+  // the thread's first chunk of h, gamma and the first 16 gate rows are all
+  // requested up front: their L2 round trip overlaps the RMS reduction
+  const bool has0 = tid < n8;
+  float4 u0 = make_float4(0.f, 0.f, 0.f, 0.f), v0 = u0;
+  uint4 gm0 = make_uint4(0, 0, 0, 0);
+  uint4 gv0[16];
+  if (has0) {
+    u0 = reinterpret_cast<const float4*>(hrow)[2 * tid];
+    v0 = reinterpret_cast<const float4*>(hrow)[2 * tid + 1];
+    gm0 = reinterpret_cast<const uint4*>(a.gamma)[tid];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) gv0[i] = has0 && i < rows ? gate_chunk(i, tid) : make_uint4(0, 0, 0, 0);
+  double ss = has0 ? sq_acc4(v0, sq_acc4(u0, 0.0)) : 0.0;
+  for (int c = tid + blockDim.x; c < n8; c += blockDim.x) {
     const float4 u = reinterpret_cast<const float4*>(hrow)[2 * c];
     const float4 v = reinterpret_cast<const float4*>(hrow)[2 * c + 1];
     ss = sq_acc4(v, sq_acc4(u, ss));
@@ -865,10 +883,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) router_small_kernel(Route
   float acc[kMaxGateRows];
 #pragma unroll
   for (int q = 0; q < kMaxGateRows; ++q) acc[q] = 0.f;
-  for (int c = tid; c < n8; c += blockDim.x) {
-    const float4 u = reinterpret_cast<const float4*>(hrow)[2 * c];
-    const float4 v = reinterpret_cast<const float4*>(hrow)[2 * c + 1];
-    const uint4 gm = reinterpret_cast<const uint4*>(a.gamma)[c];
+  auto x_of = [&](int c, float4 u, float4 v, uint4 gm) {
     const float hv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
     const uint32_t gw[4] = {gm.x, gm.y, gm.z, gm.w};
     uint32_t xw[4];
@@ -881,13 +896,37 @@ __global__ void __launch_bounds__(kSmallWarps * 32, 1) router_small_kernel(Route
     }
     const uint4 x8 = make_uint4(xw[0], xw[1], xw[2], xw[3]);
     if (a.x_out) reinterpret_cast<uint4*>(a.x_out + t * d)[c] = x8;
+    return x8;
+  };
+  // rows 16..31 (E = 16 with the next-layer gate) of one chunk, batched
+  auto rows_hi = [&](int c, uint4 x8) {
+    if (rows > 16) {
+      uint4 gv[16];
 #pragma unroll
-    for (int q = 0; q < kMaxGateRows; ++q)
-      if (q < rows) {
-        const uint16_t* grow = q < E ? a.wg + static_cast<size_t>(q) * d
-                                     : a.wg_next + static_cast<size_t>(q - E) * d;
-        acc[q] = dot8(x8, reinterpret_cast<const uint4*>(grow)[c], acc[q]);
-      }
+      for (int i = 0; i < 16; ++i) gv[i] = 16 + i < rows ? gate_chunk(16 + i, c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (16 + i < rows) acc[16 + i] = dot8(x8, gv[i], acc[16 + i]);
+    }
+  };
+  if (has0) {
+    const uint4 x8 = x_of(tid, u0, v0, gm0);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < rows) acc[i] = dot8(x8, gv0[i], acc[i]);
+    rows_hi(tid, x8);
+  }
+  for (int c = tid + blockDim.x; c < n8; c += blockDim.x) {
+    const uint4 x8 = x_of(c, reinterpret_cast<const float4*>(hrow)[2 * c],
+                          reinterpret_cast<const float4*>(hrow)[2 * c + 1],
+                          reinterpret_cast<const uint4*>(a.gamma)[c]);
+    uint4 gv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) gv[i] = i < rows ? gate_chunk(i, c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < rows) acc[i] = dot8(x8, gv[i], acc[i]);
+    rows_hi(c, x8);
   }
 #pragma unroll
   for (int q = 0; q < kMaxGateRows; ++q)
@@ -952,13 +991,16 @@ using namespace daop;
 static int g_router_single_pass = 1;
 static int g_router_prefetch = 1;
 static int g_router_tma = 1;
+static int g_router_small_bulk = 0;  // tuning: bulk router also for 8 <= T <= 128
 
-// bit 0: single pass; bit 2: bulk-copy router OFF; bits 4..7: + 1 = L2
+// bit 0: single pass; bit 2: bulk-copy router OFF; bit 3: bulk router for
+// 8 <= T <= 128 too (instead of a CTA per token); bits 4..7: + 1 = L2
 // prefetch distance of the single-pass kernel in grid-strides (0 in those
 // bits keeps the current distance)
 extern "C" int daop_set_router_mode(int32_t mode) {
   g_router_single_pass = mode & 1;
   g_router_tma = (mode & 4) ? 0 : 1;
+  g_router_small_bulk = (mode >> 3) & 1;
   if ((mode >> 4) & 15) g_router_prefetch = ((mode >> 4) & 15) - 1;
   return DAOP_OK;
 }
@@ -981,7 +1023,11 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
   RouterArgs a{h, gamma, wg, wg_next, T, d, E, k, eps, x_out, p_true, p_pred,
                topk_idx, topk_w, hist, tokens_per_seq, hist_seq_stride, g_router_prefetch};
   const int rows = wg_next ? 2 * E : E;
-  if (T <= 128 && d % 8 == 0) {  // decode-sized batch: a CTA per token
+  const int ks_small = d % (16 * kMmaWarps) == 0 ? d / (16 * kMmaWarps) : 0;
+  const bool tma_ok = rows <= 16 && E <= 8 && g_router_single_pass && g_router_tma &&
+                      (ks_small == 8 || ks_small == 16);
+  if (T <= 128 && d % 8 == 0 && !(g_router_small_bulk && tma_ok && T >= 8)) {
+    // decode-sized batch: a CTA per token
     router_small_kernel<<<static_cast<int>(T), kSmallWarps * 32, 0, as_stream(st)>>>(a);
     DAOP_CHECK_LAUNCH("router_small");
     return DAOP_OK;

@@ -454,7 +454,7 @@ class PeerEP:
         _lib.call("daop_ep_recv", self.peers.data_ptr(), self.rank, self.world, self.E, self.d,
                   self.yback_off, self.epoch, s)
         if self.cap_recv <= SKINNY_MAX_ROWS:  # batched decode: weights as the M side
-            nt = ops.skinny_nt(self.cap_recv)
+            nt = ops.skinny_nt(self.cap_recv, self.E)  # ~1.25x the mean rows per expert
             _lib.call("daop_expert_gemm_up_skinny", self.recv_x.data_ptr(), self.cap_recv, self.d,
                       self.ffn, m.slab.data_ptr(), m.n_slots, m.slot_elems,
                       self.ws.data_ptr() + self.local_off, m.slot_of[l].data_ptr(), self.E,
