@@ -22,6 +22,7 @@
 // the weight tile is shared in L2 by the CTAs working on the same group.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -955,6 +956,31 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
   return launch_pair_ew<SWIGLU, TWO_M, 8>(ta, tb, p, rows_total, st);
 }
 
+// Default rasterisation groups.  Up GEMM (m-grouped): the group's A rows
+// (group x 128 rows x d x 2 B) are re-read by every n-tile of the group and
+// must stay in L2: 8192 rows at d = 4096 (64 MB) but 4096 at d >= 5120 (the
+// 8x22B shape's 8192-row group is 100 MB and re-read A from DRAM: 30 GB per
+// launch).  Down GEMM (n-grouped): the group's W2 tiles (group x 256 rows x
+// ffn x 2 B) -- 16 tiles at ffn <= 14336, 8 above.  DAOP_GEMM_GROUPS="up,down"
+// overrides both (tuning).
+static int default_group_up(int d) {
+  static const int env = [] {
+    const char* v = getenv("DAOP_GEMM_GROUPS");
+    return v ? atoi(v) : 0;
+  }();
+  if (env) return env;
+  return d > 5120 ? 32 : 64;
+}
+static int default_group_down(int ffn) {
+  static const int env = [] {
+    const char* v = getenv("DAOP_GEMM_GROUPS");
+    const char* c = v ? strchr(v, ',') : nullptr;
+    return c ? atoi(c + 1) : 0;
+  }();
+  if (env) return env;
+  return (g_gemm_two_m & 2) ? (ffn > 14336 ? -8 : -16) : -8;
+}
+
 static void apply_persisting_l2() {
   {
     // L2::evict_last (the A operand, re-read by every n-tile of its group) is
@@ -1066,7 +1092,7 @@ extern "C" int daop_expert_gemm_up(const uint16_t* x_perm, int64_t rows, int32_t
                             static_cast<uint64_t>(slot_stride_elems) * 2};
   const uint32_t bbox[3] = {GB_K, 128, 1};
   if ((rc = make_tmap_bf16(&tb, slab, 3, bdims, bstr, bbox))) return rc;
-  GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : 64,
+  GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : default_group_up(d),
                128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0, 0,
                g_gemm_demote & 1, x_perm, d, slab, d, slot_stride_elems};
   return launch_gemm<true>(ta, tb, p, rows, as_stream(stream));
@@ -1101,7 +1127,7 @@ extern "C" int daop_expert_gemm_up_gather(const uint16_t* x, int64_t src_rows,
                             static_cast<uint64_t>(slot_stride_elems) * 2};
   const uint32_t bbox[3] = {GB_K, 128, 1};
   if ((rc = make_tmap_bf16(&tb, slab, 3, bdims, bstr, bbox))) return rc;
-  GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : 64,
+  GemmParams p{d_offsets, d_slot_of, E, d / GB_K, ffn / 128, group_m > 0 ? group_m : default_group_up(d),
                128, ffn, act, ffn, 128, g_gemm_policy >= 0 ? g_gemm_policy : 0, 0,
                g_gemm_demote & 1, x, d, slab, d, slot_stride_elems};
   p.a_perm = d_perm;
@@ -1132,7 +1158,7 @@ extern "C" int daop_expert_gemm_down(const uint16_t* act, int64_t rows, int32_t 
   if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
   // default: n-grouped raster, 16 weight n-tiles per group with the 512-row
   // tile (8 with the 256-row one); profiles/r01/gemm_two_m.txt, gemm_sweep.txt
-  const int grp = group_m != 0 ? group_m : ((g_gemm_two_m & 2) ? -16 : -8);
+  const int grp = group_m != 0 ? group_m : default_group_down(ffn);
   GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, grp,
                GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0,
                g_gemm_demote & 2, act, ffn, w2, ffn, slot_stride_elems};
@@ -1281,7 +1307,7 @@ extern "C" int daop_expert_gemm_down_combine(const uint16_t* act, int64_t rows, 
   const uint32_t bbox[3] = {GB_K, 128, 1};
   const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
   if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
-  const int grp = group_m != 0 ? group_m : ((g_gemm_two_m & 2) ? -16 : -8);
+  const int grp = group_m != 0 ? group_m : default_group_down(ffn);
   GemmParams p{d_offsets, d_slot_of, E, ffn / GB_K, d / GB_N, grp,
                GB_N, 128, y, d, GB_N, g_gemm_policy >= 0 ? g_gemm_policy : 2, 0,
                g_gemm_demote & 2, act, ffn, w2, ffn, slot_stride_elems};
@@ -1327,7 +1353,7 @@ extern "C" int daop_ep_expert_gemm_down(const uint16_t* act, int64_t rows_cap, i
   const uint16_t* w2 = slab + static_cast<int64_t>(2) * ffn * d;
   if ((rc = make_tmap_bf16(&tb, w2, 3, bdims, bstr, bbox))) return rc;
   GemmParams p{reinterpret_cast<const int64_t*>(ws + EP_LOCAL_OFF), d_slot_of, E, ffn / GB_K,
-               d / GB_N, group_m != 0 ? group_m : ((g_gemm_two_m & 2) ? -16 : -8), GB_N, 128,
+               d / GB_N, group_m != 0 ? group_m : default_group_down(ffn), GB_N, 128,
                nullptr, d, GB_N,
                g_gemm_policy >= 0 ? g_gemm_policy : 2, 0, g_gemm_demote & 2, act, ffn, w2, ffn,
                slot_stride_elems, reinterpret_cast<const uint64_t*>(ws + EP_ROWMAP),
