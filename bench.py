@@ -808,11 +808,17 @@ def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", tokens=None, hb
     else:
         def step(record=False):
             return gpu_ep_layer(m, 0, h, timings=phases if record else None)[:3]
+    if tokens is not None:
+        # batched decode right after the power-capped prefill GEMMs: let the
+        # clocks recover, then a longer warm-up and window (HBM-bound steps
+        # of ~1 ms are sensitive to the state the previous section left)
+        time.sleep(1.0)
+        warmup = max(warmup, 20)
     for _ in range(warmup):
         step()
     barrier()
     torch.cuda.synchronize()
-    kp = steps or (5 if tokens is None else 50)
+    kp = steps or (5 if tokens is None else 200)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index or 0) as clk:
@@ -889,6 +895,7 @@ def run_ep(args, world, rank, dev, tf_sus, barrier, impl="peer", tokens=None, hb
                          "peak": hbm_peak * world, "unit": "GB/s",
                          "frac": wbytes / (ms / 1e3) / 1e9 / (hbm_peak * world),
                          "bytes_per_step": wbytes, "note": "all 8 experts active at b=64"},
+            "clocks": clk.summary(),
         }
         if impl == "peer":
             ctx.close()
