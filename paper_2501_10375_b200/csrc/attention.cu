@@ -20,6 +20,8 @@
 //                        in smem), then warp-per-row GEMV over Wo (33.5 MB) + residual
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace daop {
@@ -114,6 +116,10 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   const uint4* g4 = reinterpret_cast<const uint4*>(gamma);
   const bool regs = n8 <= 2 * nt;
   const int c0 = tid, c1 = tid + nt;
+  // launched with programmatic stream serialization behind the previous
+  // layer's MoE kernel: the producer warp above already streams Wqkv; h is
+  // that kernel's output, read only after it completed (no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   float4 ha = make_float4(0.f, 0.f, 0.f, 0.f), hb = ha, hc = ha, hd = ha;
   uint4 ga = make_uint4(0u, 0u, 0u, 0u), gb = ga;
   if (regs && c0 < n8) { ha = h4[2 * c0]; hb = h4[2 * c0 + 1]; ga = g4[c0]; }
@@ -374,6 +380,7 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = blockIdx.x * rows_per_cta;
   const int n = max(0, min(d, r0 + rows_per_cta) - r0);
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   ring_init(R);
   __syncthreads();
   if (warp == AT_WARPS) {
@@ -904,8 +911,22 @@ extern "C" int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const
                         2 * stages * 8;
     DAOP_CUDA(cudaFuncSetAttribute(attn_qkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-    attn_qkv_kernel<<<sms, (AT_WARPS + 1) * 32, smem, st>>>(d_h, d_gamma, d_wqkv, d, rows, rpc,
-                                                            stages, eps, d_xa_out, qkv);
+    static const int pdl = [] {
+      const char* v = getenv("DAOP_ATTN_PDL");
+      return v ? atoi(v) : 1;
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sms);
+    cfg.blockDim = dim3((AT_WARPS + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    DAOP_CUDA(cudaLaunchKernelEx(&cfg, attn_qkv_kernel, d_h, d_gamma, d_wqkv, d, rows, rpc, stages,
+                                 eps, d_xa_out, qkv));
     DAOP_CHECK_LAUNCH("attn_qkv");
   }
   // position splits of AT_SPLIT positions (<= 64 splits: max_seq <= 4096)

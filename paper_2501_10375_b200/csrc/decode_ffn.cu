@@ -32,6 +32,7 @@
 // 2 B of gates = 704,774,144 B -> HBM roofline.
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -787,6 +788,14 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
 
 template <int DW, int DS, int DSB>
 __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) {
+  // a kernel launched after this one with programmatic stream serialization
+  // (the next decoder layer's QKV GEMV) may be scheduled onto SMs as soon as
+  // their CTAs of this grid exit; it waits (griddepcontrol.wait) for this
+  // grid's completion before reading anything it produced
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // when this launch itself is programmatic (behind the attention O-proj):
+  // everything below may read that kernel's output
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   decode_body<DW, DS, DSB>(a);
 }
 
@@ -916,11 +925,17 @@ static int launch_decode(DecodeArgs a, int grid, cudaStream_t st, const ServerAr
   cfg.blockDim = dim3(DW * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the per-pick waits
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (tuning: DAOP_MOE_PDL)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  static const int moe_pdl = [] {
+    const char* v = getenv("DAOP_MOE_PDL");
+    return v ? atoi(v) : 0;
+  }();
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (moe_pdl && !sv) ? 2 : 1;
   if (sv) DAOP_CUDA(cudaLaunchKernelEx(&cfg, skern, a, *sv));
   else DAOP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   return DAOP_OK;
