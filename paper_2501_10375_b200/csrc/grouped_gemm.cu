@@ -113,7 +113,8 @@ struct GemmParams {
   int store_cs;
   // diagnostic bits (daop_set_gemm_mode bits 20..22; results are WRONG with
   // any set): 1 epilogue skips TMEM -> global, 2 producer skips the TMA loads
-  // (MMAs on stale smem), 4 producer reloads 4 L2-hot k-blocks of one tile.
+  // (MMAs on stale smem), 4 producer reloads the tile's own first 4 k-blocks
+  // (L2-hot, spread over the L2 slices like the real operands).
   // They split a GEMM's time into MMA / operand feed / epilogue.
   int exp;
 };
@@ -683,8 +684,8 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
               tma_gather4_pair(st + P_A_BYTES + lane * 4 * GB_K * 2, &tmA, &s.full[stage],
                                kb * GB_K, gi[1][0], gi[1][1], gi[1][2], gi[1][3], pol_a);
           } else if (lane == 0) {
-            const int kx = (p.exp & 4) ? (kb & 3) * GB_K : kb * GB_K;  // EXPERIMENT: L2-hot operands
-            const int ra = (p.exp & 4) ? rank * 128 : row0;
+            const int kx = (p.exp & 4) ? (kb & 3) * GB_K : kb * GB_K;  // diagnostic: L2-hot operands
+            const int ra = row0;
             if constexpr (QUAD) {  // box `pairq` for this CTA and its twin in the other pair
               tma_load_2d_pair_mc(st + pairq * P_A_BYTES, &tmA, &s.full[stage], kx,
                                   ra + pairq * 256, static_cast<uint16_t>(0x5u << rank), pol_a);
@@ -696,7 +697,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
           }
           if (lane == 0)
             tma_load_3d_pair(st + C::A_BYTES, &tmB, &s.full[stage], (p.exp & 4) ? (kb & 3) * GB_K : kb * GB_K,
-                             (p.exp & 4) ? (leader ? 0 : p.b_half2) : brow, slot, pol_b);
+                             brow, slot, pol_b);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
