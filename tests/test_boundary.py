@@ -102,3 +102,14 @@ def test_attention_workspace_size():
     q, kv = 32 * 128, 8 * 128
     # qkv fp32 + split partials (8 kv heads x 64 splits x 4 heads x 130) + o bf16 + counters
     assert int(nb[0]) >= (q + 2 * kv) * 4 + 8 * 64 * 4 * 130 * 4 + q * 2 + 4 * 8
+
+
+def test_skinny_token_block_rule():
+    """The skinny GEMMs' token block covers ~1.25x the mean rows per expert
+    with an instantiated NT (decode b = 64 -> 32; 256-token prompt -> 80)."""
+    assert ops.skinny_nt(128, 8) == 32
+    assert ops.skinny_nt(512, 8) == 80
+    assert ops.skinny_nt(768, 8) == 128
+    assert ops.skinny_nt(10_000, 8) == 128
+    assert all(ops.skinny_nt(r, e) in ops.SKINNY_NTS for r in range(1, 2000, 37) for e in (1, 4, 8, 16))
+    assert ops.skinny_nt(64) == 64 and ops.skinny_nt(16) == 32  # by rows alone

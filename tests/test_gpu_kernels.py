@@ -494,7 +494,7 @@ def test_skinny_gemm_matches_dense(P, d, ffn, E, T):
     act = ops.expert_gemm_up(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots, m.slot_elems,
                              d, ffn)
     y = ops.expert_gemm_down(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems, d, ffn)
-    for nt in (32, 64, 128):
+    for nt in ops.SKINNY_NTS:  # 32, 48, 64, 80, 96, 128
         act2 = ops.expert_gemm_up_skinny(pr["x_perm"], pr["offsets"], so, m.slab, m.n_slots,
                                          m.slot_elems, d, ffn, nt)
         y2 = ops.expert_gemm_down_skinny(act, pr["offsets"], so, m.slab, m.n_slots, m.slot_elems,
