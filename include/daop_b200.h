@@ -197,6 +197,22 @@ int daop_combine_dense(const float* d_h, const float* d_y, const float* d_w, int
 int daop_host_expert_ffn(const uint16_t* h_x, int64_t n, const uint16_t* h_w1,
                          const uint16_t* h_w3, const uint16_t* h_w2, int32_t d, int32_t ffn,
                          float* h_y, uint16_t* h_act_scratch, int32_t threads);
+/* The slow expert restricted to ffn rows [r0, r1) (decode-sized n < 16):
+ * y (n, d) fp32 = W2[:, r0:r1] . bf16(silu(x W1[r0:r1]^T) * (x W3[r0:r1]^T)).
+ * The host's share of a slow expert split with the GPU (DaopEngine: the GPU
+ * computes rows [0, r0) from a copy pulled from the pinned pool over PCIe;
+ * both read the host's DRAM).  Replaces part of the CPU expert execution the
+ * reference prices as t_slow (simulator.py:196-234). */
+int daop_host_expert_ffn_rows(const uint16_t* x, int64_t n, const uint16_t* w1, const uint16_t* w3,
+                              const uint16_t* w2, int32_t d, int32_t ffn, int32_t r0, int32_t r1,
+                              float* y, int32_t threads);
+/* The GPU's share of that split: rows [0, rows) of W1 / W3 and columns [0, rows)
+ * of W2 from the expert's pinned host copy (h_w1/h_w3/h_w2, ffn columns / rows)
+ * into d_stage laid out as an expert with ffn = rows: [W1 | W3 | W2 (d x rows)]
+ * (three async copies on `stream`, W2 as one 2-D copy). */
+int daop_slow_split_pull(const uint16_t* h_w1, const uint16_t* h_w3, const uint16_t* h_w2,
+                         int32_t d, int32_t ffn, int32_t rows, uint16_t* d_stage,
+                         daop_stream_t stream);
 /* Pinned host memory for the expert pool (the slow tier and the migration
  * source): mmap + transparent huge pages, parallel first touch on `threads`
  * cores (<= 0: all), cudaHostRegister (*h_registered = 1; 0 when the host has

@@ -92,6 +92,8 @@ PROTOS = {
     "daop_decode_timeline": [I32, P, I32],
     "daop_combine_dense": [P, P, P, I32, I32, P, P],
     "daop_host_expert_ffn": [P, I64, P, P, P, I32, I32, P, P, I32],
+    "daop_host_expert_ffn_rows": [P, I64, P, P, P, I32, I32, I32, I32, P, I32],
+    "daop_slow_split_pull": [P, P, P, I32, I32, I32, P, P],
     "daop_host_caps": [P, P],
     "daop_host_set_grain": [I64, I64],
     "daop_host_stream_read": [P, I64, I32, P],

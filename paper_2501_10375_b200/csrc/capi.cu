@@ -95,6 +95,29 @@ int daop_graph_step(void* graph_exec, daop_stream_t stream, const void* h_src, v
 }
 
 // placement.py:123-125 -- math.floor(ecr * L * E), left to right in double
+// The GPU's share of a slow expert: rows [0, rows) of W1 and W3 and columns
+// [0, rows) of W2, pulled from the expert's pinned host copy over PCIe into a
+// staging slot laid out as an expert with ffn = rows ([W1 | W3 | W2 (d x
+// rows)]), on `stream` (three async copies; W2's columns as one 2-D copy).
+int daop_slow_split_pull(const uint16_t* h_w1, const uint16_t* h_w3, const uint16_t* h_w2,
+                         int32_t d, int32_t ffn, int32_t rows, uint16_t* d_stage,
+                         daop_stream_t stream) {
+  if (d <= 0 || ffn <= 0 || rows <= 0 || rows > ffn) {
+    set_error("slow_split_pull: invalid shape (d=%d ffn=%d rows=%d)", d, ffn, rows);
+    return DAOP_ERR_SHAPE;
+  }
+  cudaStream_t st = as_stream(stream);
+  const size_t rb = static_cast<size_t>(rows) * d * 2;
+  DAOP_CUDA(cudaMemcpyAsync(d_stage, h_w1, rb, cudaMemcpyHostToDevice, st));
+  DAOP_CUDA(cudaMemcpyAsync(d_stage + static_cast<size_t>(rows) * d, h_w3, rb,
+                            cudaMemcpyHostToDevice, st));
+  DAOP_CUDA(cudaMemcpy2DAsync(d_stage + 2 * static_cast<size_t>(rows) * d,
+                              static_cast<size_t>(rows) * 2, h_w2, static_cast<size_t>(ffn) * 2,
+                              static_cast<size_t>(rows) * 2, static_cast<size_t>(d),
+                              cudaMemcpyHostToDevice, st));
+  return DAOP_OK;
+}
+
 int daop_slot_budget(double ecr, int32_t L, int32_t E, int64_t* budget) {
   double v = (ecr * static_cast<double>(L)) * static_cast<double>(E);
   if (!std::isfinite(v)) {

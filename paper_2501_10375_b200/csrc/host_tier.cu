@@ -461,6 +461,46 @@ extern "C" int daop_host_expert_ffn(const uint16_t* x, int64_t n, const uint16_t
   return DAOP_OK;
 }
 
+// The expert restricted to ffn rows [r0, r1): act rows r0..r1-1 and
+// y = W2[:, r0:r1] . act[r0:r1] -- the host's share of a slow expert whose
+// rows [0, r0) the GPU computes from a copy pulled over PCIe (the host's
+// DRAM serves both: ~200 GB/s together vs ~170 for the host alone).
+// Decode-sized n (< 16, the AVX-512 path); y (n, d) fp32 is overwritten.
+extern "C" int daop_host_expert_ffn_rows(const uint16_t* x, int64_t n, const uint16_t* w1,
+                                         const uint16_t* w3, const uint16_t* w2, int32_t d,
+                                         int32_t ffn, int32_t r0, int32_t r1, float* y,
+                                         int32_t threads) {
+  if (n < 0 || n >= 16 || d <= 0 || ffn <= 0 || r0 < 0 || r1 > ffn || r0 >= r1) {
+    set_error("host_expert_ffn_rows: invalid shape (n=%lld d=%d ffn=%d rows %d..%d); n < 16",
+              static_cast<long long>(n), d, ffn, r0, r1);
+    return DAOP_ERR_SHAPE;
+  }
+  if (n == 0) return DAOP_OK;
+  if (threads < 1) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  host::Pool* pool = host::pool_for(threads);
+  const int nr = r1 - r0;
+  std::vector<uint16_t> act(static_cast<size_t>(n) * nr);
+  pool->run(nr, [&](int, int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+      const uint16_t* q1 = w1 + (r0 + i) * d;
+      const uint16_t* q3 = w3 + (r0 + i) * d;
+      for (int64_t t = 0; t < n; ++t) {
+        float g, u;
+        host::dot2(x + t * d, q1, q3, d, &g, &u);
+        const float sv = g / (1.0f + std::exp(-g));
+        act[t * nr + i] = host::f2bf(sv * u);
+      }
+    }
+  }, g_grain_up);
+  pool->run(d, [&](int, int64_t a, int64_t b) {
+    for (int64_t j = a; j < b; ++j) {
+      const uint16_t* q2 = w2 + j * ffn + r0;
+      for (int64_t t = 0; t < n; ++t) y[t * d + j] = host::dot_long(act.data() + t * nr, q2, nr);
+    }
+  }, g_grain_down);
+  return DAOP_OK;
+}
+
 // profiling aid: read `bytes` of host memory with the host tier's thread pool
 // (64 B vector loads, contiguous split) -- the bandwidth ceiling of the slow
 // tier's GEMV, measured on the same threads

@@ -126,6 +126,60 @@ class HostExpertPool:
         return b, b + fd * 2, b + 2 * fd * 2
 
 
+SLOW_SPLIT_FRAC = 0.28  # GPU share of a split slow expert (PCIe ~55 of ~200 GB/s host DRAM)
+
+
+class SlowSplit:
+    """One slow (host-tier) expert of a decode token executed by the host AND
+    the GPU together: the GPU pulls rows [0, R) of W1 / W3 and columns [0, R)
+    of W2 from the expert's pinned host copy over PCIe
+    (daop_slow_split_pull) and runs them through the skinny tcgen05 GEMMs
+    as an expert with ffn = R, while the host tier computes rows [R, ffn)
+    (daop_host_expert_ffn_rows); y = y_gpu + y_host (fixed order).  Both
+    halves read the host's DRAM, which serves ~200 GB/s to the two together
+    against ~170 GB/s to the host alone (`scripts/host_pcie_contention.py`),
+    so the slow tier -- the whole token time at ECR < 1 -- shrinks.  The
+    decisions (which experts are slow, stale inputs) are the reference's;
+    only the slow tier's execution changes."""
+
+    def __init__(self, pool: HostExpertPool, rows: int, device, threads: int = 0):
+        d, ffn = pool.d, pool.ffn
+        if rows <= 0 or rows >= ffn or rows % 128 or d % 128:
+            raise ConfigError(f"slow split: {rows} GPU rows of ffn {ffn} (multiple of 128 below ffn)")
+        self.pool, self.rows, self.threads = pool, rows, threads
+        self.device = torch.device(device)
+        self.stream = torch.cuda.Stream(self.device)
+        self.stage = torch.empty(3 * rows * d, dtype=torch.bfloat16, device=self.device)
+        self.x = torch.empty((1, d), dtype=torch.bfloat16, device=self.device)
+        self.x_host = torch.empty((1, d), dtype=torch.int16, pin_memory=True)
+        self.off = torch.tensor([0, 1], dtype=torch.int64, device=self.device)
+        self.slot = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.y_gpu = torch.empty((1, d), dtype=torch.float32, pin_memory=True)
+        self.y_host = np.empty((1, d), dtype=np.float32)
+        self.done = torch.cuda.Event()
+
+    def run(self, layer: int, expert: int, x_bf16: np.ndarray) -> np.ndarray:
+        """x_bf16: (1, d) bf16 bits -> y (1, d) fp32 of the whole expert."""
+        pool, R, d, ffn = self.pool, self.rows, self.pool.d, self.pool.ffn
+        x = np.ascontiguousarray(x_bf16, dtype=np.uint16).reshape(1, d)
+        w1, w3, w2 = pool.ptrs(layer, expert)
+        self.x_host.numpy()[:] = x.view(np.int16)
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            self.x.view(torch.int16).copy_(self.x_host, non_blocking=True)
+            _lib.call("daop_slow_split_pull", w1, w3, w2, d, ffn, R, self.stage.data_ptr(),
+                      self.stream.cuda_stream)
+            act = ops.expert_gemm_up_skinny(self.x, self.off, self.slot, self.stage, 1, 3 * R * d,
+                                            d, R, nt=32)
+            y = ops.expert_gemm_down_skinny(act, self.off, self.slot, self.stage, 1, 3 * R * d, d,
+                                            R, nt=32)
+            self.y_gpu.copy_(y, non_blocking=True)
+            self.done.record(self.stream)
+        _lib.call("daop_host_expert_ffn_rows", x.ctypes.data, 1, w1, w3, w2, d, ffn, R, ffn,
+                  self.y_host.ctypes.data, self.threads)
+        self.done.synchronize()
+        return self.y_gpu.numpy() + self.y_host
+
+
 def host_expert_ffn(pool: HostExpertPool, layer: int, expert: int, x_bf16: np.ndarray,
                     threads: int = 0) -> np.ndarray:
     """Slow-tier execution of one expert on (n, d) bf16 inputs -> (n, d) fp32."""
@@ -186,6 +240,9 @@ class DaopEngine:
         self.swap_in_out = swap_in_out
         self.weights_from_pred = weights_from_pred
         self.host_threads = host_threads
+        # decode slow tier split with the GPU over PCIe (SlowSplit); 0 = host only
+        self.slow_split_rows = 0
+        self._slow_split = None
         self.host_ms = 0.0  # decode: wall time inside host-tier expert calls
         self.prefill_host_ms = 0.0  # prefill: the same for the slow experts' token batches
         self._host_exec = None  # one thread feeding the host tier (decode pre-calculation)
@@ -521,6 +578,17 @@ class DaopEngine:
                   nd.ctypes.data)
         return sel[1], isf[1]
 
+    def _slow_splitter(self):
+        """The SlowSplit for slow_split_rows (None = the host tier alone)."""
+        r = int(self.slow_split_rows)
+        if r <= 0:
+            return None
+        sp = self._slow_split
+        if sp is None or sp.rows != r or sp.threads != self.host_threads:
+            sp = self._slow_split = SlowSplit(self.pool, r, self.model.slab.device,
+                                              self.host_threads)
+        return sp
+
     def decode(self, h: torch.Tensor) -> DecodeResult:
         """One decode token (h: (d,) fp32 on device) through every layer.
 
@@ -571,9 +639,12 @@ class DaopEngine:
         if self._host_exec is None:
             self._host_exec = ThreadPoolExecutor(max_workers=1, thread_name_prefix="daop-host")
 
+        split = self._slow_splitter()
+
         def host_job(l, e, xs):  # one slow expert on the host tier (GIL released)
             th0 = time.perf_counter()
-            y = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
+            y = split.run(l, e, xs) if split is not None else \
+                host_expert_ffn(self.pool, l, e, xs, self.host_threads)
             with self._host_ms_lock:
                 self.host_ms += 1e3 * (time.perf_counter() - th0)
             return y

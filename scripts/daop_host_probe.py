@@ -32,13 +32,17 @@ eng.prefill(prompt)
 toks = [eng.model.input_hidden(1, stream=401, step=i)[0] for i in range(24)]
 xs = np.random.default_rng(0).standard_normal((1, D)).astype(np.float32)
 ncpu = len(os.sched_getaffinity(0))
-for th in [0, ncpu - 1, ncpu, 2 * ncpu, 0]:
+configs = [(0, 0), (0, 4096), (0, 3072), (0, 5120), (0, 0), (0, 4096)]
+if len(sys.argv) > 1 and sys.argv[1] == "threads":
+    configs = [(0, 0), (ncpu - 1, 0), (ncpu, 0), (2 * ncpu, 0), (0, 0)]
+for th, split in configs:
     # standalone per-expert time at this thread count
     t0 = time.perf_counter()
     for e in range(8):
         host_expert_ffn(pool, 5, e, xs, th)
     solo = (time.perf_counter() - t0) / 8 * 1e3
     eng.host_threads = th
+    eng.slow_split_rows = split
     eng.host_ms = 0.0
     for t in toks[:4]:
         eng.decode(t)
@@ -50,6 +54,7 @@ for th in [0, ncpu - 1, ncpu, 2 * ncpu, 0]:
         r = eng.decode(t)
         slow += sum(1 for lp in r.plans for ex in lp.executed if ex.device == "slow")
     dt = (time.perf_counter() - t0) / n * 1e3
-    print(f"host_threads {th or ncpu:3d}: {1e3 / dt:6.2f} tok/s, {dt:6.1f} ms/token, host busy "
-          f"{eng.host_ms / n:6.1f} ms/token, {slow / n:5.1f} slow/token -> "
-          f"{eng.host_ms / max(slow, 1):5.2f} ms/expert in situ (solo {solo:5.2f})", flush=True)
+    print(f"host_threads {th or ncpu:3d} gpu split rows {split:5d}: {1e3 / dt:6.2f} tok/s, "
+          f"{dt:6.1f} ms/token, host tier busy {eng.host_ms / n:6.1f} ms/token, {slow / n:5.1f} "
+          f"slow/token -> {eng.host_ms / max(slow, 1):5.2f} ms/expert in situ (host alone, solo "
+          f"{solo:5.2f})", flush=True)

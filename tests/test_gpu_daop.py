@@ -237,3 +237,26 @@ def test_resident_prefill_graph_equals_eager(attention):
         assert torch.equal(a[0], b[0])
         for x, y in zip(a[1:], b[1:]):
             assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("rows", [128, 256])
+def test_slow_split_equals_host_expert(rows):
+    """A slow expert split between the GPU (rows [0, R) pulled from the pinned
+    pool over PCIe, skinny tcgen05 GEMMs) and the host tier (rows [R, ffn))
+    equals the host tier's whole expert within the fp32 reassociation of the
+    down sums (tried: off by default)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_10375_b200 as P
+    from paper_2501_10375_b200.daop import HostExpertPool, SlowSplit, host_expert_ffn
+    shape = P.ModelShape(2, 4, 2)
+    d, ffn = 256, 512
+    pool = HostExpertPool(shape, d, ffn, seed=5, device="cuda")
+    sp = SlowSplit(pool, rows, "cuda", threads=4)
+    from oracle import rng as R
+    xb = R.f32_to_bf16_bits(np.random.default_rng(rows).normal(size=(1, d)).astype(np.float32))
+    for layer, e in ((0, 1), (1, 3)):
+        ref = host_expert_ffn(pool, layer, e, xb, 4)
+        y = sp.run(layer, e, xb)
+        tol = 2e-3 * float(np.sqrt(np.mean(ref ** 2))) + 1e-3 * np.abs(ref).max()
+        assert np.abs(y - ref).max() <= tol

@@ -65,3 +65,31 @@ def test_chunked_schedule_is_bit_identical(n, threads):
         out.append(y)
     _lib.call("daop_host_set_grain", 32, 16)
     assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+
+
+@pytest.mark.parametrize("r0", [0, 128, 384])
+def test_host_expert_rows_sum_to_the_expert(r0):
+    """daop_host_expert_ffn_rows (the host's share of a slow expert split with
+    the GPU, daop.SlowSplit): rows [0, r0) + rows [r0, ffn) == the whole
+    expert within the fp32 reassociation of the down sums; rows [0, ffn) vs
+    the oracle."""
+    d, ffn = 256, 512
+    om = N.OracleModel(2, 4, 2, d, ffn, seed=11)
+    w1, w3, w2 = om.w1(0, 1), om.w3(0, 1), om.w2(0, 1)
+    to_bits = lambda a: np.ascontiguousarray(R.f32_to_bf16_bits(a))  # noqa: E731
+    b1, b3, b2 = to_bits(w1), to_bits(w3), to_bits(w2)
+    x = R.round_bf16(np.random.default_rng(r0).normal(size=(1, d)).astype(np.float32))
+    xb = to_bits(x)
+    ref = N.expert_ffn(x, w1, w3, w2)
+    tol = 2e-3 * float(np.sqrt(np.mean(ref ** 2))) + 1e-3 * np.abs(ref).max()
+
+    def rows(a, b):
+        y = np.empty((1, d), dtype=np.float32)
+        _lib.call("daop_host_expert_ffn_rows", xb.ctypes.data, 1, b1.ctypes.data,
+                  b3.ctypes.data, b2.ctypes.data, d, ffn, a, b, y.ctypes.data, 3)
+        return y
+
+    y = rows(r0, ffn) + (rows(0, r0) if r0 else 0)
+    assert np.abs(y - ref).max() <= tol
+    with pytest.raises(Exception):
+        rows(0, ffn + 1)
