@@ -454,6 +454,25 @@ int daop_server_stop(void* handle);
  * (d_buf [cap][4] u64 zeroed: doorbell seen, input released, body done) */
 int daop_server_trace(uint64_t* d_buf, int32_t cap);
 
+/* ------------------------------------------------ die topology (B200: two dies)
+ * SM -> die map of the current device, measured once and cached (csrc/
+ * topology.cu: one CTA per SM times loads of sampled L2 lines; lines homed on
+ * the SM's own die answer faster).  die_of_sm[smid] for smid < n_sm; *n_die =
+ * 2 when the SMs split into two clean halves, else 1 (all zeros).  Used by the
+ * prefill GEMMs' per-die tile schedule (no reference counterpart). */
+int daop_die_map(int32_t* die_of_sm, int32_t n_sm, int32_t* n_die);
+/* Per-die tile schedule of the CTA-pair prefill GEMMs (each die strides over
+ * its own share of every expert's m-tiles): n == 0 off, n < 0 the measured map
+ * (daop_die_map), n > 0 an explicit table (die of SM i = tab[i] != 0). */
+int daop_set_gemm_die_table(const int32_t* tab, int32_t n);
+/* profiling aid (under ncu, lts__t_sectors_srcunit_ltcfabric): SM `ref` reads
+ * the buffer, then SM `test` reads it (test == ref: one SM reads twice) */
+int daop_die_pair_probe(const void* d_buf, int64_t bytes, int32_t ref, int32_t test,
+                        uint32_t* d_flag, daop_stream_t stream);
+/* profiling aid: the raw measurement (lat: grid x nlines clocks, smid: grid) */
+int daop_die_probe(const uint32_t* d_buf, int32_t nlines, int32_t stride_words, int32_t grid,
+                   uint32_t* d_lat, int32_t* d_smid, daop_stream_t stream);
+
 /* ------------------------------------------------ trace files (moesim JSONL)
  * Formats one phase's token records of a RoutingTrace exactly as
  * moesim/trace.py:328-362 save_trace does ("%.17g" scores, "null" where the

@@ -23,6 +23,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <vector>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -117,6 +119,15 @@ struct GemmParams {
   // (L2-hot, spread over the L2 slices like the real operands).
   // They split a GEMM's time into MMA / operand feed / epilogue.
   int exp;
+  // per-die tile schedule (pair kernel, B200's two dies; null = one die):
+  // die_tab[smid] is the die of each SM; die_ctr (3 words, zeroed before the
+  // launch) counts the clusters of each die and the arrivals.  Every cluster
+  // takes a rank on its die; each expert's m-tiles are split between the dies
+  // in proportion to their cluster counts, and a die's clusters stride only
+  // over its own tiles -- so the A rows (and the act / y output) a die
+  // re-reads stay in that die's L2 instead of crossing the die-to-die fabric.
+  const int8_t* die_tab;
+  unsigned* die_ctr;
 };
 
 __device__ __forceinline__ int64_t off_at(const GemmParams& p, int e) {
@@ -509,8 +520,11 @@ struct PairSmem {
   uint64_t tempty[2];
   uint32_t tmem_base;
   int32_t prefix[G_MAX_EXPERTS + 1];
-  int32_t mt[G_MAX_EXPERTS];
+  int32_t mt[G_MAX_EXPERTS];   // m-tiles of expert e this CTA's schedule covers
+  int32_t mlo[G_MAX_EXPERTS];  // first of them (per-die schedule; else 0)
   int64_t off[G_MAX_EXPERTS + 1];
+  int32_t tcl, ncl;            // this cluster's first tile and the tile stride
+  int32_t dinfo[4];            // per-die schedule: die, rank, clusters on die 0 / 1
 };
 
 // raster 0: groups of G m-tiles, m fastest (the wave shares one weight tile
@@ -527,7 +541,7 @@ __device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, 
     const int grp = u / (G * nt);
     const int r = u - grp * G * nt;
     const int gm = min(G, s.mt[e] - grp * G);
-    m = grp * G + r % gm;
+    m = s.mlo[e] + grp * G + r % gm;
     n = r / gm;
   } else {
     const int mt = s.mt[e];
@@ -535,7 +549,7 @@ __device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, 
     const int r = u - grp * G * mt;
     const int gn = min(G, nt - grp * G);
     n = grp * G + r % gn;
-    m = r / gn;
+    m = s.mlo[e] + r / gn;
   }
   return true;
 }
@@ -597,15 +611,62 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
       mbar_init(&s.tempty[i], 2 * C::EPI_WARPS);  // epilogue warps x 2 CTAs (leader's copy)
     }
     fence_mbar_init();
+  }
+  const bool per_die = !QUAD && p.die_tab != nullptr;
+  if (per_die) {
+    if (threadIdx.x == 0 && leader) {  // rank on this die; wait until every cluster has one
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      const int die = p.die_tab[sm] ? 1 : 0;
+      const unsigned r = atomicAdd(p.die_ctr + die, 1u);
+      __threadfence();
+      atomicAdd(p.die_ctr + 2, 1u);
+      while (ld_acquire_gpu(p.die_ctr + 2) < static_cast<unsigned>(nclusters)) {
+      }
+      s.dinfo[0] = die;
+      s.dinfo[1] = static_cast<int>(r);
+      s.dinfo[2] = static_cast<int>(ld_acquire_gpu(p.die_ctr));
+      s.dinfo[3] = static_cast<int>(ld_acquire_gpu(p.die_ctr + 1));
+    }
+    cluster_sync_all();
+    if (threadIdx.x == 0 && !leader) {  // the leader's rank (distributed shared memory)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t v;
+        asm volatile(
+            "{\n\t.reg .u32 ra;\n\t"
+            "mapa.shared::cluster.u32 ra, %1, %2;\n\t"
+            "ld.shared::cluster.u32 %0, [ra];\n\t}"
+            : "=r"(v)
+            : "r"(smem_u32(&s.dinfo[i])), "r"(lead_cta)
+            : "memory");
+        s.dinfo[i] = static_cast<int>(v);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
     int acc = 0;
     s.prefix[0] = 0;
     for (int e = 0; e <= E; ++e) s.off[e] = off_at(p, e);
+    // per-die: expert e's m-tiles [0, split_e) go to die 0, the rest to die 1,
+    // split_e from the running total so the remainders spread over experts
+    const int64_t n0 = per_die ? s.dinfo[2] : 1, nall = per_die ? s.dinfo[2] + s.dinfo[3] : 1;
+    const int die = per_die ? s.dinfo[0] : 0;
+    int64_t cum = 0;
     for (int e = 0; e < E; ++e) {
       const int64_t me = slot_at(p, e) >= 0 ? s.off[e + 1] - s.off[e] : 0;
-      s.mt[e] = static_cast<int>((me + C::M - 1) / C::M);
+      const int mte = static_cast<int>((me + C::M - 1) / C::M);
+      const int a = static_cast<int>((cum * n0 + nall / 2) / nall);
+      cum += mte;
+      const int b = static_cast<int>((cum * n0 + nall / 2) / nall);
+      const int split = per_die ? b - a : mte;  // die 0's share of this expert
+      s.mlo[e] = die == 0 ? 0 : split;
+      s.mt[e] = die == 0 ? split : mte - split;
       acc += s.mt[e] * (QUAD ? p.n_tiles / 2 : p.n_tiles);
       s.prefix[e + 1] = acc;
     }
+    s.tcl = per_die ? s.dinfo[1] : cluster;
+    s.ncl = per_die ? (die == 0 ? s.dinfo[2] : s.dinfo[3]) : nclusters;
   }
   if (warp == 2) tmem_alloc_pair<512>(&s.tmem_base);
   tc_fence_before();
@@ -636,7 +697,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
       int stage = 0;
       uint32_t phase = 0;
       int e, m, n;
-      for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+      for (int t = s.tcl; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += s.ncl) {
         if (QUAD) n = 2 * n + pairq;
         int ks, kb0, kb1;
         split_tile(p, n, n, ks, kb0, kb1);
@@ -711,7 +772,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
       int stage = 0, acc = 0, iters = 0;
       uint32_t phase = 0, acc_phase = 0;
       int e, m, n;
-      for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+      for (int t = s.tcl; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += s.ncl) {
         if (QUAD) n = 2 * n + pairq;
         int ks, kb0, kb1;
         split_tile(p, n, n, ks, kb0, kb1);
@@ -761,7 +822,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
     int acc = 0;
     uint32_t acc_phase = 0;
     int e, m, n;
-    for (int t = cluster; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += nclusters) {
+    for (int t = s.tcl; map_tile_pair(s, E, nt, G, p.raster, t, e, m, n); t += s.ncl) {
       if (QUAD) n = 2 * n + pairq;
       int ks, kb0, kb1;
       split_tile(p, n, n, ks, kb0, kb1);
@@ -841,7 +902,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
         const int64_t grow = s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile;
         if ((p.demote & 1) && p.raster == 0 && n == nt - 1 && valid)  // A m-tile done
           l2_demote_range(p.a_ptr + grow * p.a_ld, p.a_ld * 2);
-        if ((p.demote & 2) && p.raster == 1 && m == s.mt[e] - 1) {     // B n-tile done
+        if ((p.demote & 2) && p.raster == 1 && m == s.mlo[e] + s.mt[e] - 1) {  // B n-tile done
           const int brow = n * p.b_tile_rows + (rank == 0 ? 0 : p.b_half2) + q * 32 + lane;
           l2_demote_range(p.b_ptr + static_cast<int64_t>(slot_at(p, e)) * p.b_slot_stride +
                               static_cast<int64_t>(brow) * p.b_ld,
@@ -881,6 +942,96 @@ static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
 static int g_gemm_splitk = 1;
 static int g_gemm_exp = 0;  // EXPERIMENT bits (GemmParams::exp)
 static int g_gemm_quad = 0;  // tuning: 4-CTA multicast clusters for the 512-row pair tile (mode bit 18)  // tuning: split-K for prompt-sized dense projections (_ws entry)
+
+// per-die tile schedule (GemmParams::die_tab): the device table of each SM's
+// die and a ring of per-launch counters.  g_die_mode: -1 auto (the measured
+// map, daop_die_map, when it finds two dies), 0 off, 1 the table set by
+// daop_set_gemm_die_table.
+static int g_die_mode = -1;
+static std::mutex g_die_mu;
+static std::vector<int8_t> g_die_host;  // custom table (mode 1)
+struct DieState {
+  int8_t* tab = nullptr;
+  unsigned* ctr = nullptr;
+  int slot = 0;
+  int mode = -2;  // g_die_mode the table was built for
+  bool on = false;
+};
+static DieState g_die_state[64];
+constexpr int DIE_SLOTS = 64;
+
+// (table, zeroed counters) for a launch on `st`, or nullptrs when off
+static int die_schedule(cudaStream_t st, const int8_t** tab, unsigned** ctr) {
+  *tab = nullptr;
+  *ctr = nullptr;
+  static const bool env_off = [] {
+    const char* v = getenv("DAOP_GEMM_DIE");  // "0": plain schedule (A/B runs)
+    return v && v[0] == '0';
+  }();
+  if (g_die_mode == 0 || (env_off && g_die_mode < 0)) return DAOP_OK;
+  int dev = 0;
+  DAOP_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return DAOP_OK;
+  std::lock_guard<std::mutex> lk(g_die_mu);
+  DieState& d = g_die_state[dev];
+  if (d.mode != g_die_mode) {
+    // the probe synchronises the device: never inside a stream capture (this
+    // launch runs the plain schedule; the next one outside a capture probes)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      (void)cudaGetLastError();
+      return DAOP_OK;
+    }
+    const int n = sm_count();
+    std::vector<int8_t> h(static_cast<size_t>(n), 0);
+    bool two = false;
+    if (g_die_mode == 1) {
+      for (int i = 0; i < n && i < static_cast<int>(g_die_host.size()); ++i) h[i] = g_die_host[i] ? 1 : 0;
+      two = true;
+    } else {
+      std::vector<int32_t> m(static_cast<size_t>(n));
+      int32_t nd = 1;
+      if (daop_die_map(m.data(), n, &nd) == DAOP_OK && nd == 2) {
+        for (int i = 0; i < n; ++i) h[i] = static_cast<int8_t>(m[i]);
+        two = true;
+      }
+    }
+    if (!d.tab) DAOP_CUDA(cudaMalloc(&d.tab, 1024));
+    if (!d.ctr) DAOP_CUDA(cudaMalloc(&d.ctr, DIE_SLOTS * 4 * sizeof(unsigned)));
+    DAOP_CUDA(cudaMemcpy(d.tab, h.data(), h.size(), cudaMemcpyHostToDevice));
+    d.on = two;
+    d.mode = g_die_mode;
+  }
+  if (!d.on) return DAOP_OK;
+  unsigned* c = d.ctr + 4 * d.slot;
+  d.slot = (d.slot + 1) % DIE_SLOTS;  // concurrent launches on other streams get other slots
+  DAOP_CUDA(cudaMemsetAsync(c, 0, 4 * sizeof(unsigned), st));
+  *tab = d.tab;
+  *ctr = c;
+  return DAOP_OK;
+}
+
+// co-resident clusters of a pair-kernel instantiation (the per-die schedule
+// waits for every cluster of the launch)
+static int max_active_clusters(const void* kern, int cl, int threads, size_t smem, int want) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl * want);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cl;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    return want;
+  }
+  return n < want ? n : want;
+}
 
 template <bool TWO_M>
 static size_t pair_smem_bytes() {
@@ -927,6 +1078,19 @@ static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   }
   if (max_tiles < clusters) clusters = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
   GemmParams pp = p;
+  // per-die schedule for the big grouped GEMMs only: with few m-tiles (prompt-
+  // sized dense projections, split-K) a die would get no tiles
+  if (!QUAD && p.ksplit <= 1 && rows_total / C::M >= 16) {
+    int rc = die_schedule(st, &pp.die_tab, &pp.die_ctr);
+    if (rc) return rc;
+    if (pp.die_tab) {
+      static int co[2] = {0, 0};  // per SWIGLU instantiation family (same smem / threads)
+      int& c = co[TWO_M ? 1 : 0];
+      if (!c) c = max_active_clusters(reinterpret_cast<const void*>(kern), CL, C::THREADS, smem,
+                                      sm_count() / CL);
+      if (c < clusters) clusters = c;
+    }
+  }
   pp.store_cs = g_gemm_store_cs;
   pp.exp = g_gemm_exp;
   if (p.group_m < 0) {  // negative group = n-grouped raster of |group| weight tiles
@@ -1051,6 +1215,25 @@ static int check_ffn_shape(int64_t rows, int32_t d, int32_t ffn, int32_t E) {
 // capture: a CUDA graph that captures the GEMMs calls this first
 extern "C" int daop_gemm_prepare() {
   apply_persisting_l2();
+  return DAOP_OK;
+}
+
+// per-die tile schedule of the CTA-pair GEMMs: n == 0 off, n < 0 the measured
+// SM -> die map (daop_die_map), n > 0 the given table (die of SM i = tab[i])
+extern "C" int daop_set_gemm_die_table(const int32_t* tab, int32_t n) {
+  if (n > 1024) {
+    set_error("gemm die table: %d entries (max 1024)", n);
+    return DAOP_ERR_CONFIG;
+  }
+  if (n == 0) {
+    g_die_mode = 0;
+  } else if (n < 0) {
+    g_die_mode = -1;
+  } else {
+    g_die_host.assign(tab, tab + n);
+    g_die_mode = 1;
+    for (auto& d : g_die_state) d.mode = -2;  // rebuild the device table
+  }
   return DAOP_OK;
 }
 

@@ -1,0 +1,257 @@
+// Die topology of the B200: which of the two dies each SM sits on.
+//
+// The B200 is two dies joined by the die-to-die fabric; every L2 line has a
+// home on one die, and an SM reading a line homed on the other die pulls it
+// over the fabric (ncu lts__t_sectors_srcunit_ltcfabric).  Tensor-bound
+// kernels on this GPU run power-capped, and fabric traffic is power: the
+// prefill GEMMs schedule their tiles per die (grouped_gemm.cu) so that each
+// die re-reads its own operand tiles from its own L2.
+//
+// The SM -> die map is not exposed by the driver, so it is measured: one CTA
+// per SM times a load of each of `nlines` sampled L2 lines (after a warm-up
+// that brings them into L2).  A line homed on the SM's own die answers
+// measurably faster; two SMs are on the same die when their near/far
+// patterns agree.  daop_die_map runs the probe once per device and caches
+// the result (die_of_sm[smid] in {0, 1}); it returns a single die (all 0)
+// when the patterns do not split the SMs into two clean halves.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+
+namespace daop {
+
+// Phase 0: the CTA on SM `ref` reads every line (the lines land in its die's
+// L2: their home, or the die-local copy of a line homed across the fabric --
+// lines are cached in the reading die, `scripts/die_pair_probe.py` shows it
+// with ncu's fabric counter).  Phase 1: every SM times the FIRST access of its
+// own lines (set smid: lines i * grid + smid): an SM on ref's
+// die finds all of them in its die's L2; an SM on the other die finds only the
+// half homed there and pulls the rest over the fabric (slower).  One CTA per
+// SM (large dynamic smem).  `zero` is 0 at run time: each load's address
+// depends on the clock read before it, so the timed load cannot be hoisted.
+__global__ void __launch_bounds__(32, 1) die_probe_kernel(const uint32_t* __restrict__ buf,
+                                                          int per_sm, int stride_words, int ref,
+                                                          int phase, uint32_t zero,
+                                                          uint32_t* __restrict__ lat,
+                                                          int32_t* __restrict__ smid_out) {
+  extern __shared__ uint8_t pad[];
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  const int lane = threadIdx.x;
+  if (phase == 0) {
+    if (static_cast<int>(sm) != ref) return;
+    const int n = per_sm * static_cast<int>(gridDim.x);
+    uint32_t sink = 0;
+    for (int i = lane; i < n; i += 32) {
+      uint32_t v;
+      asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(buf + static_cast<int64_t>(i) * stride_words));
+      sink += v;
+    }
+    if (sink == 0xdeadbeefu) pad[0] = 1;  // keep the loads
+    return;
+  }
+  if (lane != 0) return;
+  smid_out[blockIdx.x] = static_cast<int32_t>(sm);
+  const uint32_t sdst = static_cast<uint32_t>(__cvta_generic_to_shared(pad));
+  uint32_t v = 0;
+#pragma unroll 1
+  for (int i = 0; i < per_sm; ++i) {
+    // line i of this SM's set sits at i * grid + smid: every set samples the
+    // whole buffer (lines of both homes)
+    const uint32_t* p = buf + (static_cast<int64_t>(i) * gridDim.x + sm) * stride_words + (v & zero);
+    uint64_t t0, t1;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0)::"memory");
+    const uint32_t* q = p + (static_cast<uint32_t>(t0) & zero);
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(q) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(sdst), "r"(v) : "memory");
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1)::"memory");
+    lat[static_cast<int64_t>(blockIdx.x) * per_sm + i] = static_cast<uint32_t>(t1 - t0);
+  }
+}
+
+// Pair probe (read with ncu's fabric counter): the CTA on SM `ref` reads the
+// buffer, then the CTA on SM `test` reads it again.  Lines homed across the
+// fabric are cached in the reader's die: when ref and test share a die the
+// second read adds no fabric traffic, when they do not it pulls the other
+// half of the buffer across.  test == ref reads twice on one SM.
+__global__ void __launch_bounds__(256, 1) die_pair_kernel(const uint4* __restrict__ buf,
+                                                          int64_t n16, int ref, int test,
+                                                          unsigned* flag, uint32_t* sink) {
+  extern __shared__ uint8_t pad[];
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  const bool is_ref = static_cast<int>(sm) == ref, is_test = static_cast<int>(sm) == test;
+  if (!is_ref && !is_test) return;
+  uint32_t acc = 0;
+  const int reads = is_ref && is_test ? 2 : 1;
+  if (is_test && !is_ref && threadIdx.x == 0)
+    while (ld_acquire_gpu(flag) == 0u) {
+    }
+  __syncthreads();
+  for (int r = 0; r < reads; ++r)
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) {
+      uint4 v;
+      asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "l"(buf + i));
+      acc += v.x ^ v.y ^ v.z ^ v.w;
+    }
+  __syncthreads();
+  if (is_ref && threadIdx.x == 0) {
+    __threadfence();
+    st_release_gpu(flag, 1u);
+  }
+  if (acc == 0x9e3779b9u) sink[0] = acc;
+  pad[threadIdx.x] = 0;
+}
+
+}  // namespace daop
+
+using namespace daop;
+
+// profiling aid (run under ncu): see die_pair_kernel; flag is one device word
+// (reset here), grid = one CTA per SM
+extern "C" int daop_die_pair_probe(const void* d_buf, int64_t bytes, int32_t ref, int32_t test,
+                                   uint32_t* d_flag, daop_stream_t stream) {
+  if (bytes < 16 || bytes % 16) {
+    set_error("die_pair_probe: bytes must be a positive multiple of 16");
+    return DAOP_ERR_SHAPE;
+  }
+  cudaStream_t st = as_stream(stream);
+  DAOP_CUDA(cudaMemsetAsync(d_flag, 0, 8, st));
+  const int smem = 120 * 1024;
+  DAOP_CUDA(cudaFuncSetAttribute(die_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  die_pair_kernel<<<sm_count(), 256, smem, st>>>(static_cast<const uint4*>(d_buf), bytes / 16, ref,
+                                                 test, d_flag, d_flag + 1);
+  DAOP_CHECK_LAUNCH("die_pair_probe");
+  return DAOP_OK;
+}
+
+// profiling aid / the measurement behind daop_die_map: lat (grid x nlines)
+// clocks, smid (grid) -- buf is a device buffer of nlines * stride_words words
+extern "C" int daop_die_probe(const uint32_t* d_buf, int32_t nlines, int32_t stride_words,
+                              int32_t grid, uint32_t* d_lat, int32_t* d_smid,
+                              daop_stream_t stream) {
+  // nlines = lines per SM; d_buf holds grid * nlines lines, d_lat grid x nlines
+  if (nlines <= 0 || stride_words <= 0 || grid <= 0) {
+    set_error("die_probe: invalid arguments");
+    return DAOP_ERR_SHAPE;
+  }
+  const int smem = 120 * 1024;
+  DAOP_CUDA(cudaFuncSetAttribute(die_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
+  for (int phase = 0; phase < 2; ++phase)
+    die_probe_kernel<<<grid, 32, smem, as_stream(stream)>>>(d_buf, nlines, stride_words, 0, phase,
+                                                            0u, d_lat, d_smid);
+  DAOP_CHECK_LAUNCH("die_probe");
+  return DAOP_OK;
+}
+
+namespace {
+// Otsu threshold of the first-access latencies (fast: the line was in the
+// SM's die; slow: it crossed the fabric)
+uint32_t otsu(std::vector<uint32_t> v) {
+  std::sort(v.begin(), v.end());
+  const size_t n = v.size();
+  std::vector<double> pre(n + 1, 0.0);
+  for (size_t i = 0; i < n; ++i) pre[i + 1] = pre[i] + v[i];
+  double best = -1.0;
+  uint32_t thr = v[n / 2];
+  for (size_t i = n / 20; i < n - n / 20; ++i) {  // split after i (both classes >= 5 %)
+    if (v[i] == v[i - 1]) continue;
+    const double w0 = static_cast<double>(i) / n, w1 = 1.0 - w0;
+    const double m0 = pre[i] / i, m1 = (pre[n] - pre[i]) / (n - i);
+    const double b = w0 * w1 * (m0 - m1) * (m0 - m1);
+    if (b > best) {
+      best = b;
+      thr = v[i];
+    }
+  }
+  return thr;
+}
+
+struct DieMap {
+  int valid = 0;
+  std::vector<int32_t> die_of_sm;
+  std::vector<double> frac;  // slow fraction per probe block (diagnostic)
+};
+std::mutex g_die_mu;
+DieMap g_die[64];
+}  // namespace
+
+// SM -> die map of the current device (cached): die_of_sm[smid] for smid <
+// n_sm.  *n_die = 2 when the probe split the SMs into two halves, 1 when it
+// did not (all zeros written).
+extern "C" int daop_die_map(int32_t* die_of_sm, int32_t n_sm, int32_t* n_die) {
+  int dev = 0;
+  DAOP_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) {
+    set_error("die_map: device %d out of range", dev);
+    return DAOP_ERR_CONFIG;
+  }
+  std::lock_guard<std::mutex> lk(g_die_mu);
+  DieMap& m = g_die[dev];
+  if (!m.valid) {
+    const int sms = sm_count();
+    const int nlines = 64, stride = 160;  // lines per SM, 640 B apart
+    uint32_t* buf = nullptr;
+    uint32_t* lat = nullptr;
+    int32_t* smid = nullptr;
+    cudaError_t e = cudaMalloc(&buf, static_cast<size_t>(sms) * nlines * stride * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&lat, static_cast<size_t>(sms) * nlines * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&smid, static_cast<size_t>(sms) * 4);
+    if (e == cudaSuccess) e = cudaMemset(buf, 0, static_cast<size_t>(sms) * nlines * stride * 4);
+    int rc = DAOP_OK;
+    std::vector<uint32_t> h_lat(static_cast<size_t>(sms) * nlines);
+    std::vector<int32_t> h_smid(sms);
+    if (e == cudaSuccess) {
+      rc = daop_die_probe(buf, nlines, stride, sms, lat, smid, nullptr);
+      if (rc == DAOP_OK) e = cudaDeviceSynchronize();
+      if (rc == DAOP_OK && e == cudaSuccess)
+        e = cudaMemcpy(h_lat.data(), lat, h_lat.size() * 4, cudaMemcpyDeviceToHost);
+      if (rc == DAOP_OK && e == cudaSuccess)
+        e = cudaMemcpy(h_smid.data(), smid, h_smid.size() * 4, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(buf);
+    cudaFree(lat);
+    cudaFree(smid);
+    if (e != cudaSuccess) return cuda_fail(e, "die_map probe");
+    if (rc) return rc;
+    m.die_of_sm.assign(sms, 0);
+    // slow first accesses per SM: ~0 on ref's die, ~half on the other
+    const uint32_t thr = otsu(h_lat);
+    bool clean = true;
+    int count1 = 0;
+    std::vector<int> seen(sms, 0);
+    for (int b = 0; b < sms; ++b) {
+      int slow = 0;
+      for (int i = 0; i < nlines; ++i) slow += h_lat[static_cast<size_t>(b) * nlines + i] >= thr;
+      const double f = static_cast<double>(slow) / nlines;
+      // ref's die: ~0 (every line in the die's L2); the other die: 15-35 %
+      // (measured; the lines homed across the fabric, less the ones its
+      // neighbours' accesses already pulled over)
+      if (f > 0.03 && f < 0.08) clean = false;  // neither die clearly
+      const int s = h_smid[b];
+      if (s < 0 || s >= sms || seen[s]++) {
+        clean = false;
+        continue;
+      }
+      m.die_of_sm[s] = f >= 0.08 ? 1 : 0;
+      m.frac.push_back(f);
+    }
+    for (int s = 0; s < sms; ++s) count1 += m.die_of_sm[s];
+    for (int s = 0; s + 1 < sms; s += 2)  // the two SMs of a TPC share a die
+      if (m.die_of_sm[s] != m.die_of_sm[s + 1]) clean = false;
+    if (count1 < sms / 4 || count1 > sms - sms / 4) clean = false;
+    if (!clean) std::fill(m.die_of_sm.begin(), m.die_of_sm.end(), 0);
+    m.valid = clean ? 2 : 1;
+  }
+  *n_die = m.valid;
+  for (int s = 0; s < n_sm; ++s)
+    die_of_sm[s] = s < static_cast<int>(m.die_of_sm.size()) ? m.die_of_sm[s] : 0;
+  return DAOP_OK;
+}

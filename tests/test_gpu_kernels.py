@@ -388,6 +388,63 @@ def test_grouped_gemm_two_m_bitexact(P, d, ffn, E, T):
         assert torch.equal(outs[0][2], o[2])
 
 
+def _set_die_table(tab):
+    from paper_2501_10375_b200 import _lib
+    if tab is None:
+        _lib.call("daop_set_gemm_die_table", 0, 0)
+    elif isinstance(tab, str):  # "auto": the measured SM -> die map
+        _lib.call("daop_set_gemm_die_table", 0, -1)
+    else:
+        t = np.ascontiguousarray(tab, dtype=np.int32)
+        _lib.call("daop_set_gemm_die_table", t.ctypes.data, len(t))
+
+
+@pytest.mark.parametrize("mode", [0, 0x3000])
+@pytest.mark.parametrize("E,T", [(8, 6000), (5, 9000)])
+def test_per_die_gemm_schedule_bitexact(P, mode, E, T):
+    """The per-die tile schedule (each die's clusters stride over their share
+    of every expert's m-tiles) computes every tile exactly like the plain
+    schedule: act / y / out bit-identical for the measured map and for
+    arbitrary tables (all SMs on one die, alternating TPCs, random TPCs),
+    on the 512- and 256-row pair tiles and ragged experts."""
+    d, ffn = 512, 1024
+    n = torch.cuda.get_device_properties(0).multi_processor_count
+    tpc = np.arange(n) >> 1
+    rng = np.random.default_rng(E)
+    tables = [None, "auto", np.zeros(n), np.ones(n), tpc & 1, rng.integers(0, 2, n // 2 + 1)[tpc]]
+    outs = []
+    P[2].set_gemm_mode(mode)
+    try:
+        for tab in tables:
+            _set_die_table(tab)
+            _, _, _, _, pr, act, y, out = _gemm_case(P, d, ffn, E, T, 2)
+            off = pr["offsets"][-1].item()
+            outs.append((act[:off].clone(), y[:off].clone(), out.clone()))
+    finally:
+        P[2].set_gemm_mode(0)
+        _set_die_table("auto")
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert torch.equal(a, b)
+
+
+def test_die_map_is_tpc_consistent(P):
+    """daop_die_map: two dies on a B200, the two SMs of a TPC on the same
+    die, at least a quarter of the SMs on each (or one die when the probe
+    cannot separate them -- the GEMMs then use the plain schedule)."""
+    from paper_2501_10375_b200 import _lib
+    n = torch.cuda.get_device_properties(0).multi_processor_count
+    d = np.zeros(n, dtype=np.int32)
+    nd = np.zeros(1, dtype=np.int32)
+    _lib.call("daop_die_map", d.ctypes.data, n, nd.ctypes.data)
+    assert int(nd[0]) in (1, 2)
+    if nd[0] == 2:
+        assert np.array_equal(d[0::2], d[1::2])
+        assert n // 4 <= d.sum() <= n - n // 4
+    else:
+        assert not d.any()
+
+
 @pytest.mark.parametrize("d,ffn", [(512, 1024), (4096, 14336)])
 def test_decode_server_matches_host_call(P, d, ffn):
     """The persistent decode server answers each call exactly like the
