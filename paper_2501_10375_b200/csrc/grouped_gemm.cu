@@ -128,6 +128,10 @@ struct GemmParams {
   // re-reads stay in that die's L2 instead of crossing the die-to-die fabric.
   const int8_t* die_tab;
   unsigned* die_ctr;
+  // which dimension the dies split: 0 the m-tiles (raster 0 keeps A groups
+  // resident: each die holds its share of A), 1 the n-tiles (raster 1 keeps
+  // weight groups resident: each die holds its share of B and streams A)
+  int die_split_n;
 };
 
 __device__ __forceinline__ int64_t off_at(const GemmParams& p, int e) {
@@ -522,6 +526,8 @@ struct PairSmem {
   int32_t prefix[G_MAX_EXPERTS + 1];
   int32_t mt[G_MAX_EXPERTS];   // m-tiles of expert e this CTA's schedule covers
   int32_t mlo[G_MAX_EXPERTS];  // first of them (per-die schedule; else 0)
+  int32_t ntd[G_MAX_EXPERTS];  // n-tiles of expert e this CTA's schedule covers
+  int32_t nlo[G_MAX_EXPERTS];  // first of them
   int64_t off[G_MAX_EXPERTS + 1];
   int32_t tcl, ncl;            // this cluster's first tile and the tile stride
   int32_t dinfo[4];            // per-die schedule: die, rank, clusters on die 0 / 1
@@ -537,18 +543,19 @@ __device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, 
   e = 0;
   while (s.prefix[e + 1] <= t) ++e;
   const int u = t - s.prefix[e];
+  nt = s.ntd[e];  // (this CTA's schedule: the die's n-tiles of expert e)
   if (raster == 0) {
     const int grp = u / (G * nt);
     const int r = u - grp * G * nt;
     const int gm = min(G, s.mt[e] - grp * G);
     m = s.mlo[e] + grp * G + r % gm;
-    n = r / gm;
+    n = s.nlo[e] + r / gm;
   } else {
     const int mt = s.mt[e];
     const int grp = u / (G * mt);
     const int r = u - grp * G * mt;
     const int gn = min(G, nt - grp * G);
-    n = grp * G + r % gn;
+    n = s.nlo[e] + grp * G + r % gn;
     m = s.mlo[e] + r / gn;
   }
   return true;
@@ -648,21 +655,28 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
     int acc = 0;
     s.prefix[0] = 0;
     for (int e = 0; e <= E; ++e) s.off[e] = off_at(p, e);
-    // per-die: expert e's m-tiles [0, split_e) go to die 0, the rest to die 1,
-    // split_e from the running total so the remainders spread over experts
+    // per-die: expert e's m-tiles (or n-tiles, die_split_n) [0, split_e) go
+    // to die 0, the rest to die 1, split_e from the running total so the
+    // remainders spread over experts
     const int64_t n0 = per_die ? s.dinfo[2] : 1, nall = per_die ? s.dinfo[2] + s.dinfo[3] : 1;
     const int die = per_die ? s.dinfo[0] : 0;
+    const bool by_n = per_die && p.die_split_n;
+    const int nte = QUAD ? p.n_tiles / 2 : p.n_tiles;
     int64_t cum = 0;
     for (int e = 0; e < E; ++e) {
       const int64_t me = slot_at(p, e) >= 0 ? s.off[e + 1] - s.off[e] : 0;
       const int mte = static_cast<int>((me + C::M - 1) / C::M);
+      const int units = by_n ? (mte > 0 ? nte : 0) : mte;
       const int a = static_cast<int>((cum * n0 + nall / 2) / nall);
-      cum += mte;
+      cum += units;
       const int b = static_cast<int>((cum * n0 + nall / 2) / nall);
-      const int split = per_die ? b - a : mte;  // die 0's share of this expert
-      s.mlo[e] = die == 0 ? 0 : split;
-      s.mt[e] = die == 0 ? split : mte - split;
-      acc += s.mt[e] * (QUAD ? p.n_tiles / 2 : p.n_tiles);
+      const int split = per_die ? b - a : units;  // die 0's share of this expert
+      const int lo = die == 0 ? 0 : split, cnt = die == 0 ? split : units - split;
+      s.mlo[e] = by_n ? 0 : lo;
+      s.mt[e] = by_n ? (cnt > 0 ? mte : 0) : cnt;
+      s.nlo[e] = by_n ? lo : 0;
+      s.ntd[e] = by_n ? cnt : nte;
+      acc += s.mt[e] * s.ntd[e];
       s.prefix[e + 1] = acc;
     }
     s.tcl = per_die ? s.dinfo[1] : cluster;
@@ -900,7 +914,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
         const int row_in_tile = rank * 128 + q * 32 + lane;
         const bool valid = static_cast<int64_t>(m) * C::M + row_in_tile < me;
         const int64_t grow = s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile;
-        if ((p.demote & 1) && p.raster == 0 && n == nt - 1 && valid)  // A m-tile done
+        if ((p.demote & 1) && p.raster == 0 && n == s.nlo[e] + s.ntd[e] - 1 && valid)  // A m-tile done
           l2_demote_range(p.a_ptr + grow * p.a_ld, p.a_ld * 2);
         if ((p.demote & 2) && p.raster == 1 && m == s.mlo[e] + s.mt[e] - 1) {  // B n-tile done
           const int brow = n * p.b_tile_rows + (rank == 0 ? 0 : p.b_half2) + q * 32 + lane;
@@ -1100,6 +1114,7 @@ static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
     pp.raster = 0;
     pp.group_m = p.group_m > C::M / 128 ? p.group_m / (C::M / 128) : 1;
   }
+  pp.die_split_n = pp.raster == 1;
   kern<<<CL * clusters, C::THREADS, smem, st>>>(ta, tb, pp);
   DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
   return DAOP_OK;
