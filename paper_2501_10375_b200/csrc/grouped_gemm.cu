@@ -132,6 +132,7 @@ struct GemmParams {
   // resident: each die holds its share of A), 1 the n-tiles (raster 1 keeps
   // weight groups resident: each die holds its share of B and streams A)
   int die_split_n;
+  int no_stage;  // tuning: epilogue stores straight from the TMEM row layout (mode bit 19)
 };
 
 __device__ __forceinline__ int64_t off_at(const GemmParams& p, int e) {
@@ -514,6 +515,12 @@ struct PairCfg {
   static constexpr int EPI_WARPS = TWO_M ? EW : 4;
   static constexpr int GROUPS_PER_HALF = TWO_M ? EW / 8 : 1;  // warps per (quarter, half)
   static constexpr int THREADS = (2 + EPI_WARPS) * 32;
+  // epilogue stores staged through a 2 KB shared buffer per warp (32 rows x
+  // 64 B) so each store instruction writes 8 rows x 64 contiguous bytes
+  // instead of 32 rows x 16 B (TMEM gives a thread one row); the 16-warp
+  // variant has no shared memory left for it
+  static constexpr bool STAGE_EPI = EPI_WARPS <= 8;
+  static constexpr int STAGE_EPI_BYTES = STAGE_EPI ? EPI_WARPS * 2048 : 0;
 };
 
 
@@ -561,6 +568,23 @@ __device__ __forceinline__ bool map_tile_pair(const PairSmem& s, int E, int nt, 
   return true;
 }
 
+// Warp-staged epilogue stores.  After tcgen05.ld.32x32b a lane holds one
+// row; written straight out, every store instruction touches 32 rows x 16 B.
+// Instead each lane parks 64 B of its row in the warp's 2 KB buffer (16-byte
+// chunks XOR-swizzled by the row: conflict-free both ways) and the warp
+// writes them back as 4 rounds of 8 rows x 64 contiguous bytes.
+__device__ __forceinline__ uint32_t stg_off(int row, int chunk) {
+  return static_cast<uint32_t>(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4));
+}
+__device__ __forceinline__ void stg_put(uint8_t* stg, int lane, const uint4 (&v)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) *reinterpret_cast<uint4*>(stg + stg_off(lane, j)) = v[j];
+}
+// round r: lane -> (row r * 8 + lane / 4, chunk lane % 4)
+__device__ __forceinline__ uint4 stg_get(const uint8_t* stg, int r, int lane) {
+  return *reinterpret_cast<const uint4*>(stg + stg_off(r * 8 + (lane >> 2), lane & 3));
+}
+
 // split-K decode of a tile's n index (GemmParams::ksplit)
 __device__ __forceinline__ void split_tile(const GemmParams& p, int n_eff, int& n, int& ks, int& kb0,
                                            int& kb1) {
@@ -597,6 +621,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
   const uint32_t base_u32 = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
   PairSmem& s = *reinterpret_cast<PairSmem*>(tiles + C::STAGES * C::STAGE_BYTES);
+  uint8_t* stage_epi = tiles + C::STAGES * C::STAGE_BYTES + (sizeof(PairSmem) + 127) / 128 * 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   const uint32_t rank = crank & 1;            // rank within the CTA pair
@@ -852,7 +877,50 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
       const int64_t grow = s.off[e] + static_cast<int64_t>(m) * C::M + row_in_tile;
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * GB_N +
                           half * GB_N;
+      // staged stores: rows row0 .. row0 + 31 of the tile (this warp's lane
+      // quarter); lane L writes row row0 + r * 8 + L / 4, bytes (L % 4) * 16
+      const int64_t row0g = s.off[e] + static_cast<int64_t>(m) * C::M + half * 256 + rank * 128 + q * 32;
+      const int64_t rows_left = me - (static_cast<int64_t>(m) * C::M + half * 256 + rank * 128 + q * 32);
+      uint8_t* stg = stage_epi + (warp - 2) * 2048;
+      const bool staged = C::STAGE_EPI && !p.no_stage && p.row_dst == nullptr && p.comb_cnt == nullptr;
       if constexpr (SWIGLU) {
+        if (staged) {
+          uint16_t* outb = static_cast<uint16_t*>(p.out) + n * 128;
+#pragma unroll 1
+          for (int c = 0; c < 128 && !(p.exp & 1); c += 32) {
+            uint32_t g[32], u[32];
+            tmem_ld32(tb + c, g);
+            tmem_ld32(tb + 128 + c, u);
+            tmem_ld_wait();
+            uint4 pk[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint32_t w[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int x = 8 * i + 2 * j;
+                const float h0 = silu_fast(__uint_as_float(g[x])) * __uint_as_float(u[x]);
+                const float h1 = silu_fast(__uint_as_float(g[x + 1])) * __uint_as_float(u[x + 1]);
+                w[j] = static_cast<uint32_t>(f32_to_bf16_bits(h0)) |
+                       (static_cast<uint32_t>(f32_to_bf16_bits(h1)) << 16);
+              }
+              pk[i] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            __syncwarp();  // the previous chunk's reads of the buffer are done
+            stg_put(stg, lane, pk);
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int row = r * 8 + (lane >> 2);
+              if (row < rows_left) {
+                uint4* o = reinterpret_cast<uint4*>(outb + (row0g + row) * p.out_ld + c) + (lane & 3);
+                const uint4 v = stg_get(stg, r, lane);
+                if (p.store_cs) __stcs(o, v);
+                else *o = v;
+              }
+            }
+          }
+        } else {
         uint16_t* out = static_cast<uint16_t*>(p.out) + grow * p.out_ld + n * 128;
 #pragma unroll 1
         for (int c = sub * (128 / C::GROUPS_PER_HALF);
@@ -878,6 +946,49 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
                                           packed[4 * i + 3]);
               if (p.store_cs) __stcs(o + i, pk);
               else o[i] = pk;
+            }
+          }
+        }
+        }
+      } else if (staged) {
+        // fp32 y (+ the residual): 32 accumulator columns = two 64-byte halves
+        float* outf = static_cast<float*>(p.out) + ks * p.part_stride + n * GB_N;
+        const float* resid = p.ksplit > 1 ? nullptr : p.resid;
+#pragma unroll 1
+        for (int c = sub * (GB_N / C::GROUPS_PER_HALF);
+             c < (sub + 1) * (GB_N / C::GROUPS_PER_HALF) && !(p.exp & 1); c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tb + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint4 pk[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              pk[i] = make_uint4(v[16 * hh + 4 * i], v[16 * hh + 4 * i + 1], v[16 * hh + 4 * i + 2],
+                                 v[16 * hh + 4 * i + 3]);
+            __syncwarp();
+            stg_put(stg, lane, pk);
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int row = r * 8 + (lane >> 2);
+              if (row < rows_left) {
+                const int64_t off = (row0g + row) * p.out_ld + c + 16 * hh + 4 * (lane & 3);
+                const uint4 u4 = stg_get(stg, r, lane);
+                float4 a = make_float4(__uint_as_float(u4.x), __uint_as_float(u4.y),
+                                       __uint_as_float(u4.z), __uint_as_float(u4.w));
+                if (resid) {
+                  const float4 b = *reinterpret_cast<const float4*>(resid + n * GB_N + off);
+                  a.x += b.x;
+                  a.y += b.y;
+                  a.z += b.z;
+                  a.w += b.w;
+                }
+                float4* o = reinterpret_cast<float4*>(outf + off);
+                if (p.store_cs) __stcs(o, a);
+                else *o = a;
+              }
             }
           }
         }
@@ -954,6 +1065,7 @@ static int g_gemm_dense_skinny = 1;  // tuning: small-M dense GEMMs on the skinn
 static int g_gemm_epi16 = 0;  // tuning: 16 epilogue warps for the 512-row pair tile
 static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
 static int g_gemm_splitk = 1;
+static int g_gemm_nostage = 0;  // tuning: unstaged epilogue stores (mode bit 19)
 static int g_gemm_exp = 0;  // EXPERIMENT bits (GemmParams::exp)
 static int g_gemm_quad = 0;  // tuning: 4-CTA multicast clusters for the 512-row pair tile (mode bit 18)  // tuning: split-K for prompt-sized dense projections (_ws entry)
 
@@ -1047,9 +1159,11 @@ static int max_active_clusters(const void* kern, int cl, int threads, size_t sme
   return n < want ? n : want;
 }
 
-template <bool TWO_M>
+template <bool TWO_M, int EW = 8>
 static size_t pair_smem_bytes() {
-  return 1024 + PairCfg<TWO_M>::STAGES * PairCfg<TWO_M>::STAGE_BYTES + sizeof(PairSmem);
+  using C = PairCfg<TWO_M, EW>;
+  return 1024 + C::STAGES * C::STAGE_BYTES + (sizeof(PairSmem) + 127) / 128 * 128 +
+         C::STAGE_EPI_BYTES;
 }
 
 template <bool SWIGLU, bool TWO_M, int EW, bool QUAD = false>
@@ -1057,7 +1171,7 @@ static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
                           int64_t rows_total, cudaStream_t st) {
   using C = PairCfg<TWO_M, EW>;
   constexpr int CL = QUAD ? 4 : 2;
-  const size_t smem = pair_smem_bytes<TWO_M>();
+  const size_t smem = pair_smem_bytes<TWO_M, EW>();
   auto kern = grouped_gemm_pair_kernel<SWIGLU, TWO_M, EW, QUAD>;
   DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
@@ -1107,6 +1221,7 @@ static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   }
   pp.store_cs = g_gemm_store_cs;
   pp.exp = g_gemm_exp;
+  pp.no_stage = g_gemm_nostage;
   if (p.group_m < 0) {  // negative group = n-grouped raster of |group| weight tiles
     pp.raster = 1;
     pp.group_m = QUAD ? (-p.group_m > 1 ? -p.group_m / 2 : 1) : -p.group_m;  // (QUAD: n-pairs)
@@ -1269,6 +1384,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_splitk = !((mode >> 17) & 1);
   g_gemm_exp = (mode >> 20) & 7;
   g_gemm_quad = (mode >> 18) & 1;
+  g_gemm_nostage = (mode >> 19) & 1;
   return DAOP_OK;
 }
 

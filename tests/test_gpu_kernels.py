@@ -372,9 +372,10 @@ def test_decode_and_router_nan_input_selects_valid_ids(P):
 def test_grouped_gemm_two_m_bitexact(P, d, ffn, E, T):
     """The 512-row pair tile (two M=256 MMAs sharing B) accumulates every
     output element in the same K order as the 256-row tile: bit-identical;
-    so do the 16-epilogue-warp and the 4-CTA multicast (QUAD) variants."""
+    so do the 16-epilogue-warp and the 4-CTA multicast (QUAD) variants and the
+    unstaged epilogue stores (mode bit 19)."""
     outs = []
-    for mode in (0, 0x3000, 0x10000, 1 << 18):
+    for mode in (0, 0x3000, 0x10000, 1 << 18, 1 << 19, 0x3000 | 1 << 19):
         P[2].set_gemm_mode(mode)
         try:
             _, _, _, _, pr, act, y, out = _gemm_case(P, d, ffn, E, T, 2)
