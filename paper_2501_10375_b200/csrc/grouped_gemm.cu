@@ -882,7 +882,9 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
       const int64_t row0g = s.off[e] + static_cast<int64_t>(m) * C::M + half * 256 + rank * 128 + q * 32;
       const int64_t rows_left = me - (static_cast<int64_t>(m) * C::M + half * 256 + rank * 128 + q * 32);
       uint8_t* stg = stage_epi + (warp - 2) * 2048;
-      const bool staged = C::STAGE_EPI && !p.no_stage && p.row_dst == nullptr && p.comb_cnt == nullptr;
+      // (SwiGLU never has row_dst; the fp32 path stages EP row returns too)
+      const bool staged = C::STAGE_EPI && !p.no_stage && p.comb_cnt == nullptr &&
+                          (!SWIGLU || p.row_dst == nullptr);
       if constexpr (SWIGLU) {
         if (staged) {
           uint16_t* outb = static_cast<uint16_t*>(p.out) + n * 128;
@@ -985,7 +987,11 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
                   a.z += b.z;
                   a.w += b.w;
                 }
-                float4* o = reinterpret_cast<float4*>(outf + off);
+                // EP return: the row's slot on its source rank (peer memory)
+                float4* o = p.row_dst
+                                ? reinterpret_cast<float4*>(reinterpret_cast<float*>(p.row_dst[row0g + row]) +
+                                                            n * GB_N + c + 16 * hh + 4 * (lane & 3))
+                                : reinterpret_cast<float4*>(outf + off);
                 if (p.store_cs) __stcs(o, a);
                 else *o = a;
               }
