@@ -181,11 +181,14 @@ class SlowSplit:
 
 
 def host_expert_ffn(pool: HostExpertPool, layer: int, expert: int, x_bf16: np.ndarray,
-                    threads: int = 0) -> np.ndarray:
-    """Slow-tier execution of one expert on (n, d) bf16 inputs -> (n, d) fp32."""
+                    threads: int = 0, out: np.ndarray = None) -> np.ndarray:
+    """Slow-tier execution of one expert on (n, d) bf16 inputs -> (n, d) fp32
+    (into `out`, a C-contiguous (n, d) fp32 array, when given)."""
     x = np.ascontiguousarray(x_bf16, dtype=np.uint16)
     n = x.shape[0]
-    y = np.empty((n, pool.d), dtype=np.float32)
+    y = np.empty((n, pool.d), dtype=np.float32) if out is None else out
+    if y.shape != (n, pool.d) or y.dtype != np.float32 or not y.flags.c_contiguous:
+        raise ShapeMismatchError(f"host expert output must be C-contiguous float32 {(n, pool.d)}")
     w1, w3, w2 = pool.ptrs(layer, expert)
     _lib.call("daop_host_expert_ffn", x.ctypes.data, n, w1, w3, w2, pool.d, pool.ffn,
               y.ctypes.data, 0, threads)
@@ -245,6 +248,11 @@ class DaopEngine:
         self._slow_split = None
         self.host_ms = 0.0  # decode: wall time inside host-tier expert calls
         self.prefill_host_ms = 0.0  # prefill: the same for the slow experts' token batches
+        self.prefill_trace = None  # a list: prefill appends each layer's wall-clock timeline
+        self._ys_pin = None  # pinned staging of the slow experts' prefill outputs
+        # A/B switch: wait for a layer's migrations before its host tier starts
+        # (what a pageable index copy used to do implicitly); off = overlapped
+        self.prefill_serial_migrations = False
         self._host_exec = None  # one thread feeding the host tier (decode pre-calculation)
         self._host_ms_lock = threading.Lock()
         self.model = MoEModel(shape, d_model, d_ff, seed=seed, device=device,
@@ -350,8 +358,10 @@ class DaopEngine:
             # length (no per-layer Python / launch gaps)
             h, hist, p_host = self._prefill_resident_graph(h)
             L = 0  # the layer loop below has nothing left to do
+        tr = self.prefill_trace  # optional per-layer wall-clock timeline (list)
         for l in range(L):
             nvtx_push(f"prefill/L{l}")
+            tl = {"layer": l, "t0": time.perf_counter()} if tr is not None else None
             with nvtx_range("attention"):
                 h = self._non_moe_prefill(h, l)
             nxt = m.gate[l + 1] if l + 1 < L else None
@@ -365,6 +375,8 @@ class DaopEngine:
                 # only DAOP reallocates (experiment.py:158-163): Alg. 1 for this
                 # layer right after its gate (placement.py:188-237)
                 counts_l = hist[0, l].to(torch.int64).cpu().numpy()
+                if tl is not None:
+                    tl["hist_synced"] = time.perf_counter()
                 one = ExpertPlacement(ModelShape(1, E, k), [self.placement0.on_fast[l]],
                                       self.placement0.slot_budget)
                 after, ev1 = allocate_for_sequence(one, counts_l[None, :], self.swap_in_out)
@@ -372,15 +384,21 @@ class DaopEngine:
                        for e in ev1]
                 swaps_all.extend(evs)
                 new_sets[l] = set(after.on_fast[0])
+                if tl is not None:
+                    tl["alg1_done"] = time.perf_counter()
                 if evs:
                     mig_start, mig_evs = self._apply_swaps(l, evs)
                     swapped_in = [e.swapped_in for e in evs]
+                if tl is not None:
+                    tl["swaps_queued"] = time.perf_counter()
             pr = ops.permute(r["topk_idx"], E, r["x"])
             resident = m.resident_mask()[l]  # post-swap residence
             slow = []
             if not resident.all():  # only then does the host need the expert offsets
                 off = pr["offsets"].cpu().numpy()
                 slow = [e for e in range(E) if off[e + 1] > off[e] and not resident[e]]
+                if tl is not None:
+                    tl["offsets_synced"] = time.perf_counter()
             # slow experts' rows -> pinned host memory BEFORE the GEMMs are queued,
             # so the host tier runs while the GPU computes
             xs_host = {}
@@ -390,13 +408,23 @@ class DaopEngine:
                 xs_host[e].copy_(pr["x_perm"][a_:b_], non_blocking=True)
             x_ready = torch.cuda.Event()
             x_ready.record()
+            if tl is not None:
+                tl["xs_queued"] = time.perf_counter()
             # experts at the post-swap residence: first every expert whose weights
             # are already in HBM, then the swapped-in ones, each after its copy
             # lands (simulator.py:457-471)
             slot_now = m.slot_of[l]
             if swapped_in:
-                slot_now = slot_now.clone()
-                slot_now[swapped_in] = -1
+                # slot tables of the resident and the swapped-in experts, built on
+                # the device from a pinned mask (async): indexing a CUDA tensor with
+                # a Python list would copy the index from pageable memory, which
+                # blocks the host until the stream drains -- i.e. until this
+                # layer's migrations landed, serialising them with the host tier
+                mask = torch.zeros(E, dtype=torch.bool, pin_memory=True)
+                mask[swapped_in] = True
+                mask = mask.to(m.device, non_blocking=True)
+                slot_now = torch.where(mask, -1, m.slot_of[l])
+                slot_mig = torch.where(mask, m.slot_of[l], -1)
             rows = pr["x_perm"].shape[0]
             act = torch.empty((rows, m.ffn), dtype=torch.bfloat16, device=m.device)
             y = torch.empty((rows, d), dtype=torch.float32, device=m.device)
@@ -414,38 +442,57 @@ class DaopEngine:
                 mig_timing.append([mig_start, mig_evs[-1], g1, None])
                 for ev in mig_evs:
                     torch.cuda.current_stream().wait_event(ev)
-                slot_mig = torch.full_like(slot_now, -1)
-                slot_mig[swapped_in] = m.slot_of[l][swapped_in]
                 up(pr["x_perm"], pr["offsets"], slot_mig, m.slab, m.n_slots, m.slot_elems, d,
                    m.ffn, out=act)
                 down(act, pr["offsets"], slot_mig, m.slab, m.n_slots, m.slot_elems, d, m.ffn,
                      out=y)
+            if swapped_in and self.prefill_serial_migrations:  # A/B switch: the r02 behaviour
+                for ev in mig_evs:
+                    ev.synchronize()
+            if tl is not None:
+                tl["gemms_queued"] = time.perf_counter()
             if slow:
                 nvtx_push("experts/host_tier")
                 x_ready.synchronize()
+                if tl is not None:
+                    tl["host_start"] = time.perf_counter()
                 # the host tier's results go up on their own stream, so the GPU
                 # clock records when the slow experts finished (for the hidden-
                 # migration measurement) independently of the GEMM queue
+                # results land in pinned memory and go up asynchronously: a
+                # pageable copy would block the host tier behind the H2D copy
+                # engine's queue (this layer's migrations).  The staging rows are
+                # reused by the next layer only after this layer's combine
+                # waited for them (the next x_ready is recorded behind it).
+                if self._ys_pin is None or self._ys_pin.shape[0] < rows:
+                    self._ys_pin = torch.empty((rows, d), dtype=torch.float32, pin_memory=True)
+                ys_np = self._ys_pin.numpy()
                 with torch.cuda.stream(self.h2d_stream):
                     for e in slow:
                         a_, b_ = int(off[e]), int(off[e + 1])
                         xs = xs_host[e].view(torch.int16).numpy().view(np.uint16)
                         th0 = time.perf_counter()
-                        ys = host_expert_ffn(self.pool, l, e, xs, self.host_threads)
+                        host_expert_ffn(self.pool, l, e, xs, self.host_threads, out=ys_np[a_:b_])
                         self.prefill_host_ms += 1e3 * (time.perf_counter() - th0)
-                        y[a_:b_].copy_(torch.from_numpy(ys), non_blocking=False)
+                        y[a_:b_].copy_(self._ys_pin[a_:b_], non_blocking=True)
                         slow_execs += 1
                     hev = torch.cuda.Event(enable_timing=True)
                     hev.record(self.h2d_stream)
                 torch.cuda.current_stream().wait_event(hev)
                 if swapped_in:
                     mig_timing[-1][3] = hev
+                if tl is not None:
+                    tl["host_end"] = time.perf_counter()
                 nvtx_pop()
             out = ops.combine(h, y, pr["inv"], r["topk_w"])
             p_host[0, l].copy_(r["p"], non_blocking=True)
             if nxt is not None:
                 p_host[1, l].copy_(r["p_pred"], non_blocking=True)
             h = out
+            if tl is not None:
+                tl.update(t1=time.perf_counter(), swaps=len(swapped_in), slow=len(slow),
+                          slow_rows=[int(off[e + 1] - off[e]) for e in slow])
+                tr.append(tl)
             nvtx_pop()
         torch.cuda.synchronize()
         true_sc = np.ascontiguousarray(p_host[0].numpy().transpose(1, 0, 2), dtype=np.float64)
