@@ -1069,7 +1069,12 @@ static int g_gemm_two_m = 3;
 static int g_gemm_store_cs = 0;  // epilogue streaming stores (tuning)
 static int g_gemm_dense_skinny = 1;  // tuning: small-M dense GEMMs on the skinny kernel
 static int g_gemm_epi16 = 0;  // tuning: 16 epilogue warps for the 512-row pair tile
-static int g_gemm_persist_off = 0;  // tuning: no persisting L2 set-aside
+// persisting L2 set-aside for the evict_last operand loads: OFF by default.
+// With it on (mode bit 11), the GEMMs' persisting lines stay in L2 after the
+// GEMM and the HBM-bound kernels that follow slow down ~2x (router 160 -> 299
+// us, permutation 157 -> 331, combine 328 -> 568 at configs[3]); the GEMMs do
+// not gain from it (scripts/persist_ab.py: layer 17.70 -> 17.16 ms off)
+static int g_gemm_persist_off = 1;
 static int g_gemm_splitk = 1;
 static int g_gemm_nostage = 0;  // tuning: unstaged epilogue stores (mode bit 19)
 static int g_gemm_exp = 0;  // EXPERIMENT bits (GemmParams::exp)
@@ -1382,7 +1387,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_mode = mode & 15;
   g_gemm_policy = ((mode >> 4) & 15) ? ((mode >> 4) & 15) : -1;
   g_gemm_demote = (mode >> 8) & 7;
-  g_gemm_persist_off = (mode >> 11) & 1;
+  g_gemm_persist_off = !((mode >> 11) & 1);  // bit 11: persisting set-aside ON (tuning)
   g_gemm_two_m = ((mode >> 12) & 3) ^ 3;  // mode bits flip the default (tuning)
   g_gemm_store_cs = (mode >> 14) & 1;
   g_gemm_dense_skinny = !((mode >> 15) & 1);

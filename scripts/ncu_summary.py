@@ -15,6 +15,7 @@ KEYS = [
     "lts__t_bytes.sum", "lts__t_sector_hit_rate.pct", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
     "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg.per_second",
+    "lts__t_sectors_srcunit_ltcfabric.sum",
 ]
 
 
