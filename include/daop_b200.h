@@ -453,6 +453,10 @@ int daop_server_stop(void* handle);
 /* profiling aid: per-call GPU timestamps of servers started afterwards
  * (d_buf [cap][4] u64 zeroed: doorbell seen, input released, body done) */
 int daop_server_trace(uint64_t* d_buf, int32_t cap);
+/* decode attention: attention core + O projection as two launches (0, the
+ * default) or ONE cooperative launch whose Wo stream overlaps the attention
+ * core (1; 2: the stream waits for the split tasks' K / V) -- measured slower */
+int daop_set_attn_fused(int32_t fused);
 
 /* ------------------------------------------------ die topology (B200: two dies)
  * SM -> die map of the current device, measured once and cached (csrc/

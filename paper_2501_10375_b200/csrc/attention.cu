@@ -191,19 +191,32 @@ struct AttnArgs {
 
 constexpr int AT_SPLIT = 64;  // positions per CTA (one K tile + one V tile, 16 KB each)
 
-// CTA = (kv head g, split of AT_SPLIT positions), 256 threads.  The split's K
+// Shared-memory scratch of one attention split task
+struct SplitSmem {
+  __align__(128) uint16_t k_s[AT_SPLIT * AT_HD];
+  __align__(128) uint16_t v_s[AT_SPLIT * AT_HD];
+  float q_s[AT_MAX_GROUP][AT_HD];
+  float p_s[AT_MAX_GROUP][AT_SPLIT];
+  float ml_s[AT_MAX_GROUP][2];
+  uint64_t bar;
+  int last;
+};
+
+// One split task: kv head g, positions split * AT_SPLIT .. + AT_SPLIT - 1, on
+// 256 threads (tid 0..255) that synchronise with `sync()` (__syncthreads in
+// the standalone kernel, a named barrier in the fused one).  The split's K
 // and V rows (contiguous in the cache) arrive by two bulk copies while the
-// CTA applies RoPE to its group's q heads; scores: thread = (head, position);
-// P.V: thread = (head, 2 head dims).  The split's (m, l, acc) go to `part`.
-// The CTA whose split holds `pos` first appends the new k (RoPE) and v.
-__global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
-  __shared__ __align__(128) uint16_t k_s[AT_SPLIT * AT_HD];
-  __shared__ __align__(128) uint16_t v_s[AT_SPLIT * AT_HD];
-  __shared__ float q_s[AT_MAX_GROUP][AT_HD];
-  __shared__ float p_s[AT_MAX_GROUP][AT_SPLIT];
-  __shared__ float ml_s[AT_MAX_GROUP][2];
-  __shared__ uint64_t bar;
-  const int g = blockIdx.x, split = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+// threads apply RoPE to the group's q heads; scores: thread = (head,
+// position); P.V: thread = (head, 2 head dims).  The split's (m, l, acc) go to
+// `part`; the task whose split holds `pos` first appends the new k (RoPE) and
+// v.  The kv head's last split to finish merges all of them into o (fixed
+// split order) and returns true.
+template <class Sync>
+__device__ __forceinline__ bool attn_split_task(const AttnArgs& a, int g, int split, int used,
+                                                int tid, SplitSmem& S, Sync sync,
+                                                unsigned* loaded = nullptr) {
+  constexpr int NT = 256;
+  const int lane = tid & 31;
   const int group = a.n_heads / a.n_kv;
   const int q_dim = a.n_heads * AT_HD, kv_dim = a.n_kv * AT_HD;
   const int p0 = split * AT_SPLIT;
@@ -212,29 +225,31 @@ __global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
   uint16_t* vc = a.v_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
   const bool owns_new = a.pos >= p0 && a.pos < p0 + AT_SPLIT;
   const int n_load = owns_new ? n - 1 : n;  // rows already in the cache
+  uint16_t* k_s = S.k_s;
+  uint16_t* v_s = S.v_s;
   if (tid == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&S.bar, 1);
     fence_mbar_init();
     if (n_load > 0) {
-      mbar_arrive_expect_tx(&bar, 2 * n_load * AT_HD * 2);
-      bulk_g2s_plain(k_s, kc + static_cast<int64_t>(p0) * AT_HD, n_load * AT_HD * 2, &bar);
-      bulk_g2s_plain(v_s, vc + static_cast<int64_t>(p0) * AT_HD, n_load * AT_HD * 2, &bar);
+      mbar_arrive_expect_tx(&S.bar, 2 * n_load * AT_HD * 2);
+      bulk_g2s_plain(k_s, kc + static_cast<int64_t>(p0) * AT_HD, n_load * AT_HD * 2, &S.bar);
+      bulk_g2s_plain(v_s, vc + static_cast<int64_t>(p0) * AT_HD, n_load * AT_HD * 2, &S.bar);
     } else {
-      mbar_arrive_expect_tx(&bar, 0);
+      mbar_arrive_expect_tx(&S.bar, 0);
     }
   }
   // q of the group's heads with RoPE
-  for (int i = tid; i < group * (AT_HD / 2); i += blockDim.x) {
+  for (int i = tid; i < group * (AT_HD / 2); i += NT) {
     const int hh = i / (AT_HD / 2), j = i - hh * (AT_HD / 2);
     float x0 = a.qkv[(g * group + hh) * AT_HD + j];
     float x1 = a.qkv[(g * group + hh) * AT_HD + j + AT_HD / 2];
     rope_pair(x0, x1, j, a.pos, a.theta);
-    q_s[hh][j] = x0;
-    q_s[hh][j + AT_HD / 2] = x1;
+    S.q_s[hh][j] = x0;
+    S.q_s[hh][j + AT_HD / 2] = x1;
   }
-  if (owns_new) {  // new k (RoPE) and v -> the cache and this CTA's tile
+  if (owns_new) {  // new k (RoPE) and v -> the cache and this task's tile
     const int r = a.pos - p0;
-    for (int j = tid; j < AT_HD / 2; j += blockDim.x) {
+    for (int j = tid; j < AT_HD / 2; j += NT) {
       float k0 = a.qkv[q_dim + g * AT_HD + j];
       float k1 = a.qkv[q_dim + g * AT_HD + j + AT_HD / 2];
       rope_pair(k0, k1, j, a.pos, a.theta);
@@ -244,16 +259,17 @@ __global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
       k_s[r * AT_HD + j] = b0;
       k_s[r * AT_HD + j + AT_HD / 2] = b1;
     }
-    for (int j = tid; j < AT_HD; j += blockDim.x) {
+    for (int j = tid; j < AT_HD; j += NT) {
       const uint16_t bv = f32_to_bf16_bits(a.qkv[q_dim + kv_dim + g * AT_HD + j]);
       vc[static_cast<int64_t>(a.pos) * AT_HD + j] = bv;
       v_s[r * AT_HD + j] = bv;
     }
   }
-  __syncthreads();
-  mbar_wait(&bar, 0);
+  sync();
+  mbar_wait(&S.bar, 0);
+  if (loaded && tid == 0) atomicAdd(loaded, 1u);  // fused kernel: this task's K / V landed
   // scores: thread = (head hh, position i); group * AT_SPLIT <= 512 -> two passes max
-  for (int t = tid; t < group * AT_SPLIT; t += blockDim.x) {
+  for (int t = tid; t < group * AT_SPLIT; t += NT) {
     const int hh = t / AT_SPLIT, i = t - hh * AT_SPLIT;
     float sc = -INFINITY;
     if (i < n) {
@@ -263,106 +279,115 @@ __global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
       for (int c = 0; c < AT_HD / 8; ++c) {
         const uint4 kv = kr[(c + i) & (AT_HD / 8 - 1)];  // rotated start: no bank conflicts
         const int cc = ((c + i) & (AT_HD / 8 - 1)) * 8;
-        acc = fmaf(q_s[hh][cc + 0], bf16lo(kv.x), acc);
-        acc = fmaf(q_s[hh][cc + 1], bf16hi(kv.x), acc);
-        acc = fmaf(q_s[hh][cc + 2], bf16lo(kv.y), acc);
-        acc = fmaf(q_s[hh][cc + 3], bf16hi(kv.y), acc);
-        acc = fmaf(q_s[hh][cc + 4], bf16lo(kv.z), acc);
-        acc = fmaf(q_s[hh][cc + 5], bf16hi(kv.z), acc);
-        acc = fmaf(q_s[hh][cc + 6], bf16lo(kv.w), acc);
-        acc = fmaf(q_s[hh][cc + 7], bf16hi(kv.w), acc);
+        acc = fmaf(S.q_s[hh][cc + 0], bf16lo(kv.x), acc);
+        acc = fmaf(S.q_s[hh][cc + 1], bf16hi(kv.x), acc);
+        acc = fmaf(S.q_s[hh][cc + 2], bf16lo(kv.y), acc);
+        acc = fmaf(S.q_s[hh][cc + 3], bf16hi(kv.y), acc);
+        acc = fmaf(S.q_s[hh][cc + 4], bf16lo(kv.z), acc);
+        acc = fmaf(S.q_s[hh][cc + 5], bf16hi(kv.z), acc);
+        acc = fmaf(S.q_s[hh][cc + 6], bf16lo(kv.w), acc);
+        acc = fmaf(S.q_s[hh][cc + 7], bf16hi(kv.w), acc);
       }
       sc = acc * a.scale;
     }
-    p_s[hh][i] = sc;
+    S.p_s[hh][i] = sc;
   }
-  __syncthreads();
+  sync();
   // per head: max and exp-sum over the split (one warp per head, fixed order)
   const int warp = tid >> 5;
-  for (int hh = warp; hh < group; hh += blockDim.x / 32) {
-    float mx = fmaxf(p_s[hh][lane], p_s[hh][lane + 32]);
+  for (int hh = warp; hh < group; hh += NT / 32) {
+    float mx = fmaxf(S.p_s[hh][lane], S.p_s[hh][lane + 32]);
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float e0 = lane < n ? expf(p_s[hh][lane] - mx) : 0.f;
-    const float e1 = lane + 32 < n ? expf(p_s[hh][lane + 32] - mx) : 0.f;
-    p_s[hh][lane] = e0;
-    p_s[hh][lane + 32] = e1;
+    const float e0 = lane < n ? expf(S.p_s[hh][lane] - mx) : 0.f;
+    const float e1 = lane + 32 < n ? expf(S.p_s[hh][lane + 32] - mx) : 0.f;
+    S.p_s[hh][lane] = e0;
+    S.p_s[hh][lane + 32] = e1;
     const float se = warp_sum(e0 + e1);
     if (lane == 0) {
-      ml_s[hh][0] = mx;
-      ml_s[hh][1] = se;
+      S.ml_s[hh][0] = mx;
+      S.ml_s[hh][1] = se;
     }
   }
-  __syncthreads();
+  sync();
   // P.V: thread = (head hh, dims 2c, 2c + 1)
-  for (int t = tid; t < group * (AT_HD / 2); t += blockDim.x) {
+  for (int t = tid; t < group * (AT_HD / 2); t += NT) {
     const int hh = t / (AT_HD / 2), c = t - hh * (AT_HD / 2);
     float a0 = 0.f, a1 = 0.f;
     for (int i = 0; i < n; ++i) {
       const uint32_t vv = *reinterpret_cast<const uint32_t*>(v_s + i * AT_HD + 2 * c);
-      a0 = fmaf(p_s[hh][i], bf16lo(vv), a0);
-      a1 = fmaf(p_s[hh][i], bf16hi(vv), a1);
+      a0 = fmaf(S.p_s[hh][i], bf16lo(vv), a0);
+      a1 = fmaf(S.p_s[hh][i], bf16hi(vv), a1);
     }
     float* pr = a.part + ((static_cast<int64_t>(g) * a.splits + split) * group + hh) * (2 + AT_HD);
     pr[2 + 2 * c] = a0;
     pr[2 + 2 * c + 1] = a1;
     if (c == 0) {
-      pr[0] = ml_s[hh][0];
-      pr[1] = ml_s[hh][1];
+      pr[0] = S.ml_s[hh][0];
+      pr[1] = S.ml_s[hh][1];
     }
   }
   // the kv head's last split to finish merges all of them (fixed split order)
   __threadfence();
-  __syncthreads();
-  __shared__ int last;
+  sync();
   if (tid == 0) {
-    last = atomicAdd(a.counter + g, 1u) == static_cast<unsigned>(gridDim.y) - 1;
-    if (last) a.counter[g] = 0;  // self-resetting for the next call
+    S.last = atomicAdd(a.counter + g, 1u) == static_cast<unsigned>(used) - 1;
+    if (S.last) a.counter[g] = 0;  // self-resetting for the next call
   }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const int used = gridDim.y;
-  for (int t = tid; t < group * (AT_HD / 2); t += blockDim.x) {
-    const int hh = t / (AT_HD / 2), c = t - hh * (AT_HD / 2);
-    const float* base = a.part + (static_cast<int64_t>(g) * a.splits * group + hh) * (2 + AT_HD);
-    const int64_t stride = static_cast<int64_t>(group) * (2 + AT_HD);
-    // the partials are read in batches of 8 splits with every load of a batch
-    // issued before the first use (one L2 round trip per batch, not per split)
-    constexpr int MB = 8;
-    float m = -INFINITY;
-    for (int s0 = 0; s0 < used; s0 += MB) {
-      float mv[MB];
+  sync();
+  const bool last = S.last;
+  if (last) {
+    __threadfence();
+    for (int t = tid; t < group * (AT_HD / 2); t += NT) {
+      const int hh = t / (AT_HD / 2), c = t - hh * (AT_HD / 2);
+      const float* base = a.part + (static_cast<int64_t>(g) * a.splits * group + hh) * (2 + AT_HD);
+      const int64_t stride = static_cast<int64_t>(group) * (2 + AT_HD);
+      // the partials are read in batches of 8 splits with every load of a batch
+      // issued before the first use (one L2 round trip per batch, not per split)
+      constexpr int MB = 8;
+      float m = -INFINITY;
+      for (int s0 = 0; s0 < used; s0 += MB) {
+        float mv[MB];
 #pragma unroll
-      for (int j = 0; j < MB; ++j) mv[j] = s0 + j < used ? __ldcg(base + (s0 + j) * stride) : -INFINITY;
+        for (int j = 0; j < MB; ++j) mv[j] = s0 + j < used ? __ldcg(base + (s0 + j) * stride) : -INFINITY;
 #pragma unroll
-      for (int j = 0; j < MB; ++j) m = fmaxf(m, mv[j]);
-    }
-    float l = 0.f, o0 = 0.f, o1 = 0.f;
-    for (int s0 = 0; s0 < used; s0 += MB) {
-      float mv[MB], lv[MB], a0[MB], a1[MB];
-#pragma unroll
-      for (int j = 0; j < MB; ++j) {
-        const bool ok = s0 + j < used;
-        const float* pr = base + (s0 + j) * stride;
-        mv[j] = ok ? __ldcg(pr) : -INFINITY;
-        lv[j] = ok ? __ldcg(pr + 1) : 0.f;
-        a0[j] = ok ? __ldcg(pr + 2 + 2 * c) : 0.f;
-        a1[j] = ok ? __ldcg(pr + 3 + 2 * c) : 0.f;
+        for (int j = 0; j < MB; ++j) m = fmaxf(m, mv[j]);
       }
+      float l = 0.f, o0 = 0.f, o1 = 0.f;
+      for (int s0 = 0; s0 < used; s0 += MB) {
+        float mv[MB], lv[MB], a0[MB], a1[MB];
 #pragma unroll
-      for (int j = 0; j < MB; ++j) {  // fixed split order, as before
-        if (s0 + j < used) {
-          const float cf = expf(mv[j] - m);
-          l = fmaf(lv[j], cf, l);
-          o0 = fmaf(a0[j], cf, o0);
-          o1 = fmaf(a1[j], cf, o1);
+        for (int j = 0; j < MB; ++j) {
+          const bool ok = s0 + j < used;
+          const float* pr = base + (s0 + j) * stride;
+          mv[j] = ok ? __ldcg(pr) : -INFINITY;
+          lv[j] = ok ? __ldcg(pr + 1) : 0.f;
+          a0[j] = ok ? __ldcg(pr + 2 + 2 * c) : 0.f;
+          a1[j] = ok ? __ldcg(pr + 3 + 2 * c) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < MB; ++j) {  // fixed split order, as before
+          if (s0 + j < used) {
+            const float cf = expf(mv[j] - m);
+            l = fmaf(lv[j], cf, l);
+            o0 = fmaf(a0[j], cf, o0);
+            o1 = fmaf(a1[j], cf, o1);
+          }
         }
       }
+      const int head = g * group + hh;
+      a.o[head * AT_HD + 2 * c] = f32_to_bf16_bits(o0 / l);
+      a.o[head * AT_HD + 2 * c + 1] = f32_to_bf16_bits(o1 / l);
     }
-    const int head = g * group + hh;
-    a.o[head * AT_HD + 2 * c] = f32_to_bf16_bits(o0 / l);
-    a.o[head * AT_HD + 2 * c + 1] = f32_to_bf16_bits(o1 / l);
   }
+  sync();  // the scratch (and S.bar) is reused by the next task
+  if (tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&S.bar)) : "memory");
+  return last;
+}
+
+// CTA = (kv head, split), 256 threads: attn_split_task
+__global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
+  __shared__ SplitSmem S;
+  attn_split_task(a, blockIdx.x, blockIdx.y, gridDim.y, threadIdx.x, S, [] { __syncthreads(); });
 }
 
 // h' = h + o . Wo^T  (rows of Wo are output dims; o bf16 (q_dim) in smem)
@@ -392,6 +417,98 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   asm volatile("bar.sync 1, %0;" ::"r"(AT_WARPS * 32));
   ring_consume(R, r0, n, q_dim, os, warp, lane,
                [&](int row, float v) { h_out[row] = h[row] + v; });
+}
+
+// Attention core + O projection in ONE cooperative launch (one CTA per SM):
+// every CTA's producer warp streams its Wo rows into the ring from the first
+// cycle (the weights do not depend on o); CTAs < n_kv * used first run the
+// attention split tasks on warps 0..7 (named barrier 2); the kv heads' last
+// splits merge o and count the head; then every CTA waits for all n_kv heads,
+// reads o and finishes the GEMV + residual as attn_oproj_kernel does.  The
+// Wo stream overlaps the latency-bound attention core instead of starting
+// after it.  sync[0] counts merged heads, sync[1] exits (the last CTA out
+// resets both).
+// attention core + O projection as two launches (default) or fused in one
+// cooperative launch (DAOP_ATTN_FUSED=1 / 2, daop_set_attn_fused: measured
+// slower -- 27.7-28.1 vs 25.3 us per attention layer at ctx 512, 36-37 vs 31
+// at ctx 2000, also with the Wo stream held back until the split tasks' K / V
+// landed (mode 2); DESIGN §6 tried table)
+static int g_attn_fused = -1;
+static int attn_fused_mode() {
+  if (g_attn_fused < 0) {
+    const char* v = getenv("DAOP_ATTN_FUSED");
+    g_attn_fused = v ? atoi(v) : 0;
+  }
+  return g_attn_fused;
+}
+
+struct CoreOprojArgs {
+  AttnArgs a;
+  const float* h;
+  const uint16_t* wo;
+  int d, q_dim, rows_per_cta, stages, used;
+  float* h_out;
+  unsigned* sync;  // [0] merged heads, [1] exits, [2] split tasks whose K / V landed
+  int delay;       // producer waits for the first wave's K / V (mode 2)
+};
+
+__global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1) attn_core_oproj_kernel(CoreOprojArgs c) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  RowRing R;
+  R.S = c.stages;
+  R.ring = smem;
+  uint4* os = reinterpret_cast<uint4*>(smem + static_cast<size_t>(c.stages) * c.q_dim * 2);
+  R.full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(os) + c.q_dim * 2);
+  R.empty = R.full + c.stages;
+  SplitSmem* S2 = reinterpret_cast<SplitSmem*>(
+      reinterpret_cast<uint8_t*>(R.empty + c.stages) +
+      ((128 - (reinterpret_cast<uintptr_t>(R.empty + c.stages) & 127)) & 127));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * c.rows_per_cta;
+  const int n = max(0, min(c.d, r0 + c.rows_per_cta) - r0);
+  const int n_kv = c.a.n_kv, ntasks = n_kv * c.used;
+  ring_init(R);
+  __syncthreads();
+  if (warp == AT_WARPS) {
+    if (lane == 0) {
+      // delayed stream (mode 2): start Wo once the first wave of split tasks
+      // has its K / V in shared memory, so their latency-critical loads do
+      // not queue behind 19 MB of weight traffic
+      if (c.delay) {
+        const unsigned wave = static_cast<unsigned>(min(ntasks, 2 * static_cast<int>(gridDim.x)));
+        while (ld_acquire_gpu(c.sync + 2) < wave) __nanosleep(128);
+      }
+      ring_produce(R, c.wo, r0, n, c.q_dim);
+    }
+    return;
+  }
+  // two task slots per CTA: warps 0-7 (barrier 2) and 8-15 (barrier 3)
+  const int slot = warp >> 3, tid = threadIdx.x & 255;
+  for (int t = blockIdx.x + slot * gridDim.x; t < ntasks; t += 2 * gridDim.x) {
+    const bool merged =
+        slot == 0 ? attn_split_task(c.a, t / c.used, t % c.used, c.used, tid, S2[0],
+                                    [] { asm volatile("bar.sync 2, 256;" ::: "memory"); }, c.sync + 2)
+                  : attn_split_task(c.a, t / c.used, t % c.used, c.used, tid, S2[1],
+                                    [] { asm volatile("bar.sync 3, 256;" ::: "memory"); }, c.sync + 2);
+    if (merged && tid == 0) {  // o rows of this kv head are written
+      __threadfence();
+      atomicAdd(c.sync, 1u);
+    }
+  }
+  if (threadIdx.x == 0)
+    while (ld_acquire_gpu(c.sync) < static_cast<unsigned>(n_kv)) __nanosleep(64);
+  asm volatile("bar.sync 1, %0;" ::"r"(AT_WARPS * 32));
+  for (int i = threadIdx.x; i < c.q_dim / 8; i += AT_WARPS * 32)
+    os[i] = __ldcg(reinterpret_cast<const uint4*>(c.a.o) + i);
+  asm volatile("bar.sync 1, %0;" ::"r"(AT_WARPS * 32));
+  ring_consume(R, r0, n, c.q_dim, os, warp, lane,
+               [&](int row, float v) { c.h_out[row] = c.h[row] + v; });
+  if (threadIdx.x == 0 && atomicAdd(c.sync + 1, 1u) == gridDim.x - 1) {
+    c.sync[0] = 0;  // every CTA is past its waits: reset for the next call
+    c.sync[2] = 0;
+    __threadfence();
+    c.sync[1] = 0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -873,7 +990,7 @@ extern "C" int daop_attn_workspace(int32_t n_heads, int32_t n_kv, int32_t max_se
   const int64_t q_dim = static_cast<int64_t>(n_heads) * AT_HD;
   const int64_t kv_dim = static_cast<int64_t>(n_kv) * AT_HD;
   const int64_t part = static_cast<int64_t>(n_kv) * 64 * (n_heads / n_kv) * (2 + AT_HD) * 4;
-  *h_bytes = (q_dim + 2 * kv_dim) * 4 + part + q_dim * 2 + 4 * n_kv + 256;
+  *h_bytes = (q_dim + 2 * kv_dim) * 4 + part + q_dim * 2 + 4 * n_kv + 128 + 12 + 256;  // + fused-kernel sync line
   (void)max_seq;
   return DAOP_OK;
 }
@@ -939,6 +1056,26 @@ extern "C" int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const
   }
   AttnArgs a{qkv, d_k_cache, d_v_cache, n_heads, n_kv, max_seq, pos, splits,
              theta, 1.0f / sqrtf(static_cast<float>(AT_HD)), part, counter, o};
+  if (attn_fused_mode()) {  // attention core + O projection in one cooperative launch
+    const int rpc = (d + sms - 1) / sms;
+    const int stages = AT_WARPS;
+    const size_t smem = static_cast<size_t>(stages) * q_dim * 2 + static_cast<size_t>(q_dim) * 2 +
+                        2 * stages * 8 + 128 + 2 * sizeof(SplitSmem);
+    DAOP_CUDA(cudaFuncSetAttribute(attn_core_oproj_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    // (the fused kernel's polled words on their own 128-byte line, away from
+    // the split counters the tasks' atomics hit)
+    unsigned* sync = reinterpret_cast<unsigned*>(
+        (reinterpret_cast<uintptr_t>(counter + n_kv) + 127) & ~static_cast<uintptr_t>(127));
+    CoreOprojArgs c{a,     d_h,     d_wo, d, q_dim, rpc, stages, used, d_h_out, sync,
+                    attn_fused_mode() == 2};
+    void* args[] = {&c};
+    DAOP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(attn_core_oproj_kernel),
+                                          dim3(sms), dim3((AT_WARPS + 1) * 32), args, smem, st));
+    DAOP_CHECK_LAUNCH("attn_core_oproj");
+    return DAOP_OK;
+  }
   attn_decode_kernel<<<dim3(n_kv, used), 256, 0, st>>>(a);
   DAOP_CHECK_LAUNCH("attn_decode");
   {
@@ -966,5 +1103,10 @@ extern "C" int daop_l2_prefetch(const void* d_p0, int64_t n0, const void* d_p1, 
   l2_prefetch_kernel<<<sm_count(), 32, 0, as_stream(stream)>>>(
       static_cast<const uint8_t*>(d_p0), n0, static_cast<const uint8_t*>(d_p1), n1);
   DAOP_CHECK_LAUNCH("l2_prefetch");
+  return DAOP_OK;
+}
+
+extern "C" int daop_set_attn_fused(int32_t fused) {
+  g_attn_fused = fused < 0 ? 0 : fused > 2 ? 2 : fused;
   return DAOP_OK;
 }

@@ -204,3 +204,33 @@ def test_dense_gemm_splitk_parity(P, M, K, N, resid):
         assert torch.equal(r2, out)
     torch.cuda.synchronize()
     close(out.cpu().numpy(), ref, f"split-K gemm {M}x{K}x{N}")
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("kv,positions", [(8, [0, 5, 511, 1601, 2047]), (4, [63, 64, 900])])
+def test_fused_core_oproj_equals_two_launches(P, kv, positions, mode):
+    """The attention core + O projection as one cooperative launch (modes 1,
+    2; off by default: measured slower) is bit-identical to the two-launch path, including more split tasks than
+    SMs (kv 8 at position 1601: 208 tasks) and back-to-back calls (the
+    kernel's head / exit counters reset themselves)."""
+    pkg, A = P
+    from paper_2501_10375_b200 import _lib
+    d, heads = 4096, 32
+    outs = {}
+    for fused in (0, mode):
+        _lib.call("daop_set_attn_fused", fused)
+        att = A.AttentionStack(1, d, heads, kv, max_seq=2048, seed=5)
+        g = torch.Generator(device="cuda").manual_seed(2)
+        att.k_cache[0].copy_(torch.randn(att.k_cache[0].shape, generator=g, device="cuda"))
+        att.v_cache[0].copy_(torch.randn(att.v_cache[0].shape, generator=g, device="cuda"))
+        res = []
+        for step, pos in enumerate(positions):
+            h = torch.empty(d, dtype=torch.float32, device="cuda")
+            A.ops.fill_uniform_f32(h, 5, (4 << 56) | (7 << 32) | step, float(np.float32(np.sqrt(3))))
+            res.append(att.decode(h, 0, pos).clone())
+        torch.cuda.synchronize()
+        outs[fused] = (res, att.k_cache.clone(), att.v_cache.clone())
+    _lib.call("daop_set_attn_fused", 0)
+    for a, b in zip(outs[0][0], outs[mode][0]):
+        assert torch.equal(a, b)
+    assert torch.equal(outs[0][1], outs[mode][1]) and torch.equal(outs[0][2], outs[mode][2])
