@@ -133,6 +133,7 @@ struct GemmParams {
   // weight groups resident: each die holds its share of B and streams A)
   int die_split_n;
   int no_stage;  // tuning: epilogue stores straight from the TMEM row layout (mode bit 19)
+  int no_tmem_pipe;  // tuning: SwiGLU epilogue without overlapped TMEM reads (mode bit 23)
 };
 
 __device__ __forceinline__ int64_t off_at(const GemmParams& p, int e) {
@@ -888,12 +889,8 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
       if constexpr (SWIGLU) {
         if (staged) {
           uint16_t* outb = static_cast<uint16_t*>(p.out) + n * 128;
-#pragma unroll 1
-          for (int c = 0; c < 128 && !(p.exp & 1); c += 32) {
-            uint32_t g[32], u[32];
-            tmem_ld32(tb + c, g);
-            tmem_ld32(tb + 128 + c, u);
-            tmem_ld_wait();
+          // 32 SwiGLU outputs of this lane's row -> staging -> coalesced rows
+          auto emit = [&](int c, const uint32_t (&g)[32], const uint32_t (&u)[32]) {
             uint4 pk[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -920,6 +917,44 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
                 if (p.store_cs) __stcs(o, v);
                 else *o = v;
               }
+            }
+          };
+          if (!(p.exp & 1) && !p.no_tmem_pipe) {
+            // software-pipelined TMEM reads: the next 32 columns' tcgen05.ld
+            // are in flight while this chunk's SwiGLU and stores run
+            uint32_t ga[32], ua[32], gb[32], ub[32];
+            tmem_ld32(tb, ga);
+            tmem_ld32(tb + 128, ua);
+            tmem_ld_wait();
+            reg_fence(ga);
+            reg_fence(ua);
+            tmem_ld32(tb + 32, gb);
+            tmem_ld32(tb + 160, ub);
+            emit(0, ga, ua);
+            tmem_ld_wait();
+            reg_fence(gb);
+            reg_fence(ub);
+            tmem_ld32(tb + 64, ga);
+            tmem_ld32(tb + 192, ua);
+            emit(32, gb, ub);
+            tmem_ld_wait();
+            reg_fence(ga);
+            reg_fence(ua);
+            tmem_ld32(tb + 96, gb);
+            tmem_ld32(tb + 224, ub);
+            emit(64, ga, ua);
+            tmem_ld_wait();
+            reg_fence(gb);
+            reg_fence(ub);
+            emit(96, gb, ub);
+          } else {
+#pragma unroll 1
+            for (int c = 0; c < 128 && !(p.exp & 1); c += 32) {
+              uint32_t g[32], u[32];
+              tmem_ld32(tb + c, g);
+              tmem_ld32(tb + 128 + c, u);
+              tmem_ld_wait();
+              emit(c, g, u);
             }
           }
         } else {
@@ -1077,6 +1112,7 @@ static int g_gemm_epi16 = 0;  // tuning: 16 epilogue warps for the 512-row pair 
 static int g_gemm_persist_off = 1;
 static int g_gemm_splitk = 1;
 static int g_gemm_nostage = 0;  // tuning: unstaged epilogue stores (mode bit 19)
+static int g_gemm_no_tmem_pipe = 0;  // tuning: SwiGLU epilogue TMEM reads not overlapped (bit 23)
 static int g_gemm_exp = 0;  // EXPERIMENT bits (GemmParams::exp)
 static int g_gemm_quad = 0;  // tuning: 4-CTA multicast clusters for the 512-row pair tile (mode bit 18)  // tuning: split-K for prompt-sized dense projections (_ws entry)
 
@@ -1233,6 +1269,7 @@ static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
   pp.store_cs = g_gemm_store_cs;
   pp.exp = g_gemm_exp;
   pp.no_stage = g_gemm_nostage;
+  pp.no_tmem_pipe = g_gemm_no_tmem_pipe;
   if (p.group_m < 0) {  // negative group = n-grouped raster of |group| weight tiles
     pp.raster = 1;
     pp.group_m = QUAD ? (-p.group_m > 1 ? -p.group_m / 2 : 1) : -p.group_m;  // (QUAD: n-pairs)
@@ -1396,6 +1433,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_exp = (mode >> 20) & 7;
   g_gemm_quad = (mode >> 18) & 1;
   g_gemm_nostage = (mode >> 19) & 1;
+  g_gemm_no_tmem_pipe = (mode >> 23) & 1;
   return DAOP_OK;
 }
 

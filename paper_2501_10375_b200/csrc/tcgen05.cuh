@@ -92,6 +92,14 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// after tmem_ld_wait: the registers a tcgen05.ld filled are "redefined" here,
+// so the compiler cannot move their uses above the wait (the ld's asm outputs
+// look written at issue; the hardware writes them asynchronously)
+__device__ __forceinline__ void reg_fence(uint32_t (&r)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(r[i]));
+}
+
 // ---------------------------------------------------------------- TMA
 
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
