@@ -5,10 +5,10 @@
 mkdir -p gpurun_out/sanitize
 S=/usr/local/cuda/bin/compute-sanitizer
 : > gpurun_out/sanitize/summary.txt
-for c in ${CASES:-permute router decode prefill ep attention}; do
+for c in ${CASES:-permute router decode prefill prefill_die ep attention attention_fused}; do
   for t in memcheck racecheck synccheck initcheck; do
     log=gpurun_out/sanitize/${t}_${c}.log
-    timeout 600 $S --tool $t --error-exitcode 17 --print-limit 20 python scripts/sanitize_cases.py $c > $log 2>&1
+    timeout ${SAN_TIMEOUT:-600} $S --tool $t --error-exitcode 17 --print-limit 20 python scripts/sanitize_cases.py $c > $log 2>&1
     rc=$?
     echo "$t $c rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $log | tail -1)" >> gpurun_out/sanitize/summary.txt
   done

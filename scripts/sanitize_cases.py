@@ -58,6 +58,25 @@ def case_prefill():
         eng.prefill(m.input_hidden(T, stream=3), 0)
 
 
+def case_prefill_die():
+    # enough rows for the per-die schedule (>= 16 pair m-tiles): the die probe,
+    # the cluster ranks and the die-split tiles of both GEMMs, staged epilogue
+    m = model()
+    eng = MoEBlockEngine(m)
+    eng.prefill(m.input_hidden(4608, stream=4), 0)
+
+
+def case_attention_fused():
+    # the attention core + O-proj cooperative kernel (off by default)
+    from paper_2501_10375_b200 import _lib
+    from paper_2501_10375_b200.attention import AttentionStack
+    att = AttentionStack(1, 512, 4, 2, max_seq=256, seed=1, device="cuda")
+    _lib.call("daop_set_attn_fused", 1)
+    for pos in range(60, 63):
+        att.decode(torch.randn(512, device="cuda"), 0, pos)
+    _lib.call("daop_set_attn_fused", 0)
+
+
 def case_ep():
     from paper_2501_10375_b200.ep import PeerEP, ep_model
     G = 2
