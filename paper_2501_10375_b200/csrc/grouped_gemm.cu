@@ -1301,18 +1301,20 @@ static int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
 
 // Default rasterisation groups.  Up GEMM (m-grouped): the group's A rows
 // (group x 128 rows x d x 2 B) are re-read by every n-tile of the group and
-// must stay in L2: 8192 rows at d = 4096 (64 MB) but 4096 at d >= 5120 (the
-// 8x22B shape's 8192-row group is 100 MB and re-read A from DRAM: 30 GB per
-// launch).  Down GEMM (n-grouped): the group's W2 tiles (group x 256 rows x
-// ffn x 2 B) -- 16 tiles at ffn <= 14336, 8 above.  DAOP_GEMM_GROUPS="up,down"
-// overrides both (tuning).
+// must stay in the die's L2 (the per-die schedule splits each expert's
+// m-tiles between the dies first).  Down GEMM (n-grouped): 16 W2 tiles.
+// DAOP_GEMM_GROUPS="up,down" overrides both (tuning).
 static int default_group_up(int d) {
   static const int env = [] {
     const char* v = getenv("DAOP_GEMM_GROUPS");
     return v ? atoi(v) : 0;
   }();
   if (env) return env;
-  return d > 5120 ? 32 : 64;
+  // with the per-die schedule a die's group of an expert's A rows should stay
+  // near 32 MB: 8x7B (d 4096) keeps the whole per-die range (4096 rows, 32 MB);
+  // 8x22B (d 6144) groups 2048 rows (25 MB per die group): up 18.6 -> 17.9 ms,
+  // DRAM reads 37-42 -> 23-28 GB (profiles/r02/die/ncu_ep_groups.txt)
+  return d > 5120 ? 16 : 64;
 }
 static int default_group_down(int ffn) {
   static const int env = [] {
@@ -1321,7 +1323,7 @@ static int default_group_down(int ffn) {
     return c ? atoi(c + 1) : 0;
   }();
   if (env) return env;
-  return (g_gemm_two_m & 2) ? (ffn > 14336 ? -8 : -16) : -8;
+  return (g_gemm_two_m & 2) ? -16 : -8;  // (8x22B: -16 9.10-9.15 vs -8 9.24 ms, per-die schedule)
 }
 
 static void apply_persisting_l2() {
