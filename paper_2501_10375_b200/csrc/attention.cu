@@ -166,16 +166,24 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
                [&](int row, float v) { qkv[row] = v; });
 }
 
-// RoPE of one head vector held as hd floats in smem (pairs (i, i + hd/2))
-__device__ __forceinline__ void rope_pair(float& a, float& b, int i, int pos, float theta) {
-  const float inv = 1.0f / powf(theta, static_cast<float>(2 * i) / static_cast<float>(AT_HD));
-  const float ang = static_cast<float>(pos) * inv;
-  float s, c;
-  sincosf(ang, &s, &c);
-  const float a2 = a * c - b * s;
-  const float b2 = b * c + a * s;
+// RoPE of one head vector held as hd floats in smem (pairs (i, i + hd/2)).
+// rope_inv / rope_angle / rope_apply are the pieces every kernel uses, in the
+// same order with explicitly rounded operations, so a rotation computed from a
+// shared cos / sin table is bit-identical to rope_pair's
+__device__ __forceinline__ float rope_inv(int i, float theta) {
+  return 1.0f / powf(theta, static_cast<float>(2 * i) / static_cast<float>(AT_HD));
+}
+__device__ __forceinline__ void rope_apply(float& a, float& b, float c, float s) {
+  const float a2 = __fmaf_rn(a, c, -__fmul_rn(b, s));
+  const float b2 = __fmaf_rn(b, c, __fmul_rn(a, s));
   a = a2;
   b = b2;
+}
+__device__ __forceinline__ void rope_pair(float& a, float& b, int i, int pos, float theta) {
+  const float ang = __fmul_rn(static_cast<float>(pos), rope_inv(i, theta));
+  float s, c;
+  sincosf(ang, &s, &c);
+  rope_apply(a, b, c, s);
 }
 
 struct AttnArgs {
@@ -780,6 +788,21 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
   };
   load_tile(0);
 
+  // the CTA's 16 tokens x 64 RoPE frequencies: cos / sin computed once and
+  // shared by the group's warps (each warp used to evaluate powf + sincosf for
+  // all 32 of its (row, dim) pairs -- 4x redundant, the kernel's longest phase)
+  __shared__ float inv_s[AT_HD / 2];
+  __shared__ float2 rope_cs[FA_TOK][AT_HD / 2];
+  if (threadIdx.x < AT_HD / 2) inv_s[threadIdx.x] = rope_inv(threadIdx.x, a.theta);
+  __syncthreads();
+  for (int i = threadIdx.x; i < FA_TOK * (AT_HD / 2); i += nthr) {
+    const int r = i / (AT_HD / 2), j = i - r * (AT_HD / 2);
+    const int t = min(t0 + r, T - 1);
+    float sn, cs;
+    sincosf(__fmul_rn(static_cast<float>(a.pos0 + t), inv_s[j]), &sn, &cs);
+    rope_cs[r][j] = make_float2(cs, sn);
+  }
+  __syncthreads();
   // Q fragments: rows gr / gr + 8 = tokens t0 + gr / t0 + gr + 8; k-step ks
   // covers dims 16 ks .. 16 ks + 15; RoPE pairs (j, j + 64) = (ks, ks + 4)
   uint32_t qf[8][4];
@@ -795,7 +818,8 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
         for (int e = 0; e < 4; ++e) {
           const int j = 16 * ks + 2 * c4 + (e & 1) + 8 * (e >> 1);  // j < 64
           float x0 = q[j], x1 = q[j + AT_HD / 2];
-          rope_pair(x0, x1, j, a.pos0 + t, a.theta);
+          const float2 cs = rope_cs[min(gr + 8 * rh, T - 1 - t0)][j];  // (row clamped like t)
+          rope_apply(x0, x1, cs.x, cs.y);
           qv[rh][ks][e] = x0;
           qv[rh][ks + 4][e] = x1;
         }
