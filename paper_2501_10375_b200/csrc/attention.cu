@@ -92,6 +92,9 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
                     int stages, float eps, uint16_t* __restrict__ xa_out,
                     float* __restrict__ qkv) {
   extern __shared__ __align__(128) uint8_t smem[];
+  // the attention core (launched programmatically behind this grid) may start
+  // now: its K / V loads do not depend on this kernel's output
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   RowRing R;
   R.S = stages;
   R.ring = smem;
@@ -246,6 +249,9 @@ __device__ __forceinline__ bool attn_split_task(const AttnArgs& a, int g, int sp
       mbar_arrive_expect_tx(&S.bar, 0);
     }
   }
+  // launched programmatically behind the QKV GEMV: the cached K / V rows are
+  // already on their way; q, k, v of this token are that kernel's output
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // q of the group's heads with RoPE
   for (int i = tid; i < group * (AT_HD / 2); i += NT) {
     const int hh = i / (AT_HD / 2), j = i - hh * (AT_HD / 2);
@@ -1100,8 +1106,24 @@ extern "C" int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const
     DAOP_CHECK_LAUNCH("attn_core_oproj");
     return DAOP_OK;
   }
-  attn_decode_kernel<<<dim3(n_kv, used), 256, 0, st>>>(a);
-  DAOP_CHECK_LAUNCH("attn_decode");
+  {
+    static const int core_pdl = [] {
+      const char* v = getenv("DAOP_ATTN_CORE_PDL");
+      return v ? atoi(v) : 1;
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_kv, used);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = core_pdl ? 1 : 0;
+    DAOP_CUDA(cudaLaunchKernelEx(&cfg, attn_decode_kernel, a));
+    DAOP_CHECK_LAUNCH("attn_decode");
+  }
   {
     const int rpc = (d + sms - 1) / sms;
     const int stages = AT_WARPS;  // one stage per consumer warp (see above)
