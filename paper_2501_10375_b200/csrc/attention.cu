@@ -401,6 +401,9 @@ __device__ __forceinline__ bool attn_split_task(const AttnArgs& a, int g, int sp
 // CTA = (kv head, split), 256 threads: attn_split_task
 __global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
   __shared__ SplitSmem S;
+  // the O projection (launched programmatically behind this grid) may start
+  // streaming Wo now; it waits for this grid before reading o
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   attn_split_task(a, blockIdx.x, blockIdx.y, gridDim.y, threadIdx.x, S, [] { __syncthreads(); });
 }
 
@@ -426,6 +429,9 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
     if (lane == 0) ring_produce(R, wo, r0, n, q_dim);
     return;
   }
+  // launched programmatically behind the attention core: Wo is streaming;
+  // o is that kernel's output (no-op for a plain launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int i = threadIdx.x; i < q_dim / 8; i += AT_WARPS * 32)
     os[i] = reinterpret_cast<const uint4*>(o)[i];
   asm volatile("bar.sync 1, %0;" ::"r"(AT_WARPS * 32));
@@ -1131,8 +1137,22 @@ extern "C" int daop_attn_decode(const float* d_h, const uint16_t* d_gamma, const
                         2 * stages * 8;
     DAOP_CUDA(cudaFuncSetAttribute(attn_oproj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-    attn_oproj_kernel<<<sms, (AT_WARPS + 1) * 32, smem, st>>>(d_h, o, d_wo, d, q_dim, rpc, stages,
-                                                              d_h_out);
+    static const int oproj_pdl = [] {
+      const char* v = getenv("DAOP_ATTN_OPROJ_PDL");
+      return v ? atoi(v) : 1;
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sms);
+    cfg.blockDim = dim3((AT_WARPS + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = oproj_pdl ? 1 : 0;
+    DAOP_CUDA(cudaLaunchKernelEx(&cfg, attn_oproj_kernel, d_h, static_cast<const uint16_t*>(o), d_wo,
+                                 d, q_dim, rpc, stages, d_h_out));
     DAOP_CHECK_LAUNCH("attn_oproj");
   }
   return DAOP_OK;
