@@ -650,7 +650,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
     if (threadIdx.x == 0 && leader) {  // rank on this die; wait until every cluster has one
       uint32_t sm;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-      const int die = p.die_tab[sm] ? 1 : 0;
+      const int die = sm < 1024 && p.die_tab[sm] ? 1 : 0;  // (table: 1024 entries)
       const unsigned r = atomicAdd(p.die_ctr + die, 1u);
       __threadfence();
       atomicAdd(p.die_ctr + 2, 1u);

@@ -56,6 +56,10 @@ __global__ void __launch_bounds__(32, 1) die_probe_kernel(const uint32_t* __rest
   }
   if (lane != 0) return;
   smid_out[blockIdx.x] = static_cast<int32_t>(sm);
+  if (sm >= gridDim.x) {  // SM ids beyond the grid (non-contiguous ids): no line set
+    for (int i = 0; i < per_sm; ++i) lat[static_cast<int64_t>(blockIdx.x) * per_sm + i] = 0;
+    return;
+  }
   const uint32_t sdst = static_cast<uint32_t>(__cvta_generic_to_shared(pad));
   uint32_t v = 0;
 #pragma unroll 1
