@@ -457,6 +457,10 @@ int daop_server_trace(uint64_t* d_buf, int32_t cap);
  * default) or ONE cooperative launch whose Wo stream overlaps the attention
  * core (1; 2: the stream waits for the split tasks' K / V) -- measured slower */
 int daop_set_attn_fused(int32_t fused);
+/* profiling aid: per-CTA global-timer stamps of the decode attention kernels'
+ * last launches (h_out: [qkv, core, oproj][256 CTAs][start, end] ns); enable
+ * zeroes them */
+int daop_attn_timeline(int32_t enable, uint64_t* h_out);
 
 /* ------------------------------------------------ die topology (B200: two dies)
  * SM -> die map of the current device, measured once and cached (csrc/

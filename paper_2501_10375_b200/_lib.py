@@ -35,6 +35,7 @@ PROTOS = {
     "daop_attn_decode": [P, P, P, P, P, P, I32, I32, I32, I32, I32, F32, F32, P, P, P, P],
     "daop_server_trace": [P, I32],
     "daop_set_attn_fused": [I32],
+    "daop_attn_timeline": [I32, P],
     "daop_die_map": [P, I32, P],
     "daop_set_gemm_die_table": [P, I32],
     "daop_die_pair_probe": [P, I64, I32, I32, P, P],

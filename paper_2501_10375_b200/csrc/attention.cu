@@ -27,6 +27,23 @@
 namespace daop {
 
 constexpr int AT_WARPS = 16;    // GEMV CTAs
+
+// profiling aid (daop_attn_timeline): global-timer span of each decode
+// attention kernel's last launch -- [qkv, core, oproj][first CTA start, last
+// CTA end] -- to see the gaps between the kernels of a decoder layer
+// (per CTA, overwritten by every launch: the host takes min start / max end
+// of the last launch of each kernel)
+constexpr int AT_TL_CTAS = 256;
+__device__ unsigned long long g_attn_tl[3][AT_TL_CTAS][2];
+__device__ int g_attn_tl_on;
+__device__ __forceinline__ void attn_tl(int k, int end) {
+  const int b = blockIdx.x + blockIdx.y * gridDim.x;
+  if (g_attn_tl_on && threadIdx.x == 0 && b < AT_TL_CTAS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_attn_tl[k][b][end] = t;
+  }
+}
 constexpr int AT_HD = 128;      // head dim (Mixtral / Llama)
 constexpr int AT_MAX_GROUP = 8; // q heads per kv head
 
@@ -95,6 +112,7 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   // the attention core (launched programmatically behind this grid) may start
   // now: its K / V loads do not depend on this kernel's output
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  attn_tl(0, 0);
   RowRing R;
   R.S = stages;
   R.ring = smem;
@@ -167,6 +185,7 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   asm volatile("bar.sync 1, %0;" ::"r"(nt));
   ring_consume(R, r0, n, d, reinterpret_cast<const uint4*>(xs), warp, lane,
                [&](int row, float v) { qkv[row] = v; });
+  attn_tl(0, 1);
 }
 
 // RoPE of one head vector held as hd floats in smem (pairs (i, i + hd/2)).
@@ -404,7 +423,9 @@ __global__ void __launch_bounds__(256, 1) attn_decode_kernel(AttnArgs a) {
   // the O projection (launched programmatically behind this grid) may start
   // streaming Wo now; it waits for this grid before reading o
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  attn_tl(1, 0);
   attn_split_task(a, blockIdx.x, blockIdx.y, gridDim.y, threadIdx.x, S, [] { __syncthreads(); });
+  attn_tl(1, 1);
 }
 
 // h' = h + o . Wo^T  (rows of Wo are output dims; o bf16 (q_dim) in smem)
@@ -423,6 +444,7 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   const int r0 = blockIdx.x * rows_per_cta;
   const int n = max(0, min(d, r0 + rows_per_cta) - r0);
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  attn_tl(2, 0);
   ring_init(R);
   __syncthreads();
   if (warp == AT_WARPS) {
@@ -437,6 +459,7 @@ __global__ void __launch_bounds__((AT_WARPS + 1) * 32, 1)
   asm volatile("bar.sync 1, %0;" ::"r"(AT_WARPS * 32));
   ring_consume(R, r0, n, q_dim, os, warp, lane,
                [&](int row, float v) { h_out[row] = h[row] + v; });
+  attn_tl(2, 1);
 }
 
 // Attention core + O projection in ONE cooperative launch (one CTA per SM):
@@ -1174,5 +1197,18 @@ extern "C" int daop_l2_prefetch(const void* d_p0, int64_t n0, const void* d_p1, 
 
 extern "C" int daop_set_attn_fused(int32_t fused) {
   g_attn_fused = fused < 0 ? 0 : fused > 2 ? 2 : fused;
+  return DAOP_OK;
+}
+
+// profiling aid: enable != 0 zeroes and turns on the decode attention kernels'
+// per-CTA global-timer stamps; h_out (3 x 256 x 2 u64, optional) receives
+// them: [qkv, core, oproj][cta][start, end] of each kernel's last launch (ns)
+extern "C" int daop_attn_timeline(int32_t enable, uint64_t* h_out) {
+  if (h_out) DAOP_CUDA(cudaMemcpyFromSymbol(h_out, g_attn_tl, sizeof(g_attn_tl)));
+  if (enable) {
+    static unsigned long long zeros[3][AT_TL_CTAS][2];
+    DAOP_CUDA(cudaMemcpyToSymbol(g_attn_tl, zeros, sizeof(zeros)));
+  }
+  DAOP_CUDA(cudaMemcpyToSymbol(g_attn_tl_on, &enable, sizeof(int)));
   return DAOP_OK;
 }

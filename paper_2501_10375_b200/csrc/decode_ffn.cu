@@ -214,7 +214,10 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   uint16_t* gp_s = g_s + static_cast<size_t>(E) * d;
 
   if (threadIdx.x == 0) {
-    if (tl) g_decode_timeline[blockIdx.x][0] = gtimer();
+    if (tl) {
+      g_decode_timeline[blockIdx.x][0] = gtimer();
+      g_decode_timeline[blockIdx.x][12] = globaltimer_ns();  // (global clock: cross-kernel spans)
+    }
     for (int w = 0; w < DW; ++w)
       for (int q = 0; q < DS; ++q) mbar_init(&s.bar[w][q], 1);
     for (int q = 0; q < DK_MAX; ++q) {
@@ -713,7 +716,10 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   if (a.host_done && wrote_out) __threadfence();
   int cta_done = 0;
   if (lane == 0) {
-    if (tl) atomicMax(&g_decode_timeline[blockIdx.x][4], gtimer());
+    if (tl) {
+      atomicMax(&g_decode_timeline[blockIdx.x][4], gtimer());
+      atomicMax(&g_decode_timeline[blockIdx.x][13], globaltimer_ns());  // (the CTA's last warp)
+    }
     if (a.ep_peers) __threadfence_block();          // this warp's y rows -> the CTA finisher
     cta_done = atomicAdd(&s.fin, 1) == DW - 1;      // CTA done
   }
@@ -930,9 +936,9 @@ static int launch_decode(DecodeArgs a, int grid, cudaStream_t st, const ServerAr
   attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (tuning: DAOP_MOE_PDL)
   attr[1].val.programmaticStreamSerializationAllowed = 1;
-  static const int moe_pdl = [] {
+  static const int moe_pdl = [] {  // on: decode32 286.8-287.9 -> 288.4-288.5 tok/s (3 A/B pairs)
     const char* v = getenv("DAOP_MOE_PDL");
-    return v ? atoi(v) : 0;
+    return v ? atoi(v) : 1;
   }();
   cfg.attrs = attr;
   cfg.numAttrs = (moe_pdl && !sv) ? 2 : 1;
