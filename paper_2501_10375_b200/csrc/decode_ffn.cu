@@ -936,8 +936,8 @@ static int launch_decode(DecodeArgs a, int grid, cudaStream_t st, const ServerAr
   attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (tuning: DAOP_MOE_PDL)
   attr[1].val.programmaticStreamSerializationAllowed = 1;
-  // off: +0.3-0.5 % (decode32 286.8-287.9 -> 288.4-288.5 tok/s) does not pay
-  // for a cooperative grid whose CTAs could take SMs its primary still needs
+  // off by default: +0.3-0.5 % (decode32 286.8-287.9 -> 288.4-288.5 tok/s),
+  // inside the box-to-box spread
   static const int moe_pdl = [] {
     const char* v = getenv("DAOP_MOE_PDL");
     return v ? atoi(v) : 0;
