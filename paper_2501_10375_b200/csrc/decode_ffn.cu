@@ -85,6 +85,11 @@ struct DecodeArgs {
   // host_seq into this pinned host word once h_out / sel are in host memory
   unsigned* host_done;
   unsigned host_seq;
+  // PLAN mode launched programmatically behind the attention O-proj: the
+  // predicted experts' weight stream starts before griddepcontrol.wait (the
+  // plan reads only the previous MoE kernel's prediction, complete once an
+  // O-proj CTA of this layer has left the SM); h is read after the wait
+  int early;
   float* host_out;         // pinned host copies of h_out / sel (server mode)
   int32_t* host_sel;
 };
@@ -416,6 +421,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
     }
     __syncthreads();
     start_stream();
+    if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // h: the O-proj's output
     for (int i = threadIdx.x; i < d / 4; i += NT)  // router inputs from global
       ss = sq_acc4(reinterpret_cast<const float4*>(a.h)[i], ss);
   } else {
@@ -800,8 +806,9 @@ __global__ void __launch_bounds__(DW * 32, 1) decode_layer_kernel(DecodeArgs a) 
   // grid's completion before reading anything it produced
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // when this launch itself is programmatic (behind the attention O-proj):
-  // everything below may read that kernel's output
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // everything below may read that kernel's output (early PLAN launches wait
+  // inside decode_body, after starting their weight stream)
+  if (!(a.early && a.mode == 1)) asm volatile("griddepcontrol.wait;" ::: "memory");
   decode_body<DW, DS, DSB>(a);
 }
 
@@ -936,14 +943,31 @@ static int launch_decode(DecodeArgs a, int grid, cudaStream_t st, const ServerAr
   attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (tuning: DAOP_MOE_PDL)
   attr[1].val.programmaticStreamSerializationAllowed = 1;
-  // off by default: +0.3-0.5 % (decode32 286.8-287.9 -> 288.4-288.5 tok/s),
-  // inside the box-to-box spread
+  // every decode launch programmatic and NOT cooperative (below): headline
+  // 9,009-9,015 -> 9,155-9,159 tok/s over 3 A/B pairs (the next launch's CTAs
+  // take each SM as the previous grid's CTA leaves, instead of a cooperative
+  // grid dispatched once it fits as a whole); DAOP_MOE_PDL=0 turns it off
   static const int moe_pdl = [] {
     const char* v = getenv("DAOP_MOE_PDL");
+    return v ? atoi(v) : 1;
+  }();
+  // early PLAN launches (behind the attention O-proj): without the cooperative
+  // attribute -- a cooperative grid is dispatched only once the whole grid
+  // fits (~5 us after the O-proj's last CTA); the grid (one CTA per SM, the
+  // shared-memory footprint allows no second) is co-resident anyway once the
+  // O-proj CTAs leave, which they do without waiting on this grid
+  static const int early_coop = [] {
+    const char* v = getenv("DAOP_EARLY_COOP");
     return v ? atoi(v) : 0;
   }();
-  cfg.attrs = attr;
-  cfg.numAttrs = (moe_pdl && !sv) ? 2 : 1;
+  // programmatic launches (early PLAN layers, or DAOP_MOE_PDL=1 for every
+  // decode launch) drop the cooperative attribute the same way; the kernel
+  // waits for its predecessor (griddepcontrol.wait) before touching anything
+  // the predecessor writes or its own self-resetting workspace
+  const bool pdl = !sv && (a.early || moe_pdl);
+  const bool plain = pdl && !early_coop;
+  cfg.attrs = plain ? attr + 1 : attr;
+  cfg.numAttrs = plain ? 1 : pdl ? 2 : 1;
   if (sv) DAOP_CUDA(cudaLaunchKernelEx(&cfg, skern, a, *sv));
   else DAOP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   return DAOP_OK;
@@ -1009,6 +1033,9 @@ extern "C" int daop_decode_layer(const float* h, const uint16_t* gamma, const ui
   a.ctr = reinterpret_cast<unsigned*>(ws);
   a.pred_logits = reinterpret_cast<float*>(ws + 128);
   a.act = reinterpret_cast<uint16_t*>(ws + 128 + (static_cast<int64_t>(E) * 4 + 255) / 256 * 256);
+  // variant bit 8: early PLAN launch behind the attention O-proj (DecodeArgs::early)
+  a.early = (variant >> 8) & 1 && mode == 1 ? 1 : 0;
+  variant &= 0xff;
   int grid = sm_count();
   if (grid < E) grid = E;  // CTAs 0..E-1 own one next-layer gate row each
   cudaStream_t st = as_stream(stream);

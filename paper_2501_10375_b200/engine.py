@@ -20,6 +20,7 @@ daop.py.
 
 from __future__ import annotations
 
+import os
 import torch
 
 from . import _lib, ops
@@ -48,6 +49,8 @@ class MoEBlockEngine:
         # while layer l's MoE kernel streams its experts.  Measured slower
         # (decoder32 192.7 vs 206.4 tok/s, DESIGN §6 tried and rejected): off
         self.attn_prefetch = False
+        # decoder layers: PLAN-mode MoE launches stream before the O-proj ends
+        self.decode_early = os.environ.get("DAOP_DECODE_EARLY", "1") != "0"
 
     # ------------------------------------------------------------ decode
     def decode(self, h: torch.Tensor, layer: int = 0, *, pred_prev=None, mode: int = 0,
@@ -152,10 +155,14 @@ class MoEBlockEngine:
             b = self._pp[l % 2]
             mode = 1 if (daop and l >= start) else 0
             nxt = m.gate[l + 1] if l + 1 < L else None
+            # PLAN layers behind the attention O-proj start streaming their
+            # predicted experts before the O-proj completes (variant bit 8)
+            early = 0x100 if (attn is not None and mode == 1 and self.decode_early) else 0
             ops.decode_layer(cur, m.norm[l], m.gate[l], nxt, m.fast[l], m.slot_of[l], m.slab,
                              m.slot_elems, self.d, self.ffn, self.k, b,
                              pred_prev=self._pp[(l + 1) % 2].p_pred if mode else None,
-                             mode=mode, weights_from_pred=weights_from_pred and mode == 1)
+                             mode=mode, weights_from_pred=weights_from_pred and mode == 1,
+                             variant=early)
             cur = b.h_out
         return cur
 

@@ -234,3 +234,29 @@ def test_fused_core_oproj_equals_two_launches(P, kv, positions, mode):
     for a, b in zip(outs[0][0], outs[mode][0]):
         assert torch.equal(a, b)
     assert torch.equal(outs[0][1], outs[mode][1]) and torch.equal(outs[0][2], outs[mode][2])
+
+
+def test_decoder_token_early_plan_launch_is_bit_identical(P):
+    """Full decoder layers (attention + MoE, DAOP plans from layer 2): the
+    PLAN-mode MoE kernels launched early behind the attention O-proj (weight
+    stream started before griddepcontrol.wait, variant bit 8) give the same
+    residual and cache as the plain launches, token after token."""
+    pkg, A = P
+    from paper_2501_10375_b200.engine import MoEBlockEngine
+    from paper_2501_10375_b200.model import MoEModel
+    L, d, ffn = 4, 1024, 2048
+    outs = {}
+    for early in (False, True):
+        m = MoEModel(pkg.ModelShape(L, 8, 2), d, ffn, seed=4)
+        eng = MoEBlockEngine(m)
+        eng.decode_early = early
+        att = A.AttentionStack(L, d, 8, 2, max_seq=64, seed=4)
+        res = []
+        for t in range(5):
+            h = m.input_hidden(1, stream=11, step=t)[0]
+            res.append(eng.decode_token(h, start=2, daop=True, attn=att, pos=t).clone())
+        torch.cuda.synchronize()
+        outs[early] = (res, att.k_cache.clone())
+    for a, b in zip(outs[False][0], outs[True][0]):
+        assert torch.equal(a, b)
+    assert torch.equal(outs[False][1], outs[True][1])
