@@ -564,6 +564,7 @@ __global__ void __launch_bounds__(256) attn_norm_rows_kernel(const float* __rest
                                                              const uint16_t* __restrict__ gamma,
                                                              int d, float eps,
                                                              uint16_t* __restrict__ xa) {
+  pdl_prologue();  // (launched with launch_pdl)
   __shared__ double red[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n8 = d / 8;
   const float4* h4 = reinterpret_cast<const float4*>(h + static_cast<int64_t>(blockIdx.x) * d);
@@ -606,6 +607,7 @@ struct PrefillArgs {
 // k (RoPE) and v of every prompt token -> the cache (before any attention
 // reads it): CTA = token
 __global__ void __launch_bounds__(128) attn_prefill_append_kernel(PrefillArgs a) {
+  pdl_prologue();  // (launched with launch_pdl)
   const int t = blockIdx.x, p = a.pos0 + t;
   const int q_dim = a.n_heads * AT_HD, kv_dim = a.n_kv * AT_HD;
   const float* row = a.qkv + static_cast<int64_t>(t) * (q_dim + 2 * kv_dim);
@@ -795,6 +797,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(PrefillArgs a, int T) {
+  pdl_prologue();  // (launched with launch_pdl)
   extern __shared__ __align__(128) uint16_t fa_smem[];  // [2 stages][K | V] tiles
   const int g = blockIdx.x, t0 = blockIdx.y * FA_TOK;
   const int group = a.n_heads / a.n_kv;
@@ -1010,8 +1013,8 @@ extern "C" int daop_attn_norm_rows(const float* d_h, int64_t T, const uint16_t* 
     return DAOP_ERR_UNSUPPORTED;
   }
   if (T == 0) return DAOP_OK;
-  attn_norm_rows_kernel<<<static_cast<unsigned>(T), 256, 0, as_stream(stream)>>>(d_h, d_gamma, d,
-                                                                                 eps, d_xa);
+  DAOP_CUDA(launch_pdl(attn_norm_rows_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, as_stream(stream), d_h, d_gamma, d,
+                                                                                 eps, d_xa));
   DAOP_CHECK_LAUNCH("attn_norm_rows");
   return DAOP_OK;
 }
@@ -1030,15 +1033,15 @@ extern "C" int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, ui
   cudaStream_t st = as_stream(stream);
   PrefillArgs a{d_qkv, d_k_cache, d_v_cache, n_heads, n_kv, max_seq, pos0,
                 theta, 1.0f / sqrtf(static_cast<float>(AT_HD)), d_o};
-  attn_prefill_append_kernel<<<static_cast<unsigned>(T), 128, 0, st>>>(a);
+  DAOP_CUDA(launch_pdl(attn_prefill_append_kernel, dim3(static_cast<unsigned>(T)), dim3(128), 0, st, a));
   DAOP_CHECK_LAUNCH("attn_prefill_append");
   const size_t smem = 2 * 2 * static_cast<size_t>(FA_TILE) * 2;  // 2 stages x (K, V)
   DAOP_CUDA(cudaFuncSetAttribute(attn_prefill_mma_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const unsigned tok_tiles = static_cast<unsigned>((T + FA_TOK - 1) / FA_TOK);
-  attn_prefill_mma_kernel<<<dim3(n_kv, tok_tiles), (n_heads / n_kv) * 32, smem, st>>>(
-      a, static_cast<int>(T));
+  DAOP_CUDA(launch_pdl(attn_prefill_mma_kernel, dim3(dim3(n_kv, tok_tiles)), dim3((n_heads / n_kv) * 32), smem, st, 
+      a, static_cast<int>(T)));
   DAOP_CHECK_LAUNCH("attn_prefill");
   return DAOP_OK;
 }

@@ -3,6 +3,7 @@
 // The host decisions are pure C++ restatements of the reference, bit-exact:
 // they are pinned by tests/test_host_decisions.py against the golden vectors
 // recorded from moesim itself.
+#include <cstdlib>
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
@@ -30,6 +31,14 @@ void set_error(const char* fmt, ...) {
 int cuda_fail(cudaError_t e, const char* what) {
   set_error("CUDA error %d (%s) at %s", static_cast<int>(e), cudaGetErrorString(e), what);
   return DAOP_ERR_CUDA;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("DAOP_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 int sm_count() {

@@ -37,6 +37,37 @@ inline cudaStream_t as_stream(daop_stream_t s) { return reinterpret_cast<cudaStr
 
 int sm_count();  // cached multiProcessorCount of the current device
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch of the hot-path kernels.  A kernel launched
+// with launch_pdl starts with pdl_prologue(): it lets the NEXT kernel in the
+// stream be scheduled at once (the successor is only launched after every CTA
+// of this grid has started, so no CTA of this grid can be crowded out) and
+// then waits for its own predecessor to complete and flush before it touches
+// memory.  The successor's launch and dispatch (~2-5 us per dependent kernel
+// pair on B200) overlap this kernel.  Only kernels that begin with the
+// prologue are launched with the attribute.  DAOP_PDL=0 turns it off.
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- smem / mbarrier
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

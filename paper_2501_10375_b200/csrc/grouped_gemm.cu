@@ -615,6 +615,7 @@ template <bool SWIGLU, bool TWO_M = false, int EW = 8, bool QUAD = false>
 __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::THREADS, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  pdl_prologue();  // (launched with launch_pdl)
   static_assert(!QUAD || TWO_M, "QUAD multicast needs the 512-row pair tile");
   using C = PairCfg<TWO_M, EW>;
   constexpr int CL = QUAD ? 4 : 2;
@@ -1278,7 +1279,7 @@ static int launch_pair_ew(const CUtensorMap& ta, const CUtensorMap& tb, const Ge
     pp.group_m = p.group_m > C::M / 128 ? p.group_m / (C::M / 128) : 1;
   }
   pp.die_split_n = pp.raster == 1;
-  kern<<<CL * clusters, C::THREADS, smem, st>>>(ta, tb, pp);
+  DAOP_CUDA(launch_pdl(kern, dim3(CL * clusters), dim3(C::THREADS), smem, st, ta, tb, pp));
   DAOP_CHECK_LAUNCH(SWIGLU ? "grouped_gemm_pair_up" : "grouped_gemm_pair_down");
   return DAOP_OK;
 }
@@ -1575,6 +1576,7 @@ __global__ void __launch_bounds__(256) dense_splitk_reduce_kernel(const float4* 
                                                                   int64_t stride4,
                                                                   const float4* resid,
                                                                   float4* out, int64_t n4) {
+  pdl_prologue();  // (launched with launch_pdl)
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float4 a = resid ? resid[i] : parts[i];
@@ -1631,9 +1633,9 @@ extern "C" int daop_gemm_bf16_f32_ws(const uint16_t* a, int64_t M, int32_t K, co
   const int64_t n4 = M * static_cast<int64_t>(N) / 4;
   int64_t blocks = (n4 + 255) / 256;
   if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
-  dense_splitk_reduce_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(
+  DAOP_CUDA(launch_pdl(dense_splitk_reduce_kernel, dim3(static_cast<int>(blocks)), dim3(256), 0, st, 
       reinterpret_cast<const float4*>(ws), ksplit, p.part_stride / 4,
-      reinterpret_cast<const float4*>(resid), reinterpret_cast<float4*>(out), n4);
+      reinterpret_cast<const float4*>(resid), reinterpret_cast<float4*>(out), n4));
   DAOP_CHECK_LAUNCH("dense_splitk_reduce");
   return DAOP_OK;
 }

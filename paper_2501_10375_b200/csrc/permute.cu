@@ -23,6 +23,7 @@ constexpr int P_MAX_E = 256;
 
 __global__ void perm_count_kernel(const int32_t* __restrict__ ids, int64_t n, int64_t chunk, int E,
                                   int32_t* __restrict__ counts /* [chunks][E] */) {
+  pdl_prologue();  // (launched with launch_pdl)
   __shared__ int32_t h[P_MAX_E];
   for (int i = threadIdx.x; i < E; i += blockDim.x) h[i] = 0;
   __syncthreads();
@@ -34,6 +35,7 @@ __global__ void perm_count_kernel(const int32_t* __restrict__ ids, int64_t n, in
 
 __global__ void perm_scan_kernel(int32_t* __restrict__ counts, int nchunks, int E,
                                  int64_t* __restrict__ offsets) {
+  pdl_prologue();  // (launched with launch_pdl)
   // thread e: serial scan over chunks of expert e (totals), then thread 0 scans experts
   __shared__ int64_t tot[P_MAX_E + 1];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -60,6 +62,7 @@ __global__ void perm_scatter_kernel(const int32_t* __restrict__ ids, int64_t n, 
                                     int E, const int32_t* __restrict__ chunk_base,
                                     const int64_t* __restrict__ offsets,
                                     int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+  pdl_prologue();  // (launched with launch_pdl)
   __shared__ int32_t run[P_MAX_E];                   // running count per expert in this chunk
   __shared__ int32_t wtot[P_THREADS / 32][P_MAX_E];  // per-warp totals of the current tile
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(P_THREADS, 1)
     perm_single_kernel(const int32_t* __restrict__ ids, int64_t n, int E,
                        int64_t* __restrict__ offsets, int32_t* __restrict__ perm,
                        int32_t* __restrict__ inv) {
+  pdl_prologue();  // (launched with launch_pdl)
   __shared__ int32_t cnt[P_MAX_E];
   __shared__ int32_t run[P_MAX_E];
   __shared__ int64_t off[P_MAX_E];
@@ -150,6 +154,7 @@ __global__ void __launch_bounds__(P_THREADS, 1)
 template <int K>
 __global__ void perm_gather_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ inv,
                                    int64_t T, int k_rt, int n16, uint4* __restrict__ x_perm) {
+  pdl_prologue();  // (launched with launch_pdl)
   const int lane = threadIdx.x & 31;
   const int k = K > 0 ? K : k_rt;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
@@ -181,6 +186,7 @@ template <int K>
 __global__ void combine_kernel(const float* __restrict__ h, const float* __restrict__ y,
                                const int32_t* __restrict__ inv, const float* __restrict__ w,
                                int64_t T, int k_rt, int d4, float* __restrict__ out) {
+  pdl_prologue();  // (launched with launch_pdl)
   const int lane = threadIdx.x & 31;
   const int k = K > 0 ? K : k_rt;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < T;
@@ -241,6 +247,7 @@ __global__ void __launch_bounds__(256, 1)
     combine_bulk_kernel(const float* __restrict__ h, const float* __restrict__ y,
                         const int32_t* __restrict__ inv, const float* __restrict__ w, int64_t T,
                         int d, int stages, float* __restrict__ out) {
+  pdl_prologue();  // (launched with launch_pdl)
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t row = static_cast<uint32_t>(d) * 4;
   const uint32_t stage_bytes = row * (K + 1);
@@ -302,6 +309,7 @@ __global__ void __launch_bounds__(256, 1)
 __global__ void __launch_bounds__(32, 1)
     gather_bulk_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ inv,
                        int64_t T, int k, int d, int stages, uint16_t* __restrict__ x_perm) {
+  pdl_prologue();  // (launched with launch_pdl)
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t row = static_cast<uint32_t>(d) * 2;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * row);
@@ -341,6 +349,7 @@ template <int K>
 __global__ void combine_small_kernel(const float* __restrict__ h, const float* __restrict__ y,
                                      const int32_t* __restrict__ inv, const float* __restrict__ w,
                                      int d4, float* __restrict__ out) {
+  pdl_prologue();  // (launched with launch_pdl)
   const int64_t t = blockIdx.x;
   const float4* hr = reinterpret_cast<const float4*>(h) + t * d4;
   float4* o = reinterpret_cast<float4*>(out) + t * d4;
@@ -368,6 +377,7 @@ __global__ void combine_small_kernel(const float* __restrict__ h, const float* _
 // small batches: one CTA per token row of x, stored at its k sorted positions
 __global__ void gather_small_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ inv,
                                     int k, int n16, uint4* __restrict__ x_perm) {
+  pdl_prologue();  // (launched with launch_pdl)
   const int64_t t = blockIdx.x;
   for (int c = threadIdx.x; c < n16; c += blockDim.x) {
     const uint4 v = x[t * n16 + c];
@@ -435,12 +445,12 @@ int daop_permute(const int32_t* ids, int64_t T, int32_t k, int32_t E, const uint
   if (nchunks < 1) nchunks = 1;
   int32_t* counts = static_cast<int32_t*>(workspace);
   if (nchunks == 1) {
-    perm_single_kernel<<<1, P_THREADS, 0, st>>>(ids, n, E, offsets, perm, inv);
+    DAOP_CUDA(launch_pdl(perm_single_kernel, dim3(1), dim3(P_THREADS), 0, st, ids, n, E, offsets, perm, inv));
   } else {
-    perm_count_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts);
-    perm_scan_kernel<<<1, 256, 0, st>>>(counts, nchunks, E, offsets);
-    perm_scatter_kernel<<<nchunks, P_THREADS, 0, st>>>(ids, n, chunk, E, counts, offsets, perm,
-                                                       inv);
+    DAOP_CUDA(launch_pdl(perm_count_kernel, dim3(nchunks), dim3(P_THREADS), 0, st, ids, n, chunk, E, counts));
+    DAOP_CUDA(launch_pdl(perm_scan_kernel, dim3(1), dim3(256), 0, st, counts, nchunks, E, offsets));
+    DAOP_CUDA(launch_pdl(perm_scatter_kernel, dim3(nchunks), dim3(P_THREADS), 0, st, ids, n, chunk, E, counts, offsets, perm,
+                                                       inv));
   }
   DAOP_CHECK_LAUNCH("permute");
   if (x_perm && n > 0) {
@@ -451,18 +461,18 @@ int daop_permute(const int32_t* ids, int64_t T, int32_t k, int32_t E, const uint
     uint4* xp = reinterpret_cast<uint4*>(x_perm);
     const size_t row = static_cast<size_t>(d) * 2;
     if (T < 2 * sm_count()) {  // decode-sized batches
-      gather_small_kernel<<<static_cast<int>(T), 256, 0, st>>>(xs, inv, k, d / 8, xp);
+      DAOP_CUDA(launch_pdl(gather_small_kernel, dim3(static_cast<int>(T)), dim3(256), 0, st, xs, inv, k, d / 8, xp));
     } else if (g_gather_variant == 0 && T >= 4 * sm_count() && row % 16 == 0 && row <= 16 * 1024) {
       const int stages = static_cast<int>(std::min<size_t>(16, (48 * 1024) / row));
       const size_t smem = row * stages + 16 * 8 + 64;
       DAOP_CUDA(cudaFuncSetAttribute(gather_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-      gather_bulk_kernel<<<g_bulk_ctas_per_sm * sm_count(), 32, smem, st>>>(x, inv, T, k, d,
-                                                                         stages, x_perm);
+      DAOP_CUDA(launch_pdl(gather_bulk_kernel, dim3(g_bulk_ctas_per_sm * sm_count()), dim3(32), smem, st, x, inv, T, k, d,
+                                                                         stages, x_perm));
     } else if (k == 2)
-      perm_gather_kernel<2><<<static_cast<int>(blocks), 256, 0, st>>>(xs, inv, T, k, d / 8, xp);
+      DAOP_CUDA(launch_pdl(perm_gather_kernel<2>, dim3(static_cast<int>(blocks)), dim3(256), 0, st, xs, inv, T, k, d / 8, xp));
     else
-      perm_gather_kernel<0><<<static_cast<int>(blocks), 256, 0, st>>>(xs, inv, T, k, d / 8, xp);
+      DAOP_CUDA(launch_pdl(perm_gather_kernel<0>, dim3(static_cast<int>(blocks)), dim3(256), 0, st, xs, inv, T, k, d / 8, xp));
     DAOP_CHECK_LAUNCH("permute_gather");
   }
   return DAOP_OK;
@@ -478,13 +488,13 @@ int daop_combine(const float* h, const float* y_sorted, const int32_t* inv, cons
   int64_t blocks = (T * 32 + 255) / 256;
   const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
   if (blocks > cap) blocks = cap;
-  auto launch = [&](auto kern) {
-    kern<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(h, y_sorted, inv, w, T, k, d / 4,
-                                                                  out);
+  auto launch = [&](auto kern) -> cudaError_t {
+    return launch_pdl(kern, dim3(static_cast<int>(blocks)), dim3(256), 0, as_stream(stream), h,
+                      y_sorted, inv, w, T, k, d / 4, out);
   };
   if (k == 2 && T < 2 * sm_count()) {  // decode-sized batches
-    combine_small_kernel<2><<<static_cast<int>(T), 256, 0, as_stream(stream)>>>(
-        h, y_sorted, inv, w, d / 4, out);
+    DAOP_CUDA(launch_pdl(combine_small_kernel<2>, dim3(static_cast<int>(T)), dim3(256), 0, as_stream(stream), 
+        h, y_sorted, inv, w, d / 4, out));
     DAOP_CHECK_LAUNCH("combine_small");
     return DAOP_OK;
   }
@@ -496,16 +506,16 @@ int daop_combine(const float* h, const float* y_sorted, const int32_t* inv, cons
       DAOP_CUDA(cudaFuncSetAttribute(combine_bulk_kernel<2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-      combine_bulk_kernel<2><<<sm_count(), 256, smem, as_stream(stream)>>>(
-          h, y_sorted, inv, w, T, d, stages, out);
+      DAOP_CUDA(launch_pdl(combine_bulk_kernel<2>, dim3(sm_count()), dim3(256), smem, as_stream(stream), 
+          h, y_sorted, inv, w, T, d, stages, out));
       DAOP_CHECK_LAUNCH("combine_bulk");
       return DAOP_OK;
     }
   }
-  if (k == 1) launch(combine_kernel<1>);
-  else if (k == 2) launch(combine_kernel<2>);
-  else if (k == 4) launch(combine_kernel<4>);
-  else launch(combine_kernel<0>);
+  if (k == 1) DAOP_CUDA(launch(combine_kernel<1>));
+  else if (k == 2) DAOP_CUDA(launch(combine_kernel<2>));
+  else if (k == 4) DAOP_CUDA(launch(combine_kernel<4>));
+  else DAOP_CUDA(launch(combine_kernel<0>));
   DAOP_CHECK_LAUNCH("combine");
   return DAOP_OK;
 }

@@ -66,6 +66,7 @@ static __device__ __forceinline__ float lane_softmax_p2(float z, int lane, int E
 template <bool GATE_IN_SMEM>
 __global__ void __launch_bounds__(kRouterWarps * 32)
     router_kernel(RouterArgs a) {
+  pdl_prologue();  // (launched with launch_pdl)
   extern __shared__ __align__(16) uint8_t smem[];
   const int d = a.d, E = a.E;
   const int rows = a.wg_next ? 2 * E : E;
@@ -271,6 +272,7 @@ __device__ __forceinline__ void token_finish(const RouterArgs& a, int64_t tt, in
 }
 
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArgs a) {
+  pdl_prologue();  // (launched with launch_pdl)
   extern __shared__ __align__(16) uint8_t smem[];
   const int d = a.d, E = a.E;
   const int rows = a.wg_next ? 2 * E : E;
@@ -428,6 +430,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma_kernel(RouterArg
 // tokens of this one.
 template <int KS>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_mma1_kernel(RouterArgs a) {
+  pdl_prologue();  // (launched with launch_pdl)
   extern __shared__ __align__(16) uint8_t smem[];
   const int d = a.d, E = a.E;
   const int rows = a.wg_next ? 2 * E : E;
@@ -657,6 +660,7 @@ __device__ __forceinline__ void tile_finish(const RouterArgs& a, int64_t t0, int
 
 template <int KS>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_tma_kernel(RouterArgs a, int stages) {
+  pdl_prologue();  // (launched with launch_pdl)
   constexpr int TOK = kTmaTok;
   constexpr int S = KS * 16;                   // d-slice per warp
   constexpr int NV4 = KS / 8;                  // float4s per lane per token row of the slice
@@ -842,6 +846,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) router_tma_kernel(RouterArg
 constexpr int kSmallWarps = 16;
 
 __global__ void __launch_bounds__(kSmallWarps * 32, 1) router_small_kernel(RouterArgs a) {
+  pdl_prologue();  // (launched with launch_pdl)
   const int d = a.d, E = a.E, k = a.k;
   const int rows = a.wg_next ? 2 * E : E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
@@ -1028,7 +1033,7 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
                       (ks_small == 8 || ks_small == 16);
   if (T <= 128 && d % 8 == 0 && !(g_router_small_bulk && tma_ok && T >= 8)) {
     // decode-sized batch: a CTA per token
-    router_small_kernel<<<static_cast<int>(T), kSmallWarps * 32, 0, as_stream(st)>>>(a);
+    DAOP_CUDA(launch_pdl(router_small_kernel, dim3(static_cast<int>(T)), dim3(kSmallWarps * 32), 0, as_stream(st), a));
     DAOP_CHECK_LAUNCH("router_small");
     return DAOP_OK;
   }
@@ -1045,7 +1050,7 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
     auto launch = [&](auto kern) {
       DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-      kern<<<blocks, kMmaWarps * 32, smem, as_stream(st)>>>(a, stages);
+      DAOP_CUDA(launch_pdl(kern, dim3(blocks), dim3(kMmaWarps * 32), smem, as_stream(st), a, stages));
       return DAOP_OK;
     };
     const int rc = ks1 == 8 ? launch(router_tma_kernel<8>) : launch(router_tma_kernel<16>);
@@ -1062,7 +1067,7 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
     auto launch1 = [&](auto kern) {
       DAOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem1)));
-      kern<<<blocks, kMmaWarps * 32, smem1, as_stream(st)>>>(a);
+      DAOP_CUDA(launch_pdl(kern, dim3(blocks), dim3(kMmaWarps * 32), smem1, as_stream(st), a));
       return DAOP_OK;
     };
     int rc = ks1 == 4 ? launch1(router_mma1_kernel<4>) : ks1 == 8 ? launch1(router_mma1_kernel<8>)
@@ -1078,7 +1083,7 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
     const int blocks = static_cast<int>(ntiles < sm_count() ? ntiles : sm_count());
     DAOP_CUDA(cudaFuncSetAttribute(router_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem_mma)));
-    router_mma_kernel<<<blocks, kMmaWarps * 32, smem_mma, as_stream(st)>>>(a);
+    DAOP_CUDA(launch_pdl(router_mma_kernel, dim3(blocks), dim3(kMmaWarps * 32), smem_mma, as_stream(st), a));
     DAOP_CHECK_LAUNCH("router");
     return DAOP_OK;
   }
@@ -1089,16 +1094,16 @@ extern "C" int daop_router(const float* h, const uint16_t* gamma, const uint16_t
     if (blocks > cap) blocks = cap;
     DAOP_CUDA(cudaFuncSetAttribute(router_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-    router_kernel<true><<<static_cast<int>(blocks), kRouterWarps * 32, smem, as_stream(st)>>>(a);
+    DAOP_CUDA(launch_pdl(router_kernel<true>, dim3(static_cast<int>(blocks)), dim3(kRouterWarps * 32), smem, as_stream(st), a));
   } else if (smem <= 200 * 1024 && T >= 4096) {
     const int64_t cap1 = sm_count();
     if (blocks > cap1) blocks = cap1;
     DAOP_CUDA(cudaFuncSetAttribute(router_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-    router_kernel<true><<<static_cast<int>(blocks), kRouterWarps * 32, smem, as_stream(st)>>>(a);
+    DAOP_CUDA(launch_pdl(router_kernel<true>, dim3(static_cast<int>(blocks)), dim3(kRouterWarps * 32), smem, as_stream(st), a));
   } else {
     if (blocks > cap * 4) blocks = cap * 4;
-    router_kernel<false><<<static_cast<int>(blocks), kRouterWarps * 32, 0, as_stream(st)>>>(a);
+    DAOP_CUDA(launch_pdl(router_kernel<false>, dim3(static_cast<int>(blocks)), dim3(kRouterWarps * 32), 0, as_stream(st), a));
   }
   DAOP_CHECK_LAUNCH("router");
   return DAOP_OK;

@@ -118,6 +118,7 @@ template <bool SWIGLU, int NT>
 __global__ void __launch_bounds__(192, SkinnyCfg<SWIGLU, NT>::CTAS_PER_SM)
     skinny_gemm_kernel(const __grid_constant__ CUtensorMap tmW,
                        const __grid_constant__ CUtensorMap tmX, SkinnyParams p) {
+  pdl_prologue();  // (launched with launch_pdl)
   using C = SkinnyCfg<SWIGLU, NT>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = smem_u32(smem_raw);
@@ -308,7 +309,7 @@ static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const Ski
   const int64_t max_tiles = (rows_total / NT + p.E) * static_cast<int64_t>(p.row_tiles);
   int grid = sm_count() * C::CTAS_PER_SM;
   if (max_tiles < grid) grid = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
-  kern<<<grid, 192, smem, st>>>(tw, tx, p);
+  DAOP_CUDA(launch_pdl(kern, dim3(grid), dim3(192), smem, st, tw, tx, p));
   DAOP_CHECK_LAUNCH(SWIGLU ? "skinny_gemm_up" : "skinny_gemm_down");
   return DAOP_OK;
 }
