@@ -309,7 +309,18 @@ static int launch_skinny(const CUtensorMap& tw, const CUtensorMap& tx, const Ski
   const int64_t max_tiles = (rows_total / NT + p.E) * static_cast<int64_t>(p.row_tiles);
   int grid = sm_count() * C::CTAS_PER_SM;
   if (max_tiles < grid) grid = static_cast<int>(max_tiles < 1 ? 1 : max_tiles);
-  DAOP_CUDA(launch_pdl(kern, dim3(grid), dim3(192), smem, st, tw, tx, p));
+  static const bool skinny_pdl = [] {  // tuning: DAOP_PDL_SKINNY=0 launches it plainly
+    const char* v = getenv("DAOP_PDL_SKINNY");
+    return !(v && v[0] == '0');
+  }();
+  // decode-sized batches launch plainly: with PDL the batched-decode step
+  // (b = 64, 128 rows) took 0.454-0.455 vs 0.447 ms; prompt-sized ones gain
+  // (256-token prefill 0.636-0.642 -> 0.633-0.634 ms per layer)
+  if (skinny_pdl && rows_total > 256) {
+    DAOP_CUDA(launch_pdl(kern, dim3(grid), dim3(192), smem, st, tw, tx, p));
+  } else {
+    kern<<<grid, 192, smem, st>>>(tw, tx, p);  // (its griddepcontrol.wait is a no-op)
+  }
   DAOP_CHECK_LAUNCH(SWIGLU ? "skinny_gemm_up" : "skinny_gemm_down");
   return DAOP_OK;
 }
