@@ -27,9 +27,10 @@ of expert weights exceed the 126 MB L2, so no L2 flush is needed.
 --impl reference times that CPU path alone as the reference arm (the
 reference package itself executes no numerics -- SPEC.md:347,356 -- so its
 own algorithm restated in oracle/ is the arm).
-With N > 1 (torchrun) every rank runs the same decode on its own GPU as an
-independent replica (weak scaling; decode b=1 touches 2 experts, so expert
-parallelism cannot speed up a single token -- DESIGN.md §7).
+With N > 1 (torchrun) the headline is expert parallelism (run_b200_ep,
+BASELINE configs[4], strong scaling): a Mixtral-8x22B-shaped layer, the
+prompt's tokens and the experts sharded over the ranks, dispatch / return
+over NVLink peer memory (`--ep-headline` runs that path on one GPU).
 
   ep        BASELINE configs[4]: a Mixtral-8x22B-shaped layer, prefill of
             8 x 4096 tokens sharded over the N ranks, experts sharded E/N per
