@@ -796,12 +796,22 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
          (static_cast<uint32_t>(f32_to_bf16_bits(hi)) << 16);
 }
 
-__global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(PrefillArgs a, int T) {
+// KV split (FA_HALVES = 2 when 2 x group warps fit 256 threads): the group's
+// warps run twice, half h over the K / V tiles [h * n0, ...) of the CTA's
+// causal range with its own two-stage buffers and named barrier; half 1's
+// (m, l, O) are merged into half 0's at the end (flash-decoding style), which
+// halves the serial tile loop of the late token tiles -- the kernel's
+// critical path (the last 16 tokens see all 4 tiles of a 256-token prompt).
+constexpr int FA_HALVES_MAX = 2;
+__global__ void __launch_bounds__(256) attn_prefill_mma_kernel(PrefillArgs a, int T) {
   pdl_prologue();  // (launched with launch_pdl)
   extern __shared__ __align__(128) uint16_t fa_smem[];  // [2 stages][K | V] tiles
   const int g = blockIdx.x, t0 = blockIdx.y * FA_TOK;
   const int group = a.n_heads / a.n_kv;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = group * 32;
+  const int halves = static_cast<int>(blockDim.x) / (group * 32);  // 1 or 2
+  const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr_all = blockDim.x;
+  const int half = warp_all / group, warp = warp_all - half * group, nthr = group * 32;
+  const int htid = threadIdx.x - half * nthr;  // thread index within the half
   const int gr = lane >> 2, c4 = lane & 3;  // fragment row / column pair
   const int q_dim = a.n_heads * AT_HD, kv_dim = a.n_kv * AT_HD, ld = q_dim + 2 * kv_dim;
   const int hh = g * group + warp;  // this warp's query head
@@ -809,13 +819,17 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
   const uint16_t* vc = a.v_cache + static_cast<int64_t>(g) * a.max_seq * AT_HD;
   const int t_last = min(T, t0 + FA_TOK) - 1;
   const int n_pos = a.pos0 + t_last + 1;  // positions any row of this CTA attends to
-  const int n_tiles = (n_pos + FA_KV - 1) / FA_KV;
+  const int n_all = (n_pos + FA_KV - 1) / FA_KV;
+  const int n_first = halves == 2 ? (n_all + 1) / 2 : n_all;  // half 0: [0, n_first)
+  const int s_begin = half == 0 ? 0 : n_first, s_end = half == 0 ? n_first : n_all;
+  uint16_t* const hsm = fa_smem + static_cast<size_t>(half) * 4 * FA_TILE;  // this half's stages
+  auto hsync = [&] { asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(nthr) : "memory"); };
 
-  auto load_tile = [&](int s) {  // positions [s * 64, s * 64 + 64) -> stage s & 1
-    uint16_t* ks = fa_smem + (s & 1) * 2 * FA_TILE;
+  auto load_tile = [&](int s) {  // positions [s * 64, s * 64 + 64) -> stage s & 1 of this half
+    uint16_t* ks = hsm + (s & 1) * 2 * FA_TILE;
     uint16_t* vs = ks + FA_TILE;
     const int p0 = s * FA_KV;
-    for (int i = threadIdx.x; i < FA_KV * (AT_HD / 8); i += nthr) {
+    for (int i = htid; i < FA_KV * (AT_HD / 8); i += nthr) {
       const int r = i >> 4, c = (i & 15) * 8;
       const bool ok = p0 + r < n_pos;
       const int64_t src = static_cast<int64_t>(ok ? p0 + r : 0) * AT_HD + c;
@@ -824,7 +838,7 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  load_tile(0);
+  if (s_begin < s_end) load_tile(s_begin);
 
   // the CTA's 16 tokens x 64 RoPE frequencies: cos / sin computed once and
   // shared by the group's warps (each warp used to evaluate powf + sincosf for
@@ -833,7 +847,7 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
   __shared__ float2 rope_cs[FA_TOK][AT_HD / 2];
   if (threadIdx.x < AT_HD / 2) inv_s[threadIdx.x] = rope_inv(threadIdx.x, a.theta);
   __syncthreads();
-  for (int i = threadIdx.x; i < FA_TOK * (AT_HD / 2); i += nthr) {
+  for (int i = threadIdx.x; i < FA_TOK * (AT_HD / 2); i += nthr_all) {
     const int r = i / (AT_HD / 2), j = i - r * (AT_HD / 2);
     const int t = min(t0 + r, T - 1);
     float sn, cs;
@@ -877,15 +891,15 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-  for (int s = 0; s < n_tiles; ++s) {
-    if (s + 1 < n_tiles) {
+  for (int s = s_begin; s < s_end; ++s) {
+    if (s + 1 < s_end) {
       load_tile(s + 1);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
-    __syncthreads();
-    const uint16_t* ks_ = fa_smem + (s & 1) * 2 * FA_TILE;
+    hsync();
+    const uint16_t* ks_ = hsm + (s & 1) * 2 * FA_TILE;
     const uint16_t* vs_ = ks_ + FA_TILE;
     const int p0 = s * FA_KV;
     // ---- S = Q K^T (16 x 64)
@@ -921,8 +935,11 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
     mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
     mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
     mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    // every row sees position 0 in its first tile, so mx is finite from tile 0
-    const float al0 = expf(m0 - mx0), al1 = expf(m1 - mx1);
+    // half 0 sees position 0 in its first tile, so its mx is finite from
+    // tile 0; half 1's first tile can be fully masked for some rows (mx stays
+    // -inf: guard the rescale, e^(-inf - -inf))
+    const float al0 = mx0 == -INFINITY ? 1.f : expf(m0 - mx0);
+    const float al1 = mx1 == -INFINITY ? 1.f : expf(m1 - mx1);
     m0 = mx0;
     m1 = mx1;
     float rs0 = 0.f, rs1 = 0.f;
@@ -930,8 +947,8 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
     for (int j = 0; j < 8; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        sc[j][e] = expf(sc[j][e] - m0);
-        sc[j][2 + e] = expf(sc[j][2 + e] - m1);
+        sc[j][e] = m0 == -INFINITY ? 0.f : expf(sc[j][e] - m0);
+        sc[j][2 + e] = m1 == -INFINITY ? 0.f : expf(sc[j][2 + e] - m1);
         rs0 += sc[j][e];
         rs1 += sc[j][2 + e];
       }
@@ -966,7 +983,38 @@ __global__ void __launch_bounds__(AT_MAX_GROUP * 32) attn_prefill_mma_kernel(Pre
         mma_bf16_16816_acc(o[dn + 1], pa0, pa1, pa2, pa3, b2, b3);
       }
     }
-    __syncthreads();  // this stage is refilled two iterations from now
+    hsync();  // this stage is refilled two iterations from now
+  }
+  if (halves == 2) {  // half 1's (m, l, O) -> shared memory; half 0 merges
+    float* xch = reinterpret_cast<float*>(fa_smem + 4 * FA_TILE);  // half 1's stages (idle now)
+    float* mine = xch + static_cast<size_t>(warp * 32 + lane) * 68;
+    __syncthreads();
+    if (half == 1) {
+      mine[0] = m0;
+      mine[1] = m1;
+      mine[2] = l0;
+      mine[3] = l1;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) mine[4 + 4 * i + c] = o[i][c];
+    }
+    __syncthreads();
+    if (half == 1) return;
+    const float mb0 = mine[0], mb1 = mine[1], lb0 = mine[2], lb1 = mine[3];
+    const float mm0 = fmaxf(m0, mb0), mm1 = fmaxf(m1, mb1);
+    const float fa0 = expf(m0 - mm0), fa1 = expf(m1 - mm1);
+    const float fb0 = mb0 == -INFINITY ? 0.f : expf(mb0 - mm0);
+    const float fb1 = mb1 == -INFINITY ? 0.f : expf(mb1 - mm1);
+    l0 = l0 * fa0 + lb0 * fb0;
+    l1 = l1 * fa1 + lb1 * fb1;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      o[i][0] = o[i][0] * fa0 + mine[4 + 4 * i + 0] * fb0;
+      o[i][1] = o[i][1] * fa0 + mine[4 + 4 * i + 1] * fb0;
+      o[i][2] = o[i][2] * fa1 + mine[4 + 4 * i + 2] * fb1;
+      o[i][3] = o[i][3] * fa1 + mine[4 + 4 * i + 3] * fb1;
+    }
   }
   // ---- o = bf16(O / l) -> (T, q_dim) at this head's 128 columns
   const float inv0 = 1.0f / l0, inv1 = 1.0f / l1;
@@ -1035,13 +1083,21 @@ extern "C" int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, ui
                 theta, 1.0f / sqrtf(static_cast<float>(AT_HD)), d_o};
   DAOP_CUDA(launch_pdl(attn_prefill_append_kernel, dim3(static_cast<unsigned>(T)), dim3(128), 0, st, a));
   DAOP_CHECK_LAUNCH("attn_prefill_append");
-  const size_t smem = 2 * 2 * static_cast<size_t>(FA_TILE) * 2;  // 2 stages x (K, V)
+  // KV split over two warp groups when 2 x group warps fit the 256-thread CTA
+  // and the prompt spans more than one K / V tile (DAOP_ATTN_KV_SPLIT=0: off)
+  static const bool kv_split = [] {
+    const char* v = getenv("DAOP_ATTN_KV_SPLIT");
+    return !(v && v[0] == '0');
+  }();
+  const int group = n_heads / n_kv;
+  const int halves = kv_split && group * 64 <= 256 && pos0 + T > FA_KV ? FA_HALVES_MAX : 1;
+  const size_t smem = static_cast<size_t>(halves) * 2 * 2 * FA_TILE * 2;  // per half: 2 stages x (K, V)
   DAOP_CUDA(cudaFuncSetAttribute(attn_prefill_mma_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   const unsigned tok_tiles = static_cast<unsigned>((T + FA_TOK - 1) / FA_TOK);
-  DAOP_CUDA(launch_pdl(attn_prefill_mma_kernel, dim3(dim3(n_kv, tok_tiles)), dim3((n_heads / n_kv) * 32), smem, st, 
-      a, static_cast<int>(T)));
+  DAOP_CUDA(launch_pdl(attn_prefill_mma_kernel, dim3(dim3(n_kv, tok_tiles)),
+                       dim3(halves * group * 32), smem, st, a, static_cast<int>(T)));
   DAOP_CHECK_LAUNCH("attn_prefill");
   return DAOP_OK;
 }
