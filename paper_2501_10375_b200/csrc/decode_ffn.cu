@@ -92,6 +92,10 @@ struct DecodeArgs {
   int early;
   float* host_out;         // pinned host copies of h_out / sel (server mode)
   int32_t* host_sel;
+  // server mode: every CTA ships its own h_out rows to host_out with one bulk
+  // store as it finishes (rows_per_cta % 4 == 0: 16-byte pieces) instead of
+  // the grid's last warp pulling all d rows back from HBM and pushing them
+  int ship_cta;
 };
 
 __device__ unsigned long long g_decode_timeline[1024][16];
@@ -207,6 +211,8 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
   int* rcnt = reinterpret_cast<int*>(part + a.rows_per_cta * k * npc2_max);
   auto& s = *reinterpret_cast<DecodeSmem<DW, DS>*>(
       reinterpret_cast<uint8_t*>(rcnt) + ((a.rows_per_cta * 4 + 127) / 128) * 128);
+  float* hout_s = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(&s) +
+                                           (sizeof(DecodeSmem<DW, DS>) + 15) / 16 * 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool tl = g_decode_timeline_on != 0 && blockIdx.x < 1024;
   const bool pred_row = a.wg_next && blockIdx.x < static_cast<unsigned>(E);
@@ -710,6 +716,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
           }
           if (all_fast) {
             a.h_out[pc.row] = o;
+            if (a.ship_cta) hout_s[rr] = o;
             wrote_out = true;
           }
         }
@@ -726,10 +733,20 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
       atomicMax(&g_decode_timeline[blockIdx.x][4], gtimer());
       atomicMax(&g_decode_timeline[blockIdx.x][13], globaltimer_ns());  // (the CTA's last warp)
     }
-    if (a.ep_peers) __threadfence_block();          // this warp's y rows -> the CTA finisher
+    if (a.ep_peers || a.ship_cta) __threadfence_block();  // y rows / hout_s -> the CTA finisher
     cta_done = atomicAdd(&s.fin, 1) == DW - 1;      // CTA done
   }
   cta_done = __shfl_sync(0xffffffffu, cta_done, 0);
+  if (cta_done && a.ship_cta && all_fast && lane == 0 && L.R > 0) {
+    // decode server: this CTA's rows leave for pinned host memory now
+    __threadfence_block();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // hout_s: generic -> bulk
+    asm volatile(
+        "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+        "cp.async.bulk.commit_group;\n\t"
+        "cp.async.bulk.wait_group 0;" ::"l"(a.host_out + L.r0), "r"(smem_u32(hout_s)), "r"(L.R * 4)
+        : "memory");
+  }
   if (cta_done && a.ep_peers) {
     // expert parallelism: the finishing warp stores this CTA's block of y
     // rows (every executed pick) into slot [epoch & 1] of every peer's
@@ -773,7 +790,7 @@ __device__ __forceinline__ void decode_body(const DecodeArgs a) {
       // (two bulk DMAs through this CTA's now idle ring: HBM -> smem -> host)
       __threadfence();
       if (lane == 0) {
-        if (a.host_out && all_fast) {
+        if (a.host_out && all_fast && !a.ship_cta) {
           uint64_t* bar = &s.bar[0][0];  // re-armed below for the next call's init
           mbar_init(bar, 1);
           fence_mbar_init();
@@ -922,7 +939,8 @@ static int launch_decode(DecodeArgs a, int grid, cudaStream_t st, const ServerAr
                       (static_cast<size_t>(a.d) * 2 + 127) / 128 * 128 +
                       static_cast<size_t>(a.rows_per_cta) * a.k * npc2 * 4 +
                       (static_cast<size_t>(a.rows_per_cta) * 4 + 127) / 128 * 128 +
-                      sizeof(DecodeSmem<DW, DS>) + 128;
+                      (sizeof(DecodeSmem<DW, DS>) + 15) / 16 * 16 +
+                      static_cast<size_t>(a.rows_per_cta) * 4 + 128;  // (+ hout_s)
   if (smem > 227 * 1024) {
     set_error("decode_layer: %zu B of shared memory exceeds 227 KB (k*ffn too large)", smem);
     return DAOP_ERR_UNSUPPORTED;
@@ -1178,6 +1196,17 @@ extern "C" int daop_server_start(const uint16_t* gamma, const uint16_t* wg,
   a.sel = s->sel_dev;
   a.host_out = h_out;
   a.host_sel = sel;
+  {
+    static const int ship = [] {  // DAOP_SERVER_SHIP_CTA=0: the last warp ships all rows
+      const char* v = getenv("DAOP_SERVER_SHIP_CTA");
+      return v ? atoi(v) : 1;
+    }();
+    int g = sm_count();
+    if (g < E) g = E;
+    const int rpc = (d + g - 1) / g;
+    a.ship_cta = ship && h_out && rpc % 4 == 0 &&
+                 (reinterpret_cast<uintptr_t>(h_out) & 15) == 0 ? 1 : 0;
+  }
   a.ep_peers = nullptr;
   a.host_done = s->done;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
