@@ -461,6 +461,12 @@ int daop_set_attn_fused(int32_t fused);
  * last launches (h_out: [qkv, core, oproj][256 CTAs][start, end] ns); enable
  * zeroes them */
 int daop_attn_timeline(int32_t enable, uint64_t* h_out);
+/* profiling aid: per-CTA global-timer stamps of the CTA-pair GEMM kernel's
+ * launches since enabling (h_out: [512 CTAs][entry, setup done, last MMA
+ * commit, last epilogue warp done, last accumulator ready in an epilogue
+ * warp, fp32 epilogue: first TMEM chunk loaded] ns, max over launches);
+ * enable zeroes them */
+int daop_gemm_timeline(int32_t enable, uint64_t* h_out);
 
 /* ------------------------------------------------ die topology (B200: two dies)
  * SM -> die map of the current device, measured once and cached (csrc/

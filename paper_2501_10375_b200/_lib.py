@@ -36,6 +36,7 @@ PROTOS = {
     "daop_server_trace": [P, I32],
     "daop_set_attn_fused": [I32],
     "daop_attn_timeline": [I32, P],
+    "daop_gemm_timeline": [I32, P],
     "daop_die_map": [P, I32, P],
     "daop_set_gemm_die_table": [P, I32],
     "daop_die_pair_probe": [P, I64, I32, I32, P, P],

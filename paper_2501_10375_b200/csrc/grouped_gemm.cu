@@ -611,11 +611,27 @@ __device__ __forceinline__ void split_tile(const GemmParams& p, int n_eff, int& 
 // Measured: no gain -- only 33 four-CTA clusters fit the GPCs (132 SMs), and
 // with L2-hot operands the per-SM feed is as slow as without multicast (the
 // limit is the SM's ingress, ~36 B/clk, not L2 output).
+// profiling aid (daop_gemm_timeline): global-timer stamps of each CTA of the
+// pair kernel's last launch -- [entry, setup done (TMEM + cluster sync), last
+// MMA commit (leader), last epilogue warp done, last accumulator-ready wait
+// returned in an epilogue warp, fp32 path: last first-chunk TMEM load done]
+constexpr int GT_CTAS = 512;
+__device__ unsigned long long g_pair_tl[GT_CTAS][6];
+__device__ int g_pair_tl_on;
+__device__ __forceinline__ void pair_tl(int k) {
+  if (g_pair_tl_on && blockIdx.x < GT_CTAS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&g_pair_tl[blockIdx.x][k], t);
+  }
+}
+
 template <bool SWIGLU, bool TWO_M = false, int EW = 8, bool QUAD = false>
 __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<TWO_M, EW>::THREADS, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   pdl_prologue();  // (launched with launch_pdl)
+  if (threadIdx.x == 0) pair_tl(0);
   static_assert(!QUAD || TWO_M, "QUAD multicast needs the 512-row pair tile");
   using C = PairCfg<TWO_M, EW>;
   constexpr int CL = QUAD ? 4 : 2;
@@ -713,6 +729,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
+  if (threadIdx.x == 0) pair_tl(1);
   const uint32_t tmem_base = s.tmem_base;
   const int nt = QUAD ? p.n_tiles / 2 : p.n_tiles, G = p.group_m;
 
@@ -848,6 +865,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
           acc_phase ^= 1;
         }
       }
+      pair_tl(2);
       // drain: wait until both epilogues released the last accumulator(s)
       for (int i = 0; i < C::NACC && i < iters; ++i) {
         mbar_wait(&s.tempty[acc], acc_phase ^ 1);
@@ -868,6 +886,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
       int ks, kb0, kb1;
       split_tile(p, n, n, ks, kb0, kb1);
       mbar_wait(&s.tfull[acc], acc_phase);
+      if (lane == 0) pair_tl(4);
       tc_fence_after();
       const int64_t me = s.off[e + 1] - s.off[e];
       const int grp = (warp - 2) >> 2;  // 0 .. EPI_WARPS / 4 - 1
@@ -998,6 +1017,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
           uint32_t v[32];
           tmem_ld32(tb + c, v);
           tmem_ld_wait();
+          if (lane == 0 && c == sub * (GB_N / C::GROUPS_PER_HALF)) pair_tl(5);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint4 pk[4];
@@ -1028,6 +1048,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
                                 ? reinterpret_cast<float4*>(reinterpret_cast<float*>(p.row_dst[row0g + row]) +
                                                             n * GB_N + c + 16 * hh + 4 * (lane & 3))
                                 : reinterpret_cast<float4*>(outf + off);
+                if (p.exp & 8) continue;  // diagnostic: TMEM loads + staging only
                 if (p.store_cs) __stcs(o, a);
                 else *o = a;
               }
@@ -1081,6 +1102,7 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) pair_tl(3);
   }
   tc_fence_before();
   ep_gemm_signal_fence(p);
@@ -1433,7 +1455,7 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_dense_skinny = !((mode >> 15) & 1);
   g_gemm_epi16 = (mode >> 16) & 1;
   g_gemm_splitk = !((mode >> 17) & 1);
-  g_gemm_exp = (mode >> 20) & 7;
+  g_gemm_exp = ((mode >> 20) & 7) | (((mode >> 24) & 1) << 3);  // bit 3: no fp32 y stores
   g_gemm_quad = (mode >> 18) & 1;
   g_gemm_nostage = (mode >> 19) & 1;
   g_gemm_no_tmem_pipe = (mode >> 23) & 1;
@@ -1727,4 +1749,14 @@ extern "C" int daop_ep_expert_gemm_down(const uint16_t* act, int64_t rows_cap, i
                slot_stride_elems, reinterpret_cast<const uint64_t*>(ws + EP_ROWMAP),
                reinterpret_cast<unsigned*>(ws + EP_DONE_GEMM), d_peers, G, rank, epoch};
   return launch_gemm<false>(ta, tb, p, rows_cap, as_stream(stream));
+}
+
+extern "C" int daop_gemm_timeline(int32_t enable, uint64_t* h_out) {
+  if (h_out) DAOP_CUDA(cudaMemcpyFromSymbol(h_out, g_pair_tl, sizeof(g_pair_tl)));
+  if (enable) {
+    static unsigned long long zeros[GT_CTAS][6];
+    DAOP_CUDA(cudaMemcpyToSymbol(g_pair_tl, zeros, sizeof(zeros)));
+  }
+  DAOP_CUDA(cudaMemcpyToSymbol(g_pair_tl_on, &enable, sizeof(int)));
+  return DAOP_OK;
 }
