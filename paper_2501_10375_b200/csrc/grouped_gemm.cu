@@ -1015,8 +1015,13 @@ __global__ void __cluster_dims__(QUAD ? 4 : 2, 1, 1) __launch_bounds__(PairCfg<T
         for (int c = sub * (GB_N / C::GROUPS_PER_HALF);
              c < (sub + 1) * (GB_N / C::GROUPS_PER_HALF) && !(p.exp & 1); c += 32) {
           uint32_t v[32];
-          tmem_ld32(tb + c, v);
-          tmem_ld_wait();
+          if (p.exp & 16) {  // diagnostic: staging + stores only
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = static_cast<uint32_t>(c + i + lane);
+          } else {
+            tmem_ld32(tb + c, v);
+            tmem_ld_wait();
+          }
           if (lane == 0 && c == sub * (GB_N / C::GROUPS_PER_HALF)) pair_tl(5);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -1455,7 +1460,8 @@ extern "C" int daop_set_gemm_mode(int32_t mode) {
   g_gemm_dense_skinny = !((mode >> 15) & 1);
   g_gemm_epi16 = (mode >> 16) & 1;
   g_gemm_splitk = !((mode >> 17) & 1);
-  g_gemm_exp = ((mode >> 20) & 7) | (((mode >> 24) & 1) << 3);  // bit 3: no fp32 y stores
+  // exp bit 3: no fp32 y stores, bit 4: no fp32 TMEM loads (diagnostics)
+  g_gemm_exp = ((mode >> 20) & 7) | (((mode >> 24) & 3) << 3);
   g_gemm_quad = (mode >> 18) & 1;
   g_gemm_nostage = (mode >> 19) & 1;
   g_gemm_no_tmem_pipe = (mode >> 23) & 1;
