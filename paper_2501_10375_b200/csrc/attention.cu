@@ -838,6 +838,18 @@ __global__ void __launch_bounds__(256) attn_prefill_mma_kernel(PrefillArgs a, in
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
+  // the CTA's 16 token rows x the group's query heads staged in shared memory
+  // by coalesced 16-byte copies (each thread used to issue 64 scalar loads of
+  // its fragment elements: the kernel's top stall, lg_throttle / long
+  // scoreboard); row stride padded so the fragment reads spread over banks
+  const int q_ld = group * AT_HD + 8;
+  float* const q_s = reinterpret_cast<float*>(fa_smem + static_cast<size_t>(halves) * 4 * FA_TILE);
+  for (int i = threadIdx.x; i < FA_TOK * group * (AT_HD / 4); i += nthr_all) {
+    const int r = i / (group * (AT_HD / 4)), c = (i - r * (group * (AT_HD / 4))) * 4;
+    const int t = min(t0 + r, T - 1);
+    cp_async16(q_s + r * q_ld + c, a.qkv + static_cast<int64_t>(t) * ld + g * group * AT_HD + c, true);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   if (s_begin < s_end) load_tile(s_begin);
 
   // the CTA's 16 tokens x 64 RoPE frequencies: cos / sin computed once and
@@ -854,6 +866,8 @@ __global__ void __launch_bounds__(256) attn_prefill_mma_kernel(PrefillArgs a, in
     sincosf(__fmul_rn(static_cast<float>(a.pos0 + t), inv_s[j]), &sn, &cs);
     rope_cs[r][j] = make_float2(cs, sn);
   }
+  if (s_begin < s_end) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // Q, not tile s_begin
+  else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   // Q fragments: rows gr / gr + 8 = tokens t0 + gr / t0 + gr + 8; k-step ks
   // covers dims 16 ks .. 16 ks + 15; RoPE pairs (j, j + 64) = (ks, ks + 4)
@@ -862,8 +876,7 @@ __global__ void __launch_bounds__(256) attn_prefill_mma_kernel(PrefillArgs a, in
     float qv[2][8][4];  // [row half][ks][0..3] = dims 16ks + 2c4 + {0, 1, 8, 9}
 #pragma unroll
     for (int rh = 0; rh < 2; ++rh) {
-      const int t = min(t0 + gr + 8 * rh, T - 1);
-      const float* q = a.qkv + static_cast<int64_t>(t) * ld + hh * AT_HD;
+      const float* q = q_s + (gr + 8 * rh) * q_ld + warp * AT_HD;  // row clamped at staging
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
@@ -1091,7 +1104,8 @@ extern "C" int daop_attn_prefill(const float* d_qkv, int64_t T, int32_t pos0, ui
   }();
   const int group = n_heads / n_kv;
   const int halves = kv_split && group * 64 <= 256 && pos0 + T > FA_KV ? FA_HALVES_MAX : 1;
-  const size_t smem = static_cast<size_t>(halves) * 2 * 2 * FA_TILE * 2;  // per half: 2 stages x (K, V)
+  const size_t smem = static_cast<size_t>(halves) * 2 * 2 * FA_TILE * 2 +  // per half: 2 stages x (K, V)
+                      static_cast<size_t>(FA_TOK) * (group * AT_HD + 8) * 4;    // + staged fp32 Q rows
   DAOP_CUDA(cudaFuncSetAttribute(attn_prefill_mma_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
